@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 BFP multigrid hot path (BASELINE.json metric).
+
+Headline (`value`): BFP stencil residual throughput in GDoF/s on BASELINE.json
+config 2's fine level -- r = b - A x, 2-D 5-point, 4095^2 interior, int32
+mantissas p = 20, qcomp window (w_tmp = p + 5), int64 exact accumulation --
+with inputs resident in HBM.  One step = one windowed residual over the whole
+grid (pass 1 + the recompute launch, which exits early on the fast path).
+
+`e2e`: the same metric through the C-ABI with HOST buffers: every step uploads
+x and b (int32, pinned) and downloads r, copies inside the timed region.
+`roofline`: the dominant kernel (pass 1 of the residual) timed with CUDA events
+on its own stream, algorithmic bytes 12 B/DoF, against MEASURED_PEAKS.json.
+`cpu_baseline`: the CPU oracle port (oracle/bfp_oracle.c, OpenMP) on the same
+residual, all host threads.  `solves`: device time of the full config solves
+(C1, C2, C3, C4) replayed as CUDA graphs, with their final residual norms.
+
+`--impl reference` times the reference's CPU path (the oracle port of
+P/src/blas.cpp qcomp + EgemvKernel; the GMP reference itself cannot be built
+here) on the same config and metric.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+D, L_FINE, P_BITS = 2, 12, 20
+W_TMP = P_BITS + 5
+N_SETS = 4
+BYTES_PER_DOF = 12  # x, b read once + r written once, int32
+
+
+def dof():
+    return ((1 << L_FINE) - 1) ** D
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [t.strip() for t in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU path (oracle port) on the same config
+
+
+def cpu_residual_time(steps, warmup, budget_s=None):
+    """Time the oracle's OpenMP qcomp residual on the config-2 inputs.
+    Returns (seconds per residual, threads, steps actually run)."""
+    from oracle import ob
+    L = ob.lib()
+    x = ob.gen_uniform(D, L_FINE, P_BITS, 1, 1)
+    b = ob.gen_sine(D, L_FINE, P_BITS)
+    out = ob.OBlock(x.m.copy(), P_BITS, 0)
+    xc, bc, oc = x.c(), b.c(), out.c()
+    fl = ob.Flags()
+    threads = os.cpu_count() or 1
+    g = ob.Grid(D, L_FINE)
+    gm, ge = 1 << 14, 30  # window above the residual: exercised like the reference's gamma
+    # exact-binade gamma: the fast path, as on the GPU
+    rc = L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge,
+                                 C.byref(oc), C.byref(fl), threads)
+    assert rc == 0
+    mx = int(abs(out.m).max()) if len(out.m) else 0
+    ge = oc.e + mx.bit_length() + 1 - 16 if mx else 0
+    for _ in range(warmup):
+        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge, C.byref(oc),
+                                C.byref(fl), threads)
+    t0 = time.perf_counter()
+    n = 0
+    while n < steps:
+        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge, C.byref(oc),
+                                C.byref(fl), threads)
+        n += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    dt = (time.perf_counter() - t0) / n
+    return dt, threads, n
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    sec, threads, n = cpu_residual_time(args.steps, args.warmup)
+    v = dof() / sec / 1e9
+    line = {
+        "impl": "reference", "metric": "bfp_stencil_residual_gdofs", "value": v, "unit": "GDoF/s",
+        "n_gpus": 0, "steps": n, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": workload_config(),
+        "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": threads, "kind": "port",
+                         "sample": f"{n} full 4095^2 residuals (oracle/bfp_oracle.c OpenMP; the GMP "
+                                   f"reference is unbuildable here)"},
+        "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config():
+    return {"workload": "BASELINE config 2 fine-level BFP residual r=b-A*x (2-D 5-point, "
+                        "4095x4095 interior, int32 mantissas p=20, qcomp w_tmp=25, exact int64 "
+                        "accumulation)",
+            "dof": dof(), "bytes_per_dof": BYTES_PER_DOF,
+            "l2": f"inputs rotated over {N_SETS} (x,b,r) sets = "
+                  f"{N_SETS * 3 * dof() * 4 / 1e6:.0f} MB > 126 MB L2",
+            "parallelism": "replicas"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2307_00124_b200 as B
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    B.set_stream(stream.cuda_stream)
+    Lb = B.lib()
+    sp = C.c_void_p(stream.cuda_stream)
+    n = dof()
+
+    # inputs resident in HBM: N_SETS independent (x, b, r)
+    xs, bs, rs, gs = [], [], [], []
+    for s in range(N_SETS):
+        x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1 + s + 100 * rank, 1)
+        b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+        r = B.BfpVec.grid(D, L_FINE, 4)
+        # gamma with the exact binade of the residual: the qcomp fast path (Table 2 regime)
+        B.residual(x, b, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=r)
+        gs.append(B.inf_norm_upper(r))
+        xs.append(x)
+        bs.append(b)
+        rs.append(r)
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+
+    def step(k):
+        s = k % N_SETS
+        rc = Lb.bfp_stencil_gemv(xs[s].h, bs[s].h, m1, p1, 0, P_BITS, W_TMP, gs[s].c(), 0,
+                                 rs[s].h, sp)
+        if rc:
+            raise RuntimeError(f"bfp_stencil_gemv failed: {rc}")
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    barrier()
+    torch.cuda.synchronize()
+    B.profile_enable(True)
+    B.profile_read(reset=True)
+    l0 = B.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = B.launch_count() - l0
+    kern_ms, kern_n = B.profile_read(reset=True)
+    B.profile_enable(False)
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * n * args.steps / (ms / 1e3) / 1e9
+
+    # correctness probe of the timed work: flags must be the fast path, no device error
+    hdr = rs[0].header()
+    assert hdr.err == 0, "device error in timed residuals"
+
+    peak, peak_kind = peaks()
+    kavg_ms = kern_ms / max(kern_n, 1)
+    achieved = BYTES_PER_DOF * n / (kavg_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": args.traffic_bytes,
+            "kernel": "grid_win_kernel<int32,GemvOp> pass 1 (qcomp)", "peak_kind": peak_kind,
+            "kernel_ms": kavg_ms, "algorithmic_bytes_per_launch": BYTES_PER_DOF * n}
+
+    # e2e through the C-ABI with pinned host buffers
+    e2e = run_e2e(args, B, Lb, torch, stream, sp)
+
+    line = {
+        "metric": "bfp_stencil_residual_gdofs", "value": value, "unit": "GDoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": workload_config(),
+        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    if rank == 0 and not args.no_extras:
+        line["solves"] = run_solves(B, torch, stream)
+    if rank == 0 and not args.no_cpu:
+        sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"{nrun} full 4095^2 residuals in ~{args.cpu_budget:.0f} s "
+                                          f"(oracle/bfp_oracle.c, OpenMP)"}
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, B, Lb, torch, stream, sp):
+    import numpy as np
+    n = dof()
+    x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
+    b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+    hx = torch.empty(n, dtype=torch.int32).pin_memory()
+    hb = torch.empty(n, dtype=torch.int32).pin_memory()
+    hr = torch.empty(n, dtype=torch.int32).pin_memory()
+    hh = B._Header()
+    for src, dst in ((x, hx), (b, hb)):
+        assert Lb.bfp_vec_download_i32(src.h, C.c_void_p(dst.data_ptr()), C.byref(hh), sp) == 0
+    qx, ex = x.q, x.e
+    qb, eb = b.q, b.e
+    xd = B.BfpVec.grid(D, L_FINE, 4)
+    bd = B.BfpVec.grid(D, L_FINE, 4)
+    rd = B.BfpVec.grid(D, L_FINE, 4)
+    Lb.bfp_vec_upload_i32(xd.h, C.c_void_p(hx.data_ptr()), qx, ex, sp)
+    Lb.bfp_vec_upload_i32(bd.h, C.c_void_p(hb.data_ptr()), qb, eb, sp)
+    B.residual(xd, bd, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=rd)
+    g = B.inf_norm_upper(rd).c()
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+
+    def step():
+        assert Lb.bfp_vec_upload_i32(xd.h, C.c_void_p(hx.data_ptr()), qx, ex, sp) == 0
+        assert Lb.bfp_vec_upload_i32(bd.h, C.c_void_p(hb.data_ptr()), qb, eb, sp) == 0
+        assert Lb.bfp_stencil_gemv(xd.h, bd.h, m1, p1, 0, P_BITS, W_TMP, g, 0, rd.h, sp) == 0
+        assert Lb.bfp_vec_download_i32(rd.h, C.c_void_p(hr.data_ptr()), C.byref(hh), sp) == 0
+
+    k = max(3, min(args.steps, 20))
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"value": n * k / (ms / 1e3) / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": 2 * 4 * n,
+            "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
+            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv + bfp_vec_download_i32 (pinned host)"}
+
+
+SOLVES = {
+    "C1_1d_vcycles": dict(d=1, l_fine=20, cycles=10, x0_random=True, rhs_kind=0, p=16),
+    "C2_2d_vcycles": dict(d=2, l_fine=12, cycles=15, rhs_kind=1, p=20),
+    "C3_2d_fmg_nnq": dict(d=2, l_fine=13, l_coarse=3, cycles=1, rhs_kind=1, fmg=True,
+                          nonnormalized=True,
+                          p=[0, 0, 0] + [4 + 2 * (l - 3) for l in range(3, 32)][:29]),
+    "C4_3d_fmg": dict(d=3, l_fine=9, cycles=1, rhs_kind=1, fmg=True, p=24),
+}
+
+
+def run_solves(B, torch, stream):
+    out = {}
+    for name, kw in SOLVES.items():
+        kw = dict(kw)
+        p = kw.pop("p")
+        try:
+            mg = B.Multigrid(B.mg_config(**kw, p=p))
+            mg.solve(use_graph=True)  # capture + first replay
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 3
+            e0.record(stream)
+            for _ in range(reps):
+                mg.solve(use_graph=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
+            rec = sum(t[8] for t in tr)
+            out[name] = {"ms": ms, "launches": mg.launches(), "final_residual": hist[-1],
+                         "first_residual": hist[0], "recomputes": rec, "ops": len(tr)}
+            del mg
+        except Exception as ex:  # report, never hide
+            out[name] = {"error": str(ex)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+    return run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

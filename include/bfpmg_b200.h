@@ -1,0 +1,188 @@
+/*
+ * bfpmg_b200.h -- C-ABI of the B200-native BFP multigrid hot path.
+ *
+ * Plain pointers, sizes and status codes; no torch or CUDA types in the
+ * signatures (streams are passed as void* = cudaStream_t, 0 = default).
+ * Every call is stream-ordered and asynchronous unless it says otherwise;
+ * results that need the host (headers, flags, mantissas) come back through
+ * the explicit *_download / *_header calls, which synchronise the stream.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/proj):
+ *   bfp_vec_*            BfpBlock / BfpBlock::vec / zero_vec / dump+parse    include/bfpmg/bfp.hpp:18-56, src/bfp.cpp:26-55,230-272
+ *   bfp_normalize        normalize                                           src/bfp.cpp:97-108
+ *   bfp_quantize         quantize                                            src/bfp.cpp:110-122
+ *   bfp_inf_norm_upper   inf_norm_upper                                      src/bfp.cpp:124-148
+ *   bfp_qaxpby / nnq     qaxpby / nnqaxpby (EaxpbyKernel + qcomp|nnqcomp)     src/blas.cpp:41-72,214-218,236-240
+ *   bfp_qspmv_csr / nnq  qspmv / nnqspmv (EspmvKernel)                        src/blas.cpp:74-94,225-228,247-250
+ *   bfp_qgemv_csr / nnq  qgemv / nnqgemv (EgemvKernel)                        src/blas.cpp:96-142,230-234,252-256
+ *   bfp_qcomp_rows       qcomp/nnqcomp over a fixed exact-row ExactKernel    src/blas.cpp:144-212 (tests/test_blas.cpp:14-26)
+ *   bfp_stencil_*        EgemvKernel/EspmvKernel with the FD stencil, R, P    src/blas.cpp:96-142
+ *   bfp_mg_*             run_step / vcycle / ir / fmg                         src/multigrid.cpp:399-518
+ */
+#ifndef BFPMG_B200_H
+#define BFPMG_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (the C++ facade maps them to the reference exceptions) ---- */
+enum {
+  BFP_OK = 0,
+  BFP_ERR_ARG = 1,       /* std::invalid_argument: bad window, gamma <= 0, layout/dim mismatch */
+  BFP_ERR_WIDTH = 2,     /* an exact row needs more than 127 bits (documented limit) */
+  BFP_ERR_DOMAIN = 3,    /* std::domain_error: mantissa does not fit T_q */
+  BFP_ERR_CUDA = 4,      /* CUDA runtime failure */
+  BFP_ERR_ALIAS = 5,     /* output aliases an input */
+  BFP_ERR_NOMEM = 6,
+  BFP_ERR_STORAGE = 7    /* value does not fit the vector's mantissa storage (int32) */
+};
+
+/* ---- qcomp flags (QcompFlags, include/bfpmg/blas.hpp:98-102) ---- */
+enum {
+  BFP_FLAG_OVERFLOW = 1,
+  BFP_FLAG_UNDERFLOW = 2,
+  BFP_FLAG_RECOMPUTED = 4,
+  BFP_FLAG_NORMALIZED = 8 /* produced by qcomp (1) or nnqcomp (0) */
+};
+
+typedef struct bfp_vec_s* bfp_vec_t;
+
+/* host-visible header of a device block */
+typedef struct {
+  int64_t q;     /* mantissa width */
+  int64_t e;     /* shared exponent: values are 2^e * m_i */
+  int64_t n;     /* logical entries */
+  int64_t max_abs;/* max |m_i| */
+  int32_t flags; /* BFP_FLAG_* of the op that produced it */
+  int32_t err;   /* sticky BFP_ERR_* raised on the device */
+} bfp_header_t;
+
+/* ---- device blocks ---- */
+/* flat vector of n entries; mant_bytes 4 (int32) or 8 (int64) */
+int bfp_vec_create(int64_t n, int mant_bytes, bfp_vec_t* out);
+/* grid vector: dim 1..3, level l (n = (2^l - 1)^dim interior points, x fastest) */
+int bfp_vec_create_grid(int dim, int level, int mant_bytes, bfp_vec_t* out);
+int bfp_vec_destroy(bfp_vec_t v);
+int64_t bfp_vec_size(bfp_vec_t v);
+/* host mantissas (int64, logical order) -> device; sets q, e; checks fit T_q */
+int bfp_vec_upload(bfp_vec_t v, const int64_t* m, int64_t q, int64_t e, void* stream);
+/* same with int32 host mantissas (e2e path: no host-side widening) */
+int bfp_vec_upload_i32(bfp_vec_t v, const int32_t* m, int64_t q, int64_t e, void* stream);
+/* device -> host mantissas (pending shifts applied); synchronises the stream */
+int bfp_vec_download(bfp_vec_t v, int64_t* m, bfp_header_t* hdr, void* stream);
+int bfp_vec_download_i32(bfp_vec_t v, int32_t* m, bfp_header_t* hdr, void* stream);
+int bfp_vec_header(bfp_vec_t v, bfp_header_t* hdr, void* stream);
+/* zero_vec(n, q): all zero, e = 0 (src/bfp.cpp:53-55) */
+int bfp_vec_zero(bfp_vec_t v, int64_t q, void* stream);
+/* dump_block text (src/bfp.cpp:230-241): writes at most cap bytes, returns needed size */
+int64_t bfp_vec_dump(bfp_vec_t v, char* buf, int64_t cap, void* stream);
+/* parse_block text into a flat int64 vector (src/bfp.cpp:243-272) */
+int bfp_vec_parse(const char* text, bfp_vec_t* out, void* stream);
+
+/* ---- BFP block operations ---- */
+int bfp_normalize(bfp_vec_t x, bfp_vec_t out, void* stream);
+int bfp_quantize(bfp_vec_t x, int64_t w, bfp_vec_t out, void* stream);
+/* synchronous: scalar (m, q, e) >= max|x| rounded up to q_gamma bits */
+int bfp_inf_norm_upper(bfp_vec_t x, int64_t q_gamma, int64_t* m, int64_t* q, int64_t* e,
+                       void* stream);
+/* exact dot product sum_i m_x m_y as a 128-bit integer (hi, lo) at exponent e_x + e_y */
+int bfp_dot_exact(bfp_vec_t x, bfp_vec_t y, int64_t* hi, uint64_t* lo, int64_t* e, void* stream);
+
+/* ---- windowed BLAS (qcomp: w_tmp >= w_out; nnqcomp: w_tmp ignored) ----
+ * Scalars are BFP scalars (m, q, e); gamma = (gm, gq, ge) with gm > 0.
+ * mode: 0 = qcomp, 1 = nnqcomp.  force_recompute: QcompOptions test hook. */
+typedef struct {
+  int64_t m, q, e;
+} bfp_scalar_t;
+
+int bfp_axpby(bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta, int mode,
+              int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma, int force_recompute,
+              bfp_vec_t out, void* stream);
+
+/* CSR matrix (int64 rowptr/col/mantissas, host pointers copied to the device) */
+typedef struct bfp_csr_s* bfp_csr_t;
+int bfp_csr_create(int64_t rows, int64_t cols, const int64_t* rowptr, const int64_t* col,
+                   const int64_t* m, int64_t q, int64_t e, bfp_csr_t* out);
+int bfp_csr_destroy(bfp_csr_t a);
+int bfp_spmv_csr(bfp_csr_t a, bfp_vec_t x, int64_t m_a, int mode, int64_t w_out, int64_t w_tmp,
+                 bfp_scalar_t gamma, int force_recompute, bfp_vec_t out, void* stream);
+int bfp_gemv_csr(bfp_csr_t a, bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta,
+                 int64_t m_a, int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                 int force_recompute, bfp_vec_t out, void* stream);
+/* exact rows given as 128-bit (hi, lo) at template (q, e): the FixedKernel hook */
+int bfp_qcomp_rows(int64_t n, const int64_t* hi, const uint64_t* lo, int64_t q, int64_t e,
+                   int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                   int force_recompute, bfp_vec_t out, void* stream);
+
+/* ---- stencil family on grid vectors ---- */
+/* z = alpha*(A_l x) + beta*y ; A_l = 2^{2l} S_d (residual: alpha=-1, beta=+1) */
+int bfp_stencil_gemv(bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta, int mode,
+                     int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma, int force_recompute,
+                     bfp_vec_t out, void* stream);
+/* z = x + c*(b - A_l x)   (fused weighted-Jacobi sweep) */
+int bfp_stencil_jacobi(bfp_vec_t x, bfp_vec_t b, bfp_scalar_t c, int mode, int64_t w_out,
+                       int64_t w_tmp, bfp_scalar_t gamma, bfp_vec_t out, void* stream);
+/* z = c*r */
+int bfp_scal(bfp_vec_t r, bfp_scalar_t c, int mode, int64_t w_out, int64_t w_tmp,
+             bfp_scalar_t gamma, bfp_vec_t out, void* stream);
+/* coarse z = R r (full weighting) ; fine z = P xc ; fine z = P ec + y */
+int bfp_restrict_fw(bfp_vec_t r, int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                    bfp_vec_t out, void* stream);
+int bfp_prolong(bfp_vec_t xc, int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                bfp_vec_t out, void* stream);
+int bfp_prolong_correct(bfp_vec_t ec, bfp_vec_t y, int mode, int64_t w_out, int64_t w_tmp,
+                        bfp_scalar_t gamma, bfp_vec_t out, void* stream);
+/* Jacobi coefficient c = floor_qc(omega_d / 2d) * 2^{-2l} as a BFP scalar */
+int bfp_jacobi_coeff(int dim, int level, int64_t qc, bfp_scalar_t* c);
+
+/* ---- generators ---- */
+int bfp_gen_uniform(bfp_vec_t v, int64_t p, uint64_t seed, uint64_t stream_id, void* stream);
+int bfp_gen_sine(bfp_vec_t v, int64_t p, void* stream);
+
+/* ---- multigrid solver ---- */
+typedef struct {
+  int d, l_fine, l_coarse, nu1, nu2, n_coarse, cycles, fmg, nonnormalized, x0_random, rhs_kind,
+      qc;
+  uint64_t seed;
+  int p[32];
+} bfp_mg_config_t;
+
+typedef struct {
+  int32_t step, level, w_out, w_tmp;
+  int64_t gm, ge;
+  int32_t overflow, underflow, recomputed, normalized;
+} bfp_trace_rec_t;
+
+typedef struct bfp_mg_s* bfp_mg_t;
+int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out);
+int bfp_mg_destroy(bfp_mg_t mg);
+/* full solve on the device; use_graph != 0 replays a captured CUDA graph */
+int bfp_mg_solve(bfp_mg_t mg, int use_graph, void* stream);
+/* results (synchronise): finest-level iterate, residual history, trace */
+int bfp_mg_result(bfp_mg_t mg, int64_t* x, bfp_header_t* xh, double* hist, int hist_cap,
+                  int* n_hist, bfp_trace_rec_t* trace, int64_t trace_cap, int64_t* n_trace,
+                  void* stream);
+/* handles to the solver's finest-level vectors (x, b) for benchmarks */
+int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r);
+int64_t bfp_mg_kernel_launches(bfp_mg_t mg);
+
+/* ---- measurement hooks ----
+ * When enabled, every windowed pass-1 / nnqcomp kernel launch is bracketed by
+ * CUDA events recorded on its own stream; read() synchronises and returns the
+ * summed device time and the launch count since the last reset. */
+int bfp_profile_enable(int on);
+int bfp_profile_read(double* total_ms, int64_t* count, int reset);
+
+/* ---- misc ---- */
+const char* bfp_status_string(int status);
+int bfp_device_sync(void* stream);
+/* number of kernels this library launched since load (evidence counter) */
+int64_t bfp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,611 @@
+"""B200-native BFP multigrid hot path (arXiv 2307.00124) -- Python host mirror.
+
+A thin ctypes layer over the C-ABI of ``_lib/libbfpmg_b200.so``
+(``include/bfpmg_b200.h``).  Names, argument meaning and error behaviour
+mirror the reference C++ API (paths relative to /root/reference/proj):
+
+  BfpBlock, zero_vec, normalize, quantize     include/bfpmg/bfp.hpp:18-56, src/bfp.cpp:26-122
+  inf_norm_upper, dump_block/parse_block      src/bfp.cpp:124-148, 230-272
+  qaxpby/qsub/qspmv/qgemv (+ nnq*)            src/blas.cpp:214-258
+  qcomp/nnqcomp over fixed rows               src/blas.cpp:144-212
+  bfp_one / bfp_minus_one                     src/blas.cpp:257-258
+
+Every compute call runs on the GPU; there is no CPU fallback.  If the shared
+library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libbfpmg_b200.so")
+REPO = os.path.dirname(HERE)
+
+# status codes (include/bfpmg_b200.h)
+OK, ERR_ARG, ERR_WIDTH, ERR_DOMAIN, ERR_CUDA, ERR_ALIAS, ERR_NOMEM, ERR_STORAGE = range(8)
+FLAG_OVERFLOW, FLAG_UNDERFLOW, FLAG_RECOMPUTED, FLAG_NORMALIZED = 1, 2, 4, 8
+STEP_NAMES = ["ir-residual", "ir-correction", "v-relax0", "v-relax", "v-residual", "v-restrict",
+              "v-correct", "fmg-prolong", "final-residual"]
+
+
+class BfpError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        super().__init__(f"{what}: {status_string(status)} ({status})")
+
+
+class InvalidArgument(BfpError, ValueError):  # std::invalid_argument
+    pass
+
+
+class DomainError(BfpError, ValueError):  # std::domain_error
+    pass
+
+
+class WidthError(BfpError, OverflowError):  # exact row beyond 127 bits
+    pass
+
+
+def _raise(status: int, what: str):
+    if status == OK:
+        return
+    cls = {ERR_ARG: InvalidArgument, ERR_ALIAS: InvalidArgument, ERR_DOMAIN: DomainError,
+           ERR_STORAGE: DomainError, ERR_WIDTH: WidthError}.get(status, BfpError)
+    raise cls(status, what)
+
+
+class _Header(C.Structure):
+    _fields_ = [("q", C.c_int64), ("e", C.c_int64), ("n", C.c_int64), ("max_abs", C.c_int64),
+                ("flags", C.c_int32), ("err", C.c_int32)]
+
+
+class _Scalar(C.Structure):
+    _fields_ = [("m", C.c_int64), ("q", C.c_int64), ("e", C.c_int64)]
+
+
+class MgConfig(C.Structure):
+    _fields_ = [("d", C.c_int), ("l_fine", C.c_int), ("l_coarse", C.c_int), ("nu1", C.c_int),
+                ("nu2", C.c_int), ("n_coarse", C.c_int), ("cycles", C.c_int), ("fmg", C.c_int),
+                ("nonnormalized", C.c_int), ("x0_random", C.c_int), ("rhs_kind", C.c_int),
+                ("qc", C.c_int), ("seed", C.c_uint64), ("p", C.c_int * 32)]
+
+
+class TraceRec(C.Structure):
+    _fields_ = [("step", C.c_int32), ("level", C.c_int32), ("w_out", C.c_int32),
+                ("w_tmp", C.c_int32), ("gm", C.c_int64), ("ge", C.c_int64),
+                ("overflow", C.c_int32), ("underflow", C.c_int32), ("recomputed", C.c_int32),
+                ("normalized", C.c_int32)]
+
+
+EXPORTS = [
+    "bfp_vec_create", "bfp_vec_create_grid", "bfp_vec_destroy", "bfp_vec_size", "bfp_vec_upload",
+    "bfp_vec_upload_i32", "bfp_vec_download", "bfp_vec_download_i32", "bfp_vec_header",
+    "bfp_vec_zero", "bfp_vec_dump", "bfp_vec_parse", "bfp_normalize", "bfp_quantize",
+    "bfp_inf_norm_upper", "bfp_dot_exact", "bfp_axpby", "bfp_csr_create", "bfp_csr_destroy",
+    "bfp_spmv_csr", "bfp_gemv_csr", "bfp_qcomp_rows", "bfp_stencil_gemv", "bfp_stencil_jacobi",
+    "bfp_scal", "bfp_restrict_fw", "bfp_prolong", "bfp_prolong_correct", "bfp_jacobi_coeff",
+    "bfp_gen_uniform", "bfp_gen_sine", "bfp_mg_create", "bfp_mg_destroy", "bfp_mg_solve",
+    "bfp_mg_result", "bfp_mg_vectors", "bfp_mg_kernel_launches", "bfp_status_string",
+    "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
+]
+
+_lib: Optional[C.CDLL] = None
+
+
+def build(verbose: bool = False) -> str:
+    import subprocess
+    subprocess.run(["make", "-s", "-C", HERE], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+    return LIB_PATH
+
+
+def lib() -> C.CDLL:
+    """Load the sm_100a library (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"bfpmg_b200: CUDA library {LIB_PATH} not built (run build())")
+    L = C.CDLL(LIB_PATH)
+    i64, i32, vp, pi64 = C.c_int64, C.c_int, C.c_void_p, C.POINTER(C.c_int64)
+    S = _Scalar
+    sig = {
+        "bfp_vec_create": (i32, [i64, i32, C.POINTER(vp)]),
+        "bfp_vec_create_grid": (i32, [i32, i32, i32, C.POINTER(vp)]),
+        "bfp_vec_destroy": (i32, [vp]),
+        "bfp_vec_size": (i64, [vp]),
+        "bfp_vec_upload": (i32, [vp, vp, i64, i64, vp]),
+        "bfp_vec_upload_i32": (i32, [vp, vp, i64, i64, vp]),
+        "bfp_vec_download": (i32, [vp, vp, C.POINTER(_Header), vp]),
+        "bfp_vec_download_i32": (i32, [vp, vp, C.POINTER(_Header), vp]),
+        "bfp_vec_header": (i32, [vp, C.POINTER(_Header), vp]),
+        "bfp_vec_zero": (i32, [vp, i64, vp]),
+        "bfp_vec_dump": (i64, [vp, C.c_char_p, i64, vp]),
+        "bfp_vec_parse": (i32, [C.c_char_p, C.POINTER(vp), vp]),
+        "bfp_normalize": (i32, [vp, vp, vp]),
+        "bfp_quantize": (i32, [vp, i64, vp, vp]),
+        "bfp_inf_norm_upper": (i32, [vp, i64, pi64, pi64, pi64, vp]),
+        "bfp_dot_exact": (i32, [vp, vp, pi64, C.POINTER(C.c_uint64), pi64, vp]),
+        "bfp_axpby": (i32, [vp, vp, S, S, i32, i64, i64, S, i32, vp, vp]),
+        "bfp_csr_create": (i32, [i64, i64, vp, vp, vp, i64, i64, C.POINTER(vp)]),
+        "bfp_csr_destroy": (i32, [vp]),
+        "bfp_spmv_csr": (i32, [vp, vp, i64, i32, i64, i64, S, i32, vp, vp]),
+        "bfp_gemv_csr": (i32, [vp, vp, vp, S, S, i64, i32, i64, i64, S, i32, vp, vp]),
+        "bfp_qcomp_rows": (i32, [i64, vp, vp, i64, i64, i32, i64, i64, S, i32, vp, vp]),
+        "bfp_stencil_gemv": (i32, [vp, vp, S, S, i32, i64, i64, S, i32, vp, vp]),
+        "bfp_stencil_jacobi": (i32, [vp, vp, S, i32, i64, i64, S, vp, vp]),
+        "bfp_scal": (i32, [vp, S, i32, i64, i64, S, vp, vp]),
+        "bfp_restrict_fw": (i32, [vp, i32, i64, i64, S, vp, vp]),
+        "bfp_prolong": (i32, [vp, i32, i64, i64, S, vp, vp]),
+        "bfp_prolong_correct": (i32, [vp, vp, i32, i64, i64, S, vp, vp]),
+        "bfp_jacobi_coeff": (i32, [i32, i32, i64, C.POINTER(S)]),
+        "bfp_gen_uniform": (i32, [vp, i64, C.c_uint64, C.c_uint64, vp]),
+        "bfp_gen_sine": (i32, [vp, i64, vp]),
+        "bfp_mg_create": (i32, [C.POINTER(MgConfig), C.POINTER(vp)]),
+        "bfp_mg_destroy": (i32, [vp]),
+        "bfp_mg_solve": (i32, [vp, i32, vp]),
+        "bfp_mg_result": (i32, [vp, vp, C.POINTER(_Header), vp, i32, C.POINTER(i32), vp, i64,
+                                pi64, vp]),
+        "bfp_mg_vectors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+        "bfp_mg_kernel_launches": (i64, [vp]),
+        "bfp_status_string": (C.c_char_p, [i32]),
+        "bfp_device_sync": (i32, [vp]),
+        "bfp_launch_count": (i64, []),
+        "bfp_profile_enable": (i32, [i32]),
+        "bfp_profile_read": (i32, [C.POINTER(C.c_double), pi64, i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def status_string(st: int) -> str:
+    try:
+        return lib().bfp_status_string(st).decode()
+    except Exception:  # library not loadable
+        return str(st)
+
+
+_stream: Optional[int] = None
+
+
+def set_stream(handle: Optional[int]):
+    """Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream) for every call."""
+    global _stream
+    _stream = handle
+
+
+def _s():
+    return C.c_void_p(_stream) if _stream else None
+
+
+# ---------------------------------------------------------------------------
+# BFP scalars
+
+
+@dataclass(frozen=True)
+class Scalar:
+    """BfpScalar (m, q, e): value m * 2^e, m in T_q."""
+    m: int
+    q: int
+    e: int
+
+    def c(self) -> _Scalar:
+        return _Scalar(self.m, self.q, self.e)
+
+
+def bfp_one() -> Scalar:
+    return Scalar(1, 2, 0)
+
+
+def bfp_minus_one() -> Scalar:
+    return Scalar(-1, 1, 0)
+
+
+# ---------------------------------------------------------------------------
+# device blocks
+
+
+class BfpVec:
+    """A device BFP block: int32/int64 mantissas + one shared exponent.
+
+    ``BfpVec.grid(d, l)`` creates a grid vector with (2^l - 1)^d interior points
+    (x fastest); ``BfpVec.flat(n)`` a plain vector.  Mantissas live in HBM, the
+    header (q, e, max|m|, flags) on the device too.
+    """
+
+    def __init__(self, handle: int, dim: int, level: int, mant_bytes: int):
+        self.h = C.c_void_p(handle)
+        self.dim, self.level, self.mant_bytes = dim, level, mant_bytes
+
+    @staticmethod
+    def flat(n: int, mant_bytes: int = 8) -> "BfpVec":
+        h = C.c_void_p()
+        _raise(lib().bfp_vec_create(n, mant_bytes, C.byref(h)), "bfp_vec_create")
+        return BfpVec(h.value, 0, 0, mant_bytes)
+
+    @staticmethod
+    def grid(dim: int, level: int, mant_bytes: int = 4) -> "BfpVec":
+        h = C.c_void_p()
+        _raise(lib().bfp_vec_create_grid(dim, level, mant_bytes, C.byref(h)), "bfp_vec_create_grid")
+        return BfpVec(h.value, dim, level, mant_bytes)
+
+    @staticmethod
+    def from_mantissas(m: Sequence[int], q: int, e: int, dim: int = 0, level: int = 0,
+                       mant_bytes: int = 8) -> "BfpVec":
+        v = BfpVec.grid(dim, level, mant_bytes) if dim else BfpVec.flat(len(m), mant_bytes)
+        v.upload(m, q, e)
+        return v
+
+    def __del__(self):
+        try:
+            if self.h and self.h.value:
+                lib().bfp_vec_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def __len__(self) -> int:
+        return int(lib().bfp_vec_size(self.h))
+
+    def upload(self, m, q: int, e: int):
+        a = np.ascontiguousarray(np.asarray(m, dtype=np.int64))
+        if a.size != len(self):
+            raise InvalidArgument(ERR_ARG, "upload: size mismatch")
+        _raise(lib().bfp_vec_upload(self.h, a.ctypes.data_as(C.c_void_p), q, e, _s()), "upload")
+        hh = _Header()
+        _raise(lib().bfp_vec_header(self.h, C.byref(hh), _s()), "upload")  # check_fits
+
+    def header(self) -> _Header:
+        hh = _Header()
+        _raise(lib().bfp_vec_header(self.h, C.byref(hh), _s()), "header")
+        return hh
+
+    def download(self) -> Tuple[np.ndarray, int, int]:
+        """(mantissas int64, q, e) with pending shifts applied."""
+        n = len(self)
+        out = np.zeros(max(n, 1), dtype=np.int64)
+        hh = _Header()
+        _raise(lib().bfp_vec_download(self.h, out.ctypes.data_as(C.c_void_p), C.byref(hh), _s()),
+               "download")
+        return out[:n], int(hh.q), int(hh.e)
+
+    @property
+    def q(self) -> int:
+        return int(self.header().q)
+
+    @property
+    def e(self) -> int:
+        return int(self.header().e)
+
+    @property
+    def flags(self) -> int:
+        return int(self.header().flags)
+
+    def mantissas(self) -> np.ndarray:
+        return self.download()[0]
+
+    def is_zero(self) -> bool:
+        return self.header().max_abs == 0
+
+    def zero(self, q: int):
+        _raise(lib().bfp_vec_zero(self.h, q, _s()), "zero")
+        return self
+
+
+def zero_vec(n: int, q: int, mant_bytes: int = 8) -> BfpVec:
+    """BfpBlock::zero_vec (src/bfp.cpp:53-55): all zero, e = 0."""
+    return BfpVec.flat(n, mant_bytes).zero(q)
+
+
+def _like(x: BfpVec) -> BfpVec:
+    return BfpVec.grid(x.dim, x.level, x.mant_bytes) if x.dim else BfpVec.flat(len(x), x.mant_bytes)
+
+
+def normalize(x: BfpVec) -> BfpVec:
+    out = _like(x)
+    _raise(lib().bfp_normalize(x.h, out.h, _s()), "normalize")
+    return out
+
+
+def quantize(x: BfpVec, w: int) -> BfpVec:
+    out = _like(x)
+    _raise(lib().bfp_quantize(x.h, w, out.h, _s()), "quantize")
+    return out
+
+
+def inf_norm_upper(x: BfpVec, q_gamma: int = 16) -> Scalar:
+    m, q, e = C.c_int64(), C.c_int64(), C.c_int64()
+    _raise(lib().bfp_inf_norm_upper(x.h, q_gamma, C.byref(m), C.byref(q), C.byref(e), _s()),
+           "inf_norm_upper")
+    return Scalar(m.value, q.value, e.value)
+
+
+def dot_exact(x: BfpVec, y: BfpVec) -> Tuple[int, int]:
+    """Exact sum_i m_x m_y as a Python int, and its exponent e_x + e_y."""
+    hi, lo, e = C.c_int64(), C.c_uint64(), C.c_int64()
+    _raise(lib().bfp_dot_exact(x.h, y.h, C.byref(hi), C.byref(lo), C.byref(e), _s()), "dot_exact")
+    return (hi.value << 64) | lo.value, e.value
+
+
+def dump_block(x: BfpVec) -> str:
+    n = lib().bfp_vec_dump(x.h, None, 0, _s())
+    if n < 0:
+        _raise(int(-n), "dump_block")
+    buf = C.create_string_buffer(int(n))
+    lib().bfp_vec_dump(x.h, buf, n, _s())
+    return buf.value.decode()
+
+
+def parse_block(text: str) -> BfpVec:
+    h = C.c_void_p()
+    _raise(lib().bfp_vec_parse(text.encode(), C.byref(h), _s()), "parse_block")
+    return BfpVec(h.value, 0, 0, 8)
+
+
+# ---------------------------------------------------------------------------
+# windowed BLAS
+
+
+@dataclass
+class QcompResult:
+    z: BfpVec
+    overflow: bool
+    underflow: bool
+    recomputed: bool
+
+
+def _result(out: BfpVec) -> QcompResult:
+    f = out.header().flags
+    return QcompResult(out, bool(f & FLAG_OVERFLOW), bool(f & FLAG_UNDERFLOW),
+                       bool(f & FLAG_RECOMPUTED))
+
+
+def _chk_window(w_out, w_tmp, gamma: Scalar, qc: bool):
+    if w_out < 1 or (qc and w_out > w_tmp):
+        raise InvalidArgument(ERR_ARG, "qcomp: need 0 < w_out <= w_tmp")
+    if gamma.m <= 0:
+        raise InvalidArgument(ERR_ARG, "gamma must be > 0")
+
+
+def _out_for(x: BfpVec, n: Optional[int] = None, w: int = 0) -> BfpVec:
+    mb = 8 if (w > 32 or x.mant_bytes == 8) else x.mant_bytes
+    if x.dim:
+        return BfpVec.grid(x.dim, x.level, x.mant_bytes)
+    return BfpVec.flat(len(x) if n is None else n, mb)
+
+
+def qaxpby(x, y, alpha: Scalar, beta: Scalar, w_out, w_tmp, gamma: Scalar, force=False,
+           nn=False) -> QcompResult:
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = _out_for(x)
+    _raise(lib().bfp_axpby(x.h, y.h, alpha.c(), beta.c(), int(nn), w_out, w_tmp, gamma.c(),
+                           int(force), out.h, _s()), "qaxpby")
+    return _result(out)
+
+
+def qsub(x, y, w_out, w_tmp, gamma) -> QcompResult:
+    return qaxpby(x, y, bfp_one(), bfp_minus_one(), w_out, w_tmp, gamma)
+
+
+def nnqaxpby(x, y, alpha, beta, w_out, gamma) -> QcompResult:
+    return qaxpby(x, y, alpha, beta, w_out, w_out, gamma, nn=True)
+
+
+def nnqsub(x, y, w_out, gamma) -> QcompResult:
+    return nnqaxpby(x, y, bfp_one(), bfp_minus_one(), w_out, gamma)
+
+
+class BfpCsr:
+    """BfpCsr (include/bfpmg/bfp.hpp:62-84) on the device."""
+
+    def __init__(self, rows, cols, rowptr, col, m, q, e):
+        self.rows, self.cols, self.q, self.e = rows, cols, q, e
+        rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+        cl = np.ascontiguousarray(col if len(col) else [0], dtype=np.int64)
+        mm = np.ascontiguousarray(m if len(m) else [0], dtype=np.int64)
+        h = C.c_void_p()
+        _raise(lib().bfp_csr_create(rows, cols, rp.ctypes.data_as(C.c_void_p),
+                                    cl.ctypes.data_as(C.c_void_p), mm.ctypes.data_as(C.c_void_p),
+                                    q, e, C.byref(h)), "BfpCsr")
+        self.h = h
+        self.max_row_nnz = int(max((rp[i + 1] - rp[i] for i in range(rows)), default=0))
+
+    def __del__(self):
+        try:
+            lib().bfp_csr_destroy(self.h)
+        except Exception:
+            pass
+
+
+def qspmv(a: BfpCsr, x: BfpVec, w_out, w_tmp, gamma, m_a=0, force=False, nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = BfpVec.flat(a.rows, x.mant_bytes)
+    _raise(lib().bfp_spmv_csr(a.h, x.h, m_a, int(nn), w_out, w_tmp, gamma.c(), int(force), out.h,
+                              _s()), "qspmv")
+    return _result(out)
+
+
+def nnqspmv(a, x, w_out, gamma, m_a=0):
+    return qspmv(a, x, w_out, w_out, gamma, m_a, nn=True)
+
+
+def qgemv(a: BfpCsr, x: BfpVec, y: BfpVec, alpha, beta, w_out, w_tmp, gamma, m_a=0, force=False,
+          nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = BfpVec.flat(a.rows, x.mant_bytes)
+    _raise(lib().bfp_gemv_csr(a.h, x.h, y.h, alpha.c(), beta.c(), m_a, int(nn), w_out, w_tmp,
+                              gamma.c(), int(force), out.h, _s()), "qgemv")
+    return _result(out)
+
+
+def nnqgemv(a, x, y, alpha, beta, w_out, gamma, m_a=0):
+    return qgemv(a, x, y, alpha, beta, w_out, w_out, gamma, m_a, nn=True)
+
+
+def qcomp_rows(rows: Sequence[int], q: int, e: int, w_out, w_tmp, gamma: Scalar, force=False,
+               nn=False, mant_bytes=8) -> QcompResult:
+    """qcomp / nnqcomp over a FixedKernel of exact rows (tests/test_blas.cpp:14-26)."""
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    n = len(rows)
+    hi = np.array([(int(v) >> 64) for v in rows] or [0], dtype=np.int64)
+    lo = np.array([(int(v) & ((1 << 64) - 1)) for v in rows] or [0], dtype=np.uint64)
+    out = BfpVec.flat(n, mant_bytes)
+    _raise(lib().bfp_qcomp_rows(n, hi.ctypes.data_as(C.c_void_p), lo.ctypes.data_as(C.c_void_p),
+                                q, e, int(nn), w_out, w_tmp, gamma.c(), int(force), out.h, _s()),
+           "qcomp_rows")
+    return _result(out)
+
+
+# ---------------------------------------------------------------------------
+# stencil family
+
+
+def stencil_gemv(x, y, alpha, beta, w_out, w_tmp, gamma, force=False, nn=False, out=None):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = out or _like(x)
+    _raise(lib().bfp_stencil_gemv(x.h, y.h, alpha.c(), beta.c(), int(nn), w_out, w_tmp,
+                                  gamma.c(), int(force), out.h, _s()), "stencil_gemv")
+    return _result(out)
+
+
+def residual(x, b, w_out, w_tmp, gamma, nn=False, out=None):
+    """r = b - A x (the fine-level residual; alpha = -1, beta = +1)."""
+    return stencil_gemv(x, b, bfp_minus_one(), bfp_one(), w_out, w_tmp, gamma, nn=nn, out=out)
+
+
+def jacobi(x, b, c: Scalar, w_out, w_tmp, gamma, nn=False, out=None):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = out or _like(x)
+    _raise(lib().bfp_stencil_jacobi(x.h, b.h, c.c(), int(nn), w_out, w_tmp, gamma.c(), out.h,
+                                    _s()), "jacobi")
+    return _result(out)
+
+
+def scal(r, c: Scalar, w_out, w_tmp, gamma, nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = _like(r)
+    _raise(lib().bfp_scal(r.h, c.c(), int(nn), w_out, w_tmp, gamma.c(), out.h, _s()), "scal")
+    return _result(out)
+
+
+def restrict_fw(r, w_out, w_tmp, gamma, nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = BfpVec.grid(r.dim, r.level - 1, r.mant_bytes)
+    _raise(lib().bfp_restrict_fw(r.h, int(nn), w_out, w_tmp, gamma.c(), out.h, _s()), "restrict")
+    return _result(out)
+
+
+def prolong(xc, w_out, w_tmp, gamma, nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = BfpVec.grid(xc.dim, xc.level + 1, xc.mant_bytes)
+    _raise(lib().bfp_prolong(xc.h, int(nn), w_out, w_tmp, gamma.c(), out.h, _s()), "prolong")
+    return _result(out)
+
+
+def prolong_correct(ec, y, w_out, w_tmp, gamma, nn=False):
+    _chk_window(w_out, w_tmp, gamma, not nn)
+    out = _like(y)
+    _raise(lib().bfp_prolong_correct(ec.h, y.h, int(nn), w_out, w_tmp, gamma.c(), out.h, _s()),
+           "prolong_correct")
+    return _result(out)
+
+
+def jacobi_coeff(dim: int, level: int, qc: int = 16) -> Scalar:
+    s = _Scalar()
+    _raise(lib().bfp_jacobi_coeff(dim, level, qc, C.byref(s)), "jacobi_coeff")
+    return Scalar(s.m, s.q, s.e)
+
+
+def gen_uniform(v: BfpVec, p: int, seed: int, stream_id: int) -> BfpVec:
+    _raise(lib().bfp_gen_uniform(v.h, p, seed, stream_id, _s()), "gen_uniform")
+    return v
+
+
+def gen_sine(v: BfpVec, p: int) -> BfpVec:
+    _raise(lib().bfp_gen_sine(v.h, p, _s()), "gen_sine")
+    return v
+
+
+# ---------------------------------------------------------------------------
+# multigrid solver
+
+
+def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=False,
+              nonnormalized=False, x0_random=False, rhs_kind=1, qc=16, seed=1, p=None) -> MgConfig:
+    cfg = MgConfig()
+    cfg.d, cfg.l_fine, cfg.l_coarse, cfg.nu1, cfg.nu2 = d, l_fine, l_coarse, nu1, nu2
+    cfg.n_coarse, cfg.cycles, cfg.fmg, cfg.nonnormalized = n_coarse, cycles, int(fmg), int(nonnormalized)
+    cfg.x0_random, cfg.rhs_kind, cfg.qc, cfg.seed = int(x0_random), rhs_kind, qc, seed
+    if isinstance(p, int):
+        p = [p] * 32
+    for i in range(32):
+        cfg.p[i] = p[i] if i < len(p) else 0
+    return cfg
+
+
+class Multigrid:
+    """Device multigrid solver: IR with Jacobi V(nu1,nu2) cycles, or FMG."""
+
+    def __init__(self, cfg: MgConfig):
+        h = C.c_void_p()
+        _raise(lib().bfp_mg_create(C.byref(cfg), C.byref(h)), "bfp_mg_create")
+        self.h, self.cfg = h, cfg
+
+    def __del__(self):
+        try:
+            lib().bfp_mg_destroy(self.h)
+        except Exception:
+            pass
+
+    def solve(self, use_graph: bool = False):
+        _raise(lib().bfp_mg_solve(self.h, int(use_graph), _s()), "bfp_mg_solve")
+
+    def launches(self) -> int:
+        return int(lib().bfp_mg_kernel_launches(self.h))
+
+    def result(self, trace_cap: int = 1 << 20):
+        n = ((1 << self.cfg.l_fine) - 1) ** self.cfg.d
+        x = np.zeros(n, dtype=np.int64)
+        hh = _Header()
+        hist = np.zeros(4096, dtype=np.float64)
+        tr = (TraceRec * trace_cap)()
+        nh, nt = C.c_int(), C.c_int64()
+        _raise(lib().bfp_mg_result(self.h, x.ctypes.data_as(C.c_void_p), C.byref(hh),
+                                   hist.ctypes.data_as(C.c_void_p), 4096, C.byref(nh), tr,
+                                   trace_cap, C.byref(nt), _s()), "bfp_mg_result")
+        trace = [(t.step, t.level, t.w_out, t.w_tmp, t.gm, t.ge, t.overflow, t.underflow,
+                  t.recomputed, t.normalized) for t in tr[: min(nt.value, trace_cap)]]
+        return x, int(hh.q), int(hh.e), hist[: nh.value].tolist(), trace
+
+    def vectors(self):
+        x, b, r = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        _raise(lib().bfp_mg_vectors(self.h, C.byref(x), C.byref(b), C.byref(r)), "bfp_mg_vectors")
+        return x, b, r
+
+
+def launch_count() -> int:
+    return int(lib().bfp_launch_count())
+
+
+def device_sync():
+    _raise(lib().bfp_device_sync(_s()), "sync")
+
+
+def profile_enable(on: bool = True):
+    _raise(lib().bfp_profile_enable(int(on)), "profile_enable")
+
+
+def profile_read(reset: bool = True) -> Tuple[float, int]:
+    """(summed device ms, launches) of pass-1 / nnqcomp kernels since the last reset."""
+    t, n = C.c_double(), C.c_int64()
+    _raise(lib().bfp_profile_read(C.byref(t), C.byref(n), int(reset)), "profile_read")
+    return t.value, n.value

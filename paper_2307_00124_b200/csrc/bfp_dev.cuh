@@ -1,0 +1,473 @@
+// bfp_dev.cuh -- device-side BFP primitives, block headers and the qcomp /
+// nnqcomp window epilogue shared by every sm_100a kernel of the hot path.
+//
+// Reference semantics restated here (paths relative to /root/reference/proj):
+//   msb                    src/wideint.cpp:15-25
+//   shift_floor / wrap     src/wideint.cpp:94-107
+//   clamp (saturation)     src/blas.cpp:196-209
+//   qcomp window           src/blas.cpp:144-187
+//   nnqcomp window         src/blas.cpp:189-212
+// Every vector carries a DEVICE-resident header (exponent, width, pending
+// shift, max/min mantissa) so exponents and norms never force a host round
+// trip: a whole V-cycle is stream-ordered and graph-capturable.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bfpdev {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+// ---------------------------------------------------------------------------
+// device header of a BFP block (one per vector, 128-byte aligned)
+struct alignas(128) Hdr {
+  // published state of the block
+  int64_t q;        // declared width w_out
+  int64_t e;        // block exponent
+  int64_t shift;    // pending arithmetic right shift applied on every load (deferred qcomp)
+  int64_t max_m;    // max of STORED mantissas (pads included: >= 0)
+  int64_t min_m;    // min of STORED mantissas (<= 0)
+  int32_t flags;    // BFP_FLAG_*
+  int32_t err;      // sticky BFP_ERR_*
+  // qcomp staging, written by pass-1 finalize, read by the recompute pass
+  int64_t lam_out;
+  int32_t need_recompute;
+  int32_t pad0;
+  // cross-block accumulators (reset by each finalize)
+  unsigned long long acc_bits;  // max msb over exact rows
+  long long acc_max, acc_min;
+  unsigned int acc_done;
+  int32_t acc_err;
+};
+
+enum { FLAG_OVERFLOW = 1, FLAG_UNDERFLOW = 2, FLAG_RECOMPUTED = 4, FLAG_NORMALIZED = 8 };
+enum { ERR_WIDTH = 2, ERR_STORAGE = 7 };
+
+// device view of a vector passed to kernels by value
+struct Vec {
+  void* data;      // element 0 (after the front halo for grids)
+  Hdr* hdr;
+  int32_t ebytes;  // 4 or 8
+  int32_t dim;     // 0 = flat, 1..3 = grid
+  int32_t l;       // grid level (N = 2^l)
+  int32_t pad;
+  int64_t n;       // storage span in elements (flat: padded to 4; grid: N^dim)
+  int64_t nlog;    // logical entries
+};
+
+// trace record (bfp_trace_rec_t layout)
+struct TraceRec {
+  int32_t step, level, w_out, w_tmp;
+  int64_t gm, ge;
+  int32_t overflow, underflow, recomputed, normalized;
+};
+
+// ---------------------------------------------------------------------------
+// integer primitives
+
+__device__ __forceinline__ int bitlen64(uint64_t u) { return u ? 64 - __clzll((long long)u) : 0; }
+__device__ __forceinline__ int bitlen128(u128 u) {
+  uint64_t hi = (uint64_t)(u >> 64);
+  return hi ? 128 - __clzll((long long)hi) : bitlen64((uint64_t)u);
+}
+// msb: minimal two's complement width (msb(0) = msb(-1) = 1)
+__device__ __forceinline__ int msb(int64_t v) { return bitlen64((uint64_t)(v ^ (v >> 63))) + 1; }
+__device__ __forceinline__ int msb(i128 v) { return bitlen128((u128)(v ^ (v >> 127))) + 1; }
+__host__ __device__ __forceinline__ int msb_h(int64_t v) {
+  uint64_t u = (uint64_t)(v ^ (v >> 63));
+  int b = 0;
+  while (u) {
+    ++b;
+    u >>= 1;
+  }
+  return b + 1;
+}
+
+template <typename A> struct AccBits;
+template <> struct AccBits<int64_t> { static constexpr int value = 64; };
+template <> struct AccBits<i128> { static constexpr int value = 128; };
+
+// floor(x / 2^s) for s >= 0
+template <typename A> __device__ __forceinline__ A sar(A x, int64_t s) {
+  constexpr int B = AccBits<A>::value;
+  return s >= B - 1 ? (x < 0 ? A(-1) : A(0)) : (x >> s);
+}
+// wrap_w(floor(x / 2^s)), w <= 64, s of either sign (low bits only, no overflow)
+template <typename A> __device__ __forceinline__ int64_t wrap_shift(A x, int64_t s, int64_t w) {
+  uint64_t lo;
+  if (s >= 0) {
+    lo = (uint64_t)sar<A>(x, s);
+  } else {
+    int64_t k = -s;
+    if (k >= w) return 0;
+    lo = ((uint64_t)x) << k;
+  }
+  int sh = 64 - (int)w;
+  return (int64_t)(lo << sh) >> sh;
+}
+// floor(x / 2^s) clamped to T_w (nnqcomp, w <= 64): saturates when a left shift leaves T_w
+template <typename A> __device__ __forceinline__ int64_t shift_clamp(A x, int64_t s, int64_t w) {
+  const int64_t hi = (int64_t)((~0ull) >> (65 - w)), lo = -hi - 1;
+  A r;
+  if (s >= 0) {
+    r = sar<A>(x, s);
+  } else {
+    int64_t k = -s;
+    if (x == 0) return 0;
+    if (msb(x) + k > w) return x < 0 ? lo : hi;
+    r = x << k;
+  }
+  return r > (A)hi ? hi : (r < (A)lo ? lo : (int64_t)r);
+}
+// exact floor(x / 2^s) where the result is known to fit 64 bits (recompute pass)
+template <typename A> __device__ __forceinline__ int64_t shift_exact(A x, int64_t s) {
+  if (s >= 0) return (int64_t)sar<A>(x, s);
+  return (int64_t)(x << (-s));
+}
+
+// ---------------------------------------------------------------------------
+// stored mantissa load/store with pending shift
+
+template <typename M> __device__ __forceinline__ int64_t ldm(const Vec& v, int64_t i, int64_t sh) {
+  return ((int64_t)((const M*)v.data)[i]) >> sh;
+}
+
+// eff width of a block: smallest w with every (stored >> shift) in T_w
+__device__ __forceinline__ int eff_bits(const Hdr* h) {
+  int64_t s = h->shift;
+  int64_t a = h->max_m >> s, b = h->min_m >> s;
+  int ma = msb(a), mb = msb(b);
+  return ma > mb ? ma : mb;
+}
+__device__ __forceinline__ uint64_t max_abs(const Hdr* h) {
+  int64_t s = h->shift;
+  int64_t a = h->max_m >> s, b = h->min_m >> s;
+  uint64_t ua = a < 0 ? (uint64_t)0 - (uint64_t)a : (uint64_t)a;
+  uint64_t ub = b < 0 ? (uint64_t)0 - (uint64_t)b : (uint64_t)b;
+  return ua > ub ? ua : ub;
+}
+
+// ---------------------------------------------------------------------------
+// gamma arithmetic: 15-bit round-up values
+
+struct G15 {
+  int64_t m, e;
+};
+__host__ __device__ __forceinline__ int bitlen_h(uint64_t u) {
+  int b = 0;
+  while (u) {
+    ++b;
+    u >>= 1;
+  }
+  return b;
+}
+__host__ __device__ inline G15 g15_from(uint64_t mag, int64_t e) {
+  G15 r = {0, 0};
+  if (mag == 0) return r;
+  int b = bitlen_h(mag);
+  if (b <= 15) {
+    r.m = (int64_t)(mag << (15 - b));
+    r.e = e - (15 - b);
+  } else {
+    int s = b - 15;
+    uint64_t m = (mag >> s) + ((mag & ((1ull << s) - 1)) != 0);
+    if (m == (1ull << 15)) {
+      m >>= 1;
+      ++s;
+    }
+    r.m = (int64_t)m;
+    r.e = e + s;
+  }
+  return r;
+}
+__host__ __device__ inline G15 g15_mul(G15 a, G15 b) {
+  if (a.m == 0 || b.m == 0) return G15{0, 0};
+  return g15_from((uint64_t)a.m * (uint64_t)b.m, a.e + b.e);
+}
+__host__ __device__ inline G15 g15_add(G15 a, G15 b) {
+  if (a.m == 0) return b;
+  if (b.m == 0) return a;
+  if (a.e < b.e) {
+    G15 t = a;
+    a = b;
+    b = t;
+  }
+  int64_t gap = a.e - b.e;
+  if (gap <= 100) {
+    u128 s = ((u128)(uint64_t)a.m << gap) + (u128)(uint64_t)b.m;
+    int bl = 0;
+    {
+      uint64_t hi = (uint64_t)(s >> 64);
+      bl = hi ? 64 + bitlen_h(hi) : bitlen_h((uint64_t)s);
+    }
+    if (bl <= 64) return g15_from((uint64_t)s, b.e);
+    int sh = bl - 64;
+    uint64_t top = (uint64_t)(s >> sh) | (uint64_t)((s & ((((u128)1) << sh) - 1)) != 0);
+    return g15_from(top, b.e + sh);
+  }
+  G15 r = a;
+  r.m += 1;
+  if (r.m == (1 << 15)) {
+    r.m = 1 << 14;
+    r.e += 1;
+  }
+  return r;
+}
+
+// gamma rule: add_up chain over up to 3 terms c_t (x) X_t
+struct GTerm {
+  const Hdr* v;    // nullptr: X = 1
+  int64_t cm, ce;  // cm == 0: no coefficient
+  int32_t kind;    // 0 = norm(v), 1 = ulp(v) (zero if v is all zero)
+  int32_t pad;
+};
+struct GammaRule {
+  int32_t literal;  // 1: (lm, le) as given
+  int32_t nterms;
+  int64_t lm, le;
+  GTerm t[3];
+};
+
+__device__ inline G15 gterm_eval(const GTerm& t) {
+  G15 x;
+  if (t.v == nullptr) {
+    x = G15{1 << 14, -14};
+  } else if (t.kind == 0) {
+    x = g15_from(max_abs(t.v), t.v->e);
+  } else {
+    x = max_abs(t.v) ? g15_from(1, t.v->e) : G15{0, 0};
+  }
+  if (t.cm != 0) x = g15_mul(g15_from((uint64_t)t.cm, t.ce), x);
+  return x;
+}
+// returns (gm, ge) of the BFP scalar gamma (q = 16); degenerate 2^-400 if zero
+__device__ inline void gamma_eval(const GammaRule& r, int64_t& gm, int64_t& ge) {
+  if (r.literal) {
+    gm = r.lm;
+    ge = r.le;
+    return;
+  }
+  G15 acc{0, 0};
+  for (int i = 0; i < r.nterms; ++i) acc = g15_add(acc, gterm_eval(r.t[i]));
+  if (acc.m == 0) {
+    gm = 1 << 14;
+    ge = -400 - 14;
+  } else {
+    gm = acc.m;
+    ge = acc.e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// window context (one per op launch; computed redundantly by every block)
+
+enum { MODE_QCOMP = 0, MODE_NNQ = 1, MODE_RECOMPUTE = 2 };
+
+struct WinParams {
+  int64_t w_out, w_tmp;
+  int32_t mode, force;
+  int32_t trace_slot, step;
+  int32_t level, hist_slot;
+  TraceRec* trace;
+  double* hist;   // residual-norm history slot (ldexp(max|m|, e)), or nullptr
+  GammaRule gamma;
+};
+
+struct WinCtx {
+  int64_t e_star, mu_tmp, lam;  // lam: lam_tmp (qcomp), lam_out (nnq / recompute)
+  int64_t gm, ge;
+  int32_t store_tmp;            // qcomp: tmp fits the storage and is stored
+  int32_t skip;                 // recompute pass with nothing to do
+};
+
+// per-thread running reductions
+struct Red {
+  int bits;
+  int64_t mx, mn;
+  int err;
+  __device__ void init() {
+    bits = 1;
+    mx = INT64_MIN;
+    mn = INT64_MAX;
+    err = 0;
+  }
+  __device__ void val(int64_t v) {
+    mx = v > mx ? v : mx;
+    mn = v < mn ? v : mn;
+  }
+};
+
+__device__ __forceinline__ int64_t shfl_max64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t shfl_min64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+
+// Block reduce + cross-block atomics + last-block finalize.  `fin` is called
+// by exactly one thread of the last block to finish, after every block's
+// contribution is visible.
+template <typename Fin>
+__device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
+  __shared__ int s_bits[32], s_err[32];
+  __shared__ long long s_mx[32], s_mn[32];
+  __shared__ bool s_last;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int bits = __reduce_max_sync(0xffffffffu, r.bits);
+  int err = __reduce_or_sync(0xffffffffu, r.err);
+  int64_t mx = shfl_max64(r.mx), mn = shfl_min64(r.mn);
+  if (lane == 0) {
+    s_bits[wid] = bits;
+    s_err[wid] = err;
+    s_mx[wid] = mx;
+    s_mn[wid] = mn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      bits = s_bits[w] > bits ? s_bits[w] : bits;
+      err |= s_err[w];
+      mx = s_mx[w] > mx ? s_mx[w] : mx;
+      mn = s_mn[w] < mn ? s_mn[w] : mn;
+    }
+    atomicMax(&h->acc_bits, (unsigned long long)bits);
+    atomicMax(&h->acc_max, (long long)mx);
+    atomicMin(&h->acc_min, (long long)mn);
+    if (err) atomicOr(&h->acc_err, err);
+    __threadfence();
+    unsigned int done = atomicAdd(&h->acc_done, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    volatile Hdr* vh = h;
+    int fbits = (int)vh->acc_bits;
+    int64_t fmx = vh->acc_max, fmn = vh->acc_min;
+    int ferr = vh->acc_err;
+    // reset accumulators for the next op writing this block
+    h->acc_bits = 0;
+    h->acc_max = INT64_MIN;
+    h->acc_min = INT64_MAX;
+    h->acc_err = 0;
+    h->acc_done = 0;
+    fin(fbits < 1 ? 1 : fbits, fmx, fmn, ferr);
+  }
+}
+
+__device__ inline void write_trace(const WinParams& p, const WinCtx& c, int ovf, int unf, int rc,
+                                   int normalized) {
+  if (p.trace == nullptr || p.trace_slot < 0) return;
+  TraceRec& t = p.trace[p.trace_slot];
+  t.step = p.step;
+  t.level = p.level;
+  t.w_out = (int32_t)p.w_out;
+  t.w_tmp = (int32_t)(normalized ? p.w_tmp : p.w_out);
+  t.gm = c.gm;
+  t.ge = c.ge;
+  t.overflow = ovf;
+  t.underflow = unf;
+  t.recomputed = rc;
+  t.normalized = normalized;
+}
+
+// window setup common to all ops: e* from the op's template, gamma from the rule
+__device__ inline void win_setup(const WinParams& p, const Hdr* out_h, int64_t e_star,
+                                 int storage_bits, WinCtx& c) {
+  c.e_star = e_star;
+  c.skip = 0;
+  if (p.mode == MODE_RECOMPUTE) {
+    c.skip = !out_h->need_recompute;
+    c.lam = out_h->lam_out;
+    c.store_tmp = 1;
+    return;
+  }
+  gamma_eval(p.gamma, c.gm, c.ge);
+  c.mu_tmp = msb(c.gm) + c.ge - e_star;
+  if (p.mode == MODE_QCOMP) {
+    c.lam = c.mu_tmp - p.w_tmp;          // lam_tmp
+    c.store_tmp = p.w_tmp <= storage_bits && !p.force;
+  } else {
+    c.lam = c.mu_tmp - p.w_out;          // lam_out
+    c.store_tmp = 1;
+  }
+}
+
+// per-element window application: returns the value to store
+template <typename A>
+__device__ __forceinline__ int64_t win_apply(const WinParams& p, const WinCtx& c, A z, Red& r) {
+  if (p.mode == MODE_QCOMP) {
+    int b = msb(z);
+    r.bits = b > r.bits ? b : r.bits;
+    int64_t t = c.store_tmp ? wrap_shift<A>(z, c.lam, p.w_tmp) : 0;
+    r.val(t);
+    return t;
+  } else if (p.mode == MODE_NNQ) {
+    int64_t t = shift_clamp<A>(z, c.lam, p.w_out);
+    r.val(t);
+    return t;
+  }
+  int64_t t = shift_exact<A>(z, c.lam);
+  r.val(t);
+  return t;
+}
+
+__device__ inline void write_hist(const WinParams& p, const Hdr* h) {
+  if (p.hist == nullptr || p.hist_slot < 0) return;
+  p.hist[p.hist_slot] = ldexp((double)max_abs(h), (int)h->e);
+}
+
+// finalize for one launch (runs on one thread)
+__device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, int bits,
+                                    int64_t mx, int64_t mn, int err) {
+  if (err) h->err |= err;
+  if (p.mode == MODE_QCOMP) {
+    int64_t mu_star = bits;                 // src/blas.cpp:153,158
+    int64_t lam_out = mu_star - p.w_out;    // :164
+    int ovf = c.mu_tmp < mu_star;           // :167
+    int unf = lam_out < c.lam;              // :168
+    int rc = ovf || unf || p.force || !c.store_tmp || err;
+    h->q = p.w_out;
+    h->e = c.e_star + lam_out;
+    h->lam_out = lam_out;
+    h->need_recompute = rc;
+    if (!rc) {
+      h->shift = lam_out - c.lam;           // deferred fast-path shift (:178-184)
+      h->max_m = mx;
+      h->min_m = mn;
+      write_hist(p, h);
+    }
+    h->flags = (ovf ? FLAG_OVERFLOW : 0) | (unf ? FLAG_UNDERFLOW : 0) |
+               (rc ? FLAG_RECOMPUTED : 0) | FLAG_NORMALIZED;
+    write_trace(p, c, ovf, unf, rc, 1);
+  } else if (p.mode == MODE_NNQ) {
+    h->q = p.w_out;
+    h->e = c.e_star + c.lam;                // src/blas.cpp:211
+    h->shift = 0;
+    h->max_m = mx;
+    h->min_m = mn;
+    h->need_recompute = 0;
+    h->flags = 0;
+    write_trace(p, c, 0, 0, 0, 0);
+    write_hist(p, h);
+  } else {
+    h->shift = 0;
+    h->max_m = mx;
+    h->min_m = mn;
+    h->need_recompute = 0;
+    write_hist(p, h);
+  }
+}
+
+}  // namespace bfpdev

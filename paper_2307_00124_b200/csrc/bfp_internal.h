@@ -1,0 +1,64 @@
+// bfp_internal.h -- host-side structures and op launchers shared by the C-ABI
+// (bfp_lib.cu) and the native multigrid driver (bfp_solver.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "../../include/bfpmg_b200.h"
+#include "bfp_dev.cuh"
+#include "bfp_ops.cuh"
+
+struct bfp_vec_s {
+  int dim = 0, l = 0, ebytes = 4;
+  int64_t nlog = 0, span = 0, halo = 0;
+  char* base = nullptr;  // device allocation (halo + span + halo)
+  void* data = nullptr;  // element 0
+  bfpdev::Hdr* hdr = nullptr;
+  void* stage = nullptr;  // device staging in logical order (uploads / downloads)
+  size_t stage_bytes = 0;
+  double* tab = nullptr;  // sine table (generator)
+  int64_t tab_n = 0;
+};
+
+struct bfp_csr_s {
+  bfpdev::CsrDev d;
+  int64_t* buf = nullptr;
+};
+
+namespace bfp {
+
+using bfpdev::GammaRule;
+using bfpdev::Scal;
+using bfpdev::WinParams;
+
+bfpdev::Vec view(const bfp_vec_s* v);
+int vec_alloc(int dim, int level, int64_t n, int ebytes, bfp_vec_s** out);
+void vec_free(bfp_vec_s* v);
+int set_zero(bfp_vec_s* v, int64_t q, cudaStream_t s);
+
+WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force);
+GammaRule gamma_literal(int64_t m, int64_t e);
+
+// windowed ops (mode in p: MODE_QCOMP launches pass 1 + recompute, MODE_NNQ one pass)
+int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
+            cudaStream_t s);
+int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s* out,
+              cudaStream_t s);
+int op_scal(bfp_vec_s* r, Scal c, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
+int op_axpby(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
+             cudaStream_t s);
+int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
+int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
+int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_s* out,
+                       cudaStream_t s);
+
+int gen_uniform(bfp_vec_s* v, int64_t p, uint64_t seed, uint64_t stream_id, cudaStream_t s);
+int gen_sine(bfp_vec_s* v, int64_t p, cudaStream_t s);
+
+void jacobi_coeff(int dim, int level, int64_t qc, int64_t* cm, int64_t* ce);
+void count_launch(int n = 1);
+int64_t launches();
+
+}  // namespace bfp

@@ -1,0 +1,420 @@
+// bfp_ops.cuh -- exact-row "ExactKernel" functors for sm_100a.
+//
+// Each op mirrors one reference ExactKernel (include/bfpmg/blas.hpp:25-31):
+// setup() computes the reference template exponent e* from the DEVICE headers
+// of its operands (src/blas.cpp:41-58, 74-82, 96-120) plus a tight bound on the
+// accumulator width from the operands' ACTUAL max/min mantissas, so the
+// kernel picks int64 or __int128 accumulation uniformly per launch; eval4()
+// produces 4 consecutive exact rows at an output storage offset.
+//
+// Grid vectors use a padded layout: pitch N = 2^l on
+// every axis, index N-1 of each axis is a zero pad, plus a zero halo in front
+// and behind.  Every Dirichlet neighbour is therefore a plain load of a zero,
+// and every 4-group of outputs is one aligned 128-bit (int32) store.
+#pragma once
+#include "bfp_dev.cuh"
+
+namespace bfpdev {
+
+__host__ __device__ __forceinline__ int64_t ceil_log2_h(int64_t m) {
+  int64_t r = 0, v = 1;
+  while (v < m) {
+    v <<= 1;
+    ++r;
+  }
+  return r;
+}
+__host__ __device__ __forceinline__ int64_t imax(int64_t a, int64_t b) { return a > b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+struct Scal {
+  int64_t m, q, e;
+};
+
+// eaxpby setup (src/blas.cpp:46-58): d = ea - eb, e* = min(ea, eb)
+__device__ __forceinline__ void axpby_setup(int64_t ea, int64_t eb, int64_t& d, int64_t& es) {
+  d = ea - eb;
+  es = imin(ea, eb);
+}
+// alpha*a*2^max(d,0) + beta*b*2^max(-d,0)  (src/blas.cpp:60-72, 133-141)
+template <typename A>
+__device__ __forceinline__ A combine(int64_t am, A a, int64_t bm, A b, int64_t d) {
+  // shift counts beyond the accumulator only occur on provably-zero operands
+  // (the width bound of setup() excludes them), so clamping is exact.
+  constexpr int64_t B = AccBits<A>::value - 1;
+  A ta = (A)am * a, tb = (A)bm * b;
+  if (d < 0)
+    tb = tb << (int)imin(-d, B);
+  else
+    ta = ta << (int)imin(d, B);
+  return ta + tb;
+}
+// width bound of alpha*a*2^max(d,0) + beta*b*2^max(-d,0) given operand widths
+// (a width of 0 marks an all-zero operand, whose term is excluded)
+__device__ __forceinline__ int64_t combine_bits(int64_t am, int64_t ba, int64_t bm, int64_t bb,
+                                                int64_t d) {
+  int64_t x = (ba && am) ? msb((int64_t)am) + ba + (d > 0 ? d : 0) : 0;
+  int64_t y = (bb && bm) ? msb((int64_t)bm) + bb + (d < 0 ? -d : 0) : 0;
+  return imax(imax(x, y), 1) + 1;
+}
+// width of a block's values, 0 if the block is all zero
+__device__ __forceinline__ int64_t zbits(const Hdr* h) { return max_abs(h) ? eff_bits(h) : 0; }
+__device__ __forceinline__ int64_t grow(int64_t b, int64_t extra) { return b ? b + extra : 0; }
+
+// ---- vector loads (pending shift applied) ---------------------------------
+
+template <typename M> struct V4;
+template <> struct V4<int32_t> {
+  __device__ static __forceinline__ void load(const Vec& v, int64_t o, int64_t sh, int64_t r[4]) {
+    int4 t = __ldg(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
+    r[0] = ((int64_t)t.x) >> sh;
+    r[1] = ((int64_t)t.y) >> sh;
+    r[2] = ((int64_t)t.z) >> sh;
+    r[3] = ((int64_t)t.w) >> sh;
+  }
+  __device__ static __forceinline__ void store(const Vec& v, int64_t o, const int64_t r[4]) {
+    int4 t = make_int4((int)r[0], (int)r[1], (int)r[2], (int)r[3]);
+    *reinterpret_cast<int4*>((int32_t*)v.data + o) = t;
+  }
+};
+template <> struct V4<int64_t> {
+  __device__ static __forceinline__ void load(const Vec& v, int64_t o, int64_t sh, int64_t r[4]) {
+    const longlong2* p = reinterpret_cast<const longlong2*>((const int64_t*)v.data + o);
+    longlong2 a = __ldg(p), b = __ldg(p + 1);
+    r[0] = a.x >> sh;
+    r[1] = a.y >> sh;
+    r[2] = b.x >> sh;
+    r[3] = b.y >> sh;
+  }
+  __device__ static __forceinline__ void store(const Vec& v, int64_t o, const int64_t r[4]) {
+    longlong2* p = reinterpret_cast<longlong2*>((int64_t*)v.data + o);
+    p[0] = make_longlong2(r[0], r[1]);
+    p[1] = make_longlong2(r[2], r[3]);
+  }
+};
+template <typename M> __device__ __forceinline__ int64_t ld1(const Vec& v, int64_t o, int64_t sh) {
+  return ((int64_t)__ldg((const M*)v.data + o)) >> sh;
+}
+
+// pad mask of 4 consecutive grid storage offsets starting at o (o % 4 == 0)
+__device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4]) {
+  const int64_t N = (int64_t)1 << l, mask = N - 1;
+  bool rowpad = false;
+  if (dim >= 2) rowpad |= ((o >> l) & mask) == mask;
+  if (dim >= 3) rowpad |= ((o >> (2 * l)) & mask) == mask;
+  const int64_t ix = o & mask;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) pad[j] = rowpad || (ix + j == mask);
+}
+
+// stencil S_d applied to 4 consecutive points at storage offset o (mantissa units)
+template <typename M, typename A>
+__device__ __forceinline__ void stencil4(const Vec& x, int64_t sx, int dim, int l, int64_t o,
+                                         A g[4], int64_t c[4]) {
+  V4<M>::load(x, o, sx, c);
+  int64_t lf = ld1<M>(x, o - 1, sx), rt = ld1<M>(x, o + 4, sx);
+  A nb[4];
+  nb[0] = (A)lf + (A)c[1];
+  nb[1] = (A)c[0] + (A)c[2];
+  nb[2] = (A)c[1] + (A)c[3];
+  nb[3] = (A)c[2] + (A)rt;
+  if (dim >= 2) {
+    const int64_t N = (int64_t)1 << l;
+    int64_t u[4], d[4];
+    V4<M>::load(x, o - N, sx, u);
+    V4<M>::load(x, o + N, sx, d);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nb[j] += (A)u[j] + (A)d[j];
+    if (dim >= 3) {
+      const int64_t N2 = N * N;
+      V4<M>::load(x, o - N2, sx, u);
+      V4<M>::load(x, o + N2, sx, d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) nb[j] += (A)u[j] + (A)d[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) g[j] = (A)(2 * dim) * (A)c[j] - nb[j];
+}
+
+// ---------------------------------------------------------------------------
+// z = alpha*(A_l x) + beta*y  (EgemvKernel with A = 2^{2l} S_d)
+
+struct GemvOp {
+  Vec x, y;
+  Scal al, be;
+  int dim, l;
+  // derived
+  int64_t sx, sy, d;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    const int64_t qa_s = msb_h(2 * dim), ea_s = 2 * l, ma = 2 * dim + 1;
+    const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = ea_s + x.hdr->e;
+    (void)gq;
+    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
+    sx = x.hdr->shift;
+    sy = y.hdr->shift;
+    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1);
+    need = combine_bits(al.m, bg, be.m, zbits(y.hdr), d);
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    A g[4];
+    int64_t c[4], yv[4];
+    stencil4<M, A>(x, sx, dim, l, o, g, c);
+    V4<M>::load(y, o, sy, yv);
+    bool pad[4];
+    pad4(dim, l, o, pad);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : combine<A>(al.m, g[j], be.m, (A)yv[j], d);
+  }
+};
+
+// z = x + c*(b - A_l x): egemv(A,x,b,-1,+1) composed with eaxpby(x,r,+1,c)
+struct JacobiOp {
+  Vec x, b;
+  Scal c;
+  int dim, l;
+  int64_t sx, sb, d1, d2;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    const int64_t qa_s = msb_h(2 * dim), ma = 2 * dim + 1;
+    const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = 2 * l + x.hdr->e;
+    int64_t er;
+    axpby_setup(ge, b.hdr->e, d1, er);      // r template (alpha q=1 e=0, beta q=2 e=0)
+    (void)gq;
+    axpby_setup(x.hdr->e, c.e + er, d2, e_star);
+    sx = x.hdr->shift;
+    sb = b.hdr->shift;
+    int64_t bx = zbits(x.hdr);
+    int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
+    int64_t br = combine_bits(-1, bg, 1, zbits(b.hdr), d1);
+    need = combine_bits(1, bx, c.m, br, d2);
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    A g[4];
+    int64_t cx[4], bv[4];
+    stencil4<M, A>(x, sx, dim, l, o, g, cx);
+    V4<M>::load(b, o, sb, bv);
+    bool pad[4];
+    pad4(dim, l, o, pad);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      A r = combine<A>(-1, g[j], 1, (A)bv[j], d1);
+      z[j] = pad[j] ? A(0) : combine<A>(1, (A)cx[j], c.m, r, d2);
+    }
+  }
+};
+
+// z = c*r (pointwise over the storage span; pads stay zero)
+struct ScalOp {
+  Vec r;
+  Scal c;
+  int64_t sr;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    e_star = c.e + r.hdr->e;
+    sr = r.hdr->shift;
+    need = msb((int64_t)c.m) + eff_bits(r.hdr) + 1;
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    int64_t v[4];
+    V4<M>::load(r, o, sr, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = (A)c.m * (A)v[j];
+  }
+};
+
+// z = alpha*x*2^max(d,0) + beta*y*2^max(-d,0)  (EaxpbyKernel, pointwise)
+struct AxpbyOp {
+  Vec x, y;
+  Scal al, be;
+  int64_t sx, sy, d;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    axpby_setup(al.e + x.hdr->e, be.e + y.hdr->e, d, e_star);
+    sx = x.hdr->shift;
+    sy = y.hdr->shift;
+    need = combine_bits(al.m, zbits(x.hdr), be.m, zbits(y.hdr), d);
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    int64_t xv[4], yv[4];
+    V4<M>::load(x, o, sx, xv);
+    V4<M>::load(y, o, sy, yv);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = combine<A>(al.m, (A)xv[j], be.m, (A)yv[j], d);
+  }
+};
+
+// coarse z = R r, full weighting R = (1,2,1)^{(x)d} 2^{-2d}  (EspmvKernel)
+struct RestrictOp {
+  Vec r;       // fine, level l
+  int dim, l;  // fine level
+  int64_t sr;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    e_star = -2 * dim + r.hdr->e;
+    sr = r.hdr->shift;
+    need = eff_bits(r.hdr) + 2 * dim + 2;
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    const int lc = l - 1;
+    const int64_t Nc = (int64_t)1 << lc, mc = Nc - 1, Nf = (int64_t)1 << l;
+    bool pad[4];
+    pad4(dim, lc, o, pad);
+    const int64_t J = (o >> lc) & mc, K = (o >> (2 * lc)) & mc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t I = (o + j) & mc;
+      int64_t fc = 2 * I + 1;
+      if (dim >= 2) fc += (2 * J + 1) * Nf;
+      if (dim >= 3) fc += (2 * K + 1) * Nf * Nf;
+      A acc = 0;
+      if (!pad[j]) {
+        // x-line weights (1,2,1) on each contributing fine row
+        auto line = [&](int64_t base) -> A {
+          return (A)ld1<M>(r, base - 1, sr) + 2 * (A)ld1<M>(r, base, sr) +
+                 (A)ld1<M>(r, base + 1, sr);
+        };
+        if (dim == 1) {
+          acc = line(fc);
+        } else if (dim == 2) {
+          acc = line(fc - Nf) + 2 * line(fc) + line(fc + Nf);
+        } else {
+          const int64_t N2 = Nf * Nf;
+          A pm = line(fc - N2 - Nf) + 2 * line(fc - N2) + line(fc - N2 + Nf);
+          A p0 = line(fc - Nf) + 2 * line(fc) + line(fc + Nf);
+          A pp = line(fc + N2 - Nf) + 2 * line(fc + N2) + line(fc + N2 + Nf);
+          acc = pm + 2 * p0 + pp;
+        }
+      }
+      z[j] = acc;
+    }
+  }
+};
+
+// linear interpolation: per axis taps (i-1)>>1 and i>>1 with weight 1 each
+// (odd i -> both taps = (i-1)/2, i.e. weight 2).  Coarse pads/halo are zero.
+template <typename M, typename A>
+__device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int l, int64_t o) {
+  const int64_t Nf = (int64_t)1 << l, mf = Nf - 1;
+  const int lc = l - 1;
+  const int64_t Nc = (int64_t)1 << lc;
+  const int64_t i = o & mf;
+  const int64_t a0 = (i - 1) >> 1, a1 = i >> 1;
+  if (dim == 1) return (A)ld1<M>(xc, a0, sc) + (A)ld1<M>(xc, a1, sc);
+  const int64_t j = (o >> l) & mf;
+  const int64_t b0 = ((j - 1) >> 1) * Nc, b1 = (j >> 1) * Nc;
+  auto line = [&](int64_t rowoff) -> A {
+    return (A)ld1<M>(xc, rowoff + a0, sc) + (A)ld1<M>(xc, rowoff + a1, sc);
+  };
+  if (dim == 2) return line(b0) + line(b1);
+  const int64_t k = (o >> (2 * l)) & mf;
+  const int64_t Nc2 = Nc * Nc;
+  const int64_t c0 = ((k - 1) >> 1) * Nc2, c1 = (k >> 1) * Nc2;
+  return line(c0 + b0) + line(c0 + b1) + line(c1 + b0) + line(c1 + b1);
+}
+
+// fine z = P xc  (EspmvKernel with P, m_P = 2^d, e_P = -d, q_P = d+2)
+struct ProlongOp {
+  Vec xc;
+  int dim, l;  // fine level
+  int64_t sc;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    e_star = -dim + xc.hdr->e;
+    sc = xc.hdr->shift;
+    need = eff_bits(xc.hdr) + dim + 2;
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    bool pad[4];
+    pad4(dim, l, o, pad);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : prolong_at<M, A>(xc, sc, dim, l, o + j);
+  }
+};
+
+// fine z = P ec + y  (EgemvKernel(P, ec, y, bfp_one, bfp_one))
+struct ProlongCorrectOp {
+  Vec ec, y;
+  int dim, l;
+  int64_t sc, sy, d;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    const int64_t ge = -dim + ec.hdr->e;
+    axpby_setup(ge, y.hdr->e, d, e_star);
+    sc = ec.hdr->shift;
+    sy = y.hdr->shift;
+    int64_t bg = grow(zbits(ec.hdr), dim + 2);
+    need = combine_bits(1, bg, 1, zbits(y.hdr), d);
+  }
+  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    bool pad[4];
+    pad4(dim, l, o, pad);
+    int64_t yv[4];
+    V4<M>::load(y, o, sy, yv);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      A g = prolong_at<M, A>(ec, sc, dim, l, o + j);
+      z[j] = pad[j] ? A(0) : combine<A>(1, g, 1, (A)yv[j], d);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// flat (one row per thread, int128 accumulation) ops for the generic CSR path
+
+struct CsrDev {
+  int64_t rows, cols, q, e, max_row_nnz;
+  const int64_t *rowptr, *col, *m;
+};
+
+// z = A x  (EspmvKernel, src/blas.cpp:74-94)
+struct CsrSpmvOp {
+  CsrDev a;
+  Vec x;
+  int64_t m_a;
+  int64_t sx;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    e_star = a.e + x.hdr->e;
+    sx = x.hdr->shift;
+    need = a.q + eff_bits(x.hdr) + ceil_log2_h(imax(m_a, 1)) + 1;
+  }
+  template <typename M> __device__ __forceinline__ i128 eval1(int64_t i) {
+    i128 acc = 0;
+    for (int64_t k = a.rowptr[i]; k < a.rowptr[i + 1]; ++k)
+      acc += (i128)a.m[k] * (i128)ld1<M>(x, a.col[k], sx);
+    return acc;
+  }
+};
+
+// z = alpha A x + beta y  (EgemvKernel, src/blas.cpp:96-142)
+struct CsrGemvOp {
+  CsrDev a;
+  Vec x, y;
+  Scal al, be;
+  int64_t m_a;
+  int64_t sx, sy, d;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    const int64_t ge = a.e + x.hdr->e;
+    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
+    sx = x.hdr->shift;
+    sy = y.hdr->shift;
+    int64_t bg = grow(zbits(x.hdr), a.q + ceil_log2_h(imax(m_a, 1)) + 1);
+    need = combine_bits(al.m, bg, be.m, zbits(y.hdr), d);
+  }
+  template <typename M> __device__ __forceinline__ i128 eval1(int64_t i) {
+    i128 g = 0;
+    for (int64_t k = a.rowptr[i]; k < a.rowptr[i + 1]; ++k)
+      g += (i128)a.m[k] * (i128)ld1<M>(x, a.col[k], sx);
+    return combine<i128>(al.m, g, be.m, (i128)ld1<M>(y, i, sy), d);
+  }
+};
+
+// explicit exact rows (the test FixedKernel, tests/test_blas.cpp:14-26)
+struct RowsOp {
+  const int64_t* hi;
+  const uint64_t* lo;
+  int64_t e;
+  __device__ void setup(int64_t& e_star, int64_t& need) {
+    e_star = e;
+    need = 0;
+  }
+  template <typename M> __device__ __forceinline__ i128 eval1(int64_t i) {
+    return (i128)(((u128)(uint64_t)hi[i] << 64) | (u128)lo[i]);
+  }
+};
+
+}  // namespace bfpdev

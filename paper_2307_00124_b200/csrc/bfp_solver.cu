@@ -1,0 +1,419 @@
+// bfp_solver.cu -- native multigrid driver.
+//
+// Mirrors the reference solver structure (paths relative to /root/reference/proj):
+//   run_step   src/multigrid.cpp:399-426   (one windowed op + trace record)
+//   vcycle     src/multigrid.cpp:430-456   (correction scheme, here Jacobi V(nu1,nu2))
+//   ir         src/multigrid.cpp:458-500   (iterative refinement, residual history)
+//   fmg        src/multigrid.cpp:502-518   (zero_vec on the coarsest level, prolong, n_ir IR)
+// with the frozen config semantics of DESIGN.md.  Because exponents, norms and
+// gamma rules live in device headers, the whole solve is a static PLAN of
+// kernel launches: built once, replayed stream-ordered or as one CUDA graph.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "bfp_internal.h"
+
+using namespace bfpdev;
+using namespace bfp;
+
+namespace {
+
+enum StepKind {
+  ST_IR_RES = 0, ST_IR_CORR, ST_RELAX0, ST_RELAX, ST_V_RES, ST_RESTRICT, ST_V_CORR,
+  ST_FMG_PROLONG, ST_FINAL_RES
+};
+enum OpKind { OK_ZERO, OK_UNIFORM, OK_GEMV, OK_JACOBI, OK_SCAL, OK_AXPBY, OK_RESTRICT,
+              OK_PROLONG, OK_PCORR };
+
+struct PlanOp {
+  int kind;
+  bfp_vec_s *a = nullptr, *b = nullptr, *out = nullptr;
+  Scal s1{0, 0, 0}, s2{0, 0, 0};
+  WinParams p;
+  int64_t q = 0;
+  uint64_t seed = 0, sid = 0;
+};
+
+struct LevelBufs {
+  int l = 0;
+  int64_t p = 0;
+  Scal c{0, 0, 0};
+  bfp_vec_s *b = nullptr, *x[2] = {nullptr, nullptr}, *r[2] = {nullptr, nullptr};
+  bfp_vec_s *e[2] = {nullptr, nullptr}, *rv = nullptr, *vr = nullptr;
+};
+
+GTerm term(const bfp_vec_s* v, int64_t cm = 0, int64_t ce = 0, int kind = 0) {
+  GTerm t;
+  memset(&t, 0, sizeof(t));
+  t.v = v ? v->hdr : nullptr;
+  t.cm = cm;
+  t.ce = ce;
+  t.kind = kind;
+  return t;
+}
+GammaRule rule(std::initializer_list<GTerm> ts) {
+  GammaRule g;
+  memset(&g, 0, sizeof(g));
+  g.literal = 0;
+  g.nterms = 0;
+  for (const GTerm& t : ts) g.t[g.nterms++] = t;
+  return g;
+}
+
+}  // namespace
+
+struct bfp_mg_s {
+  bfp_mg_config_t cfg;
+  int ebytes = 4;
+  std::vector<LevelBufs> lev;  // indexed by level
+  std::vector<PlanOp> plan;
+  TraceRec* d_trace = nullptr;
+  double* d_hist = nullptr;
+  int n_trace = 0, n_hist = 0;
+  bfp_vec_s* x_final = nullptr;
+  bfp_vec_s* r_final = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t launches_per_solve = 0;
+  std::vector<bfp_vec_s*> owned;
+  int err = 0;
+
+  ~bfp_mg_s() {
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto* v : owned) vec_free(v);
+    cudaFree(d_trace);
+    cudaFree(d_hist);
+  }
+
+  bfp_vec_s* vec(int l) {
+    bfp_vec_s* v = nullptr;
+    int rc = vec_alloc(cfg.d, l, 0, ebytes, &v);
+    if (rc) {
+      err = rc;
+      return nullptr;
+    }
+    owned.push_back(v);
+    return v;
+  }
+
+  // run_step: one windowed op (qcomp, or nnqcomp in nonnormalized mode)
+  void step(int st, int level, PlanOp op, int64_t w_out, const GammaRule& g, int w_add,
+            bool hist = false) {
+    const bool normalized = !cfg.nonnormalized || st == ST_FINAL_RES;
+    op.p = win_params(normalized ? MODE_QCOMP : MODE_NNQ, w_out, w_out + w_add, 0);
+    op.p.gamma = g;
+    op.p.trace_slot = n_trace++;
+    op.p.step = st;
+    op.p.level = level;
+    if (hist) op.p.hist_slot = n_hist++;
+    plan.push_back(op);
+  }
+
+  bfp_vec_s* vcycle(int l, bfp_vec_s* r) {
+    LevelBufs& L = lev[l];
+    bfp_vec_s *e = L.e[0], *t = L.e[1];
+    PlanOp o;
+    o.kind = OK_SCAL;
+    o.a = r;
+    o.out = e;
+    o.s1 = L.c;
+    step(ST_RELAX0, l, o, L.p, rule({term(r, L.c.m, L.c.e)}), 2);
+    const int sweeps = l == cfg.l_coarse ? cfg.n_coarse : cfg.nu1;
+    auto jac = [&]() {
+      PlanOp j;
+      j.kind = OK_JACOBI;
+      j.a = e;
+      j.b = r;
+      j.out = t;
+      j.s1 = L.c;
+      step(ST_RELAX, l, j, L.p, rule({term(e), term(r, L.c.m, L.c.e)}), 3);
+      std::swap(e, t);
+    };
+    for (int s = 1; s < sweeps; ++s) jac();
+    if (l == cfg.l_coarse) return e;
+    PlanOp g;
+    g.kind = OK_GEMV;
+    g.a = e;
+    g.b = r;
+    g.out = L.rv;
+    g.s1 = Scal{-1, 1, 0};
+    g.s2 = Scal{1, 2, 0};
+    step(ST_V_RES, l, g, L.p, rule({term(r)}), 4);
+    LevelBufs& Lc = lev[l - 1];
+    PlanOp rs;
+    rs.kind = OK_RESTRICT;
+    rs.a = L.rv;
+    rs.out = Lc.vr;
+    step(ST_RESTRICT, l, rs, L.p, rule({term(L.rv)}), 6);
+    bfp_vec_s* ec = vcycle(l - 1, Lc.vr);
+    PlanOp pc;
+    pc.kind = OK_PCORR;
+    pc.a = ec;
+    pc.b = e;
+    pc.out = t;
+    step(ST_V_CORR, l, pc, L.p, rule({term(e), term(ec)}), 2);
+    std::swap(e, t);
+    for (int s = 0; s < cfg.nu2; ++s) jac();
+    return e;
+  }
+
+  // returns the buffer holding the final iterate; r_last gets the last residual buffer
+  bfp_vec_s* ir(int l, bfp_vec_s* x, int iters, bfp_vec_s** r_last) {
+    LevelBufs& L = lev[l];
+    int ri = 0;
+    bfp_vec_s* r_prev = nullptr;
+    for (int i = 1; i <= iters; ++i) {
+      const bool first = r_prev == nullptr;
+      GammaRule g = first ? rule({term(L.b), term(x, 4 * cfg.d, 2 * l, 1)}) : rule({term(r_prev)});
+      bfp_vec_s* r = L.r[ri];
+      ri ^= 1;
+      PlanOp o;
+      o.kind = OK_GEMV;
+      o.a = x;
+      o.b = L.b;
+      o.out = r;
+      o.s1 = Scal{-1, 1, 0};
+      o.s2 = Scal{1, 2, 0};
+      step(ST_IR_RES, l, o, L.p, g, first ? 5 : 4, true);
+      r_prev = r;
+      bfp_vec_s* e = vcycle(l, r);
+      bfp_vec_s* xn = (x == L.x[0]) ? L.x[1] : L.x[0];
+      PlanOp c;
+      c.kind = OK_AXPBY;
+      c.a = x;
+      c.b = e;
+      c.out = xn;
+      c.s1 = Scal{1, 2, 0};
+      c.s2 = Scal{1, 2, 0};
+      step(ST_IR_CORR, l, c, L.p, rule({term(x), term(e)}), 1);
+      x = xn;
+    }
+    *r_last = r_prev;
+    return x;
+  }
+
+  void final_residual(int l, bfp_vec_s* x, bfp_vec_s* r_last) {
+    LevelBufs& L = lev[l];
+    bfp_vec_s* r = (r_last == L.r[0]) ? L.r[1] : L.r[0];
+    PlanOp o;
+    o.kind = OK_GEMV;
+    o.a = x;
+    o.b = L.b;
+    o.out = r;
+    o.s1 = Scal{-1, 1, 0};
+    o.s2 = Scal{1, 2, 0};
+    step(ST_FINAL_RES, l, o, L.p, rule({term(r_last)}), 4, true);
+    r_final = r;
+  }
+
+  bfp_vec_s* fmg(int l) {
+    LevelBufs& L = lev[l];
+    bfp_vec_s* x = L.x[0];
+    if (l == cfg.l_coarse) {
+      PlanOp z;
+      z.kind = OK_ZERO;
+      z.out = x;
+      z.q = L.p;
+      plan.push_back(z);
+    } else {
+      bfp_vec_s* xc = fmg(l - 1);
+      PlanOp o;
+      o.kind = OK_PROLONG;
+      o.a = xc;
+      o.out = x;
+      step(ST_FMG_PROLONG, l, o, L.p, rule({term(xc)}), 1);
+    }
+    bfp_vec_s* r_last = nullptr;
+    x = ir(l, x, cfg.cycles, &r_last);
+    if (l == cfg.l_fine && r_last) final_residual(l, x, r_last);
+    return x;
+  }
+
+  int build() {
+    const int lf = cfg.l_fine, lc = cfg.l_coarse;
+    int maxp = 0;
+    for (int l = lc; l <= lf; ++l) maxp = std::max(maxp, cfg.p[l] + 6);
+    ebytes = maxp <= 32 ? 4 : 8;
+    lev.assign(lf + 1, LevelBufs());
+    for (int l = lc; l <= lf; ++l) {
+      LevelBufs& L = lev[l];
+      L.l = l;
+      L.p = cfg.p[l];
+      int64_t cm, ce;
+      jacobi_coeff(cfg.d, l, cfg.qc, &cm, &ce);
+      L.c = Scal{cm, cfg.qc, ce};
+      const bool need_rhs = cfg.fmg || l == lf;
+      if (need_rhs) {
+        L.b = vec(l);
+        L.x[0] = vec(l);
+        L.x[1] = vec(l);
+        L.r[0] = vec(l);
+        L.r[1] = vec(l);
+      }
+      L.e[0] = vec(l);
+      L.e[1] = vec(l);
+      if (l > lc) L.rv = vec(l);
+      if (l < lf) L.vr = vec(l);
+      if (err) return err;
+    }
+    // inputs (setup, outside the solve): right-hand sides
+    for (int l = lc; l <= lf; ++l) {
+      LevelBufs& L = lev[l];
+      if (!L.b) continue;
+      int rc;
+      if (cfg.rhs_kind == 1)
+        rc = gen_sine(L.b, L.p, 0);
+      else if (cfg.rhs_kind == 0)
+        rc = gen_uniform(L.b, L.p, cfg.seed, 2, 0);
+      else
+        rc = set_zero(L.b, L.p, 0);
+      if (rc) return rc;
+    }
+    // the plan
+    if (cfg.fmg) {
+      x_final = fmg(lf);
+    } else {
+      LevelBufs& L = lev[lf];
+      PlanOp init;
+      init.out = L.x[0];
+      if (cfg.x0_random) {
+        init.kind = OK_UNIFORM;
+        init.q = L.p;
+        init.seed = cfg.seed;
+        init.sid = 1;
+      } else {
+        init.kind = OK_ZERO;
+        init.q = L.p;
+      }
+      plan.push_back(init);
+      bfp_vec_s* r_last = nullptr;
+      x_final = ir(lf, L.x[0], cfg.cycles, &r_last);
+      if (r_last) final_residual(lf, x_final, r_last);
+    }
+    if (cudaMalloc(&d_trace, sizeof(TraceRec) * std::max(n_trace, 1)) != cudaSuccess ||
+        cudaMalloc(&d_hist, sizeof(double) * std::max(n_hist, 1)) != cudaSuccess)
+      return BFP_ERR_NOMEM;
+    cudaMemset(d_trace, 0, sizeof(TraceRec) * std::max(n_trace, 1));
+    cudaMemset(d_hist, 0, sizeof(double) * std::max(n_hist, 1));
+    for (auto& op : plan) {
+      op.p.trace = d_trace;
+      op.p.hist = op.p.hist_slot >= 0 ? d_hist : nullptr;
+    }
+    return cudaDeviceSynchronize() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+  }
+
+  int execute(cudaStream_t s) {
+    const int64_t before = launches();
+    for (const PlanOp& op : plan) {
+      int rc = BFP_OK;
+      switch (op.kind) {
+        case OK_ZERO: rc = set_zero(op.out, op.q, s); break;
+        case OK_UNIFORM: rc = gen_uniform(op.out, op.q, op.seed, op.sid, s); break;
+        case OK_GEMV: rc = op_gemv(op.a, op.b, op.s1, op.s2, op.p, op.out, s); break;
+        case OK_JACOBI: rc = op_jacobi(op.a, op.b, op.s1, op.p, op.out, s); break;
+        case OK_SCAL: rc = op_scal(op.a, op.s1, op.p, op.out, s); break;
+        case OK_AXPBY: rc = op_axpby(op.a, op.b, op.s1, op.s2, op.p, op.out, s); break;
+        case OK_RESTRICT: rc = op_restrict(op.a, op.p, op.out, s); break;
+        case OK_PROLONG: rc = op_prolong(op.a, op.p, op.out, s); break;
+        case OK_PCORR: rc = op_prolong_correct(op.a, op.b, op.p, op.out, s); break;
+      }
+      if (rc) return rc;
+    }
+    launches_per_solve = launches() - before;
+    return BFP_OK;
+  }
+};
+
+extern "C" {
+
+int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
+  if (!cfg || !out) return BFP_ERR_ARG;
+  if (cfg->d < 1 || cfg->d > 3 || cfg->l_coarse < 2 || cfg->l_fine < cfg->l_coarse ||
+      cfg->l_fine > 30 || cfg->nu1 < 1 || cfg->nu2 < 0 || cfg->n_coarse < 1 || cfg->cycles < 0 ||
+      cfg->qc < 2 || cfg->qc > 30)
+    return BFP_ERR_ARG;
+  for (int l = cfg->l_coarse; l <= cfg->l_fine; ++l)
+    if (cfg->p[l] < 2 || cfg->p[l] > 58) return BFP_ERR_ARG;
+  bfp_mg_s* mg = new bfp_mg_s();
+  mg->cfg = *cfg;
+  int rc = mg->build();
+  if (rc) {
+    delete mg;
+    return rc;
+  }
+  *out = mg;
+  return BFP_OK;
+}
+
+int bfp_mg_destroy(bfp_mg_t mg) {
+  delete mg;
+  return BFP_OK;
+}
+
+int bfp_mg_solve(bfp_mg_t mg, int use_graph, void* stream) {
+  if (!mg) return BFP_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (!use_graph) return mg->execute(s);
+  if (!mg->graph) {
+    // capture on a private non-default stream, then replay on the caller's
+    cudaStream_t cs;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return BFP_ERR_CUDA;
+    cudaGraph_t g;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaStreamDestroy(cs);
+      return BFP_ERR_CUDA;
+    }
+    const int64_t before = launches();
+    int rc = mg->execute(cs);
+    const int64_t n = launches() - before;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    if (e != cudaSuccess) return BFP_ERR_CUDA;
+    e = cudaGraphInstantiate(&mg->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return BFP_ERR_CUDA;
+    count_launch(-(int)n);  // captured, not launched
+  }
+  count_launch((int)mg->launches_per_solve);
+  return cudaGraphLaunch(mg->graph, s) == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+}
+
+int bfp_mg_result(bfp_mg_t mg, int64_t* x, bfp_header_t* xh, double* hist, int hist_cap,
+                  int* n_hist, bfp_trace_rec_t* trace, int64_t trace_cap, int64_t* n_trace,
+                  void* stream) {
+  if (!mg) return BFP_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int rc = bfp_vec_download(mg->x_final, x, xh, stream);
+  if (rc) return rc;
+  if (hist && hist_cap > 0)
+    cudaMemcpyAsync(hist, mg->d_hist, sizeof(double) * std::min(hist_cap, mg->n_hist),
+                    cudaMemcpyDeviceToHost, s);
+  if (trace && trace_cap > 0)
+    cudaMemcpyAsync(trace, mg->d_trace,
+                    sizeof(TraceRec) * (size_t)std::min<int64_t>(trace_cap, mg->n_trace),
+                    cudaMemcpyDeviceToHost, s);
+  if (n_hist) *n_hist = mg->n_hist;
+  if (n_trace) *n_trace = mg->n_trace;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return BFP_ERR_CUDA;
+  // sticky device errors of any solver vector
+  for (auto* v : mg->owned) {
+    Hdr h;
+    cudaMemcpy(&h, v->hdr, sizeof(h), cudaMemcpyDeviceToHost);
+    if (h.err) return h.err;
+  }
+  return BFP_OK;
+}
+
+int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r) {
+  if (!mg) return BFP_ERR_ARG;
+  const int lf = mg->cfg.l_fine;
+  if (x) *x = mg->lev[lf].x[0];
+  if (b) *b = mg->lev[lf].b;
+  if (r) *r = mg->lev[lf].r[0];
+  return BFP_OK;
+}
+
+int64_t bfp_mg_kernel_launches(bfp_mg_t mg) { return mg ? mg->launches_per_solve : -1; }
+
+}  // extern "C"
