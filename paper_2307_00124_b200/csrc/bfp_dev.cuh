@@ -35,7 +35,7 @@ struct alignas(128) Hdr {
   int32_t need_recompute;
   int32_t pad0;
   // cross-block accumulators (reset by each finalize)
-  unsigned long long acc_bits;  // max msb over exact rows
+  unsigned long long acc_or_lo, acc_or_hi;  // OR over rows of z ^ sign(z): bitlen = max msb - 1
   long long acc_max, acc_min;
   unsigned int acc_done;
   int32_t acc_err;
@@ -279,15 +279,17 @@ struct WinCtx {
   int64_t gm, ge;
   int32_t store_tmp;            // qcomp: tmp fits the storage and is stored
   int32_t skip;                 // recompute pass with nothing to do
+  int32_t rs, ls;               // stored value = (z >> rs) << ls  (lam >= 0: rs = lam)
 };
 
-// per-thread running reductions
+// per-thread running reductions.  mu* = max_i msb(z_i) is recovered exactly
+// from the bitwise OR of z_i ^ sign(z_i): bitlen(a | b) = max(bitlen a, bitlen b).
 struct Red {
-  int bits;
+  uint64_t olo, ohi;
   int64_t mx, mn;
   int err;
   __device__ void init() {
-    bits = 1;
+    olo = ohi = 0;
     mx = INT64_MIN;
     mn = INT64_MAX;
     err = 0;
@@ -297,6 +299,15 @@ struct Red {
     mn = v < mn ? v : mn;
   }
 };
+template <typename A> __device__ __forceinline__ void or_mag(A z, uint64_t& lo, uint64_t& hi);
+template <> __device__ __forceinline__ void or_mag<int64_t>(int64_t z, uint64_t& lo, uint64_t& hi) {
+  lo |= (uint64_t)(z ^ (z >> 63));
+}
+template <> __device__ __forceinline__ void or_mag<i128>(i128 z, uint64_t& lo, uint64_t& hi) {
+  u128 u = (u128)(z ^ (z >> 127));
+  lo |= (uint64_t)u;
+  hi |= (uint64_t)(u >> 64);
+}
 
 __device__ __forceinline__ int64_t shfl_max64(int64_t v) {
 #pragma unroll
@@ -314,21 +325,28 @@ __device__ __forceinline__ int64_t shfl_min64(int64_t v) {
   }
   return v;
 }
+__device__ __forceinline__ uint64_t shfl_or64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 // Block reduce + cross-block atomics + last-block finalize.  `fin` is called
 // by exactly one thread of the last block to finish, after every block's
-// contribution is visible.
+// contribution is visible: fin(mu_star, max, min, err).
 template <typename Fin>
 __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
-  __shared__ int s_bits[32], s_err[32];
+  __shared__ unsigned long long s_lo[32], s_hi[32];
+  __shared__ int s_err[32];
   __shared__ long long s_mx[32], s_mn[32];
   __shared__ bool s_last;
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  int bits = __reduce_max_sync(0xffffffffu, r.bits);
+  uint64_t lo = shfl_or64(r.olo), hi = shfl_or64(r.ohi);
   int err = __reduce_or_sync(0xffffffffu, r.err);
   int64_t mx = shfl_max64(r.mx), mn = shfl_min64(r.mn);
   if (lane == 0) {
-    s_bits[wid] = bits;
+    s_lo[wid] = lo;
+    s_hi[wid] = hi;
     s_err[wid] = err;
     s_mx[wid] = mx;
     s_mn[wid] = mn;
@@ -336,12 +354,14 @@ __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < nw; ++w) {
-      bits = s_bits[w] > bits ? s_bits[w] : bits;
+      lo |= s_lo[w];
+      hi |= s_hi[w];
       err |= s_err[w];
       mx = s_mx[w] > mx ? s_mx[w] : mx;
       mn = s_mn[w] < mn ? s_mn[w] : mn;
     }
-    atomicMax(&h->acc_bits, (unsigned long long)bits);
+    if (lo) atomicOr(&h->acc_or_lo, (unsigned long long)lo);
+    if (hi) atomicOr(&h->acc_or_hi, (unsigned long long)hi);
     atomicMax(&h->acc_max, (long long)mx);
     atomicMin(&h->acc_min, (long long)mn);
     if (err) atomicOr(&h->acc_err, err);
@@ -353,16 +373,18 @@ __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
   if (s_last && threadIdx.x == 0) {
     __threadfence();
     volatile Hdr* vh = h;
-    int fbits = (int)vh->acc_bits;
+    uint64_t flo = vh->acc_or_lo, fhi = vh->acc_or_hi;
     int64_t fmx = vh->acc_max, fmn = vh->acc_min;
     int ferr = vh->acc_err;
     // reset accumulators for the next op writing this block
-    h->acc_bits = 0;
+    h->acc_or_lo = 0;
+    h->acc_or_hi = 0;
     h->acc_max = INT64_MIN;
     h->acc_min = INT64_MAX;
     h->acc_err = 0;
     h->acc_done = 0;
-    fin(fbits < 1 ? 1 : fbits, fmx, fmn, ferr);
+    int bits = (fhi ? 64 + bitlen64(fhi) : bitlen64(flo)) + 1;  // mu* (init 1, src/blas.cpp:153)
+    fin(bits, fmx, fmn, ferr);
   }
 }
 
@@ -391,6 +413,8 @@ __device__ inline void win_setup(const WinParams& p, const Hdr* out_h, int64_t e
     c.skip = !out_h->need_recompute;
     c.lam = out_h->lam_out;
     c.store_tmp = 1;
+    c.rs = (int32_t)(c.lam >= 0 ? (c.lam > 127 ? 127 : c.lam) : 0);
+    c.ls = (int32_t)(c.lam < 0 ? (-c.lam > 64 ? 64 : -c.lam) : 0);
     return;
   }
   gamma_eval(p.gamma, c.gm, c.ge);
@@ -402,25 +426,21 @@ __device__ inline void win_setup(const WinParams& p, const Hdr* out_h, int64_t e
     c.lam = c.mu_tmp - p.w_out;          // lam_out
     c.store_tmp = 1;
   }
+  c.rs = (int32_t)(c.lam >= 0 ? (c.lam > 127 ? 127 : c.lam) : 0);
+  c.ls = (int32_t)(c.lam < 0 ? (-c.lam > 64 ? 64 : -c.lam) : 0);
 }
 
-// per-element window application: returns the value to store
-template <typename A>
-__device__ __forceinline__ int64_t win_apply(const WinParams& p, const WinCtx& c, A z, Red& r) {
-  if (p.mode == MODE_QCOMP) {
-    int b = msb(z);
-    r.bits = b > r.bits ? b : r.bits;
-    int64_t t = c.store_tmp ? wrap_shift<A>(z, c.lam, p.w_tmp) : 0;
-    r.val(t);
-    return t;
-  } else if (p.mode == MODE_NNQ) {
-    int64_t t = shift_clamp<A>(z, c.lam, p.w_out);
-    r.val(t);
-    return t;
-  }
-  int64_t t = shift_exact<A>(z, c.lam);
-  r.val(t);
-  return t;
+// stored value of an exact row: floor(z / 2^lam) truncated to the storage type.
+// qcomp fast path: when no flag fires the w_tmp wrap of src/blas.cpp:160 is the
+// identity, and when a flag fires the recompute pass overwrites the block, so
+// the wrap is never needed; the recompute pass result always fits (T_w_out).
+template <typename M, typename A>
+__device__ __forceinline__ M store_shift(A z, const WinCtx& c) {
+  constexpr int B = AccBits<A>::value;
+  A r = c.rs >= B - 1 ? (z < 0 ? A(-1) : A(0)) : (z >> c.rs);
+  if (c.ls == 0) return (M)r;
+  if (c.ls >= 64) return (M)0;
+  return (M)((uint64_t)r << c.ls);
 }
 
 __device__ inline void write_hist(const WinParams& p, const Hdr* h) {

@@ -49,24 +49,65 @@ int last_launch() {
 // ===========================================================================
 // kernels
 
-template <typename M, typename Op, typename A>
+template <typename M> struct Lim;
+template <> struct Lim<int32_t> {
+  static constexpr int32_t lo = INT32_MIN, hi = INT32_MAX;
+};
+template <> struct Lim<int64_t> {
+  static constexpr int64_t lo = INT64_MIN, hi = INT64_MAX;
+};
+
+// The window pass over 4-groups of the output storage.  MODE is a template
+// parameter so each instantiation carries only its own epilogue:
+//   QCOMP      OR-accumulate |z| bits (mu*), store floor(z/2^lam_tmp)
+//   RECOMPUTE  store floor(z/2^lam_out)
+//   NNQ        store clamp(floor(z/2^lam_out))
+// Max/min of the STORED values are tracked in the storage type.
+template <int MODE, typename M, typename Op, typename A>
 __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r) {
   const int64_t ngroups = out.n >> 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  M mx = Lim<M>::lo, mn = Lim<M>::hi;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
     A z[4];
     op.template eval4<M, A>(g * 4, z);
-    int64_t t[4];
+    M t[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) t[j] = win_apply<A>(p, c, z[j], r);
+    for (int j = 0; j < 4; ++j) {
+      if (MODE == MODE_NNQ) {
+        t[j] = (M)shift_clamp<A>(z[j], c.lam, p.w_out);
+      } else {
+        if (MODE == MODE_QCOMP) or_mag<A>(z[j], olo, ohi);
+        t[j] = store ? store_shift<M, A>(z[j], c) : (M)0;
+      }
+      mx = t[j] > mx ? t[j] : mx;
+      mn = t[j] < mn ? t[j] : mn;
+    }
     V4<M>::store(out, g * 4, t);
   }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.val((int64_t)mx);
+  r.val((int64_t)mn);
+}
+
+template <int MODE, typename M, typename Op>
+__device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r, int64_t need) {
+  if (need > 127)
+    r.err = ERR_WIDTH;
+  else if (need <= 63)
+    grid_loop<MODE, M, Op, int64_t>(op, out, p, c, r);
+  else
+    grid_loop<MODE, M, Op, i128>(op, out, p, c, r);
 }
 
 // One windowed pass over a grid (or 4-padded flat) output: qcomp pass 1,
 // nnqcomp, or the qcomp recompute pass, selected by p.mode.
-template <typename M, typename Op>
+template <int MODE, typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinParams p) {
   int64_t e_star = 0, need = 0;
   op.setup(e_star, need);
@@ -75,12 +116,7 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   if (c.skip) return;
   Red r;
   r.init();
-  if (need > 127)
-    r.err = ERR_WIDTH;
-  else if (need <= 63)
-    grid_loop<M, Op, int64_t>(op, out, p, c, r);
-  else
-    grid_loop<M, Op, i128>(op, out, p, c, r);
+  grid_body<MODE, M>(op, out, p, c, r, need);
   reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
@@ -102,7 +138,15 @@ __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinP
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < out.nlog; i += stride) {
       i128 z = op.template eval1<M>(i);
-      ((M*)out.data)[i] = (M)win_apply<i128>(p, c, z, r);
+      M t;
+      if (p.mode == MODE_NNQ) {
+        t = (M)shift_clamp<i128>(z, c.lam, p.w_out);
+      } else {
+        if (p.mode == MODE_QCOMP) or_mag<i128>(z, r.olo, r.ohi);
+        t = c.store_tmp ? store_shift<M, i128>(z, c) : (M)0;
+      }
+      ((M*)out.data)[i] = t;
+      r.val((int64_t)t);
     }
   }
   reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
@@ -426,6 +470,7 @@ int vec_alloc(int dim, int level, int64_t n, int ebytes, bfp_vec_s** out) {
   h.q = 1;
   h.acc_max = INT64_MIN;
   h.acc_min = INT64_MAX;
+  h.acc_or_lo = h.acc_or_hi = 0;
   cudaMemcpy(v->hdr, &h, sizeof(h), cudaMemcpyHostToDevice);
   *out = v;
   return BFP_OK;
@@ -503,10 +548,22 @@ static int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
   const int b = blocks_for(out->span / 4);
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
-    if (out->ebytes == 4)
-      grid_win_kernel<int32_t, Op><<<b, kThreads, 0, s>>>(op, o, pp);
-    else
-      grid_win_kernel<int64_t, Op><<<b, kThreads, 0, s>>>(op, o, pp);
+    const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * 148) : b;
+    if (out->ebytes == 4) {
+      if (pp.mode == MODE_QCOMP)
+        grid_win_kernel<MODE_QCOMP, int32_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+      else if (pp.mode == MODE_NNQ)
+        grid_win_kernel<MODE_NNQ, int32_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+      else
+        grid_win_kernel<MODE_RECOMPUTE, int32_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+    } else {
+      if (pp.mode == MODE_QCOMP)
+        grid_win_kernel<MODE_QCOMP, int64_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+      else if (pp.mode == MODE_NNQ)
+        grid_win_kernel<MODE_NNQ, int64_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+      else
+        grid_win_kernel<MODE_RECOMPUTE, int64_t, Op><<<nb, kThreads, 0, s>>>(op, o, pp);
+    }
     count_launch();
   };
   if (g_prof) {

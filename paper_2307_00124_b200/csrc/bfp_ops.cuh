@@ -72,8 +72,15 @@ template <> struct V4<int32_t> {
     r[2] = ((int64_t)t.z) >> sh;
     r[3] = ((int64_t)t.w) >> sh;
   }
-  __device__ static __forceinline__ void store(const Vec& v, int64_t o, const int64_t r[4]) {
-    int4 t = make_int4((int)r[0], (int)r[1], (int)r[2], (int)r[3]);
+  __device__ static __forceinline__ void load32(const Vec& v, int64_t o, int sh, int r[4]) {
+    int4 t = __ldg(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
+    r[0] = t.x >> sh;
+    r[1] = t.y >> sh;
+    r[2] = t.z >> sh;
+    r[3] = t.w >> sh;
+  }
+  __device__ static __forceinline__ void store(const Vec& v, int64_t o, const int32_t r[4]) {
+    int4 t = make_int4(r[0], r[1], r[2], r[3]);
     *reinterpret_cast<int4*>((int32_t*)v.data + o) = t;
   }
 };
@@ -106,6 +113,42 @@ __device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) pad[j] = rowpad || (ix + j == mask);
 }
+
+// 32-bit stencil (used when the width bound proves |S x| < 2^31)
+__device__ __forceinline__ void stencil4_32(const Vec& x, int sx, int dim, int l, int64_t o,
+                                            int g[4], int c[4]) {
+  V4<int32_t>::load32(x, o, sx, c);
+  const int32_t* p = (const int32_t*)x.data;
+  const int lf = __ldg(p + o - 1) >> sx, rt = __ldg(p + o + 4) >> sx;
+  int nb[4] = {lf + c[1], c[0] + c[2], c[1] + c[3], c[2] + rt};
+  if (dim >= 2) {
+    const int64_t N = (int64_t)1 << l;
+    int u[4], d[4];
+    V4<int32_t>::load32(x, o - N, sx, u);
+    V4<int32_t>::load32(x, o + N, sx, d);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nb[j] += u[j] + d[j];
+    if (dim >= 3) {
+      const int64_t N2 = N * N;
+      V4<int32_t>::load32(x, o - N2, sx, u);
+      V4<int32_t>::load32(x, o + N2, sx, d);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) nb[j] += u[j] + d[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) g[j] = 2 * dim * c[j] - nb[j];
+}
+// alpha*g*2^max(d,0) + beta*y*2^max(-d,0) with 32-bit operands, 64-bit result
+__device__ __forceinline__ int64_t combine32(int am, int g, int bm, int y, int64_t d) {
+  int64_t ta = (int64_t)am * (int64_t)g, tb = (int64_t)bm * (int64_t)y;
+  if (d < 0)
+    tb <<= (int)imin(-d, 63);
+  else
+    ta <<= (int)imin(d, 63);
+  return ta + tb;
+}
+__device__ __forceinline__ bool fits32(int64_t v) { return v >= INT32_MIN && v <= INT32_MAX; }
 
 // stencil S_d applied to 4 consecutive points at storage offset o (mantissa units)
 template <typename M, typename A>
@@ -146,6 +189,7 @@ struct GemvOp {
   int dim, l;
   // derived
   int64_t sx, sy, d;
+  bool narrow;  // 32-bit stencil + 64-bit combine is exact
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t qa_s = msb_h(2 * dim), ea_s = 2 * l, ma = 2 * dim + 1;
     const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = ea_s + x.hdr->e;
@@ -155,8 +199,23 @@ struct GemvOp {
     sy = y.hdr->shift;
     int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1);
     need = combine_bits(al.m, bg, be.m, zbits(y.hdr), d);
+    narrow = bg <= 31 && zbits(y.hdr) <= 31 && fits32(al.m) && fits32(be.m) && need <= 63 &&
+             sx < 32 && sy < 32;
   }
   template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
+      if (narrow) {
+        int g[4], c[4], yv[4];
+        stencil4_32(x, (int)sx, dim, l, o, g, c);
+        V4<int32_t>::load32(y, o, (int)sy, yv);
+        bool pad[4];
+        pad4(dim, l, o, pad);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          z[j] = pad[j] ? 0 : combine32((int)al.m, g[j], (int)be.m, yv[j], d);
+        return;
+      }
+    }
     A g[4];
     int64_t c[4], yv[4];
     stencil4<M, A>(x, sx, dim, l, o, g, c);
@@ -174,6 +233,7 @@ struct JacobiOp {
   Scal c;
   int dim, l;
   int64_t sx, sb, d1, d2;
+  bool narrow;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t qa_s = msb_h(2 * dim), ma = 2 * dim + 1;
     const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = 2 * l + x.hdr->e;
@@ -187,8 +247,29 @@ struct JacobiOp {
     int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
     int64_t br = combine_bits(-1, bg, 1, zbits(b.hdr), d1);
     need = combine_bits(1, bx, c.m, br, d2);
+    narrow = bg <= 31 && zbits(b.hdr) <= 31 && fits32(c.m) && need <= 63 && sx < 32 && sb < 32;
   }
   template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+    if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
+      if (narrow) {
+        int g[4], cx[4], bv[4];
+        stencil4_32(x, (int)sx, dim, l, o, g, cx);
+        V4<int32_t>::load32(b, o, (int)sb, bv);
+        bool pad[4];
+        pad4(dim, l, o, pad);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int64_t r = combine32(-1, g[j], 1, bv[j], d1);
+          int64_t cr = (int64_t)c.m * r, xx = (int64_t)cx[j];
+          if (d2 < 0)
+            cr <<= (int)imin(-d2, 63);
+          else
+            xx <<= (int)imin(d2, 63);
+          z[j] = pad[j] ? 0 : xx + cr;
+        }
+        return;
+      }
+    }
     A g[4];
     int64_t cx[4], bv[4];
     stencil4<M, A>(x, sx, dim, l, o, g, cx);
