@@ -76,12 +76,11 @@ __device__ __forceinline__ int msb(int64_t v) { return bitlen64((uint64_t)(v ^ (
 __device__ __forceinline__ int msb(i128 v) { return bitlen128((u128)(v ^ (v >> 127))) + 1; }
 __host__ __device__ __forceinline__ int msb_h(int64_t v) {
   uint64_t u = (uint64_t)(v ^ (v >> 63));
-  int b = 0;
-  while (u) {
-    ++b;
-    u >>= 1;
-  }
-  return b + 1;
+#ifdef __CUDA_ARCH__
+  return (u ? 64 - __clzll((long long)u) : 0) + 1;
+#else
+  return (u ? 64 - __builtin_clzll(u) : 0) + 1;
+#endif
 }
 
 template <typename A> struct AccBits;
@@ -155,12 +154,11 @@ struct G15 {
   int64_t m, e;
 };
 __host__ __device__ __forceinline__ int bitlen_h(uint64_t u) {
-  int b = 0;
-  while (u) {
-    ++b;
-    u >>= 1;
-  }
-  return b;
+#ifdef __CUDA_ARCH__
+  return u ? 64 - __clzll((long long)u) : 0;
+#else
+  return u ? 64 - __builtin_clzll(u) : 0;
+#endif
 }
 __host__ __device__ inline G15 g15_from(uint64_t mag, int64_t e) {
   G15 r = {0, 0};

@@ -90,8 +90,8 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
   }
   r.olo |= olo;
   r.ohi |= ohi;
-  r.val((int64_t)mx);
-  r.val((int64_t)mn);
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;  // sentinels stay neutral
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
 template <int MODE, typename M, typename Op>
@@ -107,12 +107,44 @@ __device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParam
 
 // One windowed pass over a grid (or 4-padded flat) output: qcomp pass 1,
 // nnqcomp, or the qcomp recompute pass, selected by p.mode.
+// The op setup and the gamma rule are uniform per launch: one thread evaluates
+// them from the device headers and broadcasts through shared memory.
+template <typename Op, typename M>
+__device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinParams& p, WinCtx& c,
+                                            int64_t& need) {
+  __shared__ Op s_op;
+  __shared__ WinCtx s_c;
+  __shared__ int64_t s_need;
+  if (p.mode == MODE_RECOMPUTE) {  // fast path: nothing to do, skip the op setup
+    __shared__ int s_rc;
+    if (threadIdx.x == 0) s_rc = ((volatile Hdr*)out.hdr)->need_recompute;
+    __syncthreads();
+    if (!s_rc) {
+      c.skip = 1;
+      return;
+    }
+  }
+  if (threadIdx.x == 0) {
+    int64_t e_star = 0, nd = 0;
+    Op o = op;
+    o.setup(e_star, nd);
+    WinCtx cc;
+    win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
+    s_op = o;
+    s_c = cc;
+    s_need = nd;
+  }
+  __syncthreads();
+  op = s_op;
+  c = s_c;
+  need = s_need;
+}
+
 template <int MODE, typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinParams p) {
-  int64_t e_star = 0, need = 0;
-  op.setup(e_star, need);
+  int64_t need = 0;
   WinCtx c;
-  win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), c);
+  block_setup<Op, M>(op, out, p, c, need);
   if (c.skip) return;
   Red r;
   r.init();
@@ -122,13 +154,178 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   });
 }
 
+
+// ---------------------------------------------------------------------------
+// 2.5-D register march for the 2-D / 3-D stencil ops on int32 storage (the
+// hot path).  A work item is a 4-wide x strip marching R steps along the
+// slowest axis (y in 2-D, z in 3-D): the x values at the previous / current /
+// next step stay in registers, x-neighbours come from warp shuffles, and the
+// loads of step s+1 are issued before step s is computed.  Each thread writes
+// one aligned int4 per step.
+constexpr int kMarchMinN = 128;  // GX = N/4 >= 32: a warp spans one row
+
+__device__ __forceinline__ void ld4s(const int32_t* p, int64_t o, int sh, int v[4]) {
+  // 128-bit read-only load of 4 mantissas, pending shift applied
+  int4 t = __ldg(reinterpret_cast<const int4*>(p + o));
+  v[0] = t.x >> sh;
+  v[1] = t.y >> sh;
+  v[2] = t.z >> sh;
+  v[3] = t.w >> sh;
+}
+
+// one march step: output row at wp from (P, C, Nx) along the march axis and the
+// x neighbours through the warp; prefetches the next step into (NN, Yn, ...).
+template <int MODE, int DIM, typename Op>
+struct MarchStep {
+  const Op& op;
+  const WinParams& p;
+  const WinCtx& c;
+  int64_t S, N;
+  int sx, sy, lane;
+  bool xpad, store;
+  int32_t mx, mn;
+  uint64_t olo, ohi;
+
+  __device__ __forceinline__ void prefetch(const int32_t* xp, const int32_t* yp, int NN[4],
+                                           int Yn[4], int SUn[4], int SDn[4], int& lfn,
+                                           int& rtn) const {
+    ld4s(xp, 2 * S, sx, NN);
+    ld4s(yp, S, sy, Yn);
+    if (DIM == 3) {
+      ld4s(xp, S - N, sx, SUn);
+      ld4s(xp, S + N, sx, SDn);
+    }
+    if (lane == 0) lfn = __ldg(xp + S - 1) >> sx;
+    if (lane == 31) rtn = __ldg(xp + S + 4) >> sx;
+  }
+
+  __device__ __forceinline__ void compute(int32_t* wp, const int P[4], const int C[4],
+                                          const int Nx[4], const int Y[4], const int SU[4],
+                                          const int SD[4], int lf, int rt) {
+    int left = __shfl_up_sync(0xffffffffu, C[3], 1);
+    int right = __shfl_down_sync(0xffffffffu, C[0], 1);
+    if (lane == 0) left = lf;
+    if (lane == 31) right = rt;
+    const int nb[4] = {left + C[1], C[0] + C[2], C[1] + C[3], C[2] + right};
+    int32_t tt[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int n = nb[k] + P[k] + Nx[k];
+      if (DIM == 3) n += SU[k] + SD[k];
+      const int g = 2 * DIM * C[k] - n;
+      int64_t z = op.point(g, C[k], Y[k]);
+      if (k == 3 && xpad) z = 0;
+      if (MODE == MODE_NNQ) {
+        tt[k] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+      } else {
+        if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+        tt[k] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+      }
+      mx = tt[k] > mx ? tt[k] : mx;
+      mn = tt[k] < mn ? tt[k] : mn;
+    }
+    *reinterpret_cast<int4*>(wp) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+  }
+};
+
+template <int MODE, int DIM, typename Op>
+__device__ __forceinline__ void march_loop(const Op& op, const Vec& out, const WinParams& p,
+                                           const WinCtx& c, Red& r, int R) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l, GX = N >> 2;
+  const int64_t S = DIM == 2 ? N : N * N;  // march stride
+  const int64_t rows = DIM == 3 ? N : 1;
+  const int64_t chunks = (N + R - 1) / R;
+  const int64_t items = GX * rows * chunks;
+  MarchStep<MODE, DIM, Op> st{op, p, c, S, N, op.shs(), op.shy(), (int)(threadIdx.x & 31),
+                              false, (bool)c.store_tmp, INT32_MIN, INT32_MAX, 0, 0};
+  const int sx = st.sx, sy = st.sy;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < items; w += stride) {
+    const int64_t gx = w % GX, t = w / GX;
+    const int64_t j = DIM == 3 ? t % N : 0, ch = DIM == 3 ? t / N : t;
+    const int m0 = (int)(ch * R);
+    const int64_t o0 = gx * 4 + (DIM == 3 ? j * N : 0) + (int64_t)m0 * S;
+    const int32_t* xp = (const int32_t*)op.sv().data + o0;
+    const int32_t* yp = (const int32_t*)op.yv2().data + o0;
+    int32_t* wp = (int32_t*)out.data + o0;
+    st.xpad = gx == GX - 1;
+    // the pad plane / row (index N-1 of the march axis, or row N-1 in 3-D) is written as zeros
+    const int total = (int)std::min<int64_t>(R, N - m0);
+    const bool rowpad = DIM == 3 && j == N - 1;
+    const int steps = rowpad ? 0 : (m0 + total == N ? total - 1 : total);
+    if (rowpad || m0 + total == N) {
+      const int first = rowpad ? 0 : total - 1;
+      for (int s = first; s < total; ++s)
+        *reinterpret_cast<int4*>(wp + (int64_t)s * S) = make_int4(0, 0, 0, 0);
+      st.mx = 0 > st.mx ? 0 : st.mx;
+      st.mn = 0 < st.mn ? 0 : st.mn;
+    }
+    if (steps == 0) continue;
+    int X0[4], X1[4], X2[4], X3[4], Y0[4], Y1[4];
+    int U0[4], U1[4], D0[4], D1[4];
+    int l0 = 0, r0 = 0, l1 = 0, r1 = 0;
+    ld4s(xp, -S, sx, X0);
+    ld4s(xp, 0, sx, X1);
+    ld4s(xp, S, sx, X2);
+    ld4s(yp, 0, sy, Y0);
+    if (DIM == 3) {
+      ld4s(xp, -N, sx, U0);
+      ld4s(xp, N, sx, D0);
+    }
+    if (st.lane == 0) l0 = __ldg(xp - 1) >> sx;
+    if (st.lane == 31) r0 = __ldg(xp + 4) >> sx;
+    // x buffers rotate with period 4, y / side buffers with period 2: unroll by 4
+    int s = 0;
+    for (;;) {
+      if (s + 1 < steps) st.prefetch(xp, yp, X3, Y1, U1, D1, l1, r1);
+      st.compute(wp, X0, X1, X2, Y0, U0, D0, l0, r0);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X0, Y0, U0, D0, l0, r0);
+      st.compute(wp, X1, X2, X3, Y1, U1, D1, l1, r1);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X1, Y1, U1, D1, l1, r1);
+      st.compute(wp, X2, X3, X0, Y0, U0, D0, l0, r0);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X2, Y0, U0, D0, l0, r0);
+      st.compute(wp, X3, X0, X1, Y1, U1, D1, l1, r1);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+    }
+  }
+  r.olo |= st.olo;
+  r.ohi |= st.ohi;
+  r.mx = (int64_t)st.mx > r.mx ? (int64_t)st.mx : r.mx;
+  r.mn = (int64_t)st.mn < r.mn ? (int64_t)st.mn : r.mn;
+}
+
+template <int MODE, int DIM, typename Op>
+__global__ void __launch_bounds__(kThreads, DIM == 2 ? 3 : 2) march_win_kernel(Op op, Vec out, WinParams p,
+                                                                int R) {
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63)
+    march_loop<MODE, DIM>(op, out, p, c, r, R);
+  else
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
 // one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
 template <typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
-  int64_t e_star = 0, need = 0;
-  op.setup(e_star, need);
+  int64_t need = 0;
   WinCtx c;
-  win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), c);
+  block_setup<Op, M>(op, out, p, c, need);
   if (c.skip) return;
   Red r;
   r.init();
@@ -581,6 +778,65 @@ static int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
   return last_launch();
 }
 
+// stencil ops on int32 grids of 2-D / 3-D with N >= 128 use the register march
+template <typename Op>
+static int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  if (out->ebytes != 4 || out->dim < 2 || (int64_t(1) << out->l) < kMarchMinN)
+    return launch_grid(op, out, p0, s);
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int64_t N = int64_t(1) << out->l, GX = N / 4, rows = out->dim == 3 ? N : 1;
+  static int occ2 = 0, occ3 = 0;
+  if (!occ2) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, march_win_kernel<MODE_QCOMP, 2, Op>,
+                                                  kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, march_win_kernel<MODE_QCOMP, 3, Op>,
+                                                  kThreads, 0);
+    occ2 = std::max(occ2, 1);
+    occ3 = std::max(occ3, 1);
+  }
+  const int occ = out->dim == 2 ? occ2 : occ3;
+  // one balanced resident wave: every thread marches R steps (last chunk shorter)
+  const int64_t slots = (int64_t)148 * occ * kThreads;
+  int R = (int)std::max<int64_t>(4, (GX * rows * N + slots - 1) / slots);
+  const int64_t items = GX * rows * ((N + R - 1) / R);
+  const int b = (int)std::max<int64_t>(1, std::min<int64_t>((items + kThreads - 1) / kThreads,
+                                                            (int64_t)148 * occ));
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp, int nb) {
+    if (out->dim == 2) {
+      if (pp.mode == MODE_QCOMP)
+        march_win_kernel<MODE_QCOMP, 2, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+      else if (pp.mode == MODE_NNQ)
+        march_win_kernel<MODE_NNQ, 2, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+      else
+        march_win_kernel<MODE_RECOMPUTE, 2, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+    } else {
+      if (pp.mode == MODE_QCOMP)
+        march_win_kernel<MODE_QCOMP, 3, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+      else if (pp.mode == MODE_NNQ)
+        march_win_kernel<MODE_NNQ, 3, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+      else
+        march_win_kernel<MODE_RECOMPUTE, 3, Op><<<nb, kThreads, 0, s>>>(op, o, pp, R);
+    }
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p, b);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p, b);
+  }
+  if (p.mode == MODE_QCOMP) {
+    p.mode = MODE_RECOMPUTE;
+    go(p, b);
+  }
+  return last_launch();
+}
+
 template <typename Op>
 static int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
   int rc = check_window(p0, out);
@@ -619,7 +875,7 @@ int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bf
   op.be = be;
   op.dim = x->dim;
   op.l = x->l;
-  return launch_grid(op, out, p, s);
+  return launch_march(op, out, p, s);
 }
 
 int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s* out,
@@ -632,7 +888,7 @@ int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s*
   op.c = c;
   op.dim = x->dim;
   op.l = x->l;
-  return launch_grid(op, out, p, s);
+  return launch_march(op, out, p, s);
 }
 
 int op_scal(bfp_vec_s* r, Scal c, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {

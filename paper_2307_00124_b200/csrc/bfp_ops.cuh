@@ -149,6 +149,13 @@ __device__ __forceinline__ int64_t combine32(int am, int g, int bm, int y, int64
   return ta + tb;
 }
 __device__ __forceinline__ bool fits32(int64_t v) { return v >= INT32_MIN && v <= INT32_MAX; }
+// a * 2^s + add for a 32-bit a and a uniform s in [0, 62] (exact by the width bound):
+// s <= 30 is one signed IMAD.WIDE, s >= 32 only touches the high word.
+__device__ __forceinline__ int64_t mad_pow2(int a, int s, int64_t add) {
+  if (s <= 30) return (int64_t)a * (int64_t)(1 << s) + add;
+  if (s >= 32) return (int64_t)((uint64_t)(uint32_t)(a << (s - 32)) << 32) + add;
+  return (int64_t)((uint64_t)(int64_t)a << 31) + add;
+}
 
 // stencil S_d applied to 4 consecutive points at storage offset o (mantissa units)
 template <typename M, typename A>
@@ -187,20 +194,39 @@ struct GemvOp {
   Vec x, y;
   Scal al, be;
   int dim, l;
-  // derived
+  // derived (uniform per launch)
   int64_t sx, sy, d;
-  bool narrow;  // 32-bit stencil + 64-bit combine is exact
+  bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
+  bool swap;
+  int P, Q;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t qa_s = msb_h(2 * dim), ea_s = 2 * l, ma = 2 * dim + 1;
-    const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = ea_s + x.hdr->e;
-    (void)gq;
+    const int64_t ge = 2 * l + x.hdr->e;  // e_A + e_x
     axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
-    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1);
-    need = combine_bits(al.m, bg, be.m, zbits(y.hdr), d);
-    narrow = bg <= 31 && zbits(y.hdr) <= 31 && fits32(al.m) && fits32(be.m) && need <= 63 &&
-             sx < 32 && sy < 32;
+    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1), by = zbits(y.hdr);
+    need = combine_bits(al.m, bg, be.m, by, d);
+    // z = X * P + Q * Y with (X, Y) = (g, y), P = alpha 2^d, Q = beta   when d >= 0
+    //                         (X, Y) = (y, g), P = beta 2^-d, Q = alpha  when d < 0
+    const int64_t ad = d >= 0 ? d : -d;
+    const int64_t pm = d >= 0 ? al.m : be.m, qm = d >= 0 ? be.m : al.m;
+    const int64_t bx_ = d >= 0 ? bg : by, by_ = d >= 0 ? by : bg;
+    narrow = need <= 63 && sx < 32 && sy < 32 && ad <= 30 && bg <= 31 && by <= 31 &&
+             fits32(pm) && fits32(qm) && msb(pm) + ad <= 32 &&
+             (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
+    swap = d < 0;
+    P = narrow ? (int)(pm << ad) : 0;
+    Q = (int)qm;
+  }
+  // march-kernel interface (narrow, int32 storage)
+  __device__ __forceinline__ const Vec& sv() const { return x; }
+  __device__ __forceinline__ const Vec& yv2() const { return y; }
+  __device__ __forceinline__ int shs() const { return (int)sx; }
+  __device__ __forceinline__ int shy() const { return (int)sy; }
+  __device__ __forceinline__ int64_t point(int g, int c, int yv) const {
+    (void)c;
+    const int X = swap ? yv : g, Y = swap ? g : yv;
+    return (int64_t)X * (int64_t)P + (int64_t)(Q * Y);
   }
   template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
@@ -208,11 +234,18 @@ struct GemvOp {
         int g[4], c[4], yv[4];
         stencil4_32(x, (int)sx, dim, l, o, g, c);
         V4<int32_t>::load32(y, o, (int)sy, yv);
-        bool pad[4];
-        pad4(dim, l, o, pad);
+        const uint32_t mN = (1u << l) - 1;
+        const uint32_t ix = (uint32_t)o & mN;
+        bool rowpad = false;
+        if (dim >= 2) rowpad = ((uint32_t)(o >> l) & mN) == mN;
+        if (dim >= 3) rowpad |= ((uint32_t)(o >> (2 * l)) & mN) == mN;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          z[j] = pad[j] ? 0 : combine32((int)al.m, g[j], (int)be.m, yv[j], d);
+        for (int j = 0; j < 4; ++j) {
+          const int X = swap ? yv[j] : g[j], Y = swap ? g[j] : yv[j];
+          z[j] = (int64_t)X * (int64_t)P + (int64_t)(Q * Y);
+        }
+        if (ix == mN - 3) z[3] = 0;  // x pad (only the last lane of a 4-group)
+        if (rowpad) z[0] = z[1] = z[2] = z[3] = 0;
         return;
       }
     }
@@ -234,12 +267,11 @@ struct JacobiOp {
   int dim, l;
   int64_t sx, sb, d1, d2;
   bool narrow;
+  int P1, s2;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t qa_s = msb_h(2 * dim), ma = 2 * dim + 1;
-    const int64_t gq = qa_s + x.hdr->q + ceil_log2_h(ma), ge = 2 * l + x.hdr->e;
+    const int64_t ge = 2 * l + x.hdr->e;
     int64_t er;
     axpby_setup(ge, b.hdr->e, d1, er);      // r template (alpha q=1 e=0, beta q=2 e=0)
-    (void)gq;
     axpby_setup(x.hdr->e, c.e + er, d2, e_star);
     sx = x.hdr->shift;
     sb = b.hdr->shift;
@@ -247,7 +279,21 @@ struct JacobiOp {
     int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
     int64_t br = combine_bits(-1, bg, 1, zbits(b.hdr), d1);
     need = combine_bits(1, bx, c.m, br, d2);
-    narrow = bg <= 31 && zbits(b.hdr) <= 31 && fits32(c.m) && need <= 63 && sx < 32 && sb < 32;
+    // r = -g 2^d1 + b (d1 >= 0) as one IMAD.WIDE;  z = x 2^d2 + c r (d2 >= 0)
+    narrow = bg <= 31 && zbits(b.hdr) <= 31 && fits32(c.m) && c.m >= 0 && need <= 63 &&
+             sx < 32 && sb < 32 && d1 >= 0 && d1 <= 30 && d2 >= 0 && d2 <= 62 && bx <= 31 &&
+             (bx == 0 || bx + d2 <= 63);
+    P1 = narrow ? -(1 << (int)d1) : 0;
+    s2 = narrow ? (int)d2 : 0;
+  }
+  __device__ __forceinline__ const Vec& sv() const { return x; }
+  __device__ __forceinline__ const Vec& yv2() const { return b; }
+  __device__ __forceinline__ int shs() const { return (int)sx; }
+  __device__ __forceinline__ int shy() const { return (int)sb; }
+  __device__ __forceinline__ int64_t point(int g, int cx, int bv) const {
+    const int64_t r = (int64_t)g * (int64_t)P1 + (int64_t)bv;
+    const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)c.m);
+    return mad_pow2(cx, s2, cr);
   }
   template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
@@ -255,18 +301,20 @@ struct JacobiOp {
         int g[4], cx[4], bv[4];
         stencil4_32(x, (int)sx, dim, l, o, g, cx);
         V4<int32_t>::load32(b, o, (int)sb, bv);
-        bool pad[4];
-        pad4(dim, l, o, pad);
+        const uint32_t mN = (1u << l) - 1;
+        const uint32_t ix = (uint32_t)o & mN;
+        bool rowpad = false;
+        if (dim >= 2) rowpad = ((uint32_t)(o >> l) & mN) == mN;
+        if (dim >= 3) rowpad |= ((uint32_t)(o >> (2 * l)) & mN) == mN;
+        const uint64_t cm = (uint64_t)c.m;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          int64_t r = combine32(-1, g[j], 1, bv[j], d1);
-          int64_t cr = (int64_t)c.m * r, xx = (int64_t)cx[j];
-          if (d2 < 0)
-            cr <<= (int)imin(-d2, 63);
-          else
-            xx <<= (int)imin(d2, 63);
-          z[j] = pad[j] ? 0 : xx + cr;
+          const int64_t r = (int64_t)g[j] * (int64_t)P1 + (int64_t)bv[j];
+          const int64_t cr = (int64_t)((uint64_t)r * cm);  // exact: |c r| < 2^63 by the bound
+          z[j] = mad_pow2(cx[j], s2, cr);
         }
+        if (ix == mN - 3) z[3] = 0;
+        if (rowpad) z[0] = z[1] = z[2] = z[3] = 0;
         return;
       }
     }
