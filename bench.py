@@ -328,7 +328,9 @@ def run_e2e(args, B, Lb, torch, stream, sp):
 
 
 SOLVES = {
-    "C1_1d_vcycles": dict(d=1, l_fine=20, cycles=10, x0_random=True, rhs_kind=0, p=16),
+    # x, b at 16 bits; residual + V-cycle (wdot) at 28 bits, w_add capped at 4 (int32)
+    "C1_1d_vcycles": dict(d=1, l_fine=20, cycles=10, x0_random=True, rhs_kind=0, p=16,
+                          pd=[28] * 32, w_add_cap=4),
     "C2_2d_vcycles": dict(d=2, l_fine=12, cycles=15, rhs_kind=1, p=20),
     "C3_2d_fmg_nnq": dict(d=2, l_fine=13, l_coarse=3, cycles=1, rhs_kind=1, fmg=True,
                           nonnormalized=True,

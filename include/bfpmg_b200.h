@@ -143,11 +143,17 @@ int bfp_gen_uniform(bfp_vec_t v, int64_t p, uint64_t seed, uint64_t stream_id, v
 int bfp_gen_sine(bfp_vec_t v, int64_t p, void* stream);
 
 /* ---- multigrid solver ---- */
+/* PrecisionSchedule (P/include/bfpmg/multigrid.hpp:16-27) per level: p = w (iterate),
+   pd = wdot (residual and V-cycle), pc = wcheck (right-hand side); 0 entries = p.
+   w_add_cap: GammaPolicy::w_add_cap (-1 unlimited). */
 typedef struct {
   int d, l_fine, l_coarse, nu1, nu2, n_coarse, cycles, fmg, nonnormalized, x0_random, rhs_kind,
       qc;
   uint64_t seed;
   int p[32];
+  int pd[32];
+  int pc[32];
+  int w_add_cap;
 } bfp_mg_config_t;
 
 typedef struct {

@@ -829,6 +829,8 @@ static void run_step(mg_ctx* c, int step, int level, const ob_kernel* k, int64_t
   ob_g15_gamma(gamma, &gm, &ge);
   ob_flags fl = {0, 0, 0};
   int rc;
+  /* GammaPolicy::w_tmp_for (P/src/multigrid.cpp:81-85): w_out + min(w_add, cap) */
+  if (c->cfg->w_add_cap >= 0 && w_add > c->cfg->w_add_cap) w_add = c->cfg->w_add_cap;
   int64_t w_tmp = w_out + w_add;
   if (normalized)
     rc = ob_qcomp(k, w_out, w_tmp, gm, ge, 0, out, &fl);
@@ -855,7 +857,11 @@ static void run_step(mg_ctx* c, int step, int level, const ob_kernel* k, int64_t
   r->n_trace++;
 }
 
+/* PrecisionSchedule (P/src/multigrid.cpp:13-44): w = iterate, wdot = residual and
+   V-cycle, wcheck = right-hand side; 0 entries default to w */
 static int64_t wl(const mg_ctx* c, int l) { return c->cfg->p[l]; }
+static int64_t wd(const mg_ctx* c, int l) { return c->cfg->pd[l] ? c->cfg->pd[l] : c->cfg->p[l]; }
+static int64_t wc(const ob_mg_config* cfg, int l) { return cfg->pc[l] ? cfg->pc[l] : cfg->p[l]; }
 
 /* V-cycle correction scheme on A e = r, e0 = 0 */
 static void vcycle(mg_ctx* c, int l, const ob_block* r, ob_block* e_out) {
@@ -867,11 +873,11 @@ static void vcycle(mg_ctx* c, int l, const ob_block* r, ob_block* e_out) {
   ob_kernel k;
   ob_block e = blk_alloc(N), t = blk_alloc(N);
   ob_make_scal(&k, r, cm, cfg->qc, ce);
-  run_step(c, OB_STEP_RELAX0, l, &k, wl(c, l), ob_g15_mul(c15, nrm(r)), 2, &e);
+  run_step(c, OB_STEP_RELAX0, l, &k, wd(c, l), ob_g15_mul(c15, nrm(r)), 2, &e);
   int sweeps = (l == cfg->l_coarse) ? cfg->n_coarse : cfg->nu1;
   for (int s = 1; s < sweeps && !c->err; ++s) {
     ob_make_jacobi(&k, g, &e, r, cm, cfg->qc, ce);
-    run_step(c, OB_STEP_RELAX, l, &k, wl(c, l), ob_g15_add(nrm(&e), ob_g15_mul(c15, nrm(r))), 3,
+    run_step(c, OB_STEP_RELAX, l, &k, wd(c, l), ob_g15_add(nrm(&e), ob_g15_mul(c15, nrm(r))), 3,
              &t);
     ob_block sw = e;
     e = t;
@@ -882,18 +888,18 @@ static void vcycle(mg_ctx* c, int l, const ob_block* r, ob_block* e_out) {
     int64_t Nc = ob_grid_size(gc);
     ob_block rv = blk_alloc(N), rc = blk_alloc(Nc), ec = blk_alloc(Nc);
     ob_make_stencil_gemv(&k, g, &e, r, -1, 1, 0, 1, 2, 0);
-    run_step(c, OB_STEP_V_RES, l, &k, wl(c, l), nrm(r), 4, &rv);
+    run_step(c, OB_STEP_V_RES, l, &k, wd(c, l), nrm(r), 4, &rv);
     ob_make_restrict(&k, g, &rv);
-    run_step(c, OB_STEP_RESTRICT, l, &k, wl(c, l), nrm(&rv), 6, &rc);
+    run_step(c, OB_STEP_RESTRICT, l, &k, wd(c, l), nrm(&rv), 6, &rc);
     if (!c->err) vcycle(c, l - 1, &rc, &ec);
     ob_make_prolong_correct(&k, g, &ec, &e);
-    run_step(c, OB_STEP_V_CORR, l, &k, wl(c, l), ob_g15_add(nrm(&e), nrm(&ec)), 2, &t);
+    run_step(c, OB_STEP_V_CORR, l, &k, wd(c, l), ob_g15_add(nrm(&e), nrm(&ec)), 2, &t);
     ob_block sw = e;
     e = t;
     t = sw;
     for (int s = 0; s < cfg->nu2 && !c->err; ++s) {
       ob_make_jacobi(&k, g, &e, r, cm, cfg->qc, ce);
-      run_step(c, OB_STEP_RELAX, l, &k, wl(c, l),
+      run_step(c, OB_STEP_RELAX, l, &k, wd(c, l),
                ob_g15_add(nrm(&e), ob_g15_mul(c15, nrm(r))), 3, &t);
       sw = e;
       e = t;
@@ -933,7 +939,7 @@ static void ir(mg_ctx* c, int l, ob_block* x, const ob_block* b, int iters) {
       gam = ob_g15_add(nrm(b), ob_g15_mul(ob_g15_from((uint64_t)(4 * cfg->d), 2 * (int64_t)l), ulp));
     }
     ob_make_stencil_gemv(&k, g, x, b, -1, 1, 0, 1, 2, 0);
-    run_step(c, OB_STEP_IR_RES, l, &k, wl(c, l), gam, first ? 5 : 4, &r);
+    run_step(c, OB_STEP_IR_RES, l, &k, wd(c, l), gam, first ? 5 : 4, &r);
     if (c->err) break;
     c->prev_res[l] = nrm(&r);
     c->have_prev_res[l] = 1;
@@ -951,7 +957,7 @@ static void ir(mg_ctx* c, int l, ob_block* x, const ob_block* b, int iters) {
 }
 
 static int gen_rhs(const ob_mg_config* cfg, ob_grid g, ob_block* b) {
-  int64_t p = cfg->p[g.l];
+  int64_t p = wc(cfg, g.l);
   if (cfg->rhs_kind == 1) return ob_gen_sine(g, p, b);
   if (cfg->rhs_kind == 0) return ob_gen_uniform(g, p, cfg->seed, 2, b);
   b->n = ob_grid_size(g);
@@ -987,7 +993,7 @@ static void fmg(mg_ctx* c, int l, ob_block* x_out) {
     ob_block r = blk_alloc(N);
     ob_kernel k;
     ob_make_stencil_gemv(&k, g, x_out, &b, -1, 1, 0, 1, 2, 0);
-    run_step(c, OB_STEP_FINAL_RES, l, &k, wl(c, l), c->prev_res[l], 4, &r);
+    run_step(c, OB_STEP_FINAL_RES, l, &k, wd(c, l), c->prev_res[l], 4, &r);
     push_hist(c, norm_double(&r));
     blk_free(&r);
   }
@@ -1027,7 +1033,7 @@ int ob_mg_run(const ob_mg_config* cfg, ob_mg_result* res) {
       ob_block r = blk_alloc(N);
       ob_kernel k;
       ob_make_stencil_gemv(&k, g, x, &b, -1, 1, 0, 1, 2, 0);
-      run_step(&c, OB_STEP_FINAL_RES, cfg->l_fine, &k, cfg->p[cfg->l_fine],
+      run_step(&c, OB_STEP_FINAL_RES, cfg->l_fine, &k, wd(&c, cfg->l_fine),
                c.prev_res[cfg->l_fine], 4, &r);
       push_hist(&c, norm_double(&r));
       blk_free(&r);

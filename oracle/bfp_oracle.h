@@ -156,7 +156,10 @@ typedef struct {
   int rhs_kind;     /* 0: uniform (seed, stream 2); 1: sine; 2: zero */
   int qc;           /* width of the Jacobi coefficient */
   uint64_t seed;
-  int p[32];        /* working width per level (index = level) */
+  int p[32];        /* w: iterate width per level (index = level) */
+  int pd[32];       /* wdot: residual / V-cycle width (0 = p) */
+  int pc[32];       /* wcheck: right-hand-side width (0 = p) */
+  int w_add_cap;    /* GammaPolicy::w_add_cap: -1 unlimited */
 } ob_mg_config;
 
 typedef struct {

@@ -650,7 +650,10 @@ class MgConfig:
     rhs_kind: int = 1
     qc: int = 16
     seed: int = 1
-    p: Optional[List[int]] = None  # indexed by level
+    p: Optional[List[int]] = None   # w: iterate width, indexed by level
+    pd: Optional[List[int]] = None  # wdot: residual / V-cycle width (0 / None = p)
+    pc: Optional[List[int]] = None  # wcheck: right-hand-side width (0 / None = p)
+    w_add_cap: int = -1             # GammaPolicy::w_add_cap (-1 = unlimited)
 
 
 @dataclass
@@ -670,8 +673,18 @@ class Mg:
     def w(self, l):
         return self.cfg.p[l]
 
+    def wd(self, l):
+        pd = self.cfg.pd
+        return pd[l] if pd and pd[l] else self.cfg.p[l]
+
+    def wc(self, l):
+        pc = self.cfg.pc
+        return pc[l] if pc and pc[l] else self.cfg.p[l]
+
     def step(self, name, level, k, w_out, g, w_add):
         normalized = (not self.cfg.nonnormalized) or name == "final-residual"
+        if self.cfg.w_add_cap >= 0:
+            w_add = min(w_add, self.cfg.w_add_cap)
         gam = g15_gamma(g)
         if normalized:
             out, fl = qcomp(k, w_out, w_out + w_add, gam)
@@ -688,21 +701,21 @@ class Mg:
         d = cfg.d
         c = jacobi_coeff(d, l, cfg.qc)
         c15 = g15_from(c.m[0], c.e)
-        e = self.step("v-relax0", l, Scal(r, c), self.w(l), g15_mul(c15, g15_norm(r)), 2)
+        e = self.step("v-relax0", l, Scal(r, c), self.wd(l), g15_mul(c15, g15_norm(r)), 2)
         sweeps = cfg.n_coarse if l == cfg.l_coarse else cfg.nu1
         for _ in range(1, sweeps):
-            e = self.step("v-relax", l, Jacobi(d, l, e, r, c), self.w(l),
+            e = self.step("v-relax", l, Jacobi(d, l, e, r, c), self.wd(l),
                           g15_add(g15_norm(e), g15_mul(c15, g15_norm(r))), 3)
         if l == cfg.l_coarse:
             return e
         rv = self.step("v-residual", l, StencilGemv(d, l, e, r, bfp_minus_one(), bfp_one()),
-                       self.w(l), g15_norm(r), 4)
-        rc = self.step("v-restrict", l, Restrict(d, l, rv), self.w(l), g15_norm(rv), 6)
+                       self.wd(l), g15_norm(r), 4)
+        rc = self.step("v-restrict", l, Restrict(d, l, rv), self.wd(l), g15_norm(rv), 6)
         ec = self.vcycle(l - 1, rc)
-        e = self.step("v-correct", l, ProlongCorrect(d, l, ec, e), self.w(l),
+        e = self.step("v-correct", l, ProlongCorrect(d, l, ec, e), self.wd(l),
                       g15_add(g15_norm(e), g15_norm(ec)), 2)
         for _ in range(cfg.nu2):
-            e = self.step("v-relax", l, Jacobi(d, l, e, r, c), self.w(l),
+            e = self.step("v-relax", l, Jacobi(d, l, e, r, c), self.wd(l),
                           g15_add(g15_norm(e), g15_mul(c15, g15_norm(r))), 3)
         return e
 
@@ -717,7 +730,7 @@ class Mg:
             else:
                 g = self.prev[l]
             r = self.step("ir-residual", l, StencilGemv(d, l, x, b, bfp_minus_one(), bfp_one()),
-                          self.w(l), g, 5 if first else 4)
+                          self.wd(l), g, 5 if first else 4)
             self.prev[l] = g15_norm(r)
             self.res.history.append(_norm_double(r))
             e = self.vcycle(l, r)
@@ -728,14 +741,14 @@ class Mg:
     def rhs(self, l):
         cfg = self.cfg
         if cfg.rhs_kind == 1:
-            return gen_sine(cfg.d, l, cfg.p[l])
+            return gen_sine(cfg.d, l, self.wc(l))
         if cfg.rhs_kind == 0:
-            return gen_uniform(cfg.d, l, cfg.p[l], cfg.seed, 2)
-        return zero_vec(grid_n(l) ** cfg.d, cfg.p[l])
+            return gen_uniform(cfg.d, l, self.wc(l), cfg.seed, 2)
+        return zero_vec(grid_n(l) ** cfg.d, self.wc(l))
 
     def final(self, l, x, b):
         r = self.step("final-residual", l,
-                      StencilGemv(self.cfg.d, l, x, b, bfp_minus_one(), bfp_one()), self.w(l),
+                      StencilGemv(self.cfg.d, l, x, b, bfp_minus_one(), bfp_one()), self.wd(l),
                       self.prev[l], 4)
         self.res.history.append(_norm_double(r))
 

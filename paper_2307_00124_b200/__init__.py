@@ -72,7 +72,8 @@ class MgConfig(C.Structure):
     _fields_ = [("d", C.c_int), ("l_fine", C.c_int), ("l_coarse", C.c_int), ("nu1", C.c_int),
                 ("nu2", C.c_int), ("n_coarse", C.c_int), ("cycles", C.c_int), ("fmg", C.c_int),
                 ("nonnormalized", C.c_int), ("x0_random", C.c_int), ("rhs_kind", C.c_int),
-                ("qc", C.c_int), ("seed", C.c_uint64), ("p", C.c_int * 32)]
+                ("qc", C.c_int), ("seed", C.c_uint64), ("p", C.c_int * 32), ("pd", C.c_int * 32),
+                ("pc", C.c_int * 32), ("w_add_cap", C.c_int)]
 
 
 class TraceRec(C.Structure):
@@ -539,16 +540,26 @@ def gen_sine(v: BfpVec, p: int) -> BfpVec:
 # multigrid solver
 
 
+def _lv(v):
+    if v is None:
+        return [0] * 32
+    if isinstance(v, int):
+        return [v] * 32
+    return list(v) + [0] * (32 - len(v))
+
+
 def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=False,
-              nonnormalized=False, x0_random=False, rhs_kind=1, qc=16, seed=1, p=None) -> MgConfig:
+              nonnormalized=False, x0_random=False, rhs_kind=1, qc=16, seed=1, p=None, pd=None,
+              pc=None, w_add_cap=-1) -> MgConfig:
+    """Solver config; p / pd / pc are the PrecisionSchedule w / wdot / wcheck per level."""
     cfg = MgConfig()
     cfg.d, cfg.l_fine, cfg.l_coarse, cfg.nu1, cfg.nu2 = d, l_fine, l_coarse, nu1, nu2
     cfg.n_coarse, cfg.cycles, cfg.fmg, cfg.nonnormalized = n_coarse, cycles, int(fmg), int(nonnormalized)
     cfg.x0_random, cfg.rhs_kind, cfg.qc, cfg.seed = int(x0_random), rhs_kind, qc, seed
-    if isinstance(p, int):
-        p = [p] * 32
+    p, pd, pc = _lv(p), _lv(pd), _lv(pc)
     for i in range(32):
-        cfg.p[i] = p[i] if i < len(p) else 0
+        cfg.p[i], cfg.pd[i], cfg.pc[i] = p[i], pd[i], pc[i]
+    cfg.w_add_cap = w_add_cap
     return cfg
 
 

@@ -97,9 +97,13 @@ struct bfp_mg_s {
   }
 
   // run_step: one windowed op (qcomp, or nnqcomp in nonnormalized mode)
+  int64_t wd(int l) const { return cfg.pd[l] ? cfg.pd[l] : cfg.p[l]; }
+  int64_t wc(int l) const { return cfg.pc[l] ? cfg.pc[l] : cfg.p[l]; }
+
   void step(int st, int level, PlanOp op, int64_t w_out, const GammaRule& g, int w_add,
             bool hist = false) {
     const bool normalized = !cfg.nonnormalized || st == ST_FINAL_RES;
+    if (cfg.w_add_cap >= 0 && w_add > cfg.w_add_cap) w_add = cfg.w_add_cap;
     op.p = win_params(normalized ? MODE_QCOMP : MODE_NNQ, w_out, w_out + w_add, 0);
     op.p.gamma = g;
     op.p.trace_slot = n_trace++;
@@ -117,7 +121,7 @@ struct bfp_mg_s {
     o.a = r;
     o.out = e;
     o.s1 = L.c;
-    step(ST_RELAX0, l, o, L.p, rule({term(r, L.c.m, L.c.e)}), 2);
+    step(ST_RELAX0, l, o, wd(l), rule({term(r, L.c.m, L.c.e)}), 2);
     const int sweeps = l == cfg.l_coarse ? cfg.n_coarse : cfg.nu1;
     auto jac = [&]() {
       PlanOp j;
@@ -126,7 +130,7 @@ struct bfp_mg_s {
       j.b = r;
       j.out = t;
       j.s1 = L.c;
-      step(ST_RELAX, l, j, L.p, rule({term(e), term(r, L.c.m, L.c.e)}), 3);
+      step(ST_RELAX, l, j, wd(l), rule({term(e), term(r, L.c.m, L.c.e)}), 3);
       std::swap(e, t);
     };
     for (int s = 1; s < sweeps; ++s) jac();
@@ -138,20 +142,20 @@ struct bfp_mg_s {
     g.out = L.rv;
     g.s1 = Scal{-1, 1, 0};
     g.s2 = Scal{1, 2, 0};
-    step(ST_V_RES, l, g, L.p, rule({term(r)}), 4);
+    step(ST_V_RES, l, g, wd(l), rule({term(r)}), 4);
     LevelBufs& Lc = lev[l - 1];
     PlanOp rs;
     rs.kind = OK_RESTRICT;
     rs.a = L.rv;
     rs.out = Lc.vr;
-    step(ST_RESTRICT, l, rs, L.p, rule({term(L.rv)}), 6);
+    step(ST_RESTRICT, l, rs, wd(l), rule({term(L.rv)}), 6);
     bfp_vec_s* ec = vcycle(l - 1, Lc.vr);
     PlanOp pc;
     pc.kind = OK_PCORR;
     pc.a = ec;
     pc.b = e;
     pc.out = t;
-    step(ST_V_CORR, l, pc, L.p, rule({term(e), term(ec)}), 2);
+    step(ST_V_CORR, l, pc, wd(l), rule({term(e), term(ec)}), 2);
     std::swap(e, t);
     for (int s = 0; s < cfg.nu2; ++s) jac();
     return e;
@@ -174,7 +178,7 @@ struct bfp_mg_s {
       o.out = r;
       o.s1 = Scal{-1, 1, 0};
       o.s2 = Scal{1, 2, 0};
-      step(ST_IR_RES, l, o, L.p, g, first ? 5 : 4, true);
+      step(ST_IR_RES, l, o, wd(l), g, first ? 5 : 4, true);
       r_prev = r;
       bfp_vec_s* e = vcycle(l, r);
       bfp_vec_s* xn = (x == L.x[0]) ? L.x[1] : L.x[0];
@@ -202,7 +206,7 @@ struct bfp_mg_s {
     o.out = r;
     o.s1 = Scal{-1, 1, 0};
     o.s2 = Scal{1, 2, 0};
-    step(ST_FINAL_RES, l, o, L.p, rule({term(r_last)}), 4, true);
+    step(ST_FINAL_RES, l, o, wd(l), rule({term(r_last)}), 4, true);
     r_final = r;
   }
 
@@ -232,7 +236,10 @@ struct bfp_mg_s {
   int build() {
     const int lf = cfg.l_fine, lc = cfg.l_coarse;
     int maxp = 0;
-    for (int l = lc; l <= lf; ++l) maxp = std::max(maxp, cfg.p[l] + 6);
+    for (int l = lc; l <= lf; ++l) {
+      const int cap = cfg.w_add_cap >= 0 ? std::min(cfg.w_add_cap, 6) : 6;
+      maxp = std::max(maxp, std::max<int>((int)std::max(wd(l), (int64_t)cfg.p[l]) + cap, (int)wc(l)));
+    }
     ebytes = maxp <= 32 ? 4 : 8;
     lev.assign(lf + 1, LevelBufs());
     for (int l = lc; l <= lf; ++l) {
@@ -262,11 +269,11 @@ struct bfp_mg_s {
       if (!L.b) continue;
       int rc;
       if (cfg.rhs_kind == 1)
-        rc = gen_sine(L.b, L.p, 0);
+        rc = gen_sine(L.b, wc(l), 0);
       else if (cfg.rhs_kind == 0)
-        rc = gen_uniform(L.b, L.p, cfg.seed, 2, 0);
+        rc = gen_uniform(L.b, wc(l), cfg.seed, 2, 0);
       else
-        rc = set_zero(L.b, L.p, 0);
+        rc = set_zero(L.b, wc(l), 0);
       if (rc) return rc;
     }
     // the plan
@@ -332,8 +339,10 @@ int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
       cfg->l_fine > 30 || cfg->nu1 < 1 || cfg->nu2 < 0 || cfg->n_coarse < 1 || cfg->cycles < 0 ||
       cfg->qc < 2 || cfg->qc > 30)
     return BFP_ERR_ARG;
-  for (int l = cfg->l_coarse; l <= cfg->l_fine; ++l)
+  for (int l = cfg->l_coarse; l <= cfg->l_fine; ++l) {
     if (cfg->p[l] < 2 || cfg->p[l] > 58) return BFP_ERR_ARG;
+    if (cfg->pd[l] < 0 || cfg->pd[l] > 58 || cfg->pc[l] < 0 || cfg->pc[l] > 58) return BFP_ERR_ARG;
+  }
   bfp_mg_s* mg = new bfp_mg_s();
   mg->cfg = *cfg;
   int rc = mg->build();

@@ -109,6 +109,9 @@ MG_CASES = [
          nonnormalized=True, p=[0, 0, 0] + [4 + 2 * (l - 3) for l in range(3, 32)][:29]),
     dict(name="c4_small", d=3, l_fine=4, cycles=1, rhs_kind=1, fmg=True, p=24),
     dict(name="c5_small", d=3, l_fine=4, cycles=2, x0_random=True, rhs_kind=2, p=48),
+    # three-width PrecisionSchedule (w / wdot / wcheck) with a w_add cap (config 1 style)
+    dict(name="c1_sched", d=1, l_fine=9, cycles=4, x0_random=True, rhs_kind=0, p=16,
+         pd=[28] * 32, pc=[16] * 32, w_add_cap=4),
 ]
 
 

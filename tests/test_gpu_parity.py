@@ -289,7 +289,9 @@ def test_mg_golden_gpu(B):
 
 
 @pytest.mark.parametrize("name,cfgkw,p", [
-    ("c1", dict(d=1, l_fine=14, cycles=10, x0_random=True, rhs_kind=0), 16),
+    ("c1", dict(d=1, l_fine=14, cycles=10, x0_random=True, rhs_kind=0, pd=[28] * 32,
+                w_add_cap=4), 16),
+    ("c1_flat16", dict(d=1, l_fine=12, cycles=6, x0_random=True, rhs_kind=0), 16),
     ("c2", dict(d=2, l_fine=8, cycles=15, rhs_kind=1), 20),
     ("c3", dict(d=2, l_fine=9, l_coarse=3, cycles=1, rhs_kind=1, fmg=True, nonnormalized=True),
      [0, 0, 0] + [4 + 2 * (l - 3) for l in range(3, 32)][:29]),
