@@ -222,8 +222,6 @@ def run_ours(args, world, rank, local):
     time.sleep(0.2)
     barrier()
     torch.cuda.synchronize()
-    B.profile_enable(True)
-    B.profile_read(reset=True)
     l0 = B.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -233,10 +231,31 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier()
     launches = B.launch_count() - l0
-    kern_ms, kern_n = B.profile_read(reset=True)
-    B.profile_enable(False)
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
+    # dominant-kernel time: pass 1 alone, launched back to back (the recompute launch
+    # is skipped; valid because gamma has the exact binade, checked below), timed
+    # with CUDA events on the launch stream over the whole loop
+    B.set_kernel_path(skip_recompute=True)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    B.set_kernel_path()
+    kern_ms, kern_n = k0.elapsed_time(k1), args.steps
+    for r_ in rs:
+        assert not (r_.header().flags & B.FLAG_RECOMPUTED), "recompute needed: pass-1 timing invalid"
+    # per-launch event brackets (serialising; secondary evidence)
+    B.profile_enable(True)
+    B.profile_read(reset=True)
+    for k in range(min(args.steps, 50)):
+        step(k)
+    torch.cuda.synchronize()
+    ev_ms, ev_n = B.profile_read(reset=True)
+    B.profile_enable(False)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -253,8 +272,12 @@ def run_ours(args, world, rank, local):
     achieved = BYTES_PER_DOF * n / (kavg_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": args.traffic_bytes,
-            "kernel": "grid_win_kernel<int32,GemvOp> pass 1 (qcomp)", "peak_kind": peak_kind,
-            "kernel_ms": kavg_ms, "algorithmic_bytes_per_launch": BYTES_PER_DOF * n}
+            "kernel": "bulk_win_kernel<QCOMP,GemvOp> pass 1 (TMA-bulk smem pipeline)",
+            "peak_kind": peak_kind, "kernel_ms": kavg_ms,
+            "kernel_ms_event_brackets": ev_ms / max(ev_n, 1),
+            "timing": "pass 1 back-to-back over the timed steps (recompute skipped, flags "
+                      "verified clear), CUDA events on the launch stream",
+            "algorithmic_bytes_per_launch": BYTES_PER_DOF * n}
 
     # e2e through the C-ABI with pinned host buffers
     e2e = run_e2e(args, B, Lb, torch, stream, sp)
@@ -284,47 +307,67 @@ def run_ours(args, world, rank, local):
 
 
 def run_e2e(args, B, Lb, torch, stream, sp):
-    import numpy as np
+    """Same metric through the C-ABI with pinned HOST buffers, pipelined across steps:
+    stream A uploads x, b and runs the residual into buffer k%2; stream B downloads
+    r of step k (D2H engine) while A uploads step k+1 (H2D engine)."""
     n = dof()
     x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
     b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
     hx = torch.empty(n, dtype=torch.int32).pin_memory()
     hb = torch.empty(n, dtype=torch.int32).pin_memory()
-    hr = torch.empty(n, dtype=torch.int32).pin_memory()
+    hr = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(2)]
     hh = B._Header()
     for src, dst in ((x, hx), (b, hb)):
         assert Lb.bfp_vec_download_i32(src.h, C.c_void_p(dst.data_ptr()), C.byref(hh), sp) == 0
     qx, ex = x.q, x.e
     qb, eb = b.q, b.e
-    xd = B.BfpVec.grid(D, L_FINE, 4)
-    bd = B.BfpVec.grid(D, L_FINE, 4)
-    rd = B.BfpVec.grid(D, L_FINE, 4)
-    Lb.bfp_vec_upload_i32(xd.h, C.c_void_p(hx.data_ptr()), qx, ex, sp)
-    Lb.bfp_vec_upload_i32(bd.h, C.c_void_p(hb.data_ptr()), qb, eb, sp)
-    B.residual(xd, bd, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=rd)
-    g = B.inf_norm_upper(rd).c()
+    xd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
+    bd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
+    rd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
+    Lb.bfp_vec_upload_i32(xd[0].h, C.c_void_p(hx.data_ptr()), qx, ex, sp)
+    Lb.bfp_vec_upload_i32(bd[0].h, C.c_void_p(hb.data_ptr()), qb, eb, sp)
+    B.residual(xd[0], bd[0], P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=rd[0])
+    g = B.inf_norm_upper(rd[0]).c()
     m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+    sa = stream
+    sb = torch.cuda.Stream()
+    pa, pb = C.c_void_p(sa.cuda_stream), C.c_void_p(sb.cuda_stream)
+    ev_r = [torch.cuda.Event() for _ in range(2)]
+    ev_d = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_d:
+        e.record(sb)
 
-    def step():
-        assert Lb.bfp_vec_upload_i32(xd.h, C.c_void_p(hx.data_ptr()), qx, ex, sp) == 0
-        assert Lb.bfp_vec_upload_i32(bd.h, C.c_void_p(hb.data_ptr()), qb, eb, sp) == 0
-        assert Lb.bfp_stencil_gemv(xd.h, bd.h, m1, p1, 0, P_BITS, W_TMP, g, 0, rd.h, sp) == 0
-        assert Lb.bfp_vec_download_i32(rd.h, C.c_void_p(hr.data_ptr()), C.byref(hh), sp) == 0
+    def step(k):
+        i = k & 1
+        sa.wait_event(ev_d[i])  # download of step k-2 finished with rd[i]
+        assert Lb.bfp_vec_upload_i32(xd[i].h, C.c_void_p(hx.data_ptr()), qx, ex, pa) == 0
+        assert Lb.bfp_vec_upload_i32(bd[i].h, C.c_void_p(hb.data_ptr()), qb, eb, pa) == 0
+        assert Lb.bfp_stencil_gemv(xd[i].h, bd[i].h, m1, p1, 0, P_BITS, W_TMP, g, 0, rd[i].h,
+                                   pa) == 0
+        ev_r[i].record(sa)
+        sb.wait_event(ev_r[i])
+        assert Lb.bfp_vec_download_async_i32(rd[i].h, C.c_void_p(hr[i].data_ptr()), pb) == 0
+        ev_d[i].record(sb)
 
     k = max(3, min(args.steps, 20))
-    for _ in range(2):
-        step()
+    for j in range(2):
+        step(j)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(k):
-        step()
-    e1.record(stream)
+    e0.record(sa)
+    for j in range(k):
+        step(j)
+    sa.wait_stream(sb)
+    e1.record(sa)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    # the downloaded mantissas are the residual (fast path: exponent from the header)
+    h = rd[(k - 1) & 1].header()
+    assert h.err == 0
     return {"value": n * k / (ms / 1e3) / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": 2 * 4 * n,
             "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
-            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv + bfp_vec_download_i32 (pinned host)"}
+            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (stream A) | "
+                    "bfp_vec_download_async_i32 (stream B), pinned host, double-buffered"}
 
 
 SOLVES = {

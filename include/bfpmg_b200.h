@@ -74,6 +74,9 @@ int bfp_vec_upload_i32(bfp_vec_t v, const int32_t* m, int64_t q, int64_t e, void
 /* device -> host mantissas (pending shifts applied); synchronises the stream */
 int bfp_vec_download(bfp_vec_t v, int64_t* m, bfp_header_t* hdr, void* stream);
 int bfp_vec_download_i32(bfp_vec_t v, int32_t* m, bfp_header_t* hdr, void* stream);
+/* stream-ordered download (gather + D2H into a pinned buffer), no synchronisation;
+   read q/e afterwards with bfp_vec_header */
+int bfp_vec_download_async_i32(bfp_vec_t v, int32_t* m, void* stream);
 int bfp_vec_header(bfp_vec_t v, bfp_header_t* hdr, void* stream);
 /* zero_vec(n, q): all zero, e = 0 (src/bfp.cpp:53-55) */
 int bfp_vec_zero(bfp_vec_t v, int64_t q, void* stream);
@@ -181,6 +184,11 @@ int64_t bfp_mg_kernel_launches(bfp_mg_t mg);
  * summed device time and the launch count since the last reset. */
 int bfp_profile_enable(int on);
 int bfp_profile_read(double* total_ms, int64_t* count, int reset);
+/* kernel-path switches (bit-identical results; for A/B measurement and tests):
+   bit 0: 2-D stencil via the bulk-async shared-memory pipeline (1, default) or the
+          register march (0); bit 1: disable programmatic dependent launch;
+   bit 2: skip the qcomp recompute launch (pass-1 timing only; flags must be clear) */
+int bfp_set_kernel_path(int bulk);
 
 /* ---- misc ---- */
 const char* bfp_status_string(int status);

@@ -93,6 +93,7 @@ EXPORTS = [
     "bfp_gen_uniform", "bfp_gen_sine", "bfp_mg_create", "bfp_mg_destroy", "bfp_mg_solve",
     "bfp_mg_result", "bfp_mg_vectors", "bfp_mg_kernel_launches", "bfp_status_string",
     "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
+    "bfp_set_kernel_path", "bfp_vec_download_async_i32",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -159,6 +160,8 @@ def lib() -> C.CDLL:
         "bfp_launch_count": (i64, []),
         "bfp_profile_enable": (i32, [i32]),
         "bfp_profile_read": (i32, [C.POINTER(C.c_double), pi64, i32]),
+        "bfp_set_kernel_path": (i32, [i32]),
+        "bfp_vec_download_async_i32": (i32, [vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -620,3 +623,9 @@ def profile_read(reset: bool = True) -> Tuple[float, int]:
     t, n = C.c_double(), C.c_int64()
     _raise(lib().bfp_profile_read(C.byref(t), C.byref(n), int(reset)), "profile_read")
     return t.value, n.value
+
+
+def set_kernel_path(bulk: bool = True, pdl: bool = True, skip_recompute: bool = False):
+    """Kernel-path switches (see include/bfpmg_b200.h); results are bit-identical."""
+    flags = int(bulk) | (0 if pdl else 2) | (4 if skip_recompute else 0)
+    _raise(lib().bfp_set_kernel_path(flags), "set_kernel_path")

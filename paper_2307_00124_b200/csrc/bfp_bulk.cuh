@@ -1,0 +1,62 @@
+// bfp_bulk.cuh -- bulk-async (TMA engine) staged stencil pipeline for the 2-D
+// int32 hot path on sm_100a.
+//
+// A CTA owns a strip of W = 4*T columns and marches R rows.  One elected
+// thread streams rows global -> shared with cp.async.bulk (the TMA engine's 1-D
+// bulk copy) into a ring of D+3 x-row slots and D+1 y-row slots, signalling a
+// ring of mbarriers with complete_tx; the consumers wait on the mbarrier of the
+// step, read their 4 points and the 3-row neighbourhood from shared memory,
+// and write one int4.  Bytes in flight are bounded by shared memory (D steps
+// of (W+8)+W words per CTA), not by registers.
+#pragma once
+#include "bfp_dev.cuh"
+
+namespace bfpdev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// 1-D bulk copy global -> shared (16-B aligned, size multiple of 16), completes tx on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kBulkT = 256;             // threads per CTA (one 4-group each)
+constexpr int kBulkW = 4 * kBulkT;      // strip width in columns
+constexpr int kBulkD = 4;               // prefetch depth (steps in flight)
+constexpr int kBulkXS = kBulkD + 3;     // x-row slots
+constexpr int kBulkYS = kBulkD + 1;     // y-row slots / mbarriers
+constexpr int kBulkXW = kBulkW + 8;     // x slot width (4-word halo each side)
+constexpr size_t kBulkSmem =
+    (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4 + kBulkYS * 8 + 64;
+
+}  // namespace bfpdev

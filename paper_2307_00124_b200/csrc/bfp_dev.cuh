@@ -64,6 +64,16 @@ struct TraceRec {
 };
 
 // ---------------------------------------------------------------------------
+// programmatic dependent launch (sm_90+): wait for the previous grid's results /
+// let the next grid be scheduled
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
 // integer primitives
 
 __device__ __forceinline__ int bitlen64(uint64_t u) { return u ? 64 - __clzll((long long)u) : 0; }

@@ -27,8 +27,30 @@ struct bfp_csr_s {
   int64_t* buf = nullptr;
 };
 
+namespace bfpdev {
+// fused coarse-level op list entry (bfp_lib.cu: fused_kernel)
+enum { FK_GEMV = 0, FK_JACOBI, FK_SCAL, FK_AXPBY, FK_RESTRICT, FK_PROLONG, FK_PCORR, FK_ZERO };
+constexpr int kFusedThreads = 512;
+struct FusedOp {
+  int32_t kind, pad;
+  int64_t q;
+  Vec out;
+  WinParams p;
+  union U {
+    GemvOp gemv;
+    JacobiOp jac;
+    ScalOp scal;
+    AxpbyOp axpby;
+    RestrictOp rst;
+    ProlongOp pro;
+    ProlongCorrectOp pc;
+  } u;
+};
+}  // namespace bfpdev
+
 namespace bfp {
 
+using bfpdev::FusedOp;
 using bfpdev::GammaRule;
 using bfpdev::Scal;
 using bfpdev::WinParams;
@@ -58,6 +80,9 @@ int gen_uniform(bfp_vec_s* v, int64_t p, uint64_t seed, uint64_t stream_id, cuda
 int gen_sine(bfp_vec_s* v, int64_t p, cudaStream_t s);
 
 void jacobi_coeff(int dim, int level, int64_t qc, int64_t* cm, int64_t* ce);
+int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const WinParams& p,
+               int64_t q, bfp_vec_s* out, FusedOp* f);
+int fused_launch(const FusedOp* d_ops, int n, int ebytes, cudaStream_t s);
 void count_launch(int n = 1);
 int64_t launches();
 

@@ -62,18 +62,25 @@ __device__ __forceinline__ int64_t zbits(const Hdr* h) { return max_abs(h) ? eff
 __device__ __forceinline__ int64_t grow(int64_t b, int64_t extra) { return b ? b + extra : 0; }
 
 // ---- vector loads (pending shift applied) ---------------------------------
+// NC = true: read-only (non-coherent) path, valid when the data was produced by
+// an earlier kernel; NC = false: coherent loads for the fused single-CTA kernel,
+// which reads data it wrote itself earlier in the same launch.
+template <bool NC, typename T> __device__ __forceinline__ T ldx(const T* p) {
+  if constexpr (NC) return __ldg(p);
+  else return *p;
+}
 
-template <typename M> struct V4;
-template <> struct V4<int32_t> {
+template <typename M, bool NC = true> struct V4;
+template <bool NC> struct V4<int32_t, NC> {
   __device__ static __forceinline__ void load(const Vec& v, int64_t o, int64_t sh, int64_t r[4]) {
-    int4 t = __ldg(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
+    int4 t = ldx<NC>(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
     r[0] = ((int64_t)t.x) >> sh;
     r[1] = ((int64_t)t.y) >> sh;
     r[2] = ((int64_t)t.z) >> sh;
     r[3] = ((int64_t)t.w) >> sh;
   }
   __device__ static __forceinline__ void load32(const Vec& v, int64_t o, int sh, int r[4]) {
-    int4 t = __ldg(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
+    int4 t = ldx<NC>(reinterpret_cast<const int4*>((const int32_t*)v.data + o));
     r[0] = t.x >> sh;
     r[1] = t.y >> sh;
     r[2] = t.z >> sh;
@@ -84,10 +91,10 @@ template <> struct V4<int32_t> {
     *reinterpret_cast<int4*>((int32_t*)v.data + o) = t;
   }
 };
-template <> struct V4<int64_t> {
+template <bool NC> struct V4<int64_t, NC> {
   __device__ static __forceinline__ void load(const Vec& v, int64_t o, int64_t sh, int64_t r[4]) {
     const longlong2* p = reinterpret_cast<const longlong2*>((const int64_t*)v.data + o);
-    longlong2 a = __ldg(p), b = __ldg(p + 1);
+    longlong2 a = ldx<NC>(p), b = ldx<NC>(p + 1);
     r[0] = a.x >> sh;
     r[1] = a.y >> sh;
     r[2] = b.x >> sh;
@@ -99,8 +106,9 @@ template <> struct V4<int64_t> {
     p[1] = make_longlong2(r[2], r[3]);
   }
 };
-template <typename M> __device__ __forceinline__ int64_t ld1(const Vec& v, int64_t o, int64_t sh) {
-  return ((int64_t)__ldg((const M*)v.data + o)) >> sh;
+template <typename M, bool NC = true>
+__device__ __forceinline__ int64_t ld1(const Vec& v, int64_t o, int64_t sh) {
+  return ((int64_t)ldx<NC>((const M*)v.data + o)) >> sh;
 }
 
 // pad mask of 4 consecutive grid storage offsets starting at o (o % 4 == 0)
@@ -115,23 +123,24 @@ __device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4]) {
 }
 
 // 32-bit stencil (used when the width bound proves |S x| < 2^31)
+template <bool NC>
 __device__ __forceinline__ void stencil4_32(const Vec& x, int sx, int dim, int l, int64_t o,
                                             int g[4], int c[4]) {
-  V4<int32_t>::load32(x, o, sx, c);
+  V4<int32_t, NC>::load32(x, o, sx, c);
   const int32_t* p = (const int32_t*)x.data;
-  const int lf = __ldg(p + o - 1) >> sx, rt = __ldg(p + o + 4) >> sx;
+  const int lf = ldx<NC>(p + o - 1) >> sx, rt = ldx<NC>(p + o + 4) >> sx;
   int nb[4] = {lf + c[1], c[0] + c[2], c[1] + c[3], c[2] + rt};
   if (dim >= 2) {
     const int64_t N = (int64_t)1 << l;
     int u[4], d[4];
-    V4<int32_t>::load32(x, o - N, sx, u);
-    V4<int32_t>::load32(x, o + N, sx, d);
+    V4<int32_t, NC>::load32(x, o - N, sx, u);
+    V4<int32_t, NC>::load32(x, o + N, sx, d);
 #pragma unroll
     for (int j = 0; j < 4; ++j) nb[j] += u[j] + d[j];
     if (dim >= 3) {
       const int64_t N2 = N * N;
-      V4<int32_t>::load32(x, o - N2, sx, u);
-      V4<int32_t>::load32(x, o + N2, sx, d);
+      V4<int32_t, NC>::load32(x, o - N2, sx, u);
+      V4<int32_t, NC>::load32(x, o + N2, sx, d);
 #pragma unroll
       for (int j = 0; j < 4; ++j) nb[j] += u[j] + d[j];
     }
@@ -158,11 +167,11 @@ __device__ __forceinline__ int64_t mad_pow2(int a, int s, int64_t add) {
 }
 
 // stencil S_d applied to 4 consecutive points at storage offset o (mantissa units)
-template <typename M, typename A>
+template <typename M, typename A, bool NC>
 __device__ __forceinline__ void stencil4(const Vec& x, int64_t sx, int dim, int l, int64_t o,
                                          A g[4], int64_t c[4]) {
-  V4<M>::load(x, o, sx, c);
-  int64_t lf = ld1<M>(x, o - 1, sx), rt = ld1<M>(x, o + 4, sx);
+  V4<M, NC>::load(x, o, sx, c);
+  int64_t lf = ld1<M, NC>(x, o - 1, sx), rt = ld1<M, NC>(x, o + 4, sx);
   A nb[4];
   nb[0] = (A)lf + (A)c[1];
   nb[1] = (A)c[0] + (A)c[2];
@@ -171,14 +180,14 @@ __device__ __forceinline__ void stencil4(const Vec& x, int64_t sx, int dim, int 
   if (dim >= 2) {
     const int64_t N = (int64_t)1 << l;
     int64_t u[4], d[4];
-    V4<M>::load(x, o - N, sx, u);
-    V4<M>::load(x, o + N, sx, d);
+    V4<M, NC>::load(x, o - N, sx, u);
+    V4<M, NC>::load(x, o + N, sx, d);
 #pragma unroll
     for (int j = 0; j < 4; ++j) nb[j] += (A)u[j] + (A)d[j];
     if (dim >= 3) {
       const int64_t N2 = N * N;
-      V4<M>::load(x, o - N2, sx, u);
-      V4<M>::load(x, o + N2, sx, d);
+      V4<M, NC>::load(x, o - N2, sx, u);
+      V4<M, NC>::load(x, o + N2, sx, d);
 #pragma unroll
       for (int j = 0; j < 4; ++j) nb[j] += (A)u[j] + (A)d[j];
     }
@@ -228,12 +237,19 @@ struct GemvOp {
     const int X = swap ? yv : g, Y = swap ? g : yv;
     return (int64_t)X * (int64_t)P + (int64_t)(Q * Y);
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  __device__ __forceinline__ bool swapped() const { return swap; }
+  template <bool SW> __device__ __forceinline__ int64_t point_t(int g, int c, int yv) const {
+    (void)c;
+    return SW ? (int64_t)yv * (int64_t)P + (int64_t)(Q * g)
+              : (int64_t)g * (int64_t)P + (int64_t)(Q * yv);
+  }
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
       if (narrow) {
         int g[4], c[4], yv[4];
-        stencil4_32(x, (int)sx, dim, l, o, g, c);
-        V4<int32_t>::load32(y, o, (int)sy, yv);
+        stencil4_32<NC>(x, (int)sx, dim, l, o, g, c);
+        V4<int32_t, NC>::load32(y, o, (int)sy, yv);
         const uint32_t mN = (1u << l) - 1;
         const uint32_t ix = (uint32_t)o & mN;
         bool rowpad = false;
@@ -251,8 +267,8 @@ struct GemvOp {
     }
     A g[4];
     int64_t c[4], yv[4];
-    stencil4<M, A>(x, sx, dim, l, o, g, c);
-    V4<M>::load(y, o, sy, yv);
+    stencil4<M, A, NC>(x, sx, dim, l, o, g, c);
+    V4<M, NC>::load(y, o, sy, yv);
     bool pad[4];
     pad4(dim, l, o, pad);
 #pragma unroll
@@ -295,12 +311,17 @@ struct JacobiOp {
     const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)c.m);
     return mad_pow2(cx, s2, cr);
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  __device__ __forceinline__ bool swapped() const { return false; }
+  template <bool SW> __device__ __forceinline__ int64_t point_t(int g, int cx, int bv) const {
+    return point(g, cx, bv);
+  }
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
       if (narrow) {
         int g[4], cx[4], bv[4];
-        stencil4_32(x, (int)sx, dim, l, o, g, cx);
-        V4<int32_t>::load32(b, o, (int)sb, bv);
+        stencil4_32<NC>(x, (int)sx, dim, l, o, g, cx);
+        V4<int32_t, NC>::load32(b, o, (int)sb, bv);
         const uint32_t mN = (1u << l) - 1;
         const uint32_t ix = (uint32_t)o & mN;
         bool rowpad = false;
@@ -320,8 +341,8 @@ struct JacobiOp {
     }
     A g[4];
     int64_t cx[4], bv[4];
-    stencil4<M, A>(x, sx, dim, l, o, g, cx);
-    V4<M>::load(b, o, sb, bv);
+    stencil4<M, A, NC>(x, sx, dim, l, o, g, cx);
+    V4<M, NC>::load(b, o, sb, bv);
     bool pad[4];
     pad4(dim, l, o, pad);
 #pragma unroll
@@ -342,9 +363,10 @@ struct ScalOp {
     sr = r.hdr->shift;
     need = msb((int64_t)c.m) + eff_bits(r.hdr) + 1;
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     int64_t v[4];
-    V4<M>::load(r, o, sr, v);
+    V4<M, NC>::load(r, o, sr, v);
 #pragma unroll
     for (int j = 0; j < 4; ++j) z[j] = (A)c.m * (A)v[j];
   }
@@ -361,10 +383,11 @@ struct AxpbyOp {
     sy = y.hdr->shift;
     need = combine_bits(al.m, zbits(x.hdr), be.m, zbits(y.hdr), d);
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     int64_t xv[4], yv[4];
-    V4<M>::load(x, o, sx, xv);
-    V4<M>::load(y, o, sy, yv);
+    V4<M, NC>::load(x, o, sx, xv);
+    V4<M, NC>::load(y, o, sy, yv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) z[j] = combine<A>(al.m, (A)xv[j], be.m, (A)yv[j], d);
   }
@@ -380,7 +403,8 @@ struct RestrictOp {
     sr = r.hdr->shift;
     need = eff_bits(r.hdr) + 2 * dim + 2;
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     const int lc = l - 1;
     const int64_t Nc = (int64_t)1 << lc, mc = Nc - 1, Nf = (int64_t)1 << l;
     bool pad[4];
@@ -396,8 +420,8 @@ struct RestrictOp {
       if (!pad[j]) {
         // x-line weights (1,2,1) on each contributing fine row
         auto line = [&](int64_t base) -> A {
-          return (A)ld1<M>(r, base - 1, sr) + 2 * (A)ld1<M>(r, base, sr) +
-                 (A)ld1<M>(r, base + 1, sr);
+          return (A)ld1<M, NC>(r, base - 1, sr) + 2 * (A)ld1<M, NC>(r, base, sr) +
+                 (A)ld1<M, NC>(r, base + 1, sr);
         };
         if (dim == 1) {
           acc = line(fc);
@@ -418,18 +442,18 @@ struct RestrictOp {
 
 // linear interpolation: per axis taps (i-1)>>1 and i>>1 with weight 1 each
 // (odd i -> both taps = (i-1)/2, i.e. weight 2).  Coarse pads/halo are zero.
-template <typename M, typename A>
+template <typename M, typename A, bool NC = true>
 __device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int l, int64_t o) {
   const int64_t Nf = (int64_t)1 << l, mf = Nf - 1;
   const int lc = l - 1;
   const int64_t Nc = (int64_t)1 << lc;
   const int64_t i = o & mf;
   const int64_t a0 = (i - 1) >> 1, a1 = i >> 1;
-  if (dim == 1) return (A)ld1<M>(xc, a0, sc) + (A)ld1<M>(xc, a1, sc);
+  if (dim == 1) return (A)ld1<M, NC>(xc, a0, sc) + (A)ld1<M, NC>(xc, a1, sc);
   const int64_t j = (o >> l) & mf;
   const int64_t b0 = ((j - 1) >> 1) * Nc, b1 = (j >> 1) * Nc;
   auto line = [&](int64_t rowoff) -> A {
-    return (A)ld1<M>(xc, rowoff + a0, sc) + (A)ld1<M>(xc, rowoff + a1, sc);
+    return (A)ld1<M, NC>(xc, rowoff + a0, sc) + (A)ld1<M, NC>(xc, rowoff + a1, sc);
   };
   if (dim == 2) return line(b0) + line(b1);
   const int64_t k = (o >> (2 * l)) & mf;
@@ -448,11 +472,12 @@ struct ProlongOp {
     sc = xc.hdr->shift;
     need = eff_bits(xc.hdr) + dim + 2;
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
     pad4(dim, l, o, pad);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : prolong_at<M, A>(xc, sc, dim, l, o + j);
+    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j);
   }
 };
 
@@ -469,14 +494,15 @@ struct ProlongCorrectOp {
     int64_t bg = grow(zbits(ec.hdr), dim + 2);
     need = combine_bits(1, bg, 1, zbits(y.hdr), d);
   }
-  template <typename M, typename A> __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
+  template <typename M, typename A, bool NC = true>
+  __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
     pad4(dim, l, o, pad);
     int64_t yv[4];
-    V4<M>::load(y, o, sy, yv);
+    V4<M, NC>::load(y, o, sy, yv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      A g = prolong_at<M, A>(ec, sc, dim, l, o + j);
+      A g = prolong_at<M, A, NC>(ec, sc, dim, l, o + j);
       z[j] = pad[j] ? A(0) : combine<A>(1, g, 1, (A)yv[j], d);
     }
   }

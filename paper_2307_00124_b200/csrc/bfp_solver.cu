@@ -9,6 +9,7 @@
 // gamma rules live in device headers, the whole solve is a static PLAN of
 // kernel launches: built once, replayed stream-ordered or as one CUDA graph.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -24,7 +25,7 @@ enum StepKind {
   ST_FMG_PROLONG, ST_FINAL_RES
 };
 enum OpKind { OK_ZERO, OK_UNIFORM, OK_GEMV, OK_JACOBI, OK_SCAL, OK_AXPBY, OK_RESTRICT,
-              OK_PROLONG, OK_PCORR };
+              OK_PROLONG, OK_PCORR, OK_FUSED };
 
 struct PlanOp {
   int kind;
@@ -33,7 +34,33 @@ struct PlanOp {
   WinParams p;
   int64_t q = 0;
   uint64_t seed = 0, sid = 0;
+  std::vector<PlanOp> sub;  // OK_FUSED: the coarse-level ops run by one CTA
+  FusedOp* dev = nullptr;
 };
+
+int fused_kind(int k) {
+  switch (k) {
+    case OK_GEMV: return bfpdev::FK_GEMV;
+    case OK_JACOBI: return bfpdev::FK_JACOBI;
+    case OK_SCAL: return bfpdev::FK_SCAL;
+    case OK_AXPBY: return bfpdev::FK_AXPBY;
+    case OK_RESTRICT: return bfpdev::FK_RESTRICT;
+    case OK_PROLONG: return bfpdev::FK_PROLONG;
+    case OK_PCORR: return bfpdev::FK_PCORR;
+    case OK_ZERO: return bfpdev::FK_ZERO;
+  }
+  return -1;
+}
+// levels whose padded grid has at most this many points run fused in one CTA
+// (BFP_FUSE_POINTS overrides; 0 disables fusion)
+int64_t fuse_max_points() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("BFP_FUSE_POINTS");
+    v = e ? atoll(e) : 0;  // off by default: slower than PDL-chained launches (profiles/)
+  }
+  return v;
+}
 
 struct LevelBufs {
   int l = 0;
@@ -78,7 +105,12 @@ struct bfp_mg_s {
   std::vector<bfp_vec_s*> owned;
   int err = 0;
 
+  bool in_fused = false;
+  bool fusion = true;
+
   ~bfp_mg_s() {
+    for (auto& op : plan)
+      if (op.dev) cudaFree(op.dev);
     if (graph) cudaGraphExecDestroy(graph);
     for (auto* v : owned) vec_free(v);
     cudaFree(d_trace);
@@ -113,7 +145,27 @@ struct bfp_mg_s {
     plan.push_back(op);
   }
 
+  bool fusable(int l) const {
+    int64_t pts = 1;
+    for (int a = 0; a < cfg.d; ++a) pts <<= l;
+    return fusion && !in_fused && pts <= fuse_max_points();
+  }
+  // run body() with its plan ops collected into one OK_FUSED op
+  template <typename F> bfp_vec_s* fused(F body) {
+    const size_t i0 = plan.size();
+    in_fused = true;
+    bfp_vec_s* res = body();
+    in_fused = false;
+    PlanOp f;
+    f.kind = OK_FUSED;
+    f.sub.assign(plan.begin() + i0, plan.end());
+    plan.resize(i0);
+    plan.push_back(std::move(f));
+    return res;
+  }
+
   bfp_vec_s* vcycle(int l, bfp_vec_s* r) {
+    if (fusable(l)) return fused([&]() { return vcycle(l, r); });
     LevelBufs& L = lev[l];
     bfp_vec_s *e = L.e[0], *t = L.e[1];
     PlanOp o;
@@ -211,6 +263,7 @@ struct bfp_mg_s {
   }
 
   bfp_vec_s* fmg(int l) {
+    if (fusable(l)) return fused([&]() { return fmg(l); });
     LevelBufs& L = lev[l];
     bfp_vec_s* x = L.x[0];
     if (l == cfg.l_coarse) {
@@ -305,6 +358,19 @@ struct bfp_mg_s {
     for (auto& op : plan) {
       op.p.trace = d_trace;
       op.p.hist = op.p.hist_slot >= 0 ? d_hist : nullptr;
+      if (op.kind != OK_FUSED) continue;
+      std::vector<FusedOp> h(op.sub.size());
+      for (size_t i = 0; i < op.sub.size(); ++i) {
+        PlanOp& so = op.sub[i];
+        so.p.trace = d_trace;
+        so.p.hist = so.p.hist_slot >= 0 ? d_hist : nullptr;
+        const int fk = fused_kind(so.kind);
+        if (fk < 0) return BFP_ERR_ARG;
+        int rc = fused_make(fk, so.a, so.b, so.s1, so.s2, so.p, so.q, so.out, &h[i]);
+        if (rc) return rc;
+      }
+      if (cudaMalloc(&op.dev, sizeof(FusedOp) * h.size()) != cudaSuccess) return BFP_ERR_NOMEM;
+      cudaMemcpy(op.dev, h.data(), sizeof(FusedOp) * h.size(), cudaMemcpyHostToDevice);
     }
     return cudaDeviceSynchronize() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
   }
@@ -323,6 +389,7 @@ struct bfp_mg_s {
         case OK_RESTRICT: rc = op_restrict(op.a, op.p, op.out, s); break;
         case OK_PROLONG: rc = op_prolong(op.a, op.p, op.out, s); break;
         case OK_PCORR: rc = op_prolong_correct(op.a, op.b, op.p, op.out, s); break;
+        case OK_FUSED: rc = fused_launch(op.dev, (int)op.sub.size(), ebytes, s); break;
       }
       if (rc) return rc;
     }
@@ -345,6 +412,7 @@ int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
   }
   bfp_mg_s* mg = new bfp_mg_s();
   mg->cfg = *cfg;
+  if (const char* ev = getenv("BFP_NO_FUSION")) mg->fusion = ev[0] != '1';
   int rc = mg->build();
   if (rc) {
     delete mg;

@@ -322,3 +322,31 @@ def test_full_size_residual_c2(B):
         m, q, e = res.z.download()
         assert e == want.e and np.array_equal(m, want.m)
         assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1]))
+
+
+@pytest.mark.parametrize("l", [10, 11])
+def test_stencil_paths_agree_with_oracle(B, l):
+    """2-D stencil ops through the bulk-async pipeline (N >= 1024) and through the
+    register march are both bit-exact vs the oracle (qcomp fast / recompute, nnqcomp)."""
+    d, p = 2, 20
+    ox, ob_ = ob.gen_uniform(d, l, p, 3, 1), ob.gen_sine(d, l, p)
+    c = B.jacobi_coeff(d, l, 16)
+    try:
+        for bulk in (True, False):
+            B.set_kernel_path(bulk)
+            gx = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 3, 1)
+            gb = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
+            for g, nn in ((B.Scalar(1 << 14, 16, 2 * l + 2), False), (B.Scalar(1 << 14, 16, 0), False),
+                          (B.Scalar(1 << 14, 16, 2 * l + 2), True)):
+                mode = "nn" if nn else "q"
+                res = B.residual(gx, gb, p, p + 5, g, nn=nn)
+                want, fl = ob.stencil_gemv(d, l, ox, ob_, (-1, 1, 0), (1, 2, 0), mode, p, p + 5,
+                                           g.m, g.e)
+                m, q, e = res.z.download()
+                assert e == want.e and np.array_equal(m, want.m), (bulk, g, nn)
+                j = B.jacobi(gx, res.z, c, p, p + 5, g, nn=nn)
+                wj, _ = ob.jacobi(d, l, ox, want, (c.m, c.q, c.e), mode, p, p + 5, g.m, g.e)
+                m, q, e = j.z.download()
+                assert e == wj.e and np.array_equal(m, wj.m), (bulk, "jacobi", g, nn)
+    finally:
+        B.set_kernel_path(True)
