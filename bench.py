@@ -175,13 +175,85 @@ def workload_config():
 # our arm
 
 
+def run_sharded(args, world, rank, local):
+    """N GPUs: the C2 residual z-slab sharded over the ranks (strong scaling): NCCL halo
+    exchange of one row per neighbour and MAX all-reduces of the window partials
+    (paper_2307_00124_b200/dist.py).  --sharded forces this path at N = 1."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    import paper_2307_00124_b200 as B
+    from paper_2307_00124_b200 import dist as Dm
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    B.set_stream(stream.cuda_stream)
+    n = dof()
+    lo, hi = Dm.slab_ranges(L_FINE, world)[rank]
+    nn_ = (1 << L_FINE) - 1
+    gx = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
+    gb = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+    g = B.inf_norm_upper(B.residual(gx, gb, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40)).z)
+    be = Dm.GpuBackend()
+    ds = Dm.DistStencil(Dm.TorchComm(be), be)
+
+    def slab_of(full):
+        m, q, e = full.download()
+        v = B.BfpVec.slab(D, L_FINE, lo, hi)
+        v.upload(m[lo * nn_: min(hi, nn_) * nn_], q, e)
+        return Dm.Slab(rank, v)
+    xs, bs = slab_of(gx), slab_of(gb)
+    outs = [Dm.Slab(rank, B.BfpVec.slab(D, L_FINE, lo, hi)) for _ in range(2)]
+
+    def step(k):
+        ds.gemv([xs], [bs], B.bfp_minus_one(), B.bfp_one(), P_BITS, W_TMP, g, [outs[k & 1]])
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = B.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = B.launch_count() - l0
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    # parity of the sharded result with the unsharded residual on this rank's planes
+    ref = B.residual(gx, gb, P_BITS, W_TMP, g)
+    mr, _, er = ref.z.download()
+    mo, _, eo = outs[(args.steps - 1) & 1].vec.download()
+    ok = eo == er and np.array_equal(mo, mr[lo * nn_: min(hi, nn_) * nn_])
+    okt = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    line = {
+        "metric": "bfp_stencil_residual_gdofs", "value": n * args.steps / (ms / 1e3) / 1e9,
+        "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": dict(workload_config(), parallelism=f"z-slab x{world} (NCCL halo + MAX allreduce)"),
+        "gpu_launches": int(launches), "sharded_parity_with_unsharded": bool(okt.item()),
+    }
+    dist.barrier()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args, world, rank, local):
     import torch
     torch.cuda.set_device(local)
     import paper_2307_00124_b200 as B
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     B.set_stream(stream.cuda_stream)
     Lb = B.lib()
@@ -417,6 +489,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-rank (z-slab) path even on one GPU")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="ncu dram bytes per launch of the dominant kernel (profiles/)")
@@ -426,6 +500,8 @@ def main():
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         return run_reference(args, world, rank)
+    if world > 1 or args.sharded:
+        return run_sharded(args, world, rank, local)
     return run_ours(args, world, rank, local)
 
 

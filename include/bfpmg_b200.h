@@ -138,6 +138,27 @@ int bfp_prolong(bfp_vec_t xc, int mode, int64_t w_out, int64_t w_tmp, bfp_scalar
                 bfp_vec_t out, void* stream);
 int bfp_prolong_correct(bfp_vec_t ec, bfp_vec_t y, int mode, int64_t w_out, int64_t w_tmp,
                         bfp_scalar_t gamma, bfp_vec_t out, void* stream);
+/* ---- multi-rank z-slab decomposition ----
+ * A slab holds planes [z_lo, z_hi) of the padded global grid along the slowest axis
+ * (2-D rows, 3-D planes) plus one halo plane on each side.  Stencil ops on slabs run
+ * in two stages per window: stage 0 (qcomp pass 1 / nnqcomp) and stage 1 (qcomp
+ * recompute, a no-op unless the finalized header asks for it).  Each stage writes its
+ * partials {mu*, max, -min, err} (int64[4], device) to d_part; after an all-reduce(MAX)
+ * of d_part over the ranks, bfp_window_finalize applies them to the header exactly as
+ * the single-rank finalizer does. */
+int bfp_vec_create_slab(int dim, int level, int z_lo, int z_hi, int mant_bytes, bfp_vec_t* out);
+/* device pointers: first / last owned plane and the lower / upper halo planes */
+int bfp_vec_planes(bfp_vec_t v, void** first, void** last, void** halo_lo, void** halo_hi,
+                   int64_t* plane_bytes);
+int bfp_stencil_gemv_part(bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta,
+                          int mode, int stage, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                          bfp_vec_t out, int64_t* d_part, void* stream);
+int bfp_stencil_jacobi_part(bfp_vec_t x, bfp_vec_t b, bfp_scalar_t c, int mode, int stage,
+                            int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma, bfp_vec_t out,
+                            int64_t* d_part, void* stream);
+int bfp_window_finalize(bfp_vec_t out, int mode, int stage, int64_t w_out, int64_t w_tmp,
+                        const int64_t* d_part, void* stream);
+
 /* Jacobi coefficient c = floor_qc(omega_d / 2d) * 2^{-2l} as a BFP scalar */
 int bfp_jacobi_coeff(int dim, int level, int64_t qc, bfp_scalar_t* c);
 

@@ -93,7 +93,8 @@ EXPORTS = [
     "bfp_gen_uniform", "bfp_gen_sine", "bfp_mg_create", "bfp_mg_destroy", "bfp_mg_solve",
     "bfp_mg_result", "bfp_mg_vectors", "bfp_mg_kernel_launches", "bfp_status_string",
     "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
-    "bfp_set_kernel_path", "bfp_vec_download_async_i32",
+    "bfp_set_kernel_path", "bfp_vec_download_async_i32", "bfp_vec_create_slab", "bfp_vec_planes",
+    "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -162,6 +163,12 @@ def lib() -> C.CDLL:
         "bfp_profile_read": (i32, [C.POINTER(C.c_double), pi64, i32]),
         "bfp_set_kernel_path": (i32, [i32]),
         "bfp_vec_download_async_i32": (i32, [vp, vp, vp]),
+        "bfp_vec_create_slab": (i32, [i32, i32, i32, i32, i32, C.POINTER(vp)]),
+        "bfp_vec_planes": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                 pi64]),
+        "bfp_stencil_gemv_part": (i32, [vp, vp, S, S, i32, i32, i64, i64, S, vp, vp, vp]),
+        "bfp_stencil_jacobi_part": (i32, [vp, vp, S, i32, i32, i64, i64, S, vp, vp, vp]),
+        "bfp_window_finalize": (i32, [vp, i32, i32, i64, i64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -241,6 +248,23 @@ class BfpVec:
         h = C.c_void_p()
         _raise(lib().bfp_vec_create_grid(dim, level, mant_bytes, C.byref(h)), "bfp_vec_create_grid")
         return BfpVec(h.value, dim, level, mant_bytes)
+
+    @staticmethod
+    def slab(dim: int, level: int, z_lo: int, z_hi: int, mant_bytes: int = 4) -> "BfpVec":
+        """Planes [z_lo, z_hi) of the padded global grid (slowest axis) plus halo planes."""
+        h = C.c_void_p()
+        _raise(lib().bfp_vec_create_slab(dim, level, z_lo, z_hi, mant_bytes, C.byref(h)),
+               "bfp_vec_create_slab")
+        v = BfpVec(h.value, dim, level, mant_bytes)
+        v.z_lo, v.z_hi = z_lo, z_hi
+        return v
+
+    def planes(self):
+        """(first, last, halo_lo, halo_hi) device pointers and bytes per plane."""
+        f, l, hl, hh, nb = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_int64()
+        _raise(lib().bfp_vec_planes(self.h, C.byref(f), C.byref(l), C.byref(hl), C.byref(hh),
+                                    C.byref(nb)), "bfp_vec_planes")
+        return f.value, l.value, hl.value, hh.value, nb.value
 
     @staticmethod
     def from_mantissas(m: Sequence[int], q: int, e: int, dim: int = 0, level: int = 0,

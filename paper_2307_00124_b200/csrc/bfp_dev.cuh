@@ -39,6 +39,8 @@ struct alignas(128) Hdr {
   long long acc_max, acc_min;
   unsigned int acc_done;
   int32_t acc_err;
+  // partial (multi-rank) windows: the pass-1 window context, for the finalize kernel
+  int64_t st_estar, st_mutmp, st_lam, st_gm, st_ge;
 };
 
 enum { FLAG_OVERFLOW = 1, FLAG_UNDERFLOW = 2, FLAG_RECOMPUTED = 4, FLAG_NORMALIZED = 8 };
@@ -51,9 +53,11 @@ struct Vec {
   int32_t ebytes;  // 4 or 8
   int32_t dim;     // 0 = flat, 1..3 = grid
   int32_t l;       // grid level (N = 2^l)
-  int32_t pad;
-  int64_t n;       // storage span in elements (flat: padded to 4; grid: N^dim)
+  int32_t z0;      // slab: global index of local plane 0 along the slowest axis
+  int64_t n;       // storage span in elements (flat: padded to 4; grid: nz * N^(dim-1))
   int64_t nlog;    // logical entries
+  int32_t nz;      // planes along the slowest axis held locally (N for a full grid)
+  int32_t pad;
 };
 
 // trace record (bfp_trace_rec_t layout)
@@ -279,6 +283,7 @@ struct WinParams {
   int32_t level, hist_slot;
   TraceRec* trace;
   double* hist;   // residual-norm history slot (ldexp(max|m|, e)), or nullptr
+  int64_t* part;  // multi-rank: write {mu*, max, -min, err} partials here instead of finalizing
   GammaRule gamma;
 };
 
@@ -456,9 +461,29 @@ __device__ inline void write_hist(const WinParams& p, const Hdr* h) {
   p.hist[p.hist_slot] = ldexp((double)max_abs(h), (int)h->e);
 }
 
+// multi-rank: record the launch's partial reduction and window context (one thread)
+__device__ inline void win_partial(const WinParams& p, const WinCtx& c, Hdr* h, int bits,
+                                   int64_t mx, int64_t mn, int err) {
+  p.part[0] = bits;
+  p.part[1] = mx;
+  p.part[2] = mn == INT64_MIN ? INT64_MAX : -mn;
+  p.part[3] = err;
+  if (p.mode != MODE_RECOMPUTE) {
+    h->st_estar = c.e_star;
+    h->st_mutmp = c.mu_tmp;
+    h->st_lam = c.lam;
+    h->st_gm = c.gm;
+    h->st_ge = c.ge;
+  }
+}
+
 // finalize for one launch (runs on one thread)
 __device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, int bits,
                                     int64_t mx, int64_t mn, int err) {
+  if (p.part) {
+    win_partial(p, c, h, bits, mx, mn, err);
+    return;
+  }
   if (err) h->err |= err;
   if (p.mode == MODE_QCOMP) {
     int64_t mu_star = bits;                 // src/blas.cpp:153,158

@@ -12,6 +12,7 @@
 
 struct bfp_vec_s {
   int dim = 0, l = 0, ebytes = 4;
+  int z0 = 0, nz = 0;  // slab: global index of local plane 0 / local planes (slowest axis)
   int64_t nlog = 0, span = 0, halo = 0;
   char* base = nullptr;  // device allocation (halo + span + halo)
   void* data = nullptr;  // element 0
@@ -57,6 +58,7 @@ using bfpdev::WinParams;
 
 bfpdev::Vec view(const bfp_vec_s* v);
 int vec_alloc(int dim, int level, int64_t n, int ebytes, bfp_vec_s** out);
+int vec_alloc_slab(int dim, int level, int64_t n, int z_lo, int z_hi, int ebytes, bfp_vec_s** out);
 void vec_free(bfp_vec_s* v);
 int set_zero(bfp_vec_s* v, int64_t q, cudaStream_t s);
 

@@ -259,7 +259,8 @@ __device__ __forceinline__ void march_loop(const Op& op, const Vec& out, const W
   const int64_t N = (int64_t)1 << l, GX = N >> 2;
   const int64_t S = DIM == 2 ? N : N * N;  // march stride
   const int64_t rows = DIM == 3 ? N : 1;
-  const int64_t chunks = (N + R - 1) / R;
+  const int64_t NZ = out.nz, Z0 = out.z0;  // local planes along the march axis, slab offset
+  const int64_t chunks = (NZ + R - 1) / R;
   const int64_t items = GX * rows * chunks;
   MarchStep<MODE, DIM, Op> st{op, p, c, S, N, op.shs(), op.shy(), (int)(threadIdx.x & 31),
                               false, (bool)c.store_tmp, INT32_MIN, INT32_MAX, 0, 0};
@@ -275,10 +276,11 @@ __device__ __forceinline__ void march_loop(const Op& op, const Vec& out, const W
     int32_t* wp = (int32_t*)out.data + o0;
     st.xpad = gx == GX - 1;
     // the pad plane / row (index N-1 of the march axis, or row N-1 in 3-D) is written as zeros
-    const int total = (int)std::min<int64_t>(R, N - m0);
+    const int total = (int)std::min<int64_t>(R, NZ - m0);
     const bool rowpad = DIM == 3 && j == N - 1;
-    const int steps = rowpad ? 0 : (m0 + total == N ? total - 1 : total);
-    if (rowpad || m0 + total == N) {
+    const bool padplane = Z0 + m0 + total == N;  // last local plane is the global pad plane
+    const int steps = rowpad ? 0 : (padplane ? total - 1 : total);
+    if (rowpad || padplane) {
       const int first = rowpad ? 0 : total - 1;
       for (int s = first; s < total; ++s)
         *reinterpret_cast<int4*>(wp + (int64_t)s * S) = make_int4(0, 0, 0, 0);
@@ -355,7 +357,8 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
   const int l = out.l;
   const int64_t N = (int64_t)1 << l;
   const int strips = (int)(N / kBulkW);
-  const int chunks = (int)((N + R - 1) / R);
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int chunks = (int)((NZ + R - 1) / R);
   int32_t* xsl = reinterpret_cast<int32_t*>(smem);                 // kBulkXS x (W+8)
   int32_t* ysl = xsl + kBulkXS * kBulkXW;                           // kBulkYS x W
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kBulkYS * kBulkW);
@@ -373,10 +376,10 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
     const int strip = item % strips, ch = item / strips;
     const int64_t c0 = (int64_t)strip * kBulkW;
     const int j0 = ch * R;
-    const int rows = (int)std::min<int64_t>(R, N - j0);
-    // source row clamp: rows past N read the zero back halo (row N)
-    auto xsrc = [&](int64_t row) { return X + (row > N ? N : row) * N + c0 - 4; };
-    auto ysrc = [&](int64_t row) { return Y + (row > N ? N : row) * N + c0; };
+    const int rows = (int)std::min<int64_t>(R, NZ - j0);
+    // source row clamp: rows past the slab read its back halo row (zeros or exchanged)
+    auto xsrc = [&](int64_t row) { return X + (row > NZ ? NZ : row) * N + c0 - 4; };
+    auto ysrc = [&](int64_t row) { return Y + (row > NZ ? NZ : row) * N + c0; };
     if (t == 0) {
       fence_proxy_async_smem();  // previous item's generic reads of the slots
       // prologue: x rows j0-1, j0 with group j0 (x row j0+1, y row j0) on bar[j0 % YS];
@@ -419,7 +422,7 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       const int Yv[4] = {y4.x >> sy, y4.y >> sy, y4.z >> sy, y4.w >> sy};
       const int nb[4] = {(lf >> sx) + C[1], C[0] + C[2], C[1] + C[3], C[2] + (rt >> sx)};
       int32_t tt[4];
-      const bool rowpad = j == N - 1;
+      const bool rowpad = j + Z0 == N - 1;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int g = 4 * C[k] - (nb[k] + U[k] + Dn[k]);
@@ -612,6 +615,26 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
   }
 }
 
+// multi-rank finalize: apply the all-reduced partials {mu*, max, -min, err} with the
+// window context recorded by pass 1 (exactly the single-rank win_finalize)
+__global__ void window_finalize_kernel(Vec out, WinParams p, const int64_t* part, int storage_bits) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  griddep_wait();
+  Hdr* h = out.hdr;
+  if (p.mode == MODE_RECOMPUTE && !h->need_recompute) return;  // fast path: nothing ran
+  WinCtx c;
+  c.e_star = h->st_estar;
+  c.mu_tmp = h->st_mutmp;
+  c.lam = p.mode == MODE_RECOMPUTE ? h->lam_out : h->st_lam;
+  c.gm = h->st_gm;
+  c.ge = h->st_ge;
+  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
+  c.skip = 0;
+  p.part = nullptr;
+  win_finalize(p, c, h, (int)part[0], part[1], part[2] == INT64_MAX ? INT64_MIN : -part[2],
+               (int)part[3]);
+}
+
 // one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
 template <typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
@@ -646,22 +669,42 @@ __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinP
 }
 
 // logical index <-> storage offset
+// local logical index (interior points of the vector / slab, x fastest); for slabs the
+// slowest axis starts at global plane z0
 __device__ __forceinline__ int64_t logical_of(const Vec& v, int64_t o, bool& pad) {
   if (v.dim == 0) {
     pad = o >= v.nlog;
     return o;
   }
   const int64_t N = (int64_t)1 << v.l, m = N - 1, n = N - 1;
-  int64_t ix = o & m, iy = (o >> v.l) & m, iz = (o >> (2 * v.l)) & m;
-  pad = ix == m || (v.dim >= 2 && iy == m) || (v.dim >= 3 && iz == m);
-  return ix + n * (iy + n * iz);
+  const int64_t ix = o & m;
+  if (v.dim == 1) {
+    pad = ix == m;
+    return ix;
+  }
+  if (v.dim == 2) {
+    const int64_t s = o >> v.l;  // local row
+    pad = ix == m || s + v.z0 == m;
+    return ix + n * s;
+  }
+  const int64_t iy = (o >> v.l) & m, s = o >> (2 * v.l);  // local plane
+  pad = ix == m || iy == m || s + v.z0 == m;
+  return ix + n * (iy + n * s);
 }
 __device__ __forceinline__ int64_t storage_of(const Vec& v, int64_t i) {
   if (v.dim == 0) return i;
   const int64_t n = ((int64_t)1 << v.l) - 1;
   int64_t ix = i % n, t = i / n;
-  int64_t iy = v.dim >= 2 ? t % n : 0, iz = v.dim >= 3 ? t / n : 0;
+  int64_t iy = v.dim >= 2 ? (v.dim == 2 ? t : t % n) : 0, iz = v.dim >= 3 ? t / n : 0;
+  if (v.dim == 2) return ix + (iy << v.l);
   return ix + ((iy + (iz << v.l)) << v.l);
+}
+// global logical index (generators: slab data equals the corresponding part of the
+// full vector)
+__device__ __forceinline__ int64_t global_logical(const Vec& v, int64_t local) {
+  if (v.dim < 2) return local;
+  const int64_t n = ((int64_t)1 << v.l) - 1;
+  return local + (int64_t)v.z0 * (v.dim == 2 ? n : n * n);
 }
 
 // host logical array (staged) -> padded storage, header (q, e) with T_q / storage checks
@@ -769,7 +812,7 @@ __global__ void __launch_bounds__(kThreads) uniform_kernel(Vec v, int64_t p, uin
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < v.n; o += stride) {
     bool pad;
-    int64_t i = logical_of(v, o, pad);
+    int64_t i = global_logical(v, logical_of(v, o, pad));
     int64_t m = 0;
     if (!pad) m = (int64_t)(splitmix64(key + (uint64_t)i) >> (64 - p)) - ((int64_t)1 << (p - 1));
     ((M*)v.data)[o] = (M)m;
@@ -797,8 +840,11 @@ __device__ __forceinline__ double sine_val(const Vec& v, const double* tab, doub
   if (pad) return 0.0;
   const int64_t N = (int64_t)1 << v.l, m = N - 1;
   double r = __dmul_rn(C, tab[o & m]);
-  if (v.dim >= 2) r = __dmul_rn(r, tab[(o >> v.l) & m]);
-  if (v.dim >= 3) r = __dmul_rn(r, tab[(o >> (2 * v.l)) & m]);
+  if (v.dim == 2) r = __dmul_rn(r, tab[(o >> v.l) + v.z0]);
+  if (v.dim == 3) {
+    r = __dmul_rn(r, tab[(o >> v.l) & m]);
+    r = __dmul_rn(r, tab[(o >> (2 * v.l)) + v.z0]);
+  }
   return r;
 }
 __device__ __forceinline__ void split_double(double v, int64_t& z, int64_t& k) {
@@ -907,15 +953,25 @@ Vec view(const bfp_vec_s* v) {
   d.ebytes = v->ebytes;
   d.dim = v->dim;
   d.l = v->l;
-  d.pad = 0;
+  d.z0 = v->z0;
   d.n = v->span;
   d.nlog = v->nlog;
+  d.nz = v->nz;
+  d.pad = 0;
   return d;
 }
 
 int vec_alloc(int dim, int level, int64_t n, int ebytes, bfp_vec_s** out) {
+  return vec_alloc_slab(dim, level, n, 0, -1, ebytes, out);
+}
+
+// z_hi < 0: full grid.  Otherwise a slab of planes [z_lo, z_hi) of the padded global grid
+// along the slowest axis (2-D rows, 3-D planes), with the usual halo planes around it.
+int vec_alloc_slab(int dim, int level, int64_t n, int z_lo, int z_hi, int ebytes, bfp_vec_s** out) {
   if (ebytes != 4 && ebytes != 8) return BFP_ERR_ARG;
   if (dim < 0 || dim > 3) return BFP_ERR_ARG;
+  if (z_hi >= 0 && (dim < 2 || z_lo < 0 || z_hi <= z_lo || z_hi > (1 << level)))
+    return BFP_ERR_ARG;
   bfp_vec_s* v = new bfp_vec_s();
   v->dim = dim;
   v->l = level;
@@ -934,13 +990,16 @@ int vec_alloc(int dim, int level, int64_t n, int ebytes, bfp_vec_s** out) {
       return BFP_ERR_ARG;
     }
     const int64_t N = (int64_t)1 << level, nn = N - 1;
-    v->nlog = 1;
-    v->span = 1;
-    for (int a = 0; a < dim; ++a) {
+    v->z0 = z_hi >= 0 ? z_lo : 0;
+    v->nz = z_hi >= 0 ? z_hi - z_lo : (int)N;
+    const int64_t interior = std::min<int64_t>(v->z0 + v->nz, nn) - v->z0;  // planes < N-1
+    v->nlog = interior;
+    v->span = v->nz;
+    for (int a = 1; a < dim; ++a) {
       v->nlog *= nn;
       v->span *= N;
     }
-    v->halo = dim == 1 ? 4 : 2 * (v->span / N);
+    v->halo = dim == 1 ? 4 : 2 * (v->span / v->nz);
   }
   size_t bytes = (size_t)(v->span + 2 * v->halo) * ebytes;
   if (cudaMalloc(&v->base, bytes) != cudaSuccess) {
@@ -1011,6 +1070,7 @@ WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force) {
   p.trace = nullptr;
   p.hist_slot = -1;
   p.hist = nullptr;
+  p.part = nullptr;
   return p;
 }
 GammaRule gamma_literal(int64_t m, int64_t e) {
@@ -1065,7 +1125,7 @@ static int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
   } else {
     go(p);
   }
-  if (p.mode == MODE_QCOMP) {
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
   }
@@ -1089,8 +1149,9 @@ static int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
     occ = std::max(occ, 1);
   }
   const int64_t strips = N / kBulkW, ctas = (int64_t)148 * occ;
-  const int R = (int)std::max<int64_t>(8, (strips * N + ctas - 1) / ctas);
-  const int64_t items = strips * ((N + R - 1) / R);
+  const int64_t NZ = out->nz;
+  const int R = (int)std::max<int64_t>(8, (strips * NZ + ctas - 1) / ctas);
+  const int64_t items = strips * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
@@ -1110,7 +1171,7 @@ static int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
   } else {
     go(p);
   }
-  if (p.mode == MODE_QCOMP && !g_skip_recompute) {
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
   }
@@ -1141,8 +1202,9 @@ static int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaS
   const int occ = out->dim == 2 ? occ2 : occ3;
   // one balanced resident wave: every thread marches R steps (last chunk shorter)
   const int64_t slots = (int64_t)148 * occ * kThreads;
-  int R = (int)std::max<int64_t>(4, (GX * rows * N + slots - 1) / slots);
-  const int64_t items = GX * rows * ((N + R - 1) / R);
+  const int64_t NZ = out->nz;
+  int R = (int)std::max<int64_t>(4, (GX * rows * NZ + slots - 1) / slots);
+  const int64_t items = GX * rows * ((NZ + R - 1) / R);
   const int b = (int)std::max<int64_t>(1, std::min<int64_t>((items + kThreads - 1) / kThreads,
                                                             (int64_t)148 * occ));
   WinParams p = p0;
@@ -1172,7 +1234,7 @@ static int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaS
   } else {
     go(p, b);
   }
-  if (p.mode == MODE_QCOMP) {
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p, b);
   }
@@ -1194,7 +1256,7 @@ static int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
     count_launch();
   };
   go(p);
-  if (p.mode == MODE_QCOMP) {
+  if (p.mode == MODE_QCOMP && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
   }
@@ -1203,8 +1265,9 @@ static int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaSt
 
 static bool same_grid(const bfp_vec_s* a, const bfp_vec_s* b) {
   return a->dim == b->dim && a->l == b->l && a->ebytes == b->ebytes && a->span == b->span &&
-         a->nlog == b->nlog;
+         a->nlog == b->nlog && a->z0 == b->z0 && a->nz == b->nz;
 }
+static bool full_grid(const bfp_vec_s* a) { return a->dim == 0 || a->nz == (1 << a->l); }
 
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
             cudaStream_t s) {
@@ -1217,6 +1280,7 @@ int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bf
   op.be = be;
   op.dim = x->dim;
   op.l = x->l;
+  op.z0 = x->z0;
   return launch_march(op, out, p, s);
 }
 
@@ -1230,6 +1294,7 @@ int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s*
   op.c = c;
   op.dim = x->dim;
   op.l = x->l;
+  op.z0 = x->z0;
   return launch_march(op, out, p, s);
 }
 
@@ -1255,6 +1320,7 @@ int op_axpby(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, b
 }
 
 int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
+  if (!full_grid(r) || !full_grid(out)) return BFP_ERR_ARG;  // transfers: full grids only
   if (r->dim < 1 || out->dim != r->dim || out->l != r->l - 1 || out->ebytes != r->ebytes)
     return BFP_ERR_ARG;
   RestrictOp op;
@@ -1265,6 +1331,7 @@ int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s
 }
 
 int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
+  if (!full_grid(xc) || !full_grid(out)) return BFP_ERR_ARG;
   if (xc->dim < 1 || out->dim != xc->dim || out->l != xc->l + 1 || out->ebytes != xc->ebytes)
     return BFP_ERR_ARG;
   ProlongOp op;
@@ -1276,6 +1343,7 @@ int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s
 
 int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_s* out,
                        cudaStream_t s) {
+  if (!full_grid(ec) || !full_grid(y)) return BFP_ERR_ARG;
   if (ec->dim < 1 || !same_grid(y, out) || y->dim != ec->dim || y->l != ec->l + 1 ||
       y->ebytes != ec->ebytes)
     return BFP_ERR_ARG;
@@ -1366,11 +1434,11 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
   switch (kind) {
     case FK_GEMV:
       f->u.gemv.x = view(a); f->u.gemv.y = view(b); f->u.gemv.al = s1; f->u.gemv.be = s2;
-      f->u.gemv.dim = a->dim; f->u.gemv.l = a->l;
+      f->u.gemv.dim = a->dim; f->u.gemv.l = a->l; f->u.gemv.z0 = a->z0;
       break;
     case FK_JACOBI:
       f->u.jac.x = view(a); f->u.jac.b = view(b); f->u.jac.c = s1;
-      f->u.jac.dim = a->dim; f->u.jac.l = a->l;
+      f->u.jac.dim = a->dim; f->u.jac.l = a->l; f->u.jac.z0 = a->z0;
       break;
     case FK_SCAL: f->u.scal.r = view(a); f->u.scal.c = s1; break;
     case FK_AXPBY:
@@ -1839,6 +1907,59 @@ int bfp_prolong_correct(bfp_vec_t ec, bfp_vec_t y, int mode, int64_t w_out, int6
   if (!ec || !y || !out || gamma.m <= 0) return BFP_ERR_ARG;
   return op_prolong_correct(ec, y, mkp(mode, w_out, w_tmp, gamma, 0), out, S(stream));
 }
+int bfp_vec_create_slab(int dim, int level, int z_lo, int z_hi, int mant_bytes, bfp_vec_t* out) {
+  if (dim < 2) return BFP_ERR_ARG;
+  return vec_alloc_slab(dim, level, 0, z_lo, z_hi, mant_bytes, out);
+}
+
+int bfp_vec_planes(bfp_vec_t v, void** first, void** last, void** halo_lo, void** halo_hi,
+                   int64_t* plane_bytes) {
+  if (!v || v->dim < 2) return BFP_ERR_ARG;
+  const int64_t pe = v->span / v->nz, pb = pe * v->ebytes;
+  char* d = (char*)v->data;
+  if (first) *first = d;
+  if (last) *last = d + (v->nz - 1) * pb;
+  if (halo_lo) *halo_lo = d - pb;
+  if (halo_hi) *halo_hi = d + v->nz * pb;
+  if (plane_bytes) *plane_bytes = pb;
+  return BFP_OK;
+}
+
+static WinParams mkp_part(int mode, int stage, int64_t w_out, int64_t w_tmp, bfp_scalar_t g,
+                          int64_t* d_part) {
+  WinParams p = mkp(mode, w_out, w_tmp, g, 0);
+  if (stage == 1) p.mode = MODE_RECOMPUTE;
+  p.part = d_part;
+  return p;
+}
+
+int bfp_stencil_gemv_part(bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta,
+                          int mode, int stage, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                          bfp_vec_t out, int64_t* d_part, void* stream) {
+  if (!x || !y || !out || !d_part || gamma.m <= 0 || stage < 0 || stage > 1) return BFP_ERR_ARG;
+  return op_gemv(x, y, SC(alpha), SC(beta), mkp_part(mode, stage, w_out, w_tmp, gamma, d_part),
+                 out, S(stream));
+}
+
+int bfp_stencil_jacobi_part(bfp_vec_t x, bfp_vec_t b, bfp_scalar_t c, int mode, int stage,
+                            int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma, bfp_vec_t out,
+                            int64_t* d_part, void* stream) {
+  if (!x || !b || !out || !d_part || gamma.m <= 0 || stage < 0 || stage > 1) return BFP_ERR_ARG;
+  return op_jacobi(x, b, SC(c), mkp_part(mode, stage, w_out, w_tmp, gamma, d_part), out,
+                   S(stream));
+}
+
+int bfp_window_finalize(bfp_vec_t out, int mode, int stage, int64_t w_out, int64_t w_tmp,
+                        const int64_t* d_part, void* stream) {
+  if (!out || !d_part || stage < 0 || stage > 1) return BFP_ERR_ARG;
+  WinParams p = win_params(stage == 1 ? MODE_RECOMPUTE : (mode == 1 ? MODE_NNQ : MODE_QCOMP),
+                           w_out, w_tmp, 0);
+  launch_pdl(window_finalize_kernel, 1, 32, 0, S(stream), view(out), p, d_part,
+             out->ebytes * 8);
+  count_launch();
+  return last_launch();
+}
+
 int bfp_jacobi_coeff(int dim, int level, int64_t qc, bfp_scalar_t* c) {
   if (dim < 1 || dim > 3 || qc < 2 || qc > 60 || !c) return BFP_ERR_ARG;
   int64_t cm, ce;

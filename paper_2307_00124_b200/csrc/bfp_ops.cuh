@@ -111,12 +111,17 @@ __device__ __forceinline__ int64_t ld1(const Vec& v, int64_t o, int64_t sh) {
   return ((int64_t)ldx<NC>((const M*)v.data + o)) >> sh;
 }
 
-// pad mask of 4 consecutive grid storage offsets starting at o (o % 4 == 0)
-__device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4]) {
+// pad mask of 4 consecutive grid storage offsets starting at o (o % 4 == 0); z0 is the
+// global index of local plane 0 along the slowest axis (slabs), 0 for full grids
+__device__ __forceinline__ bool plane_pad(int dim, int l, int z0, int64_t o) {
+  const int64_t mask = ((int64_t)1 << l) - 1;
+  if (dim == 2) return (o >> l) + z0 == mask;
+  if (dim == 3) return ((o >> l) & mask) == mask || (o >> (2 * l)) + z0 == mask;
+  return false;
+}
+__device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4], int z0 = 0) {
   const int64_t N = (int64_t)1 << l, mask = N - 1;
-  bool rowpad = false;
-  if (dim >= 2) rowpad |= ((o >> l) & mask) == mask;
-  if (dim >= 3) rowpad |= ((o >> (2 * l)) & mask) == mask;
+  const bool rowpad = plane_pad(dim, l, z0, o);
   const int64_t ix = o & mask;
 #pragma unroll
   for (int j = 0; j < 4; ++j) pad[j] = rowpad || (ix + j == mask);
@@ -202,7 +207,7 @@ __device__ __forceinline__ void stencil4(const Vec& x, int64_t sx, int dim, int 
 struct GemvOp {
   Vec x, y;
   Scal al, be;
-  int dim, l;
+  int dim, l, z0;  // z0: slab offset along the slowest axis (0 for full grids)
   // derived (uniform per launch)
   int64_t sx, sy, d;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
@@ -252,9 +257,7 @@ struct GemvOp {
         V4<int32_t, NC>::load32(y, o, (int)sy, yv);
         const uint32_t mN = (1u << l) - 1;
         const uint32_t ix = (uint32_t)o & mN;
-        bool rowpad = false;
-        if (dim >= 2) rowpad = ((uint32_t)(o >> l) & mN) == mN;
-        if (dim >= 3) rowpad |= ((uint32_t)(o >> (2 * l)) & mN) == mN;
+        const bool rowpad = plane_pad(dim, l, z0, o);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int X = swap ? yv[j] : g[j], Y = swap ? g[j] : yv[j];
@@ -270,7 +273,7 @@ struct GemvOp {
     stencil4<M, A, NC>(x, sx, dim, l, o, g, c);
     V4<M, NC>::load(y, o, sy, yv);
     bool pad[4];
-    pad4(dim, l, o, pad);
+    pad4(dim, l, o, pad, z0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : combine<A>(al.m, g[j], be.m, (A)yv[j], d);
   }
@@ -280,7 +283,7 @@ struct GemvOp {
 struct JacobiOp {
   Vec x, b;
   Scal c;
-  int dim, l;
+  int dim, l, z0;
   int64_t sx, sb, d1, d2;
   bool narrow;
   int P1, s2;
@@ -324,9 +327,7 @@ struct JacobiOp {
         V4<int32_t, NC>::load32(b, o, (int)sb, bv);
         const uint32_t mN = (1u << l) - 1;
         const uint32_t ix = (uint32_t)o & mN;
-        bool rowpad = false;
-        if (dim >= 2) rowpad = ((uint32_t)(o >> l) & mN) == mN;
-        if (dim >= 3) rowpad |= ((uint32_t)(o >> (2 * l)) & mN) == mN;
+        const bool rowpad = plane_pad(dim, l, z0, o);
         const uint64_t cm = (uint64_t)c.m;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -344,7 +345,7 @@ struct JacobiOp {
     stencil4<M, A, NC>(x, sx, dim, l, o, g, cx);
     V4<M, NC>::load(b, o, sb, bv);
     bool pad[4];
-    pad4(dim, l, o, pad);
+    pad4(dim, l, o, pad, z0);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       A r = combine<A>(-1, g[j], 1, (A)bv[j], d1);
