@@ -178,6 +178,9 @@ typedef struct {
   int pd[32];
   int pc[32];
   int w_add_cap;
+  /* levels whose padded grid has <= fuse_points points run as one fused CTA with their
+     vectors staged in shared memory; 0 = off, -1 = library default */
+  int fuse_points;
 } bfp_mg_config_t;
 
 typedef struct {

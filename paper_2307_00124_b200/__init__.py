@@ -73,7 +73,7 @@ class MgConfig(C.Structure):
                 ("nu2", C.c_int), ("n_coarse", C.c_int), ("cycles", C.c_int), ("fmg", C.c_int),
                 ("nonnormalized", C.c_int), ("x0_random", C.c_int), ("rhs_kind", C.c_int),
                 ("qc", C.c_int), ("seed", C.c_uint64), ("p", C.c_int * 32), ("pd", C.c_int * 32),
-                ("pc", C.c_int * 32), ("w_add_cap", C.c_int)]
+                ("pc", C.c_int * 32), ("w_add_cap", C.c_int), ("fuse_points", C.c_int)]
 
 
 class TraceRec(C.Structure):
@@ -577,7 +577,7 @@ def _lv(v):
 
 def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=False,
               nonnormalized=False, x0_random=False, rhs_kind=1, qc=16, seed=1, p=None, pd=None,
-              pc=None, w_add_cap=-1) -> MgConfig:
+              pc=None, w_add_cap=-1, fuse_points=-1) -> MgConfig:
     """Solver config; p / pd / pc are the PrecisionSchedule w / wdot / wcheck per level."""
     cfg = MgConfig()
     cfg.d, cfg.l_fine, cfg.l_coarse, cfg.nu1, cfg.nu2 = d, l_fine, l_coarse, nu1, nu2
@@ -587,6 +587,7 @@ def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=Fa
     for i in range(32):
         cfg.p[i], cfg.pd[i], cfg.pc[i] = p[i], pd[i], pc[i]
     cfg.w_add_cap = w_add_cap
+    cfg.fuse_points = fuse_points
     return cfg
 
 

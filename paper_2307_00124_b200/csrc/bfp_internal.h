@@ -32,6 +32,14 @@ namespace bfpdev {
 // fused coarse-level op list entry (bfp_lib.cu: fused_kernel)
 enum { FK_GEMV = 0, FK_JACOBI, FK_SCAL, FK_AXPBY, FK_RESTRICT, FK_PROLONG, FK_PCORR, FK_ZERO };
 constexpr int kFusedThreads = 512;
+constexpr int kArenaMaxBytes = 200 * 1024;  // dynamic shared memory of the fused kernel
+// one vector of an arena-resident fused op list: data (halos included) and header
+struct ArenaEntry {
+  char* gbase;
+  Hdr* ghdr;
+  int64_t bytes;
+  int32_t off, hoff;  // byte offsets in the CTA's shared memory
+};
 struct FusedOp {
   int32_t kind, pad;
   int64_t q;
@@ -51,6 +59,7 @@ struct FusedOp {
 
 namespace bfp {
 
+using bfpdev::ArenaEntry;
 using bfpdev::FusedOp;
 using bfpdev::GammaRule;
 using bfpdev::Scal;
@@ -84,7 +93,8 @@ int gen_sine(bfp_vec_s* v, int64_t p, cudaStream_t s);
 void jacobi_coeff(int dim, int level, int64_t qc, int64_t* cm, int64_t* ce);
 int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const WinParams& p,
                int64_t q, bfp_vec_s* out, FusedOp* f);
-int fused_launch(const FusedOp* d_ops, int n, int ebytes, cudaStream_t s);
+int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, int arena_bytes,
+                 int ebytes, cudaStream_t s);
 void count_launch(int n = 1);
 int64_t launches();
 

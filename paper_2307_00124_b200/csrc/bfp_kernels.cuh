@@ -1,0 +1,883 @@
+// bfp_kernels.cuh -- kernel templates (windowed passes over grids: generic grid
+// kernel, register march, bulk-async smem pipeline, fused CTA, flat rows) and their
+// host launchers.  Included by the op translation units (op_*.cu) and bfp_lib.cu so
+// the instantiations compile in parallel.
+#pragma once
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <utility>
+#include <vector>
+
+#include "bfp_bulk.cuh"
+#include "bfp_internal.h"
+
+namespace bfp {
+// process-wide switches and measurement hooks (defined in bfp_lib.cu)
+extern bool g_pdl;             // programmatic dependent launch for the windowed kernels
+extern bool g_skip_recompute;  // measurement only: pass 1 alone (flags must be clear)
+extern bool g_prof;            // CUDA-event brackets around pass-1 launches
+extern bool g_use_bulk;        // 2-D stencils through the bulk-async pipeline
+std::pair<cudaEvent_t, cudaEvent_t> prof_pair();
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 148 * 8;
+
+// Launch with Programmatic Dependent Launch: the grid may be scheduled while the
+// previous kernel in the stream drains; the kernel executes griddepcontrol.wait
+// before touching any data, so stream semantics are unchanged.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+inline int blocks_for(int64_t work) {
+  int64_t b = (work + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, kMaxBlocks));
+}
+inline int last_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "bfpmg_b200: launch failed: %s\n", cudaGetErrorString(e));
+    return BFP_ERR_CUDA;
+  }
+  return BFP_OK;
+}
+}  // namespace bfp
+
+using namespace bfpdev;
+using bfp::kThreads;
+using bfp::launch_pdl;
+
+
+template <typename M> struct Lim;
+template <> struct Lim<int32_t> {
+  static constexpr int32_t lo = INT32_MIN, hi = INT32_MAX;
+};
+template <> struct Lim<int64_t> {
+  static constexpr int64_t lo = INT64_MIN, hi = INT64_MAX;
+};
+
+// The window pass over 4-groups of the output storage.  MODE is a template
+// parameter so each instantiation carries only its own epilogue:
+//   QCOMP      OR-accumulate |z| bits (mu*), store floor(z/2^lam_tmp)
+//   RECOMPUTE  store floor(z/2^lam_out)
+//   NNQ        store clamp(floor(z/2^lam_out))
+// Max/min of the STORED values are tracked in the storage type.
+template <int MODE, typename M, typename Op, typename A, bool NC = true>
+__device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r) {
+  const int64_t ngroups = out.n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  M mx = Lim<M>::lo, mn = Lim<M>::hi;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+    A z[4];
+    op.template eval4<M, A, NC>(g * 4, z);
+    M t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (MODE == MODE_NNQ) {
+        t[j] = (M)shift_clamp<A>(z[j], c.lam, p.w_out);
+      } else {
+        if (MODE == MODE_QCOMP) or_mag<A>(z[j], olo, ohi);
+        t[j] = store ? store_shift<M, A>(z[j], c) : (M)0;
+      }
+      mx = t[j] > mx ? t[j] : mx;
+      mn = t[j] < mn ? t[j] : mn;
+    }
+    V4<M>::store(out, g * 4, t);
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;  // sentinels stay neutral
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE, typename M, typename Op, bool NC = true>
+__device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r, int64_t need) {
+  if (need > 127)
+    r.err = ERR_WIDTH;
+  else if (need <= 63)
+    grid_loop<MODE, M, Op, int64_t, NC>(op, out, p, c, r);
+  else
+    grid_loop<MODE, M, Op, i128, NC>(op, out, p, c, r);
+}
+
+// One windowed pass over a grid (or 4-padded flat) output: qcomp pass 1,
+// nnqcomp, or the qcomp recompute pass, selected by p.mode.
+// The op setup and the gamma rule are uniform per launch: one thread evaluates
+// them from the device headers and broadcasts through shared memory.
+template <typename Op, typename M>
+__device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinParams& p, WinCtx& c,
+                                            int64_t& need) {
+  __shared__ Op s_op;
+  __shared__ WinCtx s_c;
+  __shared__ int64_t s_need;
+  if (p.mode == MODE_RECOMPUTE) {  // fast path: nothing to do, skip the op setup
+    __shared__ int s_rc;
+    if (threadIdx.x == 0) s_rc = ((volatile Hdr*)out.hdr)->need_recompute;
+    __syncthreads();
+    if (!s_rc) {
+      c.skip = 1;
+      return;
+    }
+  }
+  if (threadIdx.x == 0) {
+    int64_t e_star = 0, nd = 0;
+    Op o = op;
+    o.setup(e_star, nd);
+    WinCtx cc;
+    win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
+    s_op = o;
+    s_c = cc;
+    s_need = nd;
+  }
+  __syncthreads();
+  op = s_op;
+  c = s_c;
+  need = s_need;
+}
+
+template <int MODE, typename M, typename Op>
+__global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinParams p) {
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, M>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  grid_body<MODE, M>(op, out, p, c, r, need);
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+
+// ---------------------------------------------------------------------------
+// 2.5-D register march for the 2-D / 3-D stencil ops on int32 storage (the
+// hot path).  A work item is a 4-wide x strip marching R steps along the
+// slowest axis (y in 2-D, z in 3-D): the x values at the previous / current /
+// next step stay in registers, x-neighbours come from warp shuffles, and the
+// loads of step s+1 are issued before step s is computed.  Each thread writes
+// one aligned int4 per step.
+constexpr int kMarchMinN = 128;  // GX = N/4 >= 32: a warp spans one row
+
+__device__ __forceinline__ void ld4s(const int32_t* p, int64_t o, int sh, int v[4]) {
+  // 128-bit read-only load of 4 mantissas, pending shift applied
+  int4 t = __ldg(reinterpret_cast<const int4*>(p + o));
+  v[0] = t.x >> sh;
+  v[1] = t.y >> sh;
+  v[2] = t.z >> sh;
+  v[3] = t.w >> sh;
+}
+
+// one march step: output row at wp from (P, C, Nx) along the march axis and the
+// x neighbours through the warp; prefetches the next step into (NN, Yn, ...).
+template <int MODE, int DIM, bool SW, typename Op>
+struct MarchStep {
+  const Op& op;
+  const WinParams& p;
+  const WinCtx& c;
+  int64_t S, N;
+  int sx, sy, lane;
+  bool xpad, store;
+  int32_t mx, mn;
+  uint64_t olo, ohi;
+
+  __device__ __forceinline__ void prefetch(const int32_t* xp, const int32_t* yp, int NN[4],
+                                           int Yn[4], int SUn[4], int SDn[4], int& lfn,
+                                           int& rtn) const {
+    ld4s(xp, 2 * S, sx, NN);
+    ld4s(yp, S, sy, Yn);
+    if (DIM == 3) {
+      ld4s(xp, S - N, sx, SUn);
+      ld4s(xp, S + N, sx, SDn);
+    }
+    if (lane == 0) lfn = __ldg(xp + S - 1) >> sx;
+    if (lane == 31) rtn = __ldg(xp + S + 4) >> sx;
+  }
+
+  __device__ __forceinline__ void compute(int32_t* wp, const int P[4], const int C[4],
+                                          const int Nx[4], const int Y[4], const int SU[4],
+                                          const int SD[4], int lf, int rt) {
+    int left = __shfl_up_sync(0xffffffffu, C[3], 1);
+    int right = __shfl_down_sync(0xffffffffu, C[0], 1);
+    if (lane == 0) left = lf;
+    if (lane == 31) right = rt;
+    const int nb[4] = {left + C[1], C[0] + C[2], C[1] + C[3], C[2] + right};
+    int32_t tt[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int n = nb[k] + P[k] + Nx[k];
+      if (DIM == 3) n += SU[k] + SD[k];
+      const int g = 2 * DIM * C[k] - n;
+      int64_t z = op.template point_t<SW>(g, C[k], Y[k]);
+      if (k == 3 && xpad) z = 0;
+      if (MODE == MODE_NNQ) {
+        tt[k] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+      } else {
+        if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+        tt[k] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+      }
+      mx = tt[k] > mx ? tt[k] : mx;
+      mn = tt[k] < mn ? tt[k] : mn;
+    }
+    *reinterpret_cast<int4*>(wp) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+  }
+};
+
+template <int MODE, int DIM, bool SW, typename Op>
+__device__ __forceinline__ void march_loop(const Op& op, const Vec& out, const WinParams& p,
+                                           const WinCtx& c, Red& r, int R) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l, GX = N >> 2;
+  const int64_t S = DIM == 2 ? N : N * N;  // march stride
+  const int64_t rows = DIM == 3 ? N : 1;
+  const int64_t NZ = out.nz, Z0 = out.z0;  // local planes along the march axis, slab offset
+  const int64_t chunks = (NZ + R - 1) / R;
+  const int64_t items = GX * rows * chunks;
+  MarchStep<MODE, DIM, SW, Op> st{op, p, c, S, N, op.shs(), op.shy(), (int)(threadIdx.x & 31),
+                              false, (bool)c.store_tmp, INT32_MIN, INT32_MAX, 0, 0};
+  const int sx = st.sx, sy = st.sy;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < items; w += stride) {
+    const int64_t gx = w % GX, t = w / GX;
+    const int64_t j = DIM == 3 ? t % N : 0, ch = DIM == 3 ? t / N : t;
+    const int m0 = (int)(ch * R);
+    const int64_t o0 = gx * 4 + (DIM == 3 ? j * N : 0) + (int64_t)m0 * S;
+    const int32_t* xp = (const int32_t*)op.sv().data + o0;
+    const int32_t* yp = (const int32_t*)op.yv2().data + o0;
+    int32_t* wp = (int32_t*)out.data + o0;
+    st.xpad = gx == GX - 1;
+    // the pad plane / row (index N-1 of the march axis, or row N-1 in 3-D) is written as zeros
+    const int total = (int)std::min<int64_t>(R, NZ - m0);
+    const bool rowpad = DIM == 3 && j == N - 1;
+    const bool padplane = Z0 + m0 + total == N;  // last local plane is the global pad plane
+    const int steps = rowpad ? 0 : (padplane ? total - 1 : total);
+    if (rowpad || padplane) {
+      const int first = rowpad ? 0 : total - 1;
+      for (int s = first; s < total; ++s)
+        *reinterpret_cast<int4*>(wp + (int64_t)s * S) = make_int4(0, 0, 0, 0);
+      st.mx = 0 > st.mx ? 0 : st.mx;
+      st.mn = 0 < st.mn ? 0 : st.mn;
+    }
+    if (steps == 0) continue;
+    int X0[4], X1[4], X2[4], X3[4], Y0[4], Y1[4];
+    int U0[4], U1[4], D0[4], D1[4];
+    int l0 = 0, r0 = 0, l1 = 0, r1 = 0;
+    ld4s(xp, -S, sx, X0);
+    ld4s(xp, 0, sx, X1);
+    ld4s(xp, S, sx, X2);
+    ld4s(yp, 0, sy, Y0);
+    if (DIM == 3) {
+      ld4s(xp, -N, sx, U0);
+      ld4s(xp, N, sx, D0);
+    }
+    if (st.lane == 0) l0 = __ldg(xp - 1) >> sx;
+    if (st.lane == 31) r0 = __ldg(xp + 4) >> sx;
+    // x buffers rotate with period 4, y / side buffers with period 2: unroll by 4
+    int s = 0;
+    for (;;) {
+      if (s + 1 < steps) st.prefetch(xp, yp, X3, Y1, U1, D1, l1, r1);
+      st.compute(wp, X0, X1, X2, Y0, U0, D0, l0, r0);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X0, Y0, U0, D0, l0, r0);
+      st.compute(wp, X1, X2, X3, Y1, U1, D1, l1, r1);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X1, Y1, U1, D1, l1, r1);
+      st.compute(wp, X2, X3, X0, Y0, U0, D0, l0, r0);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+      if (s + 1 < steps) st.prefetch(xp, yp, X2, Y0, U0, D0, l0, r0);
+      st.compute(wp, X3, X0, X1, Y1, U1, D1, l1, r1);
+      if (++s >= steps) break;
+      xp += S; yp += S; wp += S;
+    }
+  }
+  r.olo |= st.olo;
+  r.ohi |= st.ohi;
+  r.mx = (int64_t)st.mx > r.mx ? (int64_t)st.mx : r.mx;
+  r.mn = (int64_t)st.mn < r.mn ? (int64_t)st.mn : r.mn;
+}
+
+template <int MODE, int DIM, typename Op>
+__global__ void __launch_bounds__(kThreads, DIM == 2 ? 3 : 2) march_win_kernel(Op op, Vec out, WinParams p,
+                                                                int R) {
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63) {
+    if (op.swapped())
+      march_loop<MODE, DIM, true>(op, out, p, c, r, R);
+    else
+      march_loop<MODE, DIM, false>(op, out, p, c, r, R);
+  } else
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// 2-D stencil ops through the bulk-async shared-memory pipeline (bfp_bulk.cuh)
+
+template <int MODE, bool SHIFT, bool SWAP, typename Op>
+__device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r, int R, char* smem) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l;
+  const int strips = (int)(N / kBulkW);
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* xsl = reinterpret_cast<int32_t*>(smem);                 // kBulkXS x (W+8)
+  int32_t* ysl = xsl + kBulkXS * kBulkXW;                           // kBulkYS x W
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kBulkYS * kBulkW);
+  const int32_t* X = (const int32_t*)op.sv().data;
+  const int32_t* Y = (const int32_t*)op.yv2().data;
+  int32_t* O = (int32_t*)out.data;
+  const int sx = SHIFT ? op.shs() : 0, sy = SHIFT ? op.shy() : 0;
+  const int t = threadIdx.x;
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  const uint32_t tx_bytes = (uint32_t)(kBulkXW + kBulkW) * 4;
+  uint32_t parity = 0;  // bit k: phase parity of bar[k]
+  for (int item = blockIdx.x; item < strips * chunks; item += gridDim.x) {
+    const int strip = item % strips, ch = item / strips;
+    const int64_t c0 = (int64_t)strip * kBulkW;
+    const int j0 = ch * R;
+    const int rows = (int)std::min<int64_t>(R, NZ - j0);
+    // source row clamp: rows past the slab read its back halo row (zeros or exchanged)
+    auto xsrc = [&](int64_t row) { return X + (row > NZ ? NZ : row) * N + c0 - 4; };
+    auto ysrc = [&](int64_t row) { return Y + (row > NZ ? NZ : row) * N + c0; };
+    if (t == 0) {
+      fence_proxy_async_smem();  // previous item's generic reads of the slots
+      // prologue: x rows j0-1, j0 with group j0 (x row j0+1, y row j0) on bar[j0 % YS];
+      // then groups j0+1 .. j0+D
+      for (int g = 0; g <= kBulkD && g < rows; ++g) {
+        const int64_t tr = j0 + g;
+        uint64_t* b = &bar[tr % kBulkYS];
+        const uint32_t extra = g == 0 ? 2u * kBulkXW * 4 : 0u;
+        mbar_expect_tx(b, tx_bytes + extra);
+        if (g == 0) {
+          bulk_g2s(xsl + ((tr - 1 + kBulkXS) % kBulkXS) * kBulkXW, xsrc(tr - 1), kBulkXW * 4, b);
+          bulk_g2s(xsl + (tr % kBulkXS) * kBulkXW, xsrc(tr), kBulkXW * 4, b);
+        }
+        bulk_g2s(xsl + ((tr + 1) % kBulkXS) * kBulkXW, xsrc(tr + 1), kBulkXW * 4, b);
+        bulk_g2s(ysl + (tr % kBulkYS) * kBulkW, ysrc(tr), kBulkW * 4, b);
+      }
+    }
+    const bool xpad = c0 + 4 * t + 3 == N - 1;
+    const int lane = t & 31;
+    // running ring indices (no 64-bit modulo in the step loop)
+    int sp = (int)((j0 - 1 + kBulkXS) % kBulkXS), sc = (int)(j0 % kBulkXS);
+    int sn = (int)((j0 + 1) % kBulkXS), sy_ = (int)(j0 % kBulkYS);
+    for (int s = 0; s < rows; ++s) {
+      const int64_t j = j0 + s;
+      mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
+      parity ^= 1u << sy_;
+      const int32_t* xc = xsl + sc * kBulkXW + 4 + 4 * t;
+      int4 a = *reinterpret_cast<const int4*>(xsl + sp * kBulkXW + 4 + 4 * t);
+      int4 b = *reinterpret_cast<const int4*>(xc);
+      int4 d = *reinterpret_cast<const int4*>(xsl + sn * kBulkXW + 4 + 4 * t);
+      int4 y4 = *reinterpret_cast<const int4*>(ysl + sy_ * kBulkW + 4 * t);
+      // edge lanes read their outer neighbour from the halo words (branch-free)
+      const int lf0 = xc[-1], rt0 = xc[4];
+      int lf = __shfl_up_sync(0xffffffffu, b.w, 1), rt = __shfl_down_sync(0xffffffffu, b.x, 1);
+      lf = lane == 0 ? lf0 : lf;
+      rt = lane == 31 ? rt0 : rt;
+      const int C[4] = {b.x >> sx, b.y >> sx, b.z >> sx, b.w >> sx};
+      const int U[4] = {a.x >> sx, a.y >> sx, a.z >> sx, a.w >> sx};
+      const int Dn[4] = {d.x >> sx, d.y >> sx, d.z >> sx, d.w >> sx};
+      const int Yv[4] = {y4.x >> sy, y4.y >> sy, y4.z >> sy, y4.w >> sy};
+      const int nb[4] = {(lf >> sx) + C[1], C[0] + C[2], C[1] + C[3], C[2] + (rt >> sx)};
+      int32_t tt[4];
+      const bool rowpad = j + Z0 == N - 1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int g = 4 * C[k] - (nb[k] + U[k] + Dn[k]);
+        int64_t z = op.template point_t<SWAP>(g, C[k], Yv[k]);
+        if (k == 3 && xpad) z = 0;
+        if (rowpad) z = 0;
+        if (MODE == MODE_NNQ) {
+          tt[k] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+        } else {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[k] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+        }
+        mx = tt[k] > mx ? tt[k] : mx;
+        mn = tt[k] < mn ? tt[k] : mn;
+      }
+      *reinterpret_cast<int4*>(O + j * N + c0 + 4 * t) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+      // ring slots freed by this step: x row j-1 (slot sp) and y row j / its barrier (slot sy_)
+      const int free_x = sp, free_y = sy_;
+      sp = sc;
+      sc = sn;
+      sn = sn + 1 == kBulkXS ? 0 : sn + 1;
+      sy_ = sy_ + 1 == kBulkYS ? 0 : sy_ + 1;
+      __syncthreads();  // slots of x row j-1 and y row j are free
+      if (t == 0 && s + kBulkD + 1 < rows) {
+        // next group: x row tr+1 -> slot (j-1) % XS, y row tr -> slot j % YS, tr = j+D+1
+        const int64_t tr = j + kBulkD + 1;
+        uint64_t* bb = &bar[free_y];
+        fence_proxy_async_smem();
+        mbar_expect_tx(bb, tx_bytes);
+        bulk_g2s(xsl + free_x * kBulkXW, xsrc(tr + 1), kBulkXW * 4, bb);
+        bulk_g2s(ysl + free_y * kBulkW, ysrc(tr), kBulkW * 4, bb);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE, typename Op>
+__global__ void __launch_bounds__(kBulkT, 4) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
+  griddep_wait();
+  extern __shared__ __align__(128) char smem[];
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kBulkYS; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    const bool sh = (op.shs() | op.shy()) != 0, sw = op.swapped();
+    if (!sh && !sw)
+      bulk_loop<MODE, false, false>(op, out, p, c, r, R, smem);
+    else if (sh && !sw)
+      bulk_loop<MODE, true, false>(op, out, p, c, r, R, smem);
+    else if (!sh)
+      bulk_loop<MODE, false, true>(op, out, p, c, r, R, smem);
+    else
+      bulk_loop<MODE, true, true>(op, out, p, c, r, R, smem);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Fused coarse levels: one CTA interprets a list of windowed ops (the part of a
+// V-cycle / FMG on levels below the fusion threshold) with block-level
+// reductions and finalizers instead of one or two kernel launches per op.  The
+// per-op semantics are the same functions as the multi-block kernels
+// (setup, win_setup, eval4, win_finalize), so results are bit-identical.
+
+template <typename Fin>
+__device__ inline void block_reduce_finalize(Red& r, Fin fin) {
+  __shared__ unsigned long long s_lo[32], s_hi[32];
+  __shared__ int s_err[32];
+  __shared__ long long s_mx[32], s_mn[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  uint64_t lo = shfl_or64(r.olo), hi = shfl_or64(r.ohi);
+  int err = __reduce_or_sync(0xffffffffu, r.err);
+  int64_t mx = shfl_max64(r.mx), mn = shfl_min64(r.mn);
+  if (lane == 0) {
+    s_lo[wid] = lo;
+    s_hi[wid] = hi;
+    s_err[wid] = err;
+    s_mx[wid] = mx;
+    s_mn[wid] = mn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      lo |= s_lo[w];
+      hi |= s_hi[w];
+      err |= s_err[w];
+      mx = s_mx[w] > mx ? s_mx[w] : mx;
+      mn = s_mn[w] < mn ? s_mn[w] : mn;
+    }
+    const int bits = (hi ? 64 + bitlen64(hi) : bitlen64(lo)) + 1;
+    fin(bits, mx, mn, err);
+  }
+  __syncthreads();
+}
+
+template <int MODE, typename M, typename Op>
+__device__ __forceinline__ void fused_pass(Op& op, const Vec& out, const WinParams& p,
+                                           const WinCtx& c, int64_t need) {
+  Red r;
+  r.init();
+  grid_body<MODE, M, Op, false>(op, out, p, c, r, need);
+  block_reduce_finalize(r, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+// arena rebasing: vector pointers of an arena-resident op list are byte offsets into the
+// CTA's dynamic shared memory (offset 0 is never used)
+__device__ __forceinline__ void rebase(Vec& v, char* b) {
+  v.data = b + (size_t)v.data;
+  v.hdr = reinterpret_cast<Hdr*>(b + (size_t)v.hdr);
+}
+__device__ __forceinline__ void rebase_gamma(GammaRule& g, char* b) {
+  if (g.literal) return;
+  for (int i = 0; i < g.nterms; ++i)
+    if (g.t[i].v) g.t[i].v = reinterpret_cast<const Hdr*>(b + (size_t)g.t[i].v);
+}
+__device__ __forceinline__ void rebase_op(GemvOp& o, char* b) { rebase(o.x, b); rebase(o.y, b); }
+__device__ __forceinline__ void rebase_op(JacobiOp& o, char* b) { rebase(o.x, b); rebase(o.b, b); }
+__device__ __forceinline__ void rebase_op(ScalOp& o, char* b) { rebase(o.r, b); }
+__device__ __forceinline__ void rebase_op(AxpbyOp& o, char* b) { rebase(o.x, b); rebase(o.y, b); }
+__device__ __forceinline__ void rebase_op(RestrictOp& o, char* b) { rebase(o.r, b); }
+__device__ __forceinline__ void rebase_op(ProlongOp& o, char* b) { rebase(o.xc, b); }
+__device__ __forceinline__ void rebase_op(ProlongCorrectOp& o, char* b) {
+  rebase(o.ec, b);
+  rebase(o.y, b);
+}
+
+template <typename M, typename Op>
+__device__ __noinline__ void fused_run(Op op, Vec out, WinParams p, char* ab) {
+  __shared__ WinCtx s_c;
+  __shared__ int64_t s_need;
+  __shared__ alignas(16) char s_op[sizeof(Op)];
+  if (ab) {
+    rebase_op(op, ab);
+    rebase(out, ab);
+    rebase_gamma(p.gamma, ab);
+  }
+  if (threadIdx.x == 0) {
+    int64_t e_star = 0, nd = 0;
+    Op o = op;
+    o.setup(e_star, nd);
+    WinCtx cc;
+    win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
+    *reinterpret_cast<Op*>(s_op) = o;
+    s_c = cc;
+    s_need = nd;
+  }
+  __syncthreads();
+  op = *reinterpret_cast<const Op*>(s_op);
+  WinCtx c = s_c;
+  const int64_t need = s_need;
+  if (p.mode == MODE_NNQ) {
+    fused_pass<MODE_NNQ, M>(op, out, p, c, need);
+    return;
+  }
+  fused_pass<MODE_QCOMP, M>(op, out, p, c, need);
+  // header finalized by thread 0 and published by the barrier in block_reduce_finalize
+  WinParams p2 = p;
+  p2.mode = MODE_RECOMPUTE;
+  WinCtx c2;
+  win_setup(p2, out.hdr, 0, 8 * (int)sizeof(M), c2);
+  if (!c2.skip) fused_pass<MODE_RECOMPUTE, M>(op, out, p2, c2, need);
+}
+
+template <typename M>
+__device__ __noinline__ void fused_zero(Vec v, int64_t q, char* ab) {
+  if (ab) rebase(v, ab);
+  for (int64_t o = threadIdx.x; o < v.n; o += blockDim.x) ((M*)v.data)[o] = 0;
+  if (threadIdx.x == 0) {
+    Hdr* h = v.hdr;
+    h->q = q;
+    h->e = 0;
+    h->shift = 0;
+    h->max_m = 0;
+    h->min_m = 0;
+    h->flags = 0;
+    h->need_recompute = 0;
+  }
+  __syncthreads();
+}
+
+// copy between global and the arena (16-byte granules; sizes are multiples of 16)
+__device__ __forceinline__ void arena_copy(char* dst, const char* src, int64_t bytes) {
+  const int64_t n16 = bytes >> 4;
+  for (int64_t i = threadIdx.x; i < n16; i += blockDim.x)
+    reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+}
+
+template <typename M>
+__global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops, int n,
+                                                              const ArenaEntry* ar, int nar) {
+  extern __shared__ __align__(128) char arena[];
+  griddep_wait();
+  char* ab = nar > 0 ? arena : nullptr;
+  for (int k = 0; k < nar; ++k) {  // vectors + headers of the fused levels -> shared memory
+    arena_copy(arena + ar[k].off, ar[k].gbase, ar[k].bytes);
+    arena_copy(arena + ar[k].hoff, reinterpret_cast<const char*>(ar[k].ghdr), sizeof(Hdr));
+  }
+  __syncthreads();
+  for (int i = 0; i < n; ++i) {
+    const int kind = ops[i].kind;
+    switch (kind) {
+      case FK_GEMV: fused_run<M>(ops[i].u.gemv, ops[i].out, ops[i].p, ab); break;
+      case FK_JACOBI: fused_run<M>(ops[i].u.jac, ops[i].out, ops[i].p, ab); break;
+      case FK_SCAL: fused_run<M>(ops[i].u.scal, ops[i].out, ops[i].p, ab); break;
+      case FK_AXPBY: fused_run<M>(ops[i].u.axpby, ops[i].out, ops[i].p, ab); break;
+      case FK_RESTRICT: fused_run<M>(ops[i].u.rst, ops[i].out, ops[i].p, ab); break;
+      case FK_PROLONG: fused_run<M>(ops[i].u.pro, ops[i].out, ops[i].p, ab); break;
+      case FK_PCORR: fused_run<M>(ops[i].u.pc, ops[i].out, ops[i].p, ab); break;
+      case FK_ZERO: fused_zero<M>(ops[i].out, ops[i].q, ab); break;
+    }
+    __syncthreads();
+  }
+  for (int k = 0; k < nar; ++k) {  // write everything back (the fused part's outputs)
+    arena_copy(ar[k].gbase, arena + ar[k].off, ar[k].bytes);
+    arena_copy(reinterpret_cast<char*>(ar[k].ghdr), arena + ar[k].hoff, sizeof(Hdr));
+  }
+}
+
+
+// one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
+template <typename M, typename Op>
+__global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, M>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (need > 127) {
+    r.err = ERR_WIDTH;
+  } else {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < out.nlog; i += stride) {
+      i128 z = op.template eval1<M>(i);
+      M t;
+      if (p.mode == MODE_NNQ) {
+        t = (M)shift_clamp<i128>(z, c.lam, p.w_out);
+      } else {
+        if (p.mode == MODE_QCOMP) or_mag<i128>(z, r.olo, r.ohi);
+        t = c.store_tmp ? store_shift<M, i128>(z, c) : (M)0;
+      }
+      ((M*)out.data)[i] = t;
+      r.val((int64_t)t);
+    }
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+
+namespace bfp {
+
+static inline int check_window(const WinParams& p, const bfp_vec_s* out) {
+  const int sb = out->ebytes * 8;
+  if (p.w_out < 1 || p.w_out > sb) return BFP_ERR_ARG;
+  if (p.mode == MODE_QCOMP && (p.w_tmp < p.w_out || p.w_tmp > 64)) return BFP_ERR_ARG;
+  if (p.gamma.literal && p.gamma.lm <= 0) return BFP_ERR_ARG;
+  return BFP_OK;
+}
+
+// launch a grid-windowed op: nnqcomp (one pass) or qcomp (pass 1 + recompute)
+template <typename Op>
+static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int b = blocks_for(out->span / 4);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * 148) : b;
+    if (out->ebytes == 4) {
+      if (pp.mode == MODE_QCOMP)
+        launch_pdl(grid_win_kernel<MODE_QCOMP, int32_t, Op>, nb, kThreads, 0, s, op, o, pp);
+      else if (pp.mode == MODE_NNQ)
+        launch_pdl(grid_win_kernel<MODE_NNQ, int32_t, Op>, nb, kThreads, 0, s, op, o, pp);
+      else
+        launch_pdl(grid_win_kernel<MODE_RECOMPUTE, int32_t, Op>, nb, kThreads, 0, s, op, o, pp);
+    } else {
+      if (pp.mode == MODE_QCOMP)
+        launch_pdl(grid_win_kernel<MODE_QCOMP, int64_t, Op>, nb, kThreads, 0, s, op, o, pp);
+      else if (pp.mode == MODE_NNQ)
+        launch_pdl(grid_win_kernel<MODE_NNQ, int64_t, Op>, nb, kThreads, 0, s, op, o, pp);
+      else
+        launch_pdl(grid_win_kernel<MODE_RECOMPUTE, int64_t, Op>, nb, kThreads, 0, s, op, o, pp);
+    }
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
+// stencil ops on int32 grids of 2-D / 3-D with N >= 128 use the register march
+template <typename Op>
+static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int64_t N = int64_t(1) << out->l;
+  static int occ = 0;
+  if (!occ) {
+    for (auto fn : {bulk_win_kernel<MODE_QCOMP, Op>, bulk_win_kernel<MODE_NNQ, Op>,
+                    bulk_win_kernel<MODE_RECOMPUTE, Op>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk_win_kernel<MODE_QCOMP, Op>, kBulkT,
+                                                  kBulkSmem);
+    occ = std::max(occ, 1);
+  }
+  const int64_t strips = N / kBulkW, ctas = (int64_t)148 * occ;
+  const int64_t NZ = out->nz;
+  const int R = (int)std::max<int64_t>(8, (strips * NZ + ctas - 1) / ctas);
+  const int64_t items = strips * ((NZ + R - 1) / R);
+  const int b = (int)std::min<int64_t>(items, ctas);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (pp.mode == MODE_QCOMP)
+      launch_pdl(bulk_win_kernel<MODE_QCOMP, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+    else if (pp.mode == MODE_NNQ)
+      launch_pdl(bulk_win_kernel<MODE_NNQ, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+    else
+      launch_pdl(bulk_win_kernel<MODE_RECOMPUTE, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
+
+
+template <typename Op>
+static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  if (out->ebytes != 4 || out->dim < 2 || (int64_t(1) << out->l) < kMarchMinN)
+    return launch_grid(op, out, p0, s);
+  if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW)
+    return launch_bulk(op, out, p0, s);
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int64_t N = int64_t(1) << out->l, GX = N / 4, rows = out->dim == 3 ? N : 1;
+  static int occ2 = 0, occ3 = 0;
+  if (!occ2) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, march_win_kernel<MODE_QCOMP, 2, Op>,
+                                                  kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, march_win_kernel<MODE_QCOMP, 3, Op>,
+                                                  kThreads, 0);
+    occ2 = std::max(occ2, 1);
+    occ3 = std::max(occ3, 1);
+  }
+  const int occ = out->dim == 2 ? occ2 : occ3;
+  // one balanced resident wave: every thread marches R steps (last chunk shorter)
+  const int64_t slots = (int64_t)148 * occ * kThreads;
+  const int64_t NZ = out->nz;
+  int R = (int)std::max<int64_t>(4, (GX * rows * NZ + slots - 1) / slots);
+  const int64_t items = GX * rows * ((NZ + R - 1) / R);
+  const int b = (int)std::max<int64_t>(1, std::min<int64_t>((items + kThreads - 1) / kThreads,
+                                                            (int64_t)148 * occ));
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp, int nb) {
+    if (out->dim == 2) {
+      if (pp.mode == MODE_QCOMP)
+        launch_pdl(march_win_kernel<MODE_QCOMP, 2, Op>, nb, kThreads, 0, s, op, o, pp, R);
+      else if (pp.mode == MODE_NNQ)
+        launch_pdl(march_win_kernel<MODE_NNQ, 2, Op>, nb, kThreads, 0, s, op, o, pp, R);
+      else
+        launch_pdl(march_win_kernel<MODE_RECOMPUTE, 2, Op>, nb, kThreads, 0, s, op, o, pp, R);
+    } else {
+      if (pp.mode == MODE_QCOMP)
+        launch_pdl(march_win_kernel<MODE_QCOMP, 3, Op>, nb, kThreads, 0, s, op, o, pp, R);
+      else if (pp.mode == MODE_NNQ)
+        launch_pdl(march_win_kernel<MODE_NNQ, 3, Op>, nb, kThreads, 0, s, op, o, pp, R);
+      else
+        launch_pdl(march_win_kernel<MODE_RECOMPUTE, 3, Op>, nb, kThreads, 0, s, op, o, pp, R);
+    }
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p, b);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p, b);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p, b);
+  }
+  return last_launch();
+}
+
+template <typename Op>
+static inline int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int b = blocks_for(out->nlog);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (out->ebytes == 4)
+      launch_pdl(flat_win_kernel<int32_t, Op>, b, kThreads, 0, s, op, o, pp);
+    else
+      launch_pdl(flat_win_kernel<int64_t, Op>, b, kThreads, 0, s, op, o, pp);
+    count_launch();
+  };
+  go(p);
+  if (p.mode == MODE_QCOMP && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
+static inline bool same_grid(const bfp_vec_s* a, const bfp_vec_s* b) {
+  return a->dim == b->dim && a->l == b->l && a->ebytes == b->ebytes && a->span == b->span &&
+         a->nlog == b->nlog && a->z0 == b->z0 && a->nz == b->nz;
+}
+static inline bool full_grid(const bfp_vec_s* a) { return a->dim == 0 || a->nz == (1 << a->l); }
+
+}  // namespace bfp

@@ -286,6 +286,7 @@ struct JacobiOp {
   int dim, l, z0;
   int64_t sx, sb, d1, d2;
   bool narrow;
+  bool neg1;  // d1 < 0: the b term carries the power of two
   int P1, s2;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = 2 * l + x.hdr->e;
@@ -298,25 +299,36 @@ struct JacobiOp {
     int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
     int64_t br = combine_bits(-1, bg, 1, zbits(b.hdr), d1);
     need = combine_bits(1, bx, c.m, br, d2);
-    // r = -g 2^d1 + b (d1 >= 0) as one IMAD.WIDE;  z = x 2^d2 + c r (d2 >= 0)
-    narrow = bg <= 31 && zbits(b.hdr) <= 31 && fits32(c.m) && c.m >= 0 && need <= 63 &&
-             sx < 32 && sb < 32 && d1 >= 0 && d1 <= 30 && d2 >= 0 && d2 <= 62 && bx <= 31 &&
-             (bx == 0 || bx + d2 <= 63);
-    P1 = narrow ? -(1 << (int)d1) : 0;
+    // r = -g 2^d1 + b (d1 >= 0) or b 2^-d1 - g (d1 < 0): one IMAD.WIDE either way;
+    // z = x 2^d2 + c r (d2 >= 0)
+    narrow = bg <= 31 && zbits(b.hdr) <= 31 && c.m >= 0 && c.m <= 0x7fffffff && need <= 63 &&
+             sx < 32 && sb < 32 && d1 >= -30 && d1 <= 30 && d2 >= 0 && d2 <= 62 && d2 != 31 &&
+             bx <= 31 && (bx == 0 || bx + d2 <= 63);
+    neg1 = d1 < 0;
+    P1 = narrow ? (neg1 ? (1 << (int)(-d1)) : -(1 << (int)d1)) : 0;
     s2 = narrow ? (int)d2 : 0;
   }
   __device__ __forceinline__ const Vec& sv() const { return x; }
   __device__ __forceinline__ const Vec& yv2() const { return b; }
   __device__ __forceinline__ int shs() const { return (int)sx; }
   __device__ __forceinline__ int shy() const { return (int)sb; }
+  __device__ __forceinline__ int64_t rterm(int g, int bv) const {
+    const int X = neg1 ? bv : g, Y = neg1 ? -g : bv;
+    return (int64_t)X * (int64_t)P1 + (int64_t)Y;
+  }
   __device__ __forceinline__ int64_t point(int g, int cx, int bv) const {
-    const int64_t r = (int64_t)g * (int64_t)P1 + (int64_t)bv;
+    const int64_t r = rterm(g, bv);
     const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)c.m);
     return mad_pow2(cx, s2, cr);
   }
-  __device__ __forceinline__ bool swapped() const { return false; }
-  template <bool SW> __device__ __forceinline__ int64_t point_t(int g, int cx, int bv) const {
-    return point(g, cx, bv);
+  // the "swap" template slot selects the shift class of x 2^d2: d2 <= 30 (one IMAD.WIDE)
+  // or d2 >= 32 (high word only); d2 == 31 is not narrow
+  __device__ __forceinline__ bool swapped() const { return s2 >= 32; }
+  template <bool HI> __device__ __forceinline__ int64_t point_t(int g, int cx, int bv) const {
+    const int64_t r = rterm(g, bv);
+    const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)(uint32_t)c.m);  // exact by the bound
+    if (HI) return (int64_t)((uint64_t)(uint32_t)(cx << (s2 - 32)) << 32) + cr;
+    return (int64_t)cx * (int64_t)(1 << s2) + cr;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -331,7 +343,7 @@ struct JacobiOp {
         const uint64_t cm = (uint64_t)c.m;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int64_t r = (int64_t)g[j] * (int64_t)P1 + (int64_t)bv[j];
+          const int64_t r = rterm(g[j], bv[j]);
           const int64_t cr = (int64_t)((uint64_t)r * cm);  // exact: |c r| < 2^63 by the bound
           z[j] = mad_pow2(cx[j], s2, cr);
         }
@@ -399,10 +411,25 @@ struct RestrictOp {
   Vec r;       // fine, level l
   int dim, l;  // fine level
   int64_t sr;
+  bool narrow;  // int32 storage, |R r| < 2^31: vectorised 32-bit path
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = -2 * dim + r.hdr->e;
     sr = r.hdr->shift;
     need = eff_bits(r.hdr) + 2 * dim + 2;
+    narrow = need <= 31 && sr < 32 && dim >= 2;
+  }
+  // fine line weights (1,2,1) for 4 consecutive coarse points from fine row base f
+  template <bool NC>
+  __device__ __forceinline__ void line4(const int32_t* f, int sh, int w[4]) const {
+    const int4 a = ldx<NC>(reinterpret_cast<const int4*>(f));
+    const int4 b = ldx<NC>(reinterpret_cast<const int4*>(f + 4));
+    const int e = ldx<NC>(f + 8) >> sh;
+    const int v0 = a.x >> sh, v1 = a.y >> sh, v2 = a.z >> sh, v3 = a.w >> sh;
+    const int v4 = b.x >> sh, v5 = b.y >> sh, v6 = b.z >> sh, v7 = b.w >> sh;
+    w[0] = v0 + 2 * v1 + v2;
+    w[1] = v2 + 2 * v3 + v4;
+    w[2] = v4 + 2 * v5 + v6;
+    w[3] = v6 + 2 * v7 + e;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -411,6 +438,32 @@ struct RestrictOp {
     bool pad[4];
     pad4(dim, lc, o, pad);
     const int64_t J = (o >> lc) & mc, K = (o >> (2 * lc)) & mc;
+    if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
+      if (narrow) {
+        // fine columns 2I0 .. 2I0+8 of fine rows 2J..2J+2 (and planes 2K..2K+2 in 3-D)
+        const int64_t I0 = o & mc;
+        int64_t base = 2 * I0 + 2 * J * Nf;
+        if (dim >= 3) base += 2 * K * Nf * Nf;
+        const int32_t* f = (const int32_t*)r.data + base;
+        const int sh = (int)sr;
+        int acc[4] = {0, 0, 0, 0}, w[4];
+        const int planes = dim >= 3 ? 3 : 1;
+        for (int pz = 0; pz < planes; ++pz) {
+          const int wz = dim >= 3 ? (pz == 1 ? 2 : 1) : 1;
+          const int32_t* fp = f + (dim >= 3 ? pz * Nf * Nf : 0);
+#pragma unroll
+          for (int py = 0; py < 3; ++py) {
+            line4<NC>(fp + py * Nf, sh, w);
+            const int wy = (py == 1 ? 2 : 1) * wz;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] += wy * w[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) z[j] = pad[j] ? 0 : (int64_t)acc[j];
+        return;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t I = (o + j) & mc;
@@ -487,18 +540,72 @@ struct ProlongCorrectOp {
   Vec ec, y;
   int dim, l;
   int64_t sc, sy, d;
+  bool narrow, swap;  // int32 storage: g = P ec in 32 bits, z = X 2^|d| + Y (one IMAD.WIDE)
+  int P;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = -dim + ec.hdr->e;
     axpby_setup(ge, y.hdr->e, d, e_star);
     sc = ec.hdr->shift;
     sy = y.hdr->shift;
-    int64_t bg = grow(zbits(ec.hdr), dim + 2);
-    need = combine_bits(1, bg, 1, zbits(y.hdr), d);
+    int64_t bg = grow(zbits(ec.hdr), dim + 2), by = zbits(y.hdr);
+    need = combine_bits(1, bg, 1, by, d);
+    const int64_t ad = d >= 0 ? d : -d;
+    narrow = need <= 63 && bg <= 31 && by <= 31 && ad <= 30 && sc < 32 && sy < 32;
+    swap = d < 0;
+    P = narrow ? (1 << (int)ad) : 0;
+  }
+  // coarse taps of 4 consecutive fine points along x (i0 even): c[I0-1], c[I0], c[I0+1]
+  template <bool NC>
+  __device__ __forceinline__ void xline(const int32_t* c, int sh, int t[4]) const {
+    const int a = ldx<NC>(c - 1) >> sh, b = ldx<NC>(c) >> sh, e = ldx<NC>(c + 1) >> sh;
+    t[0] = a + b;
+    t[1] = 2 * b;
+    t[2] = b + e;
+    t[3] = 2 * e;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
     pad4(dim, l, o, pad);
+    if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
+      if (narrow) {
+        const int64_t Nf = (int64_t)1 << l, mf = Nf - 1, Nc = Nf >> 1;
+        const int64_t i0 = o & mf;
+        const int32_t* cb = (const int32_t*)ec.data + (i0 >> 1);
+        const int sh = (int)sc;
+        int g[4] = {0, 0, 0, 0}, t[4];
+        if (dim == 1) {
+          xline<NC>(cb, sh, g);
+        } else {
+          const int64_t j = (o >> l) & mf;
+          const int64_t r0 = ((j - 1) >> 1) * Nc, r1 = (j >> 1) * Nc;
+          int64_t p0 = 0, p1 = 0;
+          if (dim >= 3) {
+            const int64_t k = (o >> (2 * l)) & mf;
+            p0 = ((k - 1) >> 1) * Nc * Nc;
+            p1 = (k >> 1) * Nc * Nc;
+          }
+          const int np = dim >= 3 ? 2 : 1;
+          for (int pz = 0; pz < np; ++pz) {
+            const int64_t pb = pz ? p1 : p0;
+            xline<NC>(cb + pb + r0, sh, t);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) g[q] += t[q];
+            xline<NC>(cb + pb + r1, sh, t);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) g[q] += t[q];
+          }
+        }
+        int yv[4];
+        V4<int32_t, NC>::load32(y, o, (int)sy, yv);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int X = swap ? yv[q] : g[q], Y = swap ? g[q] : yv[q];
+          z[q] = pad[q] ? 0 : (int64_t)X * (int64_t)P + (int64_t)Y;
+        }
+        return;
+      }
+    }
     int64_t yv[4];
     V4<M, NC>::load(y, o, sy, yv);
 #pragma unroll

@@ -8,6 +8,7 @@
 // with the frozen config semantics of DESIGN.md.  Because exponents, norms and
 // gamma rules live in device headers, the whole solve is a static PLAN of
 // kernel launches: built once, replayed stream-ordered or as one CUDA graph.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -36,6 +37,8 @@ struct PlanOp {
   uint64_t seed = 0, sid = 0;
   std::vector<PlanOp> sub;  // OK_FUSED: the coarse-level ops run by one CTA
   FusedOp* dev = nullptr;
+  ArenaEntry* arena = nullptr;  // vectors staged in shared memory (nullptr: global)
+  int n_arena = 0, arena_bytes = 0;
 };
 
 int fused_kind(int k) {
@@ -109,8 +112,10 @@ struct bfp_mg_s {
   bool fusion = true;
 
   ~bfp_mg_s() {
-    for (auto& op : plan)
+    for (auto& op : plan) {
       if (op.dev) cudaFree(op.dev);
+      if (op.arena) cudaFree(op.arena);
+    }
     if (graph) cudaGraphExecDestroy(graph);
     for (auto* v : owned) vec_free(v);
     cudaFree(d_trace);
@@ -148,7 +153,8 @@ struct bfp_mg_s {
   bool fusable(int l) const {
     int64_t pts = 1;
     for (int a = 0; a < cfg.d; ++a) pts <<= l;
-    return fusion && !in_fused && pts <= fuse_max_points();
+    const int64_t lim = cfg.fuse_points >= 0 ? cfg.fuse_points : fuse_max_points();
+    return fusion && !in_fused && pts <= lim;
   }
   // run body() with its plan ops collected into one OK_FUSED op
   template <typename F> bfp_vec_s* fused(F body) {
@@ -369,10 +375,85 @@ struct bfp_mg_s {
         int rc = fused_make(fk, so.a, so.b, so.s1, so.s2, so.p, so.q, so.out, &h[i]);
         if (rc) return rc;
       }
+      build_arena(op, h);
       if (cudaMalloc(&op.dev, sizeof(FusedOp) * h.size()) != cudaSuccess) return BFP_ERR_NOMEM;
       cudaMemcpy(op.dev, h.data(), sizeof(FusedOp) * h.size(), cudaMemcpyHostToDevice);
     }
     return cudaDeviceSynchronize() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+  }
+
+
+  // Stage every vector touched by a fused op list in shared memory: rewrite the Vec and
+  // gamma-term pointers as arena byte offsets.  Left global if it does not fit.
+  void build_arena(PlanOp& op, std::vector<FusedOp>& h) {
+    std::vector<bfp_vec_s*> vs;
+    auto find = [&](const Hdr* hp) -> bfp_vec_s* {
+      for (auto* v : owned)
+        if (v->hdr == hp) return v;
+      return nullptr;
+    };
+    auto note = [&](const Hdr* hp) {
+      bfp_vec_s* v = find(hp);
+      if (v && std::find(vs.begin(), vs.end(), v) == vs.end()) vs.push_back(v);
+      return v != nullptr;
+    };
+    auto visit = [&](FusedOp& f, auto&& fn) {
+      fn(f.out);
+      switch (f.kind) {
+        case bfpdev::FK_GEMV: fn(f.u.gemv.x); fn(f.u.gemv.y); break;
+        case bfpdev::FK_JACOBI: fn(f.u.jac.x); fn(f.u.jac.b); break;
+        case bfpdev::FK_SCAL: fn(f.u.scal.r); break;
+        case bfpdev::FK_AXPBY: fn(f.u.axpby.x); fn(f.u.axpby.y); break;
+        case bfpdev::FK_RESTRICT: fn(f.u.rst.r); break;
+        case bfpdev::FK_PROLONG: fn(f.u.pro.xc); break;
+        case bfpdev::FK_PCORR: fn(f.u.pc.ec); fn(f.u.pc.y); break;
+      }
+    };
+    bool ok = true;
+    for (auto& f : h) {
+      visit(f, [&](bfpdev::Vec& v) { ok = ok && note(v.hdr); });
+      if (!f.p.gamma.literal)
+        for (int i = 0; i < f.p.gamma.nterms; ++i)
+          if (f.p.gamma.t[i].v) ok = ok && note(f.p.gamma.t[i].v);
+    }
+    if (!ok) return;
+    std::vector<ArenaEntry> ar;
+    int64_t off = 128;  // offset 0 is reserved (nullptr gamma terms)
+    for (auto* v : vs) {
+      ArenaEntry e;
+      e.gbase = v->base;
+      e.ghdr = v->hdr;
+      e.bytes = ((v->span + 2 * v->halo) * v->ebytes + 15) / 16 * 16;
+      e.off = (int32_t)off;
+      off += (e.bytes + 127) / 128 * 128;
+      e.hoff = (int32_t)off;
+      off += (sizeof(Hdr) + 127) / 128 * 128;
+      ar.push_back(e);
+    }
+    if (off > bfpdev::kArenaMaxBytes) return;
+    auto remap = [&](bfpdev::Vec& v) {
+      for (size_t k = 0; k < vs.size(); ++k)
+        if (vs[k]->hdr == v.hdr) {
+          v.data = (void*)(uintptr_t)(ar[k].off + vs[k]->halo * vs[k]->ebytes);
+          v.hdr = (Hdr*)(uintptr_t)ar[k].hoff;
+          return;
+        }
+    };
+    for (auto& f : h) {
+      if (!f.p.gamma.literal)
+        for (int i = 0; i < f.p.gamma.nterms; ++i)
+          if (f.p.gamma.t[i].v)
+            for (size_t k = 0; k < vs.size(); ++k)
+              if (vs[k]->hdr == f.p.gamma.t[i].v) {
+                f.p.gamma.t[i].v = (const Hdr*)(uintptr_t)ar[k].hoff;
+                break;
+              }
+      visit(f, remap);
+    }
+    if (cudaMalloc(&op.arena, sizeof(ArenaEntry) * ar.size()) != cudaSuccess) return;
+    cudaMemcpy(op.arena, ar.data(), sizeof(ArenaEntry) * ar.size(), cudaMemcpyHostToDevice);
+    op.n_arena = (int)ar.size();
+    op.arena_bytes = (int)off;
   }
 
   int execute(cudaStream_t s) {
@@ -389,7 +470,10 @@ struct bfp_mg_s {
         case OK_RESTRICT: rc = op_restrict(op.a, op.p, op.out, s); break;
         case OK_PROLONG: rc = op_prolong(op.a, op.p, op.out, s); break;
         case OK_PCORR: rc = op_prolong_correct(op.a, op.b, op.p, op.out, s); break;
-        case OK_FUSED: rc = fused_launch(op.dev, (int)op.sub.size(), ebytes, s); break;
+        case OK_FUSED:
+          rc = fused_launch(op.dev, (int)op.sub.size(), op.arena, op.n_arena, op.arena_bytes,
+                            ebytes, s);
+          break;
       }
       if (rc) return rc;
     }

@@ -1,0 +1,57 @@
+// op_fused.cu -- fused single-CTA op lists (shared-memory arena) for coarse levels.
+#include "bfp_kernels.cuh"
+
+namespace bfp {
+
+int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const WinParams& p,
+               int64_t q, bfp_vec_s* out, FusedOp* f) {
+  memset(f, 0, sizeof(*f));
+  f->kind = kind;
+  f->out = view(out);
+  f->p = p;
+  f->q = q;
+  switch (kind) {
+    case FK_GEMV:
+      f->u.gemv.x = view(a); f->u.gemv.y = view(b); f->u.gemv.al = s1; f->u.gemv.be = s2;
+      f->u.gemv.dim = a->dim; f->u.gemv.l = a->l; f->u.gemv.z0 = a->z0;
+      break;
+    case FK_JACOBI:
+      f->u.jac.x = view(a); f->u.jac.b = view(b); f->u.jac.c = s1;
+      f->u.jac.dim = a->dim; f->u.jac.l = a->l; f->u.jac.z0 = a->z0;
+      break;
+    case FK_SCAL: f->u.scal.r = view(a); f->u.scal.c = s1; break;
+    case FK_AXPBY:
+      f->u.axpby.x = view(a); f->u.axpby.y = view(b); f->u.axpby.al = s1; f->u.axpby.be = s2;
+      break;
+    case FK_RESTRICT: f->u.rst.r = view(a); f->u.rst.dim = a->dim; f->u.rst.l = a->l; break;
+    case FK_PROLONG: f->u.pro.xc = view(a); f->u.pro.dim = out->dim; f->u.pro.l = out->l; break;
+    case FK_PCORR:
+      f->u.pc.ec = view(a); f->u.pc.y = view(b); f->u.pc.dim = out->dim; f->u.pc.l = out->l;
+      break;
+    case FK_ZERO: break;
+    default: return BFP_ERR_ARG;
+  }
+  return BFP_OK;
+}
+
+int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, int arena_bytes,
+                 int ebytes, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fused_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kArenaMaxBytes);
+    cudaFuncSetAttribute(fused_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kArenaMaxBytes);
+    attr = true;
+  }
+  if (ebytes == 4)
+    launch_pdl(fused_kernel<int32_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
+               nar);
+  else
+    launch_pdl(fused_kernel<int64_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
+               nar);
+  count_launch();
+  return last_launch();
+}
+
+}  // namespace bfp

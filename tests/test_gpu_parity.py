@@ -299,8 +299,14 @@ def test_mg_golden_gpu(B):
     ("c5", dict(d=3, l_fine=5, cycles=3, x0_random=True, rhs_kind=2), 48),
 ])
 def test_mg_gpu_vs_oracle(B, name, cfgkw, p):
-    x, q, e, hist, tr = _mg_gpu(B, cfgkw, p, graph=True)
     ox, oh, otr = ob.mg_run(ob.mg_config(**cfgkw, p=p))
+    for fuse in (0, 4096):  # per-op launches, and the shared-memory fused bottom levels
+        x, q, e, hist, tr = _mg_gpu(B, dict(cfgkw, fuse_points=fuse), p, graph=True)
+        assert e == ox.e and q == ox.q, fuse
+        assert x.tolist() == ox.m.tolist(), fuse
+        assert hist == oh, fuse
+        assert [tuple(t) for t in tr] == [tuple(t) for t in otr], fuse
+    x, q, e, hist, tr = _mg_gpu(B, cfgkw, p, graph=True)
     assert e == ox.e and q == ox.q
     assert x.tolist() == ox.m.tolist()
     assert hist == oh
