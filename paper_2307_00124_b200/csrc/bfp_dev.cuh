@@ -365,6 +365,19 @@ __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
     s_mn[wid] = mn;
   }
   __syncthreads();
+  if (gridDim.x == 1) {  // single block: finalize directly, no global accumulators
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < nw; ++w) {
+        lo |= s_lo[w];
+        hi |= s_hi[w];
+        err |= s_err[w];
+        mx = s_mx[w] > mx ? s_mx[w] : mx;
+        mn = s_mn[w] < mn ? s_mn[w] : mn;
+      }
+      fin((hi ? 64 + bitlen64(hi) : bitlen64(lo)) + 1, mx, mn, err);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     for (int w = 1; w < nw; ++w) {
       lo |= s_lo[w];
@@ -423,8 +436,9 @@ __device__ inline void win_setup(const WinParams& p, const Hdr* out_h, int64_t e
   c.e_star = e_star;
   c.skip = 0;
   if (p.mode == MODE_RECOMPUTE) {
-    c.skip = !out_h->need_recompute;
-    c.lam = out_h->lam_out;
+    const volatile Hdr* vh = out_h;  // may have been finalized earlier in this launch
+    c.skip = !vh->need_recompute;
+    c.lam = vh->lam_out;
     c.store_tmp = 1;
     c.rs = (int32_t)(c.lam >= 0 ? (c.lam > 127 ? 127 : c.lam) : 0);
     c.ls = (int32_t)(c.lam < 0 ? (-c.lam > 64 ? 64 : -c.lam) : 0);

@@ -163,10 +163,29 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   Red r;
   r.init();
   grid_body<MODE, M>(op, out, p, c, r, need);
-  griddep_launch_dependents();
+  if (MODE != MODE_QCOMP || gridDim.x != 1 || p.part) griddep_launch_dependents();
   reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
+  if constexpr (MODE == MODE_QCOMP) {
+    // a single-block qcomp runs its recompute pass in the same launch (no second kernel)
+    if (gridDim.x == 1 && !p.part) {
+      __syncthreads();  // header finalized by thread 0
+      WinParams p2 = p;
+      p2.mode = MODE_RECOMPUTE;
+      WinCtx c2;
+      win_setup(p2, out.hdr, c.e_star, 8 * (int)sizeof(M), c2);
+      if (!c2.skip) {
+        Red r2;
+        r2.init();
+        grid_body<MODE_RECOMPUTE, M>(op, out, p2, c2, r2, need);
+        reduce_and_finalize(r2, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+          win_finalize(p2, c2, out.hdr, bits, mx, mn, err);
+        });
+      }
+      griddep_launch_dependents();
+    }
+  }
 }
 
 
@@ -707,7 +726,9 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
-  const int b = blocks_for(out->span / 4);
+  // tiny levels: one block (finalized without cross-block atomics)
+  const int64_t groups = out->span / 4;
+  const int b = groups <= 2048 ? 1 : blocks_for(groups);
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * 148) : b;
@@ -736,7 +757,7 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   } else {
     go(p);
   }
-  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part && b > 1) {
     p.mode = MODE_RECOMPUTE;
     go(p);
   }
