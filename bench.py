@@ -363,6 +363,11 @@ def run_ours(args, world, rank, local):
     }
     if rank == 0 and not args.no_extras:
         line["solves"] = run_solves(B, torch, stream)
+        line["residual_other_configs"] = {
+            "C4_3d_511^3_int32_p24": measure_residual(B, torch, stream, 3, 9, 24, 4),
+            "C1_1d_2^20_int32_p16": measure_residual(B, torch, stream, 1, 20, 16, 4, steps=200),
+            "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=5),
+        }
     if rank == 0 and not args.no_cpu:
         sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads,
@@ -440,6 +445,43 @@ def run_e2e(args, B, Lb, torch, stream, sp):
             "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
             "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (stream A) | "
                     "bfp_vec_download_async_i32 (stream B), pinned host, double-buffered"}
+
+
+def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
+    """Residual throughput on another config's fine level (inputs resident, qcomp with the
+    exact-binade gamma; pass 1 alone timed back to back for the kernel time)."""
+    sp = C.c_void_p(stream.cuda_stream)
+    Lb = B.lib()
+    x = B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 1, 1)
+    b_ = B.gen_sine(B.BfpVec.grid(d, l, mb), p)
+    r = B.BfpVec.grid(d, l, mb)
+    B.residual(x, b_, p, p + 5, B.Scalar(1 << 14, 16, 2 * l + 8), out=r)
+    g = B.inf_norm_upper(r).c()
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+    n = ((1 << l) - 1) ** d
+
+    def run(k):
+        for _ in range(k):
+            assert Lb.bfp_stencil_gemv(x.h, b_.h, m1, p1, 0, p, p + 5, g, 0, r.h, sp) == 0
+    run(3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / steps
+    B.set_kernel_path(skip_recompute=True)
+    e0.record(stream)
+    run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    B.set_kernel_path()
+    kern_ms = e0.elapsed_time(e1) / steps
+    assert not (r.header().flags & B.FLAG_RECOMPUTED)
+    peak, _ = peaks()
+    return {"dof": n, "mant_bytes": mb, "p": p, "gdofs": n / (step_ms / 1e3) / 1e9,
+            "kernel_ms": kern_ms, "hbm_frac": 3 * mb * n / (kern_ms / 1e3) / 1e9 / peak}
 
 
 SOLVES = {

@@ -676,6 +676,174 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
 }
 
 
+// ---------------------------------------------------------------------------
+// 3-D stencil ops through the bulk-async pipeline: a CTA owns a W3 x H3 tile of a
+// plane (warp = one row of 128 columns) and marches R planes along z.  Each step
+// streams the (H3+2) x (W3+8) x tile of plane k+1+D (y and x halos included) and
+// the H3 x W3 y tile of plane k+D, one bulk copy per row issued by the lanes of
+// warp 0, into rings of plane slots signalled by mbarriers.
+constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
+constexpr int kB3D = 3;                                       // planes in flight
+constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
+constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
+constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // words per tile
+constexpr size_t kB3Smem = (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * 4 + kB3YS * 8 + 64;
+
+template <int MODE, bool SHIFT, bool SWAP, typename Op>
+__device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const WinParams& p,
+                                           const WinCtx& c, Red& r, int R, char* smem) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l, N2 = N * N;
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int tx = (int)(N / kB3W), ty = (int)(N / kB3H);
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* xsl = reinterpret_cast<int32_t*>(smem);
+  int32_t* ysl = xsl + kB3XS * kB3XT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kB3YS * kB3YT);
+  const int32_t* X = (const int32_t*)op.sv().data;
+  const int32_t* Y = (const int32_t*)op.yv2().data;
+  int32_t* O = (int32_t*)out.data;
+  const int sx = SHIFT ? op.shs() : 0, sy = SHIFT ? op.shy() : 0;
+  const int t = threadIdx.x, lane = t & 31, wy = t >> 5;  // row of the tile
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * 4;
+  uint32_t parity = 0;
+  for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
+    const int tile = item % (tx * ty), ch = item / (tx * ty);
+    const int64_t x0 = (int64_t)(tile % tx) * kB3W, y0 = (int64_t)(tile / tx) * kB3H;
+    const int64_t k0 = (int64_t)ch * R;
+    const int planes = (int)std::min<int64_t>(R, NZ - k0);
+    // stream plane tiles: x plane kp (rows y0-1 .. y0+H3) and y plane ky, by warp 0
+    // x plane kp (rows y0-1 .. y0+H3) and y plane ky on barrier b; `first` also streams
+    // x planes kp-2, kp-1 (the start of a march) on the same barrier
+    auto issue = [&](int64_t kp, int xslot, int64_t ky, int yslot, uint64_t* b, bool first) {
+      if (lane == 0) mbar_expect_tx(b, tx_bytes + (first ? 2u * kB3XT * 4 : 0u));
+      __syncwarp();
+      auto xrow = [&](int64_t k, int slot) {
+        bulk_g2s(xsl + slot * kB3XT + lane * kB3XW,
+                 X + (k > NZ ? NZ : k) * N2 + (y0 - 1 + lane) * N + x0 - 4, kB3XW * 4, b);
+      };
+      if (lane < kB3XR) {
+        xrow(kp, xslot);
+        if (first) {
+          xrow(kp - 2, (int)((kp - 2 + kB3XS) % kB3XS));
+          xrow(kp - 1, (int)((kp - 1 + kB3XS) % kB3XS));
+        }
+      } else if (lane < kB3XR + kB3H) {
+        bulk_g2s(ysl + yslot * kB3YT + (lane - kB3XR) * kB3W,
+                 Y + (ky > NZ ? NZ : ky) * N2 + (y0 + lane - kB3XR) * N + x0, kB3W * 4, b);
+      }
+    };
+    if (wy == 0) {
+      fence_proxy_async_smem();
+      for (int g = 0; g <= kB3D && g < planes; ++g) {
+        const int64_t tk = k0 + g;
+        issue(tk + 1, (int)((tk + 1) % kB3XS), tk, (int)(tk % kB3YS), &bar[tk % kB3YS], g == 0);
+      }
+    }
+    const bool xpad = x0 + 4 * lane + 3 == N - 1;
+    const bool ypad = y0 + wy == N - 1;
+    int sp = (int)((k0 - 1 + kB3XS) % kB3XS), sc = (int)(k0 % kB3XS);
+    int sn = (int)((k0 + 1) % kB3XS), sy_ = (int)(k0 % kB3YS);
+    for (int s = 0; s < planes; ++s) {
+      const int64_t k = k0 + s;
+      mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
+      parity ^= 1u << sy_;
+      const int off = (wy + 1) * kB3XW + 4 + 4 * lane;
+      const int32_t* xc = xsl + sc * kB3XT + off;
+      const int4 b4 = *reinterpret_cast<const int4*>(xc);
+      const int4 u4 = *reinterpret_cast<const int4*>(xc - kB3XW);
+      const int4 d4 = *reinterpret_cast<const int4*>(xc + kB3XW);
+      const int4 zp = *reinterpret_cast<const int4*>(xsl + sp * kB3XT + off);
+      const int4 zn = *reinterpret_cast<const int4*>(xsl + sn * kB3XT + off);
+      const int4 y4 = *reinterpret_cast<const int4*>(ysl + sy_ * kB3YT + wy * kB3W + 4 * lane);
+      const int lf0 = xc[-1], rt0 = xc[4];
+      int lf = __shfl_up_sync(0xffffffffu, b4.w, 1), rt = __shfl_down_sync(0xffffffffu, b4.x, 1);
+      lf = lane == 0 ? lf0 : lf;
+      rt = lane == 31 ? rt0 : rt;
+      const int C[4] = {b4.x >> sx, b4.y >> sx, b4.z >> sx, b4.w >> sx};
+      const int nb[4] = {
+          (lf >> sx) + C[1] + (u4.x >> sx) + (d4.x >> sx) + (zp.x >> sx) + (zn.x >> sx),
+          C[0] + C[2] + (u4.y >> sx) + (d4.y >> sx) + (zp.y >> sx) + (zn.y >> sx),
+          C[1] + C[3] + (u4.z >> sx) + (d4.z >> sx) + (zp.z >> sx) + (zn.z >> sx),
+          C[2] + (rt >> sx) + (u4.w >> sx) + (d4.w >> sx) + (zp.w >> sx) + (zn.w >> sx)};
+      const int Yv[4] = {y4.x >> sy, y4.y >> sy, y4.z >> sy, y4.w >> sy};
+      int32_t tt[4];
+      const bool rowpad = ypad || k + Z0 == N - 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int g = 6 * C[q] - nb[q];
+        int64_t z = op.template point_t<SWAP>(g, C[q], Yv[q]);
+        if (q == 3 && xpad) z = 0;
+        if (rowpad) z = 0;
+        if (MODE == MODE_NNQ) {
+          tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+        } else {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+        }
+        mx = tt[q] > mx ? tt[q] : mx;
+        mn = tt[q] < mn ? tt[q] : mn;
+      }
+      *reinterpret_cast<int4*>(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane) =
+          make_int4(tt[0], tt[1], tt[2], tt[3]);
+      const int free_x = sp, free_y = sy_;
+      sp = sc;
+      sc = sn;
+      sn = sn + 1 == kB3XS ? 0 : sn + 1;
+      sy_ = sy_ + 1 == kB3YS ? 0 : sy_ + 1;
+      __syncthreads();  // slots of plane k-1 (x) and plane k (y) are free
+      if (wy == 0 && s + kB3D + 1 < planes) {
+        fence_proxy_async_smem();
+        const int64_t tk = k + kB3D + 1;  // x plane tk+1 -> slot free_x, y plane tk -> free_y
+        issue(tk + 1, free_x, tk, free_y, &bar[free_y], false);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE, typename Op>
+__global__ void __launch_bounds__(kB3T, 4) bulk3_win_kernel(Op op, Vec out, WinParams p, int R) {
+  extern __shared__ __align__(128) char smem[];
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kB3YS; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    const bool sh = (op.shs() | op.shy()) != 0, sw = op.swapped();
+    if (!sh && !sw)
+      bulk3_loop<MODE, false, false>(op, out, p, c, r, R, smem);
+    else if (sh && !sw)
+      bulk3_loop<MODE, true, false>(op, out, p, c, r, R, smem);
+    else if (!sh)
+      bulk3_loop<MODE, false, true>(op, out, p, c, r, R, smem);
+    else
+      bulk3_loop<MODE, true, true>(op, out, p, c, r, R, smem);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
 // one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
 template <typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
@@ -764,6 +932,52 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   return last_launch();
 }
 
+
+template <typename Op>
+static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0,
+                               cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  const int64_t N = int64_t(1) << out->l;
+  static int occ = 0;
+  if (!occ) {
+    for (auto fn : {bulk3_win_kernel<MODE_QCOMP, Op>, bulk3_win_kernel<MODE_NNQ, Op>,
+                    bulk3_win_kernel<MODE_RECOMPUTE, Op>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kB3Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk3_win_kernel<MODE_QCOMP, Op>, kB3T,
+                                                  kB3Smem);
+    occ = std::max(occ, 1);
+  }
+  const int64_t tiles = (N / kB3W) * (N / kB3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+  const int R = (int)std::max<int64_t>(4, (tiles * NZ + ctas - 1) / ctas);
+  const int64_t items = tiles * ((NZ + R - 1) / R);
+  const int b = (int)std::min<int64_t>(items, ctas);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (pp.mode == MODE_QCOMP)
+      launch_pdl(bulk3_win_kernel<MODE_QCOMP, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+    else if (pp.mode == MODE_NNQ)
+      launch_pdl(bulk3_win_kernel<MODE_NNQ, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+    else
+      launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
 // stencil ops on int32 grids of 2-D / 3-D with N >= 128 use the register march
 template <typename Op>
 static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
@@ -818,6 +1032,8 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
     return launch_grid(op, out, p0, s);
   if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW)
     return launch_bulk(op, out, p0, s);
+  if (g_use_bulk && out->dim == 3 && (int64_t(1) << out->l) >= kB3W)
+    return launch_bulk3(op, out, p0, s);
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);

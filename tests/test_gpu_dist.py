@@ -41,7 +41,7 @@ def _scatter(B, D, full, d, l, ranges):
 
 
 @pytest.mark.parametrize("d,l,P", [(2, 11, 2), (2, 11, 4), (2, 10, 8), (3, 7, 2), (3, 7, 4),
-                                   (2, 7, 4)])
+                                   (2, 7, 4), (3, 7, 64)])
 def test_sharded_stencil_matches_unsharded(B, d, l, P):
     from paper_2307_00124_b200 import dist as D
     p = 20

@@ -330,11 +330,12 @@ def test_full_size_residual_c2(B):
         assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1]))
 
 
-@pytest.mark.parametrize("l", [10, 11])
-def test_stencil_paths_agree_with_oracle(B, l):
-    """2-D stencil ops through the bulk-async pipeline (N >= 1024) and through the
-    register march are both bit-exact vs the oracle (qcomp fast / recompute, nnqcomp)."""
-    d, p = 2, 20
+@pytest.mark.parametrize("d,l", [(2, 10), (2, 11), (3, 7), (3, 8)])
+def test_stencil_paths_agree_with_oracle(B, d, l):
+    """Stencil ops through the bulk-async pipelines (2-D N >= 1024, 3-D N >= 128) and
+    through the register march are both bit-exact vs the oracle (qcomp fast /
+    recompute, nnqcomp)."""
+    p = 20
     ox, ob_ = ob.gen_uniform(d, l, p, 3, 1), ob.gen_sine(d, l, p)
     c = B.jacobi_coeff(d, l, 16)
     try:
