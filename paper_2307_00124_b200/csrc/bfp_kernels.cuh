@@ -686,44 +686,80 @@ constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
 constexpr int kB3D = 3;                                       // planes in flight
 constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
 constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
-constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // words per tile
-constexpr size_t kB3Smem = (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * 4 + kB3YS * 8 + 64;
+constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // elements per tile
+template <typename T> constexpr size_t b3_smem() {
+  return (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T) + kB3YS * 8 + 64;
+}
 
-template <int MODE, bool SHIFT, bool SWAP, typename Op>
+// 4 consecutive elements of a shared-memory tile (16-B aligned)
+template <typename T> struct S4;
+template <> struct S4<int32_t> {
+  using V = int;
+  __device__ static __forceinline__ void ld(const int32_t* p, int sh, V v[4]) {
+    const int4 t = *reinterpret_cast<const int4*>(p);
+    v[0] = t.x >> sh, v[1] = t.y >> sh, v[2] = t.z >> sh, v[3] = t.w >> sh;
+  }
+  __device__ static __forceinline__ void st(int32_t* p, const int32_t t[4]) {
+    *reinterpret_cast<int4*>(p) = make_int4(t[0], t[1], t[2], t[3]);
+  }
+};
+template <> struct S4<int64_t> {
+  using V = int64_t;
+  __device__ static __forceinline__ void ld(const int64_t* p, int sh, V v[4]) {
+    const longlong2 a = reinterpret_cast<const longlong2*>(p)[0];
+    const longlong2 b = reinterpret_cast<const longlong2*>(p)[1];
+    v[0] = a.x >> sh, v[1] = a.y >> sh, v[2] = b.x >> sh, v[3] = b.y >> sh;
+  }
+  __device__ static __forceinline__ void st(int64_t* p, const int64_t t[4]) {
+    reinterpret_cast<longlong2*>(p)[0] = make_longlong2(t[0], t[1]);
+    reinterpret_cast<longlong2*>(p)[1] = make_longlong2(t[2], t[3]);
+  }
+};
+template <typename V> __device__ __forceinline__ V shfl_up1(V v) {
+  return __shfl_up_sync(0xffffffffu, v, 1);
+}
+template <typename V> __device__ __forceinline__ V shfl_dn1(V v) {
+  return __shfl_down_sync(0xffffffffu, v, 1);
+}
+
+// T = storage type, A = accumulator of the exact rows (int64 narrow for int32
+// storage; int64 or __int128 through the ops' generic combine for int64 storage)
+template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, typename Op>
 __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const WinParams& p,
                                            const WinCtx& c, Red& r, int R, char* smem) {
+  using V = typename S4<T>::V;
   const int l = out.l;
   const int64_t N = (int64_t)1 << l, N2 = N * N;
   const int64_t NZ = out.nz, Z0 = out.z0;
   const int tx = (int)(N / kB3W), ty = (int)(N / kB3H);
   const int chunks = (int)((NZ + R - 1) / R);
-  int32_t* xsl = reinterpret_cast<int32_t*>(smem);
-  int32_t* ysl = xsl + kB3XS * kB3XT;
+  T* xsl = reinterpret_cast<T*>(smem);
+  T* ysl = xsl + kB3XS * kB3XT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kB3YS * kB3YT);
-  const int32_t* X = (const int32_t*)op.sv().data;
-  const int32_t* Y = (const int32_t*)op.yv2().data;
-  int32_t* O = (int32_t*)out.data;
+  const T* X = (const T*)op.sv().data;
+  const T* Y = (const T*)op.yv2().data;
+  T* O = (T*)out.data;
   const int sx = SHIFT ? op.shs() : 0, sy = SHIFT ? op.shy() : 0;
   const int t = threadIdx.x, lane = t & 31, wy = t >> 5;  // row of the tile
-  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  V mx = sizeof(T) == 4 ? (V)INT32_MIN : (V)INT64_MIN, mn = sizeof(T) == 4 ? (V)INT32_MAX : (V)INT64_MAX;
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
-  const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * 4;
+  const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * sizeof(T);
   uint32_t parity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
     const int64_t x0 = (int64_t)(tile % tx) * kB3W, y0 = (int64_t)(tile / tx) * kB3H;
     const int64_t k0 = (int64_t)ch * R;
     const int planes = (int)std::min<int64_t>(R, NZ - k0);
-    // stream plane tiles: x plane kp (rows y0-1 .. y0+H3) and y plane ky, by warp 0
     // x plane kp (rows y0-1 .. y0+H3) and y plane ky on barrier b; `first` also streams
     // x planes kp-2, kp-1 (the start of a march) on the same barrier
     auto issue = [&](int64_t kp, int xslot, int64_t ky, int yslot, uint64_t* b, bool first) {
-      if (lane == 0) mbar_expect_tx(b, tx_bytes + (first ? 2u * kB3XT * 4 : 0u));
+      if (lane == 0) mbar_expect_tx(b, tx_bytes + (first ? 2u * kB3XT * sizeof(T) : 0u));
       __syncwarp();
       auto xrow = [&](int64_t k, int slot) {
         bulk_g2s(xsl + slot * kB3XT + lane * kB3XW,
-                 X + (k > NZ ? NZ : k) * N2 + (y0 - 1 + lane) * N + x0 - 4, kB3XW * 4, b);
+                 X + (k > NZ ? NZ : k) * N2 + (y0 - 1 + lane) * N + x0 - 4,
+                 kB3XW * (int)sizeof(T), b);
       };
       if (lane < kB3XR) {
         xrow(kp, xslot);
@@ -733,7 +769,8 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         }
       } else if (lane < kB3XR + kB3H) {
         bulk_g2s(ysl + yslot * kB3YT + (lane - kB3XR) * kB3W,
-                 Y + (ky > NZ ? NZ : ky) * N2 + (y0 + lane - kB3XR) * N + x0, kB3W * 4, b);
+                 Y + (ky > NZ ? NZ : ky) * N2 + (y0 + lane - kB3XR) * N + x0,
+                 kB3W * (int)sizeof(T), b);
       }
     };
     if (wy == 0) {
@@ -752,43 +789,43 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
       mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
       parity ^= 1u << sy_;
       const int off = (wy + 1) * kB3XW + 4 + 4 * lane;
-      const int32_t* xc = xsl + sc * kB3XT + off;
-      const int4 b4 = *reinterpret_cast<const int4*>(xc);
-      const int4 u4 = *reinterpret_cast<const int4*>(xc - kB3XW);
-      const int4 d4 = *reinterpret_cast<const int4*>(xc + kB3XW);
-      const int4 zp = *reinterpret_cast<const int4*>(xsl + sp * kB3XT + off);
-      const int4 zn = *reinterpret_cast<const int4*>(xsl + sn * kB3XT + off);
-      const int4 y4 = *reinterpret_cast<const int4*>(ysl + sy_ * kB3YT + wy * kB3W + 4 * lane);
-      const int lf0 = xc[-1], rt0 = xc[4];
-      int lf = __shfl_up_sync(0xffffffffu, b4.w, 1), rt = __shfl_down_sync(0xffffffffu, b4.x, 1);
+      const T* xc = xsl + sc * kB3XT + off;
+      V C[4], u[4], dn[4], zp[4], zn[4], Yv[4];
+      S4<T>::ld(xc, sx, C);
+      S4<T>::ld(xc - kB3XW, sx, u);
+      S4<T>::ld(xc + kB3XW, sx, dn);
+      S4<T>::ld(xsl + sp * kB3XT + off, sx, zp);
+      S4<T>::ld(xsl + sn * kB3XT + off, sx, zn);
+      S4<T>::ld(ysl + sy_ * kB3YT + wy * kB3W + 4 * lane, sy, Yv);
+      const V lf0 = (V)(xc[-1] >> sx), rt0 = (V)(xc[4] >> sx);
+      V lf = shfl_up1(C[3]), rt = shfl_dn1(C[0]);
       lf = lane == 0 ? lf0 : lf;
       rt = lane == 31 ? rt0 : rt;
-      const int C[4] = {b4.x >> sx, b4.y >> sx, b4.z >> sx, b4.w >> sx};
-      const int nb[4] = {
-          (lf >> sx) + C[1] + (u4.x >> sx) + (d4.x >> sx) + (zp.x >> sx) + (zn.x >> sx),
-          C[0] + C[2] + (u4.y >> sx) + (d4.y >> sx) + (zp.y >> sx) + (zn.y >> sx),
-          C[1] + C[3] + (u4.z >> sx) + (d4.z >> sx) + (zp.z >> sx) + (zn.z >> sx),
-          C[2] + (rt >> sx) + (u4.w >> sx) + (d4.w >> sx) + (zp.w >> sx) + (zn.w >> sx)};
-      const int Yv[4] = {y4.x >> sy, y4.y >> sy, y4.z >> sy, y4.w >> sy};
-      int32_t tt[4];
+      T tt[4];
       const bool rowpad = ypad || k + Z0 == N - 1;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int g = 6 * C[q] - nb[q];
-        int64_t z = op.template point_t<SWAP>(g, C[q], Yv[q]);
+        const V left = q == 0 ? lf : C[q - 1], right = q == 3 ? rt : C[q + 1];
+        A z;
+        if constexpr (sizeof(T) == 4) {
+          const int nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
+          z = op.template point_t<SWAP>(6 * C[q] - nb, C[q], Yv[q]);
+        } else {
+          const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];  // |g| < 2^62 (w64)
+          z = op.template point_w<A>(6 * C[q] - nb, C[q], Yv[q]);
+        }
         if (q == 3 && xpad) z = 0;
         if (rowpad) z = 0;
         if (MODE == MODE_NNQ) {
-          tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+          tt[q] = (T)shift_clamp<A>(z, c.lam, p.w_out);
         } else {
-          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-          tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+          if (MODE == MODE_QCOMP) or_mag<A>(z, olo, ohi);
+          tt[q] = store ? store_shift<T, A>(z, c) : T(0);
         }
-        mx = tt[q] > mx ? tt[q] : mx;
-        mn = tt[q] < mn ? tt[q] : mn;
+        mx = (V)tt[q] > mx ? (V)tt[q] : mx;
+        mn = (V)tt[q] < mn ? (V)tt[q] : mn;
       }
-      *reinterpret_cast<int4*>(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane) =
-          make_int4(tt[0], tt[1], tt[2], tt[3]);
+      S4<T>::st(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane, tt);
       const int free_x = sp, free_y = sy_;
       sp = sc;
       sc = sn;
@@ -809,34 +846,51 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
-template <int MODE, typename Op>
-__global__ void __launch_bounds__(kB3T, 4) bulk3_win_kernel(Op op, Vec out, WinParams p, int R) {
+template <int MODE, typename T, typename Op>
+__global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? 4 : 2)
+    bulk3_win_kernel(Op op, Vec out, WinParams p, int R) {
   extern __shared__ __align__(128) char smem[];
   griddep_wait();
   int64_t need = 0;
   WinCtx c;
-  block_setup<Op, int32_t>(op, out, p, c, need);
+  block_setup<Op, T>(op, out, p, c, need);
   if (c.skip) return;
   Red r;
   r.init();
-  if (op.narrow && need <= 63) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * 4);
+  const bool fast = sizeof(T) == 4 ? (op.narrow && need <= 63) : (op.w64 && need <= 127);
+  if (fast) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T));
     if (threadIdx.x == 0) {
       for (int k = 0; k < kB3YS; ++k) mbar_init(&bar[k], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    const bool sh = (op.shs() | op.shy()) != 0, sw = op.swapped();
-    if (!sh && !sw)
-      bulk3_loop<MODE, false, false>(op, out, p, c, r, R, smem);
-    else if (sh && !sw)
-      bulk3_loop<MODE, true, false>(op, out, p, c, r, R, smem);
-    else if (!sh)
-      bulk3_loop<MODE, false, true>(op, out, p, c, r, R, smem);
-    else
-      bulk3_loop<MODE, true, true>(op, out, p, c, r, R, smem);
+    const bool sh = (op.shs() | op.shy()) != 0;
+    if constexpr (sizeof(T) == 4) {
+      const bool sw = op.swapped();
+      if (!sh && !sw)
+        bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem);
+      else if (sh && !sw)
+        bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem);
+      else if (!sh)
+        bulk3_loop<MODE, false, true, T, int64_t>(op, out, p, c, r, R, smem);
+      else
+        bulk3_loop<MODE, true, true, T, int64_t>(op, out, p, c, r, R, smem);
+    } else {
+      if (need <= 63) {
+        if (sh)
+          bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem);
+        else
+          bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem);
+      } else {
+        if (sh)
+          bulk3_loop<MODE, true, false, T, i128>(op, out, p, c, r, R, smem);
+        else
+          bulk3_loop<MODE, false, false, T, i128>(op, out, p, c, r, R, smem);
+      }
+    }
   } else {
-    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
+    grid_body<MODE, T>(op, out, p, c, r, need);  // exact generic path (or the width error)
   }
   griddep_launch_dependents();
   reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
@@ -933,20 +987,21 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
 }
 
 
-template <typename Op>
+template <typename T, typename Op>
 static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0,
                                cudaStream_t s) {
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
   const int64_t N = int64_t(1) << out->l;
+  constexpr size_t smem = b3_smem<T>();
   static int occ = 0;
   if (!occ) {
-    for (auto fn : {bulk3_win_kernel<MODE_QCOMP, Op>, bulk3_win_kernel<MODE_NNQ, Op>,
-                    bulk3_win_kernel<MODE_RECOMPUTE, Op>})
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kB3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk3_win_kernel<MODE_QCOMP, Op>, kB3T,
-                                                  kB3Smem);
+    for (auto fn : {bulk3_win_kernel<MODE_QCOMP, T, Op>, bulk3_win_kernel<MODE_NNQ, T, Op>,
+                    bulk3_win_kernel<MODE_RECOMPUTE, T, Op>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk3_win_kernel<MODE_QCOMP, T, Op>, kB3T,
+                                                  smem);
     occ = std::max(occ, 1);
   }
   const int64_t tiles = (N / kB3W) * (N / kB3H), ctas = (int64_t)148 * occ, NZ = out->nz;
@@ -956,11 +1011,11 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(bulk3_win_kernel<MODE_QCOMP, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_QCOMP, T, Op>, b, kB3T, smem, s, op, o, pp, R);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(bulk3_win_kernel<MODE_NNQ, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_NNQ, T, Op>, b, kB3T, smem, s, op, o, pp, R);
     else
-      launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, Op>, b, kB3T, kB3Smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R);
     count_launch();
   };
   if (g_prof) {
@@ -1028,12 +1083,13 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
 
 template <typename Op>
 static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  if (g_use_bulk && out->dim == 3 && (int64_t(1) << out->l) >= kB3W)
+    return out->ebytes == 4 ? launch_bulk3<int32_t>(op, out, p0, s)
+                            : launch_bulk3<int64_t>(op, out, p0, s);
   if (out->ebytes != 4 || out->dim < 2 || (int64_t(1) << out->l) < kMarchMinN)
     return launch_grid(op, out, p0, s);
   if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW)
     return launch_bulk(op, out, p0, s);
-  if (g_use_bulk && out->dim == 3 && (int64_t(1) << out->l) >= kB3W)
-    return launch_bulk3(op, out, p0, s);
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);

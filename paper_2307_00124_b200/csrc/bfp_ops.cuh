@@ -49,6 +49,18 @@ __device__ __forceinline__ A combine(int64_t am, A a, int64_t bm, A b, int64_t d
     ta = ta << (int)imin(d, B);
   return ta + tb;
 }
+// combine with 64-bit operand products (exact when msb(am) + bits(a) <= 63 and
+// msb(bm) + bits(b) <= 63), widened to A only for the power-of-two shift
+template <typename A>
+__device__ __forceinline__ A combine_w(int64_t am, int64_t a, int64_t bm, int64_t b, int64_t d) {
+  constexpr int64_t B = AccBits<A>::value - 1;
+  A ta = (A)(am * a), tb = (A)(bm * b);
+  if (d < 0)
+    tb = tb << (int)imin(-d, B);
+  else
+    ta = ta << (int)imin(d, B);
+  return ta + tb;
+}
 // width bound of alpha*a*2^max(d,0) + beta*b*2^max(-d,0) given operand widths
 // (a width of 0 marks an all-zero operand, whose term is excluded)
 __device__ __forceinline__ int64_t combine_bits(int64_t am, int64_t ba, int64_t bm, int64_t bb,
@@ -211,6 +223,7 @@ struct GemvOp {
   // derived (uniform per launch)
   int64_t sx, sy, d;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
+  bool w64;     // 64-bit stencil and products, A-wide shift / sum (int64 storage)
   bool swap;
   int P, Q;
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -228,6 +241,7 @@ struct GemvOp {
     narrow = need <= 63 && sx < 32 && sy < 32 && ad <= 30 && bg <= 31 && by <= 31 &&
              fits32(pm) && fits32(qm) && msb(pm) + ad <= 32 &&
              (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
+    w64 = bg <= 62 && sx < 64 && sy < 64 && msb(al.m) + bg <= 63 && msb(be.m) + by <= 63;
     swap = d < 0;
     P = narrow ? (int)(pm << ad) : 0;
     Q = (int)qm;
@@ -247,6 +261,11 @@ struct GemvOp {
     (void)c;
     return SW ? (int64_t)yv * (int64_t)P + (int64_t)(Q * g)
               : (int64_t)g * (int64_t)P + (int64_t)(Q * yv);
+  }
+  // generic exact point (int64 storage): alpha g 2^max(d,0) + beta y 2^max(-d,0)
+  template <typename A> __device__ __forceinline__ A point_w(int64_t g, int64_t c, int64_t yv) const {
+    (void)c;
+    return combine_w<A>(al.m, g, be.m, yv, d);
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -286,6 +305,7 @@ struct JacobiOp {
   int dim, l, z0;
   int64_t sx, sb, d1, d2;
   bool narrow;
+  bool w64;   // 64-bit stencil and r-term products (int64 storage)
   bool neg1;  // d1 < 0: the b term carries the power of two
   int P1, s2;
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -304,6 +324,7 @@ struct JacobiOp {
     narrow = bg <= 31 && zbits(b.hdr) <= 31 && c.m >= 0 && c.m <= 0x7fffffff && need <= 63 &&
              sx < 32 && sb < 32 && d1 >= -30 && d1 <= 30 && d2 >= 0 && d2 <= 62 && d2 != 31 &&
              bx <= 31 && (bx == 0 || bx + d2 <= 63);
+    w64 = bg <= 62 && zbits(b.hdr) <= 62 && sx < 64 && sb < 64;
     neg1 = d1 < 0;
     P1 = narrow ? (neg1 ? (1 << (int)(-d1)) : -(1 << (int)d1)) : 0;
     s2 = narrow ? (int)d2 : 0;
@@ -329,6 +350,9 @@ struct JacobiOp {
     const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)(uint32_t)c.m);  // exact by the bound
     if (HI) return (int64_t)((uint64_t)(uint32_t)(cx << (s2 - 32)) << 32) + cr;
     return (int64_t)cx * (int64_t)(1 << s2) + cr;
+  }
+  template <typename A> __device__ __forceinline__ A point_w(int64_t g, int64_t cx, int64_t bv) const {
+    return combine<A>(1, (A)cx, c.m, combine_w<A>(-1, g, 1, bv, d1), d2);
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {

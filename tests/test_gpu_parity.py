@@ -330,19 +330,19 @@ def test_full_size_residual_c2(B):
         assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1]))
 
 
-@pytest.mark.parametrize("d,l", [(2, 10), (2, 11), (3, 7), (3, 8)])
-def test_stencil_paths_agree_with_oracle(B, d, l):
-    """Stencil ops through the bulk-async pipelines (2-D N >= 1024, 3-D N >= 128) and
-    through the register march are both bit-exact vs the oracle (qcomp fast /
-    recompute, nnqcomp)."""
-    p = 20
+@pytest.mark.parametrize("d,l,mb,p", [(2, 10, 4, 20), (2, 11, 4, 20), (3, 7, 4, 20),
+                                      (3, 8, 4, 20), (3, 7, 8, 40), (3, 7, 8, 52)])
+def test_stencil_paths_agree_with_oracle(B, d, l, mb, p):
+    """Stencil ops through the bulk-async pipelines (2-D N >= 1024, 3-D N >= 128, int32
+    and int64 storage, int64 / int128 rows) and through the register march / generic
+    grid kernel are both bit-exact vs the oracle (qcomp fast / recompute, nnqcomp)."""
     ox, ob_ = ob.gen_uniform(d, l, p, 3, 1), ob.gen_sine(d, l, p)
     c = B.jacobi_coeff(d, l, 16)
     try:
         for bulk in (True, False):
             B.set_kernel_path(bulk)
-            gx = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 3, 1)
-            gb = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
+            gx = B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 3, 1)
+            gb = B.gen_sine(B.BfpVec.grid(d, l, mb), p)
             for g, nn in ((B.Scalar(1 << 14, 16, 2 * l + 2), False), (B.Scalar(1 << 14, 16, 0), False),
                           (B.Scalar(1 << 14, 16, 2 * l + 2), True)):
                 mode = "nn" if nn else "q"
