@@ -202,6 +202,21 @@ int bfp_mg_result(bfp_mg_t mg, int64_t* x, bfp_header_t* xh, double* hist, int h
 int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r);
 int64_t bfp_mg_kernel_launches(bfp_mg_t mg);
 
+/* ---- sharded solve ----
+ * Levels with >= min_planes planes per rank along the slowest axis (d >= 2) are
+ * slabs of 2^l / world planes; coarser levels are replicated on every rank.
+ * nccl_id = NULL: an in-process group of `world` ranks on the current device
+ * (bit-exact stand-in for the transport, tests); otherwise this process is `rank`
+ * of an NCCL communicator created from a unique id made by bfp_nccl_unique_id on
+ * one rank and broadcast by the caller (the current CUDA device must be set). */
+int bfp_nccl_unique_id(void* id, int id_bytes);
+int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const void* nccl_id,
+                          int min_planes, bfp_mg_t* out);
+/* per local rank: the final iterate / residual (slabs on sharded levels), global rank and
+   the lowest sharded level (64: none) */
+int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_t* r_final,
+                       int* rank, int* lowest_sharded_level);
+
 /* ---- measurement hooks ----
  * When enabled, every windowed pass-1 / nnqcomp kernel launch is bracketed by
  * CUDA events recorded on its own stream; read() synchronises and returns the

@@ -95,6 +95,7 @@ EXPORTS = [
     "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
     "bfp_set_kernel_path", "bfp_vec_download_async_i32", "bfp_vec_create_slab", "bfp_vec_planes",
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
+    "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -155,6 +156,10 @@ def lib() -> C.CDLL:
         "bfp_mg_result": (i32, [vp, vp, C.POINTER(_Header), vp, i32, C.POINTER(i32), vp, i64,
                                 pi64, vp]),
         "bfp_mg_vectors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+        "bfp_nccl_unique_id": (i32, [vp, i32]),
+        "bfp_mg_create_sharded": (i32, [C.POINTER(MgConfig), i32, i32, vp, i32, C.POINTER(vp)]),
+        "bfp_mg_rank_result": (i32, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(i32),
+                                     C.POINTER(i32)]),
         "bfp_mg_kernel_launches": (i64, [vp]),
         "bfp_status_string": (C.c_char_p, [i32]),
         "bfp_device_sync": (i32, [vp]),
@@ -273,9 +278,16 @@ class BfpVec:
         v.upload(m, q, e)
         return v
 
+    @staticmethod
+    def _view(handle: int, dim: int, level: int, mant_bytes: int, owner=None) -> "BfpVec":
+        """Non-owning view of a vector owned by the library (e.g. a solver's)."""
+        v = BfpVec(handle, dim, level, mant_bytes)
+        v._owned, v._owner = False, owner
+        return v
+
     def __del__(self):
         try:
-            if self.h and self.h.value:
+            if getattr(self, "_owned", True) and self.h and self.h.value:
                 lib().bfp_vec_destroy(self.h)
                 self.h = C.c_void_p()
         except Exception:
@@ -591,13 +603,46 @@ def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=Fa
     return cfg
 
 
-class Multigrid:
-    """Device multigrid solver: IR with Jacobi V(nu1,nu2) cycles, or FMG."""
+NCCL_ID_BYTES = 128
 
-    def __init__(self, cfg: MgConfig):
+
+def nccl_unique_id() -> bytes:
+    """An NCCL unique id (make it on one rank, broadcast it to the others)."""
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    _raise(lib().bfp_nccl_unique_id(buf, NCCL_ID_BYTES), "bfp_nccl_unique_id")
+    return buf.raw
+
+
+class Multigrid:
+    """Device multigrid solver: IR with Jacobi V(nu1,nu2) cycles, or FMG.
+
+    ``world > 1`` shards the levels with >= ``min_planes`` planes per rank into slabs
+    (d >= 2) and replicates the coarser ones; ``nccl_id`` (bytes from
+    :func:`nccl_unique_id`) makes this process ``rank`` of an NCCL group, without it
+    all ``world`` ranks run in this process on the current device."""
+
+    def __init__(self, cfg: MgConfig, world: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None, min_planes: int = 16):
         h = C.c_void_p()
-        _raise(lib().bfp_mg_create(C.byref(cfg), C.byref(h)), "bfp_mg_create")
-        self.h, self.cfg = h, cfg
+        if world == 1 and nccl_id is None:
+            _raise(lib().bfp_mg_create(C.byref(cfg), C.byref(h)), "bfp_mg_create")
+        else:
+            idb = C.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id is not None else None
+            _raise(lib().bfp_mg_create_sharded(C.byref(cfg), world, rank, idb, min_planes,
+                                               C.byref(h)), "bfp_mg_create_sharded")
+        self.h, self.cfg, self.world = h, cfg, world
+        self.local = world if nccl_id is None else 1
+
+    def rank_result(self, local_rank: int = 0):
+        """(x_final, r_final, rank, lowest sharded level) of a local rank; x/r are
+        non-owning BfpVec views (slabs on sharded levels)."""
+        x, r, rk, ls = C.c_void_p(), C.c_void_p(), C.c_int(), C.c_int()
+        _raise(lib().bfp_mg_rank_result(self.h, local_rank, C.byref(x), C.byref(r), C.byref(rk),
+                                        C.byref(ls)), "bfp_mg_rank_result")
+        mb = 4
+        xv = BfpVec._view(x.value, self.cfg.d, self.cfg.l_fine, mb, self)
+        rv = BfpVec._view(r.value, self.cfg.d, self.cfg.l_fine, mb, self)
+        return xv, rv, rk.value, ls.value
 
     def __del__(self):
         try:

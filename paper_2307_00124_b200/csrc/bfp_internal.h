@@ -72,6 +72,7 @@ void vec_free(bfp_vec_s* v);
 int set_zero(bfp_vec_s* v, int64_t q, cudaStream_t s);
 
 WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force);
+int window_finalize(bfp_vec_s* out, WinParams p, int stage, const int64_t* part, cudaStream_t s);
 GammaRule gamma_literal(int64_t m, int64_t e);
 
 // windowed ops (mode in p: MODE_QCOMP launches pass 1 + recompute, MODE_NNQ one pass)

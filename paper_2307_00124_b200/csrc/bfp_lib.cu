@@ -454,6 +454,16 @@ int set_zero(bfp_vec_s* v, int64_t q, cudaStream_t s) {
   return last_launch();
 }
 
+// finalize of a partial (multi-rank) window from all-reduced partials; p carries the
+// op's trace / history slots (stage 1 = the recompute pass)
+int window_finalize(bfp_vec_s* out, WinParams p, int stage, const int64_t* part, cudaStream_t s) {
+  if (stage == 1) p.mode = MODE_RECOMPUTE;
+  p.part = nullptr;
+  launch_pdl(window_finalize_kernel, 1, 32, 0, s, view(out), p, part, out->ebytes * 8);
+  count_launch();
+  return last_launch();
+}
+
 WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force) {
   WinParams p;
   memset(&p, 0, sizeof(p));
@@ -1030,12 +1040,8 @@ int bfp_stencil_jacobi_part(bfp_vec_t x, bfp_vec_t b, bfp_scalar_t c, int mode, 
 int bfp_window_finalize(bfp_vec_t out, int mode, int stage, int64_t w_out, int64_t w_tmp,
                         const int64_t* d_part, void* stream) {
   if (!out || !d_part || stage < 0 || stage > 1) return BFP_ERR_ARG;
-  WinParams p = win_params(stage == 1 ? MODE_RECOMPUTE : (mode == 1 ? MODE_NNQ : MODE_QCOMP),
-                           w_out, w_tmp, 0);
-  launch_pdl(window_finalize_kernel, 1, 32, 0, S(stream), view(out), p, d_part,
-             out->ebytes * 8);
-  count_launch();
-  return last_launch();
+  WinParams p = win_params(mode == 1 ? MODE_NNQ : MODE_QCOMP, w_out, w_tmp, 0);
+  return bfp::window_finalize(out, p, stage, d_part, S(stream));
 }
 
 int bfp_jacobi_coeff(int dim, int level, int64_t qc, bfp_scalar_t* c) {

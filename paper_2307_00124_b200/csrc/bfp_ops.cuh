@@ -434,6 +434,7 @@ struct AxpbyOp {
 struct RestrictOp {
   Vec r;       // fine, level l
   int dim, l;  // fine level
+  int zc;      // slab: global index of the output's local plane 0 (coarse)
   int64_t sr;
   bool narrow;  // int32 storage, |R r| < 2^31: vectorised 32-bit path
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -460,7 +461,7 @@ struct RestrictOp {
     const int lc = l - 1;
     const int64_t Nc = (int64_t)1 << lc, mc = Nc - 1, Nf = (int64_t)1 << l;
     bool pad[4];
-    pad4(dim, lc, o, pad);
+    pad4(dim, lc, o, pad, zc);  // slabs: fine z0 = 2 zc, so local fine = 2 local coarse (+1)
     const int64_t J = (o >> lc) & mc, K = (o >> (2 * lc)) & mc;
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
       if (narrow) {
@@ -520,21 +521,24 @@ struct RestrictOp {
 
 // linear interpolation: per axis taps (i-1)>>1 and i>>1 with weight 1 each
 // (odd i -> both taps = (i-1)/2, i.e. weight 2).  Coarse pads/halo are zero.
+// zp = z0(fine) - 2 z0(coarse) shifts the slowest axis when the fine output is a slab
+// (0 for slabs aligned with a coarse slab, z0 of the fine slab for a full coarse grid)
 template <typename M, typename A, bool NC = true>
-__device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int l, int64_t o) {
+__device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int l, int64_t o,
+                                        int zp = 0) {
   const int64_t Nf = (int64_t)1 << l, mf = Nf - 1;
   const int lc = l - 1;
   const int64_t Nc = (int64_t)1 << lc;
   const int64_t i = o & mf;
   const int64_t a0 = (i - 1) >> 1, a1 = i >> 1;
   if (dim == 1) return (A)ld1<M, NC>(xc, a0, sc) + (A)ld1<M, NC>(xc, a1, sc);
-  const int64_t j = (o >> l) & mf;
+  const int64_t j = dim == 2 ? (o >> l) + zp : (o >> l) & mf;
   const int64_t b0 = ((j - 1) >> 1) * Nc, b1 = (j >> 1) * Nc;
   auto line = [&](int64_t rowoff) -> A {
     return (A)ld1<M, NC>(xc, rowoff + a0, sc) + (A)ld1<M, NC>(xc, rowoff + a1, sc);
   };
   if (dim == 2) return line(b0) + line(b1);
-  const int64_t k = (o >> (2 * l)) & mf;
+  const int64_t k = (o >> (2 * l)) + zp;
   const int64_t Nc2 = Nc * Nc;
   const int64_t c0 = ((k - 1) >> 1) * Nc2, c1 = (k >> 1) * Nc2;
   return line(c0 + b0) + line(c0 + b1) + line(c1 + b0) + line(c1 + b1);
@@ -544,6 +548,7 @@ __device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int 
 struct ProlongOp {
   Vec xc;
   int dim, l;  // fine level
+  int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
   int64_t sc;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = -dim + xc.hdr->e;
@@ -553,9 +558,10 @@ struct ProlongOp {
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
-    pad4(dim, l, o, pad);
+    pad4(dim, l, o, pad, zf);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j);
+    for (int j = 0; j < 4; ++j)
+      z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j, zp);
   }
 };
 
@@ -563,6 +569,7 @@ struct ProlongOp {
 struct ProlongCorrectOp {
   Vec ec, y;
   int dim, l;
+  int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
   int64_t sc, sy, d;
   bool narrow, swap;  // int32 storage: g = P ec in 32 bits, z = X 2^|d| + Y (one IMAD.WIDE)
   int P;
@@ -590,7 +597,7 @@ struct ProlongCorrectOp {
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
-    pad4(dim, l, o, pad);
+    pad4(dim, l, o, pad, zf);
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
       if (narrow) {
         const int64_t Nf = (int64_t)1 << l, mf = Nf - 1, Nc = Nf >> 1;
@@ -601,11 +608,11 @@ struct ProlongCorrectOp {
         if (dim == 1) {
           xline<NC>(cb, sh, g);
         } else {
-          const int64_t j = (o >> l) & mf;
+          const int64_t j = dim == 2 ? (o >> l) + zp : (o >> l) & mf;
           const int64_t r0 = ((j - 1) >> 1) * Nc, r1 = (j >> 1) * Nc;
           int64_t p0 = 0, p1 = 0;
           if (dim >= 3) {
-            const int64_t k = (o >> (2 * l)) & mf;
+            const int64_t k = (o >> (2 * l)) + zp;
             p0 = ((k - 1) >> 1) * Nc * Nc;
             p1 = (k >> 1) * Nc * Nc;
           }
@@ -634,7 +641,7 @@ struct ProlongCorrectOp {
     V4<M, NC>::load(y, o, sy, yv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      A g = prolong_at<M, A, NC>(ec, sc, dim, l, o + j);
+      A g = prolong_at<M, A, NC>(ec, sc, dim, l, o + j, zp);
       z[j] = pad[j] ? A(0) : combine<A>(1, g, 1, (A)yv[j], d);
     }
   }

@@ -8,6 +8,19 @@
 // with the frozen config semantics of DESIGN.md.  Because exponents, norms and
 // gamma rules live in device headers, the whole solve is a static PLAN of
 // kernel launches: built once, replayed stream-ordered or as one CUDA graph.
+//
+// Multi-rank: levels with at least `min_planes` planes per rank
+// along the slowest axis are z-slab sharded (y-slabs in 2-D); coarser levels are
+// replicated on every rank (identical integer work, so no scatter is needed).  Every
+// rank builds the same plan over its own slabs; a sharded windowed op runs as
+//   halo exchange -> pass-1 kernel (partial window) -> all-reduce MAX of
+//   {mu*, max, -min, err} -> finalize -> [recompute pass -> all-reduce -> finalize]
+// and the sharded -> replicated boundary restricts into a coarse slab and
+// all-gathers it.  The collectives go through a Comm: NCCL (one rank per process,
+// loaded at run time) or an in-process group of ranks sharing one device (tests).
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -26,7 +39,8 @@ enum StepKind {
   ST_FMG_PROLONG, ST_FINAL_RES
 };
 enum OpKind { OK_ZERO, OK_UNIFORM, OK_GEMV, OK_JACOBI, OK_SCAL, OK_AXPBY, OK_RESTRICT,
-              OK_PROLONG, OK_PCORR, OK_FUSED };
+              OK_PROLONG, OK_PCORR, OK_FUSED, OK_COPY, OK_GATHER };
+enum { HALO_LO = 1, HALO_HI = 2 };
 
 struct PlanOp {
   int kind;
@@ -39,6 +53,8 @@ struct PlanOp {
   FusedOp* dev = nullptr;
   ArenaEntry* arena = nullptr;  // vectors staged in shared memory (nullptr: global)
   int n_arena = 0, arena_bytes = 0;
+  bool shard = false;  // output is a slab: partial window + collectives
+  int halo = 0;        // HALO_LO / HALO_HI planes of `a` exchanged before the op
 };
 
 int fused_kind(int k) {
@@ -71,6 +87,8 @@ struct LevelBufs {
   Scal c{0, 0, 0};
   bfp_vec_s *b = nullptr, *x[2] = {nullptr, nullptr}, *r[2] = {nullptr, nullptr};
   bfp_vec_s *e[2] = {nullptr, nullptr}, *rv = nullptr, *vr = nullptr;
+  bfp_vec_s* vrs = nullptr;  // coarse slab of the restriction at the shard boundary
+  bfp_vec_s* x0 = nullptr;   // sharded random initial iterate (copied in by the plan)
 };
 
 GTerm term(const bfp_vec_s* v, int64_t cm = 0, int64_t ce = 0, int kind = 0) {
@@ -93,8 +111,10 @@ GammaRule rule(std::initializer_list<GTerm> ts) {
 
 }  // namespace
 
-struct bfp_mg_s {
+struct RankSolver {
   bfp_mg_config_t cfg;
+  int rank = 0, world = 1;
+  int ls = 64;  // lowest sharded level (levels >= ls are slabs; 64 = none)
   int ebytes = 4;
   std::vector<LevelBufs> lev;  // indexed by level
   std::vector<PlanOp> plan;
@@ -111,7 +131,7 @@ struct bfp_mg_s {
   bool in_fused = false;
   bool fusion = true;
 
-  ~bfp_mg_s() {
+  ~RankSolver() {
     for (auto& op : plan) {
       if (op.dev) cudaFree(op.dev);
       if (op.arena) cudaFree(op.arena);
@@ -122,9 +142,23 @@ struct bfp_mg_s {
     cudaFree(d_hist);
   }
 
-  bfp_vec_s* vec(int l) {
+  bool sharded(int l) const { return l >= ls; }
+  // this rank's planes [lo, hi) of level l along the slowest axis
+  void slab(int l, int* lo, int* hi) const {
+    const int n = (1 << l) / world;
+    *lo = rank * n;
+    *hi = *lo + n;
+  }
+  bfp_vec_s* vec(int l, bool full = false) {
     bfp_vec_s* v = nullptr;
-    int rc = vec_alloc(cfg.d, l, 0, ebytes, &v);
+    int rc;
+    if (sharded(l) && !full) {
+      int lo, hi;
+      slab(l, &lo, &hi);
+      rc = vec_alloc_slab(cfg.d, l, 0, lo, hi, ebytes, &v);
+    } else {
+      rc = vec_alloc(cfg.d, l, 0, ebytes, &v);
+    }
     if (rc) {
       err = rc;
       return nullptr;
@@ -147,14 +181,27 @@ struct bfp_mg_s {
     op.p.step = st;
     op.p.level = level;
     if (hist) op.p.hist_slot = n_hist++;
+    mark(op);
     plan.push_back(op);
+  }
+  void mark(PlanOp& op) const {
+    if (!op.out || op.out->nz == (1 << op.out->l) || op.out->dim < 2) return;  // full grid
+    op.shard = true;
+    switch (op.kind) {
+      case OK_GEMV: case OK_JACOBI: op.halo = HALO_LO | HALO_HI; break;
+      case OK_RESTRICT: op.halo = HALO_HI; break;
+      case OK_PROLONG: case OK_PCORR:
+        op.halo = op.a->nz == (1 << op.a->l) ? 0 : HALO_LO;  // replicated coarse: no halo
+        break;
+      default: op.halo = 0;
+    }
   }
 
   bool fusable(int l) const {
     int64_t pts = 1;
     for (int a = 0; a < cfg.d; ++a) pts <<= l;
     const int64_t lim = cfg.fuse_points >= 0 ? cfg.fuse_points : fuse_max_points();
-    return fusion && !in_fused && pts <= lim;
+    return fusion && world == 1 && !in_fused && pts <= lim;
   }
   // run body() with its plan ops collected into one OK_FUSED op
   template <typename F> bfp_vec_s* fused(F body) {
@@ -205,8 +252,16 @@ struct bfp_mg_s {
     PlanOp rs;
     rs.kind = OK_RESTRICT;
     rs.a = L.rv;
-    rs.out = Lc.vr;
+    const bool boundary = sharded(l) && !sharded(l - 1);
+    rs.out = boundary ? Lc.vrs : Lc.vr;
     step(ST_RESTRICT, l, rs, wd(l), rule({term(L.rv)}), 6);
+    if (boundary) {  // coarse slabs -> the replicated coarse vector on every rank
+      PlanOp g;
+      g.kind = OK_GATHER;
+      g.a = Lc.vrs;
+      g.out = Lc.vr;
+      plan.push_back(g);
+    }
     bfp_vec_s* ec = vcycle(l - 1, Lc.vr);
     PlanOp pc;
     pc.kind = OK_PCORR;
@@ -292,6 +347,30 @@ struct bfp_mg_s {
     return x;
   }
 
+  int min_planes = 16;
+  // slab of a replicated level aligned with the sharded level above it
+  bfp_vec_s* vec_slab_of(int l) {
+    int lo, hi;
+    slab(l + 1, &lo, &hi);
+    bfp_vec_s* v = nullptr;
+    int rc = vec_alloc_slab(cfg.d, l, 0, lo / 2, hi / 2, ebytes, &v);
+    if (rc) {
+      err = rc;
+      return nullptr;
+    }
+    owned.push_back(v);
+    return v;
+  }
+  // copy this rank's planes (and the header) of a full grid into its slab (setup only)
+  int cut_slab(bfp_vec_s* full, bfp_vec_s* s) {
+    const int64_t pb = (s->span / s->nz) * s->ebytes;
+    if (cudaMemcpy(s->data, (char*)full->data + s->z0 * pb, s->nz * pb,
+                   cudaMemcpyDeviceToDevice) != cudaSuccess ||
+        cudaMemcpy(s->hdr, full->hdr, sizeof(Hdr), cudaMemcpyDeviceToDevice) != cudaSuccess)
+      return BFP_ERR_CUDA;
+    return BFP_OK;
+  }
+
   int build() {
     const int lf = cfg.l_fine, lc = cfg.l_coarse;
     int maxp = 0;
@@ -300,6 +379,9 @@ struct bfp_mg_s {
       maxp = std::max(maxp, std::max<int>((int)std::max(wd(l), (int64_t)cfg.p[l]) + cap, (int)wc(l)));
     }
     ebytes = maxp <= 32 ? 4 : 8;
+    ls = 64;
+    if (world > 1 && cfg.d >= 2)
+      for (int l = lf; l >= lc && ((1 << l) / world) >= std::max(min_planes, 2); --l) ls = l;
     lev.assign(lf + 1, LevelBufs());
     for (int l = lc; l <= lf; ++l) {
       LevelBufs& L = lev[l];
@@ -320,19 +402,25 @@ struct bfp_mg_s {
       L.e[1] = vec(l);
       if (l > lc) L.rv = vec(l);
       if (l < lf) L.vr = vec(l);
+      if (l < lf && !sharded(l) && sharded(l + 1)) L.vrs = vec_slab_of(l);
       if (err) return err;
     }
     // inputs (setup, outside the solve): right-hand sides
     for (int l = lc; l <= lf; ++l) {
       LevelBufs& L = lev[l];
       if (!L.b) continue;
+      // generators normalise over the whole grid: a slab is cut from the full vector
+      bfp_vec_s* full = L.b;
+      if (sharded(l) && vec_alloc(cfg.d, l, 0, ebytes, &full)) return BFP_ERR_NOMEM;
       int rc;
       if (cfg.rhs_kind == 1)
-        rc = gen_sine(L.b, wc(l), 0);
+        rc = gen_sine(full, wc(l), 0);
       else if (cfg.rhs_kind == 0)
-        rc = gen_uniform(L.b, wc(l), cfg.seed, 2, 0);
+        rc = gen_uniform(full, wc(l), cfg.seed, 2, 0);
       else
-        rc = set_zero(L.b, wc(l), 0);
+        rc = set_zero(full, wc(l), 0);
+      if (!rc && full != L.b) rc = cut_slab(full, L.b);
+      if (full != L.b) vec_free(full);
       if (rc) return rc;
     }
     // the plan
@@ -342,7 +430,17 @@ struct bfp_mg_s {
       LevelBufs& L = lev[lf];
       PlanOp init;
       init.out = L.x[0];
-      if (cfg.x0_random) {
+      if (cfg.x0_random && sharded(lf)) {
+        bfp_vec_s* full = nullptr;
+        if (vec_alloc(cfg.d, lf, 0, ebytes, &full)) return BFP_ERR_NOMEM;
+        L.x0 = vec(lf);
+        int rc = err ? err : gen_uniform(full, L.p, cfg.seed, 1, 0);
+        if (!rc) rc = cut_slab(full, L.x0);
+        vec_free(full);
+        if (rc) return rc;
+        init.kind = OK_COPY;
+        init.a = L.x0;
+      } else if (cfg.x0_random) {
         init.kind = OK_UNIFORM;
         init.q = L.p;
         init.seed = cfg.seed;
@@ -456,24 +554,247 @@ struct bfp_mg_s {
     op.arena_bytes = (int)off;
   }
 
+  // one op on this rank; `part` != nullptr runs a windowed op as a partial window
+  // (pass 1 with stage 0, the recompute pass with stage 1)
+  int run(const PlanOp& op, cudaStream_t s, int64_t* part = nullptr, int stage = 0) {
+    WinParams p = op.p;
+    if (part) {
+      p.part = part;
+      if (stage == 1) p.mode = MODE_RECOMPUTE;
+    }
+    switch (op.kind) {
+      case OK_ZERO: return set_zero(op.out, op.q, s);
+      case OK_UNIFORM: return gen_uniform(op.out, op.q, op.seed, op.sid, s);
+      case OK_GEMV: return op_gemv(op.a, op.b, op.s1, op.s2, p, op.out, s);
+      case OK_JACOBI: return op_jacobi(op.a, op.b, op.s1, p, op.out, s);
+      case OK_SCAL: return op_scal(op.a, op.s1, p, op.out, s);
+      case OK_AXPBY: return op_axpby(op.a, op.b, op.s1, op.s2, p, op.out, s);
+      case OK_RESTRICT: return op_restrict(op.a, p, op.out, s);
+      case OK_PROLONG: return op_prolong(op.a, p, op.out, s);
+      case OK_PCORR: return op_prolong_correct(op.a, op.b, p, op.out, s);
+      case OK_COPY:
+        if (cudaMemcpyAsync(op.out->data, op.a->data, op.a->span * op.a->ebytes,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(op.out->hdr, op.a->hdr, sizeof(Hdr), cudaMemcpyDeviceToDevice,
+                            s) != cudaSuccess)
+          return BFP_ERR_CUDA;
+        return BFP_OK;
+      case OK_FUSED:
+        return fused_launch(op.dev, (int)op.sub.size(), op.arena, op.n_arena, op.arena_bytes,
+                            ebytes, s);
+    }
+    return BFP_ERR_ARG;
+  }
+  int finalize(const PlanOp& op, const int64_t* part, int stage, cudaStream_t s) {
+    return window_finalize(op.out, op.p, stage, part, s);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// collectives between the ranks of a sharded solve
+namespace {
+
+struct Comm {
+  virtual ~Comm() {}
+  virtual int nlocal() const = 0;  // ranks driven by this process
+  // fill the lower (HALO_LO: previous rank's last plane) / upper (HALO_HI: next rank's
+  // first plane) halo planes of the slabs v[i] of the local ranks
+  virtual int halo(bfp_vec_s* const* v, int which, cudaStream_t s) = 0;
+  virtual int allreduce_max(int64_t* const* part, int n, cudaStream_t s) = 0;
+  // all-gather equal slabs into the full (replicated) vectors, header included
+  virtual int gather(bfp_vec_s* const* slab, bfp_vec_s* const* full, cudaStream_t s) = 0;
+};
+
+__global__ void part_max_kernel(int64_t* const* parts, int P, int n) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  int64_t m = parts[0][i];
+  for (int r = 1; r < P; ++r) m = parts[r][i] > m ? parts[r][i] : m;
+  for (int r = 0; r < P; ++r) parts[r][i] = m;
+}
+
+static int64_t plane_bytes(const bfp_vec_s* v) { return (v->span / v->nz) * v->ebytes; }
+
+// all ranks in this process on one device (bit-exact stand-in for the NCCL transport)
+struct LocalComm : Comm {
+  int P;
+  int64_t** d_ptrs = nullptr;  // device array of the ranks' partial buffers
+  explicit LocalComm(int p) : P(p) {}
+  ~LocalComm() override { cudaFree(d_ptrs); }
+  int nlocal() const override { return P; }
+  int halo(bfp_vec_s* const* v, int which, cudaStream_t s) override {
+    for (int r = 0; r < P; ++r) {
+      const int64_t pb = plane_bytes(v[r]);
+      char* d = (char*)v[r]->data;
+      if ((which & HALO_LO) && r > 0 &&
+          cudaMemcpyAsync(d - pb, (char*)v[r - 1]->data + (v[r - 1]->nz - 1) * pb, pb,
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return BFP_ERR_CUDA;
+      if ((which & HALO_HI) && r + 1 < P &&
+          cudaMemcpyAsync(d + v[r]->nz * pb, v[r + 1]->data, pb, cudaMemcpyDeviceToDevice, s) !=
+              cudaSuccess)
+        return BFP_ERR_CUDA;
+    }
+    return BFP_OK;
+  }
+  // the ranks' partial buffers (set once at creation)
+  int init(int64_t* const* part) {
+    if (cudaMalloc(&d_ptrs, sizeof(int64_t*) * P) != cudaSuccess) return BFP_ERR_NOMEM;
+    return cudaMemcpy(d_ptrs, part, sizeof(int64_t*) * P, cudaMemcpyHostToDevice) == cudaSuccess
+               ? BFP_OK
+               : BFP_ERR_CUDA;
+  }
+  int allreduce_max(int64_t* const* part, int n, cudaStream_t s) override {
+    (void)part;
+    part_max_kernel<<<1, 32, 0, s>>>(d_ptrs, P, n);
+    count_launch();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "bfpmg_b200: part_max launch: %s\n", cudaGetErrorString(e));
+    return e == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+  }
+  int gather(bfp_vec_s* const* slab, bfp_vec_s* const* full, cudaStream_t s) override {
+    for (int r = 0; r < P; ++r) {
+      for (int q = 0; q < P; ++q) {
+        const int64_t pb = plane_bytes(slab[q]);
+        if (cudaMemcpyAsync((char*)full[r]->data + slab[q]->z0 * pb, slab[q]->data,
+                            slab[q]->nz * pb, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+          return BFP_ERR_CUDA;
+      }
+      if (cudaMemcpyAsync(full[r]->hdr, slab[r]->hdr, sizeof(Hdr), cudaMemcpyDeviceToDevice, s) !=
+          cudaSuccess)
+        return BFP_ERR_CUDA;
+    }
+    return BFP_OK;
+  }
+};
+
+// NCCL, one rank per process; the library is the one already loaded by the host
+// framework (torch) when present, resolved at run time
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  bool load() {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    bool ok = true;
+    auto sym = [&](auto& fn, const char* s) {
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, s));
+      ok = ok && fn != nullptr;
+    };
+    sym(GetUniqueId, "ncclGetUniqueId");
+    sym(CommInitRank, "ncclCommInitRank");
+    sym(CommDestroy, "ncclCommDestroy");
+    sym(AllReduce, "ncclAllReduce");
+    sym(AllGather, "ncclAllGather");
+    sym(Send, "ncclSend");
+    sym(Recv, "ncclRecv");
+    sym(GroupStart, "ncclGroupStart");
+    sym(GroupEnd, "ncclGroupEnd");
+    return ok;
+  }
+};
+Nccl& nccl() {
+  static Nccl n;
+  return n;
+}
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  int nlocal() const override { return 1; }
+  int halo(bfp_vec_s* const* v, int which, cudaStream_t s) override {
+    Nccl& n = nccl();
+    const int64_t pb = plane_bytes(v[0]);
+    char* d = (char*)v[0]->data;
+    const int nz = v[0]->nz;
+    bool ok = n.GroupStart() == ncclSuccess;
+    if (which & HALO_LO) {  // last plane -> next rank's lower halo
+      if (rank > 0) ok = ok && n.Recv(d - pb, pb, ncclUint8, rank - 1, comm, s) == ncclSuccess;
+      if (rank + 1 < world)
+        ok = ok && n.Send(d + (nz - 1) * pb, pb, ncclUint8, rank + 1, comm, s) == ncclSuccess;
+    }
+    if (which & HALO_HI) {  // first plane -> previous rank's upper halo
+      if (rank + 1 < world)
+        ok = ok && n.Recv(d + nz * pb, pb, ncclUint8, rank + 1, comm, s) == ncclSuccess;
+      if (rank > 0) ok = ok && n.Send(d, pb, ncclUint8, rank - 1, comm, s) == ncclSuccess;
+    }
+    ok = (n.GroupEnd() == ncclSuccess) && ok;
+    return ok ? BFP_OK : BFP_ERR_CUDA;
+  }
+  int allreduce_max(int64_t* const* part, int cnt, cudaStream_t s) override {
+    return nccl().AllReduce(part[0], part[0], cnt, ncclInt64, ncclMax, comm, s) == ncclSuccess
+               ? BFP_OK
+               : BFP_ERR_CUDA;
+  }
+  int gather(bfp_vec_s* const* slab, bfp_vec_s* const* full, cudaStream_t s) override {
+    const int64_t bytes = slab[0]->nz * plane_bytes(slab[0]);
+    if (nccl().AllGather(slab[0]->data, full[0]->data, bytes, ncclUint8, comm, s) != ncclSuccess)
+      return BFP_ERR_CUDA;
+    return cudaMemcpyAsync(full[0]->hdr, slab[0]->hdr, sizeof(Hdr), cudaMemcpyDeviceToDevice,
+                           s) == cudaSuccess
+               ? BFP_OK
+               : BFP_ERR_CUDA;
+  }
+};
+
+}  // namespace
+
+// the solver handle: the local ranks' plans (one, or all ranks of an in-process group)
+struct bfp_mg_s {
+  std::vector<RankSolver*> rs;
+  Comm* comm = nullptr;
+  std::vector<int64_t*> parts;  // per local rank: {mu*, max, -min, err}
+  cudaGraphExec_t graph = nullptr;
+  int64_t launches_per_solve = 0;
+  ~bfp_mg_s() {
+    if (graph) cudaGraphExecDestroy(graph);
+    for (auto* r : rs) delete r;
+    for (auto* p : parts) cudaFree(p);
+    delete comm;
+  }
+  RankSolver* r0() const { return rs[0]; }
+
   int execute(cudaStream_t s) {
     const int64_t before = launches();
-    for (const PlanOp& op : plan) {
+    const size_t nops = r0()->plan.size();
+    const int P = (int)rs.size();
+    std::vector<bfp_vec_s*> va(P), vo(P);
+    for (size_t i = 0; i < nops; ++i) {
+      const PlanOp& op0 = r0()->plan[i];
+      for (int r = 0; r < P; ++r) {
+        va[r] = rs[r]->plan[i].a;
+        vo[r] = rs[r]->plan[i].out;
+      }
       int rc = BFP_OK;
-      switch (op.kind) {
-        case OK_ZERO: rc = set_zero(op.out, op.q, s); break;
-        case OK_UNIFORM: rc = gen_uniform(op.out, op.q, op.seed, op.sid, s); break;
-        case OK_GEMV: rc = op_gemv(op.a, op.b, op.s1, op.s2, op.p, op.out, s); break;
-        case OK_JACOBI: rc = op_jacobi(op.a, op.b, op.s1, op.p, op.out, s); break;
-        case OK_SCAL: rc = op_scal(op.a, op.s1, op.p, op.out, s); break;
-        case OK_AXPBY: rc = op_axpby(op.a, op.b, op.s1, op.s2, op.p, op.out, s); break;
-        case OK_RESTRICT: rc = op_restrict(op.a, op.p, op.out, s); break;
-        case OK_PROLONG: rc = op_prolong(op.a, op.p, op.out, s); break;
-        case OK_PCORR: rc = op_prolong_correct(op.a, op.b, op.p, op.out, s); break;
-        case OK_FUSED:
-          rc = fused_launch(op.dev, (int)op.sub.size(), op.arena, op.n_arena, op.arena_bytes,
-                            ebytes, s);
-          break;
+      if (op0.kind == OK_GATHER) {
+        rc = comm->gather(va.data(), vo.data(), s);
+      } else if (!op0.shard) {
+        for (int r = 0; r < P && !rc; ++r) rc = rs[r]->run(rs[r]->plan[i], s);
+      } else {
+        if (op0.halo) rc = comm->halo(va.data(), op0.halo, s);
+        const int stages = op0.p.mode == MODE_QCOMP ? 2 : 1;
+        for (int st = 0; st < stages && !rc; ++st) {
+          for (int r = 0; r < P && !rc; ++r) rc = rs[r]->run(rs[r]->plan[i], s, parts[r], st);
+          if (!rc) rc = comm->allreduce_max(parts.data(), 4, s);
+          for (int r = 0; r < P && !rc; ++r) rc = rs[r]->finalize(rs[r]->plan[i], parts[r], st, s);
+        }
       }
       if (rc) return rc;
     }
@@ -484,8 +805,7 @@ struct bfp_mg_s {
 
 extern "C" {
 
-int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
-  if (!cfg || !out) return BFP_ERR_ARG;
+static int check_cfg(const bfp_mg_config_t* cfg) {
   if (cfg->d < 1 || cfg->d > 3 || cfg->l_coarse < 2 || cfg->l_fine < cfg->l_coarse ||
       cfg->l_fine > 30 || cfg->nu1 < 1 || cfg->nu2 < 0 || cfg->n_coarse < 1 || cfg->cycles < 0 ||
       cfg->qc < 2 || cfg->qc > 30)
@@ -494,16 +814,84 @@ int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
     if (cfg->p[l] < 2 || cfg->p[l] > 58) return BFP_ERR_ARG;
     if (cfg->pd[l] < 0 || cfg->pd[l] > 58 || cfg->pc[l] < 0 || cfg->pc[l] > 58) return BFP_ERR_ARG;
   }
+  return BFP_OK;
+}
+
+static int make_group(const bfp_mg_config_t* cfg, int world, int rank0, int nlocal,
+                      int min_planes, Comm* comm, bfp_mg_t* out) {
   bfp_mg_s* mg = new bfp_mg_s();
-  mg->cfg = *cfg;
-  if (const char* ev = getenv("BFP_NO_FUSION")) mg->fusion = ev[0] != '1';
-  int rc = mg->build();
+  mg->comm = comm;
+  int rc = BFP_OK;
+  for (int i = 0; i < nlocal && !rc; ++i) {
+    RankSolver* r = new RankSolver();
+    r->cfg = *cfg;
+    r->rank = rank0 + i;
+    r->world = world;
+    r->min_planes = min_planes;
+    if (const char* ev = getenv("BFP_NO_FUSION")) r->fusion = ev[0] != '1';
+    mg->rs.push_back(r);
+    rc = r->build();
+    int64_t* part = nullptr;
+    if (!rc && cudaMalloc(&part, 4 * sizeof(int64_t)) != cudaSuccess) rc = BFP_ERR_NOMEM;
+    if (part) mg->parts.push_back(part);
+  }
+  // every rank must have built the same plan
+  for (size_t i = 1; i < mg->rs.size() && !rc; ++i)
+    if (mg->rs[i]->plan.size() != mg->rs[0]->plan.size()) rc = BFP_ERR_ARG;
   if (rc) {
     delete mg;
     return rc;
   }
   *out = mg;
   return BFP_OK;
+}
+
+int bfp_mg_create(const bfp_mg_config_t* cfg, bfp_mg_t* out) {
+  if (!cfg || !out) return BFP_ERR_ARG;
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  return make_group(cfg, 1, 0, 1, 16, nullptr, out);
+}
+
+int bfp_nccl_unique_id(void* id, int id_bytes) {
+  if (!id || id_bytes < (int)sizeof(ncclUniqueId)) return BFP_ERR_ARG;
+  if (!nccl().load()) return BFP_ERR_CUDA;
+  ncclUniqueId u;
+  if (nccl().GetUniqueId(&u) != ncclSuccess) return BFP_ERR_CUDA;
+  memcpy(id, &u, sizeof(u));
+  return BFP_OK;
+}
+
+int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const void* nccl_id,
+                          int min_planes, bfp_mg_t* out) {
+  if (!cfg || !out || world < 1 || min_planes < 2) return BFP_ERR_ARG;
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (world & (world - 1)) return BFP_ERR_ARG;  // slabs: world | 2^l
+  if (!nccl_id) {
+    LocalComm* c = new LocalComm(world);
+    rc = make_group(cfg, world, 0, world, min_planes, c, out);  // owns c
+    if (rc) return rc;
+    rc = c->init((*out)->parts.data());
+    if (rc) {
+      delete *out;
+      *out = nullptr;
+    }
+    return rc;
+  }
+  if (rank < 0 || rank >= world) return BFP_ERR_ARG;
+  if (!nccl().load()) return BFP_ERR_CUDA;
+  NcclComm* c = new NcclComm();
+  c->rank = rank;
+  c->world = world;
+  ncclUniqueId u;
+  memcpy(&u, nccl_id, sizeof(u));
+  if (nccl().CommInitRank(&c->comm, world, u, rank) != ncclSuccess) {
+    c->comm = nullptr;
+    delete c;
+    return BFP_ERR_CUDA;
+  }
+  return make_group(cfg, world, rank, 1, min_planes, c, out);
 }
 
 int bfp_mg_destroy(bfp_mg_t mg) {
@@ -540,38 +928,53 @@ int bfp_mg_solve(bfp_mg_t mg, int use_graph, void* stream) {
   return cudaGraphLaunch(mg->graph, s) == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
 }
 
+// results of local rank 0: its finest-level iterate (a slab when sharded), history, trace
 int bfp_mg_result(bfp_mg_t mg, int64_t* x, bfp_header_t* xh, double* hist, int hist_cap,
                   int* n_hist, bfp_trace_rec_t* trace, int64_t trace_cap, int64_t* n_trace,
                   void* stream) {
   if (!mg) return BFP_ERR_ARG;
+  RankSolver* r = mg->r0();
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int rc = bfp_vec_download(mg->x_final, x, xh, stream);
+  int rc = bfp_vec_download(r->x_final, x, xh, stream);
   if (rc) return rc;
   if (hist && hist_cap > 0)
-    cudaMemcpyAsync(hist, mg->d_hist, sizeof(double) * std::min(hist_cap, mg->n_hist),
+    cudaMemcpyAsync(hist, r->d_hist, sizeof(double) * std::min(hist_cap, r->n_hist),
                     cudaMemcpyDeviceToHost, s);
   if (trace && trace_cap > 0)
-    cudaMemcpyAsync(trace, mg->d_trace,
-                    sizeof(TraceRec) * (size_t)std::min<int64_t>(trace_cap, mg->n_trace),
+    cudaMemcpyAsync(trace, r->d_trace,
+                    sizeof(TraceRec) * (size_t)std::min<int64_t>(trace_cap, r->n_trace),
                     cudaMemcpyDeviceToHost, s);
-  if (n_hist) *n_hist = mg->n_hist;
-  if (n_trace) *n_trace = mg->n_trace;
+  if (n_hist) *n_hist = r->n_hist;
+  if (n_trace) *n_trace = r->n_trace;
   if (cudaStreamSynchronize(s) != cudaSuccess) return BFP_ERR_CUDA;
-  // sticky device errors of any solver vector
-  for (auto* v : mg->owned) {
-    Hdr h;
-    cudaMemcpy(&h, v->hdr, sizeof(h), cudaMemcpyDeviceToHost);
-    if (h.err) return h.err;
-  }
+  // sticky device errors of any solver vector of any local rank
+  for (auto* rr : mg->rs)
+    for (auto* v : rr->owned) {
+      Hdr h;
+      cudaMemcpy(&h, v->hdr, sizeof(h), cudaMemcpyDeviceToHost);
+      if (h.err) return h.err;
+    }
   return BFP_OK;
 }
 
 int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r) {
   if (!mg) return BFP_ERR_ARG;
-  const int lf = mg->cfg.l_fine;
-  if (x) *x = mg->lev[lf].x[0];
-  if (b) *b = mg->lev[lf].b;
-  if (r) *r = mg->lev[lf].r[0];
+  RankSolver* s = mg->r0();
+  const int lf = s->cfg.l_fine;
+  if (x) *x = s->lev[lf].x[0];
+  if (b) *b = s->lev[lf].b;
+  if (r) *r = s->lev[lf].r[0];
+  return BFP_OK;
+}
+
+int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_t* r_final,
+                       int* rank, int* lowest_sharded_level) {
+  if (!mg || local_rank < 0 || local_rank >= (int)mg->rs.size()) return BFP_ERR_ARG;
+  RankSolver* s = mg->rs[local_rank];
+  if (x_final) *x_final = s->x_final;
+  if (r_final) *r_final = s->r_final;
+  if (rank) *rank = s->rank;
+  if (lowest_sharded_level) *lowest_sharded_level = s->ls;
   return BFP_OK;
 }
 

@@ -23,10 +23,15 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
     case FK_AXPBY:
       f->u.axpby.x = view(a); f->u.axpby.y = view(b); f->u.axpby.al = s1; f->u.axpby.be = s2;
       break;
-    case FK_RESTRICT: f->u.rst.r = view(a); f->u.rst.dim = a->dim; f->u.rst.l = a->l; break;
-    case FK_PROLONG: f->u.pro.xc = view(a); f->u.pro.dim = out->dim; f->u.pro.l = out->l; break;
+    case FK_RESTRICT:
+      f->u.rst.r = view(a); f->u.rst.dim = a->dim; f->u.rst.l = a->l; f->u.rst.zc = 0; break;
+    case FK_PROLONG:
+      f->u.pro.xc = view(a); f->u.pro.dim = out->dim; f->u.pro.l = out->l;
+      f->u.pro.zf = f->u.pro.zp = 0;
+      break;
     case FK_PCORR:
       f->u.pc.ec = view(a); f->u.pc.y = view(b); f->u.pc.dim = out->dim; f->u.pc.l = out->l;
+      f->u.pc.zf = f->u.pc.zp = 0;
       break;
     case FK_ZERO: break;
     default: return BFP_ERR_ARG;

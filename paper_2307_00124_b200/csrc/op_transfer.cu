@@ -25,40 +25,53 @@ int op_axpby(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, b
   return launch_grid(op, out, p, s);
 }
 
+// slabs (multi-rank, dim >= 2): a fine slab [2 zc, 2 zc + 2 nzc) restricts to the coarse
+// slab [zc, zc + nzc) (one fine halo plane above); a fine slab prolongs from the aligned
+// coarse slab (one coarse halo plane below) or from a full (replicated) coarse grid
+static bool aligned(const bfp_vec_s* fine, const bfp_vec_s* coarse) {
+  return fine->dim >= 2 && fine->z0 == 2 * coarse->z0 && fine->nz == 2 * coarse->nz;
+}
+
 int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
-  if (!full_grid(r) || !full_grid(out)) return BFP_ERR_ARG;  // transfers: full grids only
   if (r->dim < 1 || out->dim != r->dim || out->l != r->l - 1 || out->ebytes != r->ebytes)
     return BFP_ERR_ARG;
+  if (!(full_grid(r) && full_grid(out)) && !aligned(r, out)) return BFP_ERR_ARG;
   RestrictOp op;
   op.r = view(r);
   op.dim = r->dim;
   op.l = r->l;
+  op.zc = out->z0;
   return launch_grid(op, out, p, s);
 }
 
+static bool prolong_ok(const bfp_vec_s* xc, const bfp_vec_s* fine) {
+  if (xc->dim < 1 || fine->dim != xc->dim || fine->l != xc->l + 1 || fine->ebytes != xc->ebytes)
+    return false;
+  return full_grid(xc) || aligned(fine, xc);
+}
+
 int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
-  if (!full_grid(xc) || !full_grid(out)) return BFP_ERR_ARG;
-  if (xc->dim < 1 || out->dim != xc->dim || out->l != xc->l + 1 || out->ebytes != xc->ebytes)
-    return BFP_ERR_ARG;
+  if (!prolong_ok(xc, out)) return BFP_ERR_ARG;
   ProlongOp op;
   op.xc = view(xc);
   op.dim = out->dim;
   op.l = out->l;
+  op.zf = out->z0;
+  op.zp = out->z0 - 2 * xc->z0;
   return launch_grid(op, out, p, s);
 }
 
 int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_s* out,
                        cudaStream_t s) {
-  if (!full_grid(ec) || !full_grid(y)) return BFP_ERR_ARG;
-  if (ec->dim < 1 || !same_grid(y, out) || y->dim != ec->dim || y->l != ec->l + 1 ||
-      y->ebytes != ec->ebytes)
-    return BFP_ERR_ARG;
+  if (!prolong_ok(ec, y) || !same_grid(y, out)) return BFP_ERR_ARG;
   if (out == y) return BFP_ERR_ALIAS;
   ProlongCorrectOp op;
   op.ec = view(ec);
   op.y = view(y);
   op.dim = y->dim;
   op.l = y->l;
+  op.zf = y->z0;
+  op.zp = y->z0 - 2 * ec->z0;
   return launch_grid(op, out, p, s);
 }
 
