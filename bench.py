@@ -176,9 +176,10 @@ def workload_config():
 
 
 def run_sharded(args, world, rank, local):
-    """N GPUs: the C2 residual z-slab sharded over the ranks (strong scaling): NCCL halo
-    exchange of one row per neighbour and MAX all-reduces of the window partials
-    (paper_2307_00124_b200/dist.py).  --sharded forces this path at N = 1."""
+    """N GPUs: the C2 residual z-slab sharded over the ranks (strong scaling) through the
+    native sharded op (bfp_dist_stencil_gemv: NCCL halo exchange of one row per
+    neighbour, partial windows, MAX all-reduces, finalize -- all enqueued on the stream),
+    one CUDA graph per step.  --sharded forces this path at N = 1."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -197,22 +198,47 @@ def run_sharded(args, world, rank, local):
     gx = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
     gb = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
     g = B.inf_norm_upper(B.residual(gx, gb, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40)).z)
-    be = Dm.GpuBackend()
-    ds = Dm.DistStencil(Dm.TorchComm(be), be)
+    idt = torch.zeros(B.NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(B.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    ops = B.DistOps(world, rank, bytes(idt.cpu().numpy().tobytes()))
 
     def slab_of(full):
         m, q, e = full.download()
         v = B.BfpVec.slab(D, L_FINE, lo, hi)
         v.upload(m[lo * nn_: min(hi, nn_) * nn_], q, e)
-        return Dm.Slab(rank, v)
+        return v
     xs, bs = slab_of(gx), slab_of(gb)
-    outs = [Dm.Slab(rank, B.BfpVec.slab(D, L_FINE, lo, hi)) for _ in range(2)]
+    outs = [B.BfpVec.slab(D, L_FINE, lo, hi) for _ in range(2)]
+    m1, p1 = B.bfp_minus_one(), B.bfp_one()
 
     def step(k):
-        ds.gemv([xs], [bs], B.bfp_minus_one(), B.bfp_one(), P_BITS, W_TMP, g, [outs[k & 1]])
+        ops.gemv([xs], [bs], m1, p1, P_BITS, W_TMP, g, [outs[k & 1]])
 
     for k in range(args.warmup):
         step(k)
+    torch.cuda.synchronize()
+    c0 = B.launch_count()
+    step(0)
+    per_step = B.launch_count() - c0  # our kernels per sharded residual (NCCL ops excluded)
+    torch.cuda.synchronize()
+    # one CUDA graph per output buffer (kernels + NCCL captured on the side stream)
+    graphs, graph_err = [], None
+    try:
+        cs = torch.cuda.Stream()
+        for k in range(2):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=cs, capture_error_mode="thread_local"):
+                B.set_stream(cs.cuda_stream)
+                step(k)
+            graphs.append(gr)
+        B.set_stream(stream.cuda_stream)
+    except Exception as ex:  # noqa: BLE001 -- report and time stream-ordered
+        B.set_stream(stream.cuda_stream)
+        graphs, graph_err = [], str(ex)
+    for k in range(args.warmup):
+        graphs[k & 1].replay() if graphs else step(k)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -220,34 +246,96 @@ def run_sharded(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):
-        step(k)
+        graphs[k & 1].replay() if graphs else step(k)
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     launches = B.launch_count() - l0
+    if graphs:  # kernels per captured step (the replays do not pass through the library)
+        launches = per_step * args.steps
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     # parity of the sharded result with the unsharded residual on this rank's planes
     ref = B.residual(gx, gb, P_BITS, W_TMP, g)
     mr, _, er = ref.z.download()
-    mo, _, eo = outs[(args.steps - 1) & 1].vec.download()
+    mo, _, eo = outs[(args.steps - 1) & 1].download()
     ok = eo == er and np.array_equal(mo, mr[lo * nn_: min(hi, nn_) * nn_])
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    solve = {} if args.no_extras else sharded_solve(B, torch, dist, stream, world, rank)
     line = {
         "metric": "bfp_stencil_residual_gdofs", "value": n * args.steps / (ms / 1e3) / 1e9,
         "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": dict(workload_config(), parallelism=f"z-slab x{world} (NCCL halo + MAX allreduce)"),
-        "gpu_launches": int(launches), "sharded_parity_with_unsharded": bool(okt.item()),
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": dict(workload_config(), parallelism=f"z-slab x{world} (NCCL halo + MAX allreduce)",
+                       l2=f"one (x, b) set + 2 outputs, {12 * n / world / 1e6:.0f} MB per rank "
+                          "(fits the 126 MB L2 from N = 2 on: strong scaling gains L2 reuse)"),
+        "gpu_launches": int(launches), "cuda_graph": bool(graphs), "graph_error": graph_err,
+        "sharded_parity_with_unsharded": bool(okt.item()),
+        "sharded_solve": solve,
     }
     dist.barrier()
+    del ops
     dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def sharded_solve(B, torch, dist, stream, world, rank, name="C4_3d_fmg", min_planes=16, reps=3):
+    """The C4 FMG solve with its fine levels z-slab sharded over the ranks (native
+    solver, NCCL halo / MAX all-reduce / all-gather inside the plan, one CUDA graph per
+    solve); strong scaling.  Parity: this rank's slab of the final iterate and the
+    residual history equal the unsharded solve's."""
+    import numpy as np
+    kw = dict(SOLVES[name])
+    cfg = B.mg_config(**kw)
+    out = {"config": name, "min_planes": min_planes}
+    try:
+        idt = torch.zeros(B.NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(B.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+        mg = B.Multigrid(cfg, world=world, rank=rank, nccl_id=nid, min_planes=min_planes)
+        mg.solve(use_graph=False)  # connections + first run outside capture
+        torch.cuda.synchronize()
+        graph = True
+        try:
+            mg.solve(use_graph=True)
+        except Exception as ex:  # noqa: BLE001 -- report and time stream-ordered
+            graph, out["graph_error"] = False, str(ex)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            mg.solve(use_graph=graph)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
+        xv, rv, rk, ls = mg.rank_result(0)
+        mx, _, ex_ = xv.download()
+        ref = B.Multigrid(cfg)
+        ref.solve(use_graph=True)
+        xr, qr, er, hr, trr = ref.result(trace_cap=1 << 16)
+        nn_ = (1 << cfg.l_fine) - 1
+        per = nn_ ** (cfg.d - 1)
+        lo = rank * ((1 << cfg.l_fine) // world) if ls <= cfg.l_fine else 0
+        ok = ex_ == er and hist == hr and tr == trr and np.array_equal(
+            mx, xr[lo * per: lo * per + len(mx)])
+        okt = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        out.update(ms=float(ms.item()), graph=graph, lowest_sharded_level=ls,
+                   parity_with_unsharded=bool(okt.item()), final_residual=hist[-1])
+        del mg, ref
+    except Exception as ex:  # noqa: BLE001 -- report, never hide
+        out["error"] = str(ex)
+    return out
 
 
 def run_ours(args, world, rank, local):

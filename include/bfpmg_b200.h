@@ -217,6 +217,21 @@ int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const
 int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_t* r_final,
                        int* rank, int* lowest_sharded_level);
 
+/* sharded single stencil ops (a fine-level residual / Jacobi sweep over z-slabs):
+ * halo exchange, pass 1 with partial windows, MAX all-reduce of {mu*, max, -min, err},
+ * finalize (+ the recompute pass) -- all stream-ordered, no host synchronisation.
+ * The vector arguments are arrays of one slab handle per local rank (world for an
+ * in-process group, 1 with NCCL). */
+typedef struct bfp_dist_s* bfp_dist_t;
+int bfp_dist_create(int world, int rank, const void* nccl_id, bfp_dist_t* out);
+int bfp_dist_destroy(bfp_dist_t d);
+int bfp_dist_stencil_gemv(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* y,
+                          bfp_scalar_t alpha, bfp_scalar_t beta, int mode, int64_t w_out,
+                          int64_t w_tmp, bfp_scalar_t gamma, bfp_vec_t const* out, void* stream);
+int bfp_dist_stencil_jacobi(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* b, bfp_scalar_t c,
+                            int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                            bfp_vec_t const* out, void* stream);
+
 /* ---- measurement hooks ----
  * When enabled, every windowed pass-1 / nnqcomp kernel launch is bracketed by
  * CUDA events recorded on its own stream; read() synchronises and returns the

@@ -95,7 +95,8 @@ EXPORTS = [
     "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
     "bfp_set_kernel_path", "bfp_vec_download_async_i32", "bfp_vec_create_slab", "bfp_vec_planes",
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
-    "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result",
+    "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result", "bfp_dist_create",
+    "bfp_dist_destroy", "bfp_dist_stencil_gemv", "bfp_dist_stencil_jacobi",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -157,6 +158,12 @@ def lib() -> C.CDLL:
                                 pi64, vp]),
         "bfp_mg_vectors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
         "bfp_nccl_unique_id": (i32, [vp, i32]),
+        "bfp_dist_create": (i32, [i32, i32, vp, C.POINTER(vp)]),
+        "bfp_dist_destroy": (i32, [vp]),
+        "bfp_dist_stencil_gemv": (i32, [vp, C.POINTER(vp), C.POINTER(vp), S, S, i32, i64, i64, S,
+                                        C.POINTER(vp), vp]),
+        "bfp_dist_stencil_jacobi": (i32, [vp, C.POINTER(vp), C.POINTER(vp), S, i32, i64, i64, S,
+                                          C.POINTER(vp), vp]),
         "bfp_mg_create_sharded": (i32, [C.POINTER(MgConfig), i32, i32, vp, i32, C.POINTER(vp)]),
         "bfp_mg_rank_result": (i32, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(i32),
                                      C.POINTER(i32)]),
@@ -611,6 +618,45 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(NCCL_ID_BYTES)
     _raise(lib().bfp_nccl_unique_id(buf, NCCL_ID_BYTES), "bfp_nccl_unique_id")
     return buf.raw
+
+
+class DistOps:
+    """Sharded stencil ops over z-slabs (native: halo exchange, partial windows, MAX
+    all-reduce and finalize enqueued on the stream, no host synchronisation).
+
+    ``nccl_id`` (from :func:`nccl_unique_id`) makes this process ``rank`` of an NCCL
+    group of ``world``; without it the ``world`` ranks run in this process (every call
+    then takes one slab per rank)."""
+
+    def __init__(self, world: int, rank: int = 0, nccl_id: Optional[bytes] = None):
+        h = C.c_void_p()
+        idb = C.create_string_buffer(nccl_id, NCCL_ID_BYTES) if nccl_id is not None else None
+        _raise(lib().bfp_dist_create(world, rank, idb, C.byref(h)), "bfp_dist_create")
+        self.h, self.world = h, world
+        self.local = world if nccl_id is None else 1
+
+    def __del__(self):
+        try:
+            lib().bfp_dist_destroy(self.h)
+        except Exception:
+            pass
+
+    def _arr(self, vs):
+        if len(vs) != self.local:
+            raise InvalidArgument(ERR_ARG, f"expected {self.local} slabs")
+        return (C.c_void_p * len(vs))(*[v.h.value for v in vs])
+
+    def gemv(self, xs, ys, alpha: Scalar, beta: Scalar, w_out: int, w_tmp: int, gamma: Scalar,
+             outs, nn: bool = False):
+        _raise(lib().bfp_dist_stencil_gemv(self.h, self._arr(xs), self._arr(ys), alpha.c(),
+                                           beta.c(), int(nn), w_out, w_tmp, gamma.c(),
+                                           self._arr(outs), _s()), "bfp_dist_stencil_gemv")
+
+    def jacobi(self, xs, bs, c: Scalar, w_out: int, w_tmp: int, gamma: Scalar, outs,
+               nn: bool = False):
+        _raise(lib().bfp_dist_stencil_jacobi(self.h, self._arr(xs), self._arr(bs), c.c(), int(nn),
+                                             w_out, w_tmp, gamma.c(), self._arr(outs), _s()),
+               "bfp_dist_stencil_jacobi")
 
 
 class Multigrid:

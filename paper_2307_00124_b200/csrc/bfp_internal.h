@@ -73,7 +73,7 @@ int set_zero(bfp_vec_s* v, int64_t q, cudaStream_t s);
 
 WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force);
 int window_finalize(bfp_vec_s* out, WinParams p, int stage, const int64_t* part, cudaStream_t s);
-GammaRule gamma_literal(int64_t m, int64_t e);
+GammaRule gamma_literal(int64_t m, int64_t e);  // (declared for the solver too)
 
 // windowed ops (mode in p: MODE_QCOMP launches pass 1 + recompute, MODE_NNQ one pass)
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,

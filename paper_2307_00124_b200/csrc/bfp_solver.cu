@@ -980,4 +980,103 @@ int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_
 
 int64_t bfp_mg_kernel_launches(bfp_mg_t mg) { return mg ? mg->launches_per_solve : -1; }
 
+// ---- sharded single ops over a communicator (the residual / Jacobi of a fine level) ----
+struct bfp_dist_s {
+  Comm* comm = nullptr;
+  std::vector<int64_t*> parts;
+  ~bfp_dist_s() {
+    for (auto* p : parts) cudaFree(p);
+    delete comm;
+  }
+};
+
+int bfp_dist_create(int world, int rank, const void* nccl_id, bfp_dist_t* out) {
+  if (!out || world < 1) return BFP_ERR_ARG;
+  bfp_dist_s* d = new bfp_dist_s();
+  int rc = BFP_OK;
+  if (!nccl_id) {
+    LocalComm* c = new LocalComm(world);
+    d->comm = c;
+    d->parts.assign(world, nullptr);
+    for (auto& p : d->parts)
+      if (cudaMalloc(&p, 4 * sizeof(int64_t)) != cudaSuccess) rc = BFP_ERR_NOMEM;
+    if (!rc) rc = c->init(d->parts.data());
+  } else {
+    if (rank < 0 || rank >= world || !nccl().load()) {
+      delete d;
+      return rank < 0 || rank >= world ? BFP_ERR_ARG : BFP_ERR_CUDA;
+    }
+    NcclComm* c = new NcclComm();
+    c->rank = rank;
+    c->world = world;
+    ncclUniqueId u;
+    memcpy(&u, nccl_id, sizeof(u));
+    if (nccl().CommInitRank(&c->comm, world, u, rank) != ncclSuccess) {
+      c->comm = nullptr;
+      rc = BFP_ERR_CUDA;
+    }
+    d->comm = c;
+    d->parts.assign(1, nullptr);
+    if (!rc && cudaMalloc(&d->parts[0], 4 * sizeof(int64_t)) != cudaSuccess) rc = BFP_ERR_NOMEM;
+  }
+  if (rc) {
+    delete d;
+    return rc;
+  }
+  *out = d;
+  return BFP_OK;
+}
+
+int bfp_dist_destroy(bfp_dist_t d) {
+  delete d;
+  return BFP_OK;
+}
+
+}  // extern "C"
+// halo exchange -> pass 1 (partials) -> all-reduce -> finalize [-> recompute -> ...]
+template <typename F>
+static int dist_window(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* out, int mode,
+                       int64_t w_out, int64_t w_tmp, bfp_scalar_t g, cudaStream_t s, F launch) {
+  const int P = d->comm->nlocal();
+  for (int r = 0; r < P; ++r)
+    if (!x[r] || !out[r] || out[r]->dim < 2) return BFP_ERR_ARG;
+  int rc = d->comm->halo(x, HALO_LO | HALO_HI, s);
+  WinParams p = win_params(mode == 1 ? MODE_NNQ : MODE_QCOMP, w_out, w_tmp, 0);
+  p.gamma = gamma_literal(g.m, g.e);
+  const int stages = mode == 1 ? 1 : 2;
+  for (int st = 0; st < stages && !rc; ++st) {
+    for (int r = 0; r < P && !rc; ++r) {
+      WinParams pr = p;
+      pr.part = d->parts[r];
+      if (st == 1) pr.mode = MODE_RECOMPUTE;
+      rc = launch(r, pr);
+    }
+    if (!rc) rc = d->comm->allreduce_max(d->parts.data(), 4, s);
+    for (int r = 0; r < P && !rc; ++r) rc = window_finalize(out[r], p, st, d->parts[r], s);
+  }
+  return rc;
+}
+extern "C" {
+
+int bfp_dist_stencil_gemv(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* y,
+                          bfp_scalar_t alpha, bfp_scalar_t beta, int mode, int64_t w_out,
+                          int64_t w_tmp, bfp_scalar_t gamma, bfp_vec_t const* out, void* stream) {
+  if (!d || !x || !y || !out || gamma.m <= 0) return BFP_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return dist_window(d, x, out, mode, w_out, w_tmp, gamma, s, [&](int r, const WinParams& p) {
+    return op_gemv(x[r], y[r], Scal{alpha.m, alpha.q, alpha.e}, Scal{beta.m, beta.q, beta.e}, p,
+                   out[r], s);
+  });
+}
+
+int bfp_dist_stencil_jacobi(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* b, bfp_scalar_t c,
+                            int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
+                            bfp_vec_t const* out, void* stream) {
+  if (!d || !x || !b || !out || gamma.m <= 0) return BFP_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return dist_window(d, x, out, mode, w_out, w_tmp, gamma, s, [&](int r, const WinParams& p) {
+    return op_jacobi(x[r], b[r], Scal{c.m, c.q, c.e}, p, out[r], s);
+  });
+}
+
 }  // extern "C"

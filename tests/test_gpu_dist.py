@@ -89,3 +89,33 @@ def test_slab_ranges():
     assert D.slab_ranges(9, 8) == [(64 * r, 64 * (r + 1)) for r in range(8)]
     with pytest.raises(ValueError):
         D.slab_ranges(3, 8)
+
+
+@pytest.mark.parametrize("d,l,P", [(2, 11, 4), (3, 7, 2), (3, 7, 8), (3, 7, 64)])
+def test_native_dist_ops_match_unsharded(B, d, l, P):
+    """The native sharded ops (bfp_dist_*: halo, partial windows, MAX all-reduce and
+    finalize enqueued in C++) equal the unsharded ops bit-exactly."""
+    from paper_2307_00124_b200 import dist as D
+    p = 20
+    ranges = D.slab_ranges(l, P)
+    gx = B.gen_uniform(B.BfpVec.grid(d, l), p, 5, 1)
+    gb = B.gen_sine(B.BfpVec.grid(d, l), p)
+    xs = [s.vec for s in _scatter(B, D, gx, d, l, ranges)]
+    bs = [s.vec for s in _scatter(B, D, gb, d, l, ranges)]
+    ops = B.DistOps(P)
+    c = B.jacobi_coeff(d, l, 16)
+    g_exact = B.inf_norm_upper(B.residual(gx, gb, p, p + 5, B.Scalar(1 << 14, 16, 0)).z)
+    for g, nn in ((g_exact, False), (B.Scalar(1 << 14, 16, 2 * l + 2), False),
+                  (B.Scalar(1 << 14, 16, 0), False), (B.Scalar(1 << 14, 16, 2 * l + 2), True)):
+        outs = [B.BfpVec.slab(d, l, lo, hi) for (lo, hi) in ranges]
+        ops.gemv(xs, bs, B.bfp_minus_one(), B.bfp_one(), p, p + 5, g, outs, nn=nn)
+        got, e = _gather([D.Slab(r, v) for r, v in enumerate(outs)])
+        ref = B.residual(gx, gb, p, p + 5, g, nn=nn)
+        m, q, er = ref.z.download()
+        assert e == er and np.array_equal(got, m), (d, l, P, g, nn)
+        assert {v.flags for v in outs} == {ref.z.flags}
+        js = [B.BfpVec.slab(d, l, lo, hi) for (lo, hi) in ranges]
+        ops.jacobi(xs, outs, c, p, p + 5, g, js, nn=nn)
+        got, e = _gather([D.Slab(r, v) for r, v in enumerate(js)])
+        m, q, er = B.jacobi(gx, ref.z, c, p, p + 5, g, nn=nn).z.download()
+        assert e == er and np.array_equal(got, m), ("jacobi", d, l, P, g, nn)
