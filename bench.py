@@ -108,9 +108,9 @@ def dist_setup(args):
 # reference arm: the CPU path (oracle port) on the same config
 
 
-def cpu_residual_time(steps, warmup, budget_s=None):
-    """Time the oracle's OpenMP qcomp residual on the config-2 inputs.
-    Returns (seconds per residual, threads, steps actually run)."""
+def cpu_residual_time(steps, warmup, budget_s=None, threads=None):
+    """Time the oracle's OpenMP qcomp residual on the config-2 inputs (all host threads,
+    or `threads`). Returns (seconds per residual, threads, steps actually run)."""
     from oracle import ob
     L = ob.lib()
     x = ob.gen_uniform(D, L_FINE, P_BITS, 1, 1)
@@ -118,7 +118,7 @@ def cpu_residual_time(steps, warmup, budget_s=None):
     out = ob.OBlock(x.m.copy(), P_BITS, 0)
     xc, bc, oc = x.c(), b.c(), out.c()
     fl = ob.Flags()
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     g = ob.Grid(D, L_FINE)
     gm, ge = 1 << 14, 30  # window above the residual: exercised like the reference's gamma
     # exact-binade gamma: the fast path, as on the GPU
@@ -140,6 +140,16 @@ def cpu_residual_time(steps, warmup, budget_s=None):
             break
     dt = (time.perf_counter() - t0) / n
     return dt, threads, n
+
+
+def host_cpu():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} threads"
 
 
 def run_reference(args, world, rank):
@@ -451,17 +461,32 @@ def run_ours(args, world, rank, local):
     }
     if rank == 0 and not args.no_extras:
         line["solves"] = run_solves(B, torch, stream)
+        ttd = {k: v for k, v in line["solves"].items()
+               if v.get("accuracy", {}).get("alg_over_disc", 1e30) <= 1.0}
+        if ttd:
+            k = min(ttd, key=lambda k: ttd[k]["ms"])
+            line["fmg_time_to_disc_accuracy"] = {
+                "config": k, "ms": ttd[k]["ms"], "alg_over_disc": ttd[k]["accuracy"]["alg_over_disc"],
+                "note": "max-norm error vs the discrete solution <= the discretisation error"}
         line["residual_other_configs"] = {
             "C4_3d_511^3_int32_p24": measure_residual(B, torch, stream, 3, 9, 24, 4),
             "C1_1d_2^20_int32_p16": measure_residual(B, torch, stream, 1, 20, 16, 4, steps=200),
             "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=5),
         }
+        line["fine_level_ops"] = {"C2": measure_ops(B, torch, stream, 2, 12, 20),
+                                  "C4": measure_ops(B, torch, stream, 3, 9, 24)}
     if rank == 0 and not args.no_cpu:
         sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
+        sec1, _, nrun1 = cpu_residual_time(10**9, 0, budget_s=args.cpu_budget / 2, threads=1)
         line["cpu_baseline"] = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads,
                                 "kind": "port",
                                 "sample": f"{nrun} full 4095^2 residuals in ~{args.cpu_budget:.0f} s "
-                                          f"(oracle/bfp_oracle.c, OpenMP)"}
+                                          f"(oracle/bfp_oracle.c, OpenMP)",
+                                "single_thread": {"value": n / sec1 / 1e9, "cores": 1,
+                                                  "sample": f"{nrun1} full 4095^2 residuals, one "
+                                                            "thread (the reference's loops are "
+                                                            "sequential)"},
+                                "host_cpu": host_cpu()}
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -572,6 +597,61 @@ def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
             "kernel_ms": kern_ms, "hbm_frac": 3 * mb * n / (kern_ms / 1e3) / 1e9 / peak}
 
 
+def measure_ops(B, torch, stream, d, l, p, steps=20):
+    """Every fine-level op of the V-cycle / FMG on one config's finest level (inputs
+    resident, gamma at the exact binade so qcomp takes the fast path): pass-1 kernel
+    time (recompute launch skipped, flags verified) and its fraction of the measured
+    HBM peak for the op's algorithmic bytes (residual / Jacobi / axpby
+    3s, scal 2s, restriction (1 + 2^-d)s and prolongation (2^-d + 1)s per fine DoF,
+    prolong + correct (2 + 2^-d)s)."""
+    sp = C.c_void_p(stream.cuda_stream)
+    L = B.lib()
+    s = 4
+    n = ((1 << l) - 1) ** d
+    x = B.gen_uniform(B.BfpVec.grid(d, l, s), p, 1, 1)
+    b = B.gen_sine(B.BfpVec.grid(d, l, s), p)
+    y = B.gen_uniform(B.BfpVec.grid(d, l, s), p, 2, 1)
+    xc = B.gen_uniform(B.BfpVec.grid(d, l - 1, s), p, 3, 1)
+    out = B.BfpVec.grid(d, l, s)
+    outc = B.BfpVec.grid(d, l - 1, s)
+    c = B.jacobi_coeff(d, l, 16).c()
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+    G = B.Scalar(1 << 14, 16, 2 * l + 8).c()
+    ops = {
+        "residual": (lambda g: L.bfp_stencil_gemv(x.h, b.h, m1, p1, 0, p, p + 5, g, 0, out.h, sp),
+                     3 * s, out),
+        "jacobi": (lambda g: L.bfp_stencil_jacobi(x.h, b.h, c, 0, p, p + 5, g, out.h, sp), 3 * s, out),
+        "scal": (lambda g: L.bfp_scal(x.h, c, 0, p, p + 5, g, out.h, sp), 2 * s, out),
+        "axpby": (lambda g: L.bfp_axpby(x.h, y.h, p1, p1, 0, p, p + 5, g, 0, out.h, sp), 3 * s, out),
+        "restrict": (lambda g: L.bfp_restrict_fw(x.h, 0, p, p + 5, g, outc.h, sp),
+                     (1 + 2.0 ** -d) * s, outc),
+        "prolong": (lambda g: L.bfp_prolong(xc.h, 0, p, p + 5, g, out.h, sp), (1 + 2.0 ** -d) * s, out),
+        "prolong_correct": (lambda g: L.bfp_prolong_correct(xc.h, y.h, 0, p, p + 5, g, out.h, sp),
+                            (2 + 2.0 ** -d) * s, out),
+    }
+    peak, _ = peaks()
+    res = {}
+    for name, (fn, bpd, o) in ops.items():
+        assert fn(G) == 0
+        g = B.inf_norm_upper(o).c()
+        for _ in range(3):
+            assert fn(g) == 0
+        B.set_kernel_path(skip_recompute=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            fn(g)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        B.set_kernel_path()
+        ms = e0.elapsed_time(e1) / steps
+        assert not (o.header().flags & B.FLAG_RECOMPUTED), name
+        res[name] = {"kernel_ms": ms, "bytes_per_dof": bpd,
+                     "hbm_frac": bpd * n / (ms / 1e3) / 1e9 / peak}
+    return {"config": f"{d}-D level {l} int32 p={p}", "dof": n, "ops": res}
+
+
 SOLVES = {
     # x, b at 16 bits; residual + V-cycle (wdot) at 28 bits, w_add capped at 4 (int32)
     "C1_1d_vcycles": dict(d=1, l_fine=20, cycles=10, x0_random=True, rhs_kind=0, p=16,
@@ -581,7 +661,42 @@ SOLVES = {
                           nonnormalized=True,
                           p=[0, 0, 0] + [4 + 2 * (l - 3) for l in range(3, 32)][:29]),
     "C4_3d_fmg": dict(d=3, l_fine=9, cycles=1, rhs_kind=1, fmg=True, p=24),
+    # FMG with two IR-V(2,2) per level: the smallest n_ir that reaches the discretisation
+    # error in max norm (alg_over_disc <= 1; one per level leaves 5x): time to disc. accuracy
+    "C4_3d_fmg_n2": dict(d=3, l_fine=9, cycles=2, rhs_kind=1, fmg=True, p=24),
 }
+
+
+def sine_accuracy(d, l, m, e):
+    """Max-norm errors of a solve with the sine right-hand side f = d pi^2 prod sin(pi x):
+    the discrete solution is u_h = (d pi^2 / lambda_h) u with
+    lambda_h = d 4 h^-2 sin^2(pi h / 2) (the sampled sine is an eigenvector of the
+    stencil), so the discretisation error and the solver's distance to u_h are exact
+    up to the rhs quantisation.  Blockwise over the slowest axis (host memory)."""
+    import numpy as np
+    n = (1 << l) - 1
+    h = 2.0 ** -l
+    s = np.sin(np.pi * (np.arange(1, n + 1) * h))
+    lam = d * 4.0 / (h * h) * np.sin(np.pi * h / 2) ** 2
+    c = d * np.pi ** 2 / lam
+    per = n ** (d - 1)
+    inner = np.ones(1)
+    for _ in range(d - 1):
+        inner = np.multiply.outer(inner, s).reshape(-1) if inner.size > 1 else s.copy()
+    if d == 1:
+        inner = np.ones(1)
+    err_h = err_u = 0.0
+    for k in range(n):
+        u = s[k] * inner if d > 1 else s
+        xv = np.ldexp(m[k * per:(k + 1) * per].astype(np.float64), e) if d > 1 else \
+            np.ldexp(m.astype(np.float64), e)
+        err_h = max(err_h, float(np.max(np.abs(xv - c * u))))
+        err_u = max(err_u, float(np.max(np.abs(xv - u))))
+        if d == 1:
+            break
+    disc = abs(1.0 - c)  # max |u - u_h| (max |u| = 1 at the grid point nearest 1/2)
+    return {"err_vs_discrete": err_h, "err_vs_continuous": err_u, "disc_err": disc,
+            "alg_over_disc": err_h / disc}
 
 
 def run_solves(B, torch, stream):
@@ -605,6 +720,8 @@ def run_solves(B, torch, stream):
             rec = sum(t[8] for t in tr)
             out[name] = {"ms": ms, "launches": mg.launches(), "final_residual": hist[-1],
                          "first_residual": hist[0], "recomputes": rec, "ops": len(tr)}
+            if kw.get("rhs_kind") == 1:
+                out[name]["accuracy"] = sine_accuracy(kw["d"], kw["l_fine"], x, e)
             del mg
         except Exception as ex:  # report, never hide
             out[name] = {"error": str(ex)}

@@ -544,21 +544,74 @@ __device__ __forceinline__ A prolong_at(const Vec& xc, int64_t sc, int dim, int 
   return line(c0 + b0) + line(c0 + b1) + line(c1 + b0) + line(c1 + b1);
 }
 
+// coarse taps of 4 consecutive fine points along x (i0 even): c[I0-1], c[I0], c[I0+1]
+template <bool NC>
+__device__ __forceinline__ void prolong_xline(const int32_t* c, int sh, int t[4]) {
+  const int a = ldx<NC>(c - 1) >> sh, b = ldx<NC>(c) >> sh, e = ldx<NC>(c + 1) >> sh;
+  t[0] = a + b;
+  t[1] = 2 * b;
+  t[2] = b + e;
+  t[3] = 2 * e;
+}
+// g = P xc at 4 consecutive fine points (int32 storage, |g| < 2^31 by the width bound)
+template <bool NC>
+__device__ __forceinline__ void prolong4_32(const Vec& xc, int sh, int dim, int l, int zp,
+                                            int64_t o, int g[4]) {
+  const int64_t Nf = (int64_t)1 << l, mf = Nf - 1, Nc = Nf >> 1;
+  const int64_t i0 = o & mf;
+  const int32_t* cb = (const int32_t*)xc.data + (i0 >> 1);
+  int t[4];
+  g[0] = g[1] = g[2] = g[3] = 0;
+  if (dim == 1) {
+    prolong_xline<NC>(cb, sh, g);
+    return;
+  }
+  const int64_t j = dim == 2 ? (o >> l) + zp : (o >> l) & mf;
+  const int64_t r0 = ((j - 1) >> 1) * Nc, r1 = (j >> 1) * Nc;
+  int64_t p0 = 0, p1 = 0;
+  if (dim >= 3) {
+    const int64_t k = (o >> (2 * l)) + zp;
+    p0 = ((k - 1) >> 1) * Nc * Nc;
+    p1 = (k >> 1) * Nc * Nc;
+  }
+  const int np = dim >= 3 ? 2 : 1;
+  for (int pz = 0; pz < np; ++pz) {
+    const int64_t pb = pz ? p1 : p0;
+    prolong_xline<NC>(cb + pb + r0, sh, t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) g[q] += t[q];
+    prolong_xline<NC>(cb + pb + r1, sh, t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) g[q] += t[q];
+  }
+}
+
 // fine z = P xc  (EspmvKernel with P, m_P = 2^d, e_P = -d, q_P = d+2)
 struct ProlongOp {
   Vec xc;
   int dim, l;  // fine level
   int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
   int64_t sc;
+  bool narrow;  // int32 storage and |P xc| < 2^31: vectorised coarse rows
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = -dim + xc.hdr->e;
     sc = xc.hdr->shift;
     need = eff_bits(xc.hdr) + dim + 2;
+    narrow = need <= 31 && sc < 32;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
     pad4(dim, l, o, pad, zf);
+    if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
+      if (narrow) {
+        int g[4];
+        prolong4_32<NC>(xc, (int)sc, dim, l, zp, o, g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) z[q] = pad[q] ? 0 : (int64_t)g[q];
+        return;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j, zp);
@@ -585,48 +638,14 @@ struct ProlongCorrectOp {
     swap = d < 0;
     P = narrow ? (1 << (int)ad) : 0;
   }
-  // coarse taps of 4 consecutive fine points along x (i0 even): c[I0-1], c[I0], c[I0+1]
-  template <bool NC>
-  __device__ __forceinline__ void xline(const int32_t* c, int sh, int t[4]) const {
-    const int a = ldx<NC>(c - 1) >> sh, b = ldx<NC>(c) >> sh, e = ldx<NC>(c + 1) >> sh;
-    t[0] = a + b;
-    t[1] = 2 * b;
-    t[2] = b + e;
-    t[3] = 2 * e;
-  }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
     bool pad[4];
     pad4(dim, l, o, pad, zf);
     if constexpr (sizeof(M) == 4 && sizeof(A) == 8) {
       if (narrow) {
-        const int64_t Nf = (int64_t)1 << l, mf = Nf - 1, Nc = Nf >> 1;
-        const int64_t i0 = o & mf;
-        const int32_t* cb = (const int32_t*)ec.data + (i0 >> 1);
-        const int sh = (int)sc;
-        int g[4] = {0, 0, 0, 0}, t[4];
-        if (dim == 1) {
-          xline<NC>(cb, sh, g);
-        } else {
-          const int64_t j = dim == 2 ? (o >> l) + zp : (o >> l) & mf;
-          const int64_t r0 = ((j - 1) >> 1) * Nc, r1 = (j >> 1) * Nc;
-          int64_t p0 = 0, p1 = 0;
-          if (dim >= 3) {
-            const int64_t k = (o >> (2 * l)) + zp;
-            p0 = ((k - 1) >> 1) * Nc * Nc;
-            p1 = (k >> 1) * Nc * Nc;
-          }
-          const int np = dim >= 3 ? 2 : 1;
-          for (int pz = 0; pz < np; ++pz) {
-            const int64_t pb = pz ? p1 : p0;
-            xline<NC>(cb + pb + r0, sh, t);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) g[q] += t[q];
-            xline<NC>(cb + pb + r1, sh, t);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) g[q] += t[q];
-          }
-        }
+        int g[4];
+        prolong4_32<NC>(ec, (int)sc, dim, l, zp, o, g);
         int yv[4];
         V4<int32_t, NC>::load32(y, o, (int)sy, yv);
 #pragma unroll

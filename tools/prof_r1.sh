@@ -1,0 +1,22 @@
+# round-1 profile captures (run under gpurun; each ncu only after its plain run exited 0)
+# usage: bash tools/prof_r1.sh bench|c4|c5
+set -x
+case "$1" in
+bench)
+  python bench.py --steps 30 --warmup 5 > gpurun_out/b6.json 2> gpurun_out/b6.err || exit 1
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/r1_launches_bench.csv \
+    python bench.py --steps 20 --warmup 3 --no-extras --no-cpu > gpurun_out/ncu_launch.log 2>&1
+  ncu --set full --import-source on --clock-control none -k regex:bulk_win_kernel -s 6 -c 2 \
+    -o gpurun_out/r1_c2_bulk python bench.py --steps 20 --warmup 3 --no-extras --no-cpu \
+    > gpurun_out/ncu_c2.log 2>&1 ;;
+c4)
+  python tools/resid_once.py 3 9 24 4 || exit 1
+  ncu --set full --import-source on --clock-control none -k regex:bulk3 -s 2 -c 2 \
+    -o gpurun_out/r1_c4_bulk3 python tools/resid_once.py 3 9 24 4 > gpurun_out/ncu_c4.log 2>&1 ;;
+c5)
+  python tools/resid_once.py 3 10 48 8 || exit 1
+  ncu --set full --clock-control none -k regex:bulk3 -s 2 -c 1 \
+    -o gpurun_out/r1_c5_bulk3 python tools/resid_once.py 3 10 48 8 > gpurun_out/ncu_c5b.log 2>&1 ;;
+esac
+ls -la gpurun_out
