@@ -597,7 +597,7 @@ def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
             "kernel_ms": kern_ms, "hbm_frac": 3 * mb * n / (kern_ms / 1e3) / 1e9 / peak}
 
 
-def measure_ops(B, torch, stream, d, l, p, steps=20):
+def measure_ops(B, torch, stream, d, l, p, steps=20, only=None):
     """Every fine-level op of the V-cycle / FMG on one config's finest level (inputs
     resident, gamma at the exact binade so qcomp takes the fast path): pass-1 kernel
     time (recompute launch skipped, flags verified) and its fraction of the measured
@@ -632,6 +632,8 @@ def measure_ops(B, torch, stream, d, l, p, steps=20):
     peak, _ = peaks()
     res = {}
     for name, (fn, bpd, o) in ops.items():
+        if only and name != only:
+            continue
         assert fn(G) == 0
         g = B.inf_norm_upper(o).c()
         for _ in range(3):

@@ -23,7 +23,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libbfpmg_b200.so")
+LIB_PATH = os.environ.get("BFPMG_LIB") or os.path.join(HERE, "_lib", "libbfpmg_b200.so")  # A/B builds
 REPO = os.path.dirname(HERE)
 
 # status codes (include/bfpmg_b200.h)

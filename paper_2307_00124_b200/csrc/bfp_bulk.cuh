@@ -7,7 +7,9 @@
 // ring of mbarriers with complete_tx; the consumers wait on the mbarrier of the
 // step, read their 4 points and the 3-row neighbourhood from shared memory,
 // and write one int4.  Bytes in flight are bounded by shared memory (D steps
-// of (W+8)+W words per CTA), not by registers.
+// of (W+8)+W words per CTA), not by registers.  Slots are handed back through
+// "empty" mbarriers (one arrival per warp) instead of a block-wide barrier, so
+// only the producer waits for the slowest warp and the others run ahead.
 #pragma once
 #include "bfp_dev.cuh"
 
@@ -27,6 +29,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -56,7 +61,8 @@ constexpr int kBulkD = 4;               // prefetch depth (steps in flight)
 constexpr int kBulkXS = kBulkD + 3;     // x-row slots
 constexpr int kBulkYS = kBulkD + 1;     // y-row slots / mbarriers
 constexpr int kBulkXW = kBulkW + 8;     // x slot width (4-word halo each side)
+// full barriers (tx completion) and empty barriers (one arrival per consumer warp)
 constexpr size_t kBulkSmem =
-    (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4 + kBulkYS * 8 + 64;
+    (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4 + 2 * kBulkYS * 8 + 64;
 
 }  // namespace bfpdev

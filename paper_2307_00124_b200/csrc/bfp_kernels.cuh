@@ -364,7 +364,10 @@ __global__ void __launch_bounds__(kThreads, DIM == 2 ? 3 : 2) march_win_kernel(O
 // ---------------------------------------------------------------------------
 // 2-D stencil ops through the bulk-async shared-memory pipeline (bfp_bulk.cuh)
 
-template <int MODE, bool SHIFT, bool SWAP, typename Op>
+// FW: the fast window of the common case -- pass 1 / recompute storing
+// floor(z / 2^rs) with 0 <= rs < 32 and no left shift: the stored int32 is the low word
+// of the shifted 64-bit row, one funnel shift (no range selects)
+template <int MODE, bool SHIFT, bool SWAP, bool FW, typename Op>
 __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r, int R, char* smem) {
   const int l = out.l;
@@ -375,6 +378,7 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
   int32_t* xsl = reinterpret_cast<int32_t*>(smem);                 // kBulkXS x (W+8)
   int32_t* ysl = xsl + kBulkXS * kBulkXW;                           // kBulkYS x W
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kBulkYS * kBulkW);
+  uint64_t* ebar = bar + kBulkYS;  // empty: all warps done with the step's freed slots
   const int32_t* X = (const int32_t*)op.sv().data;
   const int32_t* Y = (const int32_t*)op.yv2().data;
   int32_t* O = (int32_t*)out.data;
@@ -384,7 +388,8 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
   const uint32_t tx_bytes = (uint32_t)(kBulkXW + kBulkW) * 4;
-  uint32_t parity = 0;  // bit k: phase parity of bar[k]
+  uint32_t parity = 0;   // bit k: phase parity of bar[k]
+  uint32_t eparity = 0;  // bit k: phase parity of ebar[k]
   for (int item = blockIdx.x; item < strips * chunks; item += gridDim.x) {
     const int strip = item % strips, ch = item / strips;
     const int64_t c0 = (int64_t)strip * kBulkW;
@@ -442,7 +447,10 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
         int64_t z = op.template point_t<SWAP>(g, C[k], Yv[k]);
         if (k == 3 && xpad) z = 0;
         if (rowpad) z = 0;
-        if (MODE == MODE_NNQ) {
+        if constexpr (FW) {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[k] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+        } else if (MODE == MODE_NNQ) {
           tt[k] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
         } else {
           if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
@@ -458,11 +466,16 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       sc = sn;
       sn = sn + 1 == kBulkXS ? 0 : sn + 1;
       sy_ = sy_ + 1 == kBulkYS ? 0 : sy_ + 1;
-      __syncthreads();  // slots of x row j-1 and y row j are free
+      // this warp is done with x row j-1 and y row j
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ebar[free_y]);
+      const uint32_t ep = (eparity >> free_y) & 1u;
+      eparity ^= 1u << free_y;
       if (t == 0 && s + kBulkD + 1 < rows) {
         // next group: x row tr+1 -> slot (j-1) % XS, y row tr -> slot j % YS, tr = j+D+1
         const int64_t tr = j + kBulkD + 1;
         uint64_t* bb = &bar[free_y];
+        mbar_wait(&ebar[free_y], ep);  // every warp has finished step j
         fence_proxy_async_smem();
         mbar_expect_tx(bb, tx_bytes);
         bulk_g2s(xsl + free_x * kBulkXW, xsrc(tr + 1), kBulkXW * 4, bb);
@@ -490,19 +503,33 @@ __global__ void __launch_bounds__(kBulkT, 4) bulk_win_kernel(Op op, Vec out, Win
   if (op.narrow && need <= 63) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4);
     if (threadIdx.x == 0) {
-      for (int k = 0; k < kBulkYS; ++k) mbar_init(&bar[k], 1);
+      for (int k = 0; k < kBulkYS; ++k) {
+        mbar_init(&bar[k], 1);
+        mbar_init(&bar[kBulkYS + k], kBulkT / 32);
+      }
       mbar_fence_init();
     }
     __syncthreads();
     const bool sh = (op.shs() | op.shy()) != 0, sw = op.swapped();
-    if (!sh && !sw)
-      bulk_loop<MODE, false, false>(op, out, p, c, r, R, smem);
-    else if (sh && !sw)
-      bulk_loop<MODE, true, false>(op, out, p, c, r, R, smem);
-    else if (!sh)
-      bulk_loop<MODE, false, true>(op, out, p, c, r, R, smem);
-    else
-      bulk_loop<MODE, true, true>(op, out, p, c, r, R, smem);
+    const bool fw = MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32;
+    if (fw) {
+      if (!sh && !sw)
+        bulk_loop<MODE, false, false, true>(op, out, p, c, r, R, smem);
+      else if (sh && !sw)
+        bulk_loop<MODE, true, false, true>(op, out, p, c, r, R, smem);
+      else if (!sh)
+        bulk_loop<MODE, false, true, true>(op, out, p, c, r, R, smem);
+      else
+        bulk_loop<MODE, true, true, true>(op, out, p, c, r, R, smem);
+    } else if (!sh && !sw) {
+      bulk_loop<MODE, false, false, false>(op, out, p, c, r, R, smem);
+    } else if (sh && !sw) {
+      bulk_loop<MODE, true, false, false>(op, out, p, c, r, R, smem);
+    } else if (!sh) {
+      bulk_loop<MODE, false, true, false>(op, out, p, c, r, R, smem);
+    } else {
+      bulk_loop<MODE, true, true, false>(op, out, p, c, r, R, smem);
+    }
   } else {
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
   }
@@ -682,13 +709,19 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
 // streams the (H3+2) x (W3+8) x tile of plane k+1+D (y and x halos included) and
 // the H3 x W3 y tile of plane k+D, one bulk copy per row issued by the lanes of
 // warp 0, into rings of plane slots signalled by mbarriers.
+#ifndef BFP_B3_EMPTY  // A/B switch: empty mbarriers (1) or a block barrier (0) per step
+#define BFP_B3_EMPTY 0
+#endif
+#ifndef BFP_B3_MINB  // resident CTAs per SM the int32 instantiation is compiled for
+#define BFP_B3_MINB 4
+#endif
 constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
 constexpr int kB3D = 3;                                       // planes in flight
 constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
 constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
 constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // elements per tile
 template <typename T> constexpr size_t b3_smem() {
-  return (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T) + kB3YS * 8 + 64;
+  return (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T) + 2 * kB3YS * 8 + 64;
 }
 
 // 4 consecutive elements of a shared-memory tile (16-B aligned)
@@ -724,7 +757,7 @@ template <typename V> __device__ __forceinline__ V shfl_dn1(V v) {
 
 // T = storage type, A = accumulator of the exact rows (int64 narrow for int32
 // storage; int64 or __int128 through the ops' generic combine for int64 storage)
-template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, typename Op>
+template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, bool FW = false, typename Op>
 __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const WinParams& p,
                                            const WinCtx& c, Red& r, int R, char* smem) {
   using V = typename S4<T>::V;
@@ -736,6 +769,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   T* xsl = reinterpret_cast<T*>(smem);
   T* ysl = xsl + kB3XS * kB3XT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kB3YS * kB3YT);
+  uint64_t* ebar = bar + kB3YS;  // empty: all warps done with the step's freed slots
   const T* X = (const T*)op.sv().data;
   const T* Y = (const T*)op.yv2().data;
   T* O = (T*)out.data;
@@ -745,7 +779,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
   const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * sizeof(T);
-  uint32_t parity = 0;
+  uint32_t parity = 0, eparity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
     const int64_t x0 = (int64_t)(tile % tx) * kB3W, y0 = (int64_t)(tile / tx) * kB3H;
@@ -816,7 +850,10 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         }
         if (q == 3 && xpad) z = 0;
         if (rowpad) z = 0;
-        if (MODE == MODE_NNQ) {
+        if constexpr (FW && sizeof(T) == 4) {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = (T)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+        } else if (MODE == MODE_NNQ) {
           tt[q] = (T)shift_clamp<A>(z, c.lam, p.w_out);
         } else {
           if (MODE == MODE_QCOMP) or_mag<A>(z, olo, ohi);
@@ -831,8 +868,20 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
       sc = sn;
       sn = sn + 1 == kB3XS ? 0 : sn + 1;
       sy_ = sy_ + 1 == kB3YS ? 0 : sy_ + 1;
+#if BFP_B3_EMPTY
+      // this warp is done with x plane k-1 and y plane k
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ebar[free_y]);
+      const uint32_t ep = (eparity >> free_y) & 1u;
+      eparity ^= 1u << free_y;
+      if (wy == 0 && s + kB3D + 1 < planes) {
+        mbar_wait(&ebar[free_y], ep);  // every warp has finished step k
+#else
+      (void)ebar;
+      (void)eparity;
       __syncthreads();  // slots of plane k-1 (x) and plane k (y) are free
       if (wy == 0 && s + kB3D + 1 < planes) {
+#endif
         fence_proxy_async_smem();
         const int64_t tk = k + kB3D + 1;  // x plane tk+1 -> slot free_x, y plane tk -> free_y
         issue(tk + 1, free_x, tk, free_y, &bar[free_y], false);
@@ -847,7 +896,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
 }
 
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? 4 : 2)
+__global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
     bulk3_win_kernel(Op op, Vec out, WinParams p, int R) {
   extern __shared__ __align__(128) char smem[];
   griddep_wait();
@@ -861,21 +910,35 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? 4 : 2)
   if (fast) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T));
     if (threadIdx.x == 0) {
-      for (int k = 0; k < kB3YS; ++k) mbar_init(&bar[k], 1);
+      for (int k = 0; k < kB3YS; ++k) {
+        mbar_init(&bar[k], 1);
+        mbar_init(&bar[kB3YS + k], kB3T / 32);
+      }
       mbar_fence_init();
     }
     __syncthreads();
     const bool sh = (op.shs() | op.shy()) != 0;
     if constexpr (sizeof(T) == 4) {
       const bool sw = op.swapped();
-      if (!sh && !sw)
+      const bool fw = MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32;
+      if (fw) {
+        if (!sh && !sw)
+          bulk3_loop<MODE, false, false, T, int64_t, true>(op, out, p, c, r, R, smem);
+        else if (sh && !sw)
+          bulk3_loop<MODE, true, false, T, int64_t, true>(op, out, p, c, r, R, smem);
+        else if (!sh)
+          bulk3_loop<MODE, false, true, T, int64_t, true>(op, out, p, c, r, R, smem);
+        else
+          bulk3_loop<MODE, true, true, T, int64_t, true>(op, out, p, c, r, R, smem);
+      } else if (!sh && !sw) {
         bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem);
-      else if (sh && !sw)
+      } else if (sh && !sw) {
         bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem);
-      else if (!sh)
+      } else if (!sh) {
         bulk3_loop<MODE, false, true, T, int64_t>(op, out, p, c, r, R, smem);
-      else
+      } else {
         bulk3_loop<MODE, true, true, T, int64_t>(op, out, p, c, r, R, smem);
+      }
     } else {
       if (need <= 63) {
         if (sh)

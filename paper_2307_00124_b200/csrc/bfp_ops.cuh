@@ -431,6 +431,7 @@ struct AxpbyOp {
 };
 
 // coarse z = R r, full weighting R = (1,2,1)^{(x)d} 2^{-2d}  (EspmvKernel)
+
 struct RestrictOp {
   Vec r;       // fine, level l
   int dim, l;  // fine level
@@ -585,6 +586,7 @@ __device__ __forceinline__ void prolong4_32(const Vec& xc, int sh, int dim, int 
     for (int q = 0; q < 4; ++q) g[q] += t[q];
   }
 }
+
 
 // fine z = P xc  (EspmvKernel with P, m_P = 2^d, e_P = -d, q_P = d+2)
 struct ProlongOp {
