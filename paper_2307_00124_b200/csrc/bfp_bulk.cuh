@@ -55,9 +55,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-constexpr int kBulkT = 256;             // threads per CTA (one 4-group each)
+#ifndef BFP_BULK_T
+#define BFP_BULK_T 256
+#endif
+#ifndef BFP_B2_MINB  // resident CTAs per SM the 2-D pipeline is compiled for
+#define BFP_B2_MINB 4
+#endif
+constexpr int kBulkT = BFP_BULK_T;      // threads per CTA (one 4-group each)
 constexpr int kBulkW = 4 * kBulkT;      // strip width in columns
-constexpr int kBulkD = 4;               // prefetch depth (steps in flight)
+#ifndef BFP_BULK_D
+#define BFP_BULK_D 2
+#endif
+#ifndef BFP_B2_EMPTY  // A/B switch: empty mbarriers (1) or a block barrier (0) per step
+#define BFP_B2_EMPTY 1
+#endif
+constexpr int kBulkD = BFP_BULK_D;      // prefetch depth (steps in flight)
 constexpr int kBulkXS = kBulkD + 3;     // x-row slots
 constexpr int kBulkYS = kBulkD + 1;     // y-row slots / mbarriers
 constexpr int kBulkXW = kBulkW + 8;     // x slot width (4-word halo each side)

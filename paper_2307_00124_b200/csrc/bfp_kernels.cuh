@@ -466,16 +466,23 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       sc = sn;
       sn = sn + 1 == kBulkXS ? 0 : sn + 1;
       sy_ = sy_ + 1 == kBulkYS ? 0 : sy_ + 1;
+#if BFP_B2_EMPTY
       // this warp is done with x row j-1 and y row j
       __syncwarp();
       if (lane == 0) mbar_arrive(&ebar[free_y]);
       const uint32_t ep = (eparity >> free_y) & 1u;
       eparity ^= 1u << free_y;
       if (t == 0 && s + kBulkD + 1 < rows) {
+        mbar_wait(&ebar[free_y], ep);  // every warp has finished step j
+#else
+      (void)ebar;
+      (void)eparity;
+      __syncthreads();  // slots of x row j-1 and y row j are free
+      if (t == 0 && s + kBulkD + 1 < rows) {
+#endif
         // next group: x row tr+1 -> slot (j-1) % XS, y row tr -> slot j % YS, tr = j+D+1
         const int64_t tr = j + kBulkD + 1;
         uint64_t* bb = &bar[free_y];
-        mbar_wait(&ebar[free_y], ep);  // every warp has finished step j
         fence_proxy_async_smem();
         mbar_expect_tx(bb, tx_bytes);
         bulk_g2s(xsl + free_x * kBulkXW, xsrc(tr + 1), kBulkXW * 4, bb);
@@ -491,7 +498,7 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
 }
 
 template <int MODE, typename Op>
-__global__ void __launch_bounds__(kBulkT, 4) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
+__global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
   griddep_wait();
   extern __shared__ __align__(128) char smem[];
   int64_t need = 0;
@@ -716,7 +723,10 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
 #define BFP_B3_MINB 4
 #endif
 constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
-constexpr int kB3D = 3;                                       // planes in flight
+#ifndef BFP_B3_D
+#define BFP_B3_D 3
+#endif
+constexpr int kB3D = BFP_B3_D;                                // planes in flight
 constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
 constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
 constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // elements per tile
