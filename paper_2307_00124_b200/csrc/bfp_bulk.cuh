@@ -11,6 +11,8 @@
 // "empty" mbarriers (one arrival per warp) instead of a block-wide barrier, so
 // only the producer waits for the slowest warp and the others run ahead.
 #pragma once
+#include <cuda.h>  // CUtensorMap (tiled TMA descriptors; encoded through the runtime's driver entry point)
+
 #include "bfp_dev.cuh"
 
 namespace bfpdev {
@@ -61,6 +63,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #ifndef BFP_B2_MINB  // resident CTAs per SM the 2-D pipeline is compiled for
 #define BFP_B2_MINB 4
 #endif
+// 3-D tiled TMA: box at tensor coordinates (c0, c1, c2) -> shared, completes tx on bar
+__device__ __forceinline__ void tma_g2s_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                           int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 constexpr int kBulkT = BFP_BULK_T;      // threads per CTA (one 4-group each)
 constexpr int kBulkW = 4 * kBulkT;      // strip width in columns
 #ifndef BFP_BULK_D

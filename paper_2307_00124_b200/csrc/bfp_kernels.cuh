@@ -730,9 +730,19 @@ constexpr int kB3D = BFP_B3_D;                                // planes in fligh
 constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
 constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
 constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // elements per tile
-template <typename T> constexpr size_t b3_smem() {
-  return (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T) + 2 * kB3YS * 8 + 64;
+// x-plane slots padded to 128 B (TMA destinations), 128 B of slack to align the base
+template <typename T> constexpr int b3_xtp() {
+  return (int)(((kB3XT * sizeof(T) + 127) / 128 * 128) / sizeof(T));
 }
+template <typename T> constexpr size_t b3_smem() {
+  return (size_t)(kB3XS * b3_xtp<T>() + kB3YS * kB3YT) * sizeof(T) + 2 * kB3YS * 8 + 128 + 64;
+}
+// the x / y operands of a 3-D pipeline launch as tiled TMA descriptors: tensor
+// (x, y, plane) over the whole allocation (2 halo planes each side), boxes of one
+// x tile ((W+8) x (H+2)) and one y tile (W x H); out-of-range boxes fill zeros
+struct B3Maps {
+  CUtensorMap x, y;
+};
 
 // 4 consecutive elements of a shared-memory tile (16-B aligned)
 template <typename T> struct S4;
@@ -769,7 +779,9 @@ template <typename V> __device__ __forceinline__ V shfl_dn1(V v) {
 // storage; int64 or __int128 through the ops' generic combine for int64 storage)
 template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, bool FW = false, typename Op>
 __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const WinParams& p,
-                                           const WinCtx& c, Red& r, int R, char* smem) {
+                                           const WinCtx& c, Red& r, int R, char* smem,
+                                           const CUtensorMap* tmx, const CUtensorMap* tmy) {
+  constexpr int XTP = b3_xtp<T>();
   using V = typename S4<T>::V;
   const int l = out.l;
   const int64_t N = (int64_t)1 << l, N2 = N * N;
@@ -777,11 +789,9 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   const int tx = (int)(N / kB3W), ty = (int)(N / kB3H);
   const int chunks = (int)((NZ + R - 1) / R);
   T* xsl = reinterpret_cast<T*>(smem);
-  T* ysl = xsl + kB3XS * kB3XT;
+  T* ysl = xsl + kB3XS * XTP;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kB3YS * kB3YT);
   uint64_t* ebar = bar + kB3YS;  // empty: all warps done with the step's freed slots
-  const T* X = (const T*)op.sv().data;
-  const T* Y = (const T*)op.yv2().data;
   T* O = (T*)out.data;
   const int sx = SHIFT ? op.shs() : 0, sy = SHIFT ? op.shy() : 0;
   const int t = threadIdx.x, lane = t & 31, wy = t >> 5;  // row of the tile
@@ -795,27 +805,21 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
     const int64_t x0 = (int64_t)(tile % tx) * kB3W, y0 = (int64_t)(tile / tx) * kB3H;
     const int64_t k0 = (int64_t)ch * R;
     const int planes = (int)std::min<int64_t>(R, NZ - k0);
-    // x plane kp (rows y0-1 .. y0+H3) and y plane ky on barrier b; `first` also streams
-    // x planes kp-2, kp-1 (the start of a march) on the same barrier
+    // x plane kp (rows y0-1 .. y0+H3, columns x0-4 .. x0+W+3) and y plane ky on barrier
+    // b, one tiled TMA box each (tensor plane = local plane + 2 halo planes); `first`
+    // also streams x planes kp-2, kp-1 (the start of a march) on the same barrier
     auto issue = [&](int64_t kp, int xslot, int64_t ky, int yslot, uint64_t* b, bool first) {
-      if (lane == 0) mbar_expect_tx(b, tx_bytes + (first ? 2u * kB3XT * sizeof(T) : 0u));
-      __syncwarp();
-      auto xrow = [&](int64_t k, int slot) {
-        bulk_g2s(xsl + slot * kB3XT + lane * kB3XW,
-                 X + (k > NZ ? NZ : k) * N2 + (y0 - 1 + lane) * N + x0 - 4,
-                 kB3XW * (int)sizeof(T), b);
+      if (lane != 0) return;
+      mbar_expect_tx(b, tx_bytes + (first ? 2u * kB3XT * sizeof(T) : 0u));
+      auto xbox = [&](int64_t k, int slot) {
+        tma_g2s_3d(xsl + slot * XTP, tmx, (int)x0 - 4, (int)y0 - 1, (int)((k > NZ ? NZ : k) + 2), b);
       };
-      if (lane < kB3XR) {
-        xrow(kp, xslot);
-        if (first) {
-          xrow(kp - 2, (int)((kp - 2 + kB3XS) % kB3XS));
-          xrow(kp - 1, (int)((kp - 1 + kB3XS) % kB3XS));
-        }
-      } else if (lane < kB3XR + kB3H) {
-        bulk_g2s(ysl + yslot * kB3YT + (lane - kB3XR) * kB3W,
-                 Y + (ky > NZ ? NZ : ky) * N2 + (y0 + lane - kB3XR) * N + x0,
-                 kB3W * (int)sizeof(T), b);
+      xbox(kp, xslot);
+      if (first) {
+        xbox(kp - 2, (int)((kp - 2 + kB3XS) % kB3XS));
+        xbox(kp - 1, (int)((kp - 1 + kB3XS) % kB3XS));
       }
+      tma_g2s_3d(ysl + yslot * kB3YT, tmy, (int)x0, (int)y0, (int)((ky > NZ ? NZ : ky) + 2), b);
     };
     if (wy == 0) {
       fence_proxy_async_smem();
@@ -833,13 +837,13 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
       mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
       parity ^= 1u << sy_;
       const int off = (wy + 1) * kB3XW + 4 + 4 * lane;
-      const T* xc = xsl + sc * kB3XT + off;
+      const T* xc = xsl + sc * XTP + off;
       V C[4], u[4], dn[4], zp[4], zn[4], Yv[4];
       S4<T>::ld(xc, sx, C);
       S4<T>::ld(xc - kB3XW, sx, u);
       S4<T>::ld(xc + kB3XW, sx, dn);
-      S4<T>::ld(xsl + sp * kB3XT + off, sx, zp);
-      S4<T>::ld(xsl + sn * kB3XT + off, sx, zn);
+      S4<T>::ld(xsl + sp * XTP + off, sx, zp);
+      S4<T>::ld(xsl + sn * XTP + off, sx, zn);
       S4<T>::ld(ysl + sy_ * kB3YT + wy * kB3W + 4 * lane, sy, Yv);
       const V lf0 = (V)(xc[-1] >> sx), rt0 = (V)(xc[4] >> sx);
       V lf = shfl_up1(C[3]), rt = shfl_dn1(C[0]);
@@ -907,8 +911,9 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
 
 template <int MODE, typename T, typename Op>
 __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
-    bulk3_win_kernel(Op op, Vec out, WinParams p, int R) {
-  extern __shared__ __align__(128) char smem[];
+    bulk3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ B3Maps tm) {
+  extern __shared__ __align__(128) char smem_raw[];
+  char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   griddep_wait();
   int64_t need = 0;
   WinCtx c;
@@ -918,7 +923,8 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
   r.init();
   const bool fast = sizeof(T) == 4 ? (op.narrow && need <= 63) : (op.w64 && need <= 127);
   if (fast) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * kB3XT + kB3YS * kB3YT) * sizeof(T));
+    uint64_t* bar =
+        reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * b3_xtp<T>() + kB3YS * kB3YT) * sizeof(T));
     if (threadIdx.x == 0) {
       for (int k = 0; k < kB3YS; ++k) {
         mbar_init(&bar[k], 1);
@@ -933,33 +939,33 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
       const bool fw = MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32;
       if (fw) {
         if (!sh && !sw)
-          bulk3_loop<MODE, false, false, T, int64_t, true>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, false, false, T, int64_t, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else if (sh && !sw)
-          bulk3_loop<MODE, true, false, T, int64_t, true>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, true, false, T, int64_t, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else if (!sh)
-          bulk3_loop<MODE, false, true, T, int64_t, true>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, false, true, T, int64_t, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else
-          bulk3_loop<MODE, true, true, T, int64_t, true>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, true, true, T, int64_t, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else if (!sh && !sw) {
-        bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem);
+        bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else if (sh && !sw) {
-        bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem);
+        bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else if (!sh) {
-        bulk3_loop<MODE, false, true, T, int64_t>(op, out, p, c, r, R, smem);
+        bulk3_loop<MODE, false, true, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else {
-        bulk3_loop<MODE, true, true, T, int64_t>(op, out, p, c, r, R, smem);
+        bulk3_loop<MODE, true, true, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       }
     } else {
       if (need <= 63) {
         if (sh)
-          bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else
-          bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else {
         if (sh)
-          bulk3_loop<MODE, true, false, T, i128>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, true, false, T, i128>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else
-          bulk3_loop<MODE, false, false, T, i128>(op, out, p, c, r, R, smem);
+          bulk3_loop<MODE, false, false, T, i128>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       }
     }
   } else {
@@ -1060,12 +1066,42 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
 }
 
 
+// tiled TMA descriptor of a 3-D grid vector (driver entry point through the runtime)
+static inline bool encode_b3(CUtensorMap* m, const Vec& v, int bw, int bh) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<EncodeFn>(f);
+  }
+  const uint64_t N = (uint64_t)1 << v.l, eb = (uint64_t)v.ebytes;
+  char* base = (char*)v.data - 2 * N * N * eb;  // two halo planes before plane 0
+  const cuuint64_t dims[3] = {N, N, (cuuint64_t)v.nz + 4};
+  const cuuint64_t strides[2] = {N * eb, N * N * eb};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, eb == 4 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 3, base,
+            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T, typename Op>
 static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0,
                                cudaStream_t s) {
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
+  B3Maps tm;
+  if (!encode_b3(&tm.x, op.sv(), kB3XW, kB3XR) || !encode_b3(&tm.y, op.yv2(), kB3W, kB3H))
+    return BFP_ERR_CUDA;
   const int64_t N = int64_t(1) << out->l;
   constexpr size_t smem = b3_smem<T>();
   static int occ = 0;
@@ -1084,11 +1120,11 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(bulk3_win_kernel<MODE_QCOMP, T, Op>, b, kB3T, smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_QCOMP, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(bulk3_win_kernel<MODE_NNQ, T, Op>, b, kB3T, smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_NNQ, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     else
-      launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R);
+      launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     count_launch();
   };
   if (g_prof) {

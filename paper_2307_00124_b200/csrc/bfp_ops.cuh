@@ -247,8 +247,8 @@ struct GemvOp {
     Q = (int)qm;
   }
   // march-kernel interface (narrow, int32 storage)
-  __device__ __forceinline__ const Vec& sv() const { return x; }
-  __device__ __forceinline__ const Vec& yv2() const { return y; }
+  __host__ __device__ __forceinline__ const Vec& sv() const { return x; }
+  __host__ __device__ __forceinline__ const Vec& yv2() const { return y; }
   __device__ __forceinline__ int shs() const { return (int)sx; }
   __device__ __forceinline__ int shy() const { return (int)sy; }
   __device__ __forceinline__ int64_t point(int g, int c, int yv) const {
@@ -329,8 +329,8 @@ struct JacobiOp {
     P1 = narrow ? (neg1 ? (1 << (int)(-d1)) : -(1 << (int)d1)) : 0;
     s2 = narrow ? (int)d2 : 0;
   }
-  __device__ __forceinline__ const Vec& sv() const { return x; }
-  __device__ __forceinline__ const Vec& yv2() const { return b; }
+  __host__ __device__ __forceinline__ const Vec& sv() const { return x; }
+  __host__ __device__ __forceinline__ const Vec& yv2() const { return b; }
   __device__ __forceinline__ int shs() const { return (int)sx; }
   __device__ __forceinline__ int shy() const { return (int)sb; }
   __device__ __forceinline__ int64_t rterm(int g, int bv) const {
