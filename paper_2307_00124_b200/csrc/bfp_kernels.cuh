@@ -854,6 +854,16 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const V left = q == 0 ? lf : C[q - 1], right = q == 3 ? rt : C[q + 1];
+        if constexpr (sizeof(T) == 8 && FW) {  // two-word rows, window rs < 64
+          const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
+          W128 w = op.point_fw(6 * C[q] - nb, C[q], Yv[q]);
+          if ((q == 3 && xpad) || rowpad) w = W128{0, 0};
+          if (MODE == MODE_QCOMP) w_or_mag(w, olo, ohi);
+          tt[q] = (T)w_shr_lo(w, c.rs);
+          mx = (V)tt[q] > mx ? (V)tt[q] : mx;
+          mn = (V)tt[q] < mn ? (V)tt[q] : mn;
+          continue;
+        }
         A z;
         if constexpr (sizeof(T) == 4) {
           const int nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
@@ -961,6 +971,11 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
           bulk3_loop<MODE, true, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
         else
           bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+      } else if (MODE != MODE_NNQ && op.fwi && c.store_tmp && c.ls == 0 && c.rs < 64) {
+        if (sh)
+          bulk3_loop<MODE, true, false, T, i128, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+        else
+          bulk3_loop<MODE, false, false, T, i128, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else {
         if (sh)
           bulk3_loop<MODE, true, false, T, i128>(op, out, p, c, r, R, smem, &tm.x, &tm.y);

@@ -61,6 +61,35 @@ __device__ __forceinline__ A combine_w(int64_t am, int64_t a, int64_t bm, int64_
     ta = ta << (int)imin(d, B);
   return ta + tb;
 }
+// Two-word rows for the int64-storage fast window (all shift counts < 64, uniform per
+// launch): value = hi * 2^64 + lo, two's complement over 128 bits.
+struct W128 {
+  uint64_t lo;
+  int64_t hi;
+};
+__device__ __forceinline__ W128 w_shl(int64_t a, int s) {  // a * 2^s, 0 <= s < 64
+  return W128{(uint64_t)a << s, s ? (a >> (64 - s)) : (a >> 63)};
+}
+__device__ __forceinline__ W128 w_add(W128 x, int64_t b) {
+  const uint64_t lo = x.lo + (uint64_t)b;
+  return W128{lo, x.hi + (b >> 63) + (int64_t)(lo < x.lo)};
+}
+__device__ __forceinline__ W128 w_add(W128 x, W128 y) {
+  const uint64_t lo = x.lo + y.lo;
+  return W128{lo, x.hi + y.hi + (int64_t)(lo < x.lo)};
+}
+__device__ __forceinline__ W128 w_mul_u32(W128 x, uint32_t c) {  // x * c mod 2^128
+  return W128{x.lo * c, (int64_t)((uint64_t)x.hi * c + __umul64hi(x.lo, c))};
+}
+__device__ __forceinline__ int64_t w_shr_lo(W128 z, int rs) {  // low word of floor(z/2^rs)
+  return (int64_t)(rs ? (z.lo >> rs) | ((uint64_t)z.hi << (64 - rs)) : z.lo);
+}
+__device__ __forceinline__ void w_or_mag(W128 z, uint64_t& olo, uint64_t& ohi) {
+  const uint64_t s = (uint64_t)(z.hi >> 63);
+  olo |= z.lo ^ s;
+  ohi |= (uint64_t)z.hi ^ s;
+}
+
 // width bound of alpha*a*2^max(d,0) + beta*b*2^max(-d,0) given operand widths
 // (a width of 0 marks an all-zero operand, whose term is excluded)
 __device__ __forceinline__ int64_t combine_bits(int64_t am, int64_t ba, int64_t bm, int64_t bb,
@@ -224,6 +253,7 @@ struct GemvOp {
   int64_t sx, sy, d;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
   bool w64;     // 64-bit stencil and products, A-wide shift / sum (int64 storage)
+  bool fwi;     // ... and the alignment shift < 64: two-word rows (W128)
   bool swap;
   int P, Q;
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -242,6 +272,7 @@ struct GemvOp {
              fits32(pm) && fits32(qm) && msb(pm) + ad <= 32 &&
              (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
     w64 = bg <= 62 && sx < 64 && sy < 64 && msb(al.m) + bg <= 63 && msb(be.m) + by <= 63;
+    fwi = w64 && need <= 127 && ad < 64;
     swap = d < 0;
     P = narrow ? (int)(pm << ad) : 0;
     Q = (int)qm;
@@ -266,6 +297,11 @@ struct GemvOp {
   template <typename A> __device__ __forceinline__ A point_w(int64_t g, int64_t c, int64_t yv) const {
     (void)c;
     return combine_w<A>(al.m, g, be.m, yv, d);
+  }
+  __device__ __forceinline__ W128 point_fw(int64_t g, int64_t c, int64_t yv) const {
+    (void)c;
+    const int64_t a = al.m * g, b = be.m * yv;
+    return d >= 0 ? w_add(w_shl(a, (int)d), b) : w_add(w_shl(b, (int)-d), a);
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -306,6 +342,7 @@ struct JacobiOp {
   int64_t sx, sb, d1, d2;
   bool narrow;
   bool w64;   // 64-bit stencil and r-term products (int64 storage)
+  bool fwi;   // ... and every alignment shift < 64: two-word rows (W128)
   bool neg1;  // d1 < 0: the b term carries the power of two
   int P1, s2;
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -325,6 +362,8 @@ struct JacobiOp {
              sx < 32 && sb < 32 && d1 >= -30 && d1 <= 30 && d2 >= 0 && d2 <= 62 && d2 != 31 &&
              bx <= 31 && (bx == 0 || bx + d2 <= 63);
     w64 = bg <= 62 && zbits(b.hdr) <= 62 && sx < 64 && sb < 64;
+    fwi = w64 && need <= 127 && d1 > -64 && d1 < 64 && d2 >= 0 && d2 < 64 && c.m >= 0 &&
+          c.m <= 0xffffffffll && bx <= 62;
     neg1 = d1 < 0;
     P1 = narrow ? (neg1 ? (1 << (int)(-d1)) : -(1 << (int)d1)) : 0;
     s2 = narrow ? (int)d2 : 0;
@@ -353,6 +392,10 @@ struct JacobiOp {
   }
   template <typename A> __device__ __forceinline__ A point_w(int64_t g, int64_t cx, int64_t bv) const {
     return combine<A>(1, (A)cx, c.m, combine_w<A>(-1, g, 1, bv, d1), d2);
+  }
+  __device__ __forceinline__ W128 point_fw(int64_t g, int64_t cx, int64_t bv) const {
+    const W128 r = d1 >= 0 ? w_add(w_shl(-g, (int)d1), bv) : w_add(w_shl(bv, (int)-d1), -g);
+    return w_add(w_shl(cx, (int)d2), w_mul_u32(r, (uint32_t)c.m));
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {

@@ -42,12 +42,11 @@ def main():
                 v = d.get(k, "")
                 try:
                     f = float(v.replace(",", ""))
-                    if k == "gpu__time_duration.sum" and u.get(k) == "ns":
-                        f /= 1000
-                    if k.startswith("dram__bytes") and u.get(k) == "KB":
-                        f /= 1000
-                    if k.startswith("dram__bytes") and u.get(k) == "GB":
-                        f *= 1000
+                    unit = u.get(k, "")
+                    if k == "gpu__time_duration.sum":
+                        f *= {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(unit, 1.0)
+                    if k.startswith("dram__bytes"):
+                        f *= {"byte": 1e-6, "KB": 1e-3, "Kbyte": 1e-3, "GB": 1e3, "Gbyte": 1e3}.get(unit, 1.0)
                     vals.append(f"{f * sc:.3g}")
                 except ValueError:
                     vals.append(v)
