@@ -159,6 +159,14 @@ int bfp_stencil_jacobi_part(bfp_vec_t x, bfp_vec_t b, bfp_scalar_t c, int mode, 
 int bfp_window_finalize(bfp_vec_t out, int mode, int stage, int64_t w_out, int64_t w_tmp,
                         const int64_t* d_part, void* stream);
 
+/* quantize_exact (P/src/bfp.cpp:163-187): entries z_i * 2^k_i (host arrays of the
+   vector's logical size) -> m_i = floor(z_i 2^(k_i - e)), e = max(msb z_i + k_i) - w,
+   q = w; all-zero input -> e = 0.  bfp_from_doubles is from_extfloat
+   (P/src/bfp.cpp:189-194) for IEEE doubles (non-finite -> BFP_ERR_ARG). */
+int bfp_quantize_exact(const int64_t* z, const int64_t* k, int64_t n, int64_t w, bfp_vec_t out,
+                       void* stream);
+int bfp_from_doubles(const double* v, int64_t n, int64_t w, bfp_vec_t out, void* stream);
+
 /* Jacobi coefficient c = floor_qc(omega_d / 2d) * 2^{-2l} as a BFP scalar */
 int bfp_jacobi_coeff(int dim, int level, int64_t qc, bfp_scalar_t* c);
 

@@ -97,6 +97,7 @@ EXPORTS = [
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
     "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result", "bfp_dist_create",
     "bfp_dist_destroy", "bfp_dist_stencil_gemv", "bfp_dist_stencil_jacobi",
+    "bfp_quantize_exact", "bfp_from_doubles",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -158,6 +159,8 @@ def lib() -> C.CDLL:
                                 pi64, vp]),
         "bfp_mg_vectors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
         "bfp_nccl_unique_id": (i32, [vp, i32]),
+        "bfp_quantize_exact": (i32, [vp, vp, i64, i64, vp, vp]),
+        "bfp_from_doubles": (i32, [vp, i64, i64, vp, vp]),
         "bfp_dist_create": (i32, [i32, i32, vp, C.POINTER(vp)]),
         "bfp_dist_destroy": (i32, [vp]),
         "bfp_dist_stencil_gemv": (i32, [vp, C.POINTER(vp), C.POINTER(vp), S, S, i32, i64, i64, S,
@@ -564,6 +567,29 @@ def prolong_correct(ec, y, w_out, w_tmp, gamma, nn=False):
     _raise(lib().bfp_prolong_correct(ec.h, y.h, int(nn), w_out, w_tmp, gamma.c(), out.h, _s()),
            "prolong_correct")
     return _result(out)
+
+
+def quantize_exact(z: Sequence[int], k: Sequence[int], w: int, mant_bytes: int = 8,
+                   dim: int = 0, level: int = 0) -> BfpVec:
+    """quantize_exact (src/bfp.cpp:163-187) of entries z_i 2^k_i on the device (int64 z)."""
+    za = np.ascontiguousarray(np.asarray(z, dtype=np.int64))
+    ka = np.ascontiguousarray(np.asarray(k, dtype=np.int64))
+    if za.shape != ka.shape:
+        raise InvalidArgument(ERR_ARG, "quantize_exact: size mismatch")
+    out = BfpVec.grid(dim, level, mant_bytes) if dim else BfpVec.flat(len(za), mant_bytes)
+    _raise(lib().bfp_quantize_exact(za.ctypes.data_as(C.c_void_p), ka.ctypes.data_as(C.c_void_p),
+                                    len(za), w, out.h, _s()), "quantize_exact")
+    return out
+
+
+def from_doubles(v: Sequence[float], w: int, mant_bytes: int = 8, dim: int = 0,
+                 level: int = 0) -> BfpVec:
+    """from_extfloat (src/bfp.cpp:189-194) for IEEE doubles (exact z 2^k split)."""
+    a = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    out = BfpVec.grid(dim, level, mant_bytes) if dim else BfpVec.flat(len(a), mant_bytes)
+    _raise(lib().bfp_from_doubles(a.ctypes.data_as(C.c_void_p), len(a), w, out.h, _s()),
+           "from_doubles")
+    return out
 
 
 def jacobi_coeff(dim: int, level: int, qc: int = 16) -> Scalar:

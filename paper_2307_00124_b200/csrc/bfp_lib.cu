@@ -540,6 +540,86 @@ int gen_sine(bfp_vec_s* v, int64_t p, cudaStream_t s) {
   return last_launch();
 }
 
+// quantize_exact (src/bfp.cpp:163-187) over entries z_i * 2^k_i given per logical index
+// by a source: top = max msb(z_i) + k_i over nonzero entries, e_out = top - w,
+// m_i = floor(z_i * 2^(k_i - e_out)); an all-zero input gives e_out = 0
+struct SrcZK {  // mantissa / exponent pairs
+  const int64_t *z, *k;
+  __device__ bool get(int64_t i, int64_t& zz, int64_t& kk) const {
+    zz = z[i];
+    kk = k[i];
+    return zz != 0;
+  }
+};
+struct SrcDbl {  // IEEE doubles (from_extfloat, src/bfp.cpp:189-194): v = z * 2^k exactly
+  const double* v;
+  __device__ bool get(int64_t i, int64_t& zz, int64_t& kk) const {
+    const double d = v[i];
+    if (d == 0.0) return false;
+    split_double(d, zz, kk);
+    return true;
+  }
+};
+template <typename Src>
+__global__ void __launch_bounds__(kThreads) qe_top_kernel(Vec v, Src src, int64_t* top) {
+  int64_t t = INT64_MIN;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < v.n; o += stride) {
+    bool pad;
+    const int64_t i = logical_of(v, o, pad);
+    int64_t z, k;
+    if (pad || !src.get(i, z, k)) continue;
+    const int64_t b = msb(z) + k;
+    t = b > t ? b : t;
+  }
+  t = shfl_max64(t);
+  if ((threadIdx.x & 31) == 0 && t != INT64_MIN) atomicMax((long long*)top, (long long)t);
+}
+template <typename M, typename Src>
+__global__ void __launch_bounds__(kThreads) qe_write_kernel(Vec v, Src src, const int64_t* top,
+                                                            int64_t w) {
+  const int64_t tp = *top;
+  const int64_t e_out = tp != INT64_MIN ? tp - w : 0;
+  Red r;
+  r.init();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < v.n; o += stride) {
+    bool pad;
+    const int64_t i = logical_of(v, o, pad);
+    int64_t z, k, m = 0;
+    if (!pad && src.get(i, z, k)) {
+      const int64_t s = e_out - k;  // shift_floor(z, s), src/wideint.cpp:94-99
+      m = s >= 0 ? (s >= 63 ? (z < 0 ? -1 : 0) : (z >> s)) : (int64_t)((uint64_t)z << (-s));
+    }
+    ((M*)v.data)[o] = (M)m;
+    r.val(m);
+  }
+  reduce_and_finalize(r, v.hdr, [&](int, int64_t mx, int64_t mn, int) {
+    Hdr* h = v.hdr;
+    h->q = w;
+    h->e = e_out;
+    h->shift = 0;
+    h->max_m = mx;
+    h->min_m = mn;
+    h->flags = 0;
+    h->need_recompute = 0;
+    h->err = 0;
+  });
+}
+template <typename Src>
+static int quantize_exact_impl(bfp_vec_s* v, Src src, int64_t w, int64_t* top, cudaStream_t s) {
+  set_i64_kernel<<<1, 1, 0, s>>>(top, INT64_MIN);
+  Vec d = view(v);
+  const int b = blocks_for(v->span);
+  qe_top_kernel<Src><<<b, kThreads, 0, s>>>(d, src, top);
+  if (v->ebytes == 4)
+    qe_write_kernel<int32_t, Src><<<b, kThreads, 0, s>>>(d, src, top, w);
+  else
+    qe_write_kernel<int64_t, Src><<<b, kThreads, 0, s>>>(d, src, top, w);
+  count_launch(3);
+  return last_launch();
+}
+
 void jacobi_coeff(int dim, int level, int64_t qc, int64_t* cm, int64_t* ce) {
   // omega_d/(2d) = 1/3, 1/5, 1/7 floor-quantised at qc bits
   const int64_t den = dim == 1 ? 3 : (dim == 2 ? 5 : 7);
@@ -706,6 +786,44 @@ int bfp_vec_download_async_i32(bfp_vec_t v, int32_t* m, void* stream) {
 int bfp_vec_download_i32(bfp_vec_t v, int32_t* m, bfp_header_t* hdr, void* stream) {
   if (v && v->ebytes != 4) return BFP_ERR_ARG;
   return download_impl<int32_t>(v, m, hdr, stream);
+}
+
+int bfp_quantize_exact(const int64_t* z, const int64_t* k, int64_t n, int64_t w, bfp_vec_t out,
+                       void* stream) {
+  if (!out || n != out->nlog || (n > 0 && (!z || !k)) || w < 1 || w > out->ebytes * 8)
+    return BFP_ERR_ARG;
+  cudaStream_t s = S(stream);
+  int64_t* buf = nullptr;  // top scratch + z + k
+  if (cudaMallocAsync((void**)&buf, sizeof(int64_t) * (1 + 2 * (size_t)n), s) != cudaSuccess)
+    return BFP_ERR_NOMEM;
+  int rc = BFP_OK;
+  if (n > 0 && (cudaMemcpyAsync(buf + 1, z, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s) !=
+                    cudaSuccess ||
+                cudaMemcpyAsync(buf + 1 + n, k, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s) !=
+                    cudaSuccess))
+    rc = BFP_ERR_CUDA;
+  if (!rc) rc = bfp::quantize_exact_impl(out, bfp::SrcZK{buf + 1, buf + 1 + n}, w, buf, s);
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
+int bfp_from_doubles(const double* v, int64_t n, int64_t w, bfp_vec_t out, void* stream) {
+  if (!out || n != out->nlog || (n > 0 && !v) || w < 1 || w > out->ebytes * 8) return BFP_ERR_ARG;
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return BFP_ERR_ARG;
+  cudaStream_t s = S(stream);
+  char* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, sizeof(int64_t) + sizeof(double) * (size_t)n, s) !=
+      cudaSuccess)
+    return BFP_ERR_NOMEM;
+  double* d = reinterpret_cast<double*>(buf + sizeof(int64_t));
+  int rc = BFP_OK;
+  if (n > 0 &&
+      cudaMemcpyAsync(d, v, sizeof(double) * n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    rc = BFP_ERR_CUDA;
+  if (!rc) rc = bfp::quantize_exact_impl(out, bfp::SrcDbl{d}, w, (int64_t*)buf, s);
+  cudaFreeAsync(buf, s);
+  return rc;
 }
 
 int bfp_vec_zero(bfp_vec_t v, int64_t q, void* stream) {

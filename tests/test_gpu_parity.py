@@ -88,6 +88,11 @@ def test_known_answers_gpu(B):
             A = B.BfpCsr(a["rows"], a["cols"], a["rowptr"], a["col"], a["m"], a["q"], a["e"])
             with pytest.raises(B.InvalidArgument):
                 B.qspmv(A, B.BfpVec.from_mantissas(*c["x"]), 8, 8, B.Scalar(1, 2, 0), m_a=c["m_a"])
+        elif op == "quantize_exact":  # from_extfloat [1, -0.5] w3
+            r = B.quantize_exact(c["z"], c["k"], c["w"])
+            same(r, c["want"]["m"], c["want"]["e"], c["w"])
+            vals = [float(Fraction(z) * Fraction(2) ** k) for z, k in zip(c["z"], c["k"])]
+            same(B.from_doubles(vals, c["w"]), c["want"]["m"], c["want"]["e"], c["w"])
         elif op == "axpby_row":
             x = B.BfpVec.from_mantissas(*c["x"])
             y = B.BfpVec.from_mantissas(*c["y"])
@@ -99,6 +104,32 @@ def test_known_answers_gpu(B):
             continue
         n_checked += 1
     assert n_checked >= 15
+
+
+@pytest.mark.parametrize("mb", [4, 8])
+def test_quantize_exact_gpu_vs_pyref(B, mb):
+    """quantize_exact / from_extfloat on the device vs the big-int restatement (random
+    signs, magnitudes, exponents and widths, zero entries and all-zero blocks)."""
+    import math
+    r = Rng(77 + mb)
+    for it in range(60):
+        n = r.uniform(0, 40)
+        w = r.uniform(1, 31 if mb == 4 else 62)
+        z = [0 if r.uniform(0, 4) == 0 else r.uniform(-(1 << 62), 1 << 62) >> r.uniform(0, 60)
+             for _ in range(n)]
+        if it % 10 == 0:
+            z = [0] * n
+        k = [r.uniform(-80, 80) for _ in range(n)]
+        want = P.quantize_exact(z, k, w)
+        same(B.quantize_exact(z, k, w, mant_bytes=mb), want.m, want.e, w)
+        # doubles: z with at most 53 significant bits
+        zd = [v >> max(0, v.bit_length() - 53) if v > 0 else -((-v) >> max(0, (-v).bit_length() - 53))
+              for v in z]
+        vals = [math.ldexp(float(a), b) for a, b in zip(zd, k)]
+        want = P.quantize_exact(zd, k, w)
+        same(B.from_doubles(vals, w, mant_bytes=mb), want.m, want.e, w)
+    with pytest.raises(B.InvalidArgument):
+        B.from_doubles([float("nan")], 4)
 
 
 def test_domain_error_on_upload(B):
