@@ -40,7 +40,7 @@ struct ArenaEntry {
   int64_t bytes;
   int32_t off, hoff;  // byte offsets in the CTA's shared memory
 };
-struct FusedOp {
+struct alignas(16) FusedOp {
   int32_t kind, pad;
   int64_t q;
   Vec out;

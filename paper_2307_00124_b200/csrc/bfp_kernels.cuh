@@ -617,29 +617,27 @@ __device__ __forceinline__ void rebase_op(ProlongCorrectOp& o, char* b) {
   rebase(o.y, b);
 }
 
+// One op of the fused list.  The op (its FusedOp record) is staged once in shared
+// memory; thread 0 rebases it, runs the op setup and the window setup; every thread
+// then works on references into shared memory (no per-thread copies of the records).
 template <typename M, typename Op>
-__device__ __noinline__ void fused_run(Op op, Vec out, WinParams p, char* ab) {
-  __shared__ WinCtx s_c;
-  __shared__ int64_t s_need;
-  __shared__ alignas(16) char s_op[sizeof(Op)];
-  if (ab) {
-    rebase_op(op, ab);
-    rebase(out, ab);
-    rebase_gamma(p.gamma, ab);
-  }
+__device__ __noinline__ void fused_run(Op& op, Vec& out, WinParams& p, char* ab, WinCtx& s_c,
+                                       int64_t& s_need) {
   if (threadIdx.x == 0) {
+    if (ab) {
+      rebase_op(op, ab);
+      rebase(out, ab);
+      rebase_gamma(p.gamma, ab);
+    }
     int64_t e_star = 0, nd = 0;
-    Op o = op;
-    o.setup(e_star, nd);
+    op.setup(e_star, nd);
     WinCtx cc;
     win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
-    *reinterpret_cast<Op*>(s_op) = o;
     s_c = cc;
     s_need = nd;
   }
   __syncthreads();
-  op = *reinterpret_cast<const Op*>(s_op);
-  WinCtx c = s_c;
+  const WinCtx c = s_c;
   const int64_t need = s_need;
   if (p.mode == MODE_NNQ) {
     fused_pass<MODE_NNQ, M>(op, out, p, c, need);
@@ -647,10 +645,18 @@ __device__ __noinline__ void fused_run(Op op, Vec out, WinParams p, char* ab) {
   }
   fused_pass<MODE_QCOMP, M>(op, out, p, c, need);
   // header finalized by thread 0 and published by the barrier in block_reduce_finalize
+  if (!out.hdr->need_recompute) return;  // qcomp fast path (uniform: shared header)
+  if (threadIdx.x == 0) {
+    WinParams p2 = p;
+    p2.mode = MODE_RECOMPUTE;
+    WinCtx c2;
+    win_setup(p2, out.hdr, 0, 8 * (int)sizeof(M), c2);
+    s_c = c2;
+  }
+  __syncthreads();
   WinParams p2 = p;
   p2.mode = MODE_RECOMPUTE;
-  WinCtx c2;
-  win_setup(p2, out.hdr, 0, 8 * (int)sizeof(M), c2);
+  const WinCtx c2 = s_c;
   if (!c2.skip) fused_pass<MODE_RECOMPUTE, M>(op, out, p2, c2, need);
 }
 
@@ -682,27 +688,37 @@ template <typename M>
 __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops, int n,
                                                               const ArenaEntry* ar, int nar) {
   extern __shared__ __align__(128) char arena[];
+  __shared__ __align__(16) FusedOp s_f;
+  __shared__ WinCtx s_c;
+  __shared__ int64_t s_need;
   griddep_wait();
   char* ab = nar > 0 ? arena : nullptr;
   for (int k = 0; k < nar; ++k) {  // vectors + headers of the fused levels -> shared memory
     arena_copy(arena + ar[k].off, ar[k].gbase, ar[k].bytes);
     arena_copy(arena + ar[k].hoff, reinterpret_cast<const char*>(ar[k].ghdr), sizeof(Hdr));
   }
-  __syncthreads();
   for (int i = 0; i < n; ++i) {
-    const int kind = ops[i].kind;
-    switch (kind) {
-      case FK_GEMV: fused_run<M>(ops[i].u.gemv, ops[i].out, ops[i].p, ab); break;
-      case FK_JACOBI: fused_run<M>(ops[i].u.jac, ops[i].out, ops[i].p, ab); break;
-      case FK_SCAL: fused_run<M>(ops[i].u.scal, ops[i].out, ops[i].p, ab); break;
-      case FK_AXPBY: fused_run<M>(ops[i].u.axpby, ops[i].out, ops[i].p, ab); break;
-      case FK_RESTRICT: fused_run<M>(ops[i].u.rst, ops[i].out, ops[i].p, ab); break;
-      case FK_PROLONG: fused_run<M>(ops[i].u.pro, ops[i].out, ops[i].p, ab); break;
-      case FK_PCORR: fused_run<M>(ops[i].u.pc, ops[i].out, ops[i].p, ab); break;
-      case FK_ZERO: fused_zero<M>(ops[i].out, ops[i].q, ab); break;
-    }
+    static_assert(sizeof(FusedOp) % 16 == 0, "FusedOp staging copies 16-byte granules");
+    __syncthreads();  // previous op done with s_f
+    for (int k = threadIdx.x; k < (int)(sizeof(FusedOp) / 16); k += blockDim.x)
+      reinterpret_cast<int4*>(&s_f)[k] = reinterpret_cast<const int4*>(&ops[i])[k];
     __syncthreads();
+    switch (s_f.kind) {
+      case FK_GEMV: fused_run<M>(s_f.u.gemv, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_JACOBI: fused_run<M>(s_f.u.jac, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_SCAL: fused_run<M>(s_f.u.scal, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_AXPBY: fused_run<M>(s_f.u.axpby, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_RESTRICT: fused_run<M>(s_f.u.rst, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_PROLONG: fused_run<M>(s_f.u.pro, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_PCORR: fused_run<M>(s_f.u.pc, s_f.out, s_f.p, ab, s_c, s_need); break;
+      case FK_ZERO: {
+        Vec v = s_f.out;
+        fused_zero<M>(v, s_f.q, ab);
+        break;
+      }
+    }
   }
+  __syncthreads();
   for (int k = 0; k < nar; ++k) {  // write everything back (the fused part's outputs)
     arena_copy(ar[k].gbase, arena + ar[k].off, ar[k].bytes);
     arena_copy(reinterpret_cast<char*>(ar[k].ghdr), arena + ar[k].hoff, sizeof(Hdr));
