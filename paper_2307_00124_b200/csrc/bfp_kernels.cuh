@@ -1008,6 +1008,335 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
   });
 }
 
+// ---------------------------------------------------------------------------
+// 3-D prolongation (+ correction) through tiled TMA.  A CTA owns a 128 x 8 tile of
+// the fine plane and marches fine planes in pairs (2K, 2K+1): both read the
+// row sums S_K = sum over the two coarse rows of x-lines of coarse plane K, and
+// fine plane 2K also reads S_{K-1}, so each coarse plane tile (72 x 5 box) is
+// loaded and summed once per pair; P e_c (2K) = S_{K-1} + S_K, (2K+1) = 2 S_K.
+// The correction operand y arrives as two 128 x 8 boxes per pair.
+constexpr int kP3W = 128, kP3H = 8, kP3T = 256;
+constexpr int kP3CW = kP3W / 2 + 8, kP3CH = kP3H / 2 + 1;  // coarse box 72 x 5
+constexpr int kP3CT = ((kP3CW * kP3CH * 4 + 127) / 128 * 128) / 4;  // slot (words, 128 B)
+constexpr int kP3YT = kP3W * kP3H;                               // one y box
+constexpr int kP3D = 2;                                          // pairs in flight
+constexpr int kP3S = kP3D + 1;                                   // slots / barriers
+constexpr size_t kP3Smem = (size_t)kP3S * (kP3CT + 2 * kP3YT) * 4 + kP3S * 8 + 128 + 64;
+struct P3Maps {
+  CUtensorMap c, y;
+};
+
+template <int MODE, bool FW, typename Op>
+__device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r, int R, char* smem,
+                                          const CUtensorMap* tmc, const CUtensorMap* tmy) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l, N2 = N * N;
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int tx = (int)(N / kP3W), ty = (int)(N / kP3H);
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* csl = reinterpret_cast<int32_t*>(smem);
+  int32_t* ysl = csl + kP3S * kP3CT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kP3S * 2 * kP3YT);
+  int32_t* O = (int32_t*)out.data;
+  const int sc = op.shc(), sy = op.shy();
+  const int kc_off = op.zp / 2;  // coarse local plane of fine local pair K
+  const int t = threadIdx.x, lane = t & 31, wy = t >> 5;
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  const uint32_t cbytes = (uint32_t)kP3CW * kP3CH * 4, ybytes = (uint32_t)kP3YT * 4;
+  uint32_t parity = 0;
+  // local coarse rows of fine row y0 + wy and the coarse column of this thread's 4 points
+  const int r0 = ((wy - 1) >> 1) + 1, r1 = (wy >> 1) + 1, col = 2 * lane + 4;
+  for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
+    const int tile = item % (tx * ty), ch = item / (tx * ty);
+    const int64_t x0 = (int64_t)(tile % tx) * kP3W, y0 = (int64_t)(tile / tx) * kP3H;
+    const int64_t k0 = (int64_t)ch * R;
+    const int pairs = (int)(std::min<int64_t>(R, NZ - k0) / 2);
+    const int64_t K0 = k0 / 2;
+    // step s (pair K0 + s) on slot s % S: coarse plane K0 + s (and K0 - 1 at s = 0)
+    auto issue = [&](int s) {
+      const int slot = s % kP3S;
+      uint64_t* b = &bar[slot];
+      const int64_t K = K0 + s;
+      const uint32_t bytes = cbytes + (s == 0 ? cbytes : 0u) + (Op::kCorr ? 2 * ybytes : 0u);
+      mbar_expect_tx(b, bytes);
+      tma_g2s_3d(csl + slot * kP3CT, tmc, (int)(x0 / 2) - 4, (int)(y0 / 2) - 1,
+                 (int)(K + kc_off + 2), b);
+      if (s == 0)  // coarse plane K0 - 1 into the slot of step -1
+        tma_g2s_3d(csl + ((kP3S - 1) % kP3S) * kP3CT, tmc, (int)(x0 / 2) - 4, (int)(y0 / 2) - 1,
+                   (int)(K - 1 + kc_off + 2), b);
+      if (Op::kCorr)
+        for (int h = 0; h < 2; ++h)
+          tma_g2s_3d(ysl + (slot * 2 + h) * kP3YT, tmy, (int)x0, (int)y0, (int)(2 * K + h + 2), b);
+    };
+    if (t == 0) {
+      fence_proxy_async_smem();
+      for (int s = 0; s < kP3D && s < pairs; ++s) issue(s);
+    }
+    const bool xpad = x0 + 4 * lane + 3 == N - 1;
+    const bool ypad = y0 + wy == N - 1;
+    int Sp[4] = {0, 0, 0, 0};  // S_{K-1}
+    for (int s = 0; s < pairs; ++s) {
+      const int slot = s % kP3S;
+      mbar_wait(&bar[slot], (parity >> slot) & 1u);
+      parity ^= 1u << slot;
+      auto S_of = [&](int sl, int S[4]) {
+        const int32_t* cb = csl + sl * kP3CT;
+        int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const int32_t* row = cb + (rr ? r1 : r0) * kP3CW + col;
+          const int a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
+          acc[0] += a + b;
+          acc[1] += 2 * b;
+          acc[2] += b + e;
+          acc[3] += 2 * e;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S[q] = acc[q];
+      };
+      if (s == 0) S_of((kP3S - 1) % kP3S, Sp);
+      int Sc[4];
+      S_of(slot, Sc);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t k = 2 * (K0 + s) + h;  // local fine plane
+        int yv[4] = {0, 0, 0, 0};
+        if (Op::kCorr) {
+          const int4 y4 =
+              *reinterpret_cast<const int4*>(ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane);
+          yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
+        }
+        const bool rowpad = ypad || k + Z0 == N - 1;
+        int32_t tt[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+          int64_t z = op.corr(g, yv[q]);
+          if ((q == 3 && xpad) || rowpad) z = 0;
+          if constexpr (FW) {
+            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+            tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+          } else if (MODE == MODE_NNQ) {
+            tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+          } else {
+            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+            tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+          }
+          mx = tt[q] > mx ? tt[q] : mx;
+          mn = tt[q] < mn ? tt[q] : mn;
+        }
+        *reinterpret_cast<int4*>(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane) =
+            make_int4(tt[0], tt[1], tt[2], tt[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Sp[q] = Sc[q];
+      __syncthreads();  // slot of step s (and, at s = 0, of step -1) is free
+      if (t == 0 && s + kP3D < pairs) {
+        fence_proxy_async_smem();
+        issue(s + kP3D);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE, typename Op>
+__global__ void __launch_bounds__(kP3T, 4)
+    pro3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ P3Maps tm) {
+  extern __shared__ __align__(128) char smem_raw[];
+  char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (kP3CT + 2 * kP3YT) * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kP3S; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
+      pro3_loop<MODE, true>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
+    else
+      pro3_loop<MODE, false>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// 3-D full-weighting restriction through tiled TMA.  A CTA owns a 64 x 8 tile of the
+// coarse plane (4 coarse points per thread) and marches coarse planes K; fine plane p
+// contributes the row sums T_p = sum_{rows 2J..2J+2} w_y (f[2I] + 2 f[2I+1] + f[2I+2])
+// and coarse K = T_{2K} + 2 T_{2K+1} + T_{2K+2}: each fine plane tile (136 x 17 box)
+// is loaded once and T_{2K+2} is kept in registers for the next step.
+constexpr int kR3W = 64, kR3H = 8, kR3T = kR3W / 4 * kR3H;           // 128 threads
+constexpr int kR3FW = 2 * kR3W + 8, kR3FH = 2 * kR3H + 1;            // fine box 136 x 17
+constexpr int kR3FT = ((kR3FW * kR3FH * 4 + 127) / 128 * 128) / 4;   // slot (words, 128 B)
+constexpr int kR3D = 1;                                              // steps in flight
+constexpr int kR3FS = 2 * kR3D + 3, kR3B = kR3D + 1;                 // plane slots, barriers
+constexpr size_t kR3Smem = (size_t)kR3FS * kR3FT * 4 + kR3B * 8 + 128 + 64;
+struct R3Maps {
+  CUtensorMap f;
+};
+
+template <int MODE, bool FW>
+__device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
+                                          const WinParams& p, const WinCtx& c, Red& r, int R,
+                                          char* smem, const CUtensorMap* tmf) {
+  const int lc = out.l;  // coarse level
+  const int64_t Nc = (int64_t)1 << lc, Nc2 = Nc * Nc;
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int tx = (int)(Nc / kR3W), ty = (int)(Nc / kR3H);
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* fsl = reinterpret_cast<int32_t*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fsl + kR3FS * kR3FT);
+  int32_t* O = (int32_t*)out.data;
+  const int sh = (int)op.sr;
+  const int t = threadIdx.x, cy = t >> 4, cxq = t & 15;  // coarse row in tile, 4-group
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  const uint32_t pbytes = (uint32_t)kR3FW * kR3FH * 4;
+  uint32_t parity = 0;
+  for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
+    const int tile = item % (tx * ty), ch = item / (tx * ty);
+    const int64_t x0 = (int64_t)(tile % tx) * kR3W, y0 = (int64_t)(tile / tx) * kR3H;
+    const int64_t K0 = (int64_t)ch * R;
+    const int steps = (int)std::min<int64_t>(R, NZ - K0);
+    // step s: fine planes 2(K0+s)+1, +2 (and 2 K0 at s = 0); fine plane f -> slot
+    // (f - 2 K0) % FS, barrier s % B
+    auto issue = [&](int s) {
+      uint64_t* b = &bar[s % kR3B];
+      mbar_expect_tx(b, pbytes * (s == 0 ? 3u : 2u));
+      for (int j = (s == 0 ? 0 : 1); j <= 2; ++j) {
+        const int64_t f = 2 * (K0 + s) + j;  // local fine plane
+        tma_g2s_3d(fsl + (int)((f - 2 * K0) % kR3FS) * kR3FT, tmf, (int)(2 * x0) - 4,
+                   (int)(2 * y0), (int)(f + 2), b);
+      }
+    };
+    if (t == 0) {
+      fence_proxy_async_smem();
+      for (int s = 0; s <= kR3D && s < steps; ++s) issue(s);
+    }
+    // fine columns 2 I0 .. 2 I0 + 8 of this thread's 4 coarse points, rows 2 cy .. 2 cy + 2
+    const int fcol = 8 * cxq + 4, frow = 2 * cy;
+    auto T_of = [&](int64_t f, int T[4]) {
+      const int32_t* base = fsl + (int)((f - 2 * K0) % kR3FS) * kR3FT + fcol;
+      int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int py = 0; py < 3; ++py) {
+        const int32_t* row = base + (frow + py) * kR3FW;
+        const int4 a = *reinterpret_cast<const int4*>(row);
+        const int4 b = *reinterpret_cast<const int4*>(row + 4);
+        const int e = row[8] >> sh;
+        const int v0 = a.x >> sh, v1 = a.y >> sh, v2 = a.z >> sh, v3 = a.w >> sh;
+        const int v4 = b.x >> sh, v5 = b.y >> sh, v6 = b.z >> sh, v7 = b.w >> sh;
+        const int wy = py == 1 ? 2 : 1;
+        acc[0] += wy * (v0 + 2 * v1 + v2);
+        acc[1] += wy * (v2 + 2 * v3 + v4);
+        acc[2] += wy * (v4 + 2 * v5 + v6);
+        acc[3] += wy * (v6 + 2 * v7 + e);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) T[q] = acc[q];
+    };
+    const bool xpad = x0 + 4 * cxq + 3 == Nc - 1;
+    const bool ypad = y0 + cy == Nc - 1;
+    int Tp[4] = {0, 0, 0, 0};  // T_{2K}
+    for (int s = 0; s < steps; ++s) {
+      const int64_t Kc = K0 + s;
+      mbar_wait(&bar[s % kR3B], (parity >> (s % kR3B)) & 1u);
+      parity ^= 1u << (s % kR3B);
+      if (s == 0) T_of(2 * Kc, Tp);
+      int T1[4], T2[4];
+      T_of(2 * Kc + 1, T1);
+      T_of(2 * Kc + 2, T2);
+      const bool rowpad = ypad || Kc + Z0 == Nc - 1;
+      int32_t tt[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int64_t z = (int64_t)Tp[q] + 2 * (int64_t)T1[q] + (int64_t)T2[q];
+        if ((q == 3 && xpad) || rowpad) z = 0;
+        if constexpr (FW) {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+        } else if (MODE == MODE_NNQ) {
+          tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+        } else {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+        }
+        mx = tt[q] > mx ? tt[q] : mx;
+        mn = tt[q] < mn ? tt[q] : mn;
+      }
+      *reinterpret_cast<int4*>(O + Kc * Nc2 + (y0 + cy) * Nc + x0 + 4 * cxq) =
+          make_int4(tt[0], tt[1], tt[2], tt[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Tp[q] = T2[q];
+      __syncthreads();  // fine planes 2Kc, 2Kc + 1 are free
+      if (t == 0 && s + kR3D + 1 < steps) {
+        fence_proxy_async_smem();
+        issue(s + kR3D + 1);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kR3T, 8)
+    rst3_win_kernel(RestrictOp op, Vec out, WinParams p, int R, const __grid_constant__ R3Maps tm) {
+  extern __shared__ __align__(128) char smem_raw[];
+  char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<RestrictOp, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  // plane sums T_p (weights 16) in int32 need eff_bits(r) <= 27, i.e. need <= 35 in 3-D;
+  // the final combination is 64-bit
+  if (op.sr < 32 && need <= 35) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR3FS * kR3FT * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kR3B; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
+      rst3_loop<MODE, true>(op, out, p, c, r, R, smem, &tm.f);
+    else
+      rst3_loop<MODE, false>(op, out, p, c, r, R, smem, &tm.f);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
 // one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
 template <typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
@@ -1156,6 +1485,107 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
       launch_pdl(bulk3_win_kernel<MODE_NNQ, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     else
       launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
+// 3-D prolongation (+ correction), int32 storage, N >= 128: the tiled-TMA pair march
+template <typename Op>
+static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
+                              cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  P3Maps tm;
+  if (!encode_b3(&tm.c, op.cv(), kP3CW, kP3CH)) return BFP_ERR_CUDA;
+  if (Op::kCorr) {
+    if (!encode_b3(&tm.y, op.yv(), kP3W, kP3H)) return BFP_ERR_CUDA;
+  } else {
+    tm.y = tm.c;  // unused
+  }
+  const int64_t N = int64_t(1) << out->l;
+  static int occ = 0;
+  if (!occ) {
+    for (auto fn : {pro3_win_kernel<MODE_QCOMP, Op>, pro3_win_kernel<MODE_NNQ, Op>,
+                    pro3_win_kernel<MODE_RECOMPUTE, Op>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP3Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pro3_win_kernel<MODE_QCOMP, Op>, kP3T,
+                                                  kP3Smem);
+    occ = std::max(occ, 1);
+  }
+  const int64_t tiles = (N / kP3W) * (N / kP3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+  int R = (int)std::max<int64_t>(4, (tiles * NZ + ctas - 1) / ctas);
+  R += R & 1;  // whole fine-plane pairs
+  const int64_t items = tiles * ((NZ + R - 1) / R);
+  const int b = (int)std::min<int64_t>(items, ctas);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (pp.mode == MODE_QCOMP)
+      launch_pdl(pro3_win_kernel<MODE_QCOMP, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+    else if (pp.mode == MODE_NNQ)
+      launch_pdl(pro3_win_kernel<MODE_NNQ, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+    else
+      launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+
+// 3-D full-weighting restriction, int32 storage, coarse N >= 64: the tiled-TMA march
+static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinParams& p0,
+                              cudaStream_t s) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  Vec o = view(out);
+  R3Maps tm;
+  if (!encode_b3(&tm.f, op.r, kR3FW, kR3FH)) return BFP_ERR_CUDA;
+  const int64_t Nc = int64_t(1) << out->l;
+  static int occ = 0;
+  if (!occ) {
+    for (auto fn : {rst3_win_kernel<MODE_QCOMP>, rst3_win_kernel<MODE_NNQ>,
+                    rst3_win_kernel<MODE_RECOMPUTE>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kR3Smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rst3_win_kernel<MODE_QCOMP>, kR3T,
+                                                  kR3Smem);
+    occ = std::max(occ, 1);
+  }
+  const int64_t tiles = (Nc / kR3W) * (Nc / kR3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+  const int R = (int)std::max<int64_t>(2, (tiles * NZ + ctas - 1) / ctas);
+  const int64_t items = tiles * ((NZ + R - 1) / R);
+  const int b = (int)std::min<int64_t>(items, ctas);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (pp.mode == MODE_QCOMP)
+      launch_pdl(rst3_win_kernel<MODE_QCOMP>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
+    else if (pp.mode == MODE_NNQ)
+      launch_pdl(rst3_win_kernel<MODE_NNQ>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
+    else
+      launch_pdl(rst3_win_kernel<MODE_RECOMPUTE>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     count_launch();
   };
   if (g_prof) {

@@ -638,6 +638,12 @@ struct ProlongOp {
   int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
   int64_t sc;
   bool narrow;  // int32 storage and |P xc| < 2^31: vectorised coarse rows
+  static constexpr bool kCorr = false;
+  __host__ __device__ __forceinline__ const Vec& cv() const { return xc; }
+  __host__ __device__ __forceinline__ const Vec& yv() const { return xc; }  // unused
+  __device__ __forceinline__ int shc() const { return (int)sc; }
+  __device__ __forceinline__ int shy() const { return 0; }
+  __device__ __forceinline__ int64_t corr(int g, int yv) const { (void)yv; return g; }
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = -dim + xc.hdr->e;
     sc = xc.hdr->shift;
@@ -671,6 +677,15 @@ struct ProlongCorrectOp {
   int64_t sc, sy, d;
   bool narrow, swap;  // int32 storage: g = P ec in 32 bits, z = X 2^|d| + Y (one IMAD.WIDE)
   int P;
+  static constexpr bool kCorr = true;
+  __host__ __device__ __forceinline__ const Vec& cv() const { return ec; }
+  __host__ __device__ __forceinline__ const Vec& yv() const { return y; }
+  __device__ __forceinline__ int shc() const { return (int)sc; }
+  __device__ __forceinline__ int shy() const { return (int)sy; }
+  __device__ __forceinline__ int64_t corr(int g, int yy) const {
+    const int X = swap ? yy : g, Y = swap ? g : yy;
+    return (int64_t)X * (int64_t)P + (int64_t)Y;
+  }
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = -dim + ec.hdr->e;
     axpby_setup(ge, y.hdr->e, d, e_star);
