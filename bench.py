@@ -142,6 +142,19 @@ def cpu_residual_time(steps, warmup, budget_s=None, threads=None):
     return dt, threads, n
 
 
+def traffic_bytes(args):
+    """ncu dram read + write bytes per pass-1 launch of the dominant kernel, from the
+    committed capture (profiles/r1_traffic.json) unless given on the command line."""
+    if args.traffic_bytes is not None:
+        return args.traffic_bytes
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "r1_traffic.json")) as f:
+            return json.load(f)["c2_residual_pass1"]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def host_cpu():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -441,7 +454,7 @@ def run_ours(args, world, rank, local):
     kavg_ms = kern_ms / max(kern_n, 1)
     achieved = BYTES_PER_DOF * n / (kavg_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": args.traffic_bytes,
+            "frac": achieved / peak, "traffic": traffic_bytes(args),
             "kernel": "bulk_win_kernel<QCOMP,GemvOp> pass 1 (TMA-bulk smem pipeline)",
             "peak_kind": peak_kind, "kernel_ms": kavg_ms,
             "kernel_ms_event_brackets": ev_ms / max(ev_n, 1),
