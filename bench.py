@@ -287,6 +287,7 @@ def run_sharded(args, world, rank, local):
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     solve = {} if args.no_extras else sharded_solve(B, torch, dist, stream, world, rank)
+    c4 = {} if args.no_extras else sharded_residual_c4(B, torch, dist, stream, world, rank, ops)
     line = {
         "metric": "bfp_stencil_residual_gdofs", "value": n * args.steps / (ms / 1e3) / 1e9,
         "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -298,6 +299,7 @@ def run_sharded(args, world, rank, local):
         "gpu_launches": int(launches), "cuda_graph": bool(graphs), "graph_error": graph_err,
         "sharded_parity_with_unsharded": bool(okt.item()),
         "sharded_solve": solve,
+        "sharded_residual_C4": c4,
     }
     dist.barrier()
     del ops
@@ -305,6 +307,53 @@ def run_sharded(args, world, rank, local):
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def sharded_residual_c4(B, torch, dist, stream, world, rank, ops, steps=10):
+    """The C4 fine-level residual (511^3, int32 p=24) z-slab sharded over the ranks
+    (strong scaling, native sharded op, stream-ordered): per-step device time, max
+    over ranks, and parity of this rank's slab with the unsharded residual."""
+    import numpy as np
+    from paper_2307_00124_b200 import dist as Dm
+    d, l, p = 3, 9, 24
+    out = {"config": "C4 fine level 511^3 int32 p=24"}
+    try:
+        lo, hi = Dm.slab_ranges(l, world)[rank]
+        n = (1 << l) - 1
+        gx = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 1, 1)
+        gb = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
+        g = B.inf_norm_upper(B.residual(gx, gb, p, p + 5, B.Scalar(1 << 14, 16, 30)).z)
+
+        def slab_of(full):
+            m, q, e = full.download()
+            v = B.BfpVec.slab(d, l, lo, hi)
+            v.upload(m[lo * n * n: min(hi, n) * n * n], q, e)
+            return v
+        xs, bs = slab_of(gx), slab_of(gb)
+        r = B.BfpVec.slab(d, l, lo, hi)
+        m1, p1 = B.bfp_minus_one(), B.bfp_one()
+        for _ in range(3):
+            ops.gemv([xs], [bs], m1, p1, p, p + 5, g, [r])
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            ops.gemv([xs], [bs], m1, p1, p, p + 5, g, [r])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        mr, _, er = B.residual(gx, gb, p, p + 5, g).z.download()
+        mo, _, eo = r.download()
+        ok = eo == er and np.array_equal(mo, mr[lo * n * n: min(hi, n) * n * n])
+        okt = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        out.update(ms=float(ms.item()), gdofs=n ** 3 / (float(ms.item()) / 1e3) / 1e9,
+                   parity_with_unsharded=bool(okt.item()))
+    except Exception as ex:  # noqa: BLE001 -- report, never hide
+        out["error"] = str(ex)
+    return out
 
 
 def sharded_solve(B, torch, dist, stream, world, rank, name="C4_3d_fmg", min_planes=16, reps=3):

@@ -14,7 +14,9 @@ torch.cuda.set_stream(stream)
 B.set_stream(stream.cuda_stream)
 L = B.lib()
 sp = C.c_void_p(stream.cuda_stream)
-for d, l in ((2, 3), (2, 5), (2, 7), (2, 9), (3, 4), (3, 6)):
+skip = len(sys.argv) > 1 and sys.argv[1] == "skip"
+B.set_kernel_path(skip_recompute=skip)  # skip: the bound on a one-launch qcomp
+for d, l in ((2, 3), (2, 5), (2, 7), (2, 9), (2, 11), (3, 4), (3, 6), (3, 8)):
     p = 20
     x = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 1, 1)
     b = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
