@@ -175,7 +175,10 @@ int bfp_gen_uniform(bfp_vec_t v, int64_t p, uint64_t seed, uint64_t stream_id, v
 int bfp_gen_sine(bfp_vec_t v, int64_t p, void* stream);
 
 /* ---- multigrid solver ---- */
-/* PrecisionSchedule (P/include/bfpmg/multigrid.hpp:16-27) per level: p = w (iterate),
+/* nonnormalized = NormMode (P/src/multigrid.cpp:403-409): 0 normalized (qcomp),
+   1 nonnormalized (nnqcomp except the diagnostic final residual), 2 hybrid (qcomp only
+   for the IR residual of iterations <= 2, hybrid_qcomp_iters).
+   PrecisionSchedule (P/include/bfpmg/multigrid.hpp:16-27) per level: p = w (iterate),
    pd = wdot (residual and V-cycle), pc = wcheck (right-hand side); 0 entries = p.
    w_add_cap: GammaPolicy::w_add_cap (-1 unlimited). */
 typedef struct {

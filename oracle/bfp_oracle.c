@@ -795,6 +795,7 @@ typedef struct {
   int err;
   int have_prev_res[33];
   ob_g15 prev_res[33];
+  int ir_iter; /* 1-based IR iteration of the current ir() loop (hybrid mode) */
 } mg_ctx;
 
 static ob_block blk_alloc(int64_t n) {
@@ -824,7 +825,10 @@ static double norm_double(const ob_block* b) {
 static void run_step(mg_ctx* c, int step, int level, const ob_kernel* k, int64_t w_out,
                      ob_g15 gamma, int w_add, ob_block* out) {
   if (c->err) return;
-  int normalized = !c->cfg->nonnormalized || step == OB_STEP_FINAL_RES;
+  /* NormMode (P/src/multigrid.cpp:403-409): 0 normalized, 1 nonnormalized,
+     2 hybrid = qcomp only for the IR residual of iterations <= hybrid_qcomp_iters (2) */
+  int normalized = c->cfg->nonnormalized == 0 || step == OB_STEP_FINAL_RES ||
+                   (c->cfg->nonnormalized == 2 && step == OB_STEP_IR_RES && c->ir_iter <= 2);
   int64_t gm, ge;
   ob_g15_gamma(gamma, &gm, &ge);
   ob_flags fl = {0, 0, 0};
@@ -939,6 +943,7 @@ static void ir(mg_ctx* c, int l, ob_block* x, const ob_block* b, int iters) {
       gam = ob_g15_add(nrm(b), ob_g15_mul(ob_g15_from((uint64_t)(4 * cfg->d), 2 * (int64_t)l), ulp));
     }
     ob_make_stencil_gemv(&k, g, x, b, -1, 1, 0, 1, 2, 0);
+    c->ir_iter = i;
     run_step(c, OB_STEP_IR_RES, l, &k, wd(c, l), gam, first ? 5 : 4, &r);
     if (c->err) break;
     c->prev_res[l] = nrm(&r);

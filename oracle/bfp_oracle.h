@@ -151,7 +151,8 @@ typedef struct {
   int n_coarse;     /* sweeps on the coarsest level */
   int cycles;       /* IR iterations (mode 0) or IR steps per FMG level (mode 1) */
   int fmg;          /* 0: IR-V cycles at fine level, 1: FMG */
-  int nonnormalized;/* 1: nnqcomp everywhere except the diagnostic final residual */
+  int nonnormalized;/* 1: nnqcomp everywhere except the diagnostic final residual;
+                       2: hybrid, qcomp only for the IR residual of iterations <= 2 */
   int x0_random;    /* 1: x0 uniform (seed, stream 1); 0: zero_vec */
   int rhs_kind;     /* 0: uniform (seed, stream 2); 1: sine; 2: zero */
   int qc;           /* width of the Jacobi coefficient */

@@ -682,7 +682,11 @@ class Mg:
         return pc[l] if pc and pc[l] else self.cfg.p[l]
 
     def step(self, name, level, k, w_out, g, w_add):
-        normalized = (not self.cfg.nonnormalized) or name == "final-residual"
+        # NormMode (src/multigrid.cpp:403-409): 0 / False normalized, 1 / True
+        # nonnormalized, 2 hybrid (qcomp only for IR residuals of iterations <= 2)
+        nm = int(self.cfg.nonnormalized)
+        normalized = (nm == 0 or name == "final-residual" or
+                      (nm == 2 and name == "ir-residual" and self.ir_iter <= 2))
         if self.cfg.w_add_cap >= 0:
             w_add = min(w_add, self.cfg.w_add_cap)
         gam = g15_gamma(g)
@@ -722,7 +726,8 @@ class Mg:
     def ir(self, l, x, b, iters):
         d = self.cfg.d
         self.prev.pop(l, None)
-        for _ in range(iters):
+        for it in range(iters):
+            self.ir_iter = it + 1
             first = l not in self.prev
             if first:  # ||b|| + ||A|| ulp(x)
                 ulp = g15_from(1, x.e) if not x.is_zero() else (0, 0)

@@ -626,7 +626,8 @@ def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=Fa
     """Solver config; p / pd / pc are the PrecisionSchedule w / wdot / wcheck per level."""
     cfg = MgConfig()
     cfg.d, cfg.l_fine, cfg.l_coarse, cfg.nu1, cfg.nu2 = d, l_fine, l_coarse, nu1, nu2
-    cfg.n_coarse, cfg.cycles, cfg.fmg, cfg.nonnormalized = n_coarse, cycles, int(fmg), int(nonnormalized)
+    cfg.n_coarse, cfg.cycles, cfg.fmg = n_coarse, cycles, int(fmg)
+    cfg.nonnormalized = 2 if nonnormalized == "hybrid" else int(nonnormalized)  # NormMode
     cfg.x0_random, cfg.rhs_kind, cfg.qc, cfg.seed = int(x0_random), rhs_kind, qc, seed
     p, pd, pc = _lv(p), _lv(pd), _lv(pc)
     for i in range(32):

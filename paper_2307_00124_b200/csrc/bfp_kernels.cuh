@@ -24,6 +24,9 @@ std::pair<cudaEvent_t, cudaEvent_t> prof_pair();
 
 constexpr int kThreads = 256;
 constexpr int kMaxBlocks = 148 * 8;
+#ifndef BFP_GRID_UNROLL  // groups per grid-loop iteration (A/B switch)
+#define BFP_GRID_UNROLL 1
+#endif
 
 // Launch with Programmatic Dependent Launch: the grid may be scheduled while the
 // previous kernel in the stream drains; the kernel executes griddepcontrol.wait
@@ -84,9 +87,7 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
   M mx = Lim<M>::lo, mn = Lim<M>::hi;
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
-    A z[4];
-    op.template eval4<M, A, NC>(g * 4, z);
+  auto epi = [&](int64_t g, A z[4]) {
     M t[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -100,7 +101,30 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
       mn = t[j] < mn ? t[j] : mn;
     }
     V4<M>::store(out, g * 4, t);
+  };
+#if BFP_GRID_UNROLL > 1
+  // two groups per iteration: the second group's loads are issued before the first
+  // group's epilogue (more bytes in flight per thread)
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; g + stride < ngroups; g += 2 * stride) {
+    A z0[4], z1[4];
+    op.template eval4<M, A, NC>(g * 4, z0);
+    op.template eval4<M, A, NC>((g + stride) * 4, z1);
+    epi(g, z0);
+    epi(g + stride, z1);
   }
+  if (g < ngroups) {
+    A z[4];
+    op.template eval4<M, A, NC>(g * 4, z);
+    epi(g, z);
+  }
+#else
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+    A z[4];
+    op.template eval4<M, A, NC>(g * 4, z);
+    epi(g, z);
+  }
+#endif
   r.olo |= olo;
   r.ohi |= ohi;
   r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;  // sentinels stay neutral

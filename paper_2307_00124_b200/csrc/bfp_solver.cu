@@ -130,6 +130,7 @@ struct RankSolver {
 
   bool in_fused = false;
   bool fusion = true;
+  int ir_iter = 0;  // 1-based iteration of the ir() loop being planned (hybrid mode)
 
   ~RankSolver() {
     for (auto& op : plan) {
@@ -173,7 +174,10 @@ struct RankSolver {
 
   void step(int st, int level, PlanOp op, int64_t w_out, const GammaRule& g, int w_add,
             bool hist = false) {
-    const bool normalized = !cfg.nonnormalized || st == ST_FINAL_RES;
+    // NormMode (P/src/multigrid.cpp:403-409): 0 normalized, 1 nonnormalized,
+    // 2 hybrid = qcomp only for the IR residual of iterations <= 2
+    const bool normalized = cfg.nonnormalized == 0 || st == ST_FINAL_RES ||
+                            (cfg.nonnormalized == 2 && st == ST_IR_RES && ir_iter <= 2);
     if (cfg.w_add_cap >= 0 && w_add > cfg.w_add_cap) w_add = cfg.w_add_cap;
     op.p = win_params(normalized ? MODE_QCOMP : MODE_NNQ, w_out, w_out + w_add, 0);
     op.p.gamma = g;
@@ -291,6 +295,7 @@ struct RankSolver {
       o.out = r;
       o.s1 = Scal{-1, 1, 0};
       o.s2 = Scal{1, 2, 0};
+      ir_iter = i;
       step(ST_IR_RES, l, o, wd(l), g, first ? 5 : 4, true);
       r_prev = r;
       bfp_vec_s* e = vcycle(l, r);

@@ -112,6 +112,10 @@ MG_CASES = [
     # three-width PrecisionSchedule (w / wdot / wcheck) with a w_add cap (config 1 style)
     dict(name="c1_sched", d=1, l_fine=9, cycles=4, x0_random=True, rhs_kind=0, p=16,
          pd=[28] * 32, pc=[16] * 32, w_add_cap=4),
+    # NormMode::hybrid (src/multigrid.cpp:406-408): qcomp only for IR residuals 1, 2
+    dict(name="c2_hybrid", d=2, l_fine=5, cycles=4, rhs_kind=1, nonnormalized=2, p=20),
+    dict(name="c3_hybrid", d=2, l_fine=6, l_coarse=3, cycles=3, rhs_kind=1, fmg=True,
+         nonnormalized=2, p=[0, 0, 0] + [6 + 2 * (l - 3) for l in range(3, 32)][:29]),
 ]
 
 

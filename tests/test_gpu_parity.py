@@ -328,6 +328,7 @@ def test_mg_golden_gpu(B):
     ("c2", dict(d=2, l_fine=8, cycles=15, rhs_kind=1), 20),
     ("c3", dict(d=2, l_fine=9, l_coarse=3, cycles=1, rhs_kind=1, fmg=True, nonnormalized=True),
      [0, 0, 0] + [4 + 2 * (l - 3) for l in range(3, 32)][:29]),
+    ("c2_hybrid", dict(d=2, l_fine=8, cycles=6, rhs_kind=1, nonnormalized="hybrid"), 20),
     ("c4", dict(d=3, l_fine=6, cycles=1, rhs_kind=1, fmg=True), 24),
     ("c5", dict(d=3, l_fine=5, cycles=3, x0_random=True, rhs_kind=2), 48),
 ])
