@@ -537,6 +537,7 @@ def run_ours(args, world, rank, local):
         }
         line["fine_level_ops"] = {"C2": measure_ops(B, torch, stream, 2, 12, 20),
                                   "C4": measure_ops(B, torch, stream, 3, 9, 24)}
+        line["C5_precision_sweep_1gpu"] = run_c5_sweep(B, torch, stream)
     if rank == 0 and not args.no_cpu:
         sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
         sec1, _, nrun1 = cpu_residual_time(10**9, 0, budget_s=args.cpu_budget / 2, threads=1)
@@ -788,6 +789,40 @@ def run_solves(B, torch, stream):
                 out[name]["accuracy"] = sine_accuracy(kw["d"], kw["l_fine"], x, e)
             del mg
         except Exception as ex:  # report, never hide
+            out[name] = {"error": str(ex)}
+    return out
+
+
+def run_c5_sweep(B, torch, stream, ps=(4, 8, 16, 32, 48)):
+    """BASELINE config 5 on one GPU: 1023^3, x0 uniform, b = 0, 10 IR-V(2,2) cycles per
+    precision p (int32 storage for p <= 16, int64 with int128 rows above).  Device time
+    of one graph-replayed solve and the mean residual reduction per cycle.  With a flat
+    p the 4- and 8-bit residuals cannot resolve the error (cond ~ 4^10) and the iteration
+    diverges (reported as such); the `wdot24` variants keep the residual and the V-cycle
+    at 24 bits with the iterate at p bits (the C1 schedule argument)."""
+    out = {}
+    runs = [(f"p{p}", p, None) for p in ps] + [(f"p{p}_wdot24", p, 24) for p in ps if p < 24]
+    for name, p, pd in runs:
+        try:
+            extra = dict(pd=[pd] * 32, w_add_cap=4) if pd else {}
+            mg = B.Multigrid(B.mg_config(d=3, l_fine=10, cycles=10, x0_random=True, rhs_kind=2,
+                                         p=p, **extra))
+            mg.solve(use_graph=True)  # capture + first replay
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mg.solve(use_graph=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
+            rate = (hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)) if hist[0] > 0 else None
+            out[name] = {"ms": e0.elapsed_time(e1),
+                         "mant_bytes": 4 if max(p, pd or 0) + (4 if pd else 6) <= 32 else 8,
+                            "first_residual": hist[0], "final_residual": hist[-1],
+                            "reduction_per_cycle": rate,
+                            "recomputes": sum(t[8] for t in tr), "ops": len(tr)}
+            del mg
+        except Exception as ex:  # noqa: BLE001 -- report, never hide
             out[name] = {"error": str(ex)}
     return out
 
