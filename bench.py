@@ -818,9 +818,9 @@ def run_c5_sweep(B, torch, stream, ps=(4, 8, 16, 32, 48)):
             rate = (hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)) if hist[0] > 0 else None
             out[name] = {"ms": e0.elapsed_time(e1),
                          "mant_bytes": 4 if max(p, pd or 0) + (4 if pd else 6) <= 32 else 8,
-                            "first_residual": hist[0], "final_residual": hist[-1],
-                            "reduction_per_cycle": rate,
-                            "recomputes": sum(t[8] for t in tr), "ops": len(tr)}
+                         "first_residual": hist[0], "final_residual": hist[-1],
+                         "reduction_per_cycle": rate,
+                         "recomputes": sum(t[8] for t in tr), "ops": len(tr)}
             del mg
         except Exception as ex:  # noqa: BLE001 -- report, never hide
             out[name] = {"error": str(ex)}
