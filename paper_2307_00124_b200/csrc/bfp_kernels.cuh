@@ -1361,6 +1361,287 @@ __global__ void __launch_bounds__(kR3T, 8)
   });
 }
 
+// ---------------------------------------------------------------------------
+// 2-D transfers through the bulk-async row pipeline (the 2-D analogues of pro3 /
+// rst3, rows instead of planes, one cp.async.bulk per row).
+// Prolong (+ correct): a CTA owns 1024 fine columns and marches fine-row pairs
+// (2J, 2J+1) over the coarse row sums S_J (P e_c: 2J -> S_{J-1} + S_J, 2J+1 -> 2 S_J).
+constexpr int kP2T = 256, kP2W = 4 * kP2T;                       // fine strip
+constexpr int kP2CW = kP2W / 2 + 8;                              // coarse row slot (words)
+constexpr int kP2D = 2, kP2S = kP2D + 1;                         // pairs in flight, slots
+constexpr size_t kP2Smem = (size_t)kP2S * (kP2CW + 2 * kP2W) * 4 + kP2S * 8 + 128 + 64;
+
+template <int MODE, bool FW, typename Op>
+__device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const WinParams& p,
+                                          const WinCtx& c, Red& r, int R, char* smem) {
+  const int l = out.l;
+  const int64_t N = (int64_t)1 << l, Nc = N >> 1;
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int strips = (int)(N / kP2W);
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* csl = reinterpret_cast<int32_t*>(smem);
+  int32_t* ysl = csl + kP2S * kP2CW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kP2S * 2 * kP2W);
+  const int32_t* Cd = (const int32_t*)op.cv().data;
+  const int32_t* Yd = (const int32_t*)op.yv().data;
+  int32_t* O = (int32_t*)out.data;
+  const int sc = op.shc(), sy = op.shy();
+  const int kc_off = op.zp / 2;
+  const int t = threadIdx.x, col = 2 * t + 4;
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  uint32_t parity = 0;
+  for (int item = blockIdx.x; item < strips * chunks; item += gridDim.x) {
+    const int strip = item % strips, ch = item / strips;
+    const int64_t x0 = (int64_t)strip * kP2W, cx0 = x0 / 2;
+    const int64_t k0 = (int64_t)ch * R;
+    const int pairs = (int)(std::min<int64_t>(R, NZ - k0) / 2);
+    const int64_t J0 = k0 / 2;
+    auto crow = [&](int64_t J) { return Cd + (J + kc_off) * Nc + cx0 - 4; };
+    auto issue = [&](int s) {
+      const int slot = s % kP2S;
+      uint64_t* b = &bar[slot];
+      const int64_t J = J0 + s;
+      const uint32_t cb = kP2CW * 4, yb = kP2W * 4;
+      mbar_expect_tx(b, cb + (s == 0 ? cb : 0u) + (Op::kCorr ? 2 * yb : 0u));
+      bulk_g2s(csl + slot * kP2CW, crow(J), cb, b);
+      if (s == 0) bulk_g2s(csl + (kP2S - 1) * kP2CW, crow(J - 1), cb, b);
+      if (Op::kCorr)
+        for (int h = 0; h < 2; ++h)
+          bulk_g2s(ysl + (slot * 2 + h) * kP2W, Yd + (2 * J + h) * N + x0, yb, b);
+    };
+    if (t == 0) {
+      fence_proxy_async_smem();
+      for (int s = 0; s < kP2D && s < pairs; ++s) issue(s);
+    }
+    const bool xpad = x0 + 4 * t + 3 == N - 1;
+    int Sp[4] = {0, 0, 0, 0};
+    auto S_of = [&](int sl, int S[4]) {
+      const int32_t* row = csl + sl * kP2CW + col;
+      const int a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
+      S[0] = a + b;
+      S[1] = 2 * b;
+      S[2] = b + e;
+      S[3] = 2 * e;
+    };
+    for (int s = 0; s < pairs; ++s) {
+      const int slot = s % kP2S;
+      mbar_wait(&bar[slot], (parity >> slot) & 1u);
+      parity ^= 1u << slot;
+      if (s == 0) S_of(kP2S - 1, Sp);
+      int Sc[4];
+      S_of(slot, Sc);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t j = 2 * (J0 + s) + h;  // local fine row
+        int yv[4] = {0, 0, 0, 0};
+        if (Op::kCorr) {
+          const int4 y4 = *reinterpret_cast<const int4*>(ysl + (slot * 2 + h) * kP2W + 4 * t);
+          yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
+        }
+        const bool rowpad = j + Z0 == N - 1;
+        int32_t tt[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+          int64_t z = op.corr(g, yv[q]);
+          if ((q == 3 && xpad) || rowpad) z = 0;
+          if constexpr (FW) {
+            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+            tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+          } else if (MODE == MODE_NNQ) {
+            tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+          } else {
+            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+            tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+          }
+          mx = tt[q] > mx ? tt[q] : mx;
+          mn = tt[q] < mn ? tt[q] : mn;
+        }
+        *reinterpret_cast<int4*>(O + j * N + x0 + 4 * t) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Sp[q] = Sc[q];
+      __syncthreads();
+      if (t == 0 && s + kP2D < pairs) {
+        fence_proxy_async_smem();
+        issue(s + kP2D);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE, typename Op>
+__global__ void __launch_bounds__(kP2T, 4) pro2_win_kernel(Op op, Vec out, WinParams p, int R) {
+  extern __shared__ __align__(128) char smem_raw[];
+  char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<Op, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  if (op.narrow && need <= 63) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kP2S * (kP2CW + 2 * kP2W) * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kP2S; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
+      pro2_loop<MODE, true>(op, out, p, c, r, R, smem);
+    else
+      pro2_loop<MODE, false>(op, out, p, c, r, R, smem);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
+// Full weighting: a CTA owns 512 coarse columns and marches coarse rows K over the
+// fine-row sums T_p (coarse K = T_{2K} + 2 T_{2K+1} + T_{2K+2}, T_{2K+2} carried).
+constexpr int kR2T = 128, kR2W = 4 * kR2T;                       // coarse strip
+constexpr int kR2FW = 2 * kR2W + 8;                              // fine row slot (words)
+constexpr int kR2D = 2, kR2FS = 2 * kR2D + 3, kR2B = kR2D + 1;
+constexpr size_t kR2Smem = (size_t)kR2FS * kR2FW * 4 + kR2B * 8 + 128 + 64;
+
+template <int MODE, bool FW>
+__device__ __forceinline__ void rst2_loop(const RestrictOp& op, const Vec& out,
+                                          const WinParams& p, const WinCtx& c, Red& r, int R,
+                                          char* smem) {
+  const int lc = out.l;
+  const int64_t Nc = (int64_t)1 << lc, Nf = Nc << 1;
+  const int64_t NZ = out.nz, Z0 = out.z0;
+  const int strips = (int)(Nc / kR2W);
+  const int chunks = (int)((NZ + R - 1) / R);
+  int32_t* fsl = reinterpret_cast<int32_t*>(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(fsl + kR2FS * kR2FW);
+  const int32_t* F = (const int32_t*)op.r.data;
+  int32_t* O = (int32_t*)out.data;
+  const int sh = (int)op.sr;
+  const int t = threadIdx.x;
+  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  uint64_t olo = 0, ohi = 0;
+  const bool store = c.store_tmp;
+  uint32_t parity = 0;
+  for (int item = blockIdx.x; item < strips * chunks; item += gridDim.x) {
+    const int strip = item % strips, ch = item / strips;
+    const int64_t cx0 = (int64_t)strip * kR2W;
+    const int64_t K0 = (int64_t)ch * R;
+    const int steps = (int)std::min<int64_t>(R, NZ - K0);
+    auto issue = [&](int s) {
+      uint64_t* b = &bar[s % kR2B];
+      mbar_expect_tx(b, (uint32_t)kR2FW * 4 * (s == 0 ? 3u : 2u));
+      for (int j = (s == 0 ? 0 : 1); j <= 2; ++j) {
+        const int64_t f = 2 * (K0 + s) + j;  // local fine row
+        bulk_g2s(fsl + (int)((f - 2 * K0) % kR2FS) * kR2FW, F + f * Nf + 2 * cx0 - 4,
+                 kR2FW * 4, b);
+      }
+    };
+    if (t == 0) {
+      fence_proxy_async_smem();
+      for (int s = 0; s <= kR2D && s < steps; ++s) issue(s);
+    }
+    auto T_of = [&](int64_t f, int T[4]) {
+      const int32_t* row = fsl + (int)((f - 2 * K0) % kR2FS) * kR2FW + 8 * t + 4;
+      const int4 a = *reinterpret_cast<const int4*>(row);
+      const int4 b = *reinterpret_cast<const int4*>(row + 4);
+      const int e = row[8] >> sh;
+      const int v0 = a.x >> sh, v1 = a.y >> sh, v2 = a.z >> sh, v3 = a.w >> sh;
+      const int v4 = b.x >> sh, v5 = b.y >> sh, v6 = b.z >> sh, v7 = b.w >> sh;
+      T[0] = v0 + 2 * v1 + v2;
+      T[1] = v2 + 2 * v3 + v4;
+      T[2] = v4 + 2 * v5 + v6;
+      T[3] = v6 + 2 * v7 + e;
+    };
+    const bool xpad = cx0 + 4 * t + 3 == Nc - 1;
+    int Tp[4] = {0, 0, 0, 0};
+    for (int s = 0; s < steps; ++s) {
+      const int64_t Kc = K0 + s;
+      mbar_wait(&bar[s % kR2B], (parity >> (s % kR2B)) & 1u);
+      parity ^= 1u << (s % kR2B);
+      if (s == 0) T_of(2 * Kc, Tp);
+      int T1[4], T2[4];
+      T_of(2 * Kc + 1, T1);
+      T_of(2 * Kc + 2, T2);
+      const bool rowpad = Kc + Z0 == Nc - 1;
+      int32_t tt[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int64_t z = (int64_t)Tp[q] + 2 * (int64_t)T1[q] + (int64_t)T2[q];
+        if ((q == 3 && xpad) || rowpad) z = 0;
+        if constexpr (FW) {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+        } else if (MODE == MODE_NNQ) {
+          tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+        } else {
+          if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+        }
+        mx = tt[q] > mx ? tt[q] : mx;
+        mn = tt[q] < mn ? tt[q] : mn;
+      }
+      *reinterpret_cast<int4*>(O + Kc * Nc + cx0 + 4 * t) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Tp[q] = T2[q];
+      __syncthreads();
+      if (t == 0 && s + kR2D + 1 < steps) {
+        fence_proxy_async_smem();
+        issue(s + kR2D + 1);
+      }
+    }
+    __syncthreads();
+  }
+  r.olo |= olo;
+  r.ohi |= ohi;
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kR2T, 8) rst2_win_kernel(RestrictOp op, Vec out, WinParams p,
+                                                           int R) {
+  extern __shared__ __align__(128) char smem_raw[];
+  char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+  griddep_wait();
+  int64_t need = 0;
+  WinCtx c;
+  block_setup<RestrictOp, int32_t>(op, out, p, c, need);
+  if (c.skip) return;
+  Red r;
+  r.init();
+  // row sums T_p (weights 4) in int32: eff_bits(r) <= 29, need = eff + 6 <= 35 in 2-D
+  if (op.sr < 32 && need <= 35) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR2FS * kR2FW * 4);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kR2B; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
+      rst2_loop<MODE, true>(op, out, p, c, r, R, smem);
+    else
+      rst2_loop<MODE, false>(op, out, p, c, r, R, smem);
+  } else {
+    grid_body<MODE, int32_t>(op, out, p, c, r, need);
+  }
+  griddep_launch_dependents();
+  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+  });
+}
+
 // one exact row per thread, __int128 accumulation (generic CSR / fixed rows)
 template <typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinParams p) {
@@ -1625,6 +1906,67 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
     go(p);
   }
   return last_launch();
+}
+
+// one-wave launch of a row/plane-march transfer kernel (pass 1 + recompute unless partial)
+template <typename K0, typename K1, typename K2, typename... Args>
+static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int64_t units,
+                              int64_t NZ, int Rmin, bool even, bfp_vec_s* out, const WinParams& p0,
+                              cudaStream_t s, Args... args) {
+  int rc = check_window(p0, out);
+  if (rc) return rc;
+  static_assert(sizeof...(Args) >= 1, "kernel arguments");
+  static int occ = 0;  // per instantiation
+  if (!occ) {
+    cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kq, threads, smem);
+    occ = std::max(occ, 1);
+  }
+  const int64_t ctas = (int64_t)148 * occ;
+  int R = (int)std::max<int64_t>(Rmin, (units * NZ + ctas - 1) / ctas);
+  if (even) R += R & 1;
+  const int64_t items = units * ((NZ + R - 1) / R);
+  const int b = (int)std::min<int64_t>(items, ctas);
+  Vec o = view(out);
+  WinParams p = p0;
+  auto go = [&](const WinParams& pp) {
+    if (pp.mode == MODE_QCOMP)
+      launch_pdl(kq, b, threads, smem, s, args..., o, pp, R);
+    else if (pp.mode == MODE_NNQ)
+      launch_pdl(kn, b, threads, smem, s, args..., o, pp, R);
+    else
+      launch_pdl(kr, b, threads, smem, s, args..., o, pp, R);
+    count_launch();
+  };
+  if (g_prof) {
+    auto ev = prof_pair();
+    cudaEventRecord(ev.first, s);
+    go(p);
+    cudaEventRecord(ev.second, s);
+  } else {
+    go(p);
+  }
+  if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
+    p.mode = MODE_RECOMPUTE;
+    go(p);
+  }
+  return last_launch();
+}
+template <typename Op>
+static inline int launch_pro2(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
+  const int64_t N = int64_t(1) << out->l;
+  return launch_wave(pro2_win_kernel<MODE_QCOMP, Op>, pro2_win_kernel<MODE_NNQ, Op>,
+                     pro2_win_kernel<MODE_RECOMPUTE, Op>, kP2T, kP2Smem, N / kP2W, out->nz, 4,
+                     true, out, p0, s, op);
+}
+static inline int launch_rst2(const RestrictOp& op, bfp_vec_s* out, const WinParams& p0,
+                              cudaStream_t s) {
+  const int64_t Nc = int64_t(1) << out->l;
+  return launch_wave(rst2_win_kernel<MODE_QCOMP>, rst2_win_kernel<MODE_NNQ>,
+                     rst2_win_kernel<MODE_RECOMPUTE>, kR2T, kR2Smem, Nc / kR2W, out->nz, 2,
+                     false, out, p0, s, op);
 }
 
 // stencil ops on int32 grids of 2-D / 3-D with N >= 128 use the register march

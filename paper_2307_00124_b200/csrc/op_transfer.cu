@@ -42,6 +42,7 @@ int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.l = r->l;
   op.zc = out->z0;
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 6) return launch_rst3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 9) return launch_rst2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
@@ -60,6 +61,7 @@ int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.zf = out->z0;
   op.zp = out->z0 - 2 * xc->z0;
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
@@ -75,6 +77,7 @@ int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_
   op.zf = y->z0;
   op.zp = y->z0 - 2 * ec->z0;
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
