@@ -101,6 +101,14 @@ typedef struct {
   int64_t m, q, e;
 } bfp_scalar_t;
 
+/* a positive extended-precision constant: (hi 2^64 + lo) 2^e, plus a nonzero tail below
+   lo when sticky != 0 (the top 128 bits of an ExtFloat) */
+typedef struct {
+  uint64_t hi, lo;
+  int64_t e;
+  int32_t sticky, pad;
+} bfp_xf_t;
+
 int bfp_axpby(bfp_vec_t x, bfp_vec_t y, bfp_scalar_t alpha, bfp_scalar_t beta, int mode,
               int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma, int force_recompute,
               bfp_vec_t out, void* stream);
@@ -192,6 +200,17 @@ typedef struct {
   /* levels whose padded grid has <= fuse_points points run as one fused CTA with their
      vectors staged in shared memory; 0 = off, -1 = library default */
   int fuse_points;
+  /* reference-algorithm mode (P/src/multigrid.cpp:430-518), d = 1:
+     Chebyshev V(1,0) cycles, IR (r = A x - b, x - y) and FMG (fresh ir per n_ir, level 1
+     = zero_vec) on A = tridiag(-1/2, 1, -1/2), P = linear interpolation, R = 2 P^T,
+     operators quantize_csr'd at wcheck / wdot / w, coarsest level 1, gamma = Table 1
+     (gamma_policy_eval, :121-155) evaluated exactly with one final round-up.  The host
+     supplies the derived Chebyshev scalars: ref_c1 = c1 rounded to the hierarchy
+     precision (ExtFloat), ref_kres = add_up(2 c1, 1) / 4, ref_c1d / ref_c2d[l] = c1 / c2
+     floor-quantised at wdot_l (quantize_scalar_floor); rhs_kind 1 = h^2/2 d pi^2 sin. */
+  int ref_mode;
+  bfp_xf_t ref_c1, ref_kres;
+  bfp_scalar_t ref_c1d[32], ref_c2d[32];
 } bfp_mg_config_t;
 
 typedef struct {

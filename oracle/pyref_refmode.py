@@ -1,0 +1,297 @@
+"""Reference-algorithm parity mode, 1-D: a big-int restatement of the
+reference solver P/src/multigrid.cpp:430-518 -- Chebyshev V(1,0) cycles, IR and FMG
+with the Table-1 gamma chain (:121-155) -- on the reference's own 1-D p = 1 operators
+after the D = I scaling (P/src/multigrid.cpp:278-306):
+
+  A_j = tridiag(-1/2, 1, -1/2)   P_j = [1/2, 1, 1/2] (linear interpolation)
+  R_j = D_c^-1 P^T D_f = 2 P^T   (D = 2/h, so D_f / D_c = 2)
+
+Operators are quantised with quantize_csr (:216-229) at wcheck / wdot / w, the
+Chebyshev coefficients with chebyshev_coeffs_q (:183-193) from injected rho and eta
+(the power iteration of max_gen_eig_upper is not restated), rounded to nearest at the
+hierarchy precision (ExtFloat::from_mpq, P/src/extfloat.cpp:21-25) and floor-quantised
+at wdot (quantize_scalar_floor, :233-241).  The right-hand side is injected per level.
+
+The gamma chain follows gamma_policy_eval (:121-155) with ExtFloat semantics:
+mul_up / add_up round up at the operands' maximal precision (P/src/extfloat.cpp:131-140),
+exact_norm_ext (:109-117) is exact, scalar_up (:84-105) ceils to q_gamma = 16.
+
+TEST INFRASTRUCTURE ONLY (the checker of the GPU's ref mode), never the product.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Dict, List, Optional, Sequence
+
+from . import pyref as P
+
+Q_GAMMA = 16
+
+
+# ---------------------------------------------------------------------------
+# ExtFloat values: (exact rational, precision in bits)
+
+@dataclass(frozen=True)
+class XF:
+    v: Fraction
+    prec: int
+
+
+def _round(v: Fraction, prec: int, up: bool) -> Fraction:
+    """v >= 0 rounded to prec significant bits: upward (MPFR_RNDU) or to nearest, ties
+    to even (MPFR_RNDN)."""
+    if v == 0:
+        return v
+    assert v > 0
+    e = v.numerator.bit_length() - v.denominator.bit_length()
+    if Fraction(2) ** e > v:
+        e -= 1
+    s = prec - 1 - e  # v 2^s in [2^(prec-1), 2^prec)
+    scaled = v * (Fraction(2) ** s)
+    fl = scaled.numerator // scaled.denominator
+    rem = scaled - fl
+    if up:
+        q = fl + (1 if rem > 0 else 0)
+    else:
+        q = fl + (1 if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl & 1) else 0)
+    return Fraction(q) / (Fraction(2) ** s)
+
+
+def _dyadic(v: Fraction):
+    den = v.denominator
+    k = -(den.bit_length() - 1)
+    assert den == 1 << (-k), "dyadic value"
+    return v.numerator, k
+
+
+def xf_exact_norm(b: P.Block) -> XF:
+    """exact_norm_ext (P/src/multigrid.cpp:109-117)."""
+    mx = max((abs(v) for v in b.m), default=0)
+    prec = max(64, P.msb(mx) + 8)
+    return XF(Fraction(mx) * Fraction(2) ** b.e, prec)
+
+
+def mul_up(a: XF, b: XF) -> XF:
+    p = max(a.prec, b.prec)
+    return XF(_round(a.v * b.v, p, True), p)
+
+
+def add_up(a: XF, b: XF) -> XF:
+    p = max(a.prec, b.prec)
+    return XF(_round(a.v + b.v, p, True), p)
+
+
+def scalar_up(v: XF, q_gamma: int = Q_GAMMA) -> P.Block:
+    """scalar_up (P/src/multigrid.cpp:84-105): ceil to a q_gamma-bit scalar."""
+    if v.v <= 0:
+        return P.Block.scalar(1 << (q_gamma - 2), q_gamma, -400 - (q_gamma - 2))
+    z, k = _dyadic(v.v)
+    s = P.msb(z) - q_gamma
+    if s <= 0:
+        m = z << (-s)
+    else:
+        m = -((-z) >> s)  # cdiv_q_2exp
+        if P.msb(m) > q_gamma:
+            m >>= 1
+            s += 1
+    return P.Block.scalar(m, q_gamma, k + s)
+
+
+# ---------------------------------------------------------------------------
+# operators and scalars
+
+def quantize_values(vals: Sequence[Fraction], w: int):
+    """quantize_csr (P/src/multigrid.cpp:216-229) on dyadic values: (mantissas, e)."""
+    zk = [(0, 0) if v == 0 else _dyadic(v) for v in vals]
+    top = None
+    for z, k in zk:
+        if z:
+            t = P.msb(z) + k
+            top = t if top is None else max(top, t)
+    if top is None:
+        return [0] * len(zk), 0
+    e = top - w
+    return [P.shift_floor(z, e - k) for z, k in zk], e
+
+
+def csr_from(rows: int, cols: int, entries: Dict[int, List[tuple]], w: int) -> P.Csr:
+    rowptr, col, vals = [0], [], []
+    for i in range(rows):
+        for c, v in sorted(entries.get(i, [])):
+            col.append(c)
+            vals.append(v)
+        rowptr.append(len(col))
+    m, e = quantize_values(vals, w)
+    return P.Csr(rows, cols, rowptr, col, m, w, e)
+
+
+def op_a(j: int, w: int) -> P.Csr:
+    n = (1 << j) - 1
+    ent = {i: [(c, Fraction(1) if c == i else Fraction(-1, 2)) for c in (i - 1, i, i + 1)
+               if 0 <= c < n] for i in range(n)}
+    return csr_from(n, n, ent, w)
+
+
+def op_p(j: int, w: int) -> P.Csr:
+    """Linear interpolation level j-1 -> j (fine row 2k+1 <- coarse k)."""
+    nf, nc = (1 << j) - 1, (1 << (j - 1)) - 1
+    ent: Dict[int, List[tuple]] = {}
+    for k in range(nc):
+        for i, wgt in ((2 * k, Fraction(1, 2)), (2 * k + 1, Fraction(1)), (2 * k + 2, Fraction(1, 2))):
+            ent.setdefault(i, []).append((k, wgt))
+    return csr_from(nf, nc, ent, w)
+
+
+def op_r(j: int, w: int) -> P.Csr:
+    """R = 2 P^T: coarse row k <- fine 2k, 2k+1, 2k+2 with weights (1, 2, 1)."""
+    nf, nc = (1 << j) - 1, (1 << (j - 1)) - 1
+    ent = {k: [(2 * k, Fraction(1)), (2 * k + 1, Fraction(2)), (2 * k + 2, Fraction(1))]
+           for k in range(nc)}
+    return csr_from(nc, nf, ent, w)
+
+
+NORM_A_UP = Fraction(2)  # ||tridiag(-1/2, 1, -1/2)||_inf
+NORM_R_UP = Fraction(4)  # ||2 P^T||_inf
+
+
+def chebyshev(rho: Fraction, eta: Fraction):
+    """chebyshev_coeffs_q (P/src/multigrid.cpp:183-193)."""
+    alpha = (1 + eta) * rho / 2
+    c = (1 - eta) * rho / 2
+    beta = alpha - c * c / (2 * alpha)
+    return 2 / beta, Fraction(-1) / (alpha * beta)
+
+
+def eta_rational(eta: float) -> Fraction:
+    """Hierarchy::set_eta (P/src/multigrid.cpp:313-323): two-decimal etas are exact."""
+    num = round(eta * 100.0)
+    if abs(eta - num / 100.0) < 1e-12:
+        return Fraction(num, 100)
+    return Fraction(eta)
+
+
+def quantize_scalar_floor(v: Fraction, w: int) -> P.Block:
+    """quantize_scalar_floor (P/src/multigrid.cpp:233-241) of a dyadic value."""
+    z, k = _dyadic(v)
+    b = P.quantize_exact([z], [k], w)
+    return P.Block.scalar(b.m[0], w, b.e)
+
+
+# ---------------------------------------------------------------------------
+# the solver
+
+@dataclass
+class RefConfig:
+    l_fine: int
+    w: List[int]        # per level (index = level), 1..l_fine
+    wdot: List[int]
+    wcheck: List[int]
+    rho: float
+    eta: float
+    cycles: int = 1     # IR iterations (or n_ir per FMG level)
+    fmg: bool = False
+    ext_prec: int = 400  # Hierarchy precision (ExtFloat)
+    x0: Optional[P.Block] = None
+
+
+@dataclass
+class RefResult:
+    x: P.Block = None
+    history: List[float] = field(default_factory=list)
+    trace: List[tuple] = field(default_factory=list)
+
+
+STEP_IDS = {"ir-residual": 0, "ir-correction": 1, "v-relax": 3, "v-residual": 4,
+            "v-restrict": 5, "v-correct": 6, "fmg-prolong": 7}
+W_ADD = {"ir-correction": 0, "v-relax": 2, "v-residual": 4, "v-restrict": 6,
+         "v-correct": 1, "fmg-prolong": 0}  # GammaPolicy::default_w_add (:62-73)
+
+
+class RefMg:
+    def __init__(self, cfg: RefConfig, rhs: Dict[int, P.Block]):
+        self.cfg, self.res = cfg, RefResult()
+        self.b = rhs
+        self.last_res: Dict[int, XF] = {}
+        rho = Fraction(cfg.rho)
+        eta = eta_rational(cfg.eta)
+        c1, c2 = chebyshev(rho, eta)
+        self.c1x = XF(_round(c1, cfg.ext_prec, False), cfg.ext_prec)
+        c2x = -_round(-c2, cfg.ext_prec, False)
+        self.c1d = {j: quantize_scalar_floor(self.c1x.v, cfg.wdot[j]) for j in range(1, cfg.l_fine + 1)}
+        self.c2d = {j: quantize_scalar_floor(c2x, cfg.wdot[j]) for j in range(1, cfg.l_fine + 1)}
+
+    def step(self, name, level, k, w_out, g: XF, ir_iter=1):
+        w_add = (5 if ir_iter == 1 else 4) if name == "ir-residual" else W_ADD[name]
+        gam = scalar_up(g)
+        out, fl = P.qcomp(k, w_out, w_out + w_add, gam)
+        self.res.trace.append((STEP_IDS[name], level, w_out, w_out + w_add, gam.m[0], gam.e,
+                               int(fl.overflow), int(fl.underflow), int(fl.recomputed), 1))
+        return out
+
+    def vcycle(self, lev: int, r: P.Block) -> P.Block:
+        """P/src/multigrid.cpp:430-456."""
+        cfg = self.cfg
+        wd = cfg.wdot[lev]
+        rn = xf_exact_norm(r)
+        ad = op_a(lev, wd)
+        y = self.step("v-relax", lev, P.EgemvKernel(ad, r, r, self.c2d[lev], self.c1d[lev]), wd,
+                      mul_up(self.c1x, rn))
+        if lev > 1:
+            two_c1 = XF(self.c1x.v * 2, self.c1x.prec)
+            g = mul_up(add_up(two_c1, XF(Fraction(1), self.c1x.prec)), rn)
+            g = XF(g.v / 4, g.prec)
+            rv = self.step("v-residual", lev, P.EgemvKernel(ad, y, r, P.bfp_one(), P.bfp_minus_one()),
+                           wd, g)
+            rc = self.step("v-restrict", lev, P.EspmvKernel(op_r(lev, wd), rv), wd,
+                           mul_up(XF(NORM_R_UP, cfg.ext_prec), xf_exact_norm(rv)))
+            d = self.vcycle(lev - 1, rc)
+            y = self.step("v-correct", lev,
+                          P.EgemvKernel(op_p(lev, wd), d, y, P.bfp_minus_one(), P.bfp_one()), wd,
+                          add_up(xf_exact_norm(y), xf_exact_norm(d)))
+        return y
+
+    def ir(self, lev: int, x: P.Block, iters: int) -> P.Block:
+        """P/src/multigrid.cpp:458-500 (tol < 0: exactly iters iterations)."""
+        cfg = self.cfg
+        b = self.b[lev]
+        for i in range(1, iters + 1):
+            if i > 1:
+                g = self.last_res[lev]
+            elif lev > 1 and (lev - 1) in self.last_res:
+                g = self.last_res[lev - 1]
+            else:
+                g = add_up(mul_up(XF(NORM_A_UP, cfg.ext_prec), xf_exact_norm(x)), xf_exact_norm(b))
+            r = self.step("ir-residual", lev,
+                          P.EgemvKernel(op_a(lev, cfg.wcheck[lev]), x, b, P.bfp_one(), P.bfp_minus_one()),
+                          cfg.wdot[lev], g, ir_iter=i)
+            self.last_res[lev] = xf_exact_norm(r)
+            mx = max((abs(v) for v in r.m), default=0)
+            self.res.history.append(float(Fraction(mx) * Fraction(2) ** r.e))
+            y = self.vcycle(lev, r)
+            x = self.step("ir-correction", lev, P.EaxpbyKernel(x, y, P.bfp_one(), P.bfp_minus_one()),
+                          cfg.w[lev], add_up(xf_exact_norm(x), xf_exact_norm(y)))
+        return x
+
+    def fmg(self, lev: int) -> P.Block:
+        """P/src/multigrid.cpp:502-518 (each IR iteration a fresh ir(..., 1, -1) call)."""
+        cfg = self.cfg
+        if lev == 1:
+            x = P.zero_vec(1, cfg.w[1])
+        else:
+            xc = self.fmg(lev - 1)
+            x = self.step("fmg-prolong", lev, P.EspmvKernel(op_p(lev, cfg.w[lev]), xc), cfg.w[lev],
+                          xf_exact_norm(xc))
+        for _ in range(cfg.cycles):
+            x = self.ir(lev, x, 1)
+        return x
+
+    def run(self) -> RefResult:
+        cfg = self.cfg
+        if cfg.fmg:
+            self.res.x = self.fmg(cfg.l_fine)
+        else:
+            l = cfg.l_fine
+            x = cfg.x0 if cfg.x0 is not None else P.zero_vec((1 << l) - 1, cfg.w[l])
+            self.res.x = self.ir(l, x, cfg.cycles)
+        return self.res

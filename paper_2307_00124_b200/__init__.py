@@ -68,12 +68,19 @@ class _Scalar(C.Structure):
     _fields_ = [("m", C.c_int64), ("q", C.c_int64), ("e", C.c_int64)]
 
 
+class XfC(C.Structure):  # bfp_xf_t
+    _fields_ = [("hi", C.c_uint64), ("lo", C.c_uint64), ("e", C.c_int64), ("sticky", C.c_int32),
+                ("pad", C.c_int32)]
+
+
 class MgConfig(C.Structure):
     _fields_ = [("d", C.c_int), ("l_fine", C.c_int), ("l_coarse", C.c_int), ("nu1", C.c_int),
                 ("nu2", C.c_int), ("n_coarse", C.c_int), ("cycles", C.c_int), ("fmg", C.c_int),
                 ("nonnormalized", C.c_int), ("x0_random", C.c_int), ("rhs_kind", C.c_int),
                 ("qc", C.c_int), ("seed", C.c_uint64), ("p", C.c_int * 32), ("pd", C.c_int * 32),
-                ("pc", C.c_int * 32), ("w_add_cap", C.c_int), ("fuse_points", C.c_int)]
+                ("pc", C.c_int * 32), ("w_add_cap", C.c_int), ("fuse_points", C.c_int),
+                ("ref_mode", C.c_int), ("ref_c1", XfC), ("ref_kres", XfC),
+                ("ref_c1d", _Scalar * 32), ("ref_c2d", _Scalar * 32)]
 
 
 class TraceRec(C.Structure):
@@ -634,6 +641,27 @@ def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=Fa
         cfg.p[i], cfg.pd[i], cfg.pc[i] = p[i], pd[i], pc[i]
     cfg.w_add_cap = w_add_cap
     cfg.fuse_points = fuse_points
+    return cfg
+
+
+def mg_config_ref(l_fine, rho, eta, w, wdot=None, wcheck=None, cycles=1, fmg=False,
+                  x0_random=False, rhs_kind=1, seed=1, ext_prec=400, w_add_cap=-1) -> MgConfig:
+    """Reference-algorithm mode (1-D): the reference solver P/src/multigrid.cpp:430-518 on
+    its own p = 1 operators, see include/bfpmg_b200.h.  rho / eta: the Chebyshev
+    parameters (Hierarchy::set_eta); w / wdot / wcheck: PrecisionSchedule widths (int or
+    per-level list, index = level, levels 1..l_fine)."""
+    from . import refmode
+    cfg = mg_config(1, l_fine, l_coarse=1, cycles=cycles, fmg=fmg, x0_random=x0_random,
+                    rhs_kind=rhs_kind, seed=seed, p=w, pd=wdot, pc=wcheck, w_add_cap=w_add_cap,
+                    fuse_points=0)
+    cfg.ref_mode = 1
+    c1, kres, c1d, c2d = refmode.chebyshev_scalars(rho, eta, ext_prec,
+                                                   [cfg.pd[l] or cfg.p[l] for l in range(32)])
+    for dst, src in ((cfg.ref_c1, c1), (cfg.ref_kres, kres)):
+        dst.hi, dst.lo, dst.e, dst.sticky = src
+    for l in range(1, l_fine + 1):
+        cfg.ref_c1d[l].m, cfg.ref_c1d[l].q, cfg.ref_c1d[l].e = c1d[l]
+        cfg.ref_c2d[l].m, cfg.ref_c2d[l].q, cfg.ref_c2d[l].e = c2d[l]
     return cfg
 
 

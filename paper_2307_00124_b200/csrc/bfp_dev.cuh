@@ -232,13 +232,16 @@ struct GTerm {
   const Hdr* v;    // nullptr: X = 1
   int64_t cm, ce;  // cm == 0: no coefficient
   int32_t kind;    // 0 = norm(v), 1 = ulp(v) (zero if v is all zero)
-  int32_t pad;
+  int32_t sticky;  // exact rules: the coefficient has nonzero bits below cm_hi:cm
+  uint64_t cm_hi;  // exact rules: 128-bit coefficient (cm_hi:cm as unsigned)
 };
 struct GammaRule {
   int32_t literal;  // 1: (lm, le) as given
   int32_t nterms;
   int64_t lm, le;
   GTerm t[3];
+  int32_t exact;  // 1: sum_t c_t X_t evaluated exactly, one round-up at the end
+  int32_t pad;
 };
 
 __device__ inline G15 gterm_eval(const GTerm& t) {
@@ -253,11 +256,141 @@ __device__ inline G15 gterm_eval(const GTerm& t) {
   if (t.cm != 0) x = g15_mul(g15_from((uint64_t)t.cm, t.ce), x);
   return x;
 }
+// Exact gamma rules (reference-algorithm mode, gamma_policy_eval P/src/multigrid.cpp:
+// 121-155): the reference's ExtFloat chain rounds up at >= 64 / 400 bits and scalar_up
+// then ceils to 15 significant bits; nested round-ups to a coarser grid equal one, so
+// gamma = ceil_15(sum_t c_t X_t) of the exact value.  Terms are 128-bit coefficients
+// (+ a sticky tail) times 64-bit block norms, accumulated in a 256-bit window.
+struct X256 {
+  uint64_t w[4];  // w[3] most significant; value = w * 2^e (+ tail if sticky)
+  int64_t e;
+  bool sticky;
+};
+__device__ inline int x256_bitlen(const X256& a) {
+  for (int i = 3; i >= 0; --i)
+    if (a.w[i]) return 64 * i + bitlen_h(a.w[i]);
+  return 0;
+}
+// shift left by s (0 <= s < 256), bits never lost (caller guarantees headroom)
+__device__ inline void x256_shl(X256& a, int s) {
+  while (s >= 64) {
+    a.w[3] = a.w[2]; a.w[2] = a.w[1]; a.w[1] = a.w[0]; a.w[0] = 0;
+    s -= 64;
+    a.e -= 64;
+  }
+  if (s) {
+    for (int i = 3; i > 0; --i) a.w[i] = (a.w[i] << s) | (a.w[i - 1] >> (64 - s));
+    a.w[0] <<= s;
+    a.e -= s;
+  }
+}
+// shift right by s, dropped bits go to sticky
+__device__ inline void x256_shr(X256& a, int64_t s) {
+  if (s >= 256) {
+    a.sticky = a.sticky || a.w[0] || a.w[1] || a.w[2] || a.w[3];
+    a.w[0] = a.w[1] = a.w[2] = a.w[3] = 0;
+    a.e += s;
+    return;
+  }
+  while (s >= 64) {
+    a.sticky = a.sticky || a.w[0];
+    a.w[0] = a.w[1]; a.w[1] = a.w[2]; a.w[2] = a.w[3]; a.w[3] = 0;
+    s -= 64;
+    a.e += 64;
+  }
+  if (s) {
+    a.sticky = a.sticky || (a.w[0] << (64 - s));
+    for (int i = 0; i < 3; ++i) a.w[i] = (a.w[i] >> s) | (a.w[i + 1] << (64 - s));
+    a.w[3] >>= s;
+    a.e += s;
+  }
+}
+__device__ inline void x256_norm(X256& a) {  // top bit at position 254 (one bit of headroom)
+  const int b = x256_bitlen(a);
+  if (b == 0) return;
+  if (b < 255) x256_shl(a, 255 - b);
+  else if (b > 255) x256_shr(a, b - 255);
+}
+__device__ inline X256 x256_term(const GTerm& t) {
+  X256 r = {{0, 0, 0, 0}, 0, false};
+  uint64_t X;
+  int64_t ex;
+  if (t.v == nullptr) {
+    X = 1;
+    ex = 0;
+  } else {
+    X = max_abs(t.v);
+    ex = t.v->e;
+  }
+  if (X == 0) return r;
+  const uint64_t clo = (uint64_t)t.cm, chi = t.cm_hi;
+  // (chi:clo) * X  -> 192 bits
+  const u128 p0 = (u128)clo * X, p1 = (u128)chi * X;
+  r.w[0] = (uint64_t)p0;
+  const u128 mid = (p0 >> 64) + (uint64_t)p1;
+  r.w[1] = (uint64_t)mid;
+  r.w[2] = (uint64_t)(p1 >> 64) + (uint64_t)(mid >> 64);
+  r.e = t.ce + ex;
+  r.sticky = t.sticky != 0;
+  return r;
+}
+__device__ inline void exact_gamma(const GammaRule& g, int64_t& gm, int64_t& ge) {
+  X256 acc = {{0, 0, 0, 0}, 0, false};
+  bool any = false;
+  for (int i = 0; i < g.nterms; ++i) {
+    X256 t = x256_term(g.t[i]);
+    if (!x256_bitlen(t) && !t.sticky) continue;
+    x256_norm(t);
+    if (!any) {
+      acc = t;
+      any = true;
+      continue;
+    }
+    // align to the larger exponent (both normalised at bit 254), add, renormalise
+    if (acc.e < t.e) {
+      X256 s = acc;
+      acc = t;
+      t = s;
+    }
+    x256_shr(t, acc.e - t.e);
+    uint64_t carry = 0;
+    for (int k = 0; k < 4; ++k) {
+      const u128 s = (u128)acc.w[k] + t.w[k] + carry;
+      acc.w[k] = (uint64_t)s;
+      carry = (uint64_t)(s >> 64);
+    }
+    acc.sticky = acc.sticky || t.sticky;
+    x256_norm(acc);
+  }
+  if (!any) {  // zero: degenerate gamma (scalar_up, :85-89)
+    gm = 1 << 14;
+    ge = -400 - 14;
+    return;
+  }
+  // ceil to 15 significant bits: the top 15 of the 255-bit window
+  const int sh = 255 - 15;
+  uint64_t m = acc.w[3] >> (sh - 192);
+  bool rest = acc.sticky || (acc.w[3] & ((1ull << (sh - 192)) - 1)) || acc.w[2] || acc.w[1] ||
+              acc.w[0];
+  int64_t e = acc.e + sh;
+  if (rest) ++m;
+  if (m == (1ull << 15)) {
+    m >>= 1;
+    ++e;
+  }
+  gm = (int64_t)m;
+  ge = e;
+}
+
 // returns (gm, ge) of the BFP scalar gamma (q = 16); degenerate 2^-400 if zero
 __device__ inline void gamma_eval(const GammaRule& r, int64_t& gm, int64_t& ge) {
   if (r.literal) {
     gm = r.lm;
     ge = r.le;
+    return;
+  }
+  if (r.exact) {
+    exact_gamma(r, gm, ge);
     return;
   }
   G15 acc{0, 0};

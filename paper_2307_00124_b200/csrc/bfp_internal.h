@@ -76,17 +76,23 @@ int window_finalize(bfp_vec_s* out, WinParams p, int stage, const int64_t* part,
 GammaRule gamma_literal(int64_t m, int64_t e);  // (declared for the solver too)
 
 // windowed ops (mode in p: MODE_QCOMP launches pass 1 + recompute, MODE_NNQ one pass)
+// operator representation overrides (reference-algorithm mode): kDefaultRep keeps the
+// config operators (stencil e_A = 2l, full weighting e_R = -2d, prolongation e_P = -d)
+constexpr int kDefaultRep = -0x40000000;
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
-            cudaStream_t s);
+            cudaStream_t s, int ea = kDefaultRep, int gs = 0);
 int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s* out,
               cudaStream_t s);
 int op_scal(bfp_vec_s* r, Scal c, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
 int op_axpby(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
              cudaStream_t s);
-int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
-int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s);
+int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s,
+                int er = kDefaultRep, int gs = 0);
+int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s,
+               int ep = kDefaultRep, int gs = 0);
 int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_s* out,
-                       cudaStream_t s);
+                       cudaStream_t s, int ep = kDefaultRep, int gs = 0,
+                       Scal al = Scal{1, 2, 0}, Scal be = Scal{1, 2, 0});
 
 int gen_uniform(bfp_vec_s* v, int64_t p, uint64_t seed, uint64_t stream_id, cudaStream_t s);
 int gen_sine(bfp_vec_s* v, int64_t p, cudaStream_t s);

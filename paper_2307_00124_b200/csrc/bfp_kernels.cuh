@@ -1341,7 +1341,7 @@ __global__ void __launch_bounds__(kR3T, 8)
   r.init();
   // plane sums T_p (weights 16) in int32 need eff_bits(r) <= 27, i.e. need <= 35 in 3-D;
   // the final combination is 64-bit
-  if (op.sr < 32 && need <= 35) {
+  if (op.sr < 32 && need <= 35 && op.gs == 0) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR3FS * kR3FT * 4);
     if (threadIdx.x == 0) {
       for (int k = 0; k < kR3B; ++k) mbar_init(&bar[k], 1);
@@ -1622,7 +1622,7 @@ __global__ void __launch_bounds__(kR2T, 8) rst2_win_kernel(RestrictOp op, Vec ou
   Red r;
   r.init();
   // row sums T_p (weights 4) in int32: eff_bits(r) <= 29, need = eff + 6 <= 35 in 2-D
-  if (op.sr < 32 && need <= 35) {
+  if (op.sr < 32 && need <= 35 && op.gs == 0) {
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR2FS * kR2FW * 4);
     if (threadIdx.x == 0) {
       for (int k = 0; k < kR2B; ++k) mbar_init(&bar[k], 1);

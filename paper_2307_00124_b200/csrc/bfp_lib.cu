@@ -74,7 +74,7 @@ __device__ __forceinline__ int64_t logical_of(const Vec& v, int64_t o, bool& pad
   const int64_t N = (int64_t)1 << v.l, m = N - 1, n = N - 1;
   const int64_t ix = o & m;
   if (v.dim == 1) {
-    pad = ix == m;
+    pad = ix == m || o > m;  // o > m: storage padding of the 1-D level 1 (N = 2)
     return ix;
   }
   if (v.dim == 2) {
@@ -380,7 +380,7 @@ int vec_alloc_slab(int dim, int level, int64_t n, int z_lo, int z_hi, int ebytes
     v->span = (n + 3) / 4 * 4;
     v->halo = 4;
   } else {
-    if (level < 2 || level > 30 || (int64_t)dim * level > 36) {
+    if (level < (dim == 1 ? 1 : 2) || level > 30 || (int64_t)dim * level > 36) {
       delete v;
       return BFP_ERR_ARG;
     }
@@ -395,6 +395,7 @@ int vec_alloc_slab(int dim, int level, int64_t n, int z_lo, int z_hi, int ebytes
       v->span *= N;
     }
     v->halo = dim == 1 ? 4 : 2 * (v->span / v->nz);
+    if (dim == 1 && v->span < 4) v->span = 4;  // level 1: one point + pad, padded to a 4-group
   }
   size_t bytes = (size_t)(v->span + 2 * v->halo) * ebytes;
   if (cudaMalloc(&v->base, bytes) != cudaSuccess) {

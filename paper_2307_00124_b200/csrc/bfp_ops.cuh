@@ -165,7 +165,8 @@ __device__ __forceinline__ void pad4(int dim, int l, int64_t o, bool pad[4], int
   const bool rowpad = plane_pad(dim, l, z0, o);
   const int64_t ix = o & mask;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) pad[j] = rowpad || (ix + j == mask);
+  // (ix + j > mask only for the 1-D level 1, N = 2, whose storage is padded to 4)
+  for (int j = 0; j < 4; ++j) pad[j] = rowpad || (ix + j >= mask);
 }
 
 // 32-bit stencil (used when the width bound proves |S x| < 2^31)
@@ -249,6 +250,10 @@ struct GemvOp {
   Vec x, y;
   Scal al, be;
   int dim, l, z0;  // z0: slab offset along the slowest axis (0 for full grids)
+  // operator representation: e_A (2l for the config stencil) and a mantissa scale 2^gs
+  // (reference-algorithm mode: a quantize_csr'd operator has mantissas 2^gs (2d, -1),
+  // e_A = its quantized exponent -- values equal, templates as in the reference)
+  int ea, gs;
   // derived (uniform per launch)
   int64_t sx, sy, d;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
@@ -257,22 +262,23 @@ struct GemvOp {
   bool swap;
   int P, Q;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t ge = 2 * l + x.hdr->e;  // e_A + e_x
+    const int64_t ge = ea + x.hdr->e;  // e_A + e_x
     axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
-    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1), by = zbits(y.hdr);
+    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1 + gs), by = zbits(y.hdr);
     need = combine_bits(al.m, bg, be.m, by, d);
     // z = X * P + Q * Y with (X, Y) = (g, y), P = alpha 2^d, Q = beta   when d >= 0
     //                         (X, Y) = (y, g), P = beta 2^-d, Q = alpha  when d < 0
     const int64_t ad = d >= 0 ? d : -d;
     const int64_t pm = d >= 0 ? al.m : be.m, qm = d >= 0 ? be.m : al.m;
     const int64_t bx_ = d >= 0 ? bg : by, by_ = d >= 0 ? by : bg;
-    narrow = need <= 63 && sx < 32 && sy < 32 && ad <= 30 && bg <= 31 && by <= 31 &&
+    narrow = l >= 2 && need <= 63 && sx < 32 && sy < 32 && ad <= 30 && bg <= 31 && by <= 31 &&
              fits32(pm) && fits32(qm) && msb(pm) + ad <= 32 &&
              (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
     w64 = bg <= 62 && sx < 64 && sy < 64 && msb(al.m) + bg <= 63 && msb(be.m) + by <= 63;
     fwi = w64 && need <= 127 && ad < 64;
+    if (gs) narrow = w64 = fwi = false;  // scaled mantissas: the generic exact path
     swap = d < 0;
     P = narrow ? (int)(pm << ad) : 0;
     Q = (int)qm;
@@ -330,7 +336,8 @@ struct GemvOp {
     bool pad[4];
     pad4(dim, l, o, pad, z0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) z[j] = pad[j] ? A(0) : combine<A>(al.m, g[j], be.m, (A)yv[j], d);
+    for (int j = 0; j < 4; ++j)
+      z[j] = pad[j] ? A(0) : combine<A>(al.m, g[j] << gs, be.m, (A)yv[j], d);
   }
 };
 
@@ -358,7 +365,8 @@ struct JacobiOp {
     need = combine_bits(1, bx, c.m, br, d2);
     // r = -g 2^d1 + b (d1 >= 0) or b 2^-d1 - g (d1 < 0): one IMAD.WIDE either way;
     // z = x 2^d2 + c r (d2 >= 0)
-    narrow = bg <= 31 && zbits(b.hdr) <= 31 && c.m >= 0 && c.m <= 0x7fffffff && need <= 63 &&
+    narrow = l >= 2 && bg <= 31 && zbits(b.hdr) <= 31 && c.m >= 0 && c.m <= 0x7fffffff &&
+             need <= 63 &&
              sx < 32 && sb < 32 && d1 >= -30 && d1 <= 30 && d2 >= 0 && d2 <= 62 && d2 != 31 &&
              bx <= 31 && (bx == 0 || bx + d2 <= 63);
     w64 = bg <= 62 && zbits(b.hdr) <= 62 && sx < 64 && sb < 64;
@@ -479,13 +487,14 @@ struct RestrictOp {
   Vec r;       // fine, level l
   int dim, l;  // fine level
   int zc;      // slab: global index of the output's local plane 0 (coarse)
+  int er, gs;  // e_R (-2 dim: full weighting) and mantissa scale 2^gs (reference mode)
   int64_t sr;
   bool narrow;  // int32 storage, |R r| < 2^31: vectorised 32-bit path
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    e_star = -2 * dim + r.hdr->e;
+    e_star = er + r.hdr->e;
     sr = r.hdr->shift;
-    need = eff_bits(r.hdr) + 2 * dim + 2;
-    narrow = need <= 31 && sr < 32 && dim >= 2;
+    need = eff_bits(r.hdr) + 2 * dim + 2 + gs;
+    narrow = need <= 31 && sr < 32 && dim >= 2 && gs == 0;
   }
   // fine line weights (1,2,1) for 4 consecutive coarse points from fine row base f
   template <bool NC>
@@ -558,7 +567,7 @@ struct RestrictOp {
           acc = pm + 2 * p0 + pp;
         }
       }
-      z[j] = acc;
+      z[j] = acc << gs;
     }
   }
 };
@@ -636,6 +645,7 @@ struct ProlongOp {
   Vec xc;
   int dim, l;  // fine level
   int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
+  int ep, gs;  // e_P (-dim) and mantissa scale 2^gs (reference mode)
   int64_t sc;
   bool narrow;  // int32 storage and |P xc| < 2^31: vectorised coarse rows
   static constexpr bool kCorr = false;
@@ -645,10 +655,10 @@ struct ProlongOp {
   __device__ __forceinline__ int shy() const { return 0; }
   __device__ __forceinline__ int64_t corr(int g, int yv) const { (void)yv; return g; }
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    e_star = -dim + xc.hdr->e;
+    e_star = ep + xc.hdr->e;
     sc = xc.hdr->shift;
-    need = eff_bits(xc.hdr) + dim + 2;
-    narrow = need <= 31 && sc < 32;
+    need = eff_bits(xc.hdr) + dim + 2 + gs;
+    narrow = need <= 31 && sc < 32 && gs == 0;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -665,7 +675,7 @@ struct ProlongOp {
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j, zp);
+      z[j] = pad[j] ? A(0) : prolong_at<M, A, NC>(xc, sc, dim, l, o + j, zp) << gs;
   }
 };
 
@@ -674,6 +684,8 @@ struct ProlongCorrectOp {
   Vec ec, y;
   int dim, l;
   int zf, zp;  // slab: fine z0 and the slowest-axis shift of prolong_at
+  int ep, gs;  // e_P (-dim) and mantissa scale 2^gs (reference mode)
+  Scal al, be;  // z = al P ec + be y (config: +1, +1; reference V-correct: -1, +1)
   int64_t sc, sy, d;
   bool narrow, swap;  // int32 storage: g = P ec in 32 bits, z = X 2^|d| + Y (one IMAD.WIDE)
   int P;
@@ -687,14 +699,15 @@ struct ProlongCorrectOp {
     return (int64_t)X * (int64_t)P + (int64_t)Y;
   }
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t ge = -dim + ec.hdr->e;
-    axpby_setup(ge, y.hdr->e, d, e_star);
+    const int64_t ge = ep + ec.hdr->e;
+    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
     sc = ec.hdr->shift;
     sy = y.hdr->shift;
-    int64_t bg = grow(zbits(ec.hdr), dim + 2), by = zbits(y.hdr);
-    need = combine_bits(1, bg, 1, by, d);
+    int64_t bg = grow(zbits(ec.hdr), dim + 2 + gs), by = zbits(y.hdr);
+    need = combine_bits(al.m, bg, be.m, by, d);
     const int64_t ad = d >= 0 ? d : -d;
-    narrow = need <= 63 && bg <= 31 && by <= 31 && ad <= 30 && sc < 32 && sy < 32;
+    narrow = need <= 63 && bg <= 31 && by <= 31 && ad <= 30 && sc < 32 && sy < 32 && gs == 0 &&
+             al.m == 1 && be.m == 1;
     swap = d < 0;
     P = narrow ? (1 << (int)ad) : 0;
   }
@@ -720,8 +733,8 @@ struct ProlongCorrectOp {
     V4<M, NC>::load(y, o, sy, yv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      A g = prolong_at<M, A, NC>(ec, sc, dim, l, o + j, zp);
-      z[j] = pad[j] ? A(0) : combine<A>(1, g, 1, (A)yv[j], d);
+      A g = prolong_at<M, A, NC>(ec, sc, dim, l, o + j, zp) << gs;
+      z[j] = pad[j] ? A(0) : combine<A>(al.m, g, be.m, (A)yv[j], d);
     }
   }
 };

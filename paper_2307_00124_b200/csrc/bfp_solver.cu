@@ -55,6 +55,7 @@ struct PlanOp {
   int n_arena = 0, arena_bytes = 0;
   bool shard = false;  // output is a slab: partial window + collectives
   int halo = 0;        // HALO_LO / HALO_HI planes of `a` exchanged before the op
+  int rep_e = kDefaultRep, rep_gs = 0;  // operator representation (reference mode)
 };
 
 int fused_kind(int k) {
@@ -376,7 +377,198 @@ struct RankSolver {
     return BFP_OK;
   }
 
+  // ---- reference-algorithm mode (cfg.ref_mode, d = 1) --------------------------------
+  // exact gamma terms: X = norm of v, coefficient c (128-bit + sticky) 2^ce
+  static GTerm xterm(const bfp_vec_s* v, const bfp_xf_t& c) {
+    GTerm t;
+    memset(&t, 0, sizeof(t));
+    t.v = v->hdr;
+    t.cm = (int64_t)c.lo;
+    t.cm_hi = c.hi;
+    t.ce = c.e;
+    t.sticky = c.sticky;
+    return t;
+  }
+  static bfp_xf_t xint(uint64_t v) { return bfp_xf_t{0, v, 0, 0, 0}; }
+  static GammaRule xrule(std::initializer_list<GTerm> ts) {
+    GammaRule g = rule(ts);
+    g.exact = 1;
+    return g;
+  }
+  int64_t wr(int l) const { return cfg.p[l]; }
+  bfp_vec_s* ref_last[33] = {};  // last IR residual buffer per level (SolverContext)
+  // operator representations of quantize_csr at width w (pyref_refmode.quantize_values):
+  // A: mantissas 2^(w-3) (-1, 2, -1), e_A = 2 - w;  P: 2^(w-3) taps, e_P = 2 - w;
+  // R = 2 P^T: 2^(w-3) (1, 2, 1), e_R = 3 - w
+  PlanOp ref_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, int w, bfp_vec_s* out) {
+    PlanOp o;
+    o.kind = OK_GEMV;
+    o.a = x;
+    o.b = y;
+    o.out = out;
+    o.s1 = al;
+    o.s2 = be;
+    o.rep_e = 2 - w;
+    o.rep_gs = w - 3;
+    return o;
+  }
+  bfp_vec_s* vcycle_ref(int l, bfp_vec_s* r) {  // P/src/multigrid.cpp:430-456
+    LevelBufs& L = lev[l];
+    const int wd = (int)wd_(l);
+    bfp_vec_s *y = L.e[0], *y2 = L.e[1];
+    const Scal c1d{cfg.ref_c1d[l].m, cfg.ref_c1d[l].q, cfg.ref_c1d[l].e};
+    const Scal c2d{cfg.ref_c2d[l].m, cfg.ref_c2d[l].q, cfg.ref_c2d[l].e};
+    step(ST_RELAX, l, ref_gemv(r, r, c2d, c1d, wd, y), wd, xrule({xterm(r, cfg.ref_c1)}), 2);
+    if (l > 1) {
+      step(ST_V_RES, l, ref_gemv(y, r, Scal{1, 2, 0}, Scal{-1, 1, 0}, wd, L.rv), wd,
+           xrule({xterm(r, cfg.ref_kres)}), 4);
+      LevelBufs& Lc = lev[l - 1];
+      PlanOp rs;
+      rs.kind = OK_RESTRICT;
+      rs.a = L.rv;
+      rs.out = Lc.vr;
+      rs.rep_e = 3 - wd;
+      rs.rep_gs = wd - 3;
+      step(ST_RESTRICT, l, rs, wd, xrule({xterm(L.rv, xint(4))}), 6);
+      bfp_vec_s* d = vcycle_ref(l - 1, Lc.vr);
+      PlanOp pc;
+      pc.kind = OK_PCORR;
+      pc.a = d;
+      pc.b = y;
+      pc.out = y2;
+      pc.s1 = Scal{-1, 1, 0};
+      pc.s2 = Scal{1, 2, 0};
+      pc.rep_e = 2 - wd;
+      pc.rep_gs = wd - 3;
+      step(ST_V_CORR, l, pc, wd, xrule({xterm(y, xint(1)), xterm(d, xint(1))}), 1);
+      y = y2;
+    }
+    return y;
+  }
+  // IR (P/src/multigrid.cpp:458-500, tol < 0): returns the final iterate
+  bfp_vec_s* ir_ref(int l, bfp_vec_s* x, int iters) {
+    LevelBufs& L = lev[l];
+    for (int i = 1; i <= iters; ++i) {
+      GammaRule g;
+      if (i > 1)
+        g = xrule({xterm(ref_last[l], xint(1))});
+      else if (l > 1 && ref_last[l - 1])
+        g = xrule({xterm(ref_last[l - 1], xint(1))});
+      else
+        g = xrule({xterm(x, xint(2)), xterm(L.b, xint(1))});  // ||A||_inf = 2
+      bfp_vec_s* r = (ref_last[l] == L.r[0]) ? L.r[1] : L.r[0];
+      const int wc = (int)wc_(l);
+      ir_iter = i;
+      step(ST_IR_RES, l, ref_gemv(x, L.b, Scal{1, 2, 0}, Scal{-1, 1, 0}, wc, r), wd_(l), g,
+           i == 1 ? 5 : 4, true);
+      ref_last[l] = r;
+      bfp_vec_s* y = vcycle_ref(l, r);
+      bfp_vec_s* xn = (x == L.x[0]) ? L.x[1] : L.x[0];
+      PlanOp c;
+      c.kind = OK_AXPBY;
+      c.a = x;
+      c.b = y;
+      c.out = xn;
+      c.s1 = Scal{1, 2, 0};
+      c.s2 = Scal{-1, 1, 0};
+      step(ST_IR_CORR, l, c, wr(l), xrule({xterm(x, xint(1)), xterm(y, xint(1))}), 0);
+      x = xn;
+    }
+    return x;
+  }
+  bfp_vec_s* fmg_ref(int l) {  // P/src/multigrid.cpp:502-518
+    LevelBufs& L = lev[l];
+    bfp_vec_s* x = L.x[0];
+    if (l == 1) {
+      PlanOp z;
+      z.kind = OK_ZERO;
+      z.out = x;
+      z.q = wr(1);
+      plan.push_back(z);
+    } else {
+      bfp_vec_s* xc = fmg_ref(l - 1);
+      PlanOp o;
+      o.kind = OK_PROLONG;
+      o.a = xc;
+      o.out = x;
+      o.rep_e = 2 - (int)wr(l);
+      o.rep_gs = (int)wr(l) - 3;
+      step(ST_FMG_PROLONG, l, o, wr(l), xrule({xterm(xc, xint(1))}), 0);
+    }
+    for (int k = 0; k < cfg.cycles; ++k) x = ir_ref(l, x, 1);
+    return x;
+  }
+  int64_t wd_(int l) const { return wd(l); }
+  int64_t wc_(int l) const { return wc(l); }
+  int build_ref() {
+    const int lf = cfg.l_fine;
+    if (cfg.d != 1) return BFP_ERR_ARG;
+    int maxw = 0;
+    for (int l = 1; l <= lf; ++l) {
+      if (wr(l) < 3 || wd(l) < 3 || wc(l) < 3) return BFP_ERR_ARG;
+      const int cap = cfg.w_add_cap >= 0 ? std::min(cfg.w_add_cap, 6) : 6;
+      maxw = std::max(maxw, (int)std::max(std::max(wd(l), wr(l)), wc(l)) + cap);
+    }
+    ebytes = maxw <= 32 ? 4 : 8;
+    lev.assign(lf + 1, LevelBufs());
+    for (int l = 1; l <= lf; ++l) {
+      LevelBufs& L = lev[l];
+      L.l = l;
+      L.p = wr(l);
+      L.b = vec(l);
+      L.x[0] = vec(l);
+      L.x[1] = vec(l);
+      L.r[0] = vec(l);
+      L.r[1] = vec(l);
+      L.e[0] = vec(l);
+      L.e[1] = vec(l);
+      if (l > 1) L.rv = vec(l);
+      if (l < lf) L.vr = vec(l);
+      if (err) return err;
+    }
+    for (int l = 1; l <= lf; ++l) {  // right-hand sides (setup): D^-1 b at wcheck
+      LevelBufs& L = lev[l];
+      if (!cfg.fmg && l != lf) continue;
+      int rc;
+      if (cfg.rhs_kind == 1) {
+        rc = gen_sine(L.b, wc(l), 0);
+        if (!rc) {  // h^2 / 2 d pi^2 sin: exponent shift, the mantissas are unchanged
+          Hdr h;
+          if (cudaMemcpy(&h, L.b->hdr, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return BFP_ERR_CUDA;
+          if (h.max_m != 0 || h.min_m != 0) h.e -= 2 * l + 1;
+          if (cudaMemcpy(L.b->hdr, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess)
+            return BFP_ERR_CUDA;
+        }
+      } else if (cfg.rhs_kind == 0) {
+        rc = gen_uniform(L.b, wc(l), cfg.seed, 2, 0);
+      } else {
+        rc = set_zero(L.b, wc(l), 0);
+      }
+      if (rc) return rc;
+    }
+    if (cfg.fmg) {
+      x_final = fmg_ref(lf);
+    } else {
+      LevelBufs& L = lev[lf];
+      PlanOp init;
+      init.out = L.x[0];
+      init.q = L.p;
+      if (cfg.x0_random) {
+        init.kind = OK_UNIFORM;
+        init.seed = cfg.seed;
+        init.sid = 1;
+      } else {
+        init.kind = OK_ZERO;
+      }
+      plan.push_back(init);
+      x_final = ir_ref(lf, L.x[0], cfg.cycles);
+    }
+    return finish_build();
+  }
+
   int build() {
+    if (cfg.ref_mode) return build_ref();
     const int lf = cfg.l_fine, lc = cfg.l_coarse;
     int maxp = 0;
     for (int l = lc; l <= lf; ++l) {
@@ -459,6 +651,10 @@ struct RankSolver {
       x_final = ir(lf, L.x[0], cfg.cycles, &r_last);
       if (r_last) final_residual(lf, x_final, r_last);
     }
+    return finish_build();
+  }
+
+  int finish_build() {
     if (cudaMalloc(&d_trace, sizeof(TraceRec) * std::max(n_trace, 1)) != cudaSuccess ||
         cudaMalloc(&d_hist, sizeof(double) * std::max(n_hist, 1)) != cudaSuccess)
       return BFP_ERR_NOMEM;
@@ -570,13 +766,16 @@ struct RankSolver {
     switch (op.kind) {
       case OK_ZERO: return set_zero(op.out, op.q, s);
       case OK_UNIFORM: return gen_uniform(op.out, op.q, op.seed, op.sid, s);
-      case OK_GEMV: return op_gemv(op.a, op.b, op.s1, op.s2, p, op.out, s);
+      case OK_GEMV: return op_gemv(op.a, op.b, op.s1, op.s2, p, op.out, s, op.rep_e, op.rep_gs);
       case OK_JACOBI: return op_jacobi(op.a, op.b, op.s1, p, op.out, s);
       case OK_SCAL: return op_scal(op.a, op.s1, p, op.out, s);
       case OK_AXPBY: return op_axpby(op.a, op.b, op.s1, op.s2, p, op.out, s);
-      case OK_RESTRICT: return op_restrict(op.a, p, op.out, s);
-      case OK_PROLONG: return op_prolong(op.a, p, op.out, s);
-      case OK_PCORR: return op_prolong_correct(op.a, op.b, p, op.out, s);
+      case OK_RESTRICT: return op_restrict(op.a, p, op.out, s, op.rep_e, op.rep_gs);
+      case OK_PROLONG: return op_prolong(op.a, p, op.out, s, op.rep_e, op.rep_gs);
+      case OK_PCORR:
+        if (op.rep_e != kDefaultRep)
+          return op_prolong_correct(op.a, op.b, p, op.out, s, op.rep_e, op.rep_gs, op.s1, op.s2);
+        return op_prolong_correct(op.a, op.b, p, op.out, s);
       case OK_COPY:
         if (cudaMemcpyAsync(op.out->data, op.a->data, op.a->span * op.a->ebytes,
                             cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
@@ -811,6 +1010,14 @@ struct bfp_mg_s {
 extern "C" {
 
 static int check_cfg(const bfp_mg_config_t* cfg) {
+  if (cfg->ref_mode) {  // reference-algorithm mode: 1-D, levels 1 .. l_fine
+    if (cfg->d != 1 || cfg->l_fine < 1 || cfg->l_fine > 30 || cfg->cycles < 0) return BFP_ERR_ARG;
+    for (int l = 1; l <= cfg->l_fine; ++l)
+      if (cfg->p[l] < 3 || cfg->p[l] > 58 || cfg->pd[l] < 0 || cfg->pd[l] > 58 ||
+          cfg->pc[l] < 0 || cfg->pc[l] > 58 || cfg->ref_c1d[l].q < 1 || cfg->ref_c2d[l].q < 1)
+        return BFP_ERR_ARG;
+    return BFP_OK;
+  }
   if (cfg->d < 1 || cfg->d > 3 || cfg->l_coarse < 2 || cfg->l_fine < cfg->l_coarse ||
       cfg->l_fine > 30 || cfg->nu1 < 1 || cfg->nu2 < 0 || cfg->n_coarse < 1 || cfg->cycles < 0 ||
       cfg->qc < 2 || cfg->qc > 30)

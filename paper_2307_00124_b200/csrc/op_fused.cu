@@ -14,6 +14,7 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
     case FK_GEMV:
       f->u.gemv.x = view(a); f->u.gemv.y = view(b); f->u.gemv.al = s1; f->u.gemv.be = s2;
       f->u.gemv.dim = a->dim; f->u.gemv.l = a->l; f->u.gemv.z0 = a->z0;
+      f->u.gemv.ea = 2 * a->l; f->u.gemv.gs = 0;
       break;
     case FK_JACOBI:
       f->u.jac.x = view(a); f->u.jac.b = view(b); f->u.jac.c = s1;
@@ -24,14 +25,19 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
       f->u.axpby.x = view(a); f->u.axpby.y = view(b); f->u.axpby.al = s1; f->u.axpby.be = s2;
       break;
     case FK_RESTRICT:
-      f->u.rst.r = view(a); f->u.rst.dim = a->dim; f->u.rst.l = a->l; f->u.rst.zc = 0; break;
+      f->u.rst.r = view(a); f->u.rst.dim = a->dim; f->u.rst.l = a->l; f->u.rst.zc = 0;
+      f->u.rst.er = -2 * a->dim; f->u.rst.gs = 0;
+      break;
     case FK_PROLONG:
       f->u.pro.xc = view(a); f->u.pro.dim = out->dim; f->u.pro.l = out->l;
       f->u.pro.zf = f->u.pro.zp = 0;
+      f->u.pro.ep = -out->dim; f->u.pro.gs = 0;
       break;
     case FK_PCORR:
       f->u.pc.ec = view(a); f->u.pc.y = view(b); f->u.pc.dim = out->dim; f->u.pc.l = out->l;
       f->u.pc.zf = f->u.pc.zp = 0;
+      f->u.pc.ep = -out->dim; f->u.pc.gs = 0;
+      f->u.pc.al = Scal{1, 2, 0}; f->u.pc.be = Scal{1, 2, 0};
       break;
     case FK_ZERO: break;
     default: return BFP_ERR_ARG;

@@ -5,7 +5,7 @@
 namespace bfp {
 
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
-            cudaStream_t s) {
+            cudaStream_t s, int ea, int gs) {
   if (x->dim < 1 || !same_grid(x, y) || !same_grid(x, out)) return BFP_ERR_ARG;
   if (out == x || out == y) return BFP_ERR_ALIAS;
   GemvOp op;
@@ -16,6 +16,9 @@ int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bf
   op.dim = x->dim;
   op.l = x->l;
   op.z0 = x->z0;
+  op.ea = ea == kDefaultRep ? 2 * x->l : ea;
+  op.gs = gs;
+  if (gs) return launch_grid(op, out, p, s);  // scaled mantissas: generic exact path
   return launch_march(op, out, p, s);
 }
 

@@ -32,7 +32,8 @@ static bool aligned(const bfp_vec_s* fine, const bfp_vec_s* coarse) {
   return fine->dim >= 2 && fine->z0 == 2 * coarse->z0 && fine->nz == 2 * coarse->nz;
 }
 
-int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
+int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s, int er,
+                int gs) {
   if (r->dim < 1 || out->dim != r->dim || out->l != r->l - 1 || out->ebytes != r->ebytes)
     return BFP_ERR_ARG;
   if (!(full_grid(r) && full_grid(out)) && !aligned(r, out)) return BFP_ERR_ARG;
@@ -41,6 +42,9 @@ int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.dim = r->dim;
   op.l = r->l;
   op.zc = out->z0;
+  op.er = er == kDefaultRep ? -2 * r->dim : er;
+  op.gs = gs;
+  if (gs) return launch_grid(op, out, p, s);
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 6) return launch_rst3(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 9) return launch_rst2(op, out, p, s);
   return launch_grid(op, out, p, s);
@@ -52,7 +56,8 @@ static bool prolong_ok(const bfp_vec_s* xc, const bfp_vec_s* fine) {
   return full_grid(xc) || aligned(fine, xc);
 }
 
-int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s) {
+int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s, int ep,
+               int gs) {
   if (!prolong_ok(xc, out)) return BFP_ERR_ARG;
   ProlongOp op;
   op.xc = view(xc);
@@ -60,13 +65,16 @@ int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.l = out->l;
   op.zf = out->z0;
   op.zp = out->z0 - 2 * xc->z0;
+  op.ep = ep == kDefaultRep ? -out->dim : ep;
+  op.gs = gs;
+  if (gs) return launch_grid(op, out, p, s);
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
 int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_s* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, int ep, int gs, Scal al, Scal be) {
   if (!prolong_ok(ec, y) || !same_grid(y, out)) return BFP_ERR_ARG;
   if (out == y) return BFP_ERR_ALIAS;
   ProlongCorrectOp op;
@@ -76,6 +84,11 @@ int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_
   op.l = y->l;
   op.zf = y->z0;
   op.zp = y->z0 - 2 * ec->z0;
+  op.ep = ep == kDefaultRep ? -y->dim : ep;
+  op.gs = gs;
+  op.al = al;
+  op.be = be;
+  if (gs || al.m != 1 || be.m != 1) return launch_grid(op, out, p, s);
   if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);

@@ -1,0 +1,69 @@
+"""Reference-algorithm parity mode on the GPU vs its big-int
+restatement oracle/pyref_refmode.py: Chebyshev V(1,0) cycles, IR and FMG of
+P/src/multigrid.cpp:430-518 with the Table-1 gamma chain, 1-D p = 1 operators,
+coarsest level 1.  Final iterate, residual history and every trace record must match."""
+import pytest
+
+from oracle import pyref as P
+from oracle import pyref_refmode as R
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import paper_2307_00124_b200 as B
+    B.lib()
+    return B
+
+
+def _levels(v, L):
+    return [0] + ([v] * L if isinstance(v, int) else list(v[1:L + 1]))
+
+
+def _rhs(kind, L, wcheck, seed, fmg):
+    out = {}
+    for l in range(1, L + 1):
+        if not fmg and l != L:
+            continue
+        if kind == 1:
+            b = P.gen_sine(1, l, wcheck[l])
+            if any(b.m):
+                b.e -= 2 * l + 1
+        elif kind == 0:
+            b = P.gen_uniform(1, l, wcheck[l], seed, 2)
+        else:
+            b = P.zero_vec((1 << l) - 1, wcheck[l])
+        out[l] = b
+    return out
+
+
+CASES = [
+    dict(L=6, w=20, wdot=16, wcheck=24, rho=2.02, eta=0.3, cycles=1, fmg=True, rhs=1),
+    dict(L=7, w=[0] + [6 + 2 * l for l in range(1, 8)], wdot=[0] + [4 + 2 * l for l in range(1, 8)],
+         wcheck=[0] + [10 + 2 * l for l in range(1, 8)], rho=2.02, eta=0.0, cycles=2, fmg=True, rhs=1),
+    dict(L=7, w=16, wdot=16, wcheck=20, rho=2.02, eta=0.15, cycles=5, fmg=False, rhs=0, x0=True),
+    dict(L=6, w=40, wdot=36, wcheck=44, rho=2.0, eta=0.5, cycles=3, fmg=False, rhs=1),
+    dict(L=5, w=12, wdot=12, wcheck=12, rho=2.02, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}")
+def test_refmode_gpu_vs_pyref(B, case):
+    L = case["L"]
+    w, wd, wc = (_levels(case[k], L) for k in ("w", "wdot", "wcheck"))
+    seed = 3
+    x0 = P.gen_uniform(1, L, w[L], seed, 1) if case.get("x0") else None
+    cfg = R.RefConfig(l_fine=L, w=w, wdot=wd, wcheck=wc, rho=case["rho"], eta=case["eta"],
+                      cycles=case["cycles"], fmg=case["fmg"], x0=x0)
+    want = R.RefMg(cfg, _rhs(case["rhs"], L, wc, seed, case["fmg"])).run()
+    gcfg = B.mg_config_ref(L, case["rho"], case["eta"], w=w, wdot=wd, wcheck=wc,
+                           cycles=case["cycles"], fmg=case["fmg"], x0_random=bool(case.get("x0")),
+                           rhs_kind=case["rhs"], seed=seed)
+    for graph in (False, True):
+        mg = B.Multigrid(gcfg)
+        mg.solve(use_graph=graph)
+        x, q, e, hist, tr = mg.result(trace_cap=1 << 14)
+        assert [tuple(t) for t in tr] == [tuple(t) for t in want.trace], graph
+        assert hist == want.history
+        assert e == want.x.e and x.tolist() == want.x.m
