@@ -55,3 +55,43 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(B, "LIB_PATH", "/nonexistent/libbfpmg_b200.so")
     with pytest.raises(RuntimeError):
         B.lib()
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The Python mirror's ctypes structs have the C layout of include/bfpmg_b200.h."""
+    import paper_2307_00124_b200 as B
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "bfpmg_b200.h"\n'
+                   "int main(void) { printf(\"%zu %zu %zu %zu %zu\\n\", sizeof(bfp_mg_config_t),"
+                   " offsetof(bfp_mg_config_t, ref_mode), offsetof(bfp_mg_config_t, ref_c1d),"
+                   " sizeof(bfp_xf_t), sizeof(bfp_trace_rec_t)); return 0; }\n")
+    exe = tmp_path / "sz"
+    subprocess.run(["/usr/bin/gcc", "-I", os.path.join(REPO, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [ctypes.sizeof(B.MgConfig), B.MgConfig.ref_mode.offset, B.MgConfig.ref_c1d.offset,
+            ctypes.sizeof(B.XfC), ctypes.sizeof(B.TraceRec)]
+    assert got == want
+
+
+def test_refmode_host_scalars_match_the_restatement():
+    """The product's host setup of the reference mode (Chebyshev scalars) equals the
+    oracle's independent derivation."""
+    from fractions import Fraction
+
+    from oracle import pyref_refmode as R
+    from paper_2307_00124_b200 import refmode
+    for rho, eta in ((2.02, 0.3), (2.0, 0.0), (1.98765, 0.15), (3.1, 0.77)):
+        wdot = [0] + [w for w in range(3, 34)]
+        c1, kres, c1d, c2d = refmode.chebyshev_scalars(rho, eta, 400, wdot)
+        rc1, rc2 = R.chebyshev(Fraction(rho), R.eta_rational(eta))
+        c1x = R._round(rc1, 400, False)
+        c2x = -R._round(-rc2, 400, False)
+        hi, lo, e, st = c1
+        top = Fraction((hi << 64) | lo) * Fraction(2) ** e
+        assert top <= c1x < top + Fraction(2) ** (e + 1) and (st == 1) == (top != c1x)
+        for l in range(1, 32):
+            a = R.quantize_scalar_floor(c1x, wdot[l])
+            b = R.quantize_scalar_floor(c2x, wdot[l])
+            assert c1d[l] == (a.m[0], wdot[l], a.e) and c2d[l] == (b.m[0], wdot[l], b.e)

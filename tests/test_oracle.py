@@ -3,6 +3,7 @@ restatement (oracle/pyref.py) against the reference's known answers, its
 rational-oracle properties (tests/oracle.hpp), each other, and the committed
 golden fixtures.  No GPU involved."""
 import hashlib
+import random
 import json
 import os
 from fractions import Fraction
@@ -401,3 +402,19 @@ def test_mg_converges():
     x, h, tr = ob.mg_run(ob.mg_config(2, 6, cycles=6, rhs_kind=1, p=24))
     assert all(b < a for a, b in zip(h[:-1], h[1:]))
     assert h[-1] < h[0] * 1e-3
+
+
+def test_refmode_scalar_up_equals_inf_norm_upper():
+    """scalar_up (P/src/multigrid.cpp:84-105) of an exact block norm is the reference's
+    inf_norm_upper at q_gamma = 16 (P/src/bfp.cpp:124-148, pinned by known answers)."""
+    from oracle import pyref_refmode as R
+    r = random.Random(11)
+    for _ in range(300):
+        q = r.randint(2, 60)
+        m = [r.randint(-(1 << (q - 1)), (1 << (q - 1)) - 1) for _ in range(r.randint(1, 6))]
+        b = P.Block(m, q, r.randint(-50, 50))
+        if not any(m):
+            continue
+        want = P.inf_norm_upper(b, 16)
+        got = R.scalar_up(R.xf_exact_norm(b))
+        assert (got.m[0], got.e) == (want.m[0], want.e)
