@@ -188,7 +188,9 @@ int bfp_gen_sine(bfp_vec_t v, int64_t p, void* stream);
    for the IR residual of iterations <= 2, hybrid_qcomp_iters).
    PrecisionSchedule (P/include/bfpmg/multigrid.hpp:16-27) per level: p = w (iterate),
    pd = wdot (residual and V-cycle), pc = wcheck (right-hand side); 0 entries = p.
-   w_add_cap: GammaPolicy::w_add_cap (-1 unlimited). */
+   w_add_cap: GammaPolicy::w_add_cap (-1 unlimited).
+   x0_random (IR runs): 0 zero_vec, 1 seeded uniform, 2 the caller's iterate (written into
+   the x handle of bfp_mg_vectors before each solve; single rank). */
 typedef struct {
   int d, l_fine, l_coarse, nu1, nu2, n_coarse, cycles, fmg, nonnormalized, x0_random, rhs_kind,
       qc;

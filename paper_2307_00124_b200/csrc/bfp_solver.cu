@@ -554,14 +554,14 @@ struct RankSolver {
       PlanOp init;
       init.out = L.x[0];
       init.q = L.p;
-      if (cfg.x0_random) {
+      if (cfg.x0_random == 1) {
         init.kind = OK_UNIFORM;
         init.seed = cfg.seed;
         init.sid = 1;
       } else {
         init.kind = OK_ZERO;
       }
-      plan.push_back(init);
+      if (cfg.x0_random != 2) plan.push_back(init);  // 2: the caller's x0 (bfp_mg_vectors)
       x_final = ir_ref(lf, L.x[0], cfg.cycles);
     }
     return finish_build();
@@ -627,7 +627,7 @@ struct RankSolver {
       LevelBufs& L = lev[lf];
       PlanOp init;
       init.out = L.x[0];
-      if (cfg.x0_random && sharded(lf)) {
+      if (cfg.x0_random == 1 && sharded(lf)) {
         bfp_vec_s* full = nullptr;
         if (vec_alloc(cfg.d, lf, 0, ebytes, &full)) return BFP_ERR_NOMEM;
         L.x0 = vec(lf);
@@ -637,7 +637,7 @@ struct RankSolver {
         if (rc) return rc;
         init.kind = OK_COPY;
         init.a = L.x0;
-      } else if (cfg.x0_random) {
+      } else if (cfg.x0_random == 1) {
         init.kind = OK_UNIFORM;
         init.q = L.p;
         init.seed = cfg.seed;
@@ -646,7 +646,7 @@ struct RankSolver {
         init.kind = OK_ZERO;
         init.q = L.p;
       }
-      plan.push_back(init);
+      if (cfg.x0_random != 2 || world > 1) plan.push_back(init);  // 2: the caller's x0
       bfp_vec_s* r_last = nullptr;
       x_final = ir(lf, L.x[0], cfg.cycles, &r_last);
       if (r_last) final_residual(lf, x_final, r_last);

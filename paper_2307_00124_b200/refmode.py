@@ -82,3 +82,56 @@ def chebyshev_scalars(rho: float, eta: float, prec: int, wdot: List[int]):
     c1d = [_floor_scalar(c1, w) if w else (0, 1, 0) for w in wdot]
     c2d = [_floor_scalar(c2, w) if w else (0, 1, 0) for w in wdot]
     return _top128(c1), _top128(kres), c1d, c2d
+
+
+def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=None,
+                     ext_prec: int = 400, streams: int = 4):
+    """conv_rate_vcycle (P/src/multigrid.cpp:572-601) in the reference mode, 1-D: one
+    IR-V error-propagation step (b = 0) from every unit vector e_i (from_extfloat at wdot)
+    gives the columns (I - B A) e_i; the columns run as independent solves spread over
+    `streams` CUDA streams (each a replayed graph), and rho_V = sqrt(lambda_max) of the
+    generalised problem (M^T A M, A) with the level's stiffness A ~ tridiag(-1, 2, -1)
+    (rho_v_of_columns, :533-568; here in float64 -- the columns are exact).
+    Returns (rho_V, columns as (mantissas, e) per unit vector)."""
+    import ctypes as C
+
+    import numpy as np
+    import scipy.linalg
+
+    from . import BfpVec, Multigrid, _raise, lib, mg_config_ref, set_stream
+
+    n = (1 << level) - 1
+    cfg = mg_config_ref(level, rho, eta, w=w, wdot=wdot, wcheck=wcheck, cycles=1, fmg=False,
+                        rhs_kind=2, ext_prec=ext_prec)
+    cfg.x0_random = 2  # the caller's iterate
+    wd = cfg.pd[level] or cfg.p[level]
+    L = lib()
+    import torch
+    strs = [torch.cuda.Stream() for _ in range(max(1, streams))]
+    mgs = [Multigrid(cfg) for _ in strs]
+    xs, outs = [], []
+    for mg in mgs:
+        xh, _, _ = mg.vectors()
+        xs.append(BfpVec._view(xh.value, 1, level, 8, mg))
+        outs.append(mg.rank_result(0)[0])  # the final iterate (x_final)
+    cols = [None] * n
+    try:
+        for base in range(0, n, len(strs)):
+            batch = list(range(base, min(n, base + len(strs))))
+            for k, i in enumerate(batch):  # enqueue: upload e_i, replay the solve graph
+                set_stream(strs[k].cuda_stream)
+                unit = np.zeros(n, dtype=np.int64)
+                unit[i] = 1 << (wd - 2)  # from_extfloat(e_i, wdot): m = 2^(w-2), e = 2 - w
+                _raise(L.bfp_vec_upload(xs[k].h, unit.ctypes.data_as(C.c_void_p), wd, 2 - wd,
+                                        C.c_void_p(strs[k].cuda_stream)), "upload e_i")
+                mgs[k].solve(use_graph=True)
+            for k, i in enumerate(batch):
+                set_stream(strs[k].cuda_stream)
+                x, q, e = outs[k].download()
+                cols[i] = (x.copy(), e)
+    finally:
+        set_stream(None)
+    M = np.stack([np.ldexp(c[0].astype(np.float64), c[1]) for c in cols], axis=1)
+    A = 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    lam = scipy.linalg.eigh(M.T @ A @ M, A, eigvals_only=True)
+    return float(np.sqrt(max(lam.max(), 0.0))), cols

@@ -67,3 +67,21 @@ def test_refmode_gpu_vs_pyref(B, case):
         assert [tuple(t) for t in tr] == [tuple(t) for t in want.trace], graph
         assert hist == want.history
         assert e == want.x.e and x.tolist() == want.x.m
+
+
+def test_conv_rate_vcycle_columns(B):
+    """conv_rate_vcycle (P/src/multigrid.cpp:572-601): every column (I - B A) e_i of the
+    batched GPU run equals the restatement's, and rho_V is a contraction."""
+    from paper_2307_00124_b200 import refmode
+    L, w, wd, wc, rho, eta = 4, 20, 16, 24, 2.02, 0.3
+    rate, cols = refmode.conv_rate_vcycle(L, rho, eta, w=w, wdot=wd, wcheck=wc, streams=4)
+    n = (1 << L) - 1
+    lv = [0] + [w] * L, [0] + [wd] * L, [0] + [wc] * L
+    for i in range(n):
+        x0 = P.Block([0] * n, wd, 2 - wd)
+        x0.m[i] = 1 << (wd - 2)
+        cfg = R.RefConfig(l_fine=L, w=lv[0], wdot=lv[1], wcheck=lv[2], rho=rho, eta=eta, cycles=1,
+                          fmg=False, x0=x0)
+        want = R.RefMg(cfg, {L: P.zero_vec(n, wc)}).run()
+        assert cols[i][1] == want.x.e and cols[i][0].tolist() == want.x.m, i
+    assert 0.0 < rate < 1.0
