@@ -660,7 +660,7 @@ def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
             "kernel_ms": kern_ms, "hbm_frac": 3 * mb * n / (kern_ms / 1e3) / 1e9 / peak}
 
 
-def measure_ops(B, torch, stream, d, l, p, steps=20, only=None):
+def measure_ops(B, torch, stream, d, l, p, steps=20, only=None, s=4):
     """Every fine-level op of the V-cycle / FMG on one config's finest level (inputs
     resident, gamma at the exact binade so qcomp takes the fast path): pass-1 kernel
     time (recompute launch skipped, flags verified) and its fraction of the measured
@@ -669,7 +669,6 @@ def measure_ops(B, torch, stream, d, l, p, steps=20, only=None):
     prolong + correct (2 + 2^-d)s)."""
     sp = C.c_void_p(stream.cuda_stream)
     L = B.lib()
-    s = 4
     n = ((1 << l) - 1) ** d
     x = B.gen_uniform(B.BfpVec.grid(d, l, s), p, 1, 1)
     b = B.gen_sine(B.BfpVec.grid(d, l, s), p)

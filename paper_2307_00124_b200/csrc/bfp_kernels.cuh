@@ -788,6 +788,7 @@ struct B3Maps {
 template <typename T> struct S4;
 template <> struct S4<int32_t> {
   using V = int;
+  static constexpr int kLaneCols = 4;  // lane i owns columns 4i .. 4i+3
   __device__ static __forceinline__ void ld(const int32_t* p, int sh, V v[4]) {
     const int4 t = *reinterpret_cast<const int4*>(p);
     v[0] = t.x >> sh, v[1] = t.y >> sh, v[2] = t.z >> sh, v[3] = t.w >> sh;
@@ -796,16 +797,21 @@ template <> struct S4<int32_t> {
     *reinterpret_cast<int4*>(p) = make_int4(t[0], t[1], t[2], t[3]);
   }
 };
+// int64 tiles use a split-pair lane layout: lane i owns columns (2i, 2i+1) and
+// (64+2i, 64+2i+1) of the 128-wide tile, so each 16-B shared-memory load (and each
+// 16-B global store) of a warp covers 512 contiguous bytes -- conflict-free, where
+// four contiguous int64 per lane (32-B lane stride) would take two wavefronts per load.
 template <> struct S4<int64_t> {
   using V = int64_t;
+  static constexpr int kLaneCols = 2;  // column of lane i = 2i (pair A), 64 + 2i (pair B)
   __device__ static __forceinline__ void ld(const int64_t* p, int sh, V v[4]) {
     const longlong2 a = reinterpret_cast<const longlong2*>(p)[0];
-    const longlong2 b = reinterpret_cast<const longlong2*>(p)[1];
+    const longlong2 b = reinterpret_cast<const longlong2*>(p + 64)[0];
     v[0] = a.x >> sh, v[1] = a.y >> sh, v[2] = b.x >> sh, v[3] = b.y >> sh;
   }
   __device__ static __forceinline__ void st(int64_t* p, const int64_t t[4]) {
     reinterpret_cast<longlong2*>(p)[0] = make_longlong2(t[0], t[1]);
-    reinterpret_cast<longlong2*>(p)[1] = make_longlong2(t[2], t[3]);
+    reinterpret_cast<longlong2*>(p + 64)[0] = make_longlong2(t[2], t[3]);
   }
 };
 template <typename V> __device__ __forceinline__ V shfl_up1(V v) {
@@ -868,7 +874,9 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         issue(tk + 1, (int)((tk + 1) % kB3XS), tk, (int)(tk % kB3YS), &bar[tk % kB3YS], g == 0);
       }
     }
-    const bool xpad = x0 + 4 * lane + 3 == N - 1;
+    // column of the lane's point 3 (the only one that can be the x pad, column N-1)
+    const int col3 = sizeof(T) == 4 ? 4 * lane + 3 : 64 + 2 * lane + 1;
+    const bool xpad = x0 + col3 == N - 1;
     const bool ypad = y0 + wy == N - 1;
     int sp = (int)((k0 - 1 + kB3XS) % kB3XS), sc = (int)(k0 % kB3XS);
     int sn = (int)((k0 + 1) % kB3XS), sy_ = (int)(k0 % kB3YS);
@@ -876,7 +884,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
       const int64_t k = k0 + s;
       mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
       parity ^= 1u << sy_;
-      const int off = (wy + 1) * kB3XW + 4 + 4 * lane;
+      const int off = (wy + 1) * kB3XW + 4 + S4<T>::kLaneCols * lane;
       const T* xc = xsl + sc * XTP + off;
       V C[4], u[4], dn[4], zp[4], zn[4], Yv[4];
       S4<T>::ld(xc, sx, C);
@@ -884,16 +892,33 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
       S4<T>::ld(xc + kB3XW, sx, dn);
       S4<T>::ld(xsl + sp * XTP + off, sx, zp);
       S4<T>::ld(xsl + sn * XTP + off, sx, zn);
-      S4<T>::ld(ysl + sy_ * kB3YT + wy * kB3W + 4 * lane, sy, Yv);
-      const V lf0 = (V)(xc[-1] >> sx), rt0 = (V)(xc[4] >> sx);
-      V lf = shfl_up1(C[3]), rt = shfl_dn1(C[0]);
-      lf = lane == 0 ? lf0 : lf;
-      rt = lane == 31 ? rt0 : rt;
+      S4<T>::ld(ysl + sy_ * kB3YT + wy * kB3W + S4<T>::kLaneCols * lane, sy, Yv);
+      // x-neighbours of the lane's 4 points (tile halo columns -1 and 128 at the warp ends)
+      V Lf[4], Rt[4];
+      if constexpr (sizeof(T) == 4) {
+        const V lf0 = (V)(xc[-1] >> sx), rt0 = (V)(xc[4] >> sx);
+        V lf = shfl_up1(C[3]), rt = shfl_dn1(C[0]);
+        Lf[0] = lane == 0 ? lf0 : lf;
+        Rt[3] = lane == 31 ? rt0 : rt;
+        Lf[1] = C[0], Lf[2] = C[1], Lf[3] = C[2];
+        Rt[0] = C[1], Rt[1] = C[2], Rt[2] = C[3];
+      } else {  // split pairs: columns 2i, 2i+1 | 64+2i, 64+2i+1
+        const V lf0 = (V)(xc[-1] >> sx), rt0 = (V)(xc[66] >> sx);
+        const V a = shfl_up1(C[1]), b = shfl_dn1(C[2]);
+        // right of column 2i+1 is lane i+1's column 2i+2; lane 31's is column 64 (lane 0, B)
+        const V r1 = __shfl_sync(0xffffffffu, lane == 0 ? C[2] : C[0], (lane + 1) & 31);
+        // left of column 64+2i is lane i-1's column 64+2i-1; lane 0's is column 63 (lane 31, A)
+        const V l2 = __shfl_sync(0xffffffffu, lane == 31 ? C[1] : C[3], (lane + 31) & 31);
+        Lf[0] = lane == 0 ? lf0 : a, Rt[0] = C[1];
+        Lf[1] = C[0], Rt[1] = r1;
+        Lf[2] = l2, Rt[2] = C[3];
+        Lf[3] = C[2], Rt[3] = lane == 31 ? rt0 : b;
+      }
       T tt[4];
       const bool rowpad = ypad || k + Z0 == N - 1;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const V left = q == 0 ? lf : C[q - 1], right = q == 3 ? rt : C[q + 1];
+        const V left = Lf[q], right = Rt[q];
         if constexpr (sizeof(T) == 8 && FW) {  // two-word rows, window rs < 64
           const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
           W128 w = op.point_fw(6 * C[q] - nb, C[q], Yv[q]);
@@ -926,7 +951,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         mx = (V)tt[q] > mx ? (V)tt[q] : mx;
         mn = (V)tt[q] < mn ? (V)tt[q] : mn;
       }
-      S4<T>::st(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane, tt);
+      S4<T>::st(O + k * N2 + (y0 + wy) * N + x0 + S4<T>::kLaneCols * lane, tt);
       const int free_x = sp, free_y = sy_;
       sp = sc;
       sc = sn;

@@ -1,4 +1,4 @@
-"""Run one fine-level op a few times (for ncu): python tools/op_once.py d l op [steps]
+"""Run one fine-level op a few times (for ncu): python tools/op_once.py d l op [steps] [p] [s]
 op in residual, jacobi, scal, axpby, restrict, prolong, prolong_correct"""
 import os
 import sys
@@ -13,5 +13,7 @@ d, l, op = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
 steps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 stream = torch.cuda.current_stream()
 B.set_stream(stream.cuda_stream)
-r = bench.measure_ops(B, torch, stream, d, l, 24 if d == 3 else 20, steps=steps, only=op)
+p = int(sys.argv[5]) if len(sys.argv) > 5 else (24 if d == 3 else 20)
+s = int(sys.argv[6]) if len(sys.argv) > 6 else 4
+r = bench.measure_ops(B, torch, stream, d, l, p, steps=steps, only=op, s=s)
 print(r)
