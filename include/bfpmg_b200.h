@@ -202,14 +202,18 @@ typedef struct {
   /* levels whose padded grid has <= fuse_points points run as one fused CTA with their
      vectors staged in shared memory; 0 = off, -1 = library default */
   int fuse_points;
-  /* reference-algorithm mode (P/src/multigrid.cpp:430-518), d = 1:
+  /* reference-algorithm mode (P/src/multigrid.cpp:430-518), d = 1 or 2:
      Chebyshev V(1,0) cycles, IR (r = A x - b, x - y) and FMG (fresh ir per n_ir, level 1
-     = zero_vec) on A = tridiag(-1/2, 1, -1/2), P = linear interpolation, R = 2 P^T,
-     operators quantize_csr'd at wcheck / wdot / w, coarsest level 1, gamma = Table 1
+     = zero_vec) on the reference's p = 1 operators after the D = I scaling
+     (P/src/multigrid.cpp:277-306): 1-D A = tridiag(-1/2, 1, -1/2), P = linear
+     interpolation, R = 2 P^T; 2-D (P/src/fem.cpp:426-457, 542-543) A = 9-point
+     (1, -1/8 x 8), P = P1 (x) P1, R = P^T.  Operators quantize_csr'd at wcheck / wdot / w
+     (every width >= 3 in 1-D, >= 5 in 2-D), coarsest level 1, gamma = Table 1
      (gamma_policy_eval, :121-155) evaluated exactly with one final round-up.  The host
      supplies the derived Chebyshev scalars: ref_c1 = c1 rounded to the hierarchy
      precision (ExtFloat), ref_kres = add_up(2 c1, 1) / 4, ref_c1d / ref_c2d[l] = c1 / c2
-     floor-quantised at wdot_l (quantize_scalar_floor); rhs_kind 1 = h^2/2 d pi^2 sin. */
+     floor-quantised at wdot_l (quantize_scalar_floor); rhs_kind 1 = h^2 / 2^d * the
+     config's d pi^2 prod sin (the D^-1-scaled load up to a constant). */
   int ref_mode;
   bfp_xf_t ref_c1, ref_kres;
   bfp_scalar_t ref_c1d[32], ref_c2d[32];

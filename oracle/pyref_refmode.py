@@ -1,10 +1,15 @@
-"""Reference-algorithm parity mode, 1-D: a big-int restatement of the
+"""Reference-algorithm parity mode: a big-int restatement of the
 reference solver P/src/multigrid.cpp:430-518 -- Chebyshev V(1,0) cycles, IR and FMG
-with the Table-1 gamma chain (:121-155) -- on the reference's own 1-D p = 1 operators
+with the Table-1 gamma chain (:121-155) -- on the reference's own p = 1 operators
 after the D = I scaling (P/src/multigrid.cpp:278-306):
 
-  A_j = tridiag(-1/2, 1, -1/2)   P_j = [1/2, 1, 1/2] (linear interpolation)
-  R_j = D_c^-1 P^T D_f = 2 P^T   (D = 2/h, so D_f / D_c = 2)
+  1-D  A_j = tridiag(-1/2, 1, -1/2)   P_j = [1/2, 1, 1/2] (linear interpolation)
+       R_j = D_c^-1 P^T D_f = 2 P^T   (D = 2/h, so D_f / D_c = 2)
+  2-D  A_j = A1 (x) M1 + M1 (x) A1 (P/src/fem.cpp:426-457): centre 8/3, eight
+       neighbours -1/3 at every level, so D = 8/3 and D^-1 A = (1, -1/8 x 8);
+       P_j = P1 (x) P1 (P/src/fem.cpp:542-543), R_j = P^T (D_f = D_c)
+
+Vectors are in lexicographic order, x fastest (kron row index = iy * n + ix).
 
 Operators are quantised with quantize_csr (:216-229) at wcheck / wdot / w, the
 Chebyshev coefficients with chebyshev_coeffs_q (:183-193) from injected rho and eta
@@ -126,33 +131,80 @@ def csr_from(rows: int, cols: int, entries: Dict[int, List[tuple]], w: int) -> P
     return P.Csr(rows, cols, rowptr, col, m, w, e)
 
 
-def op_a(j: int, w: int) -> P.Csr:
+def _entries_a1(j: int):
     n = (1 << j) - 1
-    ent = {i: [(c, Fraction(1) if c == i else Fraction(-1, 2)) for c in (i - 1, i, i + 1)
-               if 0 <= c < n] for i in range(n)}
-    return csr_from(n, n, ent, w)
+    return {i: [(c, Fraction(1) if c == i else Fraction(-1, 2)) for c in (i - 1, i, i + 1)
+                if 0 <= c < n] for i in range(n)}
 
 
-def op_p(j: int, w: int) -> P.Csr:
+def _entries_p1(j: int):
     """Linear interpolation level j-1 -> j (fine row 2k+1 <- coarse k)."""
-    nf, nc = (1 << j) - 1, (1 << (j - 1)) - 1
+    nc = (1 << (j - 1)) - 1
     ent: Dict[int, List[tuple]] = {}
     for k in range(nc):
         for i, wgt in ((2 * k, Fraction(1, 2)), (2 * k + 1, Fraction(1)), (2 * k + 2, Fraction(1, 2))):
             ent.setdefault(i, []).append((k, wgt))
-    return csr_from(nf, nc, ent, w)
+    return ent
 
 
-def op_r(j: int, w: int) -> P.Csr:
-    """R = 2 P^T: coarse row k <- fine 2k, 2k+1, 2k+2 with weights (1, 2, 1)."""
+def _transpose(ent, scale=Fraction(1)):
+    out: Dict[int, List[tuple]] = {}
+    for i, row in ent.items():
+        for c, v in row:
+            out.setdefault(c, []).append((i, v * scale))
+    return out
+
+
+def _kron(ea, eb, nb_rows: int, nb_cols: int):
+    """kron(a, b): row ia * nb_rows + ib, column ca * nb_cols + cb (P/src/fem.cpp:364-424)."""
+    out: Dict[int, List[tuple]] = {}
+    for ia, ra in ea.items():
+        for ib, rb in eb.items():
+            out[ia * nb_rows + ib] = [(ca * nb_cols + cb, va * vb) for ca, va in ra for cb, vb in rb]
+    return out
+
+
+def _entries_a2(j: int):
+    """D^-1 (A1 (x) M1 + M1 (x) A1): centre 1, eight neighbours -1/8."""
+    n = (1 << j) - 1
+    ent = {}
+    for iy in range(n):
+        for ix in range(n):
+            row = []
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    y, x = iy + dy, ix + dx
+                    if 0 <= y < n and 0 <= x < n:
+                        row.append((y * n + x, Fraction(1) if dx == dy == 0 else Fraction(-1, 8)))
+            ent[iy * n + ix] = row
+    return ent
+
+
+def op_a(j: int, w: int, d: int = 1) -> P.Csr:
+    n = ((1 << j) - 1) ** d
+    return csr_from(n, n, _entries_a1(j) if d == 1 else _entries_a2(j), w)
+
+
+def op_p(j: int, w: int, d: int = 1) -> P.Csr:
     nf, nc = (1 << j) - 1, (1 << (j - 1)) - 1
-    ent = {k: [(2 * k, Fraction(1)), (2 * k + 1, Fraction(2)), (2 * k + 2, Fraction(1))]
-           for k in range(nc)}
-    return csr_from(nc, nf, ent, w)
+    e1 = _entries_p1(j)
+    if d == 1:
+        return csr_from(nf, nc, e1, w)
+    return csr_from(nf * nf, nc * nc, _kron(e1, e1, nf, nc), w)
 
 
-NORM_A_UP = Fraction(2)  # ||tridiag(-1/2, 1, -1/2)||_inf
-NORM_R_UP = Fraction(4)  # ||2 P^T||_inf
+def op_r(j: int, w: int, d: int = 1) -> P.Csr:
+    """1-D: R = 2 P^T (coarse row k <- fine 2k, 2k+1, 2k+2 with weights 1, 2, 1);
+    2-D: R = P^T = (P1 (x) P1)^T."""
+    nf, nc = (1 << j) - 1, (1 << (j - 1)) - 1
+    if d == 1:
+        return csr_from(nc, nf, _transpose(_entries_p1(j), Fraction(2)), w)
+    pt = _transpose(_entries_p1(j))
+    return csr_from(nc * nc, nf * nf, _kron(pt, pt, nc, nf), w)
+
+
+NORM_A_UP = Fraction(2)  # ||tridiag(-1/2, 1, -1/2)||_inf = ||(1, -1/8 x 8)||_inf
+NORM_R_UP = Fraction(4)  # ||2 P1^T||_inf = ||(P1 (x) P1)^T||_inf
 
 
 def chebyshev(rho: Fraction, eta: Fraction):
@@ -193,6 +245,7 @@ class RefConfig:
     fmg: bool = False
     ext_prec: int = 400  # Hierarchy precision (ExtFloat)
     x0: Optional[P.Block] = None
+    d: int = 1          # 1 or 2
 
 
 @dataclass
@@ -234,7 +287,7 @@ class RefMg:
         cfg = self.cfg
         wd = cfg.wdot[lev]
         rn = xf_exact_norm(r)
-        ad = op_a(lev, wd)
+        ad = op_a(lev, wd, cfg.d)
         y = self.step("v-relax", lev, P.EgemvKernel(ad, r, r, self.c2d[lev], self.c1d[lev]), wd,
                       mul_up(self.c1x, rn))
         if lev > 1:
@@ -243,11 +296,11 @@ class RefMg:
             g = XF(g.v / 4, g.prec)
             rv = self.step("v-residual", lev, P.EgemvKernel(ad, y, r, P.bfp_one(), P.bfp_minus_one()),
                            wd, g)
-            rc = self.step("v-restrict", lev, P.EspmvKernel(op_r(lev, wd), rv), wd,
+            rc = self.step("v-restrict", lev, P.EspmvKernel(op_r(lev, wd, cfg.d), rv), wd,
                            mul_up(XF(NORM_R_UP, cfg.ext_prec), xf_exact_norm(rv)))
             d = self.vcycle(lev - 1, rc)
             y = self.step("v-correct", lev,
-                          P.EgemvKernel(op_p(lev, wd), d, y, P.bfp_minus_one(), P.bfp_one()), wd,
+                          P.EgemvKernel(op_p(lev, wd, cfg.d), d, y, P.bfp_minus_one(), P.bfp_one()), wd,
                           add_up(xf_exact_norm(y), xf_exact_norm(d)))
         return y
 
@@ -263,7 +316,7 @@ class RefMg:
             else:
                 g = add_up(mul_up(XF(NORM_A_UP, cfg.ext_prec), xf_exact_norm(x)), xf_exact_norm(b))
             r = self.step("ir-residual", lev,
-                          P.EgemvKernel(op_a(lev, cfg.wcheck[lev]), x, b, P.bfp_one(), P.bfp_minus_one()),
+                          P.EgemvKernel(op_a(lev, cfg.wcheck[lev], cfg.d), x, b, P.bfp_one(), P.bfp_minus_one()),
                           cfg.wdot[lev], g, ir_iter=i)
             self.last_res[lev] = xf_exact_norm(r)
             mx = max((abs(v) for v in r.m), default=0)
@@ -280,7 +333,7 @@ class RefMg:
             x = P.zero_vec(1, cfg.w[1])
         else:
             xc = self.fmg(lev - 1)
-            x = self.step("fmg-prolong", lev, P.EspmvKernel(op_p(lev, cfg.w[lev]), xc), cfg.w[lev],
+            x = self.step("fmg-prolong", lev, P.EspmvKernel(op_p(lev, cfg.w[lev], cfg.d), xc), cfg.w[lev],
                           xf_exact_norm(xc))
         for _ in range(cfg.cycles):
             x = self.ir(lev, x, 1)
@@ -292,6 +345,6 @@ class RefMg:
             self.res.x = self.fmg(cfg.l_fine)
         else:
             l = cfg.l_fine
-            x = cfg.x0 if cfg.x0 is not None else P.zero_vec((1 << l) - 1, cfg.w[l])
+            x = cfg.x0 if cfg.x0 is not None else P.zero_vec(((1 << l) - 1) ** cfg.d, cfg.w[l])
             self.res.x = self.ir(l, x, cfg.cycles)
         return self.res

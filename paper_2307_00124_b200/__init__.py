@@ -645,13 +645,15 @@ def mg_config(d, l_fine, l_coarse=2, nu1=2, nu2=2, n_coarse=16, cycles=1, fmg=Fa
 
 
 def mg_config_ref(l_fine, rho, eta, w, wdot=None, wcheck=None, cycles=1, fmg=False,
-                  x0_random=False, rhs_kind=1, seed=1, ext_prec=400, w_add_cap=-1) -> MgConfig:
-    """Reference-algorithm mode (1-D): the reference solver P/src/multigrid.cpp:430-518 on
-    its own p = 1 operators, see include/bfpmg_b200.h.  rho / eta: the Chebyshev
-    parameters (Hierarchy::set_eta); w / wdot / wcheck: PrecisionSchedule widths (int or
-    per-level list, index = level, levels 1..l_fine)."""
+                  x0_random=False, rhs_kind=1, seed=1, ext_prec=400, w_add_cap=-1,
+                  d=1) -> MgConfig:
+    """Reference-algorithm mode (d = 1 or 2): the reference solver P/src/multigrid.cpp:430-518
+    on its own p = 1 operators (2-D: the bilinear-FEM 9-point operator, P = P1 (x) P1,
+    R = P^T), see include/bfpmg_b200.h.  rho / eta: the Chebyshev parameters
+    (Hierarchy::set_eta); w / wdot / wcheck: PrecisionSchedule widths (int or per-level
+    list, index = level, levels 1..l_fine; >= 3 in 1-D, >= 5 in 2-D)."""
     from . import refmode
-    cfg = mg_config(1, l_fine, l_coarse=1, cycles=cycles, fmg=fmg, x0_random=x0_random,
+    cfg = mg_config(d, l_fine, l_coarse=1, cycles=cycles, fmg=fmg, x0_random=x0_random,
                     rhs_kind=rhs_kind, seed=seed, p=w, pd=wdot, pc=wcheck, w_add_cap=w_add_cap,
                     fuse_points=0)
     cfg.ref_mode = 1

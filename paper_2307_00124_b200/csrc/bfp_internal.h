@@ -80,7 +80,7 @@ GammaRule gamma_literal(int64_t m, int64_t e);  // (declared for the solver too)
 // config operators (stencil e_A = 2l, full weighting e_R = -2d, prolongation e_P = -d)
 constexpr int kDefaultRep = -0x40000000;
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
-            cudaStream_t s, int ea = kDefaultRep, int gs = 0);
+            cudaStream_t s, int ea = kDefaultRep, int gs = 0, int st9 = 0);
 int op_jacobi(bfp_vec_s* x, bfp_vec_s* b, Scal c, const WinParams& p, bfp_vec_s* out,
               cudaStream_t s);
 int op_scal(bfp_vec_s* r, Scal c, const WinParams& p, bfp_vec_s* out, cudaStream_t s);

@@ -380,7 +380,7 @@ int vec_alloc_slab(int dim, int level, int64_t n, int z_lo, int z_hi, int ebytes
     v->span = (n + 3) / 4 * 4;
     v->halo = 4;
   } else {
-    if (level < (dim == 1 ? 1 : 2) || level > 30 || (int64_t)dim * level > 36) {
+    if (level < (dim == 3 ? 2 : 1) || level > 30 || (int64_t)dim * level > 36) {  // 2-D level 1: ref mode
       delete v;
       return BFP_ERR_ARG;
     }

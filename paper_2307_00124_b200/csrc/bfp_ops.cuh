@@ -243,6 +243,40 @@ __device__ __forceinline__ void stencil4(const Vec& x, int64_t sx, int dim, int 
   for (int j = 0; j < 4; ++j) g[j] = (A)(2 * dim) * (A)c[j] - nb[j];
 }
 
+// 2-D 9-point stencil (8, -1 x 8) on 4 consecutive points at storage offset o: the
+// reference's bilinear-FEM operator A1(x)M1 + M1(x)A1 after the D = I scaling
+// (centre 1, eight neighbours -1/8; P/src/fem.cpp:426-457, P/src/multigrid.cpp:277-306)
+template <typename M, typename A, bool NC>
+__device__ __forceinline__ void stencil9_4(const Vec& x, int64_t sx, int l, int64_t o, A g[4],
+                                           int64_t c[4]) {
+  const int64_t N = (int64_t)1 << l;
+  V4<M, NC>::load(x, o, sx, c);
+  A nb[4];
+  const int64_t lf = ld1<M, NC>(x, o - 1, sx), rt = ld1<M, NC>(x, o + 4, sx);
+  nb[0] = (A)lf + (A)c[1];
+  nb[1] = (A)c[0] + (A)c[2];
+  nb[2] = (A)c[1] + (A)c[3];
+  nb[3] = (A)c[2] + (A)rt;
+#pragma unroll
+  for (int r = -1; r <= 1; r += 2) {  // the rows above and below: 3 taps each
+    const int64_t ro = o + r * N;
+    int64_t v[4];
+    if (l >= 2) {
+      V4<M, NC>::load(x, ro, sx, v);
+    } else {  // level 1 (N = 2): the neighbouring rows are not 16-B aligned
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = ld1<M, NC>(x, ro + j, sx);
+    }
+    const int64_t vl = ld1<M, NC>(x, ro - 1, sx), vr = ld1<M, NC>(x, ro + 4, sx);
+    nb[0] += (A)vl + (A)v[0] + (A)v[1];
+    nb[1] += (A)v[0] + (A)v[1] + (A)v[2];
+    nb[2] += (A)v[1] + (A)v[2] + (A)v[3];
+    nb[3] += (A)v[2] + (A)v[3] + (A)vr;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) g[j] = (A)8 * (A)c[j] - nb[j];
+}
+
 // ---------------------------------------------------------------------------
 // z = alpha*(A_l x) + beta*y  (EgemvKernel with A = 2^{2l} S_d)
 
@@ -254,6 +288,7 @@ struct GemvOp {
   // (reference-algorithm mode: a quantize_csr'd operator has mantissas 2^gs (2d, -1),
   // e_A = its quantized exponent -- values equal, templates as in the reference)
   int ea, gs;
+  int st9;  // 2-D 9-point operator (reference mode, d = 2) instead of the 5-point S_2
   // derived (uniform per launch)
   int64_t sx, sy, d;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
@@ -266,7 +301,7 @@ struct GemvOp {
     axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
-    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(4 * dim) + 1 + gs), by = zbits(y.hdr);
+    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(st9 ? 16 : 4 * dim) + 1 + gs), by = zbits(y.hdr);
     need = combine_bits(al.m, bg, be.m, by, d);
     // z = X * P + Q * Y with (X, Y) = (g, y), P = alpha 2^d, Q = beta   when d >= 0
     //                         (X, Y) = (y, g), P = beta 2^-d, Q = alpha  when d < 0
@@ -278,7 +313,7 @@ struct GemvOp {
              (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
     w64 = bg <= 62 && sx < 64 && sy < 64 && msb(al.m) + bg <= 63 && msb(be.m) + by <= 63;
     fwi = w64 && need <= 127 && ad < 64;
-    if (gs) narrow = w64 = fwi = false;  // scaled mantissas: the generic exact path
+    if (gs || st9) narrow = w64 = fwi = false;  // scaled mantissas / 9-point: generic exact path
     swap = d < 0;
     P = narrow ? (int)(pm << ad) : 0;
     Q = (int)qm;
@@ -331,7 +366,10 @@ struct GemvOp {
     }
     A g[4];
     int64_t c[4], yv[4];
-    stencil4<M, A, NC>(x, sx, dim, l, o, g, c);
+    if (st9)
+      stencil9_4<M, A, NC>(x, sx, l, o, g, c);
+    else
+      stencil4<M, A, NC>(x, sx, dim, l, o, g, c);
     V4<M, NC>::load(y, o, sy, yv);
     bool pad[4];
     pad4(dim, l, o, pad, z0);

@@ -56,6 +56,7 @@ struct PlanOp {
   bool shard = false;  // output is a slab: partial window + collectives
   int halo = 0;        // HALO_LO / HALO_HI planes of `a` exchanged before the op
   int rep_e = kDefaultRep, rep_gs = 0;  // operator representation (reference mode)
+  int st9 = 0;                          // 2-D 9-point operator (reference mode, d = 2)
 };
 
 int fused_kind(int k) {
@@ -377,7 +378,7 @@ struct RankSolver {
     return BFP_OK;
   }
 
-  // ---- reference-algorithm mode (cfg.ref_mode, d = 1) --------------------------------
+  // ---- reference-algorithm mode (cfg.ref_mode, d = 1 or 2) ---------------------------
   // exact gamma terms: X = norm of v, coefficient c (128-bit + sticky) 2^ce
   static GTerm xterm(const bfp_vec_s* v, const bfp_xf_t& c) {
     GTerm t;
@@ -397,9 +398,17 @@ struct RankSolver {
   }
   int64_t wr(int l) const { return cfg.p[l]; }
   bfp_vec_s* ref_last[33] = {};  // last IR residual buffer per level (SolverContext)
-  // operator representations of quantize_csr at width w (pyref_refmode.quantize_values):
-  // A: mantissas 2^(w-3) (-1, 2, -1), e_A = 2 - w;  P: 2^(w-3) taps, e_P = 2 - w;
-  // R = 2 P^T: 2^(w-3) (1, 2, 1), e_R = 3 - w
+  // operator representations of quantize_csr at width w (pyref_refmode.quantize_values),
+  // as (kernel base stencil / taps) * 2^gs with exponent e:
+  //   1-D  A = tridiag(-1/2, 1, -1/2): 2^(w-3) (2, -1),     e_A = 2 - w
+  //        P = [1/2, 1, 1/2]:          2^(w-3) tap sums,    e_P = 2 - w
+  //        R = 2 P^T = (1, 2, 1):      2^(w-3) (1, 2, 1),   e_R = 3 - w
+  //   2-D  A = (1, -1/8 x 8):          2^(w-5) (8, -1 x 8), e_A = 2 - w   (9-point)
+  //        P = P1 (x) P1 (1, 1/2, 1/4): 2^(w-4) tap sums,   e_P = 2 - w
+  //        R = P^T (D_f = D_c):        2^(w-4) (1,2,1)^2,   e_R = 2 - w
+  int ref_a_gs(int w) const { return cfg.d == 1 ? w - 3 : w - 5; }
+  int ref_p_gs(int w) const { return cfg.d == 1 ? w - 3 : w - 4; }
+  int ref_r_e(int w) const { return cfg.d == 1 ? 3 - w : 2 - w; }
   PlanOp ref_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, int w, bfp_vec_s* out) {
     PlanOp o;
     o.kind = OK_GEMV;
@@ -409,7 +418,8 @@ struct RankSolver {
     o.s1 = al;
     o.s2 = be;
     o.rep_e = 2 - w;
-    o.rep_gs = w - 3;
+    o.rep_gs = ref_a_gs(w);
+    o.st9 = cfg.d == 2;
     return o;
   }
   bfp_vec_s* vcycle_ref(int l, bfp_vec_s* r) {  // P/src/multigrid.cpp:430-456
@@ -427,8 +437,8 @@ struct RankSolver {
       rs.kind = OK_RESTRICT;
       rs.a = L.rv;
       rs.out = Lc.vr;
-      rs.rep_e = 3 - wd;
-      rs.rep_gs = wd - 3;
+      rs.rep_e = ref_r_e(wd);
+      rs.rep_gs = ref_p_gs(wd);
       step(ST_RESTRICT, l, rs, wd, xrule({xterm(L.rv, xint(4))}), 6);
       bfp_vec_s* d = vcycle_ref(l - 1, Lc.vr);
       PlanOp pc;
@@ -439,7 +449,7 @@ struct RankSolver {
       pc.s1 = Scal{-1, 1, 0};
       pc.s2 = Scal{1, 2, 0};
       pc.rep_e = 2 - wd;
-      pc.rep_gs = wd - 3;
+      pc.rep_gs = ref_p_gs(wd);
       step(ST_V_CORR, l, pc, wd, xrule({xterm(y, xint(1)), xterm(d, xint(1))}), 1);
       y = y2;
     }
@@ -492,7 +502,7 @@ struct RankSolver {
       o.a = xc;
       o.out = x;
       o.rep_e = 2 - (int)wr(l);
-      o.rep_gs = (int)wr(l) - 3;
+      o.rep_gs = ref_p_gs((int)wr(l));
       step(ST_FMG_PROLONG, l, o, wr(l), xrule({xterm(xc, xint(1))}), 0);
     }
     for (int k = 0; k < cfg.cycles; ++k) x = ir_ref(l, x, 1);
@@ -502,10 +512,12 @@ struct RankSolver {
   int64_t wc_(int l) const { return wc(l); }
   int build_ref() {
     const int lf = cfg.l_fine;
-    if (cfg.d != 1) return BFP_ERR_ARG;
+    if (cfg.d != 1 && cfg.d != 2) return BFP_ERR_ARG;
+    // the operators' quantize_csr representations are exact from w = 3 (1-D) / 5 (2-D)
+    const int wmin = cfg.d == 1 ? 3 : 5;
     int maxw = 0;
     for (int l = 1; l <= lf; ++l) {
-      if (wr(l) < 3 || wd(l) < 3 || wc(l) < 3) return BFP_ERR_ARG;
+      if (wr(l) < wmin || wd(l) < wmin || wc(l) < wmin) return BFP_ERR_ARG;
       const int cap = cfg.w_add_cap >= 0 ? std::min(cfg.w_add_cap, 6) : 6;
       maxw = std::max(maxw, (int)std::max(std::max(wd(l), wr(l)), wc(l)) + cap);
     }
@@ -532,11 +544,11 @@ struct RankSolver {
       int rc;
       if (cfg.rhs_kind == 1) {
         rc = gen_sine(L.b, wc(l), 0);
-        if (!rc) {  // h^2 / 2 d pi^2 sin: exponent shift, the mantissas are unchanged
+        if (!rc) {  // h^2 / 2^d * d pi^2 prod sin: exponent shift, the mantissas are unchanged
           Hdr h;
           if (cudaMemcpy(&h, L.b->hdr, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
             return BFP_ERR_CUDA;
-          if (h.max_m != 0 || h.min_m != 0) h.e -= 2 * l + 1;
+          if (h.max_m != 0 || h.min_m != 0) h.e -= 2 * l + cfg.d;
           if (cudaMemcpy(L.b->hdr, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess)
             return BFP_ERR_CUDA;
         }
@@ -766,7 +778,8 @@ struct RankSolver {
     switch (op.kind) {
       case OK_ZERO: return set_zero(op.out, op.q, s);
       case OK_UNIFORM: return gen_uniform(op.out, op.q, op.seed, op.sid, s);
-      case OK_GEMV: return op_gemv(op.a, op.b, op.s1, op.s2, p, op.out, s, op.rep_e, op.rep_gs);
+      case OK_GEMV:
+        return op_gemv(op.a, op.b, op.s1, op.s2, p, op.out, s, op.rep_e, op.rep_gs, op.st9);
       case OK_JACOBI: return op_jacobi(op.a, op.b, op.s1, p, op.out, s);
       case OK_SCAL: return op_scal(op.a, op.s1, p, op.out, s);
       case OK_AXPBY: return op_axpby(op.a, op.b, op.s1, op.s2, p, op.out, s);
@@ -1010,8 +1023,8 @@ struct bfp_mg_s {
 extern "C" {
 
 static int check_cfg(const bfp_mg_config_t* cfg) {
-  if (cfg->ref_mode) {  // reference-algorithm mode: 1-D, levels 1 .. l_fine
-    if (cfg->d != 1 || cfg->l_fine < 1 || cfg->l_fine > 30 || cfg->cycles < 0) return BFP_ERR_ARG;
+  if (cfg->ref_mode) {  // reference-algorithm mode: 1-D / 2-D, levels 1 .. l_fine
+    if ((cfg->d != 1 && cfg->d != 2) || cfg->l_fine < 1 || cfg->l_fine > 30 || cfg->cycles < 0) return BFP_ERR_ARG;
     for (int l = 1; l <= cfg->l_fine; ++l)
       if (cfg->p[l] < 3 || cfg->p[l] > 58 || cfg->pd[l] < 0 || cfg->pd[l] > 58 ||
           cfg->pc[l] < 0 || cfg->pc[l] > 58 || cfg->ref_c1d[l].q < 1 || cfg->ref_c2d[l].q < 1)

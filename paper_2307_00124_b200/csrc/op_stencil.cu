@@ -5,8 +5,9 @@
 namespace bfp {
 
 int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bfp_vec_s* out,
-            cudaStream_t s, int ea, int gs) {
+            cudaStream_t s, int ea, int gs, int st9) {
   if (x->dim < 1 || !same_grid(x, y) || !same_grid(x, out)) return BFP_ERR_ARG;
+  if (st9 && x->dim != 2) return BFP_ERR_ARG;
   if (out == x || out == y) return BFP_ERR_ALIAS;
   GemvOp op;
   op.x = view(x);
@@ -18,7 +19,8 @@ int op_gemv(bfp_vec_s* x, bfp_vec_s* y, Scal al, Scal be, const WinParams& p, bf
   op.z0 = x->z0;
   op.ea = ea == kDefaultRep ? 2 * x->l : ea;
   op.gs = gs;
-  if (gs) return launch_grid(op, out, p, s);  // scaled mantissas: generic exact path
+  op.st9 = st9;
+  if (gs || st9) return launch_grid(op, out, p, s);  // scaled mantissas / 9-point: generic path
   return launch_march(op, out, p, s);
 }
 

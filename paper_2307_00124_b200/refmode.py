@@ -84,14 +84,26 @@ def chebyshev_scalars(rho: float, eta: float, prec: int, wdot: List[int]):
     return _top128(c1), _top128(kres), c1d, c2d
 
 
+def _stiffness(level: int, d: int):
+    """The level's stiffness up to a constant (the generalised eigenproblem is scale-free):
+    1-D tridiag(-1, 2, -1); 2-D the 9-point (8, -1 x 8) of A1 (x) M1 + M1 (x) A1."""
+    import numpy as np
+    n = (1 << level) - 1
+    t = 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    if d == 1:
+        return t
+    m = 4.0 * np.eye(n) + np.eye(n, k=1) + np.eye(n, k=-1)  # 6/h M1
+    return np.kron(t, m) + np.kron(m, t)                    # 6 (A1 (x) M1 + M1 (x) A1)
+
+
 def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=None,
-                     ext_prec: int = 400, streams: int = 4):
-    """conv_rate_vcycle (P/src/multigrid.cpp:572-601) in the reference mode, 1-D: one
-    IR-V error-propagation step (b = 0) from every unit vector e_i (from_extfloat at wdot)
-    gives the columns (I - B A) e_i; the columns run as independent solves spread over
-    `streams` CUDA streams (each a replayed graph), and rho_V = sqrt(lambda_max) of the
-    generalised problem (M^T A M, A) with the level's stiffness A ~ tridiag(-1, 2, -1)
-    (rho_v_of_columns, :533-568; here in float64 -- the columns are exact).
+                     ext_prec: int = 400, streams: int = 4, d: int = 1):
+    """conv_rate_vcycle (P/src/multigrid.cpp:572-601) in the reference mode (d = 1 or 2):
+    one IR-V error-propagation step (b = 0) from every unit vector e_i (from_extfloat at
+    wdot) gives the columns (I - B A) e_i; the columns run as independent solves spread
+    over `streams` CUDA streams (each a replayed graph), and rho_V = sqrt(lambda_max) of
+    the generalised problem (M^T A M, A) with the level's stiffness A (rho_v_of_columns,
+    :533-568; here in float64 -- the columns are exact).
     Returns (rho_V, columns as (mantissas, e) per unit vector)."""
     import ctypes as C
 
@@ -100,9 +112,9 @@ def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=No
 
     from . import BfpVec, Multigrid, _raise, lib, mg_config_ref, set_stream
 
-    n = (1 << level) - 1
+    n = ((1 << level) - 1) ** d
     cfg = mg_config_ref(level, rho, eta, w=w, wdot=wdot, wcheck=wcheck, cycles=1, fmg=False,
-                        rhs_kind=2, ext_prec=ext_prec)
+                        rhs_kind=2, ext_prec=ext_prec, d=d)
     cfg.x0_random = 2  # the caller's iterate
     wd = cfg.pd[level] or cfg.p[level]
     L = lib()
@@ -112,7 +124,7 @@ def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=No
     xs, outs = [], []
     for mg in mgs:
         xh, _, _ = mg.vectors()
-        xs.append(BfpVec._view(xh.value, 1, level, 8, mg))
+        xs.append(BfpVec._view(xh.value, d, level, 8, mg))
         outs.append(mg.rank_result(0)[0])  # the final iterate (x_final)
     cols = [None] * n
     try:
@@ -132,6 +144,6 @@ def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=No
     finally:
         set_stream(None)
     M = np.stack([np.ldexp(c[0].astype(np.float64), c[1]) for c in cols], axis=1)
-    A = 2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)
+    A = _stiffness(level, d)
     lam = scipy.linalg.eigh(M.T @ A @ M, A, eigvals_only=True)
     return float(np.sqrt(max(lam.max(), 0.0))), cols

@@ -1,7 +1,8 @@
 """Reference-algorithm parity mode on the GPU vs its big-int
 restatement oracle/pyref_refmode.py: Chebyshev V(1,0) cycles, IR and FMG of
-P/src/multigrid.cpp:430-518 with the Table-1 gamma chain, 1-D p = 1 operators,
-coarsest level 1.  Final iterate, residual history and every trace record must match."""
+P/src/multigrid.cpp:430-518 with the Table-1 gamma chain, 1-D and 2-D p = 1 operators
+(2-D: the 9-point bilinear-FEM operator, P = P1 (x) P1, R = P^T), coarsest level 1.
+Final iterate, residual history and every trace record must match."""
 import pytest
 
 from oracle import pyref as P
@@ -21,19 +22,19 @@ def _levels(v, L):
     return [0] + ([v] * L if isinstance(v, int) else list(v[1:L + 1]))
 
 
-def _rhs(kind, L, wcheck, seed, fmg):
+def _rhs(kind, L, wcheck, seed, fmg, d=1):
     out = {}
     for l in range(1, L + 1):
         if not fmg and l != L:
             continue
         if kind == 1:
-            b = P.gen_sine(1, l, wcheck[l])
+            b = P.gen_sine(d, l, wcheck[l])
             if any(b.m):
-                b.e -= 2 * l + 1
+                b.e -= 2 * l + d
         elif kind == 0:
-            b = P.gen_uniform(1, l, wcheck[l], seed, 2)
+            b = P.gen_uniform(d, l, wcheck[l], seed, 2)
         else:
-            b = P.zero_vec((1 << l) - 1, wcheck[l])
+            b = P.zero_vec(((1 << l) - 1) ** d, wcheck[l])
         out[l] = b
     return out
 
@@ -45,21 +46,29 @@ CASES = [
     dict(L=7, w=16, wdot=16, wcheck=20, rho=2.02, eta=0.15, cycles=5, fmg=False, rhs=0, x0=True),
     dict(L=6, w=40, wdot=36, wcheck=44, rho=2.0, eta=0.5, cycles=3, fmg=False, rhs=1),
     dict(L=5, w=12, wdot=12, wcheck=12, rho=2.02, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
+    # 2-D: rho = lambda_max(D^-1 A) of the 9-point operator is < 2 (Gershgorin); the
+    # reference estimates it by power iteration (P/src/linalg.cpp:272-295), injected here
+    dict(d=2, L=5, w=20, wdot=16, wcheck=24, rho=1.6, eta=0.3, cycles=1, fmg=True, rhs=1),
+    dict(d=2, L=5, w=[0] + [6 + 2 * l for l in range(1, 6)], wdot=[0] + [5 + 2 * l for l in range(1, 6)],
+         wcheck=[0] + [10 + 2 * l for l in range(1, 6)], rho=1.6, eta=0.1, cycles=2, fmg=True, rhs=1),
+    dict(d=2, L=5, w=16, wdot=16, wcheck=20, rho=1.7, eta=0.2, cycles=4, fmg=False, rhs=0, x0=True),
+    dict(d=2, L=6, w=40, wdot=36, wcheck=44, rho=1.6, eta=0.5, cycles=2, fmg=False, rhs=1),
+    dict(d=2, L=4, w=8, wdot=8, wcheck=8, rho=1.6, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}")
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c.get('d', 1)}_L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}")
 def test_refmode_gpu_vs_pyref(B, case):
-    L = case["L"]
+    L, d = case["L"], case.get("d", 1)
     w, wd, wc = (_levels(case[k], L) for k in ("w", "wdot", "wcheck"))
     seed = 3
-    x0 = P.gen_uniform(1, L, w[L], seed, 1) if case.get("x0") else None
+    x0 = P.gen_uniform(d, L, w[L], seed, 1) if case.get("x0") else None
     cfg = R.RefConfig(l_fine=L, w=w, wdot=wd, wcheck=wc, rho=case["rho"], eta=case["eta"],
-                      cycles=case["cycles"], fmg=case["fmg"], x0=x0)
-    want = R.RefMg(cfg, _rhs(case["rhs"], L, wc, seed, case["fmg"])).run()
+                      cycles=case["cycles"], fmg=case["fmg"], x0=x0, d=d)
+    want = R.RefMg(cfg, _rhs(case["rhs"], L, wc, seed, case["fmg"], d)).run()
     gcfg = B.mg_config_ref(L, case["rho"], case["eta"], w=w, wdot=wd, wcheck=wc,
                            cycles=case["cycles"], fmg=case["fmg"], x0_random=bool(case.get("x0")),
-                           rhs_kind=case["rhs"], seed=seed)
+                           rhs_kind=case["rhs"], seed=seed, d=d)
     for graph in (False, True):
         mg = B.Multigrid(gcfg)
         mg.solve(use_graph=graph)
@@ -69,19 +78,21 @@ def test_refmode_gpu_vs_pyref(B, case):
         assert e == want.x.e and x.tolist() == want.x.m
 
 
-def test_conv_rate_vcycle_columns(B):
+@pytest.mark.parametrize("d,L", [(1, 4), (2, 3)])
+def test_conv_rate_vcycle_columns(B, d, L):
     """conv_rate_vcycle (P/src/multigrid.cpp:572-601): every column (I - B A) e_i of the
     batched GPU run equals the restatement's, and rho_V is a contraction."""
     from paper_2307_00124_b200 import refmode
-    L, w, wd, wc, rho, eta = 4, 20, 16, 24, 2.02, 0.3
-    rate, cols = refmode.conv_rate_vcycle(L, rho, eta, w=w, wdot=wd, wcheck=wc, streams=4)
-    n = (1 << L) - 1
+    w, wd, wc, eta = 20, 16, 24, 0.3
+    rho = 2.02 if d == 1 else 1.6
+    rate, cols = refmode.conv_rate_vcycle(L, rho, eta, w=w, wdot=wd, wcheck=wc, streams=4, d=d)
+    n = ((1 << L) - 1) ** d
     lv = [0] + [w] * L, [0] + [wd] * L, [0] + [wc] * L
     for i in range(n):
         x0 = P.Block([0] * n, wd, 2 - wd)
         x0.m[i] = 1 << (wd - 2)
         cfg = R.RefConfig(l_fine=L, w=lv[0], wdot=lv[1], wcheck=lv[2], rho=rho, eta=eta, cycles=1,
-                          fmg=False, x0=x0)
+                          fmg=False, x0=x0, d=d)
         want = R.RefMg(cfg, {L: P.zero_vec(n, wc)}).run()
         assert cols[i][1] == want.x.e and cols[i][0].tolist() == want.x.m, i
     assert 0.0 < rate < 1.0

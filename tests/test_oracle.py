@@ -418,3 +418,54 @@ def test_refmode_scalar_up_equals_inf_norm_upper():
         want = P.inf_norm_upper(b, 16)
         got = R.scalar_up(R.xf_exact_norm(b))
         assert (got.m[0], got.e) == (want.m[0], want.e)
+
+
+@pytest.mark.parametrize("j", [2, 3, 4])
+def test_refmode_2d_operators_from_fem(j):
+    """The 2-D reference-mode operators of oracle/pyref_refmode.py equal the reference's
+    construction in exact arithmetic: A = A1 (x) M1 + M1 (x) A1 with A1 = (1/h)
+    tridiag(-1, 2, -1), M1 = (h/6) tridiag(1, 4, 1) (P/src/fem.cpp:426-457, 677-700),
+    scaled to D^-1 A; P = P1 (x) P1 (:542-543); R = D_c^-1 P^T D_f
+    (P/src/multigrid.cpp:277-306)."""
+    from oracle import pyref_refmode as R
+
+    def tri(n, a, b, s):
+        return [[s * (b if i == k else a if abs(i - k) == 1 else 0) for k in range(n)]
+                for i in range(n)]
+
+    def kron(a, b):
+        ra, ca, rb, cb = len(a), len(a[0]), len(b), len(b[0])
+        return [[a[i // rb][k // cb] * b[i % rb][k % cb] for k in range(ca * cb)]
+                for i in range(ra * rb)]
+
+    def dense(ent, rows, cols):
+        m = [[Fraction(0)] * cols for _ in range(rows)]
+        for i, row in ent.items():
+            for c, v in row:
+                m[i][c] += v
+        return m
+
+    def stiff(jj):
+        n, h = (1 << jj) - 1, Fraction(1, 1 << jj)
+        a1, m1 = tri(n, Fraction(-1), Fraction(2), 1 / h), tri(n, Fraction(1), Fraction(4), h / 6)
+        return [[x + y for x, y in zip(r1, r2)] for r1, r2 in zip(kron(a1, m1), kron(m1, a1))]
+
+    A, Ac = stiff(j), stiff(j - 1)
+    n, nc = len(A), len(Ac)
+    D, Dc = [A[i][i] for i in range(n)], [Ac[i][i] for i in range(nc)]
+    assert all(v == Fraction(8, 3) for v in D + Dc)  # D_f = D_c: R = P^T
+    assert dense(R._entries_a2(j), n, n) == [[A[i][k] / D[i] for k in range(n)] for i in range(n)]
+    nf1, nc1 = (1 << j) - 1, (1 << (j - 1)) - 1
+    P1 = dense(R._entries_p1(j), nf1, nc1)
+    Pk = kron(P1, P1)
+    Pt = [[Pk[i][k] * D[i] / Dc[k] for i in range(n)] for k in range(nc)]
+    # quantize_csr at a width where every value is exact: the CSR values are the operator
+    w = 12
+    for op, want in ((R.op_a(j, w, 2), [[A[i][k] / D[i] for k in range(n)] for i in range(n)]),
+                     (R.op_p(j, w, 2), Pk), (R.op_r(j, w, 2), Pt)):
+        got = [[Fraction(0)] * len(want[0]) for _ in range(len(want))]
+        for i in range(op.rows):
+            for t in range(op.rowptr[i], op.rowptr[i + 1]):
+                got[i][op.col[t]] = Fraction(op.m[t]) * Fraction(2) ** op.e
+        assert got == want
+    assert R.op_a(j, w, 2).e == 2 - w and R.op_p(j, w, 2).e == 2 - w and R.op_r(j, w, 2).e == 2 - w
