@@ -417,6 +417,8 @@ struct WinParams {
   TraceRec* trace;
   double* hist;   // residual-norm history slot (ldexp(max|m|, e)), or nullptr
   int64_t* part;  // multi-rank: write {mu*, max, -min, err} partials here instead of finalizing
+  int32_t defer;  // multi-block pass 1: accumulate only, a deferred-finalize kernel follows
+  int32_t pad_;
   GammaRule gamma;
 };
 
@@ -477,53 +479,67 @@ __device__ __forceinline__ uint64_t shfl_or64(uint64_t v) {
   return v;
 }
 
+// Block reduction of the per-thread running values; the result is valid in thread 0.
+struct BlockRed {
+  uint64_t lo, hi;
+  int err;
+  int64_t mx, mn;
+};
+__device__ inline BlockRed block_reduce(const Red& r) {
+  __shared__ unsigned long long s_lo[32], s_hi[32];
+  __shared__ int s_err[32];
+  __shared__ long long s_mx[32], s_mn[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  BlockRed b;
+  b.lo = shfl_or64(r.olo);
+  b.hi = shfl_or64(r.ohi);
+  b.err = __reduce_or_sync(0xffffffffu, r.err);
+  b.mx = shfl_max64(r.mx);
+  b.mn = shfl_min64(r.mn);
+  if (lane == 0) {
+    s_lo[wid] = b.lo;
+    s_hi[wid] = b.hi;
+    s_err[wid] = b.err;
+    s_mx[wid] = b.mx;
+    s_mn[wid] = b.mn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      b.lo |= s_lo[w];
+      b.hi |= s_hi[w];
+      b.err |= s_err[w];
+      b.mx = s_mx[w] > b.mx ? s_mx[w] : b.mx;
+      b.mn = s_mn[w] < b.mn ? s_mn[w] : b.mn;
+    }
+  }
+  return b;
+}
+__device__ __forceinline__ int mu_bits(uint64_t lo, uint64_t hi) {
+  return (hi ? 64 + bitlen64(hi) : bitlen64(lo)) + 1;  // mu* (init 1, src/blas.cpp:153)
+}
+// one block's contribution to the header accumulators (fire-and-forget atomics)
+__device__ __forceinline__ void accumulate(Hdr* h, const BlockRed& b) {
+  if (b.lo) atomicOr(&h->acc_or_lo, (unsigned long long)b.lo);
+  if (b.hi) atomicOr(&h->acc_or_hi, (unsigned long long)b.hi);
+  atomicMax(&h->acc_max, (long long)b.mx);
+  atomicMin(&h->acc_min, (long long)b.mn);
+  if (b.err) atomicOr(&h->acc_err, b.err);
+}
+
 // Block reduce + cross-block atomics + last-block finalize.  `fin` is called
 // by exactly one thread of the last block to finish, after every block's
 // contribution is visible: fin(mu_star, max, min, err).
 template <typename Fin>
 __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
-  __shared__ unsigned long long s_lo[32], s_hi[32];
-  __shared__ int s_err[32];
-  __shared__ long long s_mx[32], s_mn[32];
   __shared__ bool s_last;
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  uint64_t lo = shfl_or64(r.olo), hi = shfl_or64(r.ohi);
-  int err = __reduce_or_sync(0xffffffffu, r.err);
-  int64_t mx = shfl_max64(r.mx), mn = shfl_min64(r.mn);
-  if (lane == 0) {
-    s_lo[wid] = lo;
-    s_hi[wid] = hi;
-    s_err[wid] = err;
-    s_mx[wid] = mx;
-    s_mn[wid] = mn;
-  }
-  __syncthreads();
+  BlockRed b = block_reduce(r);
   if (gridDim.x == 1) {  // single block: finalize directly, no global accumulators
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < nw; ++w) {
-        lo |= s_lo[w];
-        hi |= s_hi[w];
-        err |= s_err[w];
-        mx = s_mx[w] > mx ? s_mx[w] : mx;
-        mn = s_mn[w] < mn ? s_mn[w] : mn;
-      }
-      fin((hi ? 64 + bitlen64(hi) : bitlen64(lo)) + 1, mx, mn, err);
-    }
+    if (threadIdx.x == 0) fin(mu_bits(b.lo, b.hi), b.mx, b.mn, b.err);
     return;
   }
   if (threadIdx.x == 0) {
-    for (int w = 1; w < nw; ++w) {
-      lo |= s_lo[w];
-      hi |= s_hi[w];
-      err |= s_err[w];
-      mx = s_mx[w] > mx ? s_mx[w] : mx;
-      mn = s_mn[w] < mn ? s_mn[w] : mn;
-    }
-    if (lo) atomicOr(&h->acc_or_lo, (unsigned long long)lo);
-    if (hi) atomicOr(&h->acc_or_hi, (unsigned long long)hi);
-    atomicMax(&h->acc_max, (long long)mx);
-    atomicMin(&h->acc_min, (long long)mn);
-    if (err) atomicOr(&h->acc_err, err);
+    accumulate(h, b);
     __threadfence();
     unsigned int done = atomicAdd(&h->acc_done, 1u);
     s_last = (done == gridDim.x - 1);
@@ -542,8 +558,7 @@ __device__ inline void reduce_and_finalize(Red& r, Hdr* h, Fin fin) {
     h->acc_min = INT64_MAX;
     h->acc_err = 0;
     h->acc_done = 0;
-    int bits = (fhi ? 64 + bitlen64(fhi) : bitlen64(flo)) + 1;  // mu* (init 1, src/blas.cpp:153)
-    fin(bits, fmx, fmn, ferr);
+    fin(mu_bits(flo, fhi), fmx, fmn, ferr);
   }
 }
 
@@ -667,6 +682,33 @@ __device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h,
     h->min_m = mn;
     h->need_recompute = 0;
     write_hist(p, h);
+  }
+}
+
+// Reduction + finalize of a windowed pass.  A multi-block pass 1 (qcomp or nnqcomp)
+// launched with p.defer only accumulates: each block's partial goes to the header with
+// fire-and-forget atomics and block 0 records the window context; the stream-ordered
+// deferred-finalize kernel (one thread, bfp_lib.cu) then applies win_finalize from the
+// accumulators.  The kernel boundary makes every contribution visible, so the
+// threadfence / counter / last-block round trips of reduce_and_finalize (~2 us on a
+// dependent chain) leave the critical path.
+template <typename Fin>
+__device__ inline void window_reduce(Red& r, Hdr* h, const WinParams& p, const WinCtx& c,
+                                     Fin fin) {
+  if (!p.defer || gridDim.x == 1 || p.mode == MODE_RECOMPUTE) {
+    reduce_and_finalize(r, h, fin);
+    return;
+  }
+  BlockRed b = block_reduce(r);
+  if (threadIdx.x == 0) {
+    accumulate(h, b);
+    if (blockIdx.x == 0) {
+      h->st_estar = c.e_star;
+      h->st_mutmp = c.mu_tmp;
+      h->st_lam = c.lam;
+      h->st_gm = c.gm;
+      h->st_ge = c.ge;
+    }
   }
 }
 

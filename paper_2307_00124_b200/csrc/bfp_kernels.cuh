@@ -21,6 +21,14 @@ extern bool g_skip_recompute;  // measurement only: pass 1 alone (flags must be 
 extern bool g_prof;            // CUDA-event brackets around pass-1 launches
 extern bool g_use_bulk;        // 2-D stencils through the bulk-async pipeline
 std::pair<cudaEvent_t, cudaEvent_t> prof_pair();
+// the one-thread finalize of a deferred multi-block pass 1 (bfp_lib.cu)
+int launch_deferred_finalize(const bfpdev::Vec& out, const bfpdev::WinParams& p, int storage_bits,
+                             cudaStream_t s);
+// pass 1 on more than one block finalizes through the deferred kernel (not multi-rank
+// partials, which have their own finalize)
+inline int defer_ok(const bfpdev::WinParams& p, int blocks) {
+  return blocks > 1 && p.part == nullptr && p.mode != bfpdev::MODE_RECOMPUTE;
+}
 
 constexpr int kThreads = 256;
 constexpr int kMaxBlocks = 148 * 8;
@@ -188,7 +196,7 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   r.init();
   grid_body<MODE, M>(op, out, p, c, r, need);
   if (MODE != MODE_QCOMP || gridDim.x != 1 || p.part) griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
   if constexpr (MODE == MODE_QCOMP) {
@@ -380,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, DIM == 2 ? 3 : 2) march_win_kernel(O
   } else
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -565,7 +573,7 @@ __global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Ve
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1052,7 +1060,7 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
     grid_body<MODE, T>(op, out, p, c, r, need);  // exact generic path (or the width error)
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1223,7 +1231,7 @@ __global__ void __launch_bounds__(kP3T, 4)
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1381,7 +1389,7 @@ __global__ void __launch_bounds__(kR3T, 8)
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1528,7 +1536,7 @@ __global__ void __launch_bounds__(kP2T, 4) pro2_win_kernel(Op op, Vec out, WinPa
     grid_body<MODE, int32_t>(op, out, p, c, r, need);
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1662,7 +1670,7 @@ __global__ void __launch_bounds__(kR2T, 8) rst2_win_kernel(RestrictOp op, Vec ou
     grid_body<MODE, int32_t>(op, out, p, c, r, need);
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1695,7 +1703,7 @@ __global__ void __launch_bounds__(kThreads) flat_win_kernel(Op op, Vec out, WinP
     }
   }
   griddep_launch_dependents();
-  reduce_and_finalize(r, out.hdr, [&](int bits, int64_t mx, int64_t mn, int err) {
+  window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
     win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
 }
@@ -1740,6 +1748,7 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
     }
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -1748,6 +1757,8 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part && b > 1) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -1817,6 +1828,7 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
       launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -1825,6 +1837,8 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -1871,6 +1885,7 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
       launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -1879,6 +1894,8 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -1918,6 +1935,7 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
       launch_pdl(rst3_win_kernel<MODE_RECOMPUTE>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -1926,6 +1944,8 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -1965,6 +1985,7 @@ static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int
       launch_pdl(kr, b, threads, smem, s, args..., o, pp, R);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -1973,6 +1994,8 @@ static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -2025,6 +2048,7 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
       launch_pdl(bulk_win_kernel<MODE_RECOMPUTE, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -2033,6 +2057,8 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
   } else {
     go(p);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);
@@ -2051,6 +2077,11 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
     return launch_grid(op, out, p0, s);
   if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW)
     return launch_bulk(op, out, p0, s);
+  // below the bulk pipeline's size a resident wave holds every 4-group with one group per
+  // thread: the generic grid kernel issues all of a group's loads at once, where the march
+  // (>= 4 dependent steps per thread) is latency-bound on these L2-resident levels
+  static const bool march_mid = getenv("BFP_MARCH_MID") != nullptr;  // A/B switch
+  if (!march_mid && out->dim == 2) return launch_grid(op, out, p0, s);
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
@@ -2091,6 +2122,7 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
     }
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   if (g_prof) {
     auto ev = prof_pair();
     cudaEventRecord(ev.first, s);
@@ -2099,6 +2131,8 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
   } else {
     go(p, b);
   }
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !g_skip_recompute && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p, b);
@@ -2120,7 +2154,10 @@ static inline int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0,
       launch_pdl(flat_win_kernel<int64_t, Op>, b, kThreads, 0, s, op, o, pp);
     count_launch();
   };
+  p.defer = defer_ok(p, b);
   go(p);
+  if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
+  p.defer = 0;
   if (p.mode == MODE_QCOMP && !p.part) {
     p.mode = MODE_RECOMPUTE;
     go(p);

@@ -63,6 +63,44 @@ __global__ void window_finalize_kernel(Vec out, WinParams p, const int64_t* part
                (int)part[3]);
 }
 
+// deferred finalize of a multi-block pass 1 (bfpdev::window_reduce): the blocks'
+// accumulated {OR, max, min, err} and block 0's window context -> win_finalize, then the
+// accumulators are reset for the next op writing this vector
+__global__ void deferred_finalize_kernel(Vec out, WinParams p, int storage_bits) {
+  griddep_wait();
+  griddep_launch_dependents();  // dependents still wait for this grid's completion
+  if (threadIdx.x != 0) return;
+  Hdr* h = out.hdr;
+  const volatile Hdr* vh = h;
+  const uint64_t lo = vh->acc_or_lo, hi = vh->acc_or_hi;
+  const int64_t mx = vh->acc_max, mn = vh->acc_min;
+  const int err = vh->acc_err;
+  WinCtx c;
+  c.e_star = vh->st_estar;
+  c.mu_tmp = vh->st_mutmp;
+  c.lam = vh->st_lam;
+  c.gm = vh->st_gm;
+  c.ge = vh->st_ge;
+  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
+  c.skip = 0;
+  c.rs = c.ls = 0;
+  h->acc_or_lo = 0;
+  h->acc_or_hi = 0;
+  h->acc_max = INT64_MIN;
+  h->acc_min = INT64_MAX;
+  h->acc_err = 0;
+  p.defer = 0;
+  win_finalize(p, c, h, mu_bits(lo, hi), mx, mn, err);
+}
+
+namespace bfp {
+int launch_deferred_finalize(const Vec& out, const WinParams& p, int storage_bits, cudaStream_t s) {
+  launch_pdl(deferred_finalize_kernel, 1, 32, 0, s, out, p, storage_bits);
+  count_launch();
+  return BFP_OK;
+}
+}  // namespace bfp
+
 // logical index <-> storage offset
 // local logical index (interior points of the vector / slab, x fastest); for slabs the
 // slowest axis starts at global plane z0
