@@ -331,6 +331,11 @@ def test_mg_golden_gpu(B):
     ("c2_hybrid", dict(d=2, l_fine=8, cycles=6, rhs_kind=1, nonnormalized="hybrid"), 20),
     ("c4", dict(d=3, l_fine=6, cycles=1, rhs_kind=1, fmg=True), 24),
     ("c5", dict(d=3, l_fine=5, cycles=3, x0_random=True, rhs_kind=2), 48),
+    # the V(nu1, nu2) x n_ir variants of the FMG time-to-accuracy sweep (tools/fmg_sweep.py)
+    ("c4_v21_n2", dict(d=3, l_fine=6, cycles=2, rhs_kind=1, fmg=True, nu2=1), 24),
+    ("c4_v10_n3_nc4", dict(d=3, l_fine=5, cycles=3, rhs_kind=1, fmg=True, nu1=1, nu2=0,
+                           n_coarse=4), 24),
+    ("c2_v12", dict(d=2, l_fine=7, cycles=3, rhs_kind=1, nu1=1, nu2=2), 20),
 ])
 def test_mg_gpu_vs_oracle(B, name, cfgkw, p):
     ox, oh, otr = ob.mg_run(ob.mg_config(**cfgkw, p=p))
