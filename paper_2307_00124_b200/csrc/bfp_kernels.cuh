@@ -1719,6 +1719,14 @@ static inline int check_window(const WinParams& p, const bfp_vec_s* out) {
   return BFP_OK;
 }
 
+// tiny levels run as one block (finalize and qcomp recompute in the same launch); above
+// two 4-groups per thread a multi-block pass plus the deferred finalize is faster
+// (measured: tools/op_latency.py)
+#ifndef BFP_SINGLE_BLOCK_GROUPS
+#define BFP_SINGLE_BLOCK_GROUPS 512
+#endif
+constexpr int64_t kSingleBlockGroups = BFP_SINGLE_BLOCK_GROUPS;
+
 // launch a grid-windowed op: nnqcomp (one pass) or qcomp (pass 1 + recompute)
 template <typename Op>
 static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
@@ -1727,7 +1735,7 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   Vec o = view(out);
   // tiny levels: one block (finalized without cross-block atomics)
   const int64_t groups = out->span / 4;
-  const int b = groups <= 2048 ? 1 : blocks_for(groups);
+  const int b = groups <= kSingleBlockGroups ? 1 : blocks_for(groups);
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * 148) : b;
