@@ -419,6 +419,9 @@ struct WinParams {
   int64_t* part;  // multi-rank: write {mu*, max, -min, err} partials here instead of finalizing
   int32_t defer;  // multi-block pass 1: accumulate only, a deferred-finalize kernel follows
   int32_t pad_;
+#ifdef BFP_TIMING
+  long long* dbg;  // phase stamps of grid_win_kernel launches (measurement builds)
+#endif
   GammaRule gamma;
 };
 
@@ -639,12 +642,12 @@ __device__ inline void win_partial(const WinParams& p, const WinCtx& c, Hdr* h, 
   }
 }
 
-// finalize for one launch (runs on one thread)
-__device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, int bits,
-                                    int64_t mx, int64_t mn, int err) {
+// finalize for one launch (runs on one thread); returns need_recompute
+__device__ inline int win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, int bits,
+                                   int64_t mx, int64_t mn, int err) {
   if (p.part) {
     win_partial(p, c, h, bits, mx, mn, err);
-    return;
+    return 0;
   }
   if (err) h->err |= err;
   if (p.mode == MODE_QCOMP) {
@@ -666,6 +669,7 @@ __device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h,
     h->flags = (ovf ? FLAG_OVERFLOW : 0) | (unf ? FLAG_UNDERFLOW : 0) |
                (rc ? FLAG_RECOMPUTED : 0) | FLAG_NORMALIZED;
     write_trace(p, c, ovf, unf, rc, 1);
+    return rc;
   } else if (p.mode == MODE_NNQ) {
     h->q = p.w_out;
     h->e = c.e_star + c.lam;                // src/blas.cpp:211
@@ -683,6 +687,7 @@ __device__ inline void win_finalize(const WinParams& p, const WinCtx& c, Hdr* h,
     h->need_recompute = 0;
     write_hist(p, h);
   }
+  return 0;
 }
 
 // Reduction + finalize of a windowed pass.  A multi-block pass 1 (qcomp or nnqcomp)

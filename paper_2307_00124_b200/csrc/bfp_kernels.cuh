@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -54,6 +55,12 @@ inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kern, args...);
 }
+// smallest level a pipelined (bulk / TMA) kernel takes over from the generic grid kernel;
+// BFP_<NAME> in the environment overrides the default (A/B measurements)
+inline int min_level(const char* name, int def) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : def;
+}
 inline int blocks_for(int64_t work) {
   int64_t b = (work + kThreads - 1) / kThreads;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, kMaxBlocks));
@@ -67,6 +74,28 @@ inline int last_launch() {
   return BFP_OK;
 }
 }  // namespace bfp
+
+// measurement builds (-DBFP_TIMING): thread 0 of block 0 of each grid_win_kernel launch
+// records %globaltimer at its phase boundaries into bfp_dbg_stamps (bfp_lib.cu)
+#ifdef BFP_TIMING
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define BFP_STAMP(k)                                                         \
+  long long _st##k = (threadIdx.x == 0 && blockIdx.x == 0) ? gtimer() : 0;  \
+  (void)_st##k
+#define BFP_STAMP_END()                                                                \
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p.dbg) {                                  \
+    unsigned i = atomicAdd(reinterpret_cast<unsigned*>(p.dbg), 1u) % 4095 + 1;          \
+    long long* d = p.dbg + 8 * i;                                                      \
+    d[0] = _st0; d[1] = _st1; d[2] = _st2; d[3] = _st3; d[4] = _st4; d[6] = gtimer();   \
+  }
+#else
+#define BFP_STAMP(k)
+#define BFP_STAMP_END()
+#endif
 
 using namespace bfpdev;
 using bfp::kThreads;
@@ -187,22 +216,35 @@ __device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinPar
 
 template <int MODE, typename M, typename Op>
 __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinParams p) {
+  BFP_STAMP(0);
   griddep_wait();
+  BFP_STAMP(1);
   int64_t need = 0;
   WinCtx c;
   block_setup<Op, M>(op, out, p, c, need);
+  BFP_STAMP(2);
   if (c.skip) return;
   Red r;
   r.init();
   grid_body<MODE, M>(op, out, p, c, r, need);
+  BFP_STAMP(3);
   if (MODE != MODE_QCOMP || gridDim.x != 1 || p.part) griddep_launch_dependents();
+  __shared__ int s_rc;  // single block: thread 0's finalize verdict (need_recompute)
   window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
-    win_finalize(p, c, out.hdr, bits, mx, mn, err);
+    s_rc = win_finalize(p, c, out.hdr, bits, mx, mn, err);
   });
+  BFP_STAMP(4);
   if constexpr (MODE == MODE_QCOMP) {
-    // a single-block qcomp runs its recompute pass in the same launch (no second kernel)
+    // a single-block qcomp runs its recompute pass in the same launch (no second kernel);
+    // the fast path decides from shared memory, without re-reading the header
     if (gridDim.x == 1 && !p.part) {
       __syncthreads();  // header finalized by thread 0
+      if (!s_rc) {
+        BFP_STAMP(5);
+        griddep_launch_dependents();
+        BFP_STAMP_END();
+        return;
+      }
       WinParams p2 = p;
       p2.mode = MODE_RECOMPUTE;
       WinCtx c2;
@@ -215,9 +257,11 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
           win_finalize(p2, c2, out.hdr, bits, mx, mn, err);
         });
       }
+      BFP_STAMP(5);
       griddep_launch_dependents();
     }
   }
+  BFP_STAMP_END();
 }
 
 
@@ -2078,12 +2122,15 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
 
 template <typename Op>
 static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
-  if (g_use_bulk && out->dim == 3 && (int64_t(1) << out->l) >= kB3W)
+  // level 7 (2M points, L2-resident) is faster on the one-group-per-thread grid kernel
+  static const int b3_min = min_level("BFP_B3_MIN_L", 8);  // kB3W = 128 columns
+  if (g_use_bulk && out->dim == 3 && (int64_t(1) << out->l) >= kB3W && out->l >= b3_min)
     return out->ebytes == 4 ? launch_bulk3<int32_t>(op, out, p0, s)
                             : launch_bulk3<int64_t>(op, out, p0, s);
   if (out->ebytes != 4 || out->dim < 2 || (int64_t(1) << out->l) < kMarchMinN)
     return launch_grid(op, out, p0, s);
-  if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW)
+  static const int b2_min = min_level("BFP_B2_MIN_L", 10);  // kBulkW = 1024 columns
+  if (g_use_bulk && out->dim == 2 && (int64_t(1) << out->l) >= kBulkW && out->l >= b2_min)
     return launch_bulk(op, out, p0, s);
   // below the bulk pipeline's size a resident wave holds every 4-group with one group per
   // thread: the generic grid kernel issues all of a group's loads at once, where the march

@@ -101,6 +101,17 @@ int launch_deferred_finalize(const Vec& out, const WinParams& p, int storage_bit
 }
 }  // namespace bfp
 
+#ifdef BFP_TIMING
+static long long* g_dbg = nullptr;  // record 0: launch counter; 4095 ring records of 8 stamps
+extern "C" int bfp_dbg_stamps(long long* out, int n) {
+  cudaDeviceSynchronize();
+  if (!g_dbg) return 0;
+  cudaMemcpy(out, g_dbg, sizeof(long long) * 8 * (size_t)n, cudaMemcpyDeviceToHost);
+  cudaMemset(g_dbg, 0, sizeof(long long) * 8 * 4096);
+  return 1;
+}
+#endif
+
 // logical index <-> storage offset
 // local logical index (interior points of the vector / slab, x fastest); for slabs the
 // slowest axis starts at global plane z0
@@ -506,6 +517,13 @@ int window_finalize(bfp_vec_s* out, WinParams p, int stage, const int64_t* part,
 WinParams win_params(int mode, int64_t w_out, int64_t w_tmp, int force) {
   WinParams p;
   memset(&p, 0, sizeof(p));
+#ifdef BFP_TIMING
+  if (!g_dbg) {
+    cudaMalloc(&g_dbg, sizeof(long long) * 8 * 4096);
+    cudaMemset(g_dbg, 0, sizeof(long long) * 8 * 4096);
+  }
+  p.dbg = g_dbg;
+#endif
   p.w_out = w_out;
   p.w_tmp = mode == MODE_QCOMP ? w_tmp : w_out;
   p.mode = mode;

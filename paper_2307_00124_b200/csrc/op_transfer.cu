@@ -45,8 +45,9 @@ int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.er = er == kDefaultRep ? -2 * r->dim : er;
   op.gs = gs;
   if (gs) return launch_grid(op, out, p, s);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 6) return launch_rst3(op, out, p, s);
-  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 9) return launch_rst2(op, out, p, s);
+  static const int r3 = min_level("BFP_RST3_MIN_L", 7), r2 = min_level("BFP_RST2_MIN_L", 9);
+  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= r3) return launch_rst3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= r2) return launch_rst2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
@@ -68,8 +69,9 @@ int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.ep = ep == kDefaultRep ? -out->dim : ep;
   op.gs = gs;
   if (gs) return launch_grid(op, out, p, s);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
-  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
+  static const int p3 = min_level("BFP_PRO3_MIN_L", 7), p2 = min_level("BFP_PRO2_MIN_L", 10);
+  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= p3) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= p2) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
@@ -89,8 +91,9 @@ int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_
   op.al = al;
   op.be = be;
   if (gs || al.m != 1 || be.m != 1) return launch_grid(op, out, p, s);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= 7) return launch_pro3(op, out, p, s);
-  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= 10) return launch_pro2(op, out, p, s);
+  static const int p3 = min_level("BFP_PRO3_MIN_L", 7), p2 = min_level("BFP_PRO2_MIN_L", 10);
+  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= p3) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= p2) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
 
