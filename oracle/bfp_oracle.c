@@ -198,6 +198,30 @@ static void axpby_setup(int64_t qa, int64_t ea, int64_t qb, int64_t eb, int64_t*
   *e = min64(ea, eb);
 }
 
+/* The same with all-zero terms dropped (za / zb: the term is zero on every row).  When
+ * exactly one term is zero its alignment shift goes too: d = 0, e* = the other term's
+ * exponent, and *zd grows by e* - min(ea, eb).  Every row is then the reference row
+ * / 2^zd exactly, so qcomp/nnqcomp windows are unchanged; only qcomp's all-zero anchor
+ * (mu* = 1, P/src/blas.cpp:153) needs zd.  This keeps rows within 127 bits where a zero
+ * block at e = 0 meets a far-away operand (b = 0 and a diverging iterate, C5 p = 4);
+ * the reference's mpz rows are merely long there.  pyref.py keeps the plain template. */
+static void axpby_setup_z(int64_t qa, int64_t ea, int za, int64_t qb, int64_t eb, int zb,
+                          int64_t* d, int64_t* q, int64_t* e, int64_t* zd) {
+  axpby_setup(qa, ea, qb, eb, d, q, e);
+  if (!za != !zb) {
+    const int64_t ee = za ? eb : ea;
+    *zd += ee - *e;
+    *e = ee;
+    *d = 0;
+    *q = max64(qa, qb) + 1;
+  }
+}
+static int blk_zero(const ob_block* b) {
+  for (int64_t i = 0; i < b->n; ++i)
+    if (b->m[i]) return 0;
+  return 1;
+}
+
 /* alpha*a*2^max(d,0) + beta*b*2^max(-d,0) with alpha/beta mantissas.
  * P/src/blas.cpp:60-72 (row) and 133-141 */
 static inline int axpby_combine(i128 am, i128 a, i128 bm, i128 b, int64_t d, i128* out) {
@@ -223,7 +247,8 @@ int ob_make_axpby(ob_kernel* k, const ob_block* x, const ob_block* y, int64_t am
   if (x->n != y->n) return OB_ERR_ARG;
   memset(k, 0, sizeof(*k));
   int64_t qa = aq + x->q, qb = bq + y->q, ea = ae + x->e, eb = be + y->e;
-  axpby_setup(qa, ea, qb, eb, &k->p[6], &k->q, &k->e);
+  axpby_setup_z(qa, ea, am == 0 || blk_zero(x), qb, eb, bm == 0 || blk_zero(y), &k->p[6], &k->q,
+                &k->e, &k->zd);
   k->p[0] = am; k->p[1] = aq; k->p[2] = ae;
   k->p[3] = bm; k->p[4] = bq; k->p[5] = be;
   k->ptr[0] = x->m;
@@ -274,7 +299,8 @@ int ob_make_gemv(ob_kernel* k, const ob_csr* a, const ob_block* x, const ob_bloc
   if (m_a < a->max_row_nnz) return OB_ERR_ARG;
   memset(k, 0, sizeof(*k));
   int64_t gq = a->q + x->q + ceil_log2(max64(m_a, 1)), ge = a->e + x->e;
-  axpby_setup(aq + gq, ae + ge, bq + y->q, be + y->e, &k->p[6], &k->q, &k->e);
+  axpby_setup_z(aq + gq, ae + ge, am == 0 || blk_zero(x), bq + y->q, be + y->e,
+                bm == 0 || blk_zero(y), &k->p[6], &k->q, &k->e, &k->zd);
   k->p[0] = am; k->p[1] = aq; k->p[2] = ae;
   k->p[3] = bm; k->p[4] = bq; k->p[5] = be;
   k->p[7] = gq; k->p[8] = ge;
@@ -323,7 +349,7 @@ int ob_qcomp(const ob_kernel* k, int64_t w_out, int64_t w_tmp, int64_t gm, int64
   const int64_t mu_tmp = msb128(gm) + ge - k->e;      /* :150 */
   const int64_t lam_tmp = mu_tmp - w_tmp;             /* :151 */
   i128* tmp = (i128*)malloc(sizeof(i128) * (size_t)(n > 0 ? n : 1));
-  int64_t mu_star = 1;                                /* :153 */
+  int64_t mu_star = 1 - k->zd; /* :153 (mu* = 1 in the reference's coordinates) */
   int err = 0;
 #pragma omp parallel for reduction(max : mu_star) reduction(| : err) schedule(static)
   for (int64_t i = 0; i < n; ++i) { /* :156-162 */
@@ -447,7 +473,8 @@ int ob_make_stencil_gemv(ob_kernel* k, ob_grid g, const ob_block* x, const ob_bl
   int64_t qa, ea, ma;
   ob_stencil_desc(g, &qa, &ea, &ma);
   int64_t gq = qa + x->q + ceil_log2(ma), ge = ea + x->e;
-  axpby_setup(aq + gq, ae + ge, bq + y->q, be + y->e, &k->p[6], &k->q, &k->e);
+  axpby_setup_z(aq + gq, ae + ge, am == 0 || blk_zero(x), bq + y->q, be + y->e,
+                bm == 0 || blk_zero(y), &k->p[6], &k->q, &k->e, &k->zd);
   k->p[0] = am; k->p[1] = aq; k->p[2] = ae;
   k->p[3] = bm; k->p[4] = bq; k->p[5] = be;
   k->p[7] = gq; k->p[8] = ge;
@@ -476,10 +503,14 @@ int ob_make_jacobi(ob_kernel* k, ob_grid g, const ob_block* x, const ob_block* b
   int64_t qa, ea, ma, d1, qr, er, d2;
   ob_stencil_desc(g, &qa, &ea, &ma);
   int64_t gq = qa + x->q + ceil_log2(ma), ge = ea + x->e;
+  const int zx = blk_zero(x), zb = blk_zero(b);
+  int64_t zr = 0, e_ref = min64(x->e, ce + min64(ge, b->e)); /* the reference chain's e* */
   /* r = egemv(A, x, b, bfp_minus_one, bfp_one): alpha q=1 e=0, beta q=2 e=0 */
-  axpby_setup(1 + gq, ge, 2 + b->q, b->e, &d1, &qr, &er);
+  axpby_setup_z(1 + gq, ge, zx, 2 + b->q, b->e, zb, &d1, &qr, &er, &zr);
   /* z = eaxpby(x, r, bfp_one, c) */
-  axpby_setup(2 + x->q, x->e, cq + qr, ce + er, &d2, &k->q, &k->e);
+  axpby_setup_z(2 + x->q, x->e, zx, cq + qr, ce + er, cm == 0 || (zx && zb), &d2, &k->q, &k->e,
+                &zr);
+  k->zd = k->e - e_ref;
   k->p[0] = cm;
   k->p[1] = d1;
   k->p[2] = d2;
@@ -621,7 +652,8 @@ int ob_make_prolong_correct(ob_kernel* k, ob_grid gf, const ob_block* ec, const 
   if (gf.l < 2 || ec->n != ob_grid_size(gc) || y->n != ob_grid_size(gf)) return OB_ERR_DIM;
   memset(k, 0, sizeof(*k));
   int64_t gq = (gf.d + 2) + ec->q + gf.d, ge = -(int64_t)gf.d + ec->e;
-  axpby_setup(2 + gq, ge, 2 + y->q, y->e, &k->p[6], &k->q, &k->e);
+  axpby_setup_z(2 + gq, ge, blk_zero(ec), 2 + y->q, y->e, blk_zero(y), &k->p[6], &k->q, &k->e,
+                &k->zd);
   k->p[10] = gf.d;
   k->p[11] = ob_grid_n(gf);
   k->p[12] = ob_grid_n(gc);

@@ -61,6 +61,7 @@ typedef struct ob_kernel {
   const void* a; /* kernel specific state */
   int64_t p[24];
   const int64_t* ptr[8];
+  int64_t zd; /* e - e_ref >= 0: rows are the reference rows / 2^zd (axpby_setup_z) */
 } ob_kernel;
 
 typedef struct {

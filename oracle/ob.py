@@ -35,7 +35,8 @@ class Flags(C.Structure):
 
 class Kernel(C.Structure):
     _fields_ = [("q", C.c_int64), ("e", C.c_int64), ("n", C.c_int64), ("row", C.c_void_p),
-                ("a", C.c_void_p), ("p", C.c_int64 * 24), ("ptr", C.c_void_p * 8)]
+                ("a", C.c_void_p), ("p", C.c_int64 * 24), ("ptr", C.c_void_p * 8),
+                ("zd", C.c_int64)]
 
 
 class Csr(C.Structure):

@@ -33,7 +33,7 @@ struct alignas(128) Hdr {
   // qcomp staging, written by pass-1 finalize, read by the recompute pass
   int64_t lam_out;
   int32_t need_recompute;
-  int32_t pad0;
+  int32_t st_zd;  // pass-1 elision shift of the window context (WinCtx::zd), with st_*
   // cross-block accumulators (reset by each finalize)
   unsigned long long acc_or_lo, acc_or_hi;  // OR over rows of z ^ sign(z): bitlen = max msb - 1
   long long acc_max, acc_min;
@@ -431,7 +431,24 @@ struct WinCtx {
   int32_t store_tmp;            // qcomp: tmp fits the storage and is stored
   int32_t skip;                 // recompute pass with nothing to do
   int32_t rs, ls;               // stored value = (z >> rs) << ls  (lam >= 0: rs = lam)
+  int64_t zd;                   // e* - e*_ref >= 0 when the op's template drops an all-zero
+                                // term (op_zd): rows are z_ref / 2^zd, see win_finalize
 };
+
+// Ops whose eaxpby template drops an all-zero term carry `zd` (axpby_setup_z); the
+// window runs in the shifted coordinates, which changes nothing but the all-zero result.
+template <class T, class = void> struct HasZd {
+  static constexpr bool value = false;
+};
+template <class T> struct HasZd<T, decltype((void)T::zd_tag)> {
+  static constexpr bool value = true;
+};
+template <class Op> __device__ __forceinline__ int64_t op_zd(const Op& o) {
+  if constexpr (HasZd<Op>::value)
+    return o.zd;
+  else
+    return 0;
+}
 
 // per-thread running reductions.  mu* = max_i msb(z_i) is recovered exactly
 // from the bitwise OR of z_i ^ sign(z_i): bitlen(a | b) = max(bitlen a, bitlen b).
@@ -586,6 +603,7 @@ __device__ inline void win_setup(const WinParams& p, const Hdr* out_h, int64_t e
                                  int storage_bits, WinCtx& c) {
   c.e_star = e_star;
   c.skip = 0;
+  c.zd = 0;
   if (p.mode == MODE_RECOMPUTE) {
     const volatile Hdr* vh = out_h;  // may have been finalized earlier in this launch
     c.skip = !vh->need_recompute;
@@ -617,7 +635,10 @@ __device__ __forceinline__ M store_shift(A z, const WinCtx& c) {
   constexpr int B = AccBits<A>::value;
   A r = c.rs >= B - 1 ? (z < 0 ? A(-1) : A(0)) : (z >> c.rs);
   if (c.ls == 0) return (M)r;
-  if (c.ls >= 64) return (M)0;
+  // ls >= storage bits only happens when qcomp overflows (lam_tmp >= 1 - w_tmp on the
+  // fast path), so these values are never the result: keep just their zero-ness, which
+  // the all-zero test of win_finalize reads (mx, mn)
+  if (c.ls >= 8 * (int)sizeof(M)) return (M)((r > 0) - (r < 0));
   return (M)((uint64_t)r << c.ls);
 }
 
@@ -639,6 +660,7 @@ __device__ inline void win_partial(const WinParams& p, const WinCtx& c, Hdr* h, 
     h->st_lam = c.lam;
     h->st_gm = c.gm;
     h->st_ge = c.ge;
+    h->st_zd = (int32_t)c.zd;
   }
 }
 
@@ -649,9 +671,18 @@ __device__ inline int win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, 
     win_partial(p, c, h, bits, mx, mn, err);
     return 0;
   }
+  int64_t mu_star = bits;                   // src/blas.cpp:153,158
+  if (p.mode == MODE_QCOMP && c.zd > 0 && bits <= 1) {
+    // mu* starts at 1 in the reference's coordinates, 1 - zd in the op's (an all-zero
+    // result); rows in {0, -1} are told apart by their stored values (store_shift keeps
+    // -1 nonzero)
+    if (!c.store_tmp)
+      err |= ERR_WIDTH;  // nothing stored (w_tmp beyond the storage, forced): fail loudly
+    else if (mn >= 0 && mx <= 0)
+      mu_star = 1 - c.zd;
+  }
   if (err) h->err |= err;
   if (p.mode == MODE_QCOMP) {
-    int64_t mu_star = bits;                 // src/blas.cpp:153,158
     int64_t lam_out = mu_star - p.w_out;    // :164
     int ovf = c.mu_tmp < mu_star;           // :167
     int unf = lam_out < c.lam;              // :168
@@ -713,6 +744,7 @@ __device__ inline void window_reduce(Red& r, Hdr* h, const WinParams& p, const W
       h->st_lam = c.lam;
       h->st_gm = c.gm;
       h->st_ge = c.ge;
+      h->st_zd = (int32_t)c.zd;
     }
   }
 }

@@ -204,6 +204,7 @@ __device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinPar
     o.setup(e_star, nd);
     WinCtx cc;
     win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
+    cc.zd = op_zd(o);
     s_op = o;
     s_c = cc;
     s_need = nd;
@@ -709,6 +710,7 @@ __device__ __noinline__ void fused_run(Op& op, Vec& out, WinParams& p, char* ab,
     op.setup(e_star, nd);
     WinCtx cc;
     win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
+    cc.zd = op_zd(op);
     s_c = cc;
     s_need = nd;
   }

@@ -56,6 +56,8 @@ __global__ void window_finalize_kernel(Vec out, WinParams p, const int64_t* part
   c.lam = p.mode == MODE_RECOMPUTE ? h->lam_out : h->st_lam;
   c.gm = h->st_gm;
   c.ge = h->st_ge;
+  c.zd = h->st_zd;
+  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
   c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
   c.skip = 0;
   p.part = nullptr;
@@ -81,9 +83,11 @@ __global__ void deferred_finalize_kernel(Vec out, WinParams p, int storage_bits)
   c.lam = vh->st_lam;
   c.gm = vh->st_gm;
   c.ge = vh->st_ge;
+  c.zd = vh->st_zd;
   c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
   c.skip = 0;
-  c.rs = c.ls = 0;
+  c.rs = 0;
+  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
   h->acc_or_lo = 0;
   h->acc_or_hi = 0;
   h->acc_max = INT64_MIN;

@@ -36,6 +36,24 @@ __device__ __forceinline__ void axpby_setup(int64_t ea, int64_t eb, int64_t& d, 
   d = ea - eb;
   es = imin(ea, eb);
 }
+// eaxpby setup with all-zero terms dropped: when exactly one term is zero (za / zb), its
+// alignment shift is dropped too (d = 0, e* = the other term's exponent) and zd grows by
+// e* - min(ea, eb).  Every row then equals the reference row / 2^zd exactly (the dropped
+// term contributes nothing), so qcomp/nnqcomp give identical windows in these shifted
+// coordinates (only an all-zero qcomp result needs zd: win_finalize).  Without it a zero
+// block at e = 0 next to a far-away operand (b = 0 with a diverging iterate, C5 p = 4)
+// would push the rows past 127 bits where the reference's mpz rows are just long.
+__device__ __forceinline__ void axpby_setup_z(int64_t ea, int64_t eb, bool za, bool zb,
+                                              int64_t& d, int64_t& es, int64_t& zd) {
+  axpby_setup(ea, eb, d, es);
+  if (za != zb) {
+    const int64_t ee = za ? eb : ea;
+    zd += ee - es;
+    es = ee;
+    d = 0;
+  }
+}
+__device__ __forceinline__ bool hdr_zero(const Hdr* h) { return max_abs(h) == 0; }
 // alpha*a*2^max(d,0) + beta*b*2^max(-d,0)  (src/blas.cpp:60-72, 133-141)
 template <typename A>
 __device__ __forceinline__ A combine(int64_t am, A a, int64_t bm, A b, int64_t d) {
@@ -290,15 +308,18 @@ struct GemvOp {
   int ea, gs;
   int st9;  // 2-D 9-point operator (reference mode, d = 2) instead of the 5-point S_2
   // derived (uniform per launch)
-  int64_t sx, sy, d;
+  int64_t sx, sy, d, zd;
   bool narrow;  // 32-bit stencil and products, 64-bit combine: exact by the width bound
   bool w64;     // 64-bit stencil and products, A-wide shift / sum (int64 storage)
   bool fwi;     // ... and the alignment shift < 64: two-word rows (W128)
   bool swap;
   int P, Q;
+  static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = ea + x.hdr->e;  // e_A + e_x
-    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
+    zd = 0;
+    axpby_setup_z(al.e + ge, be.e + y.hdr->e, al.m == 0 || hdr_zero(x.hdr),
+                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
     int64_t bg = grow(zbits(x.hdr), ceil_log2_h(st9 ? 16 : 4 * dim) + 1 + gs), by = zbits(y.hdr);
@@ -390,11 +411,17 @@ struct JacobiOp {
   bool fwi;   // ... and every alignment shift < 64: two-word rows (W128)
   bool neg1;  // d1 < 0: the b term carries the power of two
   int P1, s2;
+  int64_t zd;
+  static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = 2 * l + x.hdr->e;
-    int64_t er;
-    axpby_setup(ge, b.hdr->e, d1, er);      // r template (alpha q=1 e=0, beta q=2 e=0)
-    axpby_setup(x.hdr->e, c.e + er, d2, e_star);
+    const bool zx = hdr_zero(x.hdr), zb = hdr_zero(b.hdr);
+    // reference template chain (e* only; the rows are those of the chain below * 2^zd)
+    const int64_t es_ref = imin(x.hdr->e, c.e + imin(ge, b.hdr->e));
+    int64_t er, zr = 0;  // zr: unused (zd is taken against the reference chain directly)
+    axpby_setup_z(ge, b.hdr->e, zx, zb, d1, er, zr);  // r template (alpha q=1 e=0, beta q=2 e=0)
+    axpby_setup_z(x.hdr->e, c.e + er, zx, c.m == 0 || (zx && zb), d2, e_star, zr);
+    zd = e_star - es_ref;
     sx = x.hdr->shift;
     sb = b.hdr->shift;
     int64_t bx = zbits(x.hdr);
@@ -502,9 +529,12 @@ struct ScalOp {
 struct AxpbyOp {
   Vec x, y;
   Scal al, be;
-  int64_t sx, sy, d;
+  int64_t sx, sy, d, zd;
+  static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    axpby_setup(al.e + x.hdr->e, be.e + y.hdr->e, d, e_star);
+    zd = 0;
+    axpby_setup_z(al.e + x.hdr->e, be.e + y.hdr->e, al.m == 0 || hdr_zero(x.hdr),
+                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
     need = combine_bits(al.m, zbits(x.hdr), be.m, zbits(y.hdr), d);
@@ -736,9 +766,13 @@ struct ProlongCorrectOp {
     const int X = swap ? yy : g, Y = swap ? g : yy;
     return (int64_t)X * (int64_t)P + (int64_t)Y;
   }
+  int64_t zd;
+  static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = ep + ec.hdr->e;
-    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
+    zd = 0;
+    axpby_setup_z(al.e + ge, be.e + y.hdr->e, al.m == 0 || hdr_zero(ec.hdr),
+                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
     sc = ec.hdr->shift;
     sy = y.hdr->shift;
     int64_t bg = grow(zbits(ec.hdr), dim + 2 + gs), by = zbits(y.hdr);
@@ -810,10 +844,13 @@ struct CsrGemvOp {
   Vec x, y;
   Scal al, be;
   int64_t m_a;
-  int64_t sx, sy, d;
+  int64_t sx, sy, d, zd;
+  static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const int64_t ge = a.e + x.hdr->e;
-    axpby_setup(al.e + ge, be.e + y.hdr->e, d, e_star);
+    zd = 0;
+    axpby_setup_z(al.e + ge, be.e + y.hdr->e, al.m == 0 || hdr_zero(x.hdr),
+                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
     sx = x.hdr->shift;
     sy = y.hdr->shift;
     int64_t bg = grow(zbits(x.hdr), a.q + ceil_log2_h(imax(m_a, 1)) + 1);
