@@ -816,6 +816,9 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
 #ifndef BFP_B3_MINB  // resident CTAs per SM the int32 instantiation is compiled for
 #define BFP_B3_MINB 4
 #endif
+#ifndef BFP_B3_SPLIT
+#define BFP_B3_SPLIT 1  // int64 residual through SplitWin (A/B: -DBFP_B3_SPLIT=0)
+#endif
 constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
 #ifndef BFP_B3_D
 #define BFP_B3_D 3
@@ -875,9 +878,31 @@ template <typename V> __device__ __forceinline__ V shfl_dn1(V v) {
   return __shfl_down_sync(0xffffffffu, v, 1);
 }
 
+// Split window for int64 storage (SP): with z = X 2^ad + Y (|X|, |Y| < 2^62, ad < 64) and
+// the window shift rs < 64, the stored value is exact in 64-bit arithmetic,
+//   t = floor(z / 2^rs) = X 2^(ad-rs) + (Y >> rs)        (ad >= rs)
+//                       = (X + (Y >> ad)) >> (rs - ad)   (ad <  rs)
+// (computed mod 2^64; exact because need - rs <= 63 bounds |t|), and mu* = max msb(z)
+// follows from t: msb(z) = msb(t) + rs unless t is 0 or -1, in which case |z| < 2^rs
+// and z = zl = X 2^ad + Y mod 2^64 exactly.  Each thread ORs t ^ sign and zl ^ sign and
+// folds them into the usual 128-bit OR (a thread with any t outside {0, -1} dominates
+// every row of every thread without one), so the finalize is unchanged.  Replaces the
+// two-word rows of FW for the GemvOp residual: no 128-bit shifts, adds or compares.
+struct SplitWin {
+  uint64_t m0, m1;  // 2^ad, and 2^(ad-rs) or 1
+  int s1, s2;       // rs, 0  or  ad, rs - ad
+};
+template <typename T, typename = void> struct HasSplit {
+  static constexpr bool value = false;
+};
+template <typename T> struct HasSplit<T, decltype((void)T::split_tag)> {
+  static constexpr bool value = true;
+};
+
 // T = storage type, A = accumulator of the exact rows (int64 narrow for int32
 // storage; int64 or __int128 through the ops' generic combine for int64 storage)
-template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, bool FW = false, typename Op>
+template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, bool FW = false,
+          bool SP = false, typename Op>
 __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const WinParams& p,
                                            const WinCtx& c, Red& r, int R, char* smem,
                                            const CUtensorMap* tmx, const CUtensorMap* tmy) {
@@ -899,6 +924,16 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
   const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * sizeof(T);
+  SplitWin sw{};
+  uint64_t ot = 0, oz = 0;  // SP: OR of t ^ sign, zl ^ sign
+  if constexpr (SP) {
+    const int ad = (int)(op.d < 0 ? -op.d : op.d), rs = c.rs;
+    sw.m0 = 1ull << ad;
+    if (ad >= rs)
+      sw.m1 = 1ull << (ad - rs), sw.s1 = rs, sw.s2 = 0;
+    else
+      sw.m1 = 1, sw.s1 = ad, sw.s2 = rs - ad;
+  }
   uint32_t parity = 0, eparity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
@@ -973,9 +1008,24 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const V left = Lf[q], right = Rt[q];
+        if constexpr (sizeof(T) == 8 && SP) {  // split window (SplitWin)
+          const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
+          int64_t tq, zl;
+          op.template point_sp<SWAP>(6 * C[q] - nb, Yv[q], sw.m0, sw.m1, sw.s1, sw.s2, tq, zl);
+          if ((q == 3 && xpad) || rowpad) tq = zl = 0;
+          if (MODE == MODE_QCOMP) {
+            const uint64_t sg = (uint64_t)(tq >> 63);
+            ot |= (uint64_t)tq ^ sg;
+            oz |= (uint64_t)zl ^ sg;
+          }
+          tt[q] = (T)tq;
+          mx = (V)tt[q] > mx ? (V)tt[q] : mx;
+          mn = (V)tt[q] < mn ? (V)tt[q] : mn;
+          continue;
+        }
         if constexpr (sizeof(T) == 8 && FW) {  // two-word rows, window rs < 64
           const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
-          W128 w = op.point_fw(6 * C[q] - nb, C[q], Yv[q]);
+          W128 w = op.template point_fw<SWAP>(6 * C[q] - nb, C[q], Yv[q]);
           if ((q == 3 && xpad) || rowpad) w = W128{0, 0};
           if (MODE == MODE_QCOMP) w_or_mag(w, olo, ohi);
           tt[q] = (T)w_shr_lo(w, c.rs);
@@ -1032,10 +1082,34 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
     }
     __syncthreads();
   }
+  if constexpr (SP && MODE == MODE_QCOMP) {  // fold: msb(z) = msb(t) + rs, else zl
+    const int rs = c.rs;
+    if (ot) {
+      olo |= ot << rs;
+      ohi |= rs ? ot >> (64 - rs) : 0;
+    } else {
+      olo |= oz;
+    }
+  }
   r.olo |= olo;
   r.ohi |= ohi;
   r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
+// the four (SHIFT, SWAP) instantiations of one bulk3_loop flavour, chosen per launch
+template <int MODE, typename T, typename A, bool FW, bool SP, typename Op>
+__device__ __forceinline__ void b3_dispatch(bool sh, bool sw, const Op& op, const Vec& out,
+                                            const WinParams& p, const WinCtx& c, Red& r, int R,
+                                            char* smem, const B3Maps& tm) {
+  if (sh && sw)
+    bulk3_loop<MODE, true, true, T, A, FW, SP>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+  else if (sh)
+    bulk3_loop<MODE, true, false, T, A, FW, SP>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+  else if (sw)
+    bulk3_loop<MODE, false, true, T, A, FW, SP>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+  else
+    bulk3_loop<MODE, false, false, T, A, FW, SP>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
 }
 
 template <int MODE, typename T, typename Op>
@@ -1091,10 +1165,14 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
         else
           bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else if (MODE != MODE_NNQ && op.fwi && c.store_tmp && c.ls == 0 && c.rs < 64) {
-        if (sh)
-          bulk3_loop<MODE, true, false, T, i128, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
-        else
-          bulk3_loop<MODE, false, false, T, i128, true>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
+        bool split = false;
+        if constexpr (HasSplit<Op>::value) {
+          split = BFP_B3_SPLIT && need - c.rs <= 63;
+          if (split)
+            b3_dispatch<MODE, T, int64_t, false, true>(sh, op.fw_swap(), op, out, p, c, r, R, smem, tm);
+        }
+        if (!split)
+          b3_dispatch<MODE, T, i128, true, false>(sh, op.fw_swap(), op, out, p, c, r, R, smem, tm);
       } else {
         if (sh)
           bulk3_loop<MODE, true, false, T, i128>(op, out, p, c, r, R, smem, &tm.x, &tm.y);

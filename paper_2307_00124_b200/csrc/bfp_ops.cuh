@@ -79,6 +79,9 @@ __device__ __forceinline__ A combine_w(int64_t am, int64_t a, int64_t bm, int64_
     ta = ta << (int)imin(d, B);
   return ta + tb;
 }
+#ifndef BFP_W128_PTX
+#define BFP_W128_PTX 1
+#endif
 // Two-word rows for the int64-storage fast window (all shift counts < 64, uniform per
 // launch): value = hi * 2^64 + lo, two's complement over 128 bits.
 struct W128 {
@@ -88,16 +91,29 @@ struct W128 {
 __device__ __forceinline__ W128 w_shl(int64_t a, int s) {  // a * 2^s, 0 <= s < 64
   return W128{(uint64_t)a << s, s ? (a >> (64 - s)) : (a >> 63)};
 }
-__device__ __forceinline__ W128 w_add(W128 x, int64_t b) {
-  const uint64_t lo = x.lo + (uint64_t)b;
-  return W128{lo, x.hi + (b >> 63) + (int64_t)(lo < x.lo)};
-}
+// two-word adds through the carry chain (add.cc / addc: four IADD3s, no compare/select)
 __device__ __forceinline__ W128 w_add(W128 x, W128 y) {
+#if BFP_W128_PTX
+  W128 r;
+  asm("add.cc.u64 %0, %2, %4;\n\taddc.u64 %1, %3, %5;"
+      : "=l"(r.lo), "=l"(r.hi)
+      : "l"(x.lo), "l"(x.hi), "l"(y.lo), "l"(y.hi));
+  return r;
+#else
   const uint64_t lo = x.lo + y.lo;
   return W128{lo, x.hi + y.hi + (int64_t)(lo < x.lo)};
+#endif
+}
+__device__ __forceinline__ W128 w_add(W128 x, int64_t b) {
+  return w_add(x, W128{(uint64_t)b, b >> 63});
 }
 __device__ __forceinline__ W128 w_mul_u32(W128 x, uint32_t c) {  // x * c mod 2^128
-  return W128{x.lo * c, (int64_t)((uint64_t)x.hi * c + __umul64hi(x.lo, c))};
+  // 32-bit limbs: four IMAD.WIDE.U32 / IMAD, each limb product absorbing the carry word
+  const uint64_t p0 = (uint64_t)(uint32_t)x.lo * c;
+  const uint64_t p1 = (uint64_t)(uint32_t)(x.lo >> 32) * c + (p0 >> 32);
+  const uint64_t p2 = (uint64_t)(uint32_t)x.hi * c + (p1 >> 32);
+  const uint32_t p3 = (uint32_t)((uint64_t)x.hi >> 32) * c + (uint32_t)(p2 >> 32);
+  return W128{(p1 << 32) | (uint32_t)p0, (int64_t)(((uint64_t)p3 << 32) | (uint32_t)p2)};
 }
 __device__ __forceinline__ int64_t w_shr_lo(W128 z, int rs) {  // low word of floor(z/2^rs)
   return (int64_t)(rs ? (z.lo >> rs) | ((uint64_t)z.hi << (64 - rs)) : z.lo);
@@ -360,10 +376,26 @@ struct GemvOp {
     (void)c;
     return combine_w<A>(al.m, g, be.m, yv, d);
   }
+  // two-word rows; SW = (d < 0) is uniform per launch (fw_swap) and templated
+  __device__ __forceinline__ bool fw_swap() const { return d < 0; }
+  template <bool SW>
   __device__ __forceinline__ W128 point_fw(int64_t g, int64_t c, int64_t yv) const {
     (void)c;
     const int64_t a = al.m * g, b = be.m * yv;
-    return d >= 0 ? w_add(w_shl(a, (int)d), b) : w_add(w_shl(b, (int)-d), a);
+    return SW ? w_add(w_shl(b, (int)-d), a) : w_add(w_shl(a, (int)d), b);
+  }
+  // split window (int64 storage, qcomp pass 1 / recompute): the stored value
+  // t = floor(z / 2^rs) and the low word zl = z mod 2^64 in 64-bit arithmetic only
+  // (SplitWin, bfp_kernels.cuh); z = X 2^|d| + Y with (X, Y) = (alpha g, beta y) or,
+  // SW (d < 0), (beta y, alpha g)
+  static constexpr int split_tag = 0;
+  template <bool SW>
+  __device__ __forceinline__ void point_sp(int64_t g, int64_t yv, uint64_t m0, uint64_t m1,
+                                           int s1, int s2, int64_t& t, int64_t& zl) const {
+    const int64_t a = al.m * g, b = be.m * yv;  // exact: w64 bounds |a|, |b| < 2^62
+    const int64_t X = SW ? b : a, Y = SW ? a : b;
+    zl = (int64_t)((uint64_t)X * m0 + (uint64_t)Y);
+    t = (int64_t)((uint64_t)X * m1 + (uint64_t)(Y >> s1)) >> s2;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -466,8 +498,10 @@ struct JacobiOp {
   template <typename A> __device__ __forceinline__ A point_w(int64_t g, int64_t cx, int64_t bv) const {
     return combine<A>(1, (A)cx, c.m, combine_w<A>(-1, g, 1, bv, d1), d2);
   }
+  __device__ __forceinline__ bool fw_swap() const { return d1 < 0; }
+  template <bool SW>
   __device__ __forceinline__ W128 point_fw(int64_t g, int64_t cx, int64_t bv) const {
-    const W128 r = d1 >= 0 ? w_add(w_shl(-g, (int)d1), bv) : w_add(w_shl(bv, (int)-d1), -g);
+    const W128 r = SW ? w_add(w_shl(bv, (int)-d1), -g) : w_add(w_shl(-g, (int)d1), bv);
     return w_add(w_shl(cx, (int)d2), w_mul_u32(r, (uint32_t)c.m));
   }
   template <typename M, typename A, bool NC = true>

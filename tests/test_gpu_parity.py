@@ -396,3 +396,25 @@ def test_stencil_paths_agree_with_oracle(B, d, l, mb, p):
                 assert e == wj.e and np.array_equal(m, wj.m), (bulk, "jacobi", g, nn)
     finally:
         B.set_kernel_path(True)
+
+
+@pytest.mark.parametrize("p", [40, 48, 52])
+def test_int64_residual_windows_vs_oracle(B, p):
+    """3-D int64 residuals through the bulk pipeline over the window regimes of the
+    split-window path (SplitWin, bfp_kernels.cuh): alignment d of both signs (X/Y swap),
+    window shift rs above and below |d|, rows all in {0, -1} (mu* from the low words),
+    rs >= 64 / left-shift windows (the two-word fallback), overflow and underflow."""
+    d, l = 3, 7
+    ox, obb = ob.gen_uniform(d, l, p, 5, 1), ob.gen_sine(d, l, p)
+    gx = ggrid(B, d, l, ox.m, ox.q, ox.e, mb=8)
+    for off in (-40, -12, 0, 9, 30):
+        bo = ob.OBlock(obb.m, obb.q, obb.e + off)
+        gb = ggrid(B, d, l, bo.m, bo.q, bo.e, mb=8)
+        for ge in range(-70, 80, 9):
+            g = B.Scalar(1 << 14, 16, ge)
+            res = B.residual(gx, gb, p, p + 5, g)
+            want, fl = ob.stencil_gemv(d, l, ox, bo, (-1, 1, 0), (1, 2, 0), "q", p, p + 5,
+                                       g.m, g.e)
+            m, q, e = res.z.download()
+            assert e == want.e and np.array_equal(m, want.m), (off, ge)
+            assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1])), (off, ge)
