@@ -533,6 +533,9 @@ def run_ours(args, world, rank, local):
         line["residual_other_configs"] = {
             "C4_3d_511^3_int32_p24": measure_residual(B, torch, stream, 3, 9, 24, 4),
             "C1_1d_2^20_int32_p16": measure_residual(B, torch, stream, 1, 20, 16, 4, steps=200),
+            # config 1 is L2-resident; the %HBM claim for 1-D needs n beyond L2
+            "C1_1d_2^28_int32_p16_probe": measure_residual(B, torch, stream, 1, 28, 16, 4,
+                                                           steps=10),
             "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=5),
         }
         line["fine_level_ops"] = {"C2": measure_ops(B, torch, stream, 2, 12, 20),
@@ -629,7 +632,9 @@ def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
     sp = C.c_void_p(stream.cuda_stream)
     Lb = B.lib()
     x = B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 1, 1)
-    b_ = B.gen_sine(B.BfpVec.grid(d, l, mb), p)
+    # config 1's right-hand side is uniform (stream 2); the others are the sine rhs
+    b_ = (B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 1, 2) if d == 1 else
+          B.gen_sine(B.BfpVec.grid(d, l, mb), p))
     r = B.BfpVec.grid(d, l, mb)
     B.residual(x, b_, p, p + 5, B.Scalar(1 << 14, 16, 2 * l + 8), out=r)
     g = B.inf_norm_upper(r).c()

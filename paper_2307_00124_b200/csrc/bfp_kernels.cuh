@@ -33,6 +33,15 @@ inline int defer_ok(const bfpdev::WinParams& p, int blocks) {
 
 constexpr int kThreads = 256;
 constexpr int kMaxBlocks = 148 * 8;
+#ifndef BFP_B2_EARLY  // 2-D bulk pipeline: first item's loads issued before the op setup (A/B)
+#define BFP_B2_EARLY 1
+#endif
+#ifndef BFP_SETUP_PREFETCH  // warp-parallel header prefetch before the one-thread setup (A/B)
+#define BFP_SETUP_PREFETCH 1
+#endif
+#ifndef BFP_GRID_SPLIT  // int32-storage split window in the grid kernel (A/B switch)
+#define BFP_GRID_SPLIT 1
+#endif
 #ifndef BFP_GRID_UNROLL  // groups per grid-loop iteration (A/B switch)
 #define BFP_GRID_UNROLL 1
 #endif
@@ -116,6 +125,48 @@ template <> struct Lim<int64_t> {
 //   RECOMPUTE  store floor(z/2^lam_out)
 //   NNQ        store clamp(floor(z/2^lam_out))
 // Max/min of the STORED values are tracked in the storage type.
+// SP (int32 storage, GemvOp::eval4_sp): the split window of bulk3_loop -- the stored value
+// t = floor(z / 2^rs) and the low word zl in 64-bit arithmetic, mu* from t (+ rs) or zl.
+template <int MODE, typename M, typename Op>
+__device__ __forceinline__ void grid_loop_sp(Op& op, const Vec& out, const WinCtx& c, Red& r) {
+  const int64_t ngroups = out.n >> 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const SplitWin sw = split_win(op.d, c.rs);
+  M mx = Lim<M>::lo, mn = Lim<M>::hi;
+  uint64_t ot = 0, oz = 0;
+  auto epi = [&](int64_t g, const int64_t t[4], const int64_t zl[4]) {
+    M tt[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (MODE == MODE_QCOMP) {
+        const uint64_t sg = (uint64_t)(t[j] >> 63);
+        ot |= (uint64_t)t[j] ^ sg;
+        oz |= (uint64_t)zl[j] ^ sg;
+      }
+      tt[j] = (M)t[j];
+      mx = tt[j] > mx ? tt[j] : mx;
+      mn = tt[j] < mn ? tt[j] : mn;
+    }
+    V4<M>::store(out, g * 4, tt);
+  };
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+    int64_t t[4], zl[4];
+    op.template eval4_sp<true>(g * 4, sw, t, zl);
+    epi(g, t, zl);
+  }
+  if (MODE == MODE_QCOMP) {
+    const int rs = c.rs;
+    if (ot) {
+      r.olo |= ot << rs;
+      r.ohi |= rs ? ot >> (64 - rs) : 0;
+    } else {
+      r.olo |= oz;
+    }
+  }
+  r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
+  r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
+}
+
 template <int MODE, typename M, typename Op, typename A, bool NC = true>
 __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r) {
@@ -168,9 +219,19 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
-template <int MODE, typename M, typename Op, bool NC = true>
+// SPLIT: the grid kernel's own body may take the split window; the pipelines' exact
+// fallbacks do not (it would only add registers to their hot loops)
+template <int MODE, typename M, typename Op, bool NC = true, bool SPLIT = false>
 __device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r, int64_t need) {
+  if constexpr (SPLIT && HasSplit<Op>::value && sizeof(M) == 4 && NC && MODE != MODE_NNQ) {
+    // int32 storage beyond the narrow path (1-D fine levels: A x sits 2l bits above b)
+    if (BFP_GRID_SPLIT && !op.narrow && need <= 127 && op.sp32 && c.store_tmp && c.ls == 0 &&
+        c.rs < 64 && need - c.rs <= 63) {
+      grid_loop_sp<MODE, M, Op>(op, out, c, r);
+      return;
+    }
+  }
   if (need > 127)
     r.err = ERR_WIDTH;
   else if (need <= 63)
@@ -183,6 +244,37 @@ __device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParam
 // nnqcomp, or the qcomp recompute pass, selected by p.mode.
 // The op setup and the gamma rule are uniform per launch: one thread evaluates
 // them from the device headers and broadcasts through shared memory.
+// The block headers an op's setup reads (published state: the first 64 bytes of each).
+__device__ __forceinline__ int op_hdrs(const GemvOp& o, const Hdr** h) { h[0] = o.x.hdr, h[1] = o.y.hdr; return 2; }
+__device__ __forceinline__ int op_hdrs(const JacobiOp& o, const Hdr** h) { h[0] = o.x.hdr, h[1] = o.b.hdr; return 2; }
+__device__ __forceinline__ int op_hdrs(const AxpbyOp& o, const Hdr** h) { h[0] = o.x.hdr, h[1] = o.y.hdr; return 2; }
+__device__ __forceinline__ int op_hdrs(const ProlongCorrectOp& o, const Hdr** h) { h[0] = o.ec.hdr, h[1] = o.y.hdr; return 2; }
+__device__ __forceinline__ int op_hdrs(const CsrGemvOp& o, const Hdr** h) { h[0] = o.x.hdr, h[1] = o.y.hdr; return 2; }
+__device__ __forceinline__ int op_hdrs(const ScalOp& o, const Hdr** h) { h[0] = o.r.hdr; return 1; }
+__device__ __forceinline__ int op_hdrs(const RestrictOp& o, const Hdr** h) { h[0] = o.r.hdr; return 1; }
+__device__ __forceinline__ int op_hdrs(const ProlongOp& o, const Hdr** h) { h[0] = o.xc.hdr; return 1; }
+__device__ __forceinline__ int op_hdrs(const CsrSpmvOp& o, const Hdr** h) { h[0] = o.x.hdr; return 1; }
+template <typename Op> __device__ __forceinline__ int op_hdrs(const Op&, const Hdr**) { return 0; }
+
+// Warp 0 pulls the headers the one-thread setup will read (the op's operands and the
+// gamma rule's norm terms) into L1 with one parallel round trip; thread 0's setup then
+// runs on L1 hits instead of a chain of dependent L2 reads.
+template <typename Op>
+__device__ __forceinline__ void prefetch_setup_hdrs(const Op& op, const WinParams& p) {
+  const int lane = threadIdx.x & 31;
+  const Hdr* h[8];
+  int n = op_hdrs(op, h);
+  if (!p.gamma.literal)
+    for (int i = 0; i < p.gamma.nterms && i < 3; ++i)
+      if (p.gamma.t[i].v) h[n++] = p.gamma.t[i].v;
+  if (lane < 2 * n) {  // sectors 0 and 1 (q, e, shift, max_m, min_m, ...) of header lane/2
+    const int64_t* a = (const int64_t*)h[lane >> 1] + (lane & 1) * 4;
+    int64_t v;
+    asm volatile("ld.global.ca.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    (void)v;
+  }
+}
+
 template <typename Op, typename M>
 __device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinParams& p, WinCtx& c,
                                             int64_t& need) {
@@ -198,6 +290,9 @@ __device__ __forceinline__ void block_setup(Op& op, const Vec& out, const WinPar
       return;
     }
   }
+#if BFP_SETUP_PREFETCH
+  if (threadIdx.x < 32) prefetch_setup_hdrs(op, p);
+#endif
   if (threadIdx.x == 0) {
     int64_t e_star = 0, nd = 0;
     Op o = op;
@@ -227,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   if (c.skip) return;
   Red r;
   r.init();
-  grid_body<MODE, M>(op, out, p, c, r, need);
+  grid_body<MODE, M, Op, true, true>(op, out, p, c, r, need);
   BFP_STAMP(3);
   if (MODE != MODE_QCOMP || gridDim.x != 1 || p.part) griddep_launch_dependents();
   __shared__ int s_rc;  // single block: thread 0's finalize verdict (need_recompute)
@@ -444,7 +539,45 @@ __global__ void __launch_bounds__(kThreads, DIM == 2 ? 3 : 2) march_win_kernel(O
 // FW: the fast window of the common case -- pass 1 / recompute storing
 // floor(z / 2^rs) with 0 <= rs < 32 and no left shift: the stored int32 is the low word
 // of the shifted 64-bit row, one funnel shift (no range selects)
-template <int MODE, bool SHIFT, bool SWAP, bool FW, typename Op>
+// Prologue of one item of the 2-D bulk pipeline (thread 0): x rows j0-1, j0 with group j0
+// (x row j0+1, y row j0) on bar[j0 % YS]; then groups j0+1 .. j0+D.  Needs only the
+// operands' addresses, so the kernel can issue the first item's before the op setup.
+template <typename Op>
+__device__ __forceinline__ int bulk_prologue(const Op& op, const Vec& out, int R, char* smem,
+                                             int item) {
+  const int64_t N = (int64_t)1 << out.l;
+  const int strips = (int)(N / kBulkW);
+  const int64_t NZ = out.nz;
+  int32_t* xsl = reinterpret_cast<int32_t*>(smem);
+  int32_t* ysl = xsl + kBulkXS * kBulkXW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kBulkYS * kBulkW);
+  const int32_t* X = (const int32_t*)op.sv().data;
+  const int32_t* Y = (const int32_t*)op.yv2().data;
+  const int strip = item % strips, ch = item / strips;
+  const int64_t c0 = (int64_t)strip * kBulkW;
+  const int j0 = ch * R;
+  const int rows = (int)std::min<int64_t>(R, NZ - j0);
+  auto xsrc = [&](int64_t row) { return X + (row > NZ ? NZ : row) * N + c0 - 4; };
+  auto ysrc = [&](int64_t row) { return Y + (row > NZ ? NZ : row) * N + c0; };
+  const uint32_t tx_bytes = (uint32_t)(kBulkXW + kBulkW) * 4;
+  fence_proxy_async_smem();  // previous item's generic reads of the slots
+  int g = 0;
+  for (; g <= kBulkD && g < rows; ++g) {
+    const int64_t tr = j0 + g;
+    uint64_t* b = &bar[tr % kBulkYS];
+    const uint32_t extra = g == 0 ? 2u * kBulkXW * 4 : 0u;
+    mbar_expect_tx(b, tx_bytes + extra);
+    if (g == 0) {
+      bulk_g2s(xsl + ((tr - 1 + kBulkXS) % kBulkXS) * kBulkXW, xsrc(tr - 1), kBulkXW * 4, b);
+      bulk_g2s(xsl + (tr % kBulkXS) * kBulkXW, xsrc(tr), kBulkXW * 4, b);
+    }
+    bulk_g2s(xsl + ((tr + 1) % kBulkXS) * kBulkXW, xsrc(tr + 1), kBulkXW * 4, b);
+    bulk_g2s(ysl + (tr % kBulkYS) * kBulkW, ysrc(tr), kBulkW * 4, b);
+  }
+  return g;  // groups issued (one barrier phase each, on bar[(j0 + k) % YS])
+}
+
+template <int MODE, bool SHIFT, bool SWAP, bool FW, bool EARLY, typename Op>
 __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r, int R, char* smem) {
   const int l = out.l;
@@ -475,23 +608,8 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
     // source row clamp: rows past the slab read its back halo row (zeros or exchanged)
     auto xsrc = [&](int64_t row) { return X + (row > NZ ? NZ : row) * N + c0 - 4; };
     auto ysrc = [&](int64_t row) { return Y + (row > NZ ? NZ : row) * N + c0; };
-    if (t == 0) {
-      fence_proxy_async_smem();  // previous item's generic reads of the slots
-      // prologue: x rows j0-1, j0 with group j0 (x row j0+1, y row j0) on bar[j0 % YS];
-      // then groups j0+1 .. j0+D
-      for (int g = 0; g <= kBulkD && g < rows; ++g) {
-        const int64_t tr = j0 + g;
-        uint64_t* b = &bar[tr % kBulkYS];
-        const uint32_t extra = g == 0 ? 2u * kBulkXW * 4 : 0u;
-        mbar_expect_tx(b, tx_bytes + extra);
-        if (g == 0) {
-          bulk_g2s(xsl + ((tr - 1 + kBulkXS) % kBulkXS) * kBulkXW, xsrc(tr - 1), kBulkXW * 4, b);
-          bulk_g2s(xsl + (tr % kBulkXS) * kBulkXW, xsrc(tr), kBulkXW * 4, b);
-        }
-        bulk_g2s(xsl + ((tr + 1) % kBulkXS) * kBulkXW, xsrc(tr + 1), kBulkXW * 4, b);
-        bulk_g2s(ysl + (tr % kBulkYS) * kBulkW, ysrc(tr), kBulkW * 4, b);
-      }
-    }
+    // the first item's prologue may have been issued before the op setup (EARLY)
+    if (t == 0 && !(EARLY && item == (int)blockIdx.x)) bulk_prologue(op, out, R, smem, item);
     const bool xpad = c0 + 4 * t + 3 == N - 1;
     const int lane = t & 31;
     // running ring indices (no 64-bit modulo in the step loop)
@@ -578,15 +696,29 @@ template <int MODE, typename Op>
 __global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
   griddep_wait();
   extern __shared__ __align__(128) char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4);
+  // Early prologue: the first item's loads go out before the (one-thread, ~1.7 us) op
+  // setup, which they then overlap; if the setup rules the pipeline out they are drained.
+  constexpr bool EARLY = BFP_B2_EARLY && MODE != MODE_RECOMPUTE;
+  const int64_t N = (int64_t)1 << out.l;
+  const int items = (int)(N / kBulkW) * (int)((out.nz + R - 1) / R);
+  int early_groups = 0;
+  if (EARLY && threadIdx.x == 0) {
+    for (int k = 0; k < kBulkYS; ++k) {
+      mbar_init(&bar[k], 1);
+      mbar_init(&bar[kBulkYS + k], kBulkT / 32);
+    }
+    mbar_fence_init();
+    if ((int)blockIdx.x < items) early_groups = bulk_prologue(op, out, R, smem, blockIdx.x);
+  }
   int64_t need = 0;
   WinCtx c;
   block_setup<Op, int32_t>(op, out, p, c, need);
-  if (c.skip) return;
+  if (c.skip) return;  // (RECOMPUTE only: no early prologue)
   Red r;
   r.init();
   if (op.narrow && need <= 63) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4);
-    if (threadIdx.x == 0) {
+    if (!EARLY && threadIdx.x == 0) {
       for (int k = 0; k < kBulkYS; ++k) {
         mbar_init(&bar[k], 1);
         mbar_init(&bar[kBulkYS + k], kBulkT / 32);
@@ -598,23 +730,27 @@ __global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Ve
     const bool fw = MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32;
     if (fw) {
       if (!sh && !sw)
-        bulk_loop<MODE, false, false, true>(op, out, p, c, r, R, smem);
+        bulk_loop<MODE, false, false, true, EARLY>(op, out, p, c, r, R, smem);
       else if (sh && !sw)
-        bulk_loop<MODE, true, false, true>(op, out, p, c, r, R, smem);
+        bulk_loop<MODE, true, false, true, EARLY>(op, out, p, c, r, R, smem);
       else if (!sh)
-        bulk_loop<MODE, false, true, true>(op, out, p, c, r, R, smem);
+        bulk_loop<MODE, false, true, true, EARLY>(op, out, p, c, r, R, smem);
       else
-        bulk_loop<MODE, true, true, true>(op, out, p, c, r, R, smem);
+        bulk_loop<MODE, true, true, true, EARLY>(op, out, p, c, r, R, smem);
     } else if (!sh && !sw) {
-      bulk_loop<MODE, false, false, false>(op, out, p, c, r, R, smem);
+      bulk_loop<MODE, false, false, false, EARLY>(op, out, p, c, r, R, smem);
     } else if (sh && !sw) {
-      bulk_loop<MODE, true, false, false>(op, out, p, c, r, R, smem);
+      bulk_loop<MODE, true, false, false, EARLY>(op, out, p, c, r, R, smem);
     } else if (!sh) {
-      bulk_loop<MODE, false, true, false>(op, out, p, c, r, R, smem);
+      bulk_loop<MODE, false, true, false, EARLY>(op, out, p, c, r, R, smem);
     } else {
-      bulk_loop<MODE, true, true, false>(op, out, p, c, r, R, smem);
+      bulk_loop<MODE, true, true, false, EARLY>(op, out, p, c, r, R, smem);
     }
   } else {
+    if (EARLY && threadIdx.x == 0) {  // drain the early prologue before leaving the smem
+      const int j0 = ((int)blockIdx.x / (int)(N / kBulkW)) * R;
+      for (int g = 0; g < early_groups; ++g) mbar_wait(&bar[(j0 + g) % kBulkYS], 0u);
+    }
     grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic fallback
   }
   griddep_launch_dependents();
@@ -888,17 +1024,6 @@ template <typename V> __device__ __forceinline__ V shfl_dn1(V v) {
 // folds them into the usual 128-bit OR (a thread with any t outside {0, -1} dominates
 // every row of every thread without one), so the finalize is unchanged.  Replaces the
 // two-word rows of FW for the GemvOp residual: no 128-bit shifts, adds or compares.
-struct SplitWin {
-  uint64_t m0, m1;  // 2^ad, and 2^(ad-rs) or 1
-  int s1, s2;       // rs, 0  or  ad, rs - ad
-};
-template <typename T, typename = void> struct HasSplit {
-  static constexpr bool value = false;
-};
-template <typename T> struct HasSplit<T, decltype((void)T::split_tag)> {
-  static constexpr bool value = true;
-};
-
 // T = storage type, A = accumulator of the exact rows (int64 narrow for int32
 // storage; int64 or __int128 through the ops' generic combine for int64 storage)
 template <int MODE, bool SHIFT, bool SWAP, typename T, typename A, bool FW = false,
@@ -926,14 +1051,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * sizeof(T);
   SplitWin sw{};
   uint64_t ot = 0, oz = 0;  // SP: OR of t ^ sign, zl ^ sign
-  if constexpr (SP) {
-    const int ad = (int)(op.d < 0 ? -op.d : op.d), rs = c.rs;
-    sw.m0 = 1ull << ad;
-    if (ad >= rs)
-      sw.m1 = 1ull << (ad - rs), sw.s1 = rs, sw.s2 = 0;
-    else
-      sw.m1 = 1, sw.s1 = ad, sw.s2 = rs - ad;
-  }
+  if constexpr (SP) sw = split_win(op.d, c.rs);
   uint32_t parity = 0, eparity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);

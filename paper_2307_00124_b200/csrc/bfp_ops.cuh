@@ -46,14 +46,27 @@ __device__ __forceinline__ void axpby_setup(int64_t ea, int64_t eb, int64_t& d, 
 __device__ __forceinline__ void axpby_setup_z(int64_t ea, int64_t eb, bool za, bool zb,
                                               int64_t& d, int64_t& es, int64_t& zd) {
   axpby_setup(ea, eb, d, es);
+#ifndef BFP_AB_NO_ELIDE
   if (za != zb) {
     const int64_t ee = za ? eb : ea;
     zd += ee - es;
     es = ee;
     d = 0;
   }
+#endif
 }
 __device__ __forceinline__ bool hdr_zero(const Hdr* h) { return max_abs(h) == 0; }
+// One read of a block's published state for the one-thread op setups: every derived
+// quantity below comes from these four words (no re-reads between the setup's stores).
+struct HSnap {
+  int64_t e, shift, bits;  // bits = zbits (0: the block is all zero)
+};
+__device__ __forceinline__ HSnap hsnap(const Hdr* h) {
+  const int64_t e = h->e, s = h->shift, mx = h->max_m, mn = h->min_m;
+  const int64_t a = mx >> s, b = mn >> s;
+  const int ma = msb(a), mb = msb(b);
+  return HSnap{e, s, (a | b) ? (ma > mb ? ma : mb) : 0};
+}
 // alpha*a*2^max(d,0) + beta*b*2^max(-d,0)  (src/blas.cpp:60-72, 133-141)
 template <typename A>
 __device__ __forceinline__ A combine(int64_t am, A a, int64_t bm, A b, int64_t d) {
@@ -311,6 +324,33 @@ __device__ __forceinline__ void stencil9_4(const Vec& x, int64_t sx, int l, int6
   for (int j = 0; j < 4; ++j) g[j] = (A)8 * (A)c[j] - nb[j];
 }
 
+// split-window parameters (see bulk3_loop / grid_loop in bfp_kernels.cuh)
+struct SplitWin {
+  uint64_t m0, m1;  // 2^ad, and 2^(ad-rs) or 1
+  int s1, s2;       // rs, 0  or  ad, rs - ad
+  int a0, a1;       // the multipliers' exponents: ad, and ad - rs or 0
+};
+template <typename T, typename = void> struct HasSplit {
+  static constexpr bool value = false;
+};
+template <typename T> struct HasSplit<T, decltype((void)T::split_tag)> {
+  static constexpr bool value = true;
+};
+
+
+__device__ __forceinline__ SplitWin split_win(int64_t d, int rs) {
+  const int ad = (int)(d < 0 ? -d : d);
+  SplitWin sw;
+  sw.m0 = 1ull << ad;
+  sw.a0 = ad;
+  if (ad >= rs)
+    sw.a1 = ad - rs, sw.s1 = rs, sw.s2 = 0;
+  else
+    sw.a1 = 0, sw.s1 = ad, sw.s2 = rs - ad;
+  sw.m1 = 1ull << sw.a1;
+  return sw;
+}
+
 // ---------------------------------------------------------------------------
 // z = alpha*(A_l x) + beta*y  (EgemvKernel with A = 2^{2l} S_d)
 
@@ -329,31 +369,50 @@ struct GemvOp {
   bool w64;     // 64-bit stencil and products, A-wide shift / sum (int64 storage)
   bool fwi;     // ... and the alignment shift < 64: two-word rows (W128)
   bool swap;
-  int P, Q;
+  bool sp32;  // 32-bit operand products, alignment < 64: split window (eval4_sp)
+  int P, Q, PX, QY;
   static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t ge = ea + x.hdr->e;  // e_A + e_x
-    zd = 0;
-    axpby_setup_z(al.e + ge, be.e + y.hdr->e, al.m == 0 || hdr_zero(x.hdr),
-                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
-    sx = x.hdr->shift;
-    sy = y.hdr->shift;
-    int64_t bg = grow(zbits(x.hdr), ceil_log2_h(st9 ? 16 : 4 * dim) + 1 + gs), by = zbits(y.hdr);
-    need = combine_bits(al.m, bg, be.m, by, d);
+    const HSnap hx = hsnap(x.hdr), hy = hsnap(y.hdr);
+    const int64_t ge = ea + hx.e;  // e_A + e_x
+    int64_t dd, es, z = 0;
+    axpby_setup_z(al.e + ge, be.e + hy.e, al.m == 0 || hx.bits == 0, be.m == 0 || hy.bits == 0,
+                  dd, es, z);
+    e_star = es;
+    const int64_t ssx = hx.shift, ssy = hy.shift;
+    const int64_t bg = grow(hx.bits, ceil_log2_h(st9 ? 16 : 4 * dim) + 1 + gs), by = hy.bits;
+    const int64_t nd = combine_bits(al.m, bg, be.m, by, dd);
+    need = nd;
     // z = X * P + Q * Y with (X, Y) = (g, y), P = alpha 2^d, Q = beta   when d >= 0
     //                         (X, Y) = (y, g), P = beta 2^-d, Q = alpha  when d < 0
-    const int64_t ad = d >= 0 ? d : -d;
-    const int64_t pm = d >= 0 ? al.m : be.m, qm = d >= 0 ? be.m : al.m;
-    const int64_t bx_ = d >= 0 ? bg : by, by_ = d >= 0 ? by : bg;
-    narrow = l >= 2 && need <= 63 && sx < 32 && sy < 32 && ad <= 30 && bg <= 31 && by <= 31 &&
-             fits32(pm) && fits32(qm) && msb(pm) + ad <= 32 &&
-             (by_ == 0 || msb(qm) + by_ <= 32) && (bx_ == 0 || msb(pm) + ad + bx_ <= 63);
-    w64 = bg <= 62 && sx < 64 && sy < 64 && msb(al.m) + bg <= 63 && msb(be.m) + by <= 63;
-    fwi = w64 && need <= 127 && ad < 64;
-    if (gs || st9) narrow = w64 = fwi = false;  // scaled mantissas / 9-point: generic exact path
-    swap = d < 0;
-    P = narrow ? (int)(pm << ad) : 0;
+    const int64_t ad = dd >= 0 ? dd : -dd;
+    const int64_t pm = dd >= 0 ? al.m : be.m, qm = dd >= 0 ? be.m : al.m;
+    const int64_t bx_ = dd >= 0 ? bg : by, by_ = dd >= 0 ? by : bg;
+    const int mp = msb(pm), mq = msb(qm);
+    // 32-bit operands: stencil, y and the Q product in 32 bits
+    const bool ops32 = !gs && !st9 && ssx < 32 && ssy < 32 && bg <= 31 && by <= 31 &&
+                       fits32(pm) && fits32(qm) && (by_ == 0 || mq + by_ <= 32);
+    const bool nar = ops32 && l >= 2 && nd <= 63 && ad <= 30 && mp + ad <= 32 &&
+                     (bx_ == 0 || mp + ad + bx_ <= 63);
+    const bool x32 = ops32 && (bx_ == 0 || mp + bx_ <= 32);  // ... and the P product
+    // beyond the narrow path (1-D: h^-2 = 2^{2l} puts A x ~40 bits above b at config 1):
+    // the split window of the grid kernel
+    const bool sp = x32 && ad <= 63;
+    const bool w6 = !gs && !st9 && bg <= 62 && ssx < 64 && ssy < 64 && msb(al.m) + bg <= 63 &&
+                    msb(be.m) + by <= 63;
+    d = dd;
+    zd = z;
+    sx = ssx;
+    sy = ssy;
+    narrow = nar;
+    sp32 = sp;
+    w64 = w6;
+    fwi = w6 && nd <= 127 && ad < 64;
+    swap = dd < 0;
+    P = nar ? (int)(pm << ad) : 0;
     Q = (int)qm;
+    PX = sp ? (int)pm : 0;
+    QY = sp ? (int)qm : 0;
   }
   // march-kernel interface (narrow, int32 storage)
   __host__ __device__ __forceinline__ const Vec& sv() const { return x; }
@@ -396,6 +455,28 @@ struct GemvOp {
     const int64_t X = SW ? b : a, Y = SW ? a : b;
     zl = (int64_t)((uint64_t)X * m0 + (uint64_t)Y);
     t = (int64_t)((uint64_t)X * m1 + (uint64_t)(Y >> s1)) >> s2;
+  }
+  // split window over int32 storage (grid_loop SP): t = floor(z / 2^rs) and zl = z mod 2^64
+  // from 32-bit operand products X = PX * (g | y), Y = QY * (y | g), z = X 2^ad + Y
+  template <bool NC>
+  __device__ __forceinline__ void eval4_sp(int64_t o, const SplitWin& w, int64_t t[4],
+                                           int64_t zl[4]) const {
+    int g[4], c[4], yv[4];
+    stencil4_32<NC>(x, (int)sx, dim, l, o, g, c);
+    V4<int32_t, NC>::load32(y, o, (int)sy, yv);
+    const uint32_t mN = (1u << l) - 1;
+    const bool xpad = ((uint32_t)o & mN) == mN - 3;
+    const bool rowpad = plane_pad(dim, l, z0, o);
+    const int s1 = w.s1 > 31 ? 31 : w.s1;  // floor(Y / 2^s1) of a 32-bit Y
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int X = (swap ? yv[j] : g[j]) * PX, Y = (swap ? g[j] : yv[j]) * QY;
+      const int64_t xs = (int64_t)X;
+      zl[j] = (int64_t)(((uint64_t)xs << w.a0) + (uint64_t)(int64_t)Y);
+      t[j] = (int64_t)(((uint64_t)xs << w.a1) + (uint64_t)(int64_t)(Y >> s1)) >> w.s2;
+    }
+    if (xpad) t[3] = zl[3] = 0;
+    if (rowpad) t[0] = t[1] = t[2] = t[3] = zl[0] = zl[1] = zl[2] = zl[3] = 0;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -446,32 +527,39 @@ struct JacobiOp {
   int64_t zd;
   static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t ge = 2 * l + x.hdr->e;
-    const bool zx = hdr_zero(x.hdr), zb = hdr_zero(b.hdr);
+    const HSnap hx = hsnap(x.hdr), hb = hsnap(b.hdr);
+    const int64_t ge = 2 * l + hx.e;
+    const bool zx = hx.bits == 0, zb = hb.bits == 0;
     // reference template chain (e* only; the rows are those of the chain below * 2^zd)
-    const int64_t es_ref = imin(x.hdr->e, c.e + imin(ge, b.hdr->e));
-    int64_t er, zr = 0;  // zr: unused (zd is taken against the reference chain directly)
-    axpby_setup_z(ge, b.hdr->e, zx, zb, d1, er, zr);  // r template (alpha q=1 e=0, beta q=2 e=0)
-    axpby_setup_z(x.hdr->e, c.e + er, zx, c.m == 0 || (zx && zb), d2, e_star, zr);
-    zd = e_star - es_ref;
-    sx = x.hdr->shift;
-    sb = b.hdr->shift;
-    int64_t bx = zbits(x.hdr);
-    int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
-    int64_t br = combine_bits(-1, bg, 1, zbits(b.hdr), d1);
-    need = combine_bits(1, bx, c.m, br, d2);
+    const int64_t es_ref = imin(hx.e, c.e + imin(ge, hb.e));
+    int64_t er, zr = 0, dd1, dd2, es;  // zr: unused (zd is taken against the reference chain)
+    axpby_setup_z(ge, hb.e, zx, zb, dd1, er, zr);  // r template (alpha q=1 e=0, beta q=2 e=0)
+    axpby_setup_z(hx.e, c.e + er, zx, c.m == 0 || (zx && zb), dd2, es, zr);
+    e_star = es;
+    const int64_t ssx = hx.shift, ssb = hb.shift;
+    const int64_t bx = hx.bits, bbb = hb.bits;
+    const int64_t bg = grow(bx, ceil_log2_h(4 * dim) + 1);
+    const int64_t br = combine_bits(-1, bg, 1, bbb, dd1);
+    const int64_t nd = combine_bits(1, bx, c.m, br, dd2);
+    need = nd;
     // r = -g 2^d1 + b (d1 >= 0) or b 2^-d1 - g (d1 < 0): one IMAD.WIDE either way;
     // z = x 2^d2 + c r (d2 >= 0)
-    narrow = l >= 2 && bg <= 31 && zbits(b.hdr) <= 31 && c.m >= 0 && c.m <= 0x7fffffff &&
-             need <= 63 &&
-             sx < 32 && sb < 32 && d1 >= -30 && d1 <= 30 && d2 >= 0 && d2 <= 62 && d2 != 31 &&
-             bx <= 31 && (bx == 0 || bx + d2 <= 63);
-    w64 = bg <= 62 && zbits(b.hdr) <= 62 && sx < 64 && sb < 64;
-    fwi = w64 && need <= 127 && d1 > -64 && d1 < 64 && d2 >= 0 && d2 < 64 && c.m >= 0 &&
+    const bool nar = l >= 2 && bg <= 31 && bbb <= 31 && c.m >= 0 && c.m <= 0x7fffffff &&
+                     nd <= 63 && ssx < 32 && ssb < 32 && dd1 >= -30 && dd1 <= 30 && dd2 >= 0 &&
+                     dd2 <= 62 && dd2 != 31 && bx <= 31 && (bx == 0 || bx + dd2 <= 63);
+    const bool w6 = bg <= 62 && bbb <= 62 && ssx < 64 && ssb < 64;
+    d1 = dd1;
+    d2 = dd2;
+    zd = es - es_ref;
+    sx = ssx;
+    sb = ssb;
+    narrow = nar;
+    w64 = w6;
+    fwi = w6 && nd <= 127 && dd1 > -64 && dd1 < 64 && dd2 >= 0 && dd2 < 64 && c.m >= 0 &&
           c.m <= 0xffffffffll && bx <= 62;
-    neg1 = d1 < 0;
-    P1 = narrow ? (neg1 ? (1 << (int)(-d1)) : -(1 << (int)d1)) : 0;
-    s2 = narrow ? (int)d2 : 0;
+    neg1 = dd1 < 0;
+    P1 = nar ? (neg1 ? (1 << (int)(-dd1)) : -(1 << (int)dd1)) : 0;
+    s2 = nar ? (int)dd2 : 0;
   }
   __host__ __device__ __forceinline__ const Vec& sv() const { return x; }
   __host__ __device__ __forceinline__ const Vec& yv2() const { return b; }
@@ -566,12 +654,16 @@ struct AxpbyOp {
   int64_t sx, sy, d, zd;
   static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    zd = 0;
-    axpby_setup_z(al.e + x.hdr->e, be.e + y.hdr->e, al.m == 0 || hdr_zero(x.hdr),
-                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
-    sx = x.hdr->shift;
-    sy = y.hdr->shift;
-    need = combine_bits(al.m, zbits(x.hdr), be.m, zbits(y.hdr), d);
+    const HSnap hx = hsnap(x.hdr), hy = hsnap(y.hdr);
+    int64_t dd, es, z = 0;
+    axpby_setup_z(al.e + hx.e, be.e + hy.e, al.m == 0 || hx.bits == 0, be.m == 0 || hy.bits == 0,
+                  dd, es, z);
+    e_star = es;
+    need = combine_bits(al.m, hx.bits, be.m, hy.bits, dd);
+    d = dd;
+    zd = z;
+    sx = hx.shift;
+    sy = hy.shift;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -803,19 +895,25 @@ struct ProlongCorrectOp {
   int64_t zd;
   static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
-    const int64_t ge = ep + ec.hdr->e;
-    zd = 0;
-    axpby_setup_z(al.e + ge, be.e + y.hdr->e, al.m == 0 || hdr_zero(ec.hdr),
-                  be.m == 0 || hdr_zero(y.hdr), d, e_star, zd);
-    sc = ec.hdr->shift;
-    sy = y.hdr->shift;
-    int64_t bg = grow(zbits(ec.hdr), dim + 2 + gs), by = zbits(y.hdr);
-    need = combine_bits(al.m, bg, be.m, by, d);
-    const int64_t ad = d >= 0 ? d : -d;
-    narrow = need <= 63 && bg <= 31 && by <= 31 && ad <= 30 && sc < 32 && sy < 32 && gs == 0 &&
-             al.m == 1 && be.m == 1;
-    swap = d < 0;
-    P = narrow ? (1 << (int)ad) : 0;
+    const HSnap hc = hsnap(ec.hdr), hy = hsnap(y.hdr);
+    const int64_t ge = ep + hc.e;
+    int64_t dd, es, z = 0;
+    axpby_setup_z(al.e + ge, be.e + hy.e, al.m == 0 || hc.bits == 0, be.m == 0 || hy.bits == 0,
+                  dd, es, z);
+    e_star = es;
+    const int64_t bg = grow(hc.bits, dim + 2 + gs), by = hy.bits;
+    const int64_t nd = combine_bits(al.m, bg, be.m, by, dd);
+    need = nd;
+    const int64_t ad = dd >= 0 ? dd : -dd;
+    const bool nar = nd <= 63 && bg <= 31 && by <= 31 && ad <= 30 && hc.shift < 32 &&
+                     hy.shift < 32 && gs == 0 && al.m == 1 && be.m == 1;
+    d = dd;
+    zd = z;
+    sc = hc.shift;
+    sy = hy.shift;
+    narrow = nar;
+    swap = dd < 0;
+    P = nar ? (1 << (int)ad) : 0;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {

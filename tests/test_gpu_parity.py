@@ -418,3 +418,42 @@ def test_int64_residual_windows_vs_oracle(B, p):
             m, q, e = res.z.download()
             assert e == want.e and np.array_equal(m, want.m), (off, ge)
             assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1])), (off, ge)
+
+
+@pytest.mark.parametrize("l", [18, 20, 24])
+def test_1d_wide_alignment_residual_vs_oracle(B, l):
+    """1-D residuals at config-1 scale and beyond: h^-2 = 2^{2l} puts A x ~2l bits above
+    b (alignment d = 2l + e_x - e_b >= 31), the 32-bit-operand path with a 64-bit
+    alignment shift (GemvOp::wsh); uniform x and b (config 1), window regimes from
+    underflow to overflow, and the swapped alignment (b scaled far above A x)."""
+    d, p = 1, 16
+    ox, obu = ob.gen_uniform(d, l, p, 1, 1), ob.gen_uniform(d, l, p, 1, 2)
+    gx = ggrid(B, d, l, ox.m, ox.q, ox.e)
+    for off in (0, 2 * l + 40):
+        bo = ob.OBlock(obu.m, obu.q, obu.e + off)
+        gb = ggrid(B, d, l, bo.m, bo.q, bo.e)
+        for ge in (2 * l + off - 12, 2 * l + off + 2, 2 * l + off + 20, 0):
+            g = B.Scalar(1 << 14, 16, ge)
+            res = B.residual(gx, gb, p, p + 5, g)
+            want, fl = ob.stencil_gemv(d, l, ox, bo, (-1, 1, 0), (1, 2, 0), "q", p, p + 5,
+                                       g.m, g.e)
+            m, q, e = res.z.download()
+            assert e == want.e and np.array_equal(m, want.m), (off, ge)
+            assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1])), (off, ge)
+            nn = B.residual(gx, gb, p, p + 5, g, nn=True)
+            wn, _ = ob.stencil_gemv(d, l, ox, bo, (-1, 1, 0), (1, 2, 0), "nn", p, p + 5, g.m, g.e)
+            m, q, e = nn.z.download()
+            assert e == wn.e and np.array_equal(m, wn.m), ("nn", off, ge)
+
+
+def test_c1_solve_full_size_vs_oracle(B):
+    """BASELINE config 1 at its full size (2^20 - 1 points, 10 IR-V(2,2) cycles, the
+    frozen wdot = 28 schedule): iterate, residual history and trace bit-exact."""
+    kw = dict(d=1, l_fine=20, cycles=10, x0_random=True, rhs_kind=0, w_add_cap=4)
+    ox, oh, otr = ob.mg_run(ob.mg_config(**kw, p=16, pd=28))
+    mg = B.Multigrid(B.mg_config(**kw, p=16, pd=[28] * 32))
+    mg.solve(use_graph=True)
+    x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
+    assert e == ox.e and x.tolist() == ox.m.tolist()
+    assert hist == oh
+    assert [tuple(t) for t in tr] == [tuple(t) for t in otr]

@@ -13,7 +13,8 @@ d, l, p, mb = (int(a) for a in sys.argv[1:5])
 steps = int(sys.argv[5]) if len(sys.argv) > 5 else 3
 B.set_kernel_path(bulk=(sys.argv[6] != "0") if len(sys.argv) > 6 else True)
 x = B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 1, 1)
-b = B.gen_sine(B.BfpVec.grid(d, l, mb), p)
+b = (B.gen_uniform(B.BfpVec.grid(d, l, mb), p, 1, 2) if d == 1 else
+     B.gen_sine(B.BfpVec.grid(d, l, mb), p))  # config 1: uniform rhs
 r = B.BfpVec.grid(d, l, mb)
 B.residual(x, b, p, p + 5, B.Scalar(1 << 14, 16, 2 * l + 8), out=r)
 g = B.inf_norm_upper(r).c()
