@@ -1486,32 +1486,57 @@ __global__ void __launch_bounds__(kP3T, 4)
 // is loaded once and T_{2K+2} is kept in registers for the next step.
 constexpr int kR3W = 64, kR3H = 8, kR3T = kR3W / 4 * kR3H;           // 128 threads
 constexpr int kR3FW = 2 * kR3W + 8, kR3FH = 2 * kR3H + 1;            // fine box 136 x 17
-constexpr int kR3FT = ((kR3FW * kR3FH * 4 + 127) / 128 * 128) / 4;   // slot (words, 128 B)
 constexpr int kR3D = 1;                                              // steps in flight
 constexpr int kR3FS = 2 * kR3D + 3, kR3B = kR3D + 1;                 // plane slots, barriers
-constexpr size_t kR3Smem = (size_t)kR3FS * kR3FT * 4 + kR3B * 8 + 128 + 64;
+// plane slot in elements of the storage type (128-B multiple)
+template <typename T> constexpr int r3_ft() {
+  return (int)(((kR3FW * kR3FH * sizeof(T) + 127) / 128 * 128) / sizeof(T));
+}
+template <typename T> constexpr size_t r3_smem() {
+  return (size_t)kR3FS * r3_ft<T>() * sizeof(T) + kR3B * 8 + 128 + 64;
+}
+// one fine row segment of 9 values (columns 2 I0 - ... of 4 coarse points), shifted
+__device__ __forceinline__ void r3_row(const int32_t* row, int sh, int v[9]) {
+  const int4 a = *reinterpret_cast<const int4*>(row);
+  const int4 b = *reinterpret_cast<const int4*>(row + 4);
+  v[0] = a.x >> sh, v[1] = a.y >> sh, v[2] = a.z >> sh, v[3] = a.w >> sh;
+  v[4] = b.x >> sh, v[5] = b.y >> sh, v[6] = b.z >> sh, v[7] = b.w >> sh;
+  v[8] = row[8] >> sh;
+}
+__device__ __forceinline__ void r3_row(const int64_t* row, int sh, int64_t v[9]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const longlong2 a = reinterpret_cast<const longlong2*>(row)[k];
+    v[2 * k] = a.x >> sh, v[2 * k + 1] = a.y >> sh;
+  }
+  v[8] = row[8] >> sh;
+}
 struct R3Maps {
   CUtensorMap f;
 };
 
-template <int MODE, bool FW>
+// T = storage type: int32 (plane sums in int32, need <= 35) or int64 (C5; plane sums in
+// int64, need <= 63); the box and the march are the same, the slot holds T elements
+template <int MODE, bool FW, typename T>
 __device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
                                           const WinParams& p, const WinCtx& c, Red& r, int R,
                                           char* smem, const CUtensorMap* tmf) {
+  using V = typename std::conditional<sizeof(T) == 4, int, int64_t>::type;
+  constexpr int kR3FT = r3_ft<T>();
   const int lc = out.l;  // coarse level
   const int64_t Nc = (int64_t)1 << lc, Nc2 = Nc * Nc;
   const int64_t NZ = out.nz, Z0 = out.z0;
   const int tx = (int)(Nc / kR3W), ty = (int)(Nc / kR3H);
   const int chunks = (int)((NZ + R - 1) / R);
-  int32_t* fsl = reinterpret_cast<int32_t*>(smem);
+  T* fsl = reinterpret_cast<T*>(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(fsl + kR3FS * kR3FT);
-  int32_t* O = (int32_t*)out.data;
+  T* O = (T*)out.data;
   const int sh = (int)op.sr;
   const int t = threadIdx.x, cy = t >> 4, cxq = t & 15;  // coarse row in tile, 4-group
-  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  T mx = Lim<T>::lo, mn = Lim<T>::hi;
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
-  const uint32_t pbytes = (uint32_t)kR3FW * kR3FH * 4;
+  const uint32_t pbytes = (uint32_t)(kR3FW * kR3FH * sizeof(T));
   uint32_t parity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
@@ -1535,57 +1560,61 @@ __device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
     }
     // fine columns 2 I0 .. 2 I0 + 8 of this thread's 4 coarse points, rows 2 cy .. 2 cy + 2
     const int fcol = 8 * cxq + 4, frow = 2 * cy;
-    auto T_of = [&](int64_t f, int T[4]) {
-      const int32_t* base = fsl + (int)((f - 2 * K0) % kR3FS) * kR3FT + fcol;
-      int acc[4] = {0, 0, 0, 0};
+    auto T_of = [&](int64_t f, V Ts[4]) {
+      const T* base = fsl + (int)((f - 2 * K0) % kR3FS) * kR3FT + fcol;
+      V acc[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int py = 0; py < 3; ++py) {
-        const int32_t* row = base + (frow + py) * kR3FW;
-        const int4 a = *reinterpret_cast<const int4*>(row);
-        const int4 b = *reinterpret_cast<const int4*>(row + 4);
-        const int e = row[8] >> sh;
-        const int v0 = a.x >> sh, v1 = a.y >> sh, v2 = a.z >> sh, v3 = a.w >> sh;
-        const int v4 = b.x >> sh, v5 = b.y >> sh, v6 = b.z >> sh, v7 = b.w >> sh;
-        const int wy = py == 1 ? 2 : 1;
-        acc[0] += wy * (v0 + 2 * v1 + v2);
-        acc[1] += wy * (v2 + 2 * v3 + v4);
-        acc[2] += wy * (v4 + 2 * v5 + v6);
-        acc[3] += wy * (v6 + 2 * v7 + e);
+        V v[9];
+        r3_row(base + (frow + py) * kR3FW, sh, v);
+        const V wy = py == 1 ? 2 : 1;
+        acc[0] += wy * (v[0] + 2 * v[1] + v[2]);
+        acc[1] += wy * (v[2] + 2 * v[3] + v[4]);
+        acc[2] += wy * (v[4] + 2 * v[5] + v[6]);
+        acc[3] += wy * (v[6] + 2 * v[7] + v[8]);
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) T[q] = acc[q];
+      for (int q = 0; q < 4; ++q) Ts[q] = acc[q];
     };
     const bool xpad = x0 + 4 * cxq + 3 == Nc - 1;
     const bool ypad = y0 + cy == Nc - 1;
-    int Tp[4] = {0, 0, 0, 0};  // T_{2K}
+    V Tp[4] = {0, 0, 0, 0};  // T_{2K}
     for (int s = 0; s < steps; ++s) {
       const int64_t Kc = K0 + s;
       mbar_wait(&bar[s % kR3B], (parity >> (s % kR3B)) & 1u);
       parity ^= 1u << (s % kR3B);
       if (s == 0) T_of(2 * Kc, Tp);
-      int T1[4], T2[4];
+      V T1[4], T2[4];
       T_of(2 * Kc + 1, T1);
       T_of(2 * Kc + 2, T2);
       const bool rowpad = ypad || Kc + Z0 == Nc - 1;
-      int32_t tt[4];
+      T tt[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         int64_t z = (int64_t)Tp[q] + 2 * (int64_t)T1[q] + (int64_t)T2[q];
         if ((q == 3 && xpad) || rowpad) z = 0;
         if constexpr (FW) {
           if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-          tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+          if constexpr (sizeof(T) == 4)
+            tt[q] = (T)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+          else
+            tt[q] = (T)(z >> c.rs);
         } else if (MODE == MODE_NNQ) {
-          tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+          tt[q] = (T)shift_clamp<int64_t>(z, c.lam, p.w_out);
         } else {
           if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-          tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+          tt[q] = store ? store_shift<T, int64_t>(z, c) : (T)0;
         }
         mx = tt[q] > mx ? tt[q] : mx;
         mn = tt[q] < mn ? tt[q] : mn;
       }
-      *reinterpret_cast<int4*>(O + Kc * Nc2 + (y0 + cy) * Nc + x0 + 4 * cxq) =
-          make_int4(tt[0], tt[1], tt[2], tt[3]);
+      T* dst = O + Kc * Nc2 + (y0 + cy) * Nc + x0 + 4 * cxq;
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+      } else {
+        reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
+        reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) Tp[q] = T2[q];
       __syncthreads();  // fine planes 2Kc, 2Kc + 1 are free
@@ -1602,33 +1631,34 @@ __device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kR3T, 8)
+template <int MODE, typename T>
+__global__ void __launch_bounds__(kR3T, sizeof(T) == 4 ? 8 : 2)
     rst3_win_kernel(RestrictOp op, Vec out, WinParams p, int R, const __grid_constant__ R3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   griddep_wait();
   int64_t need = 0;
   WinCtx c;
-  block_setup<RestrictOp, int32_t>(op, out, p, c, need);
+  block_setup<RestrictOp, T>(op, out, p, c, need);
   if (c.skip) return;
   Red r;
   r.init();
   // plane sums T_p (weights 16) in int32 need eff_bits(r) <= 27, i.e. need <= 35 in 3-D;
-  // the final combination is 64-bit
-  if (op.sr < 32 && need <= 35 && op.gs == 0) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR3FS * kR3FT * 4);
+  // int64 storage sums in int64 (need <= 63); the final combination is 64-bit
+  const bool fast = sizeof(T) == 4 ? (op.sr < 32 && need <= 35) : (op.sr < 64 && need <= 63);
+  if (fast && op.gs == 0) {
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kR3FS * r3_ft<T>() * sizeof(T));
     if (threadIdx.x == 0) {
       for (int k = 0; k < kR3B; ++k) mbar_init(&bar[k], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
-      rst3_loop<MODE, true>(op, out, p, c, r, R, smem, &tm.f);
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < (sizeof(T) == 4 ? 32 : 64))
+      rst3_loop<MODE, true, T>(op, out, p, c, r, R, smem, &tm.f);
     else
-      rst3_loop<MODE, false>(op, out, p, c, r, R, smem, &tm.f);
+      rst3_loop<MODE, false, T>(op, out, p, c, r, R, smem, &tm.f);
   } else {
-    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
+    grid_body<MODE, T>(op, out, p, c, r, need);  // exact generic path
   }
   griddep_launch_dependents();
   window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
@@ -2154,8 +2184,10 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
 }
 
 // 3-D full-weighting restriction, int32 storage, coarse N >= 64: the tiled-TMA march
+template <typename T>
 static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinParams& p0,
                               cudaStream_t s) {
+  constexpr size_t kR3Smem = r3_smem<T>();
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
@@ -2164,10 +2196,10 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
   const int64_t Nc = int64_t(1) << out->l;
   static int occ = 0;
   if (!occ) {
-    for (auto fn : {rst3_win_kernel<MODE_QCOMP>, rst3_win_kernel<MODE_NNQ>,
-                    rst3_win_kernel<MODE_RECOMPUTE>})
+    for (auto fn : {rst3_win_kernel<MODE_QCOMP, T>, rst3_win_kernel<MODE_NNQ, T>,
+                    rst3_win_kernel<MODE_RECOMPUTE, T>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kR3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rst3_win_kernel<MODE_QCOMP>, kR3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rst3_win_kernel<MODE_QCOMP, T>, kR3T,
                                                   kR3Smem);
     occ = std::max(occ, 1);
   }
@@ -2178,11 +2210,11 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(rst3_win_kernel<MODE_QCOMP>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
+      launch_pdl(rst3_win_kernel<MODE_QCOMP, T>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(rst3_win_kernel<MODE_NNQ>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
+      launch_pdl(rst3_win_kernel<MODE_NNQ, T>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     else
-      launch_pdl(rst3_win_kernel<MODE_RECOMPUTE>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
+      launch_pdl(rst3_win_kernel<MODE_RECOMPUTE, T>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     count_launch();
   };
   p.defer = defer_ok(p, b);

@@ -46,7 +46,8 @@ int op_restrict(bfp_vec_s* r, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.gs = gs;
   if (gs) return launch_grid(op, out, p, s);
   static const int r3 = min_level("BFP_RST3_MIN_L", 7), r2 = min_level("BFP_RST2_MIN_L", 9);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= r3) return launch_rst3(op, out, p, s);
+  if (g_use_bulk && out->dim == 3 && out->l >= r3)
+    return out->ebytes == 4 ? launch_rst3<int32_t>(op, out, p, s) : launch_rst3<int64_t>(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= r2) return launch_rst2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }

@@ -234,7 +234,9 @@ def _oblock(g):
 @pytest.mark.parametrize("d,l,mb", [(1, 2, 4), (1, 9, 4), (1, 9, 8), (2, 2, 4), (2, 6, 4),
                                     (2, 6, 8), (3, 2, 4), (3, 4, 4), (3, 4, 8),
                                     # pipelined transfer kernels (3-D l >= 7, 2-D l >= 10)
-                                    (1, 12, 4), (2, 9, 4), (2, 10, 4), (3, 7, 4)])
+                                    (1, 12, 4), (2, 9, 4), (2, 10, 4), (3, 7, 4),
+                                    # 3-D transfer marches (coarse l >= 7), int32 and int64
+                                    (3, 8, 4), (3, 8, 8)])
 def test_grid_ops_gpu_vs_oracle(B, d, l, mb):
     r = Rng(1000 + 100 * d + 10 * l + mb)
     for it in range(3):
