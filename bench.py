@@ -539,7 +539,9 @@ def run_ours(args, world, rank, local):
             "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=5),
         }
         line["fine_level_ops"] = {"C2": measure_ops(B, torch, stream, 2, 12, 20),
-                                  "C4": measure_ops(B, torch, stream, 3, 9, 24)}
+                                  "C4": measure_ops(B, torch, stream, 3, 9, 24),
+                                  "C5": measure_ops(B, torch, stream, 3, 10, 48, steps=5, s=8)}
+        torch.cuda.empty_cache()
         line["C5_precision_sweep_1gpu"] = run_c5_sweep(B, torch, stream)
     if rank == 0 and not args.no_cpu:
         sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
@@ -718,7 +720,7 @@ def measure_ops(B, torch, stream, d, l, p, steps=20, only=None, s=4):
         assert not (o.header().flags & B.FLAG_RECOMPUTED), name
         res[name] = {"kernel_ms": ms, "bytes_per_dof": bpd,
                      "hbm_frac": bpd * n / (ms / 1e3) / 1e9 / peak}
-    return {"config": f"{d}-D level {l} int32 p={p}", "dof": n, "ops": res}
+    return {"config": f"{d}-D level {l} int{8 * s} p={p}", "dof": n, "ops": res}
 
 
 SOLVES = {

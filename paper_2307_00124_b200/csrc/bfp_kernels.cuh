@@ -1316,16 +1316,20 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
 // The correction operand y arrives as two 128 x 8 boxes per pair.
 constexpr int kP3W = 128, kP3H = 8, kP3T = 256;
 constexpr int kP3CW = kP3W / 2 + 8, kP3CH = kP3H / 2 + 1;  // coarse box 72 x 5
-constexpr int kP3CT = ((kP3CW * kP3CH * 4 + 127) / 128 * 128) / 4;  // slot (words, 128 B)
+template <typename T> constexpr int p3_ct() {  // coarse slot in elements (128-B multiple)
+  return (int)(((kP3CW * kP3CH * sizeof(T) + 127) / 128 * 128) / sizeof(T));
+}
 constexpr int kP3YT = kP3W * kP3H;                               // one y box
 constexpr int kP3D = 2;                                          // pairs in flight
 constexpr int kP3S = kP3D + 1;                                   // slots / barriers
-constexpr size_t kP3Smem = (size_t)kP3S * (kP3CT + 2 * kP3YT) * 4 + kP3S * 8 + 128 + 64;
+template <typename T> constexpr size_t p3_smem() {
+  return (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T) + kP3S * 8 + 128 + 64;
+}
 struct P3Maps {
   CUtensorMap c, y;
 };
 
-template <int MODE, bool FW, typename Op>
+template <int MODE, bool FW, typename T, typename Op>
 __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r, int R, char* smem,
                                           const CUtensorMap* tmc, const CUtensorMap* tmy) {
@@ -1334,17 +1338,19 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
   const int64_t NZ = out.nz, Z0 = out.z0;
   const int tx = (int)(N / kP3W), ty = (int)(N / kP3H);
   const int chunks = (int)((NZ + R - 1) / R);
-  int32_t* csl = reinterpret_cast<int32_t*>(smem);
-  int32_t* ysl = csl + kP3S * kP3CT;
+  using V = typename std::conditional<sizeof(T) == 4, int, int64_t>::type;
+  constexpr int kP3CT = p3_ct<T>();
+  T* csl = reinterpret_cast<T*>(smem);
+  T* ysl = csl + kP3S * kP3CT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kP3S * 2 * kP3YT);
-  int32_t* O = (int32_t*)out.data;
+  T* O = (T*)out.data;
   const int sc = op.shc(), sy = op.shy();
   const int kc_off = op.zp / 2;  // coarse local plane of fine local pair K
   const int t = threadIdx.x, lane = t & 31, wy = t >> 5;
-  int32_t mx = INT32_MIN, mn = INT32_MAX;
+  T mx = Lim<T>::lo, mn = Lim<T>::hi;
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
-  const uint32_t cbytes = (uint32_t)kP3CW * kP3CH * 4, ybytes = (uint32_t)kP3YT * 4;
+  const uint32_t cbytes = (uint32_t)(kP3CW * kP3CH * sizeof(T)), ybytes = (uint32_t)(kP3YT * sizeof(T));
   uint32_t parity = 0;
   // local coarse rows of fine row y0 + wy and the coarse column of this thread's 4 points
   const int r0 = ((wy - 1) >> 1) + 1, r1 = (wy >> 1) + 1, col = 2 * lane + 4;
@@ -1376,18 +1382,18 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
     }
     const bool xpad = x0 + 4 * lane + 3 == N - 1;
     const bool ypad = y0 + wy == N - 1;
-    int Sp[4] = {0, 0, 0, 0};  // S_{K-1}
+    V Sp[4] = {0, 0, 0, 0};  // S_{K-1}
     for (int s = 0; s < pairs; ++s) {
       const int slot = s % kP3S;
       mbar_wait(&bar[slot], (parity >> slot) & 1u);
       parity ^= 1u << slot;
-      auto S_of = [&](int sl, int S[4]) {
-        const int32_t* cb = csl + sl * kP3CT;
-        int acc[4] = {0, 0, 0, 0};
+      auto S_of = [&](int sl, V S[4]) {
+        const T* cb = csl + sl * kP3CT;
+        V acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-          const int32_t* row = cb + (rr ? r1 : r0) * kP3CW + col;
-          const int a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
+          const T* row = cb + (rr ? r1 : r0) * kP3CW + col;
+          const V a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
           acc[0] += a + b;
           acc[1] += 2 * b;
           acc[2] += b + e;
@@ -1397,38 +1403,56 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
         for (int q = 0; q < 4; ++q) S[q] = acc[q];
       };
       if (s == 0) S_of((kP3S - 1) % kP3S, Sp);
-      int Sc[4];
+      V Sc[4];
       S_of(slot, Sc);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t k = 2 * (K0 + s) + h;  // local fine plane
-        int yv[4] = {0, 0, 0, 0};
+        V yv[4] = {0, 0, 0, 0};
         if (Op::kCorr) {
-          const int4 y4 =
-              *reinterpret_cast<const int4*>(ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane);
-          yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
+          const T* yp = ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane;
+          if constexpr (sizeof(T) == 4) {
+            const int4 y4 = *reinterpret_cast<const int4*>(yp);
+            yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
+          } else {
+            const longlong2 a = reinterpret_cast<const longlong2*>(yp)[0];
+            const longlong2 b = reinterpret_cast<const longlong2*>(yp)[1];
+            yv[0] = a.x >> sy, yv[1] = a.y >> sy, yv[2] = b.x >> sy, yv[3] = b.y >> sy;
+          }
         }
         const bool rowpad = ypad || k + Z0 == N - 1;
-        int32_t tt[4];
+        T tt[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
-          int64_t z = op.corr(g, yv[q]);
+          const V g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+          int64_t z;
+          if constexpr (sizeof(T) == 4)
+            z = op.corr(g, yv[q]);
+          else
+            z = op.corr_w(g, yv[q]);
           if ((q == 3 && xpad) || rowpad) z = 0;
           if constexpr (FW) {
             if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-            tt[q] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+            if constexpr (sizeof(T) == 4)
+              tt[q] = (T)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+            else
+              tt[q] = (T)(z >> c.rs);
           } else if (MODE == MODE_NNQ) {
-            tt[q] = (int32_t)shift_clamp<int64_t>(z, c.lam, p.w_out);
+            tt[q] = (T)shift_clamp<int64_t>(z, c.lam, p.w_out);
           } else {
             if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-            tt[q] = store ? store_shift<int32_t, int64_t>(z, c) : 0;
+            tt[q] = store ? store_shift<T, int64_t>(z, c) : (T)0;
           }
           mx = tt[q] > mx ? tt[q] : mx;
           mn = tt[q] < mn ? tt[q] : mn;
         }
-        *reinterpret_cast<int4*>(O + k * N2 + (y0 + wy) * N + x0 + 4 * lane) =
-            make_int4(tt[0], tt[1], tt[2], tt[3]);
+        T* dst = O + k * N2 + (y0 + wy) * N + x0 + 4 * lane;
+        if constexpr (sizeof(T) == 4) {
+          *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+        } else {
+          reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
+          reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+        }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) Sp[q] = Sc[q];
@@ -1446,31 +1470,33 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
-template <int MODE, typename Op>
-__global__ void __launch_bounds__(kP3T, 4)
+template <int MODE, typename T, typename Op>
+__global__ void __launch_bounds__(kP3T, sizeof(T) == 4 ? 4 : 2)
     pro3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ P3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   griddep_wait();
   int64_t need = 0;
   WinCtx c;
-  block_setup<Op, int32_t>(op, out, p, c, need);
+  block_setup<Op, T>(op, out, p, c, need);
   if (c.skip) return;
   Red r;
   r.init();
-  if (op.narrow && need <= 63) {
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (kP3CT + 2 * kP3YT) * 4);
+  const bool fast = sizeof(T) == 4 ? (op.narrow && need <= 63) : op.wide;
+  if (fast) {
+    uint64_t* bar =
+        reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T));
     if (threadIdx.x == 0) {
       for (int k = 0; k < kP3S; ++k) mbar_init(&bar[k], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < 32)
-      pro3_loop<MODE, true>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
+    if (MODE != MODE_NNQ && c.store_tmp && c.ls == 0 && c.rs < (sizeof(T) == 4 ? 32 : 64))
+      pro3_loop<MODE, true, T>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
     else
-      pro3_loop<MODE, false>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
+      pro3_loop<MODE, false, T>(op, out, p, c, r, R, smem, &tm.c, &tm.y);
   } else {
-    grid_body<MODE, int32_t>(op, out, p, c, r, need);  // exact generic path
+    grid_body<MODE, T>(op, out, p, c, r, need);  // exact generic path
   }
   griddep_launch_dependents();
   window_reduce(r, out.hdr, p, c, [&](int bits, int64_t mx, int64_t mn, int err) {
@@ -2127,9 +2153,10 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
 }
 
 // 3-D prolongation (+ correction), int32 storage, N >= 128: the tiled-TMA pair march
-template <typename Op>
+template <typename T, typename Op>
 static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
                               cudaStream_t s) {
+  constexpr size_t kP3Smem = p3_smem<T>();
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
@@ -2143,10 +2170,10 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
   const int64_t N = int64_t(1) << out->l;
   static int occ = 0;
   if (!occ) {
-    for (auto fn : {pro3_win_kernel<MODE_QCOMP, Op>, pro3_win_kernel<MODE_NNQ, Op>,
-                    pro3_win_kernel<MODE_RECOMPUTE, Op>})
+    for (auto fn : {pro3_win_kernel<MODE_QCOMP, T, Op>, pro3_win_kernel<MODE_NNQ, T, Op>,
+                    pro3_win_kernel<MODE_RECOMPUTE, T, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pro3_win_kernel<MODE_QCOMP, Op>, kP3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pro3_win_kernel<MODE_QCOMP, T, Op>, kP3T,
                                                   kP3Smem);
     occ = std::max(occ, 1);
   }
@@ -2158,11 +2185,11 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(pro3_win_kernel<MODE_QCOMP, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_QCOMP, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(pro3_win_kernel<MODE_NNQ, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_NNQ, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
     else
-      launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
     count_launch();
   };
   p.defer = defer_ok(p, b);

@@ -847,12 +847,15 @@ struct ProlongOp {
   __host__ __device__ __forceinline__ const Vec& yv() const { return xc; }  // unused
   __device__ __forceinline__ int shc() const { return (int)sc; }
   __device__ __forceinline__ int shy() const { return 0; }
+  bool wide;    // int64 storage and |P xc| < 2^63: the 3-D march in 64 bits
   __device__ __forceinline__ int64_t corr(int g, int yv) const { (void)yv; return g; }
+  __device__ __forceinline__ int64_t corr_w(int64_t g, int64_t yv) const { (void)yv; return g; }
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = ep + xc.hdr->e;
     sc = xc.hdr->shift;
     need = eff_bits(xc.hdr) + dim + 2 + gs;
     narrow = need <= 31 && sc < 32 && gs == 0;
+    wide = need <= 63 && sc < 64 && gs == 0;
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -892,6 +895,13 @@ struct ProlongCorrectOp {
     const int X = swap ? yy : g, Y = swap ? g : yy;
     return (int64_t)X * (int64_t)P + (int64_t)Y;
   }
+  // int64 storage (wide): z = X 2^|d| + Y in 64 bits, exact by need <= 63
+  bool wide;
+  int AD;
+  __device__ __forceinline__ int64_t corr_w(int64_t g, int64_t yy) const {
+    const int64_t X = swap ? yy : g, Y = swap ? g : yy;
+    return (int64_t)((uint64_t)X << AD) + Y;
+  }
   int64_t zd;
   static constexpr int zd_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
@@ -912,6 +922,9 @@ struct ProlongCorrectOp {
     sc = hc.shift;
     sy = hy.shift;
     narrow = nar;
+    wide = nd <= 63 && ad < 64 && hc.shift < 64 && hy.shift < 64 && gs == 0 && al.m == 1 &&
+           be.m == 1;
+    AD = wide ? (int)ad : 0;
     swap = dd < 0;
     P = nar ? (1 << (int)ad) : 0;
   }

@@ -71,7 +71,8 @@ int op_prolong(bfp_vec_s* xc, const WinParams& p, bfp_vec_s* out, cudaStream_t s
   op.gs = gs;
   if (gs) return launch_grid(op, out, p, s);
   static const int p3 = min_level("BFP_PRO3_MIN_L", 7), p2 = min_level("BFP_PRO2_MIN_L", 10);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= p3) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 3 && out->l >= p3)
+    return out->ebytes == 4 ? launch_pro3<int32_t>(op, out, p, s) : launch_pro3<int64_t>(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= p2) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
@@ -93,7 +94,8 @@ int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_
   op.be = be;
   if (gs || al.m != 1 || be.m != 1) return launch_grid(op, out, p, s);
   static const int p3 = min_level("BFP_PRO3_MIN_L", 7), p2 = min_level("BFP_PRO2_MIN_L", 10);
-  if (g_use_bulk && out->dim == 3 && out->ebytes == 4 && out->l >= p3) return launch_pro3(op, out, p, s);
+  if (g_use_bulk && out->dim == 3 && out->l >= p3)
+    return out->ebytes == 4 ? launch_pro3<int32_t>(op, out, p, s) : launch_pro3<int64_t>(op, out, p, s);
   if (g_use_bulk && out->dim == 2 && out->ebytes == 4 && out->l >= p2) return launch_pro2(op, out, p, s);
   return launch_grid(op, out, p, s);
 }
