@@ -566,8 +566,10 @@ def run_ours(args, world, rank, local):
 
 def run_e2e(args, B, Lb, torch, stream, sp):
     """Same metric through the C-ABI with pinned HOST buffers, pipelined across steps:
-    stream A uploads x, b and runs the residual into buffer k%2; stream B downloads
-    r of step k (D2H engine) while A uploads step k+1 (H2D engine)."""
+    stream A[k%2] uploads x, b and runs the residual into buffer k%2; stream B downloads
+    r of step k (D2H engine) while A[(k+1)%2] uploads step k+1 (H2D engine). Two upload
+    streams keep the H2D engine busy through step k's scatter and residual kernels.
+    `pcie_h2d_gbs`: one step's H2D bytes copied alone (the bound of this arm)."""
     n = dof()
     x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
     b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
@@ -587,9 +589,11 @@ def run_e2e(args, B, Lb, torch, stream, sp):
     B.residual(xd[0], bd[0], P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=rd[0])
     g = B.inf_norm_upper(rd[0]).c()
     m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+    sas = [stream, torch.cuda.Stream()]
     sa = stream
     sb = torch.cuda.Stream()
-    pa, pb = C.c_void_p(sa.cuda_stream), C.c_void_p(sb.cuda_stream)
+    pas = [C.c_void_p(s_.cuda_stream) for s_ in sas]
+    pb = C.c_void_p(sb.cuda_stream)
     ev_r = [torch.cuda.Event() for _ in range(2)]
     ev_d = [torch.cuda.Event() for _ in range(2)]
     for e in ev_d:
@@ -597,6 +601,7 @@ def run_e2e(args, B, Lb, torch, stream, sp):
 
     def step(k):
         i = k & 1
+        sa, pa = sas[i], pas[i]
         sa.wait_event(ev_d[i])  # download of step k-2 finished with rd[i]
         assert Lb.bfp_vec_upload_i32(xd[i].h, C.c_void_p(hx.data_ptr()), qx, ex, pa) == 0
         assert Lb.bfp_vec_upload_i32(bd[i].h, C.c_void_p(hb.data_ptr()), qb, eb, pa) == 0
@@ -613,18 +618,34 @@ def run_e2e(args, B, Lb, torch, stream, sp):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(sa)
+    sas[1].wait_stream(sa)
     for j in range(k):
         step(j)
     sa.wait_stream(sb)
+    sa.wait_stream(sas[1])
     e1.record(sa)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    # the PCIe bound: one step's H2D bytes (x and b) alone, pinned, same engine
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dx, db = torch.empty(n, dtype=torch.int32, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(sa):
+        for _ in range(2):
+            dx.copy_(hx, non_blocking=True)
+        h0.record(sa)
+        for _ in range(5):
+            dx.copy_(hx, non_blocking=True)
+            db.copy_(hb, non_blocking=True)
+        h1.record(sa)
+    torch.cuda.synchronize()
+    h2d_gbs = 5 * 2 * 4 * n / (h0.elapsed_time(h1) / 1e3) / 1e9
     # the downloaded mantissas are the residual (fast path: exponent from the header)
     h = rd[(k - 1) & 1].header()
     assert h.err == 0
     return {"value": n * k / (ms / 1e3) / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": 2 * 4 * n,
             "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
-            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (stream A) | "
+            "pcie_h2d_gbs": h2d_gbs, "pcie_bound_frac": 2 * 4 * n / (ms / k / 1e3) / 1e9 / h2d_gbs,
+            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (streams A0/A1 by step parity) | "
                     "bfp_vec_download_async_i32 (stream B), pinned host, double-buffered"}
 
 
