@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -69,6 +70,58 @@ inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
 inline int min_level(const char* name, int def) {
   const char* v = getenv(name);
   return v ? atoi(v) : def;
+}
+// March depth R (planes per work item) of a one-wave plane march over `units` tiles x NZ
+// planes on `ctas` resident CTAs, items handed out round robin (item = unit + chunk *
+// units, CTA b takes b, b + ctas, ...).  R = ceil(units NZ / ctas) minimises the item
+// count but can leave a short last chunk on a second round for some CTAs (C4: R = 222
+// gives 290 planes on the busiest CTA against 221 on average); this picks, among the
+// chunk counts 1..64, the R (a multiple of `step`, >= Rmin) with the smallest busiest-CTA
+// load, counting `ovh` planes per item for the march prologue.  BFP_MARCH_BALANCE=0 in
+// the environment restores the plain R (A/B).
+inline int march_R(int64_t units, int64_t NZ, int64_t ctas, int Rmin, int step, int ovh) {
+  auto plain = [&] {
+    int64_t R = std::max<int64_t>(Rmin, (units * NZ + ctas - 1) / ctas);
+    return (int)((R + step - 1) / step * step);
+  };
+  static const bool on = [] {
+    const char* v = getenv("BFP_MARCH_BALANCE");
+    return !(v && v[0] == '0');
+  }();
+  if (!on || units <= 0 || NZ <= 0) return plain();
+  struct Key {
+    int64_t u, nz, c;
+    int rm, st, ov, R;
+  };
+  static Key cache[64];
+  static int ncache = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].u == units && cache[i].nz == NZ && cache[i].c == ctas && cache[i].rm == Rmin &&
+        cache[i].st == step && cache[i].ov == ovh)
+      return cache[i].R;
+  auto makespan = [&](int64_t R) {
+    const int64_t nc = (NZ + R - 1) / R, items = units * nc, last = NZ - (nc - 1) * R;
+    const int64_t L0 = (nc - 1) * units;  // first item of the last chunk
+    int64_t worst = 0;
+    for (int64_t b = 0; b < std::min(items, ctas); ++b) {
+      const int64_t cnt = (items - 1 - b) / ctas + 1;
+      const int64_t jmin = b >= L0 ? 0 : (L0 - b + ctas - 1) / ctas;
+      const int64_t nlast = std::max<int64_t>(0, cnt - jmin);
+      worst = std::max(worst, cnt * (R + ovh) - nlast * (R - last));
+    }
+    return worst;
+  };
+  int64_t bestR = plain(), best = makespan(bestR);
+  for (int64_t nc = 1; nc <= 64; ++nc) {
+    int64_t R = std::max<int64_t>(Rmin, (NZ + nc - 1) / nc);
+    R = (R + step - 1) / step * step;
+    const int64_t m = makespan(R);
+    if (m < best) best = m, bestR = R;
+  }
+  if (ncache < 64) cache[ncache++] = Key{units, NZ, ctas, Rmin, step, ovh, (int)bestR};
+  return (int)bestR;
 }
 inline int blocks_for(int64_t work) {
   int64_t b = (work + kThreads - 1) / kThreads;
@@ -2121,7 +2174,7 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
     occ = std::max(occ, 1);
   }
   const int64_t tiles = (N / kB3W) * (N / kB3H), ctas = (int64_t)148 * occ, NZ = out->nz;
-  const int R = (int)std::max<int64_t>(4, (tiles * NZ + ctas - 1) / ctas);
+  const int R = march_R(tiles, NZ, ctas, 4, 1, 2);
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   WinParams p = p0;
@@ -2178,8 +2231,7 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
     occ = std::max(occ, 1);
   }
   const int64_t tiles = (N / kP3W) * (N / kP3H), ctas = (int64_t)148 * occ, NZ = out->nz;
-  int R = (int)std::max<int64_t>(4, (tiles * NZ + ctas - 1) / ctas);
-  R += R & 1;  // whole fine-plane pairs
+  const int R = march_R(tiles, NZ, ctas, 4, 2, 1);  // whole fine-plane pairs
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   WinParams p = p0;
@@ -2231,7 +2283,7 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
     occ = std::max(occ, 1);
   }
   const int64_t tiles = (Nc / kR3W) * (Nc / kR3H), ctas = (int64_t)148 * occ, NZ = out->nz;
-  const int R = (int)std::max<int64_t>(2, (tiles * NZ + ctas - 1) / ctas);
+  const int R = march_R(tiles, NZ, ctas, 2, 1, 1);
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   WinParams p = p0;
@@ -2279,8 +2331,7 @@ static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int
     occ = std::max(occ, 1);
   }
   const int64_t ctas = (int64_t)148 * occ;
-  int R = (int)std::max<int64_t>(Rmin, (units * NZ + ctas - 1) / ctas);
-  if (even) R += R & 1;
+  const int R = march_R(units, NZ, ctas, Rmin, even ? 2 : 1, 1);
   const int64_t items = units * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   Vec o = view(out);
@@ -2344,7 +2395,7 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
   }
   const int64_t strips = N / kBulkW, ctas = (int64_t)148 * occ;
   const int64_t NZ = out->nz;
-  const int R = (int)std::max<int64_t>(8, (strips * NZ + ctas - 1) / ctas);
+  const int R = march_R(strips, NZ, ctas, 8, 1, 2);
   const int64_t items = strips * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
   WinParams p = p0;
