@@ -1002,25 +1002,44 @@ __global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops
 #ifndef BFP_B3_EMPTY  // A/B switch: empty mbarriers (1) or a block barrier (0) per step
 #define BFP_B3_EMPTY 0
 #endif
-#ifndef BFP_B3_MINB  // resident CTAs per SM the int32 instantiation is compiled for
-#define BFP_B3_MINB 4
-#endif
 #ifndef BFP_B3_SPLIT
 #define BFP_B3_SPLIT 1  // int64 residual through SplitWin (A/B: -DBFP_B3_SPLIT=0)
 #endif
 constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
-#ifndef BFP_B3_D
-#define BFP_B3_D 3
+// planes in flight (D; rings of D+3 x and D+1 y slots) and resident CTAs per SM the
+// kernel is compiled for, per storage type and op, swept on the B200 after the balanced
+// march depth (tools/ab_b3.sh, profiles/r1_ab_b3.txt; 3-D 511^3 int32 / 1023^3 int64):
+// int32 residual D = 2 at 4 CTAs/SM (0.92 of HBM; D = 3: 0.81), int32 Jacobi D = 4 at 3
+// CTAs/SM (0.84; D = 3 at 4: 0.81), int64 D = 3 at 2 CTAs/SM (residual 0.92, Jacobi
+// 0.71; D = 2: 0.89 / 0.71, D = 4: 0.75 / 0.56).  -DBFP_B3_D / -DBFP_B3_MINB override (A/B).
+template <typename Op, typename = void> struct B3Tune {
+  static constexpr int D = 2, MINB = 4;
+};
+template <typename Op> struct B3Tune<Op, decltype((void)Op::b3_depth)> {
+  static constexpr int D = Op::b3_depth, MINB = Op::b3_minb;
+};
+template <typename T, typename Op> constexpr int b3_d() {
+#ifdef BFP_B3_D
+  return BFP_B3_D;
+#else
+  return sizeof(T) == 8 ? 3 : B3Tune<Op>::D;
 #endif
-constexpr int kB3D = BFP_B3_D;                                // planes in flight
-constexpr int kB3XS = kB3D + 3, kB3YS = kB3D + 1;
+}
+template <typename T, typename Op> constexpr int b3_minb() {
+#ifdef BFP_B3_MINB
+  return sizeof(T) == 8 ? 2 : BFP_B3_MINB;
+#else
+  return sizeof(T) == 8 ? 2 : B3Tune<Op>::MINB;
+#endif
+}
 constexpr int kB3XW = kB3W + 8, kB3XR = kB3H + 2;             // x tile row width / rows
 constexpr int kB3XT = kB3XW * kB3XR, kB3YT = kB3W * kB3H;     // elements per tile
 // x-plane slots padded to 128 B (TMA destinations), 128 B of slack to align the base
 template <typename T> constexpr int b3_xtp() {
   return (int)(((kB3XT * sizeof(T) + 127) / 128 * 128) / sizeof(T));
 }
-template <typename T> constexpr size_t b3_smem() {
+template <typename T, typename Op> constexpr size_t b3_smem() {
+  constexpr int kB3XS = b3_d<T, Op>() + 3, kB3YS = b3_d<T, Op>() + 1;
   return (size_t)(kB3XS * b3_xtp<T>() + kB3YS * kB3YT) * sizeof(T) + 2 * kB3YS * 8 + 128 + 64;
 }
 // the x / y operands of a 3-D pipeline launch as tiled TMA descriptors: tensor
@@ -1085,6 +1104,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
                                            const WinCtx& c, Red& r, int R, char* smem,
                                            const CUtensorMap* tmx, const CUtensorMap* tmy) {
   constexpr int XTP = b3_xtp<T>();
+  constexpr int kB3D = b3_d<T, Op>(), kB3XS = kB3D + 3, kB3YS = kB3D + 1;
   using V = typename S4<T>::V;
   const int l = out.l;
   const int64_t N = (int64_t)1 << l, N2 = N * N;
@@ -1284,7 +1304,7 @@ __device__ __forceinline__ void b3_dispatch(bool sh, bool sw, const Op& op, cons
 }
 
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
+__global__ void __launch_bounds__(kB3T, b3_minb<T, Op>())
     bulk3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ B3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1298,7 +1318,9 @@ __global__ void __launch_bounds__(kB3T, sizeof(T) == 4 ? BFP_B3_MINB : 2)
   const bool fast = sizeof(T) == 4 ? (op.narrow && need <= 63) : (op.w64 && need <= 127);
   if (fast) {
     uint64_t* bar =
-        reinterpret_cast<uint64_t*>(smem + (size_t)(kB3XS * b3_xtp<T>() + kB3YS * kB3YT) * sizeof(T));
+        reinterpret_cast<uint64_t*>(smem + (size_t)((b3_d<T, Op>() + 3) * b3_xtp<T>() +
+                                                    (b3_d<T, Op>() + 1) * kB3YT) * sizeof(T));
+    constexpr int kB3YS = b3_d<T, Op>() + 1;
     if (threadIdx.x == 0) {
       for (int k = 0; k < kB3YS; ++k) {
         mbar_init(&bar[k], 1);
@@ -2163,7 +2185,7 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
   if (!encode_b3(&tm.x, op.sv(), kB3XW, kB3XR) || !encode_b3(&tm.y, op.yv2(), kB3W, kB3H))
     return BFP_ERR_CUDA;
   const int64_t N = int64_t(1) << out->l;
-  constexpr size_t smem = b3_smem<T>();
+  constexpr size_t smem = b3_smem<T, Op>();
   static int occ = 0;
   if (!occ) {
     for (auto fn : {bulk3_win_kernel<MODE_QCOMP, T, Op>, bulk3_win_kernel<MODE_NNQ, T, Op>,

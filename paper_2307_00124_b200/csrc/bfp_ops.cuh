@@ -526,6 +526,7 @@ struct JacobiOp {
   int P1, s2;
   int64_t zd;
   static constexpr int zd_tag = 0;
+  static constexpr int b3_depth = 4, b3_minb = 3;  // bulk3 tuning (int32; B3Tune)
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const HSnap hx = hsnap(x.hdr), hb = hsnap(b.hdr);
     const int64_t ge = 2 * l + hx.e;
