@@ -61,7 +61,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define BFP_BULK_T 256
 #endif
 #ifndef BFP_B2_MINB  // resident CTAs per SM the 2-D pipeline is compiled for
-#define BFP_B2_MINB 4
+#define BFP_B2_MINB 3    // with D = 3 (tools/ab_b2.sh, profiles/r1_ab_b2.txt)
 #endif
 // 3-D tiled TMA: box at tensor coordinates (c0, c1, c2) -> shared, completes tx on bar
 __device__ __forceinline__ void tma_g2s_3d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -76,7 +76,9 @@ __device__ __forceinline__ void tma_g2s_3d(void* dst, const CUtensorMap* map, in
 constexpr int kBulkT = BFP_BULK_T;      // threads per CTA (one 4-group each)
 constexpr int kBulkW = 4 * kBulkT;      // strip width in columns
 #ifndef BFP_BULK_D
-#define BFP_BULK_D 2
+// C2 4095^2 after the balanced march depth: D = 3 at 3 CTAs/SM residual 0.81, Jacobi 0.77;
+// D = 2 at 4/SM 0.78 / 0.75; D = 4 at 3/SM 0.81 / 0.76; D = 4 at 2/SM 0.77 / 0.71
+#define BFP_BULK_D 3
 #endif
 #ifndef BFP_B2_EMPTY  // A/B switch: empty mbarriers (1) or a block barrier (0) per step
 #define BFP_B2_EMPTY 1
