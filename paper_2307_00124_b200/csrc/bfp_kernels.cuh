@@ -1395,7 +1395,13 @@ template <typename T> constexpr int p3_ct() {  // coarse slot in elements (128-B
   return (int)(((kP3CW * kP3CH * sizeof(T) + 127) / 128 * 128) / sizeof(T));
 }
 constexpr int kP3YT = kP3W * kP3H;                               // one y box
-constexpr int kP3D = 2;                                          // pairs in flight
+#ifndef BFP_P3_D
+#define BFP_P3_D 2
+#endif
+#ifndef BFP_P3_MINB  // resident CTAs per SM of the int32 instantiation
+#define BFP_P3_MINB 4
+#endif
+constexpr int kP3D = BFP_P3_D;                                    // pairs in flight
 constexpr int kP3S = kP3D + 1;                                   // slots / barriers
 template <typename T> constexpr size_t p3_smem() {
   return (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T) + kP3S * 8 + 128 + 64;
@@ -1546,7 +1552,7 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
 }
 
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kP3T, sizeof(T) == 4 ? 4 : 2)
+__global__ void __launch_bounds__(kP3T, sizeof(T) == 4 ? BFP_P3_MINB : 2)
     pro3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ P3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1774,7 +1780,13 @@ __global__ void __launch_bounds__(kR3T, sizeof(T) == 4 ? 8 : 2)
 // (2J, 2J+1) over the coarse row sums S_J (P e_c: 2J -> S_{J-1} + S_J, 2J+1 -> 2 S_J).
 constexpr int kP2T = 256, kP2W = 4 * kP2T;                       // fine strip
 constexpr int kP2CW = kP2W / 2 + 8;                              // coarse row slot (words)
-constexpr int kP2D = 2, kP2S = kP2D + 1;                         // pairs in flight, slots
+#ifndef BFP_P2_D
+#define BFP_P2_D 2
+#endif
+#ifndef BFP_P2_MINB
+#define BFP_P2_MINB 4
+#endif
+constexpr int kP2D = BFP_P2_D, kP2S = kP2D + 1;                   // pairs in flight, slots
 constexpr size_t kP2Smem = (size_t)kP2S * (kP2CW + 2 * kP2W) * 4 + kP2S * 8 + 128 + 64;
 
 template <int MODE, bool FW, typename Op>
@@ -1884,7 +1896,7 @@ __device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const Wi
 }
 
 template <int MODE, typename Op>
-__global__ void __launch_bounds__(kP2T, 4) pro2_win_kernel(Op op, Vec out, WinParams p, int R) {
+__global__ void __launch_bounds__(kP2T, BFP_P2_MINB) pro2_win_kernel(Op op, Vec out, WinParams p, int R) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
   griddep_wait();
