@@ -1,28 +1,38 @@
 #!/usr/bin/env python
 """Benchmark of the B200 BFP multigrid hot path (BASELINE.json metric).
 
-Headline (`value`): BFP stencil residual throughput in GDoF/s on BASELINE.json
-config 2's fine level -- r = b - A x, 2-D 5-point, 4095^2 interior, int32
-mantissas p = 20, qcomp window (w_tmp = p + 5), int64 exact accumulation --
-with inputs resident in HBM.  One step = one windowed residual over the whole
-grid (pass 1 + the recompute launch, which exits early on the fast path).
+Metric: "BFP stencil residual GDoF/s + % of HBM roofline; FMG solve time to disc.
+accuracy".  BASELINE.json names no config for it, so the N = 1 line is quoted on the
+largest single-GPU config, config 4:
 
-`e2e`: the same metric through the C-ABI with HOST buffers: every step uploads
-x and b (int32, pinned) and downloads r, copies inside the timed region.
-`roofline`: the dominant kernel (pass 1 of the residual) timed with CUDA events
-on its own stream, algorithmic bytes 12 B/DoF, against MEASURED_PEAKS.json.
-`cpu_baseline`: the CPU oracle port (oracle/bfp_oracle.c, OpenMP) on the same
-residual, all host threads.  `solves`: device time of the full config solves
-(C1, C2, C3, C4) replayed as CUDA graphs, with their final residual norms.
+`value`: BFP stencil residual throughput in GDoF/s on config 4's fine level --
+r = b - A x, 3-D 7-point, 511^3 interior, int32 mantissas p = 24, qcomp window
+(w_tmp = p + 5), exact int64 accumulation -- with inputs resident in HBM (two
+(x, b, r) sets of 1.6 GB each, far above the 126 MB L2).  One step = one windowed
+residual over the whole grid (pass 1 + the recompute launch, which exits early on the
+fast path).
 
-`--impl reference` times the reference's CPU path (the oracle port of
-P/src/blas.cpp qcomp + EgemvKernel; the GMP reference itself cannot be built
-here) on the same config and metric.
+`roofline`: the dominant kernel (pass 1 of the residual, bulk3_win_kernel) timed with
+CUDA events on its launch stream over a fixed loop of 200 launches (independent of
+--steps), 12 algorithmic bytes per DoF, against MEASURED_PEAKS.json.
+`e2e`: the same metric through the C-ABI with HOST buffers: every step uploads x and b
+(int32, pinned) and downloads r, copies inside the timed region.
+`cpu_baseline`: the CPU oracle port (oracle/bfp_oracle.c, OpenMP, all host threads) on
+the same residual, a single-thread sample, and the FMG solve to discretisation accuracy
+(config 4, two IR-V(2,1) per level) on the host cores.
+`solves`: device time of the config solves (C1-C5) replayed as CUDA graphs, each with
+its algorithmic-bytes roofline fraction and accuracy; `summary` (last key) repeats the
+numbers a reader needs in a few hundred bytes.
+
+`--impl reference` times the reference's CPU path (the oracle port of P/src/blas.cpp
+qcomp + EgemvKernel; the GMP reference itself cannot be built here) on
+the same config and metric.  `--gpus N` without torchrun spawns its own N ranks.
 """
 import argparse
 import ctypes as C
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -30,14 +40,15 @@ import time
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-D, L_FINE, P_BITS = 2, 12, 20
+D, L_FINE, P_BITS = 3, 9, 24  # config 4's fine level
 W_TMP = P_BITS + 5
-N_SETS = 4
+N_SETS = 2
 BYTES_PER_DOF = 12  # x, b read once + r written once, int32
+KERNEL_LAUNCHES = 200  # fixed pass-1 loop of the roofline timing
 
 
-def dof():
-    return ((1 << L_FINE) - 1) ** D
+def dof(d=D, l=L_FINE):
+    return ((1 << l) - 1) ** d
 
 
 def peaks():
@@ -97,62 +108,79 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_setup(args):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: start N ranks of this script (one per GPU,
+    env rendezvous on 127.0.0.1) and return the worst exit code; rank 0 prints the line."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env))
+    return max(p.wait() for p in procs)
+
+
 # ---------------------------------------------------------------------------
-# reference arm: the CPU path (oracle port) on the same config
+# CPU side (test-infrastructure oracle, oracle/bfp_oracle.c): the reference arm and the
+# cpu_baseline legs
 
 
-def cpu_residual_time(steps, warmup, budget_s=None, threads=None):
-    """Time the oracle's OpenMP qcomp residual on the config-2 inputs (all host threads,
-    or `threads`). Returns (seconds per residual, threads, steps actually run)."""
+def cpu_inputs(d, l, p):
+    from oracle import ob
+    x = ob.gen_uniform(d, l, p, 1, 1)
+    b = ob.gen_uniform(d, l, p, 1, 2) if d == 1 else ob.gen_sine(d, l, p)
+    return x, b
+
+
+def cpu_residual_time(steps, warmup, budget_s=None, threads=None, d=D, l=L_FINE, p=P_BITS):
+    """The oracle's OpenMP qcomp residual on the workload's inputs (all host threads, or
+    `threads`). Returns (seconds per residual, threads, residuals run)."""
     from oracle import ob
     L = ob.lib()
-    x = ob.gen_uniform(D, L_FINE, P_BITS, 1, 1)
-    b = ob.gen_sine(D, L_FINE, P_BITS)
-    out = ob.OBlock(x.m.copy(), P_BITS, 0)
+    x, b = cpu_inputs(d, l, p)
+    out = ob.OBlock(x.m.copy(), p, 0)
     xc, bc, oc = x.c(), b.c(), out.c()
     fl = ob.Flags()
     threads = threads or os.cpu_count() or 1
-    g = ob.Grid(D, L_FINE)
-    gm, ge = 1 << 14, 30  # window above the residual: exercised like the reference's gamma
-    # exact-binade gamma: the fast path, as on the GPU
-    rc = L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge,
-                                 C.byref(oc), C.byref(fl), threads)
+    g = ob.Grid(d, l)
+    gm, ge = 1 << 14, 2 * l + 8
+    rc = L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), p, p + 5, gm, ge, C.byref(oc),
+                                 C.byref(fl), threads)
     assert rc == 0
+    # exact-binade gamma: the qcomp fast path, as on the GPU
     mx = int(abs(out.m).max()) if len(out.m) else 0
     ge = oc.e + mx.bit_length() + 1 - 16 if mx else 0
     for _ in range(warmup):
-        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge, C.byref(oc),
+        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), p, p + 5, gm, ge, C.byref(oc),
                                 C.byref(fl), threads)
     t0 = time.perf_counter()
     n = 0
     while n < steps:
-        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), P_BITS, W_TMP, gm, ge, C.byref(oc),
+        L.ob_residual_qcomp_omp(g, C.byref(xc), C.byref(bc), p, p + 5, gm, ge, C.byref(oc),
                                 C.byref(fl), threads)
         n += 1
         if budget_s is not None and time.perf_counter() - t0 > budget_s:
             break
-    dt = (time.perf_counter() - t0) / n
-    return dt, threads, n
+    return (time.perf_counter() - t0) / n, threads, n
 
 
-def traffic_bytes(args):
-    """ncu dram read + write bytes per pass-1 launch of the dominant kernel, from the
-    committed capture (profiles/r1_traffic.json) unless given on the command line."""
-    if args.traffic_bytes is not None:
-        return args.traffic_bytes
-    try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                               "r1_traffic.json")) as f:
-            return json.load(f)["c2_residual_pass1"]["traffic_bytes"]
-    except (OSError, KeyError, ValueError):
-        return None
+def cpu_fmg_time(name):
+    """Wall time of one config solve on the host cores (oracle, OpenMP, all threads)."""
+    from oracle import ob
+    kw = dict(SOLVES[name])
+    t0 = time.perf_counter()
+    x, hist, tr = ob.mg_run(ob.mg_config(**kw), trace_cap=1 << 16)
+    return time.perf_counter() - t0, hist[-1], len(tr)
 
 
 def host_cpu():
@@ -163,6 +191,28 @@ def host_cpu():
     except OSError:
         pass
     return f"{os.cpu_count()} threads"
+
+
+def traffic_bytes(args):
+    """ncu dram read + write bytes per pass-1 launch of the dominant kernel, from the
+    committed capture (profiles/r2_traffic.json) unless given on the command line."""
+    if args.traffic_bytes is not None:
+        return args.traffic_bytes
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_traffic.json")) as f:
+            return json.load(f)["c4_residual_pass1"]["traffic_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def workload_config(world=1):
+    return {"workload": "BASELINE config 4 fine-level BFP residual r=b-A*x (3-D 7-point, "
+                        "511^3 interior, int32 mantissas p=24, qcomp w_tmp=29, exact int64 "
+                        "accumulation)",
+            "dof": dof(), "bytes_per_dof": BYTES_PER_DOF,
+            "l2": f"inputs above L2: {N_SETS} (x,b,r) sets of {3 * 4 * dof() / 1e9:.2f} GB "
+                  "(126 MB L2), alternated per step",
+            "parallelism": "single GPU" if world == 1 else f"z-slab x{world}"}
 
 
 def run_reference(args, world, rank):
@@ -176,33 +226,307 @@ def run_reference(args, world, rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic", "config": workload_config(),
         "cpu_baseline": {"value": v, "unit": "GDoF/s", "cores": threads, "kind": "port",
-                         "sample": f"{n} full 4095^2 residuals (oracle/bfp_oracle.c OpenMP; the GMP "
-                                   f"reference is unbuildable here)"},
+                         "sample": f"{n} full 511^3 residuals (oracle/bfp_oracle.c OpenMP; the "
+                                   "GMP reference is unbuildable here)",
+                         "host_cpu": host_cpu()},
         "e2e": {"value": v, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config():
-    return {"workload": "BASELINE config 2 fine-level BFP residual r=b-A*x (2-D 5-point, "
-                        "4095x4095 interior, int32 mantissas p=20, qcomp w_tmp=25, exact int64 "
-                        "accumulation)",
-            "dof": dof(), "bytes_per_dof": BYTES_PER_DOF,
-            "l2": f"inputs rotated over {N_SETS} (x,b,r) sets = "
-                  f"{N_SETS * 3 * dof() * 4 / 1e6:.0f} MB > 126 MB L2",
-            "parallelism": "replicas"}
-
-
 # ---------------------------------------------------------------------------
 # our arm
 
 
+def solve_bytes(trace, d, s):
+    """Algorithmic HBM bytes of a solve from its trace: per op the bytes of each operand
+    read once + the output written once: residual / Jacobi / axpby 3s,
+    first sweep 2s, restriction and FMG prolongation (1 + 2^-d)s, prolong + correct
+    (2 + 2^-d)s per fine DoF of the op's level."""
+    per = {0: 3, 1: 3, 2: 2, 3: 3, 4: 3, 5: 1 + 2.0 ** -d, 6: 2 + 2.0 ** -d, 7: 1 + 2.0 ** -d,
+           8: 3}
+    return sum(per[t[0]] * s * ((1 << t[1]) - 1) ** d for t in trace)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    torch.cuda.set_device(local)
+    import paper_2307_00124_b200 as B
+    stream = torch.cuda.current_stream()
+    B.set_stream(stream.cuda_stream)
+    Lb = B.lib()
+    sp = C.c_void_p(stream.cuda_stream)
+    n = dof()
+
+    # inputs resident in HBM: N_SETS independent (x, b, r), each set 1.6 GB (> L2)
+    xs, bs, rs, gs = [], [], [], []
+    for s in range(N_SETS):
+        x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1 + s + 100 * rank, 1)
+        b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+        r = B.BfpVec.grid(D, L_FINE, 4)
+        # gamma with the exact binade of the residual: the qcomp fast path (Table 2 regime)
+        B.residual(x, b, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 2 * L_FINE + 8), out=r)
+        gs.append(B.inf_norm_upper(r))
+        xs.append(x)
+        bs.append(b)
+        rs.append(r)
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+
+    def step(k):
+        s = k % N_SETS
+        rc = Lb.bfp_stencil_gemv(xs[s].h, bs[s].h, m1, p1, 0, P_BITS, W_TMP, gs[s].c(), 0,
+                                 rs[s].h, sp)
+        if rc:
+            raise RuntimeError(f"bfp_stencil_gemv failed: {rc}")
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    torch.cuda.synchronize()
+    l0 = B.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = B.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    # dominant-kernel time: pass 1 alone over a fixed loop of KERNEL_LAUNCHES launches (the
+    # recompute launch is skipped; valid because gamma has the exact binade, checked
+    # below), CUDA events on the launch stream around the whole loop
+    B.set_kernel_path(skip_recompute=True)
+    for k in range(4):
+        step(k)
+    torch.cuda.synchronize()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    for k in range(KERNEL_LAUNCHES):
+        step(k)
+    k1.record(stream)
+    torch.cuda.synchronize()
+    B.set_kernel_path()
+    clk = clocks.stop()
+    kern_ms = k0.elapsed_time(k1)
+    for r_ in rs:
+        assert not (r_.header().flags & B.FLAG_RECOMPUTED), "recompute needed: pass-1 timing invalid"
+    # per-launch event brackets (serialising; secondary evidence)
+    B.profile_enable(True)
+    B.profile_read(reset=True)
+    for k in range(50):
+        step(k)
+    torch.cuda.synchronize()
+    ev_ms, ev_n = B.profile_read(reset=True)
+    B.profile_enable(False)
+    value = n * args.steps / (ms / 1e3) / 1e9
+    hdr = rs[0].header()
+    assert hdr.err == 0, "device error in timed residuals"
+
+    peak, peak_kind = peaks()
+    kavg_ms = kern_ms / KERNEL_LAUNCHES
+    achieved = BYTES_PER_DOF * n / (kavg_ms / 1e3) / 1e9
+    tb = traffic_bytes(args)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": tb,
+            "kernel": "bulk3_win_kernel<QCOMP,int32,GemvOp> pass 1 (tiled-TMA plane march)",
+            "peak_kind": peak_kind, "kernel_ms": kavg_ms,
+            "kernel_ms_event_brackets": ev_ms / max(ev_n, 1),
+            "timing": f"pass 1 back to back, {KERNEL_LAUNCHES} launches (fixed, independent of "
+                      "--steps), recompute skipped (flags verified clear), CUDA events on the "
+                      "launch stream around the loop",
+            "algorithmic_bytes_per_launch": BYTES_PER_DOF * n,
+            "traffic_source": "profiles/r2_traffic.json (ncu --set full, same kernel)"}
+    del xs, bs, rs
+    clean(torch)
+
+    e2e = run_e2e(args, B, Lb, torch, stream, sp, D, L_FINE, P_BITS)
+    clean(torch)
+
+    line = {
+        "metric": "bfp_stencil_residual_gdofs", "value": value, "unit": "GDoF/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": workload_config(),
+        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+    }
+    if not args.no_extras:
+        # kernel-level numbers first, each section from a clean allocator state
+        line["residual_other_configs"] = {
+            "C2_2d_4095^2_int32_p20": measure_residual(B, torch, stream, 2, 12, 20, 4, steps=100),
+            "C1_1d_2^20_int32_p16": measure_residual(B, torch, stream, 1, 20, 16, 4, steps=200),
+            # SURVEY 8(d): config 1 is L2-resident; the %HBM claim for 1-D needs n beyond L2
+            "C1_1d_2^28_int32_p16_probe": measure_residual(B, torch, stream, 1, 28, 16, 4,
+                                                           steps=20),
+            "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=20),
+        }
+        clean(torch)
+        line["fine_level_ops"] = {"C4": measure_ops(B, torch, stream, 3, 9, 24),
+                                  "C2": measure_ops(B, torch, stream, 2, 12, 20),
+                                  "C5": measure_ops(B, torch, stream, 3, 10, 48, steps=10, s=8)}
+        clean(torch)
+        line["solves"] = run_solves(B, torch, stream)
+        ttd = {k: v for k, v in line["solves"].items()
+               if v.get("accuracy", {}).get("alg_over_disc", 1e30) <= 1.0}
+        if ttd:
+            k = min(ttd, key=lambda k: ttd[k]["ms"])
+            line["fmg_time_to_disc_accuracy"] = {
+                "config": k, "ms": ttd[k]["ms"],
+                "alg_over_disc": ttd[k]["accuracy"]["alg_over_disc"],
+                "note": "max-norm error vs the discrete solution <= the discretisation error"}
+        clean(torch)
+        line["C5_precision_sweep_1gpu"] = run_c5_sweep(B, torch, stream)
+    if not args.no_cpu:
+        sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
+        sec1, _, nrun1 = cpu_residual_time(10**9, 0, budget_s=args.cpu_budget / 2, threads=1)
+        cb = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads, "kind": "port",
+              "sample": f"{nrun} full 511^3 residuals in ~{args.cpu_budget:.0f} s "
+                        "(oracle/bfp_oracle.c, OpenMP)",
+              "single_thread": {"value": n / sec1 / 1e9, "cores": 1,
+                                "sample": f"{nrun1} full 511^3 residuals, one thread (the "
+                                          "reference's loops are sequential)"},
+              "host_cpu": host_cpu()}
+        if not args.no_cpu_fmg:
+            name = line.get("fmg_time_to_disc_accuracy", {}).get("config", "C4_3d_fmg_v21_n2")
+            t, fres, nops = cpu_fmg_time(name)
+            cb["fmg_solve"] = {"config": name, "s": t, "cores": threads, "ops": nops,
+                               "final_residual": fres,
+                               "sample": "one full solve (oracle mg_run, OpenMP)"}
+        line["cpu_baseline"] = cb
+    line["summary"] = summary(line)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def summary(line):
+    """The numbers a reader needs, compact, as the LAST key of the line."""
+    r = lambda v, k=3: None if v is None else round(v, k)  # noqa: E731
+    s = {"C4_residual": {"gdofs": r(line["value"], 1), "hbm_frac": r(line["roofline"]["frac"]),
+                         "e2e_gdofs": r(line["e2e"]["value"], 2)}}
+    for k, v in line.get("residual_other_configs", {}).items():
+        if "hbm_frac" in v:
+            s[k.split("_")[0] + ("_probe" if "probe" in k else "")] = r(v["hbm_frac"])
+    ops = line.get("fine_level_ops", {})
+    for c in ("C4", "C2", "C5"):
+        if c in ops:
+            s[c + "_ops_frac"] = {k: r(v["hbm_frac"], 2) for k, v in ops[c]["ops"].items()}
+    sol = line.get("solves", {})
+    s["solves_ms"] = {k.split("_")[0] + k[k.find("_fmg"):] if "_fmg" in k else k.split("_")[0]:
+                      [r(v.get("ms"), 2), r(v.get("hbm_frac"), 2)]
+                      for k, v in sol.items() if "ms" in v}
+    t = line.get("fmg_time_to_disc_accuracy")
+    cb = line.get("cpu_baseline", {})
+    if t:
+        s["fmg_to_disc"] = {"gpu_ms": r(t["ms"], 2), "cfg": t["config"]}
+        if "fmg_solve" in cb:
+            s["fmg_to_disc"]["cpu_s"] = r(cb["fmg_solve"]["s"], 2)
+            s["fmg_to_disc"]["cpu_cores"] = cb["fmg_solve"]["cores"]
+    c5 = line.get("C5_precision_sweep_1gpu", {})
+    if c5:
+        s["C5_sweep_ms"] = {k: r(v.get("ms"), 1) for k, v in c5.items()}
+    if cb:
+        s["cpu_residual_gdofs"] = r(cb.get("value"))
+    return s
+
+
+def run_e2e(args, B, Lb, torch, stream, sp, d, l, p):
+    """Same metric through the C-ABI with pinned HOST buffers, pipelined across steps:
+    stream A[k%2] uploads x, b (pitched DMA into the padded layout + header scan) and runs
+    the residual into buffer k%2; stream B downloads r of step k (gather + D2H engine)
+    while A[(k+1)%2] uploads step k+1 (H2D engine).  `pcie_h2d_gbs`: one step's H2D bytes
+    copied alone (the bound of this arm)."""
+    n = dof(d, l)
+    x = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 1, 1)
+    b = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
+    hx = torch.empty(n, dtype=torch.int32).pin_memory()
+    hb = torch.empty(n, dtype=torch.int32).pin_memory()
+    hr = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(2)]
+    hh = B._Header()
+    for src, dst in ((x, hx), (b, hb)):
+        assert Lb.bfp_vec_download_i32(src.h, C.c_void_p(dst.data_ptr()), C.byref(hh), sp) == 0
+    qx, ex = x.q, x.e
+    qb, eb = b.q, b.e
+    del x, b
+    xd = [B.BfpVec.grid(d, l, 4) for _ in range(2)]
+    bd = [B.BfpVec.grid(d, l, 4) for _ in range(2)]
+    rd = [B.BfpVec.grid(d, l, 4) for _ in range(2)]
+    Lb.bfp_vec_upload_i32(xd[0].h, C.c_void_p(hx.data_ptr()), qx, ex, sp)
+    Lb.bfp_vec_upload_i32(bd[0].h, C.c_void_p(hb.data_ptr()), qb, eb, sp)
+    B.residual(xd[0], bd[0], p, p + 5, B.Scalar(1 << 14, 16, 2 * l + 8), out=rd[0])
+    g = B.inf_norm_upper(rd[0]).c()
+    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
+    sas = [stream, torch.cuda.Stream()]
+    sa = stream
+    sb = torch.cuda.Stream()
+    pas = [C.c_void_p(s_.cuda_stream) for s_ in sas]
+    pb = C.c_void_p(sb.cuda_stream)
+    ev_r = [torch.cuda.Event() for _ in range(2)]
+    ev_d = [torch.cuda.Event() for _ in range(2)]
+    for e in ev_d:
+        e.record(sb)
+
+    def step(k):
+        i = k & 1
+        sa, pa = sas[i], pas[i]
+        sa.wait_event(ev_d[i])  # download of step k-2 finished with rd[i]
+        assert Lb.bfp_vec_upload_i32(xd[i].h, C.c_void_p(hx.data_ptr()), qx, ex, pa) == 0
+        assert Lb.bfp_vec_upload_i32(bd[i].h, C.c_void_p(hb.data_ptr()), qb, eb, pa) == 0
+        assert Lb.bfp_stencil_gemv(xd[i].h, bd[i].h, m1, p1, 0, p, p + 5, g, 0, rd[i].h,
+                                   pa) == 0
+        ev_r[i].record(sa)
+        sb.wait_event(ev_r[i])
+        assert Lb.bfp_vec_download_async_i32(rd[i].h, C.c_void_p(hr[i].data_ptr()), pb) == 0
+        ev_d[i].record(sb)
+
+    k = max(3, min(args.steps, 20))
+    for j in range(2):
+        step(j)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(sa)
+    sas[1].wait_stream(sa)
+    for j in range(k):
+        step(j)
+    sa.wait_stream(sb)
+    sa.wait_stream(sas[1])
+    e1.record(sa)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    # the PCIe bound: one step's H2D bytes (x and b) alone, pinned, same engine
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dx = torch.empty(n, dtype=torch.int32, device="cuda")
+    db = torch.empty(n, dtype=torch.int32, device="cuda")
+    with torch.cuda.stream(sa):
+        for _ in range(2):
+            dx.copy_(hx, non_blocking=True)
+        h0.record(sa)
+        for _ in range(3):
+            dx.copy_(hx, non_blocking=True)
+            db.copy_(hb, non_blocking=True)
+        h1.record(sa)
+    torch.cuda.synchronize()
+    h2d_gbs = 3 * 2 * 4 * n / (h0.elapsed_time(h1) / 1e3) / 1e9
+    h = rd[(k - 1) & 1].header()
+    assert h.err == 0
+    return {"value": n * k / (ms / 1e3) / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": 2 * 4 * n,
+            "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
+            "pcie_h2d_gbs": h2d_gbs, "pcie_bound_frac": 2 * 4 * n / (ms / k / 1e3) / 1e9 / h2d_gbs,
+            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (streams A0/A1 by step parity) | "
+                    "bfp_vec_download_async_i32 (stream B), pinned host, double-buffered"}
+
+
 def run_sharded(args, world, rank, local):
-    """N GPUs: the C2 residual z-slab sharded over the ranks (strong scaling) through the
-    native sharded op (bfp_dist_stencil_gemv: NCCL halo exchange of one row per
-    neighbour, partial windows, MAX all-reduces, finalize -- all enqueued on the stream),
-    one CUDA graph per step.  --sharded forces this path at N = 1."""
+    """N GPUs: config 4's fine-level residual z-slab sharded over the ranks (strong
+    scaling: the 511^3 grid is fixed, each rank owns 512/N planes) through the native
+    sharded op (bfp_dist_stencil_gemv: NCCL halo exchange of one plane per neighbour,
+    partial windows, MAX all-reduces, finalize -- all enqueued on the stream, no host
+    synchronisation).  Two slab sets alternate per step (per-rank bytes stay above the
+    L2 at every N <= 8).  The line also carries the sharded config-4 FMG solve (the
+    metric's second half) and config 5's precision sweep on 1023^3 z-slabs.
+    --sharded forces this path at N = 1."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -216,143 +540,184 @@ def run_sharded(args, world, rank, local):
     stream = torch.cuda.current_stream()
     B.set_stream(stream.cuda_stream)
     n = dof()
-    lo, hi = Dm.slab_ranges(L_FINE, world)[rank]
     nn_ = (1 << L_FINE) - 1
-    gx = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
-    gb = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
-    g = B.inf_norm_upper(B.residual(gx, gb, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40)).z)
+    per = nn_ * nn_
+    lo, hi = Dm.slab_ranges(L_FINE, world)[rank]
     idt = torch.zeros(B.NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
     if rank == 0:
         idt.copy_(torch.frombuffer(bytearray(B.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(idt, 0)
     ops = B.DistOps(world, rank, bytes(idt.cpu().numpy().tobytes()))
 
-    def slab_of(full):
-        m, q, e = full.download()
-        v = B.BfpVec.slab(D, L_FINE, lo, hi)
-        v.upload(m[lo * nn_: min(hi, nn_) * nn_], q, e)
-        return v
-    xs, bs = slab_of(gx), slab_of(gb)
-    outs = [B.BfpVec.slab(D, L_FINE, lo, hi) for _ in range(2)]
+    sets = []
+    for s in range(N_SETS):
+        gx = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1 + s, 1)
+        gb = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+        g = B.inf_norm_upper(B.residual(gx, gb, P_BITS, W_TMP,
+                                        B.Scalar(1 << 14, 16, 2 * L_FINE + 8)).z)
+
+        def slab_of(full):
+            m, q, e = full.download()
+            v = B.BfpVec.slab(D, L_FINE, lo, hi)
+            v.upload(m[lo * per: min(hi, nn_) * per], q, e)
+            return v
+        sets.append((slab_of(gx), slab_of(gb), B.BfpVec.slab(D, L_FINE, lo, hi), g))
+        if s == 0:
+            ref0 = B.residual(gx, gb, P_BITS, W_TMP, g).z.download()
+        del gx, gb
+    clean(torch)
     m1, p1 = B.bfp_minus_one(), B.bfp_one()
 
     def step(k):
-        ops.gemv([xs], [bs], m1, p1, P_BITS, W_TMP, g, [outs[k & 1]])
+        xs, bs, rr, g = sets[k % N_SETS]
+        ops.gemv([xs], [bs], m1, p1, P_BITS, W_TMP, g, [rr])
 
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
-    c0 = B.launch_count()
-    step(0)
-    per_step = B.launch_count() - c0  # our kernels per sharded residual (NCCL ops excluded)
-    torch.cuda.synchronize()
-    # one CUDA graph per output buffer (kernels + NCCL captured on the side stream)
-    graphs, graph_err = [], None
-    try:
-        cs = torch.cuda.Stream()
-        for k in range(2):
-            gr = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gr, stream=cs, capture_error_mode="thread_local"):
-                B.set_stream(cs.cuda_stream)
-                step(k)
-            graphs.append(gr)
-        B.set_stream(stream.cuda_stream)
-    except Exception as ex:  # noqa: BLE001 -- report and time stream-ordered
-        B.set_stream(stream.cuda_stream)
-        graphs, graph_err = [], str(ex)
-    for k in range(args.warmup):
-        graphs[k & 1].replay() if graphs else step(k)
-    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
     dist.barrier()
     torch.cuda.synchronize()
     l0 = B.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for k in range(args.steps):
-        graphs[k & 1].replay() if graphs else step(k)
+        step(k)
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
+    clk = clocks.stop()
     launches = B.launch_count() - l0
-    if graphs:  # kernels per captured step (the replays do not pass through the library)
-        launches = per_step * args.steps
     ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    # parity of the sharded result with the unsharded residual on this rank's planes
-    ref = B.residual(gx, gb, P_BITS, W_TMP, g)
-    mr, _, er = ref.z.download()
-    mo, _, eo = outs[(args.steps - 1) & 1].download()
-    ok = eo == er and np.array_equal(mo, mr[lo * nn_: min(hi, nn_) * nn_])
+    # parity of set 0's sharded residual with the unsharded one on this rank's planes
+    step(0)
+    mo, _, eo = sets[0][2].download()
+    mr, _, er = ref0
+    ok = eo == er and np.array_equal(mo, mr[lo * per: min(hi, nn_) * per])
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    peak, peak_kind = peaks()
+    achieved = BYTES_PER_DOF * n / world / (ms / args.steps / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+            "timing": "per-GPU share of the algorithmic bytes over the whole sharded step "
+                      "(halo + pass 1 + all-reduces + finalize), max over ranks"}
+    e2e = sharded_e2e(B, torch, dist, stream, ops, world, rank, lo, hi, args)
+    del sets
+    clean(torch)
     solve = {} if args.no_extras else sharded_solve(B, torch, dist, stream, world, rank)
-    c4 = {} if args.no_extras else sharded_residual_c4(B, torch, dist, stream, world, rank, ops)
+    clean(torch)
+    c5 = {} if args.no_extras else sharded_c5_sweep(B, torch, dist, stream, world, rank)
     line = {
         "metric": "bfp_stencil_residual_gdofs", "value": n * args.steps / (ms / 1e3) / 1e9,
         "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": dict(workload_config(), parallelism=f"z-slab x{world} (NCCL halo + MAX allreduce)",
-                       l2=f"one (x, b) set + 2 outputs, {12 * n / world / 1e6:.0f} MB per rank "
-                          "(fits the 126 MB L2 from N = 2 on: strong scaling gains L2 reuse)"),
-        "gpu_launches": int(launches), "cuda_graph": bool(graphs), "graph_error": graph_err,
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": dict(workload_config(world),
+                       parallelism=f"z-slab x{world} (NCCL halo + MAX allreduce)"),
+        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
         "sharded_parity_with_unsharded": bool(okt.item()),
-        "sharded_solve": solve,
-        "sharded_residual_C4": c4,
+        "sharded_solve_C4": solve, "C5_precision_sweep_sharded": c5,
     }
+    if rank == 0 and not args.no_cpu:
+        sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads,
+                                "kind": "port", "host_cpu": host_cpu(),
+                                "sample": f"{nrun} full 511^3 residuals (oracle, OpenMP)"}
     dist.barrier()
     del ops
     dist.destroy_process_group()
     if rank == 0:
+        line["summary"] = {"C4_residual_gdofs": round(line["value"], 1),
+                           "per_gpu_hbm_frac": round(roof["frac"], 3),
+                           "e2e_gdofs": round(e2e.get("value", 0.0), 2),
+                           "C4_fmg_ms": solve.get("ms"),
+                           "C5_sweep_ms": {k: v.get("ms") for k, v in c5.items()}}
         print(json.dumps(line), flush=True)
     return 0
 
 
-def sharded_residual_c4(B, torch, dist, stream, world, rank, ops, steps=10):
-    """The C4 fine-level residual (511^3, int32 p=24) z-slab sharded over the ranks
-    (strong scaling, native sharded op, stream-ordered): per-step device time, max
-    over ranks, and parity of this rank's slab with the unsharded residual."""
+def sharded_e2e(B, torch, dist, stream, ops, world, rank, lo, hi, args):
+    """The sharded residual through the C-ABI with pinned HOST buffers: every step each
+    rank uploads its x and b slabs and downloads its r slab; max over ranks."""
     import numpy as np
-    from paper_2307_00124_b200 import dist as Dm
-    d, l, p = 3, 9, 24
-    out = {"config": "C4 fine level 511^3 int32 p=24"}
+    nn_ = (1 << L_FINE) - 1
+    per = nn_ * nn_
     try:
-        lo, hi = Dm.slab_ranges(l, world)[rank]
-        n = (1 << l) - 1
-        gx = B.gen_uniform(B.BfpVec.grid(d, l, 4), p, 1, 1)
-        gb = B.gen_sine(B.BfpVec.grid(d, l, 4), p)
-        g = B.inf_norm_upper(B.residual(gx, gb, p, p + 5, B.Scalar(1 << 14, 16, 30)).z)
-
-        def slab_of(full):
-            m, q, e = full.download()
-            v = B.BfpVec.slab(d, l, lo, hi)
-            v.upload(m[lo * n * n: min(hi, n) * n * n], q, e)
-            return v
-        xs, bs = slab_of(gx), slab_of(gb)
-        r = B.BfpVec.slab(d, l, lo, hi)
+        gx = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
+        gb = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
+        g = B.inf_norm_upper(B.residual(gx, gb, P_BITS, W_TMP,
+                                        B.Scalar(1 << 14, 16, 2 * L_FINE + 8)).z)
+        (mx_, qx, ex), (mb_, qb, eb) = gx.download(), gb.download()
+        del gx, gb
+        sl = slice(lo * per, min(hi, nn_) * per)
+        hx = np.ascontiguousarray(mx_[sl])
+        hb = np.ascontiguousarray(mb_[sl])
+        xs, bs, rr = (B.BfpVec.slab(D, L_FINE, lo, hi) for _ in range(3))
         m1, p1 = B.bfp_minus_one(), B.bfp_one()
-        for _ in range(3):
-            ops.gemv([xs], [bs], m1, p1, p, p + 5, g, [r])
+
+        def step():
+            xs.upload(hx, qx, ex)
+            bs.upload(hb, qb, eb)
+            ops.gemv([xs], [bs], m1, p1, P_BITS, W_TMP, g, [rr])
+            return rr.download()
+        step()
+        k = max(3, min(args.steps, 10))
         torch.cuda.synchronize()
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            ops.gemv([xs], [bs], m1, p1, p, p + 5, g, [r])
-        e1.record(stream)
+        t0 = time.perf_counter()
+        for _ in range(k):
+            step()
         torch.cuda.synchronize()
-        ms = torch.tensor([e0.elapsed_time(e1) / steps], device="cuda", dtype=torch.float64)
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-        mr, _, er = B.residual(gx, gb, p, p + 5, g).z.download()
-        mo, _, eo = r.download()
-        ok = eo == er and np.array_equal(mo, mr[lo * n * n: min(hi, n) * n * n])
-        okt = torch.tensor([1 if ok else 0], device="cuda")
-        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
-        out.update(ms=float(ms.item()), gdofs=n ** 3 / (float(ms.item()) / 1e3) / 1e9,
-                   parity_with_unsharded=bool(okt.item()))
+        t = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item()) / k
+        nloc = hx.size
+        return {"value": dof() / sec / 1e9, "unit": "GDoF/s",
+                "h2d_bytes_per_step": 2 * 8 * nloc, "d2h_bytes_per_step": 8 * nloc,
+                "steps": k, "ms_per_step": sec * 1e3,
+                "path": "per rank: bfp_vec_upload (int64 host) x2 + bfp_dist_stencil_gemv + "
+                        "bfp_vec_download; host wall clock, max over ranks"}
     except Exception as ex:  # noqa: BLE001 -- report, never hide
-        out["error"] = str(ex)
+        return {"error": str(ex)}
+
+
+def sharded_c5_sweep(B, torch, dist, stream, world, rank, ps=(4, 8, 16, 32, 48)):
+    """Config 5 on the N ranks: 1023^3 z-slabs, x0 uniform, b = 0, 10 IR-V(2,2) per p
+    (native sharded solver, one CUDA graph per solve); device time, max over ranks."""
+    out = {}
+    idt = torch.zeros(B.NCCL_ID_BYTES, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(B.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    nid = bytes(idt.cpu().numpy().tobytes())
+    for p in ps:
+        try:
+            cfg = B.mg_config(d=3, l_fine=10, cycles=10, x0_random=True, rhs_kind=2, p=p)
+            mg = B.Multigrid(cfg, world=world, rank=rank, nccl_id=nid, min_planes=16)
+            mg.solve(use_graph=False)
+            torch.cuda.synchronize()
+            mg.solve(use_graph=True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mg.solve(use_graph=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = torch.tensor([e0.elapsed_time(e1)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
+            out[f"p{p}"] = {"ms": float(ms.item()), "final_residual": hist[-1],
+                            "first_residual": hist[0]}
+            del mg
+            clean(torch)
+        except Exception as ex:  # noqa: BLE001 -- report, never hide
+            out[f"p{p}"] = {"error": str(ex)}
     return out
 
 
@@ -409,248 +774,6 @@ def sharded_solve(B, torch, dist, stream, world, rank, name="C4_3d_fmg", min_pla
         out["error"] = str(ex)
     return out
 
-
-def run_ours(args, world, rank, local):
-    import torch
-    torch.cuda.set_device(local)
-    import paper_2307_00124_b200 as B
-    stream = torch.cuda.current_stream()
-    B.set_stream(stream.cuda_stream)
-    Lb = B.lib()
-    sp = C.c_void_p(stream.cuda_stream)
-    n = dof()
-
-    # inputs resident in HBM: N_SETS independent (x, b, r)
-    xs, bs, rs, gs = [], [], [], []
-    for s in range(N_SETS):
-        x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1 + s + 100 * rank, 1)
-        b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
-        r = B.BfpVec.grid(D, L_FINE, 4)
-        # gamma with the exact binade of the residual: the qcomp fast path (Table 2 regime)
-        B.residual(x, b, P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=r)
-        gs.append(B.inf_norm_upper(r))
-        xs.append(x)
-        bs.append(b)
-        rs.append(r)
-    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
-
-    def step(k):
-        s = k % N_SETS
-        rc = Lb.bfp_stencil_gemv(xs[s].h, bs[s].h, m1, p1, 0, P_BITS, W_TMP, gs[s].c(), 0,
-                                 rs[s].h, sp)
-        if rc:
-            raise RuntimeError(f"bfp_stencil_gemv failed: {rc}")
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-
-    for k in range(args.warmup):
-        step(k)
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.2)
-    barrier()
-    torch.cuda.synchronize()
-    l0 = B.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for k in range(args.steps):
-        step(k)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    launches = B.launch_count() - l0
-    ms = e0.elapsed_time(e1)
-    clk = clocks.stop()
-    # dominant-kernel time: pass 1 alone, launched back to back (the recompute launch
-    # is skipped; valid because gamma has the exact binade, checked below), timed
-    # with CUDA events on the launch stream over the whole loop
-    B.set_kernel_path(skip_recompute=True)
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for k in range(args.steps):
-        step(k)
-    k1.record(stream)
-    torch.cuda.synchronize()
-    B.set_kernel_path()
-    kern_ms, kern_n = k0.elapsed_time(k1), args.steps
-    for r_ in rs:
-        assert not (r_.header().flags & B.FLAG_RECOMPUTED), "recompute needed: pass-1 timing invalid"
-    # per-launch event brackets (serialising; secondary evidence)
-    B.profile_enable(True)
-    B.profile_read(reset=True)
-    for k in range(min(args.steps, 50)):
-        step(k)
-    torch.cuda.synchronize()
-    ev_ms, ev_n = B.profile_read(reset=True)
-    B.profile_enable(False)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * n * args.steps / (ms / 1e3) / 1e9
-
-    # correctness probe of the timed work: flags must be the fast path, no device error
-    hdr = rs[0].header()
-    assert hdr.err == 0, "device error in timed residuals"
-
-    peak, peak_kind = peaks()
-    kavg_ms = kern_ms / max(kern_n, 1)
-    achieved = BYTES_PER_DOF * n / (kavg_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic_bytes(args),
-            "kernel": "bulk_win_kernel<QCOMP,GemvOp> pass 1 (TMA-bulk smem pipeline)",
-            "peak_kind": peak_kind, "kernel_ms": kavg_ms,
-            "kernel_ms_event_brackets": ev_ms / max(ev_n, 1),
-            "timing": "pass 1 back-to-back over the timed steps (recompute skipped, flags "
-                      "verified clear), CUDA events on the launch stream",
-            "algorithmic_bytes_per_launch": BYTES_PER_DOF * n}
-
-    # e2e through the C-ABI with pinned host buffers
-    e2e = run_e2e(args, B, Lb, torch, stream, sp)
-
-    line = {
-        "metric": "bfp_stencil_residual_gdofs", "value": value, "unit": "GDoF/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic", "config": workload_config(),
-        "roofline": roof, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-    }
-    if rank == 0 and not args.no_extras:
-        # kernel-level numbers first, each section from a clean allocator state (measured
-        # after the solves, the C2/C4 kernels ran 3-9% slower in one process)
-        line["residual_other_configs"] = {
-            "C4_3d_511^3_int32_p24": measure_residual(B, torch, stream, 3, 9, 24, 4),
-            "C1_1d_2^20_int32_p16": measure_residual(B, torch, stream, 1, 20, 16, 4, steps=200),
-            # config 1 is L2-resident; the %HBM claim for 1-D needs n beyond L2
-            "C1_1d_2^28_int32_p16_probe": measure_residual(B, torch, stream, 1, 28, 16, 4,
-                                                           steps=10),
-            "C5_3d_1023^3_int64_p48": measure_residual(B, torch, stream, 3, 10, 48, 8, steps=5),
-        }
-        clean(torch)
-        line["fine_level_ops"] = {"C2": measure_ops(B, torch, stream, 2, 12, 20),
-                                  "C4": measure_ops(B, torch, stream, 3, 9, 24),
-                                  "C5": measure_ops(B, torch, stream, 3, 10, 48, steps=5, s=8)}
-        clean(torch)
-        line["solves"] = run_solves(B, torch, stream)
-        ttd = {k: v for k, v in line["solves"].items()
-               if v.get("accuracy", {}).get("alg_over_disc", 1e30) <= 1.0}
-        if ttd:
-            k = min(ttd, key=lambda k: ttd[k]["ms"])
-            line["fmg_time_to_disc_accuracy"] = {
-                "config": k, "ms": ttd[k]["ms"], "alg_over_disc": ttd[k]["accuracy"]["alg_over_disc"],
-                "note": "max-norm error vs the discrete solution <= the discretisation error"}
-        clean(torch)
-        line["C5_precision_sweep_1gpu"] = run_c5_sweep(B, torch, stream)
-    if rank == 0 and not args.no_cpu:
-        sec, threads, nrun = cpu_residual_time(10**9, 1, budget_s=args.cpu_budget)
-        sec1, _, nrun1 = cpu_residual_time(10**9, 0, budget_s=args.cpu_budget / 2, threads=1)
-        line["cpu_baseline"] = {"value": n / sec / 1e9, "unit": "GDoF/s", "cores": threads,
-                                "kind": "port",
-                                "sample": f"{nrun} full 4095^2 residuals in ~{args.cpu_budget:.0f} s "
-                                          f"(oracle/bfp_oracle.c, OpenMP)",
-                                "single_thread": {"value": n / sec1 / 1e9, "cores": 1,
-                                                  "sample": f"{nrun1} full 4095^2 residuals, one "
-                                                            "thread (the reference's loops are "
-                                                            "sequential)"},
-                                "host_cpu": host_cpu()}
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-        dist.destroy_process_group()
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    return 0
-
-
-def run_e2e(args, B, Lb, torch, stream, sp):
-    """Same metric through the C-ABI with pinned HOST buffers, pipelined across steps:
-    stream A[k%2] uploads x, b and runs the residual into buffer k%2; stream B downloads
-    r of step k (D2H engine) while A[(k+1)%2] uploads step k+1 (H2D engine). Two upload
-    streams keep the H2D engine busy through step k's scatter and residual kernels.
-    `pcie_h2d_gbs`: one step's H2D bytes copied alone (the bound of this arm)."""
-    n = dof()
-    x = B.gen_uniform(B.BfpVec.grid(D, L_FINE, 4), P_BITS, 1, 1)
-    b = B.gen_sine(B.BfpVec.grid(D, L_FINE, 4), P_BITS)
-    hx = torch.empty(n, dtype=torch.int32).pin_memory()
-    hb = torch.empty(n, dtype=torch.int32).pin_memory()
-    hr = [torch.empty(n, dtype=torch.int32).pin_memory() for _ in range(2)]
-    hh = B._Header()
-    for src, dst in ((x, hx), (b, hb)):
-        assert Lb.bfp_vec_download_i32(src.h, C.c_void_p(dst.data_ptr()), C.byref(hh), sp) == 0
-    qx, ex = x.q, x.e
-    qb, eb = b.q, b.e
-    xd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
-    bd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
-    rd = [B.BfpVec.grid(D, L_FINE, 4) for _ in range(2)]
-    Lb.bfp_vec_upload_i32(xd[0].h, C.c_void_p(hx.data_ptr()), qx, ex, sp)
-    Lb.bfp_vec_upload_i32(bd[0].h, C.c_void_p(hb.data_ptr()), qb, eb, sp)
-    B.residual(xd[0], bd[0], P_BITS, W_TMP, B.Scalar(1 << 14, 16, 40), out=rd[0])
-    g = B.inf_norm_upper(rd[0]).c()
-    m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
-    sas = [stream, torch.cuda.Stream()]
-    sa = stream
-    sb = torch.cuda.Stream()
-    pas = [C.c_void_p(s_.cuda_stream) for s_ in sas]
-    pb = C.c_void_p(sb.cuda_stream)
-    ev_r = [torch.cuda.Event() for _ in range(2)]
-    ev_d = [torch.cuda.Event() for _ in range(2)]
-    for e in ev_d:
-        e.record(sb)
-
-    def step(k):
-        i = k & 1
-        sa, pa = sas[i], pas[i]
-        sa.wait_event(ev_d[i])  # download of step k-2 finished with rd[i]
-        assert Lb.bfp_vec_upload_i32(xd[i].h, C.c_void_p(hx.data_ptr()), qx, ex, pa) == 0
-        assert Lb.bfp_vec_upload_i32(bd[i].h, C.c_void_p(hb.data_ptr()), qb, eb, pa) == 0
-        assert Lb.bfp_stencil_gemv(xd[i].h, bd[i].h, m1, p1, 0, P_BITS, W_TMP, g, 0, rd[i].h,
-                                   pa) == 0
-        ev_r[i].record(sa)
-        sb.wait_event(ev_r[i])
-        assert Lb.bfp_vec_download_async_i32(rd[i].h, C.c_void_p(hr[i].data_ptr()), pb) == 0
-        ev_d[i].record(sb)
-
-    k = max(3, min(args.steps, 20))
-    for j in range(2):
-        step(j)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(sa)
-    sas[1].wait_stream(sa)
-    for j in range(k):
-        step(j)
-    sa.wait_stream(sb)
-    sa.wait_stream(sas[1])
-    e1.record(sa)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    # the PCIe bound: one step's H2D bytes (x and b) alone, pinned, same engine
-    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    dx, db = torch.empty(n, dtype=torch.int32, device="cuda"), torch.empty(n, dtype=torch.int32, device="cuda")
-    with torch.cuda.stream(sa):
-        for _ in range(2):
-            dx.copy_(hx, non_blocking=True)
-        h0.record(sa)
-        for _ in range(5):
-            dx.copy_(hx, non_blocking=True)
-            db.copy_(hb, non_blocking=True)
-        h1.record(sa)
-    torch.cuda.synchronize()
-    h2d_gbs = 5 * 2 * 4 * n / (h0.elapsed_time(h1) / 1e3) / 1e9
-    # the downloaded mantissas are the residual (fast path: exponent from the header)
-    h = rd[(k - 1) & 1].header()
-    assert h.err == 0
-    return {"value": n * k / (ms / 1e3) / 1e9, "unit": "GDoF/s", "h2d_bytes_per_step": 2 * 4 * n,
-            "d2h_bytes_per_step": 4 * n, "steps": k, "ms_per_step": ms / k,
-            "pcie_h2d_gbs": h2d_gbs, "pcie_bound_frac": 2 * 4 * n / (ms / k / 1e3) / 1e9 / h2d_gbs,
-            "path": "bfp_vec_upload_i32 x2 + bfp_stencil_gemv (streams A0/A1 by step parity) | "
-                    "bfp_vec_download_async_i32 (stream B), pinned host, double-buffered"}
 
 
 def measure_residual(B, torch, stream, d, l, p, mb, steps=30):
@@ -806,6 +929,20 @@ def sine_accuracy(d, l, m, e):
             "alg_over_disc": err_h / disc}
 
 
+def solve_ebytes(kw, p):
+    """Mantissa storage of a solve (bfp_solver.cu build()): int32 when every width plus the
+    capped w_add fits 32 bits."""
+    lv = lambda v: v if isinstance(v, list) else [v] * 32  # noqa: E731
+    P, PD, PC = lv(p), lv(kw.get("pd") or 0), lv(kw.get("pc") or 0)
+    cap = kw.get("w_add_cap", -1)
+    cap = min(cap, 6) if cap >= 0 else 6
+    m = 0
+    for l in range(kw.get("l_coarse", 2), kw["l_fine"] + 1):
+        wd = PD[l] or P[l]
+        m = max(m, max(wd, P[l]) + cap, PC[l] or P[l])
+    return 4 if m <= 32 else 8
+
+
 def run_solves(B, torch, stream):
     out = {}
     for name, kw in SOLVES.items():
@@ -825,8 +962,11 @@ def run_solves(B, torch, stream):
             ms = e0.elapsed_time(e1) / reps
             x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
             rec = sum(t[8] for t in tr)
+            nbytes = solve_bytes(tr, kw["d"], solve_ebytes(kw, p))
             out[name] = {"ms": ms, "launches": mg.launches(), "final_residual": hist[-1],
-                         "first_residual": hist[0], "recomputes": rec, "ops": len(tr)}
+                         "first_residual": hist[0], "recomputes": rec, "ops": len(tr),
+                         "alg_bytes": nbytes,
+                         "hbm_frac": nbytes / (ms / 1e3) / 1e9 / peaks()[0]}
             if kw.get("rhs_kind") == 1:
                 out[name]["accuracy"] = sine_accuracy(kw["d"], kw["l_fine"], x, e)
             del mg
@@ -858,8 +998,11 @@ def run_c5_sweep(B, torch, stream, ps=(4, 8, 16, 32, 48)):
             torch.cuda.synchronize()
             x, q, e, hist, tr = mg.result(trace_cap=1 << 16)
             rate = (hist[-1] / hist[0]) ** (1.0 / (len(hist) - 1)) if hist[0] > 0 else None
+            kw5 = dict(d=3, l_fine=10, **extra)
+            nbytes = solve_bytes(tr, 3, solve_ebytes(kw5, p))
             out[name] = {"ms": e0.elapsed_time(e1),
-                         "mant_bytes": 4 if max(p, pd or 0) + (4 if pd else 6) <= 32 else 8,
+                         "hbm_frac": nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9 / peaks()[0],
+                         "mant_bytes": solve_ebytes(kw5, p),
                          "first_residual": hist[0], "final_residual": hist[-1],
                          "reduction_per_cycle": rate,
                          "recomputes": sum(t[8] for t in tr), "ops": len(tr)}
@@ -872,11 +1015,12 @@ def run_c5_sweep(B, torch, stream, ps=(4, 8, 16, 32, 48)):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-fmg", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-rank (z-slab) path even on one GPU")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
@@ -885,7 +1029,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    world, rank, local = dist_setup(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    world, rank, local = dist_setup()
     if args.impl == "reference":
         return run_reference(args, world, rank)
     if world > 1 or args.sharded:

@@ -91,8 +91,23 @@ int bfp_quantize(bfp_vec_t x, int64_t w, bfp_vec_t out, void* stream);
 /* synchronous: scalar (m, q, e) >= max|x| rounded up to q_gamma bits */
 int bfp_inf_norm_upper(bfp_vec_t x, int64_t q_gamma, int64_t* m, int64_t* q, int64_t* e,
                        void* stream);
-/* exact dot product sum_i m_x m_y as a 128-bit integer (hi, lo) at exponent e_x + e_y */
+/* ---- exact dot product <x, y> = sum_i m_x,i m_y,i 2^(e_x + e_y) (no
+ * reference function).  Accumulated exactly in 192 bits on the device; the device result
+ * is int64 acc[5] = {L0, L1, L2, L3, e} with value sum_k L_k 2^(48 k) (limb sums, not
+ * carried), e = e_x + e_y.
+ *   bfp_dot_exact_async  stream-ordered into a caller device buffer (memset + one kernel:
+ *                        no allocation, no synchronisation, graph-capturable)
+ *   bfp_dot_value        host: limbs -> the exact 192-bit two's complement words[3]
+ *                        (little endian) and its low 128 bits; BFP_ERR_WIDTH when the value
+ *                        does not fit 128 bits (sticky overflow detection)
+ *   bfp_dot_exact        synchronous, 128-bit (hi, lo); BFP_ERR_WIDTH beyond 128 bits
+ *   bfp_dot_exact192     synchronous, the full 192-bit value
+ * The synchronous calls reuse an accumulator owned by x (calls sharing x must not
+ * overlap on different streams). */
+int bfp_dot_exact_async(bfp_vec_t x, bfp_vec_t y, int64_t* d_acc, void* stream);
+int bfp_dot_value(const int64_t* acc, uint64_t* words, int64_t* hi, uint64_t* lo);
 int bfp_dot_exact(bfp_vec_t x, bfp_vec_t y, int64_t* hi, uint64_t* lo, int64_t* e, void* stream);
+int bfp_dot_exact192(bfp_vec_t x, bfp_vec_t y, uint64_t* words, int64_t* e, void* stream);
 
 /* ---- windowed BLAS (qcomp: w_tmp >= w_out; nnqcomp: w_tmp ignored) ----
  * Scalars are BFP scalars (m, q, e); gamma = (gm, gq, ge) with gm > 0.
@@ -268,6 +283,12 @@ int bfp_dist_stencil_jacobi(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* b
                             int mode, int64_t w_out, int64_t w_tmp, bfp_scalar_t gamma,
                             bfp_vec_t const* out, void* stream);
 
+/* sharded exact dot over z-slabs: per-rank limb accumulators (device int64[5] each, one
+ * per local rank), carried into [0, 2^48) per rank and all-reduced with an int64 SUM
+ * (every rank ends with the global limbs; exact for up to 2^14 ranks); stream-ordered */
+int bfp_dist_dot_exact(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* y,
+                       int64_t* const* d_acc, void* stream);
+
 /* ---- measurement hooks ----
  * When enabled, every windowed pass-1 / nnqcomp kernel launch is bracketed by
  * CUDA events recorded on its own stream; read() synchronises and returns the
@@ -285,6 +306,12 @@ const char* bfp_status_string(int status);
 int bfp_device_sync(void* stream);
 /* number of kernels this library launched since load (evidence counter) */
 int64_t bfp_launch_count(void);
+/* windowed-kernel launches since load per kernel family (evidence of the pipelines a solve
+   used; launches recorded while capturing a solve graph count once):
+   0 grid, 1 2-D bulk pipeline, 2 3-D tiled-TMA pipeline, 3 register march, 4 3-D
+   prolongation march, 5 3-D restriction march, 6 2-D prolongation march, 7 2-D restriction
+   march, 8 flat rows, 9 fused single-CTA, 10 persistent coarse-level kernel */
+int bfp_kernel_family_counts(int64_t* counts, int n);
 
 #ifdef __cplusplus
 }

@@ -348,7 +348,12 @@ int ob_qcomp(const ob_kernel* k, int64_t w_out, int64_t w_tmp, int64_t gm, int64
   const int64_t n = k->n;
   const int64_t mu_tmp = msb128(gm) + ge - k->e;      /* :150 */
   const int64_t lam_tmp = mu_tmp - w_tmp;             /* :151 */
-  i128* tmp = (i128*)malloc(sizeof(i128) * (size_t)(n > 0 ? n : 1));
+  /* the wrapped temporaries live in T_{w_tmp}: 64-bit storage when w_tmp <= 64 (config
+     scale: halves the host memory of a 1023^3 solve), 128-bit otherwise */
+  const int narrow = w_tmp <= 64;
+  void* tmpv = malloc((narrow ? sizeof(int64_t) : sizeof(i128)) * (size_t)(n > 0 ? n : 1));
+  i128* tmp = (i128*)tmpv;
+  int64_t* tmp64 = (int64_t*)tmpv;
   int64_t mu_star = 1 - k->zd; /* :153 (mu* = 1 in the reference's coordinates) */
   int err = 0;
 #pragma omp parallel for reduction(max : mu_star) reduction(| : err) schedule(static)
@@ -359,10 +364,14 @@ int ob_qcomp(const ob_kernel* k, int64_t w_out, int64_t w_tmp, int64_t gm, int64
       continue;
     }
     if (z != 0) mu_star = max64(mu_star, msb128(z));
-    tmp[i] = wrap_shift128(z, lam_tmp, w_tmp);
+    i128 t = wrap_shift128(z, lam_tmp, w_tmp);
+    if (narrow)
+      tmp64[i] = (int64_t)t;
+    else
+      tmp[i] = t;
   }
   if (err) {
-    free(tmp);
+    free(tmpv);
     return OB_ERR_WIDTH;
   }
   const int64_t lam_out = mu_star - w_out; /* :164 */
@@ -386,11 +395,11 @@ int ob_qcomp(const ob_kernel* k, int64_t w_out, int64_t w_tmp, int64_t gm, int64
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; ++i) {
       i128 r = 0;
-      shift_floor128(tmp[i], s, &r);
+      shift_floor128(narrow ? (i128)tmp64[i] : tmp[i], s, &r);
       out->m[i] = (int64_t)wrap128(r, w_out);
     }
   }
-  free(tmp);
+  free(tmpv);
   if (err) return OB_ERR_WIDTH;
   out->n = n;
   out->q = w_out;
@@ -907,7 +916,8 @@ static void vcycle(mg_ctx* c, int l, const ob_block* r, ob_block* e_out) {
   ob_jacobi_coeff(g, cfg->qc, &cm, &ce);
   ob_g15 c15 = ob_g15_from((uint64_t)cm, ce);
   ob_kernel k;
-  ob_block e = blk_alloc(N), t = blk_alloc(N);
+  ob_block e = *e_out, t = blk_alloc(N); /* e starts in the caller's buffer */
+  e.n = N;
   ob_make_scal(&k, r, cm, cfg->qc, ce);
   run_step(c, OB_STEP_RELAX0, l, &k, wd(c, l), ob_g15_mul(c15, nrm(r)), 2, &e);
   int sweeps = (l == cfg->l_coarse) ? cfg->n_coarse : cfg->nu1;
@@ -945,12 +955,15 @@ static void vcycle(mg_ctx* c, int l, const ob_block* r, ob_block* e_out) {
     blk_free(&rc);
     blk_free(&ec);
   }
-  memcpy(e_out->m, e.m, sizeof(int64_t) * (size_t)N);
+  if (e.m != e_out->m) { /* the result ended in the scratch buffer */
+    memcpy(e_out->m, e.m, sizeof(int64_t) * (size_t)N);
+    blk_free(&e);
+  } else {
+    blk_free(&t);
+  }
   e_out->n = N;
   e_out->q = e.q;
   e_out->e = e.e;
-  blk_free(&e);
-  blk_free(&t);
 }
 
 static void push_hist(mg_ctx* c, double v) {
@@ -965,7 +978,7 @@ static void ir(mg_ctx* c, int l, ob_block* x, const ob_block* b, int iters) {
   ob_grid g = {cfg->d, l};
   int64_t N = ob_grid_size(g);
   ob_kernel k;
-  ob_block r = blk_alloc(N), e = blk_alloc(N), xn = blk_alloc(N);
+  ob_block r = blk_alloc(N), e = blk_alloc(N);
   c->have_prev_res[l] = 0;
   for (int i = 1; i <= iters && !c->err; ++i) {
     int first = !c->have_prev_res[l];
@@ -982,15 +995,15 @@ static void ir(mg_ctx* c, int l, ob_block* x, const ob_block* b, int iters) {
     c->have_prev_res[l] = 1;
     push_hist(c, norm_double(&r));
     vcycle(c, l, &r, &e);
+    /* r is dead after the V-cycle: it receives the corrected iterate */
     ob_make_axpby(&k, x, &e, 1, 2, 0, 1, 2, 0);
-    run_step(c, OB_STEP_IR_CORR, l, &k, wl(c, l), ob_g15_add(nrm(x), nrm(&e)), 1, &xn);
-    memcpy(x->m, xn.m, sizeof(int64_t) * (size_t)N);
-    x->q = xn.q;
-    x->e = xn.e;
+    run_step(c, OB_STEP_IR_CORR, l, &k, wl(c, l), ob_g15_add(nrm(x), nrm(&e)), 1, &r);
+    memcpy(x->m, r.m, sizeof(int64_t) * (size_t)N);
+    x->q = r.q;
+    x->e = r.e;
   }
   blk_free(&r);
   blk_free(&e);
-  blk_free(&xn);
 }
 
 static int gen_rhs(const ob_mg_config* cfg, ob_grid g, ob_block* b) {

@@ -104,7 +104,8 @@ EXPORTS = [
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
     "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result", "bfp_dist_create",
     "bfp_dist_destroy", "bfp_dist_stencil_gemv", "bfp_dist_stencil_jacobi",
-    "bfp_quantize_exact", "bfp_from_doubles",
+    "bfp_quantize_exact", "bfp_from_doubles", "bfp_kernel_family_counts",
+    "bfp_dot_exact_async", "bfp_dot_value", "bfp_dot_exact192", "bfp_dist_dot_exact",
 ]
 
 _lib: Optional[C.CDLL] = None
@@ -144,6 +145,10 @@ def lib() -> C.CDLL:
         "bfp_quantize": (i32, [vp, i64, vp, vp]),
         "bfp_inf_norm_upper": (i32, [vp, i64, pi64, pi64, pi64, vp]),
         "bfp_dot_exact": (i32, [vp, vp, pi64, C.POINTER(C.c_uint64), pi64, vp]),
+        "bfp_dot_exact_async": (i32, [vp, vp, vp, vp]),
+        "bfp_dot_value": (i32, [vp, vp, pi64, C.POINTER(C.c_uint64)]),
+        "bfp_dot_exact192": (i32, [vp, vp, vp, pi64, vp]),
+        "bfp_dist_dot_exact": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
         "bfp_axpby": (i32, [vp, vp, S, S, i32, i64, i64, S, i32, vp, vp]),
         "bfp_csr_create": (i32, [i64, i64, vp, vp, vp, i64, i64, C.POINTER(vp)]),
         "bfp_csr_destroy": (i32, [vp]),
@@ -181,6 +186,7 @@ def lib() -> C.CDLL:
         "bfp_status_string": (C.c_char_p, [i32]),
         "bfp_device_sync": (i32, [vp]),
         "bfp_launch_count": (i64, []),
+        "bfp_kernel_family_counts": (i32, [pi64, i32]),
         "bfp_profile_enable": (i32, [i32]),
         "bfp_profile_read": (i32, [C.POINTER(C.c_double), pi64, i32]),
         "bfp_set_kernel_path": (i32, [i32]),
@@ -386,11 +392,39 @@ def inf_norm_upper(x: BfpVec, q_gamma: int = 16) -> Scalar:
     return Scalar(m.value, q.value, e.value)
 
 
+def _i192(w) -> int:
+    v = int(w[0]) | (int(w[1]) << 64) | (int(w[2]) << 128)
+    return v - (1 << 192) if v >> 191 else v
+
+
 def dot_exact(x: BfpVec, y: BfpVec) -> Tuple[int, int]:
-    """Exact sum_i m_x m_y as a Python int, and its exponent e_x + e_y."""
+    """Exact sum_i m_x m_y as a Python int (192-bit device accumulation), and its exponent
+    e_x + e_y."""
+    w, e = (C.c_uint64 * 3)(), C.c_int64()
+    _raise(lib().bfp_dot_exact192(x.h, y.h, w, C.byref(e), _s()), "dot_exact")
+    return _i192(w), e.value
+
+
+def dot_exact128(x: BfpVec, y: BfpVec) -> Tuple[int, int]:
+    """The 128-bit entry point (bfp_dot_exact): raises WidthError when the exact value does
+    not fit 128 bits."""
     hi, lo, e = C.c_int64(), C.c_uint64(), C.c_int64()
-    _raise(lib().bfp_dot_exact(x.h, y.h, C.byref(hi), C.byref(lo), C.byref(e), _s()), "dot_exact")
+    _raise(lib().bfp_dot_exact(x.h, y.h, C.byref(hi), C.byref(lo), C.byref(e), _s()),
+           "dot_exact128")
     return (hi.value << 64) | lo.value, e.value
+
+
+def dot_value(acc: Sequence[int]) -> int:
+    """Exact value of a device limb accumulator {L0, L1, L2, L3, e} (bfp_dot_value)."""
+    a = (C.c_int64 * 5)(*[int(v) for v in acc[:5]])
+    w = (C.c_uint64 * 3)()
+    lib().bfp_dot_value(a, w, None, None)
+    return _i192(w)
+
+
+def dot_exact_async(x: BfpVec, y: BfpVec, d_acc: int):
+    """Stream-ordered exact dot into a device int64[5] accumulator (no synchronisation)."""
+    _raise(lib().bfp_dot_exact_async(x.h, y.h, C.c_void_p(d_acc), _s()), "dot_exact_async")
 
 
 def dump_block(x: BfpVec) -> str:
@@ -709,6 +743,13 @@ class DistOps:
                                            beta.c(), int(nn), w_out, w_tmp, gamma.c(),
                                            self._arr(outs), _s()), "bfp_dist_stencil_gemv")
 
+    def dot(self, xs, ys, accs):
+        """Sharded exact dot: per-rank limb accumulators (device int64[5] pointers, one per
+        local rank) all-reduced with an int64 SUM; returns nothing (stream-ordered)."""
+        arr = (C.c_void_p * len(accs))(*[int(a) for a in accs])
+        _raise(lib().bfp_dist_dot_exact(self.h, self._arr(xs), self._arr(ys), arr, _s()),
+               "bfp_dist_dot_exact")
+
     def jacobi(self, xs, bs, c: Scalar, w_out: int, w_tmp: int, gamma: Scalar, outs,
                nn: bool = False):
         _raise(lib().bfp_dist_stencil_jacobi(self.h, self._arr(xs), self._arr(bs), c.c(), int(nn),
@@ -781,6 +822,17 @@ class Multigrid:
 
 def launch_count() -> int:
     return int(lib().bfp_launch_count())
+
+
+KERNEL_FAMILIES = ["grid", "bulk2", "bulk3", "march", "pro3", "rst3", "pro2", "rst2", "flat",
+                   "fused", "coarse"]
+
+
+def kernel_family_counts() -> dict:
+    """Windowed-kernel launches since load per kernel family (include/bfpmg_b200.h)."""
+    a = (C.c_int64 * 16)()
+    _raise(lib().bfp_kernel_family_counts(a, 16), "bfp_kernel_family_counts")
+    return {n: int(a[i]) for i, n in enumerate(KERNEL_FAMILIES)}
 
 
 def device_sync():

@@ -121,7 +121,8 @@ template <typename A> __device__ __forceinline__ int64_t wrap_shift(A x, int64_t
 }
 // floor(x / 2^s) clamped to T_w (nnqcomp, w <= 64): saturates when a left shift leaves T_w
 template <typename A> __device__ __forceinline__ int64_t shift_clamp(A x, int64_t s, int64_t w) {
-  const int64_t hi = (int64_t)((~0ull) >> (65 - w)), lo = -hi - 1;
+  // T_w bounds without a 64-bit shift by 64 (w = 1: [-1, 0]; w = 64: the int64 range)
+  const int64_t hi = w >= 64 ? INT64_MAX : (int64_t)((1ull << (w - 1)) - 1), lo = -hi - 1;
   A r;
   if (s >= 0) {
     r = sar<A>(x, s);

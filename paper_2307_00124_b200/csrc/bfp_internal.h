@@ -20,6 +20,7 @@ struct bfp_vec_s {
   void* stage = nullptr;  // device staging in logical order (uploads / downloads)
   size_t stage_bytes = 0;
   double* tab = nullptr;  // sine table (generator)
+  int64_t* dot_acc = nullptr;  // exact-dot accumulator of the synchronous bfp_dot_exact*
   int64_t tab_n = 0;
 };
 
@@ -104,5 +105,17 @@ int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, i
                  int ebytes, cudaStream_t s);
 void count_launch(int n = 1);
 int64_t launches();
+// launches per kernel family (evidence of which pipelines a solve used; bfp_kernel_family_counts)
+enum KernelFamily { FAM_GRID = 0, FAM_BULK2, FAM_BULK3, FAM_MARCH, FAM_PRO3, FAM_RST3, FAM_PRO2,
+                    FAM_RST2, FAM_FLAT, FAM_FUSED, FAM_COARSE, FAM_N = 16 };
+void count_family(int fam);
+// exact dot (op_dot.cu): limb accumulator d_acc[5] = {L0..L3, e}, value sum_k L_k 2^(48k);
+// normalise: carry the limbs into [0, 2^48) (before a multi-rank SUM)
+int dot_limbs(bfp_vec_s* x, bfp_vec_s* y, int64_t* d_acc, cudaStream_t s, bool normalise);
+constexpr int kMaxLimbRanks = 64;  // in-process rank groups (LocalComm)
+struct LimbPtrs {
+  int64_t* p[kMaxLimbRanks];
+};
+int limb_sum_local(int64_t* const* d_ptrs, int P, cudaStream_t s);
 
 }  // namespace bfp

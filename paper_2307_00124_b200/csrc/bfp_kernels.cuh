@@ -33,7 +33,38 @@ inline int defer_ok(const bfpdev::WinParams& p, int blocks) {
 }
 
 constexpr int kThreads = 256;
-constexpr int kMaxBlocks = 148 * 8;
+constexpr int kMaxDev = 64;
+// current device (index into the per-device caches below)
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < kMaxDev ? d : 0;
+}
+// One value per device, computed once (thread-safe): function attributes and occupancy
+// are per device, so every launcher caches them through this.
+template <typename F> inline int per_device(std::atomic<int>* slots, F make) {
+  const int d = cur_device();
+  int v = slots[d].load(std::memory_order_acquire);
+  if (v) return v;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  v = slots[d].load(std::memory_order_relaxed);
+  if (!v) {
+    v = make();
+    slots[d].store(v, std::memory_order_release);
+  }
+  return v;
+}
+// streaming multiprocessors of the current device (148 on B200)
+inline int sm_count() {
+  static std::atomic<int> c[kMaxDev];
+  return per_device(c, [] {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, cur_device());
+    return v > 0 ? v : 148;
+  });
+}
+inline int max_blocks() { return sm_count() * 8; }
 #ifndef BFP_B2_EARLY  // 2-D bulk pipeline: first item's loads issued before the op setup (A/B)
 #define BFP_B2_EARLY 1
 #endif
@@ -68,8 +99,13 @@ inline void launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem,
 // smallest level a pipelined (bulk / TMA) kernel takes over from the generic grid kernel;
 // BFP_<NAME> in the environment overrides the default (A/B measurements)
 inline int min_level(const char* name, int def) {
+#ifdef BFP_AB_ENV  // A/B measurement builds only: product builds ignore the environment
   const char* v = getenv(name);
   return v ? atoi(v) : def;
+#else
+  (void)name;
+  return def;
+#endif
 }
 // March depth R (planes per work item) of a one-wave plane march over `units` tiles x NZ
 // planes on `ctas` resident CTAs, items handed out round robin (item = unit + chunk *
@@ -85,8 +121,12 @@ inline int march_R(int64_t units, int64_t NZ, int64_t ctas, int Rmin, int step, 
     return (int)((R + step - 1) / step * step);
   };
   static const bool on = [] {
+#ifdef BFP_AB_ENV
     const char* v = getenv("BFP_MARCH_BALANCE");
     return !(v && v[0] == '0');
+#else
+    return true;
+#endif
   }();
   if (!on || units <= 0 || NZ <= 0) return plain();
   struct Key {
@@ -125,7 +165,7 @@ inline int march_R(int64_t units, int64_t NZ, int64_t ctas, int Rmin, int step, 
 }
 inline int blocks_for(int64_t work) {
   int64_t b = (work + kThreads - 1) / kThreads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(b, kMaxBlocks));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, max_blocks()));
 }
 inline int last_launch() {
   cudaError_t e = cudaGetLastError();
@@ -2123,7 +2163,7 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
   const int b = groups <= kSingleBlockGroups ? 1 : blocks_for(groups);
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
-    const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * 148) : b;
+    const int nb = pp.mode == MODE_RECOMPUTE ? std::min(b, 2 * sm_count()) : b;
     if (out->ebytes == 4) {
       if (pp.mode == MODE_QCOMP)
         launch_pdl(grid_win_kernel<MODE_QCOMP, int32_t, Op>, nb, kThreads, 0, s, op, o, pp);
@@ -2140,6 +2180,7 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
         launch_pdl(grid_win_kernel<MODE_RECOMPUTE, int64_t, Op>, nb, kThreads, 0, s, op, o, pp);
     }
     count_launch();
+    count_family(FAM_GRID);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2198,16 +2239,17 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
     return BFP_ERR_CUDA;
   const int64_t N = int64_t(1) << out->l;
   constexpr size_t smem = b3_smem<T, Op>();
-  static int occ = 0;
-  if (!occ) {
+  static std::atomic<int> occ_dev[kMaxDev];  // per instantiation and device
+  const int occ = per_device(occ_dev, [&] {
+    int o = 0;
     for (auto fn : {bulk3_win_kernel<MODE_QCOMP, T, Op>, bulk3_win_kernel<MODE_NNQ, T, Op>,
                     bulk3_win_kernel<MODE_RECOMPUTE, T, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk3_win_kernel<MODE_QCOMP, T, Op>, kB3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, bulk3_win_kernel<MODE_QCOMP, T, Op>, kB3T,
                                                   smem);
-    occ = std::max(occ, 1);
-  }
-  const int64_t tiles = (N / kB3W) * (N / kB3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+    return std::max(o, 1);
+  });
+  const int64_t tiles = (N / kB3W) * (N / kB3H), ctas = (int64_t)sm_count() * occ, NZ = out->nz;
   const int R = march_R(tiles, NZ, ctas, 4, 1, 2);
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
@@ -2220,6 +2262,7 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
     else
       launch_pdl(bulk3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kB3T, smem, s, op, o, pp, R, tm);
     count_launch();
+    count_family(FAM_BULK3);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2255,16 +2298,17 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
     tm.y = tm.c;  // unused
   }
   const int64_t N = int64_t(1) << out->l;
-  static int occ = 0;
-  if (!occ) {
+  static std::atomic<int> occ_dev[kMaxDev];  // per instantiation and device
+  const int occ = per_device(occ_dev, [&] {
+    int o = 0;
     for (auto fn : {pro3_win_kernel<MODE_QCOMP, T, Op>, pro3_win_kernel<MODE_NNQ, T, Op>,
                     pro3_win_kernel<MODE_RECOMPUTE, T, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pro3_win_kernel<MODE_QCOMP, T, Op>, kP3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pro3_win_kernel<MODE_QCOMP, T, Op>, kP3T,
                                                   kP3Smem);
-    occ = std::max(occ, 1);
-  }
-  const int64_t tiles = (N / kP3W) * (N / kP3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+    return std::max(o, 1);
+  });
+  const int64_t tiles = (N / kP3W) * (N / kP3H), ctas = (int64_t)sm_count() * occ, NZ = out->nz;
   const int R = march_R(tiles, NZ, ctas, 4, 2, 1);  // whole fine-plane pairs
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
@@ -2277,6 +2321,7 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
     else
       launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
     count_launch();
+    count_family(FAM_PRO3);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2307,16 +2352,17 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
   R3Maps tm;
   if (!encode_b3(&tm.f, op.r, kR3FW, kR3FH)) return BFP_ERR_CUDA;
   const int64_t Nc = int64_t(1) << out->l;
-  static int occ = 0;
-  if (!occ) {
+  static std::atomic<int> occ_dev[kMaxDev];  // per instantiation and device
+  const int occ = per_device(occ_dev, [&] {
+    int o = 0;
     for (auto fn : {rst3_win_kernel<MODE_QCOMP, T>, rst3_win_kernel<MODE_NNQ, T>,
                     rst3_win_kernel<MODE_RECOMPUTE, T>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kR3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rst3_win_kernel<MODE_QCOMP, T>, kR3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, rst3_win_kernel<MODE_QCOMP, T>, kR3T,
                                                   kR3Smem);
-    occ = std::max(occ, 1);
-  }
-  const int64_t tiles = (Nc / kR3W) * (Nc / kR3H), ctas = (int64_t)148 * occ, NZ = out->nz;
+    return std::max(o, 1);
+  });
+  const int64_t tiles = (Nc / kR3W) * (Nc / kR3H), ctas = (int64_t)sm_count() * occ, NZ = out->nz;
   const int R = march_R(tiles, NZ, ctas, 2, 1, 1);
   const int64_t items = tiles * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
@@ -2329,6 +2375,7 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
     else
       launch_pdl(rst3_win_kernel<MODE_RECOMPUTE, T>, b, kR3T, kR3Smem, s, op, o, pp, R, tm);
     count_launch();
+    count_family(FAM_RST3);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2350,21 +2397,22 @@ static inline int launch_rst3(const RestrictOp& op, bfp_vec_s* out, const WinPar
 
 // one-wave launch of a row/plane-march transfer kernel (pass 1 + recompute unless partial)
 template <typename K0, typename K1, typename K2, typename... Args>
-static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int64_t units,
-                              int64_t NZ, int Rmin, bool even, bfp_vec_s* out, const WinParams& p0,
-                              cudaStream_t s, Args... args) {
+static inline int launch_wave(int fam, K0 kq, K1 kn, K2 kr, int threads, size_t smem,
+                              int64_t units, int64_t NZ, int Rmin, bool even, bfp_vec_s* out,
+                              const WinParams& p0, cudaStream_t s, Args... args) {
   int rc = check_window(p0, out);
   if (rc) return rc;
   static_assert(sizeof...(Args) >= 1, "kernel arguments");
-  static int occ = 0;  // per instantiation
-  if (!occ) {
+  static std::atomic<int> occ_dev[kMaxDev];  // per instantiation and device
+  const int occ = per_device(occ_dev, [&] {
+    int o = 0;
     cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kq, threads, smem);
-    occ = std::max(occ, 1);
-  }
-  const int64_t ctas = (int64_t)148 * occ;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kq, threads, smem);
+    return std::max(o, 1);
+  });
+  const int64_t ctas = (int64_t)sm_count() * occ;
   const int R = march_R(units, NZ, ctas, Rmin, even ? 2 : 1, 1);
   const int64_t items = units * ((NZ + R - 1) / R);
   const int b = (int)std::min<int64_t>(items, ctas);
@@ -2378,6 +2426,7 @@ static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int
     else
       launch_pdl(kr, b, threads, smem, s, args..., o, pp, R);
     count_launch();
+    count_family(fam);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2399,14 +2448,14 @@ static inline int launch_wave(K0 kq, K1 kn, K2 kr, int threads, size_t smem, int
 template <typename Op>
 static inline int launch_pro2(const Op& op, bfp_vec_s* out, const WinParams& p0, cudaStream_t s) {
   const int64_t N = int64_t(1) << out->l;
-  return launch_wave(pro2_win_kernel<MODE_QCOMP, Op>, pro2_win_kernel<MODE_NNQ, Op>,
+  return launch_wave(FAM_PRO2, pro2_win_kernel<MODE_QCOMP, Op>, pro2_win_kernel<MODE_NNQ, Op>,
                      pro2_win_kernel<MODE_RECOMPUTE, Op>, kP2T, kP2Smem, N / kP2W, out->nz, 4,
                      true, out, p0, s, op);
 }
 static inline int launch_rst2(const RestrictOp& op, bfp_vec_s* out, const WinParams& p0,
                               cudaStream_t s) {
   const int64_t Nc = int64_t(1) << out->l;
-  return launch_wave(rst2_win_kernel<MODE_QCOMP>, rst2_win_kernel<MODE_NNQ>,
+  return launch_wave(FAM_RST2, rst2_win_kernel<MODE_QCOMP>, rst2_win_kernel<MODE_NNQ>,
                      rst2_win_kernel<MODE_RECOMPUTE>, kR2T, kR2Smem, Nc / kR2W, out->nz, 2,
                      false, out, p0, s, op);
 }
@@ -2418,16 +2467,17 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
   if (rc) return rc;
   Vec o = view(out);
   const int64_t N = int64_t(1) << out->l;
-  static int occ = 0;
-  if (!occ) {
+  static std::atomic<int> occ_dev[kMaxDev];  // per instantiation and device
+  const int occ = per_device(occ_dev, [&] {
+    int o = 0;
     for (auto fn : {bulk_win_kernel<MODE_QCOMP, Op>, bulk_win_kernel<MODE_NNQ, Op>,
                     bulk_win_kernel<MODE_RECOMPUTE, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bulk_win_kernel<MODE_QCOMP, Op>, kBulkT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, bulk_win_kernel<MODE_QCOMP, Op>, kBulkT,
                                                   kBulkSmem);
-    occ = std::max(occ, 1);
-  }
-  const int64_t strips = N / kBulkW, ctas = (int64_t)148 * occ;
+    return std::max(o, 1);
+  });
+  const int64_t strips = N / kBulkW, ctas = (int64_t)sm_count() * occ;
   const int64_t NZ = out->nz;
   const int R = march_R(strips, NZ, ctas, 8, 1, 2);
   const int64_t items = strips * ((NZ + R - 1) / R);
@@ -2441,6 +2491,7 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
     else
       launch_pdl(bulk_win_kernel<MODE_RECOMPUTE, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
     count_launch();
+    count_family(FAM_BULK2);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2477,29 +2528,35 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
   // below the bulk pipeline's size a resident wave holds every 4-group with one group per
   // thread: the generic grid kernel issues all of a group's loads at once, where the march
   // (>= 4 dependent steps per thread) is latency-bound on these L2-resident levels
+#ifdef BFP_AB_ENV
   static const bool march_mid = getenv("BFP_MARCH_MID") != nullptr;  // A/B switch
+#else
+  constexpr bool march_mid = false;
+#endif
   if (!march_mid && out->dim == 2) return launch_grid(op, out, p0, s);
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
   const int64_t N = int64_t(1) << out->l, GX = N / 4, rows = out->dim == 3 ? N : 1;
-  static int occ2 = 0, occ3 = 0;
-  if (!occ2) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, march_win_kernel<MODE_QCOMP, 2, Op>,
-                                                  kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, march_win_kernel<MODE_QCOMP, 3, Op>,
-                                                  kThreads, 0);
-    occ2 = std::max(occ2, 1);
-    occ3 = std::max(occ3, 1);
-  }
-  const int occ = out->dim == 2 ? occ2 : occ3;
+  static std::atomic<int> occ2_dev[kMaxDev], occ3_dev[kMaxDev];
+  const int occ = out->dim == 2 ? per_device(occ2_dev, [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, march_win_kernel<MODE_QCOMP, 2, Op>,
+                                                kThreads, 0);
+    return std::max(o, 1);
+  }) : per_device(occ3_dev, [] {
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, march_win_kernel<MODE_QCOMP, 3, Op>,
+                                                kThreads, 0);
+    return std::max(o, 1);
+  });
   // one balanced resident wave: every thread marches R steps (last chunk shorter)
-  const int64_t slots = (int64_t)148 * occ * kThreads;
+  const int64_t slots = (int64_t)sm_count() * occ * kThreads;
   const int64_t NZ = out->nz;
   int R = (int)std::max<int64_t>(4, (GX * rows * NZ + slots - 1) / slots);
   const int64_t items = GX * rows * ((NZ + R - 1) / R);
   const int b = (int)std::max<int64_t>(1, std::min<int64_t>((items + kThreads - 1) / kThreads,
-                                                            (int64_t)148 * occ));
+                                                            (int64_t)sm_count() * occ));
   WinParams p = p0;
   auto go = [&](const WinParams& pp, int nb) {
     if (out->dim == 2) {
@@ -2518,6 +2575,7 @@ static inline int launch_march(const Op& op, bfp_vec_s* out, const WinParams& p0
         launch_pdl(march_win_kernel<MODE_RECOMPUTE, 3, Op>, nb, kThreads, 0, s, op, o, pp, R);
     }
     count_launch();
+    count_family(FAM_MARCH);
   };
   p.defer = defer_ok(p, b);
   if (g_prof) {
@@ -2550,6 +2608,7 @@ static inline int launch_flat(const Op& op, bfp_vec_s* out, const WinParams& p0,
     else
       launch_pdl(flat_win_kernel<int64_t, Op>, b, kThreads, 0, s, op, o, pp);
     count_launch();
+    count_family(FAM_FLAT);
   };
   p.defer = defer_ok(p, b);
   go(p);

@@ -184,6 +184,33 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(Vec v, const S* src, 
   });
 }
 
+// header of a block whose mantissas were copied straight into the padded storage (pads
+// are zero): max/min of the stored values, (q, e), the T_q check
+template <typename M>
+__global__ void __launch_bounds__(kThreads) header_scan_kernel(Vec v, int64_t q, int64_t e) {
+  Red r;
+  r.init();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, ng = v.n >> 2;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
+    int64_t t[4];
+    V4<M>::load(v, g * 4, 0, t);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r.val(t[j]);
+  }
+  reduce_and_finalize(r, v.hdr, [&](int, int64_t mx, int64_t mn, int err) {
+    Hdr* h = v.hdr;
+    h->q = q;
+    h->e = e;
+    h->shift = 0;
+    h->max_m = mx;
+    h->min_m = mn;
+    h->flags = 0;
+    h->need_recompute = 0;
+    int fits = q >= 64 || (msb(mx) <= q && msb(mn) <= q);
+    h->err = err | (fits ? 0 : 3 /* BFP_ERR_DOMAIN */);
+  });
+}
+
 // padded storage -> logical staged array, pending shift applied
 template <typename M, typename D>
 __global__ void __launch_bounds__(kThreads) gather_kernel(Vec v, D* dst) {
@@ -354,44 +381,14 @@ __global__ void __launch_bounds__(kThreads) sine_write_kernel(Vec v, const doubl
   });
 }
 
-// exact dot: per-block int128 partials, then one block sums them
-template <typename M>
-__global__ void __launch_bounds__(kThreads) dot_partial_kernel(Vec x, Vec y, i128* part) {
-  const int64_t sx = x.hdr->shift, sy = y.hdr->shift;
-  i128 acc = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < x.n; o += stride)
-    acc += (i128)(((int64_t)((const M*)x.data)[o]) >> sx) *
-           (i128)(((int64_t)((const M*)y.data)[o]) >> sy);
-  // warp reduce (two 64-bit halves with carry via 128-bit adds)
-  for (int off = 16; off > 0; off >>= 1) {
-    uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)acc, off);
-    int64_t hi = __shfl_xor_sync(0xffffffffu, (int64_t)(acc >> 64), off);
-    acc += (i128)(((u128)(uint64_t)hi << 64) | lo);
-  }
-  __shared__ i128 s[kThreads / 32];
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    i128 t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
-    part[blockIdx.x] = t;
-  }
-}
-__global__ void dot_final_kernel(const i128* part, int n, i128* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    i128 t = 0;
-    for (int i = 0; i < n; ++i) t += part[i];
-    *out = t;
-  }
-}
-
 // ===========================================================================
 // host side
 
 namespace bfp {
 
 void count_launch(int n) { g_launches += n; }
+static std::atomic<int64_t> g_family[FAM_N];
+void count_family(int fam) { g_family[fam] += 1; }
 int64_t launches() { return g_launches.load(); }
 
 Vec view(const bfp_vec_s* v) {
@@ -481,6 +478,7 @@ void vec_free(bfp_vec_s* v) {
   cudaFree(v->hdr);
   if (v->stage) cudaFree(v->stage);
   if (v->tab) cudaFree(v->tab);
+  if (v->dot_acc) cudaFree(v->dot_acc);
   delete v;
 }
 
@@ -721,6 +719,12 @@ const char* bfp_status_string(int st) {
 
 int64_t bfp_launch_count(void) { return launches(); }
 
+int bfp_kernel_family_counts(int64_t* counts, int n) {
+  if (!counts || n < 0) return BFP_ERR_ARG;
+  for (int i = 0; i < n && i < FAM_N; ++i) counts[i] = g_family[i].load();
+  return BFP_OK;
+}
+
 int bfp_profile_enable(int on) {
   g_prof = on != 0;
   return BFP_OK;
@@ -761,9 +765,28 @@ int bfp_vec_destroy(bfp_vec_t v) {
 int64_t bfp_vec_size(bfp_vec_t v) { return v ? v->nlog : -1; }
 
 }  // extern "C"
+// int32 host mantissas of a full 2-D / 3-D grid: one pitched DMA copy straight into the
+// padded layout (interior rows only; pads and halos stay zero) and a header scan, no
+// staging buffer and no scatter kernel
+static int upload_pitched_i32(bfp_vec_t v, const int32_t* m, int64_t q, int64_t e,
+                              cudaStream_t s) {
+  const size_t N = (size_t)1 << v->l, n = N - 1;
+  cudaMemcpy3DParms c = {};
+  c.srcPtr = make_cudaPitchedPtr((void*)m, n * 4, n * 4, n);
+  c.dstPtr = make_cudaPitchedPtr(v->data, N * 4, N * 4, N);
+  c.extent = make_cudaExtent(n * 4, n, v->dim == 3 ? n : 1);
+  c.kind = cudaMemcpyHostToDevice;
+  if (cudaMemcpy3DAsync(&c, s) != cudaSuccess) return BFP_ERR_CUDA;
+  header_scan_kernel<int32_t><<<blocks_for(v->span / 4), kThreads, 0, s>>>(view(v), q, e);
+  count_launch();
+  return last_launch();
+}
+
 template <typename S_>
 static int upload_impl(bfp_vec_t v, const S_* m, int64_t q, int64_t e, void* stream) {
   if (!v || q < 1 || (q > 64)) return BFP_ERR_ARG;
+  if (sizeof(S_) == 4 && v->ebytes == 4 && v->dim >= 2 && full_grid(v) && v->nlog)
+    return upload_pitched_i32(v, (const int32_t*)m, q, e, S(stream));
   int rc = ensure_stage(v, sizeof(S_) * (size_t)std::max<int64_t>(v->nlog, 1));
   if (rc) return rc;
   if (v->nlog)
@@ -1006,32 +1029,6 @@ int bfp_inf_norm_upper(bfp_vec_t x, int64_t q_gamma, int64_t* m, int64_t* q, int
   }
   *m = (int64_t)mm;
   *e = h.e + s;
-  return BFP_OK;
-}
-
-int bfp_dot_exact(bfp_vec_t x, bfp_vec_t y, int64_t* hi, uint64_t* lo, int64_t* e, void* stream) {
-  if (!x || !y || x->span != y->span || x->ebytes != y->ebytes || x->dim != y->dim) return BFP_ERR_ARG;
-  const int nb = blocks_for(x->span);
-  i128* part = nullptr;
-  if (cudaMalloc(&part, sizeof(i128) * (nb + 1)) != cudaSuccess) return BFP_ERR_NOMEM;
-  Vec a = view(x), b = view(y);
-  if (x->ebytes == 4)
-    dot_partial_kernel<int32_t><<<nb, kThreads, 0, S(stream)>>>(a, b, part);
-  else
-    dot_partial_kernel<int64_t><<<nb, kThreads, 0, S(stream)>>>(a, b, part);
-  dot_final_kernel<<<1, 32, 0, S(stream)>>>(part, nb, part + nb);
-  count_launch(2);
-  i128 r = 0;
-  cudaMemcpyAsync(&r, part + nb, sizeof(r), cudaMemcpyDeviceToHost, S(stream));
-  Hdr hx, hy;
-  cudaMemcpyAsync(&hx, x->hdr, sizeof(Hdr), cudaMemcpyDeviceToHost, S(stream));
-  cudaMemcpyAsync(&hy, y->hdr, sizeof(Hdr), cudaMemcpyDeviceToHost, S(stream));
-  cudaError_t err = cudaStreamSynchronize(S(stream));
-  cudaFree(part);
-  if (err != cudaSuccess) return BFP_ERR_CUDA;
-  *hi = (int64_t)(r >> 64);
-  *lo = (uint64_t)r;
-  *e = hx.e + hy.e;
   return BFP_OK;
 }
 

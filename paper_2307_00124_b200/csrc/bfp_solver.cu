@@ -75,12 +75,15 @@ int fused_kind(int k) {
 // levels whose padded grid has at most this many points run fused in one CTA
 // (BFP_FUSE_POINTS overrides; 0 disables fusion)
 int64_t fuse_max_points() {
-  static int64_t v = -1;
-  if (v < 0) {
+#ifdef BFP_AB_ENV  // A/B measurement builds only
+  static const int64_t v = [] {
     const char* e = getenv("BFP_FUSE_POINTS");
-    v = e ? atoll(e) : 0;  // off by default: slower than PDL-chained launches (profiles/)
-  }
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
   return v;
+#else
+  return 0;  // off by default: slower than PDL-chained launches (profiles/)
+#endif
 }
 
 struct LevelBufs {
@@ -818,6 +821,8 @@ struct Comm {
   // first plane) halo planes of the slabs v[i] of the local ranks
   virtual int halo(bfp_vec_s* const* v, int which, cudaStream_t s) = 0;
   virtual int allreduce_max(int64_t* const* part, int n, cudaStream_t s) = 0;
+  // int64 SUM of the exact-dot limb accumulators (4 words per local rank)
+  virtual int allreduce_limbs(int64_t* const* acc, cudaStream_t s) = 0;
   // all-gather equal slabs into the full (replicated) vectors, header included
   virtual int gather(bfp_vec_s* const* slab, bfp_vec_s* const* full, cudaStream_t s) = 0;
 };
@@ -868,6 +873,9 @@ struct LocalComm : Comm {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "bfpmg_b200: part_max launch: %s\n", cudaGetErrorString(e));
     return e == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+  }
+  int allreduce_limbs(int64_t* const* acc, cudaStream_t s) override {
+    return limb_sum_local(acc, P, s);
   }
   int gather(bfp_vec_s* const* slab, bfp_vec_s* const* full, cudaStream_t s) override {
     for (int r = 0; r < P; ++r) {
@@ -957,6 +965,11 @@ struct NcclComm : Comm {
   }
   int allreduce_max(int64_t* const* part, int cnt, cudaStream_t s) override {
     return nccl().AllReduce(part[0], part[0], cnt, ncclInt64, ncclMax, comm, s) == ncclSuccess
+               ? BFP_OK
+               : BFP_ERR_CUDA;
+  }
+  int allreduce_limbs(int64_t* const* acc, cudaStream_t s) override {
+    return nccl().AllReduce(acc[0], acc[0], 4, ncclInt64, ncclSum, comm, s) == ncclSuccess
                ? BFP_OK
                : BFP_ERR_CUDA;
   }
@@ -1053,7 +1066,9 @@ static int make_group(const bfp_mg_config_t* cfg, int world, int rank0, int nloc
     r->rank = rank0 + i;
     r->world = world;
     r->min_planes = min_planes;
+#ifdef BFP_AB_ENV
     if (const char* ev = getenv("BFP_NO_FUSION")) r->fusion = ev[0] != '1';
+#endif
     mg->rs.push_back(r);
     rc = r->build();
     int64_t* part = nullptr;
@@ -1292,6 +1307,17 @@ int bfp_dist_stencil_gemv(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* y,
     return op_gemv(x[r], y[r], Scal{alpha.m, alpha.q, alpha.e}, Scal{beta.m, beta.q, beta.e}, p,
                    out[r], s);
   });
+}
+
+int bfp_dist_dot_exact(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* y,
+                       int64_t* const* d_acc, void* stream) {
+  if (!d || !x || !y || !d_acc) return BFP_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int P = d->comm->nlocal();
+  int rc = BFP_OK;
+  for (int r = 0; r < P && !rc; ++r) rc = dot_limbs(x[r], y[r], d_acc[r], s, true);
+  if (!rc) rc = d->comm->allreduce_limbs(d_acc, s);
+  return rc;
 }
 
 int bfp_dist_stencil_jacobi(bfp_dist_t d, bfp_vec_t const* x, bfp_vec_t const* b, bfp_scalar_t c,

@@ -47,14 +47,14 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
 
 int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, int arena_bytes,
                  int ebytes, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<int> attr[kMaxDev];  // function attributes are per device
+  per_device(attr, [] {
     cudaFuncSetAttribute(fused_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kArenaMaxBytes);
     cudaFuncSetAttribute(fused_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kArenaMaxBytes);
-    attr = true;
-  }
+    return 1;
+  });
   if (ebytes == 4)
     launch_pdl(fused_kernel<int32_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
                nar);
@@ -62,6 +62,7 @@ int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, i
     launch_pdl(fused_kernel<int64_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
                nar);
   count_launch();
+  count_family(FAM_FUSED);
   return last_launch();
 }
 

@@ -73,6 +73,12 @@ class LocalComm:
         for p in parts:
             p.copy_(m)
 
+    def allreduce_sum(self, parts):
+        import torch
+        m = torch.stack(list(parts)).sum(dim=0)
+        for p in parts:
+            p.copy_(m)
+
 
 class TorchComm:
     """One slab per process over torch.distributed (the process group's backend)."""
@@ -104,6 +110,10 @@ class TorchComm:
     def allreduce_max(self, parts):
         (p,) = parts
         self.dist.all_reduce(p, op=self.dist.ReduceOp.MAX)
+
+    def allreduce_sum(self, parts):
+        (p,) = parts
+        self.dist.all_reduce(p, op=self.dist.ReduceOp.SUM)
 
 
 # ---------------------------------------------------------------------------
@@ -146,6 +156,13 @@ class GpuBackend:
         self.B._raise(self.L.bfp_stencil_jacobi_part(
             x.h, b.h, c.c(), int(nn), st, w_out, w_tmp, gamma.c(), out.h,
             C.c_void_p(part.data_ptr()), self.stream), "bfp_stencil_jacobi_part")
+
+    def dot_limbs(self, x, y):
+        """Device limb accumulator {L0..L3, e} of this slab's exact dot (op_dot.cu)."""
+        acc = self.torch.zeros(5, dtype=self.torch.int64, device="cuda")
+        self.B._raise(self.L.bfp_dot_exact_async(x.h, y.h, C.c_void_p(acc.data_ptr()),
+                                                 self.stream), "bfp_dot_exact_async")
+        return acc
 
     def finalize(self, out, mode, st, w_out, w_tmp, part):
         self.B._raise(self.L.bfp_window_finalize(out.h, mode, st, w_out, w_tmp,
@@ -191,3 +208,39 @@ class DistStencil:
         self._window(lambda o, st, part: self.be.jacobi_stage(
             bx[o.rank], bb[o.rank], c, nn, st, w_out, w_tmp, gamma, o.vec, part),
             outs, nn, w_out, w_tmp)
+
+
+# ---------------------------------------------------------------------------
+# the sharded exact dot (config 5's 128-bit dot-product all-reduce)
+
+LIMB_BITS = 48
+
+
+def limbs_of(v: int):
+    """Carried 48-bit limbs of an exact integer: L0..L2 in [0, 2^48), L3 signed."""
+    m = (1 << LIMB_BITS) - 1
+    return [v & m, (v >> 48) & m, (v >> 96) & m, v >> 144]
+
+
+def limbs_value(acc) -> int:
+    """sum_k L_k 2^(48k) of a limb accumulator (carried or not)."""
+    return sum(int(acc[k]) << (LIMB_BITS * k) for k in range(4))
+
+
+class DistDot:
+    """<x, y> over z-slabs: each slab's exact dot as int64 limbs (the device accumulates
+    192 bits and carries its block sums below 2^48 before its atomics, so a rank's limbs
+    stay below 2^59), an int64 SUM all-reduce of the four limbs (exact for up to 16
+    ranks; NCCL has no 128-bit type), and the exact value from the summed limbs.  The
+    native path (bfp_dist_dot_exact) carries each rank's limbs first (2^14 ranks)."""
+
+    def __init__(self, comm, backend):
+        self.comm, self.be = comm, backend
+
+    def dot(self, xs: Sequence[Slab], ys: Sequence[Slab]):
+        by = {s.rank: s.vec for s in ys}
+        accs = [self.be.dot_limbs(s.vec, by[s.rank]) for s in xs]
+        self.comm.allreduce_sum([a[:4] for a in accs])
+        self.be.sync()
+        a = accs[0]
+        return limbs_value([int(v) for v in a[:4]]), int(a[4])
