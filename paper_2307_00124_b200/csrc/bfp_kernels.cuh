@@ -853,187 +853,6 @@ __global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Ve
 }
 
 // ---------------------------------------------------------------------------
-// Fused coarse levels: one CTA interprets a list of windowed ops (the part of a
-// V-cycle / FMG on levels below the fusion threshold) with block-level
-// reductions and finalizers instead of one or two kernel launches per op.  The
-// per-op semantics are the same functions as the multi-block kernels
-// (setup, win_setup, eval4, win_finalize), so results are bit-identical.
-
-template <typename Fin>
-__device__ inline void block_reduce_finalize(Red& r, Fin fin) {
-  __shared__ unsigned long long s_lo[32], s_hi[32];
-  __shared__ int s_err[32];
-  __shared__ long long s_mx[32], s_mn[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  uint64_t lo = shfl_or64(r.olo), hi = shfl_or64(r.ohi);
-  int err = __reduce_or_sync(0xffffffffu, r.err);
-  int64_t mx = shfl_max64(r.mx), mn = shfl_min64(r.mn);
-  if (lane == 0) {
-    s_lo[wid] = lo;
-    s_hi[wid] = hi;
-    s_err[wid] = err;
-    s_mx[wid] = mx;
-    s_mn[wid] = mn;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < nw; ++w) {
-      lo |= s_lo[w];
-      hi |= s_hi[w];
-      err |= s_err[w];
-      mx = s_mx[w] > mx ? s_mx[w] : mx;
-      mn = s_mn[w] < mn ? s_mn[w] : mn;
-    }
-    const int bits = (hi ? 64 + bitlen64(hi) : bitlen64(lo)) + 1;
-    fin(bits, mx, mn, err);
-  }
-  __syncthreads();
-}
-
-template <int MODE, typename M, typename Op>
-__device__ __forceinline__ void fused_pass(Op& op, const Vec& out, const WinParams& p,
-                                           const WinCtx& c, int64_t need) {
-  Red r;
-  r.init();
-  grid_body<MODE, M, Op, false>(op, out, p, c, r, need);
-  block_reduce_finalize(r, [&](int bits, int64_t mx, int64_t mn, int err) {
-    win_finalize(p, c, out.hdr, bits, mx, mn, err);
-  });
-}
-
-// arena rebasing: vector pointers of an arena-resident op list are byte offsets into the
-// CTA's dynamic shared memory (offset 0 is never used)
-__device__ __forceinline__ void rebase(Vec& v, char* b) {
-  v.data = b + (size_t)v.data;
-  v.hdr = reinterpret_cast<Hdr*>(b + (size_t)v.hdr);
-}
-__device__ __forceinline__ void rebase_gamma(GammaRule& g, char* b) {
-  if (g.literal) return;
-  for (int i = 0; i < g.nterms; ++i)
-    if (g.t[i].v) g.t[i].v = reinterpret_cast<const Hdr*>(b + (size_t)g.t[i].v);
-}
-__device__ __forceinline__ void rebase_op(GemvOp& o, char* b) { rebase(o.x, b); rebase(o.y, b); }
-__device__ __forceinline__ void rebase_op(JacobiOp& o, char* b) { rebase(o.x, b); rebase(o.b, b); }
-__device__ __forceinline__ void rebase_op(ScalOp& o, char* b) { rebase(o.r, b); }
-__device__ __forceinline__ void rebase_op(AxpbyOp& o, char* b) { rebase(o.x, b); rebase(o.y, b); }
-__device__ __forceinline__ void rebase_op(RestrictOp& o, char* b) { rebase(o.r, b); }
-__device__ __forceinline__ void rebase_op(ProlongOp& o, char* b) { rebase(o.xc, b); }
-__device__ __forceinline__ void rebase_op(ProlongCorrectOp& o, char* b) {
-  rebase(o.ec, b);
-  rebase(o.y, b);
-}
-
-// One op of the fused list.  The op (its FusedOp record) is staged once in shared
-// memory; thread 0 rebases it, runs the op setup and the window setup; every thread
-// then works on references into shared memory (no per-thread copies of the records).
-template <typename M, typename Op>
-__device__ __noinline__ void fused_run(Op& op, Vec& out, WinParams& p, char* ab, WinCtx& s_c,
-                                       int64_t& s_need) {
-  if (threadIdx.x == 0) {
-    if (ab) {
-      rebase_op(op, ab);
-      rebase(out, ab);
-      rebase_gamma(p.gamma, ab);
-    }
-    int64_t e_star = 0, nd = 0;
-    op.setup(e_star, nd);
-    WinCtx cc;
-    win_setup(p, out.hdr, e_star, 8 * (int)sizeof(M), cc);
-    cc.zd = op_zd(op);
-    s_c = cc;
-    s_need = nd;
-  }
-  __syncthreads();
-  const WinCtx c = s_c;
-  const int64_t need = s_need;
-  if (p.mode == MODE_NNQ) {
-    fused_pass<MODE_NNQ, M>(op, out, p, c, need);
-    return;
-  }
-  fused_pass<MODE_QCOMP, M>(op, out, p, c, need);
-  // header finalized by thread 0 and published by the barrier in block_reduce_finalize
-  if (!out.hdr->need_recompute) return;  // qcomp fast path (uniform: shared header)
-  if (threadIdx.x == 0) {
-    WinParams p2 = p;
-    p2.mode = MODE_RECOMPUTE;
-    WinCtx c2;
-    win_setup(p2, out.hdr, 0, 8 * (int)sizeof(M), c2);
-    s_c = c2;
-  }
-  __syncthreads();
-  WinParams p2 = p;
-  p2.mode = MODE_RECOMPUTE;
-  const WinCtx c2 = s_c;
-  if (!c2.skip) fused_pass<MODE_RECOMPUTE, M>(op, out, p2, c2, need);
-}
-
-template <typename M>
-__device__ __noinline__ void fused_zero(Vec v, int64_t q, char* ab) {
-  if (ab) rebase(v, ab);
-  for (int64_t o = threadIdx.x; o < v.n; o += blockDim.x) ((M*)v.data)[o] = 0;
-  if (threadIdx.x == 0) {
-    Hdr* h = v.hdr;
-    h->q = q;
-    h->e = 0;
-    h->shift = 0;
-    h->max_m = 0;
-    h->min_m = 0;
-    h->flags = 0;
-    h->need_recompute = 0;
-  }
-  __syncthreads();
-}
-
-// copy between global and the arena (16-byte granules; sizes are multiples of 16)
-__device__ __forceinline__ void arena_copy(char* dst, const char* src, int64_t bytes) {
-  const int64_t n16 = bytes >> 4;
-  for (int64_t i = threadIdx.x; i < n16; i += blockDim.x)
-    reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
-}
-
-template <typename M>
-__global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedOp* ops, int n,
-                                                              const ArenaEntry* ar, int nar) {
-  extern __shared__ __align__(128) char arena[];
-  __shared__ __align__(16) FusedOp s_f;
-  __shared__ WinCtx s_c;
-  __shared__ int64_t s_need;
-  griddep_wait();
-  char* ab = nar > 0 ? arena : nullptr;
-  for (int k = 0; k < nar; ++k) {  // vectors + headers of the fused levels -> shared memory
-    arena_copy(arena + ar[k].off, ar[k].gbase, ar[k].bytes);
-    arena_copy(arena + ar[k].hoff, reinterpret_cast<const char*>(ar[k].ghdr), sizeof(Hdr));
-  }
-  for (int i = 0; i < n; ++i) {
-    static_assert(sizeof(FusedOp) % 16 == 0, "FusedOp staging copies 16-byte granules");
-    __syncthreads();  // previous op done with s_f
-    for (int k = threadIdx.x; k < (int)(sizeof(FusedOp) / 16); k += blockDim.x)
-      reinterpret_cast<int4*>(&s_f)[k] = reinterpret_cast<const int4*>(&ops[i])[k];
-    __syncthreads();
-    switch (s_f.kind) {
-      case FK_GEMV: fused_run<M>(s_f.u.gemv, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_JACOBI: fused_run<M>(s_f.u.jac, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_SCAL: fused_run<M>(s_f.u.scal, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_AXPBY: fused_run<M>(s_f.u.axpby, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_RESTRICT: fused_run<M>(s_f.u.rst, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_PROLONG: fused_run<M>(s_f.u.pro, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_PCORR: fused_run<M>(s_f.u.pc, s_f.out, s_f.p, ab, s_c, s_need); break;
-      case FK_ZERO: {
-        Vec v = s_f.out;
-        fused_zero<M>(v, s_f.q, ab);
-        break;
-      }
-    }
-  }
-  __syncthreads();
-  for (int k = 0; k < nar; ++k) {  // write everything back (the fused part's outputs)
-    arena_copy(ar[k].gbase, arena + ar[k].off, ar[k].bytes);
-    arena_copy(reinterpret_cast<char*>(ar[k].ghdr), arena + ar[k].hoff, sizeof(Hdr));
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 // 3-D stencil ops through the bulk-async pipeline: a CTA owns a W3 x H3 tile of a
 // plane (warp = one row of 128 columns) and marches R planes along z.  Each step
 // streams the (H3+2) x (W3+8) x tile of plane k+1+D (y and x halos included) and
