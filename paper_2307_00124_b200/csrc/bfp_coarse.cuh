@@ -69,7 +69,7 @@ __device__ __forceinline__ void rebase_op(ProlongCorrectOp& o, char* b) {
 constexpr int kCoarseWarps = kFusedThreads / 32;
 
 struct CoarseShared {
-  FusedOp f[2];
+  FusedOp f[4];  // record ring (the generic engine uses two slots, the lean engine four)
   WinCtx c;
   int64_t need;
   int rc;  // the op just finalized needs its recompute pass
@@ -174,6 +174,28 @@ __device__ __forceinline__ void arena_copy(char* dst, const char* src, int64_t b
 
 }  // namespace bfpdev
 
+// measurement builds (-DBFP_COARSE_TIMING): thread 0's clock64 per phase, summed over launches
+#ifdef BFP_COARSE_TIMING
+__device__ long long g_coarse_prof[16];
+__device__ int g_coarse_ops[4096 * 4];  // per op of the last launch: kind, prepare, body, finalize clk
+#define CPROF_OP(i, j, v) \
+  if (threadIdx.x == 0 && (i) < 4096) g_coarse_ops[4 * (i) + (j)] = (int)(v)
+#define CPROF_T() long long _ct = clock64()
+#define CPROF(k)                                                    \
+  if (threadIdx.x == 0) {                                           \
+    const long long _n = clock64();                                 \
+    atomicAdd((unsigned long long*)&g_coarse_prof[k], (unsigned long long)(_n - _ct)); \
+    _ct = _n;                                                       \
+  }
+#define CPROF_CNT(k, v) \
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)&g_coarse_prof[k], (unsigned long long)(v))
+#else
+#define CPROF_T()
+#define CPROF(k)
+#define CPROF_CNT(k, v)
+#define CPROF_OP(i, j, v)
+#endif
+
 template <typename M>
 __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* ops, int n,
                                                                const ArenaEntry* ar, int nar) {
@@ -187,7 +209,9 @@ __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* op
   if (t < kChunks)
     reinterpret_cast<int4*>(&sh.f[0])[t] = __ldg(reinterpret_cast<const int4*>(&ops[0]) + t);
   if (t == 0) sh.rc = 0;
+  CPROF_T();
   griddep_wait();
+  CPROF(0);
   for (int k = 0; k < nar; ++k) {  // headers always, data while it fits -> shared memory
     const ArenaEntry e = ar[k];
     if (e.bytes) arena_copy(arena + e.off, e.gbase, e.bytes);
@@ -195,10 +219,15 @@ __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* op
       reinterpret_cast<int4*>(arena + e.hoff)[t] = reinterpret_cast<const int4*>(e.ghdr)[t];
   }
   __syncthreads();
+  CPROF(1);
   if (t == 0) coarse_prepare<M>(sh.f[0], arena, sh);
+  CPROF(2);
+  CPROF_CNT(8, 1);
+  CPROF_CNT(9, n);
   int i = 0;
   while (true) {
     __syncthreads();  // (1) window context of op i published; earlier data visible
+    CPROF(3);
     if (sh.rc) {
       // qcomp recompute pass of op i - 1 (a flag fired): floor(z / 2^lam_out) from the
       // still-live inputs (P/src/blas.cpp:170-176)
@@ -236,10 +265,19 @@ __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* op
     const int kind = f.kind, mode = f.p.mode;
     Red r;
     r.init();
+#ifdef BFP_COARSE_TIMING
+    const long long _b0 = clock64();
+#endif
     coarse_body<M>(f, mode, sh, r);
+#ifdef BFP_COARSE_TIMING
+    CPROF_OP(i, 0, kind);
+    CPROF_OP(i, 2, clock64() - _b0);
+#endif
+    CPROF(4);
     if (kind != FK_ZERO) coarse_publish(r, sh);
     if (pre) reinterpret_cast<int4*>(&sh.f[(i + 1) & 1])[t] = nx;
     __syncthreads();  // (2) warp partials and the next record published
+    CPROF(5);
     if (t < 32) {
       int bits = 1, err = 0;
       int64_t mx = 0, mn = 0;
@@ -258,10 +296,18 @@ __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* op
         } else {
           rc = win_finalize(f.p, sh.c, f.out.hdr, bits, mx, mn, err);
         }
+#ifdef BFP_COARSE_TIMING
+        CPROF_OP(i, 3, clock64() - _ct);
+#endif
+        CPROF(6);
         if (rc)
           sh.rc = 1;
         else if (i + 1 < n)
           coarse_prepare<M>(sh.f[(i + 1) & 1], arena, sh);
+#ifdef BFP_COARSE_TIMING
+        CPROF_OP(i + 1, 1, clock64() - _ct);
+#endif
+        CPROF(2);
       }
     }
     ++i;
@@ -274,4 +320,5 @@ __global__ void __launch_bounds__(kFusedThreads) coarse_kernel(const FusedOp* op
     if (t < (int)(sizeof(Hdr) / 16))
       reinterpret_cast<int4*>(e.ghdr)[t] = reinterpret_cast<const int4*>(arena + e.hoff)[t];
   }
+  CPROF(7);
 }

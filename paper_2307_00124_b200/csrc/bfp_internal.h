@@ -30,20 +30,23 @@ struct bfp_csr_s {
 };
 
 namespace bfpdev {
-// fused coarse-level op list entry (bfp_lib.cu: fused_kernel)
+// fused coarse-level op list entry (bfp_coarse.cuh: coarse_kernel)
 enum { FK_GEMV = 0, FK_JACOBI, FK_SCAL, FK_AXPBY, FK_RESTRICT, FK_PROLONG, FK_PCORR, FK_ZERO };
 constexpr int kFusedThreads = 512;
 constexpr int kArenaMaxBytes = 200 * 1024;  // dynamic shared memory of the fused kernel
+constexpr int kLeanMaxVec = 128;  // block headers of one fused list (lean engine)
 // one vector of an arena-resident fused op list: data (halos included) and header
 struct ArenaEntry {
   char* gbase;
   Hdr* ghdr;
-  int64_t bytes;
+  int64_t bytes;      // data bytes staged in shared memory (0: the data stays global)
   int32_t off, hoff;  // byte offsets in the CTA's shared memory
+  int32_t wb, pad;    // written by the op list: copied back when the launch ends
 };
 struct alignas(16) FusedOp {
   int32_t kind, pad;
   int64_t q;
+  uint64_t rb[2];  // bit w: the record's 8-byte word w is an arena offset (rebased on fetch)
   Vec out;
   WinParams p;
   union U {
@@ -102,7 +105,7 @@ void jacobi_coeff(int dim, int level, int64_t qc, int64_t* cm, int64_t* ce);
 int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const WinParams& p,
                int64_t q, bfp_vec_s* out, FusedOp* f);
 int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, int arena_bytes,
-                 int ebytes, cudaStream_t s);
+                 int zoff, int64_t* zglobal, int loff, int ebytes, cudaStream_t s);
 void count_launch(int n = 1);
 int64_t launches();
 // launches per kernel family (evidence of which pipelines a solve used; bfp_kernel_family_counts)

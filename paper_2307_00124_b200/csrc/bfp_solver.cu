@@ -52,7 +52,8 @@ struct PlanOp {
   std::vector<PlanOp> sub;  // OK_FUSED: the coarse-level ops run by one CTA
   FusedOp* dev = nullptr;
   ArenaEntry* arena = nullptr;  // vectors staged in shared memory (nullptr: global)
-  int n_arena = 0, arena_bytes = 0;
+  int n_arena = 0, arena_bytes = 0, zoff = 0, loff = 0;
+  int64_t* zbuf = nullptr;  // lean engine: global row buffer when shared memory is too small
   bool shard = false;  // output is a slab: partial window + collectives
   int halo = 0;        // HALO_LO / HALO_HI planes of `a` exchanged before the op
   int rep_e = kDefaultRep, rep_gs = 0;  // operator representation (reference mode)
@@ -141,6 +142,7 @@ struct RankSolver {
     for (auto& op : plan) {
       if (op.dev) cudaFree(op.dev);
       if (op.arena) cudaFree(op.arena);
+      if (op.zbuf) cudaFree(op.zbuf);
     }
     if (graph) cudaGraphExecDestroy(graph);
     for (auto* v : owned) vec_free(v);
@@ -675,10 +677,15 @@ struct RankSolver {
       return BFP_ERR_NOMEM;
     cudaMemset(d_trace, 0, sizeof(TraceRec) * std::max(n_trace, 1));
     cudaMemset(d_hist, 0, sizeof(double) * std::max(n_hist, 1));
+    std::vector<PlanOp> built;
+    built.reserve(plan.size());
     for (auto& op : plan) {
       op.p.trace = d_trace;
       op.p.hist = op.p.hist_slot >= 0 ? d_hist : nullptr;
-      if (op.kind != OK_FUSED) continue;
+      if (op.kind != OK_FUSED) {
+        built.push_back(std::move(op));
+        continue;
+      }
       std::vector<FusedOp> h(op.sub.size());
       for (size_t i = 0; i < op.sub.size(); ++i) {
         PlanOp& so = op.sub[i];
@@ -689,30 +696,46 @@ struct RankSolver {
         int rc = fused_make(fk, so.a, so.b, so.s1, so.s2, so.p, so.q, so.out, &h[i]);
         if (rc) return rc;
       }
-      build_arena(op, h);
+      if (!build_arena(op, h)) {
+        // the list's state does not fit one CTA's shared memory: one launch per op instead
+        if (err) return err;
+        for (auto& so : op.sub) built.push_back(std::move(so));
+        continue;
+      }
       if (cudaMalloc(&op.dev, sizeof(FusedOp) * h.size()) != cudaSuccess) return BFP_ERR_NOMEM;
       cudaMemcpy(op.dev, h.data(), sizeof(FusedOp) * h.size(), cudaMemcpyHostToDevice);
+      built.push_back(std::move(op));
     }
+    plan = std::move(built);
     return cudaDeviceSynchronize() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
   }
 
 
-  // Stage every vector touched by a fused op list in shared memory: rewrite the Vec and
-  // gamma-term pointers as arena byte offsets.  Left global if it does not fit.
-  void build_arena(PlanOp& op, std::vector<FusedOp>& h) {
+  // Stage the state of a fused op list in the CTA's shared memory: every block header the
+  // list touches (always), and the vectors' data while it fits (smallest first); Vec and
+  // gamma-term pointers become arena byte offsets.  Vectors the list writes are copied back
+  // when the launch ends.
+  bool build_arena(PlanOp& op, std::vector<FusedOp>& h) {
     std::vector<bfp_vec_s*> vs;
+    std::vector<char> written;
     auto find = [&](const Hdr* hp) -> bfp_vec_s* {
       for (auto* v : owned)
         if (v->hdr == hp) return v;
       return nullptr;
     };
-    auto note = [&](const Hdr* hp) {
+    auto note = [&](const Hdr* hp, bool w) {
       bfp_vec_s* v = find(hp);
-      if (v && std::find(vs.begin(), vs.end(), v) == vs.end()) vs.push_back(v);
-      return v != nullptr;
+      if (!v) return false;
+      auto it = std::find(vs.begin(), vs.end(), v);
+      if (it == vs.end()) {
+        vs.push_back(v);
+        written.push_back(w);
+      } else if (w) {
+        written[it - vs.begin()] = 1;
+      }
+      return true;
     };
     auto visit = [&](FusedOp& f, auto&& fn) {
-      fn(f.out);
       switch (f.kind) {
         case bfpdev::FK_GEMV: fn(f.u.gemv.x); fn(f.u.gemv.y); break;
         case bfpdev::FK_JACOBI: fn(f.u.jac.x); fn(f.u.jac.b); break;
@@ -723,51 +746,99 @@ struct RankSolver {
         case bfpdev::FK_PCORR: fn(f.u.pc.ec); fn(f.u.pc.y); break;
       }
     };
+    // the lean engine's row buffer (8 bytes per output element of the largest op): shared
+    // memory when it fits next to the headers, else a global scratch buffer
+    int64_t zbytes = 0;
+    if (ebytes == 4)
+      for (auto& f : h) zbytes = std::max<int64_t>(zbytes, f.out.n * 8);
+    zbytes = (zbytes + 127) / 128 * 128;
+    auto zglobal = [&]() {
+      op.zoff = 0;
+      if (zbytes && cudaMalloc(&op.zbuf, zbytes) != cudaSuccess) err = BFP_ERR_NOMEM;
+    };
     bool ok = true;
     for (auto& f : h) {
-      visit(f, [&](bfpdev::Vec& v) { ok = ok && note(v.hdr); });
+      ok = ok && note(f.out.hdr, true);
+      visit(f, [&](bfpdev::Vec& v) { ok = ok && note(v.hdr, false); });
       if (!f.p.gamma.literal)
         for (int i = 0; i < f.p.gamma.nterms; ++i)
-          if (f.p.gamma.t[i].v) ok = ok && note(f.p.gamma.t[i].v);
+          if (f.p.gamma.t[i].v) ok = ok && note(f.p.gamma.t[i].v, false);
     }
-    if (!ok) return;
-    std::vector<ArenaEntry> ar;
+    if (!ok || vs.size() > (size_t)bfpdev::kLeanMaxVec || h.size() > 30000) return false;
+    std::vector<ArenaEntry> ar(vs.size());
     int64_t off = 128;  // offset 0 is reserved (nullptr gamma terms)
-    for (auto* v : vs) {
-      ArenaEntry e;
-      e.gbase = v->base;
-      e.ghdr = v->hdr;
-      e.bytes = ((v->span + 2 * v->halo) * v->ebytes + 15) / 16 * 16;
-      e.off = (int32_t)off;
-      off += (e.bytes + 127) / 128 * 128;
+    for (size_t k = 0; k < vs.size(); ++k) {
+      ArenaEntry& e = ar[k];
+      memset(&e, 0, sizeof(e));
+      e.gbase = vs[k]->base;
+      e.ghdr = vs[k]->hdr;
+      e.wb = written[k];
       e.hoff = (int32_t)off;
       off += (sizeof(Hdr) + 127) / 128 * 128;
-      ar.push_back(e);
     }
-    if (off > bfpdev::kArenaMaxBytes) return;
-    auto remap = [&](bfpdev::Vec& v) {
-      for (size_t k = 0; k < vs.size(); ++k)
-        if (vs[k]->hdr == v.hdr) {
-          v.data = (void*)(uintptr_t)(ar[k].off + vs[k]->halo * vs[k]->ebytes);
-          v.hdr = (Hdr*)(uintptr_t)ar[k].hoff;
-          return;
-        }
+    // the lean engine's per-op log
+    op.loff = (int)off;
+    if (ebytes == 4) off += ((int64_t)h.size() * 48 + 127) / 128 * 128;
+    if (off > bfpdev::kArenaMaxBytes) return false;
+    if (off + zbytes <= bfpdev::kArenaMaxBytes) {
+      op.zoff = (int)off;
+      off += zbytes;
+    } else {
+      zglobal();
+    }
+    std::vector<size_t> order(vs.size());
+    for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+    auto vbytes = [&](size_t k) {
+      return ((vs[k]->span + 2 * vs[k]->halo) * vs[k]->ebytes + 15) / 16 * 16;
     };
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t x, size_t y) { return vbytes(x) < vbytes(y); });
+    for (size_t k : order) {
+      const int64_t b = vbytes(k), pad = (b + 127) / 128 * 128;
+      if (off + pad > bfpdev::kArenaMaxBytes) break;
+      ar[k].bytes = b;
+      ar[k].off = (int32_t)off;
+      off += pad;
+    }
     for (auto& f : h) {
+      // every rewritten pointer is marked in f.rb (the lean engine rebases on fetch)
+      auto mark = [&](const void* field) {
+        const size_t w = ((const char*)field - (const char*)&f) / 8;
+        f.rb[w >> 6] |= 1ull << (w & 63);
+      };
+      auto remap = [&](bfpdev::Vec& v) {
+        for (size_t k = 0; k < vs.size(); ++k)
+          if (vs[k]->hdr == v.hdr) {
+            if (ar[k].bytes) {
+              v.data = (void*)(uintptr_t)(ar[k].off + vs[k]->halo * vs[k]->ebytes);
+              mark(&v.data);
+            }
+            v.hdr = (Hdr*)(uintptr_t)ar[k].hoff;
+            mark(&v.hdr);
+            return;
+          }
+      };
       if (!f.p.gamma.literal)
         for (int i = 0; i < f.p.gamma.nterms; ++i)
           if (f.p.gamma.t[i].v)
             for (size_t k = 0; k < vs.size(); ++k)
               if (vs[k]->hdr == f.p.gamma.t[i].v) {
                 f.p.gamma.t[i].v = (const Hdr*)(uintptr_t)ar[k].hoff;
+                mark(&f.p.gamma.t[i].v);
                 break;
               }
+      remap(f.out);
       visit(f, remap);
     }
-    if (cudaMalloc(&op.arena, sizeof(ArenaEntry) * ar.size()) != cudaSuccess) return;
+    static_assert(sizeof(FusedOp) <= 128 * 8, "FusedOp::rb marks at most 128 words");
+    if (cudaMalloc(&op.arena, sizeof(ArenaEntry) * ar.size()) != cudaSuccess) {
+      err = BFP_ERR_NOMEM;
+      return false;
+    }
     cudaMemcpy(op.arena, ar.data(), sizeof(ArenaEntry) * ar.size(), cudaMemcpyHostToDevice);
     op.n_arena = (int)ar.size();
     op.arena_bytes = (int)off;
+    return err == 0;
   }
 
   // one op on this rank; `part` != nullptr runs a windowed op as a partial window
@@ -801,7 +872,7 @@ struct RankSolver {
         return BFP_OK;
       case OK_FUSED:
         return fused_launch(op.dev, (int)op.sub.size(), op.arena, op.n_arena, op.arena_bytes,
-                            ebytes, s);
+                            op.zoff, op.zbuf, op.loff, ebytes, s);
     }
     return BFP_ERR_ARG;
   }

@@ -1,5 +1,5 @@
 // op_fused.cu -- fused single-CTA op lists (shared-memory arena) for coarse levels.
-#include "bfp_kernels.cuh"
+#include "bfp_lean.cuh"
 
 namespace bfp {
 
@@ -46,20 +46,21 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
 }
 
 int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, int arena_bytes,
-                 int ebytes, cudaStream_t s) {
+                 int zoff, int64_t* zglobal, int loff, int ebytes, cudaStream_t s) {
   static std::atomic<int> attr[kMaxDev];  // function attributes are per device
   per_device(attr, [] {
-    cudaFuncSetAttribute(fused_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(lean_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kArenaMaxBytes);
-    cudaFuncSetAttribute(fused_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(coarse_kernel<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kArenaMaxBytes);
     return 1;
   });
+  // int32 storage: the lean engine (generic path inside); int64 storage: the generic engine
   if (ebytes == 4)
-    launch_pdl(fused_kernel<int32_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
-               nar);
+    launch_pdl(lean_kernel, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar, nar, zoff,
+               zglobal, loff);
   else
-    launch_pdl(fused_kernel<int64_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
+    launch_pdl(coarse_kernel<int64_t>, 1, kFusedThreads, (size_t)arena_bytes, s, d_ops, n, d_ar,
                nar);
   count_launch();
   count_family(FAM_FUSED);
@@ -67,3 +68,19 @@ int fused_launch(const FusedOp* d_ops, int n, const ArenaEntry* d_ar, int nar, i
 }
 
 }  // namespace bfp
+
+#ifdef BFP_COARSE_TIMING
+// measurement builds: per-phase clock totals of coarse_kernel (read and reset)
+extern "C" int bfp_dbg_coarse(long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_coarse_prof, sizeof(long long) * 16);
+  long long z[16] = {};
+  cudaMemcpyToSymbol(g_coarse_prof, z, sizeof(z));
+  return 16;
+}
+extern "C" int bfp_dbg_coarse_ops(int* out, int n) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_coarse_ops, sizeof(int) * 4 * (size_t)n);
+  return n;
+}
+#endif
