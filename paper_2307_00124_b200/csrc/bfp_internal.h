@@ -43,10 +43,30 @@ struct ArenaEntry {
   int32_t off, hoff;  // byte offsets in the CTA's shared memory
   int32_t wb, pad;    // written by the op list: copied back when the launch ends
 };
+// The lean engine's digest of an op record (host-filled, bfp_solver.cu): everything its
+// control lane and workers need that is static, in one 64-byte block.
+struct LeanRec {
+  uint8_t ok;           // statically eligible for the fast path (lean_static_ok)
+  uint8_t vout, va, vb; // arena vector ids of the output and the two operands (0xff: none)
+  uint8_t gv[3];        // vector ids of the gamma terms (0xff: X = 1)
+  uint8_t ng;           // gamma terms
+  int16_t w_out, nnq;
+  int32_t n4;           // 4-groups of the output
+  int8_t dim, l;
+  int8_t nnq_next;      // the next op of the list is nnqcomp
+  int8_t pad1;
+  int32_t ea;           // e_A (gemv), 2l (jacobi), e_R (restrict), e_P (prolong / pcorr)
+  int32_t am, ae, bm, be;  // coefficients: gemv / axpby / pcorr alpha, beta; jacobi / scal c
+  const int32_t* x;     // operand data (arena offsets until rebased)
+  const int32_t* y;
+  int32_t* out;
+};
+static_assert(sizeof(LeanRec) == 64, "LeanRec is four 16-byte chunks");
 struct alignas(16) FusedOp {
   int32_t kind, pad;
   int64_t q;
   uint64_t rb[2];  // bit w: the record's 8-byte word w is an arena offset (rebased on fetch)
+  LeanRec lr;
   Vec out;
   WinParams p;
   union U {

@@ -27,8 +27,15 @@
 //     else -- wide rows, reference-mode operators, exact or literal gamma rules, exponents out
 //     of range -- takes the generic path of bfp_coarse.cuh inside the same launch (cold
 //     code), with the block headers it reads materialised from the log first.
-//   * op records are prefetched two ops ahead and their arena pointers rebased by the
-//     prefetching threads (FusedOp::rb marks the pointer words).
+//   * the host digests every record into a 64-byte LeanRec (static eligibility, vector ids,
+//     coefficients, data pointers), so the control lane's setup has no per-kind record
+//     parsing; it runs in two halves: PRE (record digest, operand states, gamma producers ->
+//     registers) while the workers run the previous op's body, POST (alignment, widths,
+//     window) after the previous op's core finalize, with that op's fresh output state
+//     forwarded in registers.
+//   * op records are prefetched three ops ahead through registers (loads issued during one
+//     op, stored to shared memory during the next: no thread waits on the load) and their
+//     arena pointers rebased on the way (FusedOp::rb marks the pointer words).
 #pragma once
 #include "bfp_coarse.cuh"
 
@@ -36,29 +43,30 @@ namespace bfpdev {
 
 constexpr int kLeanWorkers = kFusedThreads - 32;
 
-struct LeanOp {  // window context of a fast op, published by the control lane
-  int fast, kind, nnq;
-  int needmm;    // qcomp: reduce max / min of z in the body (the next op is nnqcomp)
-  int dim, l;
+// dynamic window context of a fast op, published by the control lane (the static part is
+// the record's LeanRec)
+struct LeanDyn {
+  int fast;
   int sx, sy;    // pending shifts of the operands
   int P, Q;      // gemv / pcorr: z = X P + Q Y; jacobi: P1 and s2
   int swap;      // gemv / pcorr: operands swapped (d < 0); jacobi: neg1
-  unsigned cm;   // jacobi: c.m
-  int am, bm, d; // axpby / scal: coefficients and alignment
-  int lam, wout; // nnqcomp window
-  int n4;        // 4-groups of the output
-  const int32_t *x, *y;
-  int32_t* out;
+  int d;         // axpby: alignment
+  int lam;       // nnqcomp window
+  int needmm;    // reduce max / min in the body (nnqcomp, or qcomp before an nnqcomp op)
 };
 
-// compact state of a vector for the control lane's setups
-struct FH {
-  int e, s, bits, eff;  // exponent, pending shift, width (0: all zero), eff_bits
-  int ok;
+// compact state of a vector for the control lane's setups (16 bytes: one shared load)
+struct alignas(16) FH {
+  int e, s;    // exponent, pending shift
+  int bits;    // width, 0: all zero
+  int effok;   // eff_bits | ok << 8
 };
+__device__ __forceinline__ FH make_fh(int e, int s, int bits, int eff, bool ok) {
+  return FH{e, s, bits, eff | ((int)ok << 8)};
+}
 // one record per op of the list (shared memory)
 enum { LOG_NONE = 0, LOG_FASTQ, LOG_FASTN, LOG_GENERIC, LOG_ZERO };
-struct LogRec {
+struct alignas(16) LogRec {
   int e_out, lam, mu;  // block exponent, lam_out, mu*
   int mx, mn;          // max / min of the stored mantissas (pending shift applied)
   int gm, ge;          // nnqcomp: gamma
@@ -71,7 +79,7 @@ struct LogRec {
 static_assert(sizeof(LogRec) == 48, "LogRec layout (host sizes the log)");
 
 struct LeanShared {
-  LeanOp op;
+  LeanDyn dyn;
   int lam_store;  // lam_out of the op being stored
   unsigned long long orv[kCoarseWarps];
   long long mx[kCoarseWarps], mn[kCoarseWarps];
@@ -187,25 +195,18 @@ __device__ __forceinline__ NormSrc lean_norm(const LeanShared& ls, const LogRec*
   return NormSrc{a > b ? a : b, r.e_out};
 }
 // gamma of a config-mode rule from the norms of its terms; the fast
-// path only admits rules with 32-bit coefficients (lean_rule_ok)
-__device__ __forceinline__ bool lean_rule_ok(const GammaRule& g) {
-  if (g.literal || g.exact || g.nterms > 3) return false;
-  for (int i = 0; i < g.nterms; ++i)
-    if (g.t[i].cm < 0 || g.t[i].cm > 0xffffffffll || !small_e(g.t[i].ce)) return false;
-  return true;
-}
-template <typename VidFn>
-__device__ __forceinline__ void lean_gamma(const GammaRule& g, const LeanShared& ls,
-                                           const LogRec* log, const short* prod, VidFn vid,
-                                           int& gm, int& ge) {
+// path only admits rules with 32-bit coefficients (LeanRec::ok)
+__device__ __forceinline__ void lean_gamma(const GammaRule& g, const LeanRec& lr,
+                                           const LeanShared& ls, const LogRec* log,
+                                           const short* prod, int& gm, int& ge) {
   G32 acc{0, 0};
   for (int i = 0; i < g.nterms; ++i) {
     const GTerm& t = g.t[i];
     G32 x;
-    if (t.v == nullptr) {
+    if (lr.gv[i] == 0xff) {
       x = G32{1 << 14, -14};
     } else {
-      const NormSrc ns = lean_norm(ls, log, vid(t.v), prod[i]);
+      const NormSrc ns = lean_norm(ls, log, lr.gv[i], prod[i]);
       x = t.kind == 0 ? g32_from(ns.mag, ns.e) : (ns.mag ? g32_from(1u, ns.e) : G32{0, 0});
     }
     if (t.cm != 0) x = g32_mul(g32_from((unsigned)t.cm, (int)t.ce), x);
@@ -220,7 +221,51 @@ __device__ __forceinline__ void lean_gamma(const GammaRule& g, const LeanShared&
   }
 }
 
-// ---- the control lane's per-op state (registers) ------------------------------------
+__device__ __forceinline__ int clog2_4dim(int dim) { return dim == 1 ? 2 : (dim == 2 ? 3 : 4); }
+
+// ---- the control lane's setup, first half: everything that does not depend on the op in
+// flight (registers only; runs while the workers are in the previous op's body) ----------
+struct LeanPre {
+  int kind, ok, nnq, needmm, w_out;
+  int vout, va, vb;
+  int dim, l, ea, am, ae, bm, be;
+  FH ha, hb;
+  int gv[3], gok;
+  short prod[3];
+};
+__device__ __forceinline__ void lean_pre(const FusedOp& f, const FusedOp* next,
+                                         const LeanShared& ls, LeanPre& q) {
+  const LeanRec lr = f.lr;
+  q.kind = f.kind;
+  q.ok = lr.ok;
+  q.nnq = lr.nnq;
+  // a qcomp op followed by an nnqcomp op reduces max / min in its body: the next setup
+  // needs them (gamma, width) before this op's store phase has finished
+  (void)next;
+  q.needmm = lr.nnq || lr.nnq_next;
+  q.w_out = lr.w_out;
+  q.vout = lr.vout;
+  q.va = lr.va;
+  q.vb = lr.vb;
+  q.dim = lr.dim;
+  q.l = lr.l;
+  q.ea = lr.ea;
+  q.am = lr.am, q.ae = lr.ae, q.bm = lr.bm, q.be = lr.be;
+  q.ha = lr.va != 0xff ? ls.fh[lr.va] : FH{0, 0, 0, 0x101};
+  q.hb = lr.vb != 0xff ? ls.fh[lr.vb] : FH{0, 0, 0, 0x101};
+  q.gok = 1;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    q.gv[i] = lr.gv[i];
+    q.prod[i] = -1;
+    if (lr.gv[i] != 0xff) {
+      q.prod[i] = (short)ls.lastw[lr.gv[i]];
+      q.gok &= ls.fh[lr.gv[i]].effok >> 8;
+    }
+  }
+}
+
+// the control lane's per-op state (registers)
 struct LeanState {
   int e_star, zd;  // template exponent, zero-term elision shift
   int w_out, nnq;
@@ -229,283 +274,212 @@ struct LeanState {
   short prod[3];
 };
 
-__device__ __forceinline__ int clog2_4dim(int dim) { return dim == 1 ? 2 : (dim == 2 ? 3 : 4); }
-
-// Lean setup of op record f (control lane): true when the op runs on the fast path.
-// Restates the setups of bfp_ops.cuh (template exponent, zero-term elision, width bounds and
-// the `narrow` conditions) in 32-bit arithmetic on the compact vector states; every rejected
-// case takes the generic path.
-template <typename VidFn>
-__device__ __forceinline__ bool lean_setup(const FusedOp& f, const FusedOp* next, LeanShared& ls,
-                                           const LogRec* log, VidFn vid, LeanState& st) {
-  LeanOp& o = ls.op;
-  const WinParams& p = f.p;
-  o.kind = f.kind;
-  o.out = (int32_t*)f.out.data;
-  o.n4 = (int)(f.out.n >> 2);
-  o.nnq = 0;
-  o.needmm = 0;
-  st.vout = vid(f.out.hdr);
-  st.nnq = 0;
-  if (f.kind == FK_ZERO) return true;
-  if (p.part || p.force || p.w_tmp > 32 || p.w_out > 32 || p.w_out < 1) return false;
-  if (p.mode != MODE_QCOMP && p.mode != MODE_NNQ) return false;
-  if (!lean_rule_ok(p.gamma)) return false;
-  st.w_out = (int)p.w_out;
-  st.nnq = p.mode == MODE_NNQ;
-  o.nnq = st.nnq;
-  // a qcomp op followed by an nnqcomp op reduces max / min in its body: the next setup
-  // needs them (gamma, width) before this op's store phase has finished
-  o.needmm = !st.nnq && next != nullptr && next->p.mode == MODE_NNQ;
-  o.wout = st.w_out;
+// ---- second half: alignment, width bounds and the `narrow` conditions of bfp_ops.cuh in
+// 32-bit arithmetic, from the pre-loaded state with the previous op's output forwarded
+// (fv: its vector id, ff: its fresh state, fi: its op index).  True: the op is fast. ------
+__device__ __forceinline__ bool lean_post(const FusedOp& f, const LeanPre& qs, int fv,
+                                          const FH& ff, int fi, LeanShared& ls,
+                                          const LogRec* log, LeanState& st) {
+  LeanPre q = qs;
+  LeanDyn o;
+  o.sx = o.sy = o.P = o.Q = o.swap = o.d = o.lam = 0;
+  o.needmm = q.needmm;
+  st.vout = q.vout;
+  st.nnq = q.nnq;
+  st.w_out = q.w_out;
   st.zd = 0;
-  const FH* fh = ls.fh;
-  switch (f.kind) {
-    case FK_GEMV: {
-      const GemvOp& g = f.u.gemv;
-      if (g.st9 || g.gs || g.l < 2 || g.z0 || !small_e(g.al.e) || !small_e(g.be.e)) return false;
-      if (g.al.m != (int)g.al.m || g.be.m != (int)g.be.m) return false;
-      const FH hx = fh[vid(g.x.hdr)], hy = fh[vid(g.y.hdr)];
-      if (!hx.ok || !hy.ok) return false;
-      const int am = (int)g.al.m, bm = (int)g.be.m;
-      int dd, es, zd;
-      lean_align((int)g.al.e + g.ea + hx.e, (int)g.be.e + hy.e, am == 0 || hx.bits == 0,
-                 bm == 0 || hy.bits == 0, dd, es, zd);
-      const int bg = hx.bits ? hx.bits + clog2_4dim(g.dim) + 1 : 0, by = hy.bits;
-      const int nd = lean_cbits(am, bg, bm, by, dd);
-      const int ad = dd >= 0 ? dd : -dd;
-      const int pm = dd >= 0 ? am : bm, qm = dd >= 0 ? bm : am;
-      const int bx_ = dd >= 0 ? bg : by, by_ = dd >= 0 ? by : bg;
-      const int mp = msb32(pm), mq = msb32(qm);
-      const bool nar = bg <= 31 && by <= 31 && (by_ == 0 || mq + by_ <= 32) && nd <= 63 &&
-                       ad <= 30 && mp + ad <= 32 && (bx_ == 0 || mp + ad + bx_ <= 63);
-      if (!nar) return false;
-      st.e_star = es;
-      st.zd = zd;
-      o.dim = g.dim;
-      o.l = g.l;
-      o.sx = hx.s;
-      o.sy = hy.s;
-      o.P = pm << ad;
-      o.Q = qm;
-      o.swap = dd < 0;
-      o.x = (const int32_t*)g.x.data;
-      o.y = (const int32_t*)g.y.data;
-      break;
+  bool fast = q.ok;
+  if (q.kind != FK_ZERO) {
+    if (q.va == fv) q.ha = ff;
+    if (q.vb == fv) q.hb = ff;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      st.prod[i] = q.prod[i];
+      if (q.gv[i] == fv) {
+        st.prod[i] = (short)fi;
+        q.gok &= ff.effok >> 8;
+      }
     }
-    case FK_JACOBI: {
-      const JacobiOp& j = f.u.jac;
-      if (j.l < 2 || j.z0 || !small_e(j.c.e) || j.c.m < 0 || j.c.m > 0x7fffffff) return false;
-      const FH hx = fh[vid(j.x.hdr)], hb = fh[vid(j.b.hdr)];
-      if (!hx.ok || !hb.ok) return false;
-      const int cm = (int)j.c.m, ce = (int)j.c.e;
-      const int ge = 2 * j.l + hx.e;
-      const bool zx = hx.bits == 0, zb = hb.bits == 0;
-      const int gb = ge < hb.e ? ge : hb.e;
-      const int es_ref = hx.e < ce + gb ? hx.e : ce + gb;
-      int dd1, er, zr, dd2, es;
-      lean_align(ge, hb.e, zx, zb, dd1, er, zr);
-      lean_align(hx.e, ce + er, zx, cm == 0 || (zx && zb), dd2, es, zr);
-      const int bx = hx.bits, bbb = hb.bits;
-      const int bg = bx ? bx + clog2_4dim(j.dim) + 1 : 0;
-      const int br = lean_cbits(-1, bg, 1, bbb, dd1);
-      const int nd = lean_cbits(1, bx, cm, br, dd2);
-      const bool nar = bg <= 31 && bbb <= 31 && nd <= 63 && dd1 >= -30 && dd1 <= 30 &&
-                       dd2 >= 0 && dd2 <= 62 && dd2 != 31 && bx <= 31 &&
-                       (bx == 0 || bx + dd2 <= 63);
-      if (!nar) return false;
-      st.e_star = es;
-      st.zd = es - es_ref;
-      o.dim = j.dim;
-      o.l = j.l;
-      o.sx = hx.s;
-      o.sy = hb.s;
-      o.swap = dd1 < 0;
-      o.P = dd1 < 0 ? (1 << -dd1) : -(1 << dd1);
-      o.Q = dd2;
-      o.cm = (unsigned)cm;
-      o.x = (const int32_t*)j.x.data;
-      o.y = (const int32_t*)j.b.data;
-      break;
+    const FH hx = q.ha, hy = q.hb;
+    const int effx = hx.effok & 0xff;
+    fast = fast && q.gok && (hx.effok >> 8) && (hy.effok >> 8);
+    switch (q.kind) {
+      case FK_GEMV: {
+        const int am = q.am, bm = q.bm;
+        int dd, es, zd;
+        lean_align(q.ae + q.ea + hx.e, q.be + hy.e, am == 0 || hx.bits == 0,
+                   bm == 0 || hy.bits == 0, dd, es, zd);
+        const int bg = hx.bits ? hx.bits + clog2_4dim(q.dim) + 1 : 0, by = hy.bits;
+        const int nd = lean_cbits(am, bg, bm, by, dd);
+        const int ad = dd >= 0 ? dd : -dd;
+        const int pm = dd >= 0 ? am : bm, qm = dd >= 0 ? bm : am;
+        const int bx_ = dd >= 0 ? bg : by, by_ = dd >= 0 ? by : bg;
+        const int mp = msb32(pm), mq = msb32(qm);
+        fast = fast && bg <= 31 && by <= 31 && (by_ == 0 || mq + by_ <= 32) && nd <= 63 &&
+               ad <= 30 && mp + ad <= 32 && (bx_ == 0 || mp + ad + bx_ <= 63);
+        st.e_star = es;
+        st.zd = zd;
+        o.P = pm << (ad & 31);
+        o.Q = qm;
+        o.swap = dd < 0;
+        break;
+      }
+      case FK_JACOBI: {
+        const int cm = q.am, ce = q.ae;
+        const int ge = q.ea + hx.e;  // 2l + e_x
+        const bool zx = hx.bits == 0, zb = hy.bits == 0;
+        const int gb = ge < hy.e ? ge : hy.e;
+        const int es_ref = hx.e < ce + gb ? hx.e : ce + gb;
+        int dd1, er, zr, dd2, es;
+        lean_align(ge, hy.e, zx, zb, dd1, er, zr);
+        lean_align(hx.e, ce + er, zx, cm == 0 || (zx && zb), dd2, es, zr);
+        const int bx = hx.bits, bbb = hy.bits;
+        const int bg = bx ? bx + clog2_4dim(q.dim) + 1 : 0;
+        const int br = lean_cbits(-1, bg, 1, bbb, dd1);
+        const int nd = lean_cbits(1, bx, cm, br, dd2);
+        fast = fast && bg <= 31 && bbb <= 31 && nd <= 63 && dd1 >= -30 && dd1 <= 30 && dd2 >= 0 &&
+               dd2 <= 62 && dd2 != 31 && bx <= 31 && (bx == 0 || bx + dd2 <= 63);
+        st.e_star = es;
+        st.zd = es - es_ref;
+        const int a1 = (dd1 < 0 ? -dd1 : dd1) & 31;
+        o.swap = dd1 < 0;
+        o.P = dd1 < 0 ? (1 << a1) : -(1 << a1);
+        o.Q = dd2;
+        break;
+      }
+      case FK_SCAL:
+        st.e_star = q.ae + hx.e;
+        break;
+      case FK_AXPBY: {
+        int dd, es, zd;
+        lean_align(q.ae + hx.e, q.be + hy.e, q.am == 0 || hx.bits == 0,
+                   q.bm == 0 || hy.bits == 0, dd, es, zd);
+        // (a shift count beyond 62 only meets a zero operand)
+        fast = fast && lean_cbits(q.am, hx.bits, q.bm, hy.bits, dd) <= 63;
+        st.e_star = es;
+        st.zd = zd;
+        o.d = dd;
+        break;
+      }
+      case FK_RESTRICT:
+        fast = fast && effx + 2 * q.dim + 2 <= 31;
+        st.e_star = q.ea + hx.e;
+        break;
+      case FK_PROLONG:
+        fast = fast && effx + q.dim + 2 <= 31;
+        st.e_star = q.ea + hx.e;
+        break;
+      case FK_PCORR: {
+        int dd, es, zd;
+        lean_align(q.ae + q.ea + hx.e, q.be + hy.e, hx.bits == 0, hy.bits == 0, dd, es, zd);
+        const int bg = hx.bits ? hx.bits + q.dim + 2 : 0, by = hy.bits;
+        const int nd = lean_cbits(1, bg, 1, by, dd);
+        const int ad = dd >= 0 ? dd : -dd;
+        fast = fast && nd <= 63 && bg <= 31 && by <= 31 && ad <= 30;
+        st.e_star = es;
+        st.zd = zd;
+        o.swap = dd < 0;
+        o.P = 1 << (ad & 31);
+        break;
+      }
+      default: fast = false;
     }
-    case FK_SCAL: {
-      const ScalOp& s = f.u.scal;
-      if (!small_e(s.c.e) || s.c.m != (int)s.c.m) return false;
-      const FH hr = fh[vid(s.r.hdr)];
-      if (!hr.ok) return false;
-      st.e_star = (int)s.c.e + hr.e;
-      o.sx = hr.s;
-      o.am = (int)s.c.m;
-      o.x = (const int32_t*)s.r.data;
-      break;
-    }
-    case FK_AXPBY: {
-      const AxpbyOp& a = f.u.axpby;
-      if (!small_e(a.al.e) || !small_e(a.be.e) || a.al.m != (int)a.al.m || a.be.m != (int)a.be.m)
-        return false;
-      const FH hx = fh[vid(a.x.hdr)], hy = fh[vid(a.y.hdr)];
-      if (!hx.ok || !hy.ok) return false;
-      const int am = (int)a.al.m, bm = (int)a.be.m;
-      int dd, es, zd;
-      lean_align((int)a.al.e + hx.e, (int)a.be.e + hy.e, am == 0 || hx.bits == 0,
-                 bm == 0 || hy.bits == 0, dd, es, zd);
-      const int nd = lean_cbits(am, hx.bits, bm, hy.bits, dd);
-      if (nd > 63) return false;  // (a shift count beyond 62 only meets a zero operand)
-      st.e_star = es;
-      st.zd = zd;
-      o.sx = hx.s;
-      o.sy = hy.s;
-      o.am = am;
-      o.bm = bm;
-      o.d = dd;
-      o.x = (const int32_t*)a.x.data;
-      o.y = (const int32_t*)a.y.data;
-      break;
-    }
-    case FK_RESTRICT: {
-      const RestrictOp& r = f.u.rst;
-      if (r.gs || r.zc || r.l < 3) return false;
-      const FH hr = fh[vid(r.r.hdr)];
-      if (!hr.ok || hr.eff + 2 * r.dim + 2 > 31) return false;
-      st.e_star = r.er + hr.e;
-      o.dim = r.dim;
-      o.l = r.l;
-      o.sx = hr.s;
-      o.x = (const int32_t*)r.r.data;
-      break;
-    }
-    case FK_PROLONG: {
-      const ProlongOp& q = f.u.pro;
-      if (q.gs || q.zf || q.zp || q.l < 3) return false;
-      const FH hc = fh[vid(q.xc.hdr)];
-      if (!hc.ok || hc.eff + q.dim + 2 > 31) return false;
-      st.e_star = q.ep + hc.e;
-      o.dim = q.dim;
-      o.l = q.l;
-      o.sx = hc.s;
-      o.x = (const int32_t*)q.xc.data;
-      break;
-    }
-    case FK_PCORR: {
-      const ProlongCorrectOp& q = f.u.pc;
-      if (q.gs || q.zf || q.zp || q.l < 3 || q.al.m != 1 || q.be.m != 1 || !small_e(q.al.e) ||
-          !small_e(q.be.e))
-        return false;
-      const FH hc = fh[vid(q.ec.hdr)], hy = fh[vid(q.y.hdr)];
-      if (!hc.ok || !hy.ok) return false;
-      int dd, es, zd;
-      lean_align((int)q.al.e + q.ep + hc.e, (int)q.be.e + hy.e, hc.bits == 0, hy.bits == 0, dd, es,
-                 zd);
-      const int bg = hc.bits ? hc.bits + q.dim + 2 : 0, by = hy.bits;
-      const int nd = lean_cbits(1, bg, 1, by, dd);
-      const int ad = dd >= 0 ? dd : -dd;
-      if (!(nd <= 63 && bg <= 31 && by <= 31 && ad <= 30)) return false;
-      st.e_star = es;
-      st.zd = zd;
-      o.dim = q.dim;
-      o.l = q.l;
-      o.sx = hc.s;
-      o.sy = hy.s;
-      o.swap = dd < 0;
-      o.P = 1 << ad;
-      o.x = (const int32_t*)q.ec.data;
-      o.y = (const int32_t*)q.y.data;
-      break;
-    }
-    default: return false;
-  }
-  // producers of the gamma terms as of now (the rule is evaluated when the list ends)
-  for (int i = 0; i < 3; ++i) {
-    st.prod[i] = -1;
-    if (i < p.gamma.nterms && p.gamma.t[i].v) {
-      const int v = vid(p.gamma.t[i].v);
-      if (!fh[v].ok) return false;
-      st.prod[i] = (short)ls.lastw[v];
+    o.sx = hx.s;
+    o.sy = hy.s;
+    if (fast && st.nnq) {  // nnqcomp: gamma fixes the window before the body (:189-212)
+      lean_gamma(f.p.gamma, f.lr, ls, log, st.prod, st.gm, st.ge);
+      const int lam = msb32(st.gm) + st.ge - st.e_star - st.w_out;
+      fast = lam >= -62 && lam <= 1000;
+      o.lam = lam;
     }
   }
-  if (st.nnq) {  // nnqcomp: gamma fixes the window before the body (P/src/blas.cpp:189-212)
-    lean_gamma(p.gamma, ls, log, st.prod, vid, st.gm, st.ge);
-    const int lam = msb32(st.gm) + st.ge - st.e_star - st.w_out;
-    if (lam < -62 || lam > 1000) return false;
-    o.lam = lam;
-  }
-  return true;
+  o.fast = fast;
+  ls.dyn = o;
+  return fast;
+}
+
+// data pointers of a record are arena byte offsets (below kArenaMaxBytes) or global
+template <typename T> __device__ __forceinline__ T* lean_ptr(T* p, char* arena) {
+  return (uintptr_t)p < (uintptr_t)kArenaMaxBytes ? reinterpret_cast<T*>(arena + (uintptr_t)p) : p;
 }
 
 // ---- worker bodies: 4 exact rows of one output group --------------------------------
-__device__ __forceinline__ void lean_eval4(const LeanOp& c, int o, int64_t z[4]) {
-  switch (c.kind) {
+__device__ __forceinline__ void lean_eval4(int kind, const LeanRec& s, const LeanDyn& c, int o,
+                                           int64_t z[4]) {
+  const int dim = s.dim, l = s.l;
+  switch (kind) {
     case FK_GEMV: {
       Vec xv;
-      xv.data = (void*)c.x;
+      xv.data = (void*)s.x;
       int g[4], cc[4], yv[4];
-      stencil4_32<false>(xv, c.sx, c.dim, c.l, o, g, cc);
-      const int4 t = *reinterpret_cast<const int4*>(c.y + o);
+      stencil4_32<false>(xv, c.sx, dim, l, o, g, cc);
+      const int4 t = *reinterpret_cast<const int4*>(s.y + o);
       yv[0] = t.x >> c.sy, yv[1] = t.y >> c.sy, yv[2] = t.z >> c.sy, yv[3] = t.w >> c.sy;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int X = c.swap ? yv[j] : g[j], Y = c.swap ? g[j] : yv[j];
         z[j] = (int64_t)X * (int64_t)c.P + (int64_t)(c.Q * Y);
       }
-      const unsigned mN = (1u << c.l) - 1;
+      const unsigned mN = (1u << l) - 1;
       if (((unsigned)o & mN) == mN - 3) z[3] = 0;
-      if (plane_pad(c.dim, c.l, 0, o)) z[0] = z[1] = z[2] = z[3] = 0;
+      if (plane_pad(dim, l, 0, o)) z[0] = z[1] = z[2] = z[3] = 0;
       break;
     }
     case FK_JACOBI: {
       Vec xv;
-      xv.data = (void*)c.x;
+      xv.data = (void*)s.x;
       int g[4], cx[4], bv[4];
-      stencil4_32<false>(xv, c.sx, c.dim, c.l, o, g, cx);
-      const int4 t = *reinterpret_cast<const int4*>(c.y + o);
+      stencil4_32<false>(xv, c.sx, dim, l, o, g, cx);
+      const int4 t = *reinterpret_cast<const int4*>(s.y + o);
       bv[0] = t.x >> c.sy, bv[1] = t.y >> c.sy, bv[2] = t.z >> c.sy, bv[3] = t.w >> c.sy;
+      const uint64_t cm = (uint64_t)(unsigned)s.am;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int X = c.swap ? bv[j] : g[j], Y = c.swap ? -g[j] : bv[j];
         const int64_t r = (int64_t)X * (int64_t)c.P + (int64_t)Y;
-        const int64_t cr = (int64_t)((uint64_t)r * (uint64_t)c.cm);
+        const int64_t cr = (int64_t)((uint64_t)r * cm);
         z[j] = mad_pow2(cx[j], c.Q, cr);
       }
-      const unsigned mN = (1u << c.l) - 1;
+      const unsigned mN = (1u << l) - 1;
       if (((unsigned)o & mN) == mN - 3) z[3] = 0;
-      if (plane_pad(c.dim, c.l, 0, o)) z[0] = z[1] = z[2] = z[3] = 0;
+      if (plane_pad(dim, l, 0, o)) z[0] = z[1] = z[2] = z[3] = 0;
       break;
     }
     case FK_SCAL: {
-      const int4 t = *reinterpret_cast<const int4*>(c.x + o);
-      z[0] = (int64_t)c.am * (int64_t)(t.x >> c.sx);
-      z[1] = (int64_t)c.am * (int64_t)(t.y >> c.sx);
-      z[2] = (int64_t)c.am * (int64_t)(t.z >> c.sx);
-      z[3] = (int64_t)c.am * (int64_t)(t.w >> c.sx);
+      const int4 t = *reinterpret_cast<const int4*>(s.x + o);
+      z[0] = (int64_t)s.am * (int64_t)(t.x >> c.sx);
+      z[1] = (int64_t)s.am * (int64_t)(t.y >> c.sx);
+      z[2] = (int64_t)s.am * (int64_t)(t.z >> c.sx);
+      z[3] = (int64_t)s.am * (int64_t)(t.w >> c.sx);
       break;
     }
     case FK_AXPBY: {
-      const int4 a = *reinterpret_cast<const int4*>(c.x + o);
-      const int4 b = *reinterpret_cast<const int4*>(c.y + o);
-      z[0] = combine32(c.am, a.x >> c.sx, c.bm, b.x >> c.sy, c.d);
-      z[1] = combine32(c.am, a.y >> c.sx, c.bm, b.y >> c.sy, c.d);
-      z[2] = combine32(c.am, a.z >> c.sx, c.bm, b.z >> c.sy, c.d);
-      z[3] = combine32(c.am, a.w >> c.sx, c.bm, b.w >> c.sy, c.d);
+      const int4 a = *reinterpret_cast<const int4*>(s.x + o);
+      const int4 b = *reinterpret_cast<const int4*>(s.y + o);
+      z[0] = combine32(s.am, a.x >> c.sx, s.bm, b.x >> c.sy, c.d);
+      z[1] = combine32(s.am, a.y >> c.sx, s.bm, b.y >> c.sy, c.d);
+      z[2] = combine32(s.am, a.z >> c.sx, s.bm, b.z >> c.sy, c.d);
+      z[3] = combine32(s.am, a.w >> c.sx, s.bm, b.w >> c.sy, c.d);
       break;
     }
     case FK_RESTRICT: {
-      const int lc = c.l - 1;
-      const int Nc = 1 << lc, mc = Nc - 1, Nf = 1 << c.l;
+      const int lc = l - 1;
+      const int Nc = 1 << lc, mc = Nc - 1, Nf = 1 << l;
       bool pad[4];
-      pad4(c.dim, lc, o, pad, 0);
+      pad4(dim, lc, o, pad, 0);
       const int I0 = o & mc, J = (o >> lc) & mc, K = (o >> (2 * lc)) & mc;
       int acc[4] = {0, 0, 0, 0}, w[4];
       RestrictOp ro;
-      if (c.dim == 1) {
-        ro.template line4<false>(c.x + 2 * I0, c.sx, acc);
+      if (dim == 1) {
+        ro.template line4<false>(s.x + 2 * I0, c.sx, acc);
       } else {
         int base = 2 * I0 + 2 * J * Nf;
-        if (c.dim >= 3) base += 2 * K * Nf * Nf;
-        const int32_t* fb = c.x + base;
-        const int planes = c.dim >= 3 ? 3 : 1;
+        if (dim >= 3) base += 2 * K * Nf * Nf;
+        const int32_t* fb = s.x + base;
+        const int planes = dim >= 3 ? 3 : 1;
         for (int pz = 0; pz < planes; ++pz) {
-          const int wz = c.dim >= 3 ? (pz == 1 ? 2 : 1) : 1;
-          const int32_t* fp = fb + (c.dim >= 3 ? pz * Nf * Nf : 0);
+          const int wz = dim >= 3 ? (pz == 1 ? 2 : 1) : 1;
+          const int32_t* fp = fb + (dim >= 3 ? pz * Nf * Nf : 0);
 #pragma unroll
           for (int py = 0; py < 3; ++py) {
             ro.template line4<false>(fp + py * Nf, c.sx, w);
@@ -521,23 +495,23 @@ __device__ __forceinline__ void lean_eval4(const LeanOp& c, int o, int64_t z[4])
     }
     case FK_PROLONG: {
       Vec xv;
-      xv.data = (void*)c.x;
+      xv.data = (void*)s.x;
       bool pad[4];
-      pad4(c.dim, c.l, o, pad, 0);
+      pad4(dim, l, o, pad, 0);
       int g[4];
-      prolong4_32<false>(xv, c.sx, c.dim, c.l, 0, o, g);
+      prolong4_32<false>(xv, c.sx, dim, l, 0, o, g);
 #pragma unroll
       for (int q = 0; q < 4; ++q) z[q] = pad[q] ? 0 : (int64_t)g[q];
       break;
     }
     default: {  // FK_PCORR
       Vec xv;
-      xv.data = (void*)c.x;
+      xv.data = (void*)s.x;
       bool pad[4];
-      pad4(c.dim, c.l, o, pad, 0);
+      pad4(dim, l, o, pad, 0);
       int g[4], yv[4];
-      prolong4_32<false>(xv, c.sx, c.dim, c.l, 0, o, g);
-      const int4 t = *reinterpret_cast<const int4*>(c.y + o);
+      prolong4_32<false>(xv, c.sx, dim, l, 0, o, g);
+      const int4 t = *reinterpret_cast<const int4*>(s.y + o);
       yv[0] = t.x >> c.sy, yv[1] = t.y >> c.sy, yv[2] = t.z >> c.sy, yv[3] = t.w >> c.sy;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -550,8 +524,89 @@ __device__ __forceinline__ void lean_eval4(const LeanOp& c, int o, int64_t z[4])
 
 }  // namespace bfpdev
 
+namespace bfpdev {
+constexpr int kHdrStride = (int)((sizeof(Hdr) + 127) / 128 * 128);  // arena header pitch
+__device__ __forceinline__ Hdr* lean_hdr_at(char* arena, int v) {
+  return reinterpret_cast<Hdr*>(arena + 128 + kHdrStride * v);
+}
+// compact state of vector v from its block header
+__device__ __forceinline__ LH lean_refresh(int v, LeanShared& ls, char* arena) {
+  const LH h = lean_hdr(lean_hdr_at(arena, v));
+  ls.fh[v] = make_fh(h.e, h.s, h.bits, h.eff, h.ok);
+  return h;
+}
+// block header of a vector from the log entry of its last writer (fast ops keep only the
+// compact state current; the generic path and the end of the list need the header)
+__device__ __forceinline__ void lean_materialize(int v, const LeanShared& ls, const LogRec* log,
+                                                 char* arena) {
+  const int j = ls.lastw[v];
+  if (j < 0) return;
+  const LogRec& r = log[j];
+  if (r.st == LOG_GENERIC) return;
+  Hdr* h = lean_hdr_at(arena, v);
+  h->q = r.q;
+  h->e = r.e_out;
+  h->shift = 0;
+  h->max_m = r.mx;
+  h->min_m = r.mn;
+  h->flags = r.flags;
+  h->lam_out = r.lam;
+  h->need_recompute = 0;
+}
+// The generic path for op i of the list (bfp_coarse.cuh: setup + gamma, deferred-shift pass,
+// finalize, recompute pass when a flag fires), on the block headers: the operands' headers
+// are materialised from the log first, the output's compact state refreshed after.
+__device__ __noinline__ void lean_generic(FusedOp& f, int i, int nar, char* arena,
+                                          CoarseShared& sh, LeanShared& ls, LogRec* log) {
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int v = 0; v < nar; ++v) lean_materialize(v, ls, log, arena);
+    coarse_prepare<int32_t>(f, arena, sh);
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    Red r;
+    r.init();
+    const int mode = pass ? MODE_RECOMPUTE : f.p.mode;
+    if (!(pass && sh.c.skip)) coarse_body<int32_t>(f, mode, sh, r);
+    coarse_publish(r, sh);
+    __syncthreads();
+    if (t < 32) {
+      int bits = 1, err = 0;
+      int64_t mx = 0, mn = 0;
+      coarse_totals(sh, bits, mx, mn, err);
+      if (t == 0) {
+        int rc = 0;
+        if (!(pass && sh.c.skip)) rc = win_finalize(f.p, sh.c, f.out.hdr, bits, mx, mn, err);
+        if (rc && !pass) {
+          f.p.mode = MODE_RECOMPUTE;
+          WinCtx c2;
+          win_setup(f.p, f.out.hdr, sh.c.e_star, 32, c2);
+          sh.c = c2;
+        }
+        sh.rc = rc && !pass;
+      }
+    }
+    __syncthreads();
+    if (!sh.rc) break;
+  }
+  if (t == 0) {
+    const int v = f.lr.vout;
+    const LH h = lean_refresh(v, ls, arena);
+    LogRec& r = log[i];
+    r.st = LOG_GENERIC;
+    r.e_out = h.e;
+    // effective extremes (pending shift applied); a header beyond 32 bits makes every
+    // consumer generic, which reads the header itself
+    r.mx = (int)(f.out.hdr->max_m >> h.s);
+    r.mn = (int)(f.out.hdr->min_m >> h.s);
+    ls.lastw[v] = i;
+  }
+}
+}  // namespace bfpdev
+
 // measurement builds (-DBFP_COARSE_TIMING): the lean engine's per-phase clocks share
-// g_coarse_prof (slots: 0 wait, 1 arena, 2 setup, 3 barrier A, 4 body, 5 barrier B,
+// g_coarse_prof (slots: 0 wait, 1 arena, 2 post-setup, 3 barrier A, 4 pre-setup, 5 barrier B,
 // 6 totals + core finalize, 7 writeback, 10 barrier C, 11 generic ops, 12 epilogue)
 __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops, int n,
                                                              const ArenaEntry* ar, int nar,
@@ -565,34 +620,29 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   int64_t* zbuf = zglobal ? zglobal : reinterpret_cast<int64_t*>(arena + zoff);
   LogRec* log = reinterpret_cast<LogRec*>(arena + loff);
-  // block headers sit at arena offsets 128 + k kHdrStride: header pointer -> vector id k
-  constexpr int kHdrStride = (int)((sizeof(Hdr) + 127) / 128 * 128);
-  const char* hbase = arena + 128;
-  auto vid = [hbase](const Hdr* h) { return (int)(((const char*)h - hbase) / kHdrStride); };
-  // record k -> slot k & 3, arena pointers rebased on the way (words marked in rb)
-  auto fetch = [&](int k, int c) {
-    const int4* src = reinterpret_cast<const int4*>(&ops[k]);
-    int4 v = __ldg(src + c);
-    const int4 m = __ldg(src + 1);  // chunk 0: {kind, pad, q}; chunk 1: {rb[0], rb[1]}
-    const uint64_t rb0 = ((uint64_t)(unsigned)m.y << 32) | (unsigned)m.x;
-    const uint64_t rb1 = ((uint64_t)(unsigned)m.w << 32) | (unsigned)m.z;
-    const int w0 = 2 * c;
-    auto marked = [&](int w) { return (int)(((w < 64 ? rb0 >> w : rb1 >> (w - 64))) & 1); };
-    if (marked(w0)) {
-      const uint64_t a = (uint64_t)(uintptr_t)arena + (((uint64_t)(unsigned)v.y << 32) | (unsigned)v.x);
-      v.x = (int)(unsigned)a;
-      v.y = (int)(unsigned)(a >> 32);
-    }
-    if (marked(w0 + 1)) {
-      const uint64_t a = (uint64_t)(uintptr_t)arena + (((uint64_t)(unsigned)v.w << 32) | (unsigned)v.z);
-      v.z = (int)(unsigned)a;
-      v.w = (int)(unsigned)(a >> 32);
-    }
-    reinterpret_cast<int4*>(&sh.f[k & 3])[c] = v;
+  // Record k -> slot k & 3 with cp.async (one 16-byte chunk per stager thread, no
+  // registers): issued during op k - 3, waited for during op k - 2, read from op k - 1 on.
+  // Arena offsets in the record stay offsets; their readers rebase (lean_ptr / the generic
+  // path's coarse_prepare).
+  const int wt = t - 32;  // worker index; workers 0 .. kChunks - 1 stage the records
+  const bool stager = wt >= 0 && wt < kChunks;
+  auto issue = [&](int k) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(reinterpret_cast<int4*>(&sh.f[k & 3]) + wt);
+    const int4* src = reinterpret_cast<const int4*>(&ops[k]) + wt;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
   };
-  // records 0 and 1 do not depend on the previous kernel: fetch them before the wait
-  if (t < kChunks) fetch(0, t);
-  if (n > 1 && t >= 64 && t < 64 + kChunks) fetch(1, t - 64);
+  auto landed = [&]() { asm volatile("cp.async.wait_all;" ::: "memory"); };
+  // records do not depend on the previous kernel: the first three are fetched before the
+  // wait, and the rest of the list is pulled into L2
+  if (stager) {
+    issue(0);
+    if (n > 1) issue(1);
+    if (n > 2) issue(2);
+    landed();
+  }
+  for (int64_t b = (int64_t)t * 128 + 3 * (int64_t)sizeof(FusedOp); b < (int64_t)n * (int64_t)sizeof(FusedOp);
+       b += (int64_t)kFusedThreads * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(ops) + b));
   if (t == 0) sh.rc = 0;
   CPROF_T();
   griddep_wait();
@@ -606,13 +656,8 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
   for (int k = t; k < n; k += kFusedThreads) log[k].st = LOG_NONE;
   __syncthreads();
   // compact vector states and the norms at entry, one thread per header
-  auto refresh = [&](int v) {
-    const LH h = lean_hdr(reinterpret_cast<const Hdr*>(hbase + kHdrStride * v));
-    ls.fh[v] = FH{h.e, h.s, h.bits, h.eff, (int)h.ok};
-    return h;
-  };
   if (t < nar) {
-    const LH h = refresh(t);
+    const LH h = lean_refresh(t, ls, arena);
     ls.init_e[t] = h.e;
     ls.init_mag[t] = h.mag;  // (only read when ok: a header out of range makes its ops generic)
     ls.lastw[t] = -1;
@@ -620,121 +665,64 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
   __syncthreads();
   CPROF(1);
   LeanState st;
-  if (t == 0) ls.op.fast = lean_setup(sh.f[0], n > 1 ? &sh.f[1] : nullptr, ls, log, vid, st);
+  __shared__ LeanPre pre;  // control lane only: written by the first half, read by the second
+  const FH nofh = FH{0, 0, 0, 0};
+  if (t == 0) {
+    lean_pre(sh.f[0], nullptr, ls, pre);
+    lean_post(sh.f[0], pre, -1, nofh, -1, ls, log, st);
+  }
   CPROF(2);
   CPROF_CNT(8, 1);
   CPROF_CNT(9, n);
-  // block header of a vector from the log entry of its last writer (fast ops keep only the
-  // compact state current; the generic path and the end of the list need the header)
-  auto materialize = [&](int v) {
-    const int j = ls.lastw[v];
-    if (j < 0) return;
-    const LogRec& r = log[j];
-    if (r.st == LOG_GENERIC) return;
-    Hdr* h = reinterpret_cast<Hdr*>(arena + 128 + kHdrStride * v);
-    h->q = r.q;
-    h->e = r.e_out;
-    h->shift = 0;
-    h->max_m = r.mx;
-    h->min_m = r.mn;
-    h->flags = r.flags;
-    h->lam_out = r.lam;
-    h->need_recompute = 0;
-  };
   for (int i = 0; i < n; ++i) {
     __syncthreads();  // (A) context of op i published; the data of op i - 1 is visible
     CPROF(3);
     FusedOp& f = sh.f[i & 3];
-    if (!ls.op.fast) {
-      // ---- generic path (bfp_coarse.cuh): setup + gamma, deferred-shift pass, finalize,
-      // recompute pass when a flag fires; reads and writes the block headers ----
-      if (i + 2 < n && t >= 32 && t < 32 + kChunks) fetch(i + 2, t - 32);
-      if (t == 0) {
-        for (int v = 0; v < nar; ++v) materialize(v);
-#ifdef BFP_LEAN_DEBUG
-        if (f.kind == FK_RESTRICT) {
-          const int v = vid(f.u.rst.r.hdr), gv = vid(f.p.gamma.t[0].v);
-          const Hdr* h = f.u.rst.r.hdr;
-          printf("op %d restrict l=%d: in vid %d gamma vid %d lastw %d hdr e=%lld mx=%lld mn=%lld sh=%lld | log st=%d e=%d mx=%d\n",
-                 i, f.u.rst.l, v, gv, ls.lastw[v], (long long)h->e, (long long)h->max_m,
-                 (long long)h->min_m, (long long)h->shift, ls.lastw[v] >= 0 ? log[ls.lastw[v]].st : -9,
-                 ls.lastw[v] >= 0 ? log[ls.lastw[v]].e_out : 0, ls.lastw[v] >= 0 ? log[ls.lastw[v]].mx : 0);
-        }
+#ifdef BFP_COARSE_TIMING
+    const long long _w0 = clock64();
 #endif
-        coarse_prepare<int32_t>(f, arena, sh);
-      }
-      __syncthreads();
-      for (int pass = 0; pass < 2; ++pass) {
-        Red r;
-        r.init();
-        const int mode = pass ? MODE_RECOMPUTE : f.p.mode;
-        if (!(pass && sh.c.skip)) coarse_body<int32_t>(f, mode, sh, r);
-        coarse_publish(r, sh);
-        __syncthreads();
-        if (t < 32) {
-          int bits = 1, err = 0;
-          int64_t mx = 0, mn = 0;
-          coarse_totals(sh, bits, mx, mn, err);
-          if (t == 0) {
-            int rc = 0;
-            if (!(pass && sh.c.skip)) rc = win_finalize(f.p, sh.c, f.out.hdr, bits, mx, mn, err);
-            if (rc && !pass) {
-              f.p.mode = MODE_RECOMPUTE;
-              WinCtx c2;
-              win_setup(f.p, f.out.hdr, sh.c.e_star, 32, c2);
-              sh.c = c2;
-            }
-            sh.rc = rc && !pass;
-          }
-        }
-        __syncthreads();
-        if (!sh.rc) break;
-      }
-      if (t == 0) {
-        const int v = vid(f.out.hdr);
-        const LH h = refresh(v);
-        LogRec& r = log[i];
-        r.st = LOG_GENERIC;
-        r.e_out = h.e;
-        // effective extremes (pending shift applied); a header beyond 32 bits makes every
-        // consumer generic, which reads the header itself
-        r.mx = (int)(f.out.hdr->max_m >> h.s);
-        r.mn = (int)(f.out.hdr->min_m >> h.s);
-        ls.lastw[v] = i;
-        if (i + 1 < n)
-          ls.op.fast = lean_setup(sh.f[(i + 1) & 3], i + 2 < n ? &sh.f[(i + 2) & 3] : nullptr, ls,
-                                  log, vid, st);
+    if (stager) {  // record i + 2 (issued during op i - 1) has landed; fetch record i + 3
+      landed();
+      if (i + 3 < n) issue(i + 3);
+    }
+#ifdef BFP_COARSE_TIMING
+    if (t == 32 && i < 4096) g_coarse_ops[4 * i] = (int)(clock64() - _w0);
+#endif
+    if (!ls.dyn.fast) {
+      lean_generic(f, i, nar, arena, sh, ls, log);
+      if (t == 0 && i + 1 < n) {
+        lean_pre(sh.f[(i + 1) & 3], nullptr, ls, pre);
+        lean_post(sh.f[(i + 1) & 3], pre, -1, nofh, -1, ls, log, st);
       }
       CPROF(11);
       continue;
     }
     // ---- fast path ----
-    const int kind = ls.op.kind;
-    int32_t* st_out = nullptr;  // the workers' copies for the store phase (the control lane
-    int st_n4 = 0, st_mm = 0;   // rewrites ls.op for op i + 1 meanwhile)
-#ifdef BFP_COARSE_TIMING
-    const long long _b0 = clock64();
-#endif
+    const int kind = f.kind;
+    int32_t* st_out = nullptr;  // the workers' copies for the store phase
+    int st_n4 = 0, st_mm = 0;
     if (warp > 0) {
-      const int wt = t - 32;
-      if (i + 2 < n && wt < kChunks) fetch(i + 2, wt);
-      const LeanOp c = ls.op;
-      st_out = c.out;
-      st_n4 = c.n4;
-      st_mm = c.needmm || c.nnq;
+      LeanRec s = f.lr;
+      s.x = lean_ptr(s.x, arena);
+      s.y = lean_ptr(s.y, arena);
+      s.out = lean_ptr(s.out, arena);
+      const LeanDyn c = ls.dyn;
+      st_out = s.out;
+      st_n4 = s.n4;
+      st_mm = c.needmm;
       if (kind == FK_ZERO) {
-        for (int g = wt; g < c.n4; g += kLeanWorkers)
-          reinterpret_cast<int4*>(c.out)[g] = make_int4(0, 0, 0, 0);
+        for (int g = wt; g < s.n4; g += kLeanWorkers)
+          reinterpret_cast<int4*>(s.out)[g] = make_int4(0, 0, 0, 0);
       } else {
         // OR of z ^ sign(z) (mu*), with the sign in bit 63 (all rows in {0, -1}: any -1?)
         uint64_t orv = 0;
         int64_t mx = INT64_MIN, mn = INT64_MAX;
-        for (int g = wt; g < c.n4; g += kLeanWorkers) {
+        for (int g = wt; g < s.n4; g += kLeanWorkers) {
           int64_t z[4];
-          lean_eval4(c, 4 * g, z);
+          lean_eval4(kind, s, c, 4 * g, z);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            if (c.nnq) z[j] = shift_clamp<int64_t>(z[j], c.lam, c.wout);
+            if (s.nnq) z[j] = shift_clamp<int64_t>(z[j], c.lam, s.w_out);
             orv |= (uint64_t)(z[j] ^ (z[j] >> 63)) | ((uint64_t)z[j] & 0x8000000000000000ull);
             if (st_mm) {
               mx = z[j] > mx ? z[j] : mx;
@@ -758,33 +746,32 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
           }
         }
       }
+    } else if (t == 0 && i + 1 < n) {
+      lean_pre(sh.f[(i + 1) & 3], nullptr, ls, pre);  // first half of the next op's setup
     }
 #ifdef BFP_COARSE_TIMING
-    if (t == 479 && i < 4096) {
-      g_coarse_ops[4 * i] = kind;
-      g_coarse_ops[4 * i + 2] = (int)(clock64() - _b0);
-    }
+    if (t == 32 && i < 4096) g_coarse_ops[4 * i + 2] = (int)(clock64() - _w0);
 #endif
     CPROF(4);
     __syncthreads();  // (B) warp partials published
     CPROF(5);
+    FH ff = nofh;  // control lane: the fresh state of this op's output
     if (warp == 0) {
-      LogRec& r = log[i];
       if (kind == FK_ZERO) {
         if (t == 0) {  // zero_vec (P/src/bfp.cpp:53-55)
+          LogRec r;
           r.st = LOG_ZERO;
           r.q = (short)f.q;
-          r.e_out = 0;
-          r.lam = 0;
-          r.mx = r.mn = 0;
-          r.flags = 0;
-          ls.fh[st.vout] = FH{0, 0, 0, 1, 1};
+          r.e_out = r.lam = r.mu = r.mx = r.mn = r.flags = 0;
+          log[i] = r;
+          ff = make_fh(0, 0, 0, 1, true);
+          ls.fh[st.vout] = ff;
           ls.lastw[st.vout] = i;
         }
       } else {
         const bool on = lane >= 1 && lane < kCoarseWarps;
         const uint64_t o2 = redux_or64(on ? ls.orv[lane] : 0ull);
-        const int mm = ls.op.needmm || ls.op.nnq;
+        const int mm = ls.dyn.needmm;
         int64_t tmx = 0, tmn = 0;
         if (mm) {
           tmx = redux_max64(on ? ls.mx[lane] : INT64_MIN);
@@ -795,9 +782,11 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
           const bool anyneg = (o2 >> 63) != 0;
           const uint64_t mag = o2 & 0x7fffffffffffffffull;
           const bool allzero = mag == 0 && !anyneg;
+          LogRec r;
+          r.gm = r.ge = 0;
           if (st.nnq) {
             lam = 0;  // rows were clamped in the body; e_out = e* + lam_out (:211)
-            e_out = st.e_star + ls.op.lam;
+            e_out = st.e_star + ls.dyn.lam;
             r.st = LOG_FASTN;
             r.gm = st.gm;
             r.ge = st.ge;
@@ -805,11 +794,11 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
             r.mn = (int)tmn;
             const int ma = msb32((int)tmx), mb = msb32((int)tmn);
             const int eff = ma > mb ? ma : mb;
-            ls.fh[st.vout] = FH{e_out, 0, allzero ? 0 : eff, eff, (int)small_e(e_out)};
+            ff = make_fh(e_out, 0, allzero ? 0 : eff, eff, small_e(e_out));
           } else {
-            mu = bitlen64(mag) + 1;                      // mu* (init 1, P/src/blas.cpp:153)
-            if (st.zd > 0 && allzero) mu = 1 - st.zd;    // all-zero anchor in the op's coordinates
-            lam = mu - st.w_out;                         // :164
+            mu = bitlen64(mag) + 1;                    // mu* (init 1, P/src/blas.cpp:153)
+            if (st.zd > 0 && allzero) mu = 1 - st.zd;  // all-zero anchor in the op's coordinates
+            lam = mu - st.w_out;                       // :164
             e_out = st.e_star + lam;
             r.st = LOG_FASTQ;
             if (mm) {  // the next op is nnqcomp: extremes of the stored values now
@@ -820,8 +809,7 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
               r.mn = INT32_MAX;
             }
             // a normalised block: width w_out unless every row is zero
-            ls.fh[st.vout] = FH{e_out, 0, allzero ? 0 : st.w_out, allzero ? 1 : st.w_out,
-                                (int)small_e(e_out)};
+            ff = make_fh(e_out, 0, allzero ? 0 : st.w_out, allzero ? 1 : st.w_out, small_e(e_out));
           }
           ls.lam_store = lam;
           r.e_out = e_out;
@@ -833,6 +821,9 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
           r.prod[0] = st.prod[0];
           r.prod[1] = st.prod[1];
           r.prod[2] = st.prod[2];
+          r.pad = 0;
+          log[i] = r;
+          ls.fh[st.vout] = ff;
           ls.lastw[st.vout] = i;
         }
       }
@@ -848,7 +839,7 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
         const int lam = ls.lam_store;
         const int rs = lam >= 0 ? (lam > 63 ? 63 : lam) : 0, lsh = lam < 0 ? -lam : 0;
         int smx = INT32_MIN, smn = INT32_MAX;
-        for (int g = t - 32; g < st_n4; g += kLeanWorkers) {
+        for (int g = wt; g < st_n4; g += kLeanWorkers) {
           const longlong2* zp = reinterpret_cast<const longlong2*>(zbuf + 4 * (size_t)g);
           const longlong2 a = zp[0], b = zp[1];
           int4 v;
@@ -870,8 +861,8 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
         }
       }
     } else if (t == 0 && i + 1 < n) {
-      ls.op.fast = lean_setup(sh.f[(i + 1) & 3], i + 2 < n ? &sh.f[(i + 2) & 3] : nullptr, ls, log,
-                              vid, st);
+      // second half of the next op's setup, with this op's output state forwarded
+      lean_post(sh.f[(i + 1) & 3], pre, st.vout, ff, i, ls, log, st);
 #ifdef BFP_COARSE_TIMING
       if (i + 1 < 4096) g_coarse_ops[4 * (i + 1) + 1] = (int)(clock64() - _ct);
 #endif
@@ -881,13 +872,12 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
   __syncthreads();
   griddep_launch_dependents();
   // ---- end of the list: gamma, flags, trace and history of every fast op, one thread per
-  // op (records re-read from global memory: their gamma terms name vectors by arena offset)
+  // op (records re-read from global memory) ----
   for (int k = t; k < n; k += kFusedThreads) {
     LogRec& r = log[k];
     if (r.st != LOG_FASTQ && r.st != LOG_FASTN) continue;
     const FusedOp& g = ops[k];
     const WinParams& p = g.p;
-    auto gvid = [](const Hdr* h) { return (int)(((uintptr_t)h - 128) / kHdrStride); };
     WinCtx c;
     if (r.st == LOG_FASTN) {
       c.gm = r.gm;
@@ -895,7 +885,7 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
       write_trace(p, c, 0, 0, 0, 0);
     } else {
       int gm, ge;
-      lean_gamma(p.gamma, ls, log, r.prod, gvid, gm, ge);
+      lean_gamma(p.gamma, g.lr, ls, log, r.prod, gm, ge);
       c.gm = gm;
       c.ge = ge;
       const int mu_tmp = msb32(gm) + ge - r.e_star;
@@ -912,15 +902,7 @@ __global__ void __launch_bounds__(kFusedThreads) lean_kernel(const FusedOp* ops,
     }
   }
   __syncthreads();
-#ifdef BFP_LEAN_LOGDUMP
-  for (int k = t; k < n && k < 1024; k += kFusedThreads) {  // the log of the last launch
-    g_coarse_ops[4 * k] = ops[k].kind * 16 + log[k].st;
-    g_coarse_ops[4 * k + 1] = log[k].e_out;
-    g_coarse_ops[4 * k + 2] = log[k].mx;
-    g_coarse_ops[4 * k + 3] = log[k].mn;
-  }
-#endif
-  if (t < nar) materialize(t);
+  if (t < nar) lean_materialize(t, ls, log, arena);
   __syncthreads();
   CPROF(12);
   for (int k = 0; k < nar; ++k) {  // publish the fused part's outputs

@@ -73,18 +73,19 @@ int fused_kind(int k) {
   }
   return -1;
 }
-// levels whose padded grid has at most this many points run fused in one CTA
-// (BFP_FUSE_POINTS overrides; 0 disables fusion)
-int64_t fuse_max_points() {
+// Levels whose padded grid has at most this many points run inside one CTA (the lean coarse
+// engine, bfp_lean.cuh).  Measured on B200 (tools/fuse_sweep.py, profiles/r2/r2b_fuse_sweep.txt):
+// 4096 points is the best threshold in 2-D and 3-D (beyond it the rows no longer fit the
+// CTA's shared memory); 1-D levels are cheap per launch and gain up to ~1024 points.
+int64_t fuse_max_points(int d) {
 #ifdef BFP_AB_ENV  // A/B measurement builds only
   static const int64_t v = [] {
     const char* e = getenv("BFP_FUSE_POINTS");
-    return e ? (int64_t)atoll(e) : (int64_t)0;
+    return e ? (int64_t)atoll(e) : (int64_t)-1;
   }();
-  return v;
-#else
-  return 0;  // off by default: slower than PDL-chained launches (profiles/)
+  if (v >= 0) return v;
 #endif
+  return d == 1 ? 1024 : 4096;
 }
 
 struct LevelBufs {
@@ -211,8 +212,8 @@ struct RankSolver {
   bool fusable(int l) const {
     int64_t pts = 1;
     for (int a = 0; a < cfg.d; ++a) pts <<= l;
-    const int64_t lim = cfg.fuse_points >= 0 ? cfg.fuse_points : fuse_max_points();
-    return fusion && world == 1 && !in_fused && pts <= lim;
+    const int64_t lim = cfg.fuse_points >= 0 ? cfg.fuse_points : fuse_max_points(cfg.d);
+    return fusion && !sharded(l) && !in_fused && pts <= lim;
   }
   // run body() with its plan ops collected into one OK_FUSED op
   template <typename F> bfp_vec_s* fused(F body) {
@@ -696,6 +697,8 @@ struct RankSolver {
         int rc = fused_make(fk, so.a, so.b, so.s1, so.s2, so.p, so.q, so.out, &h[i]);
         if (rc) return rc;
       }
+      for (size_t i = 0; i + 1 < h.size(); ++i)
+        h[i].lr.nnq_next = h[i + 1].kind != bfpdev::FK_ZERO && h[i + 1].p.mode == MODE_NNQ;
       if (!build_arena(op, h)) {
         // the list's state does not fit one CTA's shared memory: one launch per op instead
         if (err) return err;
@@ -829,6 +832,30 @@ struct RankSolver {
               }
       remap(f.out);
       visit(f, remap);
+      // the lean digest: vector ids (header offsets -> index) and the operands' data
+      constexpr int64_t kStride = (sizeof(Hdr) + 127) / 128 * 128;
+      auto vid = [&](const void* hdr_off) { return (uint8_t)(((uintptr_t)hdr_off - 128) / kStride); };
+      auto dptr = [&](const void** slot, const void* data) {
+        *slot = data;
+        if ((uintptr_t)data != 0 && (uintptr_t)data < (uintptr_t)bfpdev::kArenaMaxBytes) mark(slot);
+      };
+      bfpdev::LeanRec& lr = f.lr;
+      lr.vout = vid(f.out.hdr);
+      dptr((const void**)&lr.out, f.out.data);
+      int na = 0;
+      visit(f, [&](bfpdev::Vec& v) {
+        if (na == 0) {
+          lr.va = vid(v.hdr);
+          dptr((const void**)&lr.x, v.data);
+        } else {
+          lr.vb = vid(v.hdr);
+          dptr((const void**)&lr.y, v.data);
+        }
+        ++na;
+      });
+      if (!f.p.gamma.literal)
+        for (int i = 0; i < f.p.gamma.nterms && i < 3; ++i)
+          if (f.p.gamma.t[i].v) lr.gv[i] = vid(f.p.gamma.t[i].v);
     }
     static_assert(sizeof(FusedOp) <= 128 * 8, "FusedOp::rb marks at most 128 words");
     if (cudaMalloc(&op.arena, sizeof(ArenaEntry) * ar.size()) != cudaSuccess) {

@@ -3,6 +3,76 @@
 
 namespace bfp {
 
+// The lean engine's digest of the record (bfp_internal.h: LeanRec): the static fields, and
+// `ok` = every static condition of the fast path holds (the dynamic ones -- operand widths
+// and exponents -- are checked per op on the device, bfp_lean.cuh: lean_post).  Vector ids
+// and data pointers are filled in when the arena is laid out (bfp_solver.cu).
+static void lean_digest(FusedOp* f) {
+  LeanRec& r = f->lr;
+  memset(&r, 0, sizeof(r));
+  r.vout = r.va = r.vb = 0xff;
+  r.gv[0] = r.gv[1] = r.gv[2] = 0xff;
+  const WinParams& p = f->p;
+  auto small_e = [](int64_t e) { return e > -(1 << 20) && e < (1 << 20); };
+  auto fits = [](int64_t m) { return m == (int64_t)(int32_t)m; };
+  r.n4 = (int32_t)(f->out.n >> 2);
+  r.w_out = (int16_t)p.w_out;
+  r.nnq = p.mode == MODE_NNQ;
+  bool ok = f->out.ebytes == 4;
+  if (f->kind != FK_ZERO) {
+    ok = ok && !p.part && !p.force && p.w_tmp <= 32 && p.w_out >= 1 && p.w_out <= 32 &&
+         (p.mode == MODE_QCOMP || p.mode == MODE_NNQ);
+    const GammaRule& g = p.gamma;
+    ok = ok && !g.literal && !g.exact && g.nterms <= 3;
+    for (int i = 0; ok && i < g.nterms; ++i)
+      ok = g.t[i].cm >= 0 && g.t[i].cm <= 0xffffffffll && small_e(g.t[i].ce);
+    r.ng = (uint8_t)(g.literal ? 0 : g.nterms);
+  }
+  auto coef = [&](const Scal& a, const Scal& b) {
+    ok = ok && fits(a.m) && fits(b.m) && small_e(a.e) && small_e(b.e);
+    r.am = (int32_t)a.m, r.ae = (int32_t)a.e, r.bm = (int32_t)b.m, r.be = (int32_t)b.e;
+  };
+  switch (f->kind) {
+    case FK_GEMV: {
+      const GemvOp& g = f->u.gemv;
+      ok = ok && !g.st9 && !g.gs && g.l >= 2 && !g.z0;
+      coef(g.al, g.be);
+      r.dim = (int8_t)g.dim, r.l = (int8_t)g.l, r.ea = g.ea;
+      break;
+    }
+    case FK_JACOBI: {
+      const JacobiOp& j = f->u.jac;
+      ok = ok && j.l >= 2 && !j.z0 && j.c.m >= 0 && j.c.m <= 0x7fffffff;
+      coef(j.c, Scal{0, 0, 0});
+      r.dim = (int8_t)j.dim, r.l = (int8_t)j.l, r.ea = 2 * j.l;
+      break;
+    }
+    case FK_SCAL: coef(f->u.scal.c, Scal{0, 0, 0}); break;
+    case FK_AXPBY: coef(f->u.axpby.al, f->u.axpby.be); break;
+    case FK_RESTRICT: {
+      const RestrictOp& q = f->u.rst;
+      ok = ok && !q.gs && !q.zc && q.l >= 3;
+      r.dim = (int8_t)q.dim, r.l = (int8_t)q.l, r.ea = q.er;
+      break;
+    }
+    case FK_PROLONG: {
+      const ProlongOp& q = f->u.pro;
+      ok = ok && !q.gs && !q.zf && !q.zp && q.l >= 3;
+      r.dim = (int8_t)q.dim, r.l = (int8_t)q.l, r.ea = q.ep;
+      break;
+    }
+    case FK_PCORR: {
+      const ProlongCorrectOp& q = f->u.pc;
+      ok = ok && !q.gs && !q.zf && !q.zp && q.l >= 3 && q.al.m == 1 && q.be.m == 1;
+      coef(q.al, q.be);
+      r.dim = (int8_t)q.dim, r.l = (int8_t)q.l, r.ea = q.ep;
+      break;
+    }
+    default: break;
+  }
+  r.ok = ok;
+}
+
 int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const WinParams& p,
                int64_t q, bfp_vec_s* out, FusedOp* f) {
   memset(f, 0, sizeof(*f));
@@ -42,6 +112,7 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
     case FK_ZERO: break;
     default: return BFP_ERR_ARG;
   }
+  lean_digest(f);
   return BFP_OK;
 }
 

@@ -37,7 +37,7 @@ for k, nm in enumerate(names):
 ops = (C.c_int * (4 * 64))()
 B.lib().bfp_dbg_coarse_ops(ops, 64)
 kn = ["gemv", "jacobi", "scal", "axpby", "restrict", "prolong", "pcorr", "zero"]
-print("  last launch, first ops: kind prepare body totals+finalize (clk)")
+print("  last launch, first ops: t32 fetch | post-setup | t32 A->B | totals+core (clk)")
 for i in range(40):
     k, a, b, c = ops[4 * i:4 * i + 4]
-    print(f"   {i:3d} {kn[k] if 0 <= k < 8 else k:9s} {a:7d} {b:7d} {c:7d}")
+    print(f"   {i:3d} {k:7d} {a:7d} {b:7d} {c:7d}")
