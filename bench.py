@@ -842,16 +842,17 @@ def measure_ops(B, torch, stream, d, l, p, steps=20, only=None, s=4):
     c = B.jacobi_coeff(d, l, 16).c()
     m1, p1 = B.bfp_minus_one().c(), B.bfp_one().c()
     G = B.Scalar(1 << 14, 16, 2 * l + 8).c()
+    # windows as the solver sets them (w_tmp = w_out + w_add per step)
     ops = {
-        "residual": (lambda g: L.bfp_stencil_gemv(x.h, b.h, m1, p1, 0, p, p + 5, g, 0, out.h, sp),
+        "residual": (lambda g: L.bfp_stencil_gemv(x.h, b.h, m1, p1, 0, p, p + 4, g, 0, out.h, sp),
                      3 * s, out),
-        "jacobi": (lambda g: L.bfp_stencil_jacobi(x.h, b.h, c, 0, p, p + 5, g, out.h, sp), 3 * s, out),
-        "scal": (lambda g: L.bfp_scal(x.h, c, 0, p, p + 5, g, out.h, sp), 2 * s, out),
-        "axpby": (lambda g: L.bfp_axpby(x.h, y.h, p1, p1, 0, p, p + 5, g, 0, out.h, sp), 3 * s, out),
-        "restrict": (lambda g: L.bfp_restrict_fw(x.h, 0, p, p + 5, g, outc.h, sp),
+        "jacobi": (lambda g: L.bfp_stencil_jacobi(x.h, b.h, c, 0, p, p + 3, g, out.h, sp), 3 * s, out),
+        "scal": (lambda g: L.bfp_scal(x.h, c, 0, p, p + 2, g, out.h, sp), 2 * s, out),
+        "axpby": (lambda g: L.bfp_axpby(x.h, y.h, p1, p1, 0, p, p + 1, g, 0, out.h, sp), 3 * s, out),
+        "restrict": (lambda g: L.bfp_restrict_fw(x.h, 0, p, p + 6, g, outc.h, sp),
                      (1 + 2.0 ** -d) * s, outc),
-        "prolong": (lambda g: L.bfp_prolong(xc.h, 0, p, p + 5, g, out.h, sp), (1 + 2.0 ** -d) * s, out),
-        "prolong_correct": (lambda g: L.bfp_prolong_correct(xc.h, y.h, 0, p, p + 5, g, out.h, sp),
+        "prolong": (lambda g: L.bfp_prolong(xc.h, 0, p, p + 1, g, out.h, sp), (1 + 2.0 ** -d) * s, out),
+        "prolong_correct": (lambda g: L.bfp_prolong_correct(xc.h, y.h, 0, p, p + 2, g, out.h, sp),
                             (2 + 2.0 ** -d) * s, out),
     }
     peak, _ = peaks()

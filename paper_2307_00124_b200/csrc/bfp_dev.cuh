@@ -80,6 +80,19 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 // ---------------------------------------------------------------------------
 // integer primitives
 
+// 32 x 32 -> 64-bit signed multiply(-add): one IMAD.WIDE on the FMA pipe (the compiler
+// otherwise widens a product with a launch-uniform factor to a 64 x 64 multiply)
+__device__ __forceinline__ int64_t mul_wide(int a, int b) {
+  int64_t r;
+  asm("mul.wide.s32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ int64_t mad_wide(int a, int b, int64_t c) {
+  int64_t r;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+
 __device__ __forceinline__ int bitlen64(uint64_t u) { return u ? 64 - __clzll((long long)u) : 0; }
 __device__ __forceinline__ int bitlen128(u128 u) {
   uint64_t hi = (uint64_t)(u >> 64);

@@ -1248,6 +1248,17 @@ __global__ void __launch_bounds__(kB3T, b3_minb<T, Op>())
 // fine plane 2K also reads S_{K-1}, so each coarse plane tile (72 x 5 box) is
 // loaded and summed once per pair; P e_c (2K) = S_{K-1} + S_K, (2K+1) = 2 S_K.
 // The correction operand y arrives as two 128 x 8 boxes per pair.
+#ifdef BFP_P3_TIMING
+__device__ long long g_p3_prof[8];
+#define P3T(k)                                                                       \
+  if (threadIdx.x == 0 && blockIdx.x == 0) {                                         \
+    const long long _n = clock64();                                                  \
+    atomicAdd((unsigned long long*)&g_p3_prof[k], (unsigned long long)(_n - _pt));   \
+    _pt = _n;                                                                        \
+  }
+#else
+#define P3T(k)
+#endif
 constexpr int kP3W = 128, kP3H = 8, kP3T = 256;
 constexpr int kP3CW = kP3W / 2 + 8, kP3CH = kP3H / 2 + 1;  // coarse box 72 x 5
 template <typename T> constexpr int p3_ct() {  // coarse slot in elements (128-B multiple)
@@ -1258,17 +1269,26 @@ constexpr int kP3YT = kP3W * kP3H;                               // one y box
 #define BFP_P3_D 2
 #endif
 #ifndef BFP_P3_MINB  // resident CTAs per SM of the int32 instantiation
-#define BFP_P3_MINB 4
+#define BFP_P3_MINB 3
 #endif
 constexpr int kP3D = BFP_P3_D;                                    // pairs in flight
 constexpr int kP3S = kP3D + 1;                                   // slots / barriers
 template <typename T> constexpr size_t p3_smem() {
-  return (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T) + kP3S * 8 + 128 + 64;
+  return (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T) + 2 * kP3S * 8 + 128 + 64;
 }
 struct P3Maps {
   CUtensorMap c, y;
 };
 
+// Warp-specialised: warps 0..7 (kP3T threads) are the consumers, warp 8 is the producer.
+// Lane 0 of the producer streams the boxes into a ring of kP3S slots, waiting on the slot's
+// EMPTY mbarrier (one arrival per consumer warp) and signalling its FULL mbarrier through
+// complete_tx; the consumers never execute a block barrier, a proxy fence or a TMA issue
+// (measured before: of ~2200 clk per step, 640 were the elected consumer thread's fence +
+// issue with the other warps idle behind it, profiles/r2/r2c_p3_phases.txt).  Ring step j of
+// an item: j = 0 loads coarse plane K0 - 1 alone (S_{K0-1}), j >= 1 loads coarse plane
+// K0 + j - 1 and the two y boxes of pair K0 + j - 1.  The ring position runs on across
+// items, so nothing drains between them.
 template <int MODE, bool FW, typename T, typename Op>
 __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const WinParams& p,
                                           const WinCtx& c, Red& r, int R, char* smem,
@@ -1282,53 +1302,65 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
   constexpr int kP3CT = p3_ct<T>();
   T* csl = reinterpret_cast<T*>(smem);
   T* ysl = csl + kP3S * kP3CT;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ysl + kP3S * 2 * kP3YT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ysl + kP3S * 2 * kP3YT);
+  uint64_t* empty = full + kP3S;
   T* O = (T*)out.data;
   const int sc = op.shc(), sy = op.shy();
   const int kc_off = op.zp / 2;  // coarse local plane of fine local pair K
   const int t = threadIdx.x, lane = t & 31, wy = t >> 5;
+  const bool producer = t >= kP3T;
   T mx = Lim<T>::lo, mn = Lim<T>::hi;
   uint64_t olo = 0, ohi = 0;
+  uint32_t o32lo = 0, o32hi = 0;  // int32 fast window: OR of z ^ sign(z) in two words
   const bool store = c.store_tmp;
   const uint32_t cbytes = (uint32_t)(kP3CW * kP3CH * sizeof(T)), ybytes = (uint32_t)(kP3YT * sizeof(T));
-  uint32_t parity = 0;
+  uint32_t ring = 0;  // ring position of the item's step 0 (both roles advance it alike)
   // local coarse rows of fine row y0 + wy and the coarse column of this thread's 4 points
   const int r0 = ((wy - 1) >> 1) + 1, r1 = (wy >> 1) + 1, col = 2 * lane + 4;
+  // int32 fast window: z = g Pg + y Py as two IMAD.WIDE (no operand selects).  No pad
+  // masking there: a fine pad index has both coarse taps on the coarse pad (index N/2 - 1,
+  // stored zero) and y's own pad is zero, so its row is 0 Pg + 0 Py.
+  [[maybe_unused]] int Pg = 1, Py = 0;
+  if constexpr (Op::kCorr && sizeof(T) == 4) {
+    Pg = op.swap ? 1 : op.P;
+    Py = op.swap ? op.P : 1;
+  }
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
     const int64_t x0 = (int64_t)(tile % tx) * kP3W, y0 = (int64_t)(tile / tx) * kP3H;
     const int64_t k0 = (int64_t)ch * R;
     const int pairs = (int)(std::min<int64_t>(R, NZ - k0) / 2);
     const int64_t K0 = k0 / 2;
-    // step s (pair K0 + s) on slot s % S: coarse plane K0 + s (and K0 - 1 at s = 0)
-    auto issue = [&](int s) {
-      const int slot = s % kP3S;
-      uint64_t* b = &bar[slot];
-      const int64_t K = K0 + s;
-      const uint32_t bytes = cbytes + (s == 0 ? cbytes : 0u) + (Op::kCorr ? 2 * ybytes : 0u);
-      mbar_expect_tx(b, bytes);
-      tma_g2s_3d(csl + slot * kP3CT, tmc, (int)(x0 / 2) - 4, (int)(y0 / 2) - 1,
-                 (int)(K + kc_off + 2), b);
-      if (s == 0)  // coarse plane K0 - 1 into the slot of step -1
-        tma_g2s_3d(csl + ((kP3S - 1) % kP3S) * kP3CT, tmc, (int)(x0 / 2) - 4, (int)(y0 / 2) - 1,
-                   (int)(K - 1 + kc_off + 2), b);
-      if (Op::kCorr)
-        for (int h = 0; h < 2; ++h)
-          tma_g2s_3d(ysl + (slot * 2 + h) * kP3YT, tmy, (int)x0, (int)y0, (int)(2 * K + h + 2), b);
-    };
-    if (t == 0) {
-      fence_proxy_async_smem();
-      for (int s = 0; s < kP3D && s < pairs; ++s) issue(s);
+    if (producer) {
+      if (lane == 0) {
+        for (int j = 0; j <= pairs; ++j) {
+          const uint32_t g = ring + (uint32_t)j, slot = g % kP3S;
+          // the slot's previous user (ring step g - kP3S) has been read by every consumer warp
+          mbar_wait(&empty[slot], ((g / kP3S) & 1u) ^ 1u);
+          fence_proxy_async_smem();
+          uint64_t* b = &full[slot];
+          const int64_t K = K0 + j - 1;
+          mbar_expect_tx(b, cbytes + (Op::kCorr && j > 0 ? 2 * ybytes : 0u));
+          tma_g2s_3d(csl + slot * kP3CT, tmc, (int)(x0 / 2) - 4, (int)(y0 / 2) - 1,
+                     (int)(K + kc_off + 2), b);
+          if (Op::kCorr && j > 0)
+            for (int h = 0; h < 2; ++h)
+              tma_g2s_3d(ysl + (slot * 2 + h) * kP3YT, tmy, (int)x0, (int)y0, (int)(2 * K + h + 2), b);
+        }
+      }
+      ring += (uint32_t)pairs + 1u;
+      continue;
     }
     const bool xpad = x0 + 4 * lane + 3 == N - 1;
     const bool ypad = y0 + wy == N - 1;
+    T* dstp = O + 2 * K0 * N2 + (y0 + wy) * N + x0 + 4 * lane;
     V Sp[4] = {0, 0, 0, 0};  // S_{K-1}
-    for (int s = 0; s < pairs; ++s) {
-      const int slot = s % kP3S;
-      mbar_wait(&bar[slot], (parity >> slot) & 1u);
-      parity ^= 1u << slot;
-      auto S_of = [&](int sl, V S[4]) {
-        const T* cb = csl + sl * kP3CT;
+    for (int j = 0; j <= pairs; ++j) {
+      const uint32_t g = ring + (uint32_t)j, slot = g % kP3S;
+      mbar_wait(&full[slot], (g / kP3S) & 1u);
+      V Sc[4];
+      {
+        const T* cb = csl + slot * kP3CT;
         V acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
@@ -1340,78 +1372,106 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
           acc[3] += 2 * e;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) S[q] = acc[q];
-      };
-      if (s == 0) S_of((kP3S - 1) % kP3S, Sp);
-      V Sc[4];
-      S_of(slot, Sc);
+        for (int q = 0; q < 4; ++q) Sc[q] = acc[q];
+      }
+      if (j > 0) {
+        const int s = j - 1;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t k = 2 * (K0 + s) + h;  // local fine plane
-        V yv[4] = {0, 0, 0, 0};
-        if (Op::kCorr) {
-          const T* yp = ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane;
-          if constexpr (sizeof(T) == 4) {
-            const int4 y4 = *reinterpret_cast<const int4*>(yp);
-            yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
-          } else {
-            const longlong2 a = reinterpret_cast<const longlong2*>(yp)[0];
-            const longlong2 b = reinterpret_cast<const longlong2*>(yp)[1];
-            yv[0] = a.x >> sy, yv[1] = a.y >> sy, yv[2] = b.x >> sy, yv[3] = b.y >> sy;
+        for (int h = 0; h < 2; ++h) {
+          if constexpr (FW && sizeof(T) == 4) {
+            int y4[4] = {0, 0, 0, 0};
+            if constexpr (Op::kCorr) {
+              const int4 yy = *reinterpret_cast<const int4*>(ysl + (slot * 2 + h) * kP3YT +
+                                                             wy * kP3W + 4 * lane);
+              y4[0] = yy.x >> sy, y4[1] = yy.y >> sy, y4[2] = yy.z >> sy, y4[3] = yy.w >> sy;
+            }
+            int tq[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int gq = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+              if constexpr (Op::kCorr) {
+                const int64_t z = mad_wide(gq, Pg, mul_wide(y4[q], Py));
+                const uint32_t zl = (uint32_t)z, zh = (uint32_t)((uint64_t)z >> 32);
+                if (MODE == MODE_QCOMP) {
+                  const uint32_t sg = (uint32_t)((int)zh >> 31);
+                  o32lo |= zl ^ sg;
+                  o32hi |= zh ^ sg;
+                }
+                tq[q] = (int)__funnelshift_r(zl, zh, c.rs);
+              } else {
+                if (MODE == MODE_QCOMP) o32lo |= (uint32_t)(gq ^ (gq >> 31));
+                tq[q] = gq >> c.rs;
+              }
+              mx = tq[q] > mx ? tq[q] : mx;
+              mn = tq[q] < mn ? tq[q] : mn;
+            }
+            *reinterpret_cast<int4*>(dstp) = make_int4(tq[0], tq[1], tq[2], tq[3]);
+            dstp += N2;
+            continue;
           }
-        }
-        const bool rowpad = ypad || k + Z0 == N - 1;
-        T tt[4];
+          const int64_t k = 2 * (K0 + s) + h;  // local fine plane
+          V yv[4] = {0, 0, 0, 0};
+          if (Op::kCorr) {
+            const T* yp = ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane;
+            if constexpr (sizeof(T) == 4) {
+              const int4 y4 = *reinterpret_cast<const int4*>(yp);
+              yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
+            } else {
+              const longlong2 a = reinterpret_cast<const longlong2*>(yp)[0];
+              const longlong2 b = reinterpret_cast<const longlong2*>(yp)[1];
+              yv[0] = a.x >> sy, yv[1] = a.y >> sy, yv[2] = b.x >> sy, yv[3] = b.y >> sy;
+            }
+          }
+          const bool rowpad = ypad || k + Z0 == N - 1;
+          T tt[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const V g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
-          int64_t z;
-          if constexpr (sizeof(T) == 4)
-            z = op.corr(g, yv[q]);
-          else
-            z = op.corr_w(g, yv[q]);
-          if ((q == 3 && xpad) || rowpad) z = 0;
-          if constexpr (FW) {
-            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+          for (int q = 0; q < 4; ++q) {
+            const V gq = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+            int64_t z;
             if constexpr (sizeof(T) == 4)
-              tt[q] = (T)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+              z = op.corr(gq, yv[q]);
             else
-              tt[q] = (T)(z >> c.rs);
-          } else if (MODE == MODE_NNQ) {
-            tt[q] = (T)shift_clamp<int64_t>(z, c.lam, p.w_out);
-          } else {
-            if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
-            tt[q] = store ? store_shift<T, int64_t>(z, c) : (T)0;
+              z = op.corr_w(gq, yv[q]);
+            if ((q == 3 && xpad) || rowpad) z = 0;
+            if constexpr (FW) {
+              if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+              if constexpr (sizeof(T) == 4)
+                tt[q] = (T)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
+              else
+                tt[q] = (T)(z >> c.rs);
+            } else if (MODE == MODE_NNQ) {
+              tt[q] = (T)shift_clamp<int64_t>(z, c.lam, p.w_out);
+            } else {
+              if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
+              tt[q] = store ? store_shift<T, int64_t>(z, c) : (T)0;
+            }
+            mx = tt[q] > mx ? tt[q] : mx;
+            mn = tt[q] < mn ? tt[q] : mn;
           }
-          mx = tt[q] > mx ? tt[q] : mx;
-          mn = tt[q] < mn ? tt[q] : mn;
-        }
-        T* dst = O + k * N2 + (y0 + wy) * N + x0 + 4 * lane;
-        if constexpr (sizeof(T) == 4) {
-          *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
-        } else {
-          reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
-          reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+          T* dst = O + k * N2 + (y0 + wy) * N + x0 + 4 * lane;
+          if constexpr (sizeof(T) == 4) {
+            *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+          } else {
+            reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
+            reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+          }
         }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) Sp[q] = Sc[q];
-      __syncthreads();  // slot of step s (and, at s = 0, of step -1) is free
-      if (t == 0 && s + kP3D < pairs) {
-        fence_proxy_async_smem();
-        issue(s + kP3D);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // this warp is done with the slot
     }
-    __syncthreads();
+    ring += (uint32_t)pairs + 1u;
   }
-  r.olo |= olo;
+  r.olo |= olo | ((uint64_t)o32hi << 32) | o32lo;
   r.ohi |= ohi;
   r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
 }
 
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kP3T, sizeof(T) == 4 ? BFP_P3_MINB : 2)
+__global__ void __launch_bounds__(kP3T + 32, sizeof(T) == 4 ? BFP_P3_MINB : 2)
     pro3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ P3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1427,7 +1487,10 @@ __global__ void __launch_bounds__(kP3T, sizeof(T) == 4 ? BFP_P3_MINB : 2)
     uint64_t* bar =
         reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T));
     if (threadIdx.x == 0) {
-      for (int k = 0; k < kP3S; ++k) mbar_init(&bar[k], 1);
+      for (int k = 0; k < kP3S; ++k) {
+        mbar_init(&bar[k], 1);                    // full: the producer's expect_tx arrival
+        mbar_init(&bar[kP3S + k], kP3T / 32);     // empty: one arrival per consumer warp
+      }
       mbar_fence_init();
     }
     __syncthreads();
@@ -1667,6 +1730,7 @@ __device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const Wi
   const int t = threadIdx.x, col = 2 * t + 4;
   int32_t mx = INT32_MIN, mn = INT32_MAX;
   uint64_t olo = 0, ohi = 0;
+  uint32_t o32lo = 0, o32hi = 0;  // fast window: OR of z ^ sign(z) in two words
   const bool store = c.store_tmp;
   uint32_t parity = 0;
   for (int item = blockIdx.x; item < strips * chunks; item += gridDim.x) {
@@ -1693,6 +1757,14 @@ __device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const Wi
       for (int s = 0; s < kP2D && s < pairs; ++s) issue(s);
     }
     const bool xpad = x0 + 4 * t + 3 == N - 1;
+    // fast window: z = g Pg + y Py as two IMAD.WIDE, output pointer advanced per row, no pad
+    // masking (a fine pad index has both coarse taps on the coarse pad; see pro3_loop)
+    [[maybe_unused]] int Pg = 1, Py = 0;
+    if constexpr (Op::kCorr) {
+      Pg = op.swap ? 1 : op.P;
+      Py = op.swap ? op.P : 1;
+    }
+    int32_t* dstp = O + 2 * J0 * N + x0 + 4 * t;
     int Sp[4] = {0, 0, 0, 0};
     auto S_of = [&](int sl, int S[4]) {
       const int32_t* row = csl + sl * kP2CW + col;
@@ -1711,6 +1783,36 @@ __device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const Wi
       S_of(slot, Sc);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        if constexpr (FW) {
+          int y4[4] = {0, 0, 0, 0};
+          if constexpr (Op::kCorr) {
+            const int4 yy = *reinterpret_cast<const int4*>(ysl + (slot * 2 + h) * kP2W + 4 * t);
+            y4[0] = yy.x >> sy, y4[1] = yy.y >> sy, y4[2] = yy.z >> sy, y4[3] = yy.w >> sy;
+          }
+          int tq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int g = h ? 2 * Sc[q] : Sp[q] + Sc[q];
+            if constexpr (Op::kCorr) {
+              const int64_t z = mad_wide(g, Pg, mul_wide(y4[q], Py));
+              const uint32_t zl = (uint32_t)z, zh = (uint32_t)((uint64_t)z >> 32);
+              if (MODE == MODE_QCOMP) {
+                const uint32_t sg = (uint32_t)((int)zh >> 31);
+                o32lo |= zl ^ sg;
+                o32hi |= zh ^ sg;
+              }
+              tq[q] = (int)__funnelshift_r(zl, zh, c.rs);
+            } else {
+              if (MODE == MODE_QCOMP) o32lo |= (uint32_t)(g ^ (g >> 31));
+              tq[q] = g >> c.rs;
+            }
+            mx = tq[q] > mx ? tq[q] : mx;
+            mn = tq[q] < mn ? tq[q] : mn;
+          }
+          *reinterpret_cast<int4*>(dstp) = make_int4(tq[0], tq[1], tq[2], tq[3]);
+          dstp += N;
+          continue;
+        }
         const int64_t j = 2 * (J0 + s) + h;  // local fine row
         int yv[4] = {0, 0, 0, 0};
         if (Op::kCorr) {
@@ -1748,7 +1850,7 @@ __device__ __forceinline__ void pro2_loop(const Op& op, const Vec& out, const Wi
     }
     __syncthreads();
   }
-  r.olo |= olo;
+  r.olo |= olo | ((uint64_t)o32hi << 32) | o32lo;
   r.ohi |= ohi;
   r.mx = (int64_t)mx > r.mx ? (int64_t)mx : r.mx;
   r.mn = (int64_t)mn < r.mn ? (int64_t)mn : r.mn;
@@ -2123,7 +2225,7 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
     for (auto fn : {pro3_win_kernel<MODE_QCOMP, T, Op>, pro3_win_kernel<MODE_NNQ, T, Op>,
                     pro3_win_kernel<MODE_RECOMPUTE, T, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kP3Smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pro3_win_kernel<MODE_QCOMP, T, Op>, kP3T,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, pro3_win_kernel<MODE_QCOMP, T, Op>, kP3T + 32,
                                                   kP3Smem);
     return std::max(o, 1);
   });
@@ -2134,11 +2236,11 @@ static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(pro3_win_kernel<MODE_QCOMP, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_QCOMP, T, Op>, b, kP3T + 32, kP3Smem, s, op, o, pp, R, tm);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(pro3_win_kernel<MODE_NNQ, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_NNQ, T, Op>, b, kP3T + 32, kP3Smem, s, op, o, pp, R, tm);
     else
-      launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kP3T, kP3Smem, s, op, o, pp, R, tm);
+      launch_pdl(pro3_win_kernel<MODE_RECOMPUTE, T, Op>, b, kP3T + 32, kP3Smem, s, op, o, pp, R, tm);
     count_launch();
     count_family(FAM_PRO3);
   };

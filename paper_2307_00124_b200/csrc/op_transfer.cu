@@ -101,3 +101,14 @@ int op_prolong_correct(bfp_vec_s* ec, bfp_vec_s* y, const WinParams& p, bfp_vec_
 }
 
 }  // namespace bfp
+
+#ifdef BFP_P3_TIMING
+// measurement builds: per-phase clocks of block 0 / thread 0 of the pro3 marches (read + reset)
+extern "C" int bfp_dbg_p3(long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_p3_prof, sizeof(long long) * 8);
+  long long z[8] = {};
+  cudaMemcpyToSymbol(g_p3_prof, z, sizeof(z));
+  return 8;
+}
+#endif
