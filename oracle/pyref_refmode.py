@@ -246,6 +246,7 @@ class RefConfig:
     ext_prec: int = 400  # Hierarchy precision (ExtFloat)
     x0: Optional[P.Block] = None
     d: int = 1          # 1 or 2
+    w_add_cap: int = -1  # GammaPolicy::w_add_cap (P/src/multigrid.cpp:75-79); < 0: unlimited
 
 
 @dataclass
@@ -276,6 +277,8 @@ class RefMg:
 
     def step(self, name, level, k, w_out, g: XF, ir_iter=1):
         w_add = (5 if ir_iter == 1 else 4) if name == "ir-residual" else W_ADD[name]
+        if self.cfg.w_add_cap >= 0:  # GammaPolicy::w_tmp_for
+            w_add = min(w_add, self.cfg.w_add_cap)
         gam = scalar_up(g)
         out, fl = P.qcomp(k, w_out, w_out + w_add, gam)
         self.res.trace.append((STEP_IDS[name], level, w_out, w_out + w_add, gam.m[0], gam.e,
@@ -338,6 +341,14 @@ class RefMg:
         for _ in range(cfg.cycles):
             x = self.ir(lev, x, 1)
         return x
+
+    def recomputes_at_level(self, level: int) -> int:
+        """SolverTrace::recomputes_at_level (P/src/multigrid.cpp:165-170)."""
+        return sum(1 for t in self.res.trace if t[1] == level and (t[6] or t[7]))
+
+    def calls_at_level(self, level: int) -> int:
+        """SolverTrace::calls_at_level (:172-177)."""
+        return sum(1 for t in self.res.trace if t[1] == level)
 
     def run(self) -> RefResult:
         cfg = self.cfg

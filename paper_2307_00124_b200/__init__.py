@@ -653,6 +653,122 @@ def gen_sine(v: BfpVec, p: int) -> BfpVec:
 # multigrid solver
 
 
+class PrecisionSchedule:
+    """Per-level mantissa widths, 1-based (index 0 unused): wcheck (inputs / matrices), w
+    (working) and wdot (inner), with wcheck >= w >= wdot >= 1 -- the reference's
+    PrecisionSchedule (P/include/bfpmg/multigrid.hpp:16-27, P/src/multigrid.cpp:13-44)."""
+
+    def __init__(self, wcheck: Sequence[int], w: Sequence[int], wdot: Sequence[int]):
+        self.wcheck, self.w, self.wdot = list(wcheck), list(w), list(wdot)
+
+    @classmethod
+    def flat(cls, levels: int, wc: int, ww: int, wd: int) -> "PrecisionSchedule":
+        return cls([0] + [wc] * levels, [0] + [ww] * levels, [0] + [wd] * levels)
+
+    @classmethod
+    def affine(cls, levels: int, m: int, k: int, q_check: int, q_w: int,
+               q_dot: int) -> "PrecisionSchedule":
+        """wcheck_j = (m + k) j + q_check, w_j = k j + q_w, wdot_j = m j + q_dot, clamped so
+        that the ordering invariant holds on every level (:22-35)."""
+        wc, w, wd = [0], [0], [0]
+        for j in range(1, levels + 1):
+            wj = k * j + q_w
+            w.append(wj)
+            wc.append(max((m + k) * j + q_check, wj))
+            wd.append(min(m * j + q_dot, wj))
+        return cls(wc, w, wd)
+
+    def levels(self) -> int:
+        return len(self.w) - 1
+
+    def validate(self) -> None:
+        """Raises ValueError (the reference's std::invalid_argument, :37-44)."""
+        for j in range(1, self.levels() + 1):
+            if not (self.wcheck[j] >= self.w[j] >= self.wdot[j] >= 1):
+                raise ValueError(f"PrecisionSchedule: width ordering violated at level {j}")
+
+
+# step names of the reference (P/src/multigrid.cpp:49-60); the config-mode driver adds the
+# first sweep from zero and the diagnostic final residual (DESIGN.md section 3.2)
+REF_STEP_NAMES = {"ir-residual", "ir-correction", "v-relax", "v-residual", "v-restrict",
+                  "v-correct", "fmg-prolong"}
+
+
+def gamma_str(gm: int, ge: int, digits: int = 6) -> str:
+    """gamma = gm 2^ge printed like the reference's ExtFloat::str(6) (mpfr "%.6Rg",
+    P/src/extfloat.cpp:65-73): the exact value rounded to `digits` significant digits."""
+    from fractions import Fraction
+    v = Fraction(gm) * (Fraction(2) ** ge)
+    try:
+        f = float(v)
+        if f != 0.0 and Fraction(f) == v:
+            return "%.*g" % (digits, f)
+    except OverflowError:
+        pass
+    if v == 0:
+        return "0"
+    # beyond double range: scientific notation from the exact rational
+    import math
+    neg, a = v < 0, abs(v)
+    e10 = int(math.floor((a.numerator.bit_length() - a.denominator.bit_length()) * 0.30103))
+    while a >= Fraction(10) ** (e10 + 1):
+        e10 += 1
+    while a < Fraction(10) ** e10:
+        e10 -= 1
+    scaled = a / Fraction(10) ** (e10 - digits + 1)
+    n = int(scaled)
+    rem = scaled - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2):
+        n += 1
+    if n == 10 ** digits:
+        n //= 10
+        e10 += 1
+    mant = str(n).rstrip("0") or "0"
+    mant = mant[0] + ("." + mant[1:] if len(mant) > 1 else "")
+    return ("-" if neg else "") + f"{mant}e{'+' if e10 >= 0 else '-'}{abs(e10):02d}"
+
+
+@dataclass
+class TraceRecord:
+    """One run_step record (P/include/bfpmg/multigrid.hpp:74-87)."""
+    step: int
+    level: int
+    w_out: int
+    w_tmp: int
+    gm: int
+    ge: int
+    overflow: int
+    underflow: int
+    recomputed: int
+    normalized: int
+
+    def step_name(self) -> str:
+        return STEP_NAMES[self.step]
+
+    def to_line(self) -> str:
+        """TraceRecord::to_line (P/src/multigrid.cpp:157-163), byte for byte."""
+        return (f"{self.step_name()} level={self.level} w_out={self.w_out} w_tmp={self.w_tmp} "
+                f"gamma={gamma_str(self.gm, self.ge)} overflow={int(bool(self.overflow))} "
+                f"underflow={int(bool(self.underflow))} recompute={int(bool(self.recomputed))} "
+                f"normalized={int(bool(self.normalized))}")
+
+
+class SolverTrace:
+    """SolverTrace (P/include/bfpmg/multigrid.hpp:89-94) over a solve's trace records."""
+
+    def __init__(self, records):
+        self.records = [r if isinstance(r, TraceRecord) else TraceRecord(*r) for r in records]
+
+    def recomputes_at_level(self, level: int) -> int:  # P/src/multigrid.cpp:165-170
+        return sum(1 for r in self.records if r.level == level and (r.overflow or r.underflow))
+
+    def calls_at_level(self, level: int) -> int:       # :172-177
+        return sum(1 for r in self.records if r.level == level)
+
+    def lines(self) -> List[str]:
+        return [r.to_line() for r in self.records]
+
+
 def _lv(v):
     if v is None:
         return [0] * 32
@@ -687,6 +803,9 @@ def mg_config_ref(l_fine, rho, eta, w, wdot=None, wcheck=None, cycles=1, fmg=Fal
     (Hierarchy::set_eta); w / wdot / wcheck: PrecisionSchedule widths (int or per-level
     list, index = level, levels 1..l_fine; >= 3 in 1-D, >= 5 in 2-D)."""
     from . import refmode
+    if isinstance(w, PrecisionSchedule):  # the reference's schedule object
+        w.validate()
+        w, wdot, wcheck = w.w, w.wdot, w.wcheck
     cfg = mg_config(d, l_fine, l_coarse=1, cycles=cycles, fmg=fmg, x0_random=x0_random,
                     rhs_kind=rhs_kind, seed=seed, p=w, pd=wdot, pc=wcheck, w_add_cap=w_add_cap,
                     fuse_points=0)
@@ -813,6 +932,10 @@ class Multigrid:
         trace = [(t.step, t.level, t.w_out, t.w_tmp, t.gm, t.ge, t.overflow, t.underflow,
                   t.recomputed, t.normalized) for t in tr[: min(nt.value, trace_cap)]]
         return x, int(hh.q), int(hh.e), hist[: nh.value].tolist(), trace
+
+    def trace(self, trace_cap: int = 1 << 20) -> SolverTrace:
+        """The solve's records as the reference's SolverTrace."""
+        return SolverTrace(self.result(trace_cap)[4])
 
     def vectors(self):
         x, b, r = C.c_void_p(), C.c_void_p(), C.c_void_p()

@@ -1140,8 +1140,17 @@ static int check_cfg(const bfp_mg_config_t* cfg) {
       if (cfg->p[l] < 3 || cfg->p[l] > 58 || cfg->pd[l] < 0 || cfg->pd[l] > 58 ||
           cfg->pc[l] < 0 || cfg->pc[l] > 58 || cfg->ref_c1d[l].q < 1 || cfg->ref_c2d[l].q < 1)
         return BFP_ERR_ARG;
+    // PrecisionSchedule::validate (P/src/multigrid.cpp:37-44, enforced by the reference's
+    // Hierarchy at :259): wcheck >= w >= wdot >= 1 on every level (0 entries mean w)
+    for (int l = 1; l <= cfg->l_fine; ++l) {
+      const int w = cfg->p[l], wd = cfg->pd[l] ? cfg->pd[l] : w, wc = cfg->pc[l] ? cfg->pc[l] : w;
+      if (!(wc >= w && w >= wd && wd >= 1)) return BFP_ERR_ARG;
+    }
     return BFP_OK;
   }
+  // (config mode keeps wdot > w legal: the frozen config 1 runs its residual and V-cycle at
+  // 28 bits over a 16-bit iterate, DESIGN.md section 3.4 -- a relaxation of the reference's
+  // ordering invariant that the reference-algorithm mode does not share)
   if (cfg->d < 1 || cfg->d > 3 || cfg->l_coarse < 2 || cfg->l_fine < cfg->l_coarse ||
       cfg->l_fine > 30 || cfg->nu1 < 1 || cfg->nu2 < 0 || cfg->n_coarse < 1 || cfg->cycles < 0 ||
       cfg->qc < 2 || cfg->qc > 30)

@@ -147,3 +147,23 @@ def conv_rate_vcycle(level: int, rho: float, eta: float, w, wdot=None, wcheck=No
     A = _stiffness(level, d)
     lam = scipy.linalg.eigh(M.T @ A @ M, A, eigvals_only=True)
     return float(np.sqrt(max(lam.max(), 0.0))), cols
+
+
+def recompute_table(level: int, rho: float, eta: float, w, wdot=None, wcheck=None, n_ir: int = 1,
+                    caps=(-1, 4, 2, 0), rhs_kind: int = 1, d: int = 1, ext_prec: int = 400):
+    """The reference's recompute table (cmd_recompute_table, P/src/experiments.cpp:556-600):
+    the FMG solve of the reference-algorithm mode under GammaPolicy::w_add_cap = inf, 4, 2, 0,
+    and for each cap the recomputations and calls at the finest level
+    (SolverTrace::recomputes_at_level / calls_at_level, P/src/multigrid.cpp:165-177).
+    Returns rows (cap, recomputes, calls) -- cap -1 is the table's "inf"."""
+    from . import Multigrid, mg_config_ref
+
+    rows = []
+    for cap in caps:
+        cfg = mg_config_ref(level, rho, eta, w=w, wdot=wdot, wcheck=wcheck, cycles=n_ir, fmg=True,
+                            rhs_kind=rhs_kind, ext_prec=ext_prec, w_add_cap=cap, d=d)
+        mg = Multigrid(cfg)
+        mg.solve(use_graph=True)
+        tr = mg.trace()
+        rows.append((cap, tr.recomputes_at_level(level), tr.calls_at_level(level)))
+    return rows

@@ -95,3 +95,12 @@ def test_refmode_host_scalars_match_the_restatement():
             a = R.quantize_scalar_floor(c1x, wdot[l])
             b = R.quantize_scalar_floor(c2x, wdot[l])
             assert c1d[l] == (a.m[0], wdot[l], a.e) and c2d[l] == (b.m[0], wdot[l], b.e)
+
+
+def test_cpp_facade_compiles():
+    """include/bfpmg_b200.hpp (the reference-named C++ facade) builds against the C-ABI
+    with g++ alone (no CUDA headers in the facade)."""
+    import __graft_entry__ as g
+    g.build_facade_test()
+    assert os.path.exists(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "tests", "cpp", "_build", "facade_test"))

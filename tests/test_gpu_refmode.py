@@ -96,3 +96,55 @@ def test_conv_rate_vcycle_columns(B, d, L):
         want = R.RefMg(cfg, {L: P.zero_vec(n, wc)}).run()
         assert cols[i][1] == want.x.e and cols[i][0].tolist() == want.x.m, i
     assert 0.0 < rate < 1.0
+
+
+@pytest.mark.parametrize("d,L,w,wd,wc", [(1, 7, 14, 10, 18), (2, 5, 12, 9, 16)])
+def test_recompute_table_vs_pyref(B, d, L, w, wd, wc):
+    """The reference's Table 2 (cmd_recompute_table, P/src/experiments.cpp:556-600): per
+    w_add cap, recomputations and calls at the finest level of the FMG solve
+    (SolverTrace::recomputes_at_level / calls_at_level) -- GPU counts equal the
+    restatement's, the records' to_line text included, and the counts grow as the cap
+    shrinks (the table's own check)."""
+    from paper_2307_00124_b200 import refmode
+    rho, eta = (2.02, 0.3) if d == 1 else (1.6, 0.3)
+    rows = refmode.recompute_table(L, rho, eta, w=w, wdot=wd, wcheck=wc, n_ir=2, d=d)
+    lv = [0] + [w] * L, [0] + [wd] * L, [0] + [wc] * L
+    prev = -1
+    for cap, rec, calls in rows:
+        cfg = R.RefConfig(l_fine=L, w=lv[0], wdot=lv[1], wcheck=lv[2], rho=rho, eta=eta, cycles=2,
+                          fmg=True, d=d, w_add_cap=cap)
+        mg = R.RefMg(cfg, _rhs(1, L, lv[2], 3, True, d))
+        mg.run()
+        assert (rec, calls) == (mg.recomputes_at_level(L), mg.calls_at_level(L)), cap
+        assert rec >= prev, rows
+        prev = rec
+    assert rows[-1][1] > 0  # cap 0: no headroom, the narrow window recomputes
+    # the trace text of one run, line by line (TraceRecord::to_line, :157-163)
+    gcfg = B.mg_config_ref(L, rho, eta, w=B.PrecisionSchedule.flat(L, wc, w, wd), cycles=2,
+                           fmg=True, rhs_kind=1, d=d, w_add_cap=2)
+    mg = B.Multigrid(gcfg)
+    mg.solve()
+    lines = mg.trace().lines()
+    cfg = R.RefConfig(l_fine=L, w=lv[0], wdot=lv[1], wcheck=lv[2], rho=rho, eta=eta, cycles=2,
+                      fmg=True, d=d, w_add_cap=2)
+    want = R.RefMg(cfg, _rhs(1, L, lv[2], 3, True, d)).run()
+    assert len(lines) == len(want.trace)
+    for line, t in zip(lines, want.trace):
+        assert line == B.TraceRecord(*t).to_line()
+        assert line.split()[0] in B.REF_STEP_NAMES
+
+
+def test_refmode_schedule_validate(B):
+    """PrecisionSchedule::validate (P/src/multigrid.cpp:37-44): the reference mode rejects
+    schedules that break wcheck >= w >= wdot >= 1, in the mirror and in the C-ABI."""
+    s = B.PrecisionSchedule.affine(6, 1, 2, 8, 4, 2)
+    s.validate()
+    assert s.w[3] == 10 and s.wcheck[3] == 17 and s.wdot[3] == 5
+    bad = B.PrecisionSchedule.flat(5, 20, 16, 18)  # wdot > w
+    with pytest.raises(ValueError):
+        bad.validate()
+    with pytest.raises(ValueError):
+        B.mg_config_ref(5, 2.02, 0.3, w=bad)
+    cfg = B.mg_config_ref(5, 2.02, 0.3, w=16, wdot=18, wcheck=20)  # raw widths: the C-ABI checks
+    with pytest.raises(B.BfpError):
+        B.Multigrid(cfg)
