@@ -701,8 +701,34 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
     // source row clamp: rows past the slab read its back halo row (zeros or exchanged)
     auto xsrc = [&](int64_t row) { return X + (row > NZ ? NZ : row) * N + c0 - 4; };
     auto ysrc = [&](int64_t row) { return Y + (row > NZ ? NZ : row) * N + c0; };
-    // the first item's prologue may have been issued before the op setup (EARLY)
-    if (t == 0 && !(EARLY && item == (int)blockIdx.x)) bulk_prologue(op, out, R, smem, item);
+    // Warp 8 is the producer (lane 0 issues every bulk copy); warps 0..7 only consume.
+    // The first item's prologue may have been issued before the op setup (EARLY, thread 0).
+    if (t >= kBulkT) {
+      if (t == kBulkT) {
+        if (!(EARLY && item == (int)blockIdx.x)) bulk_prologue(op, out, R, smem, item);
+        int fx = (int)((j0 - 1 + kBulkXS) % kBulkXS), fy = (int)(j0 % kBulkYS);
+        for (int s = 0; s < rows; ++s) {
+          // step j0 + s frees x row j - 1 (slot fx) and y row j / its barrier (slot fy)
+          const uint32_t ep = (eparity >> fy) & 1u;
+          eparity ^= 1u << fy;
+          if (s + kBulkD + 1 < rows) {
+            mbar_wait(&ebar[fy], ep);  // every consumer warp has finished step j
+            const int64_t tr = j0 + s + kBulkD + 1;
+            uint64_t* bb = &bar[fy];
+            fence_proxy_async_smem();
+            mbar_expect_tx(bb, tx_bytes);
+            bulk_g2s(xsl + fx * kBulkXW, xsrc(tr + 1), kBulkXW * 4, bb);
+            bulk_g2s(ysl + fy * kBulkW, ysrc(tr), kBulkW * 4, bb);
+          }
+          fx = fx + 1 == kBulkXS ? 0 : fx + 1;
+          fy = fy + 1 == kBulkYS ? 0 : fy + 1;
+        }
+      }
+      // the consumers' full-barrier phases of this item, for the bookkeeping below
+      for (int s = 0; s < rows; ++s) parity ^= 1u << ((j0 + s) % kBulkYS);
+      __syncthreads();
+      continue;
+    }
     const bool xpad = c0 + 4 * t + 3 == N - 1;
     const int lane = t & 31;
     // running ring indices (no 64-bit modulo in the step loop)
@@ -754,28 +780,11 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       sc = sn;
       sn = sn + 1 == kBulkXS ? 0 : sn + 1;
       sy_ = sy_ + 1 == kBulkYS ? 0 : sy_ + 1;
-#if BFP_B2_EMPTY
-      // this warp is done with x row j-1 and y row j
+      // this warp is done with x row j-1 and y row j: the producer refills their slots
+      (void)free_x;
       __syncwarp();
       if (lane == 0) mbar_arrive(&ebar[free_y]);
-      const uint32_t ep = (eparity >> free_y) & 1u;
       eparity ^= 1u << free_y;
-      if (t == 0 && s + kBulkD + 1 < rows) {
-        mbar_wait(&ebar[free_y], ep);  // every warp has finished step j
-#else
-      (void)ebar;
-      (void)eparity;
-      __syncthreads();  // slots of x row j-1 and y row j are free
-      if (t == 0 && s + kBulkD + 1 < rows) {
-#endif
-        // next group: x row tr+1 -> slot (j-1) % XS, y row tr -> slot j % YS, tr = j+D+1
-        const int64_t tr = j + kBulkD + 1;
-        uint64_t* bb = &bar[free_y];
-        fence_proxy_async_smem();
-        mbar_expect_tx(bb, tx_bytes);
-        bulk_g2s(xsl + free_x * kBulkXW, xsrc(tr + 1), kBulkXW * 4, bb);
-        bulk_g2s(ysl + free_y * kBulkW, ysrc(tr), kBulkW * 4, bb);
-      }
     }
     __syncthreads();
   }
@@ -786,7 +795,7 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
 }
 
 template <int MODE, typename Op>
-__global__ void __launch_bounds__(kBulkT, BFP_B2_MINB) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
+__global__ void __launch_bounds__(kBulkT + 32, BFP_B2_MINB) bulk_win_kernel(Op op, Vec out, WinParams p, int R) {
   griddep_wait();
   extern __shared__ __align__(128) char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)(kBulkXS * kBulkXW + kBulkYS * kBulkW) * 4);
@@ -2394,7 +2403,7 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
     for (auto fn : {bulk_win_kernel<MODE_QCOMP, Op>, bulk_win_kernel<MODE_NNQ, Op>,
                     bulk_win_kernel<MODE_RECOMPUTE, Op>})
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, bulk_win_kernel<MODE_QCOMP, Op>, kBulkT,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, bulk_win_kernel<MODE_QCOMP, Op>, kBulkT + 32,
                                                   kBulkSmem);
     return std::max(o, 1);
   });
@@ -2406,11 +2415,11 @@ static inline int launch_bulk(const Op& op, bfp_vec_s* out, const WinParams& p0,
   WinParams p = p0;
   auto go = [&](const WinParams& pp) {
     if (pp.mode == MODE_QCOMP)
-      launch_pdl(bulk_win_kernel<MODE_QCOMP, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+      launch_pdl(bulk_win_kernel<MODE_QCOMP, Op>, b, kBulkT + 32, kBulkSmem, s, op, o, pp, R);
     else if (pp.mode == MODE_NNQ)
-      launch_pdl(bulk_win_kernel<MODE_NNQ, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+      launch_pdl(bulk_win_kernel<MODE_NNQ, Op>, b, kBulkT + 32, kBulkSmem, s, op, o, pp, R);
     else
-      launch_pdl(bulk_win_kernel<MODE_RECOMPUTE, Op>, b, kBulkT, kBulkSmem, s, op, o, pp, R);
+      launch_pdl(bulk_win_kernel<MODE_RECOMPUTE, Op>, b, kBulkT + 32, kBulkSmem, s, op, o, pp, R);
     count_launch();
     count_family(FAM_BULK2);
   };
