@@ -895,6 +895,10 @@ SOLVES = {
     # the fastest V(nu1, nu2) x n_ir variant below the discretisation error in the sweep of
     # tools/fmg_sweep.py (V(2,1) x 2: alg/disc 0.56, 12% faster than V(2,2) x 2)
     "C4_3d_fmg_v21_n2": dict(d=3, l_fine=9, cycles=2, rhs_kind=1, fmg=True, p=24, nu2=1),
+    # the fastest below the discretisation error in the second sweep (tools/fmg_sweep2.py):
+    # V(2,0) x 2 with the coarsest level at 7^3 and 32 coarse sweeps (alg/disc 0.84)
+    "C4_3d_fmg_v20_n2_lc3": dict(d=3, l_fine=9, l_coarse=3, cycles=2, rhs_kind=1, fmg=True,
+                                 p=24, nu2=0, n_coarse=32),
 }
 
 

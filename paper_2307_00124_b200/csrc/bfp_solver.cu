@@ -46,7 +46,7 @@ struct PlanOp {
   int kind;
   bfp_vec_s *a = nullptr, *b = nullptr, *out = nullptr;
   Scal s1{0, 0, 0}, s2{0, 0, 0};
-  WinParams p;
+  WinParams p{};  // (ops without a window -- zero_vec, copies -- keep it zeroed)
   int64_t q = 0;
   uint64_t seed = 0, sid = 0;
   std::vector<PlanOp> sub;  // OK_FUSED: the coarse-level ops run by one CTA
@@ -680,6 +680,9 @@ struct RankSolver {
     cudaMemset(d_hist, 0, sizeof(double) * std::max(n_hist, 1));
     std::vector<PlanOp> built;
     built.reserve(plan.size());
+#ifdef BFP_DEBUG_BUILD
+    fprintf(stderr, "finish_build: %zu plan ops\n", plan.size());
+#endif
     for (auto& op : plan) {
       op.p.trace = d_trace;
       op.p.hist = op.p.hist_slot >= 0 ? d_hist : nullptr;
@@ -688,6 +691,9 @@ struct RankSolver {
         continue;
       }
       std::vector<FusedOp> h(op.sub.size());
+#ifdef BFP_DEBUG_BUILD
+      fprintf(stderr, "fused list of %zu ops\n", op.sub.size());
+#endif
       for (size_t i = 0; i < op.sub.size(); ++i) {
         PlanOp& so = op.sub[i];
         so.p.trace = d_trace;
@@ -699,6 +705,9 @@ struct RankSolver {
       }
       for (size_t i = 0; i + 1 < h.size(); ++i)
         h[i].lr.nnq_next = h[i + 1].kind != bfpdev::FK_ZERO && h[i + 1].p.mode == MODE_NNQ;
+#ifdef BFP_DEBUG_BUILD
+      fprintf(stderr, "  made, building arena\n");
+#endif
       if (!build_arena(op, h)) {
         // the list's state does not fit one CTA's shared memory: one launch per op instead
         if (err) return err;
@@ -710,6 +719,9 @@ struct RankSolver {
       built.push_back(std::move(op));
     }
     plan = std::move(built);
+#ifdef BFP_DEBUG_BUILD
+    fprintf(stderr, "finish_build done: %zu ops\n", plan.size());
+#endif
     return cudaDeviceSynchronize() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
   }
 
@@ -767,6 +779,9 @@ struct RankSolver {
         for (int i = 0; i < f.p.gamma.nterms; ++i)
           if (f.p.gamma.t[i].v) ok = ok && note(f.p.gamma.t[i].v, false);
     }
+#ifdef BFP_DEBUG_BUILD
+    fprintf(stderr, "  arena: ok=%d vectors=%zu ops=%zu\n", (int)ok, vs.size(), h.size());
+#endif
     if (!ok || vs.size() > (size_t)bfpdev::kLeanMaxVec || h.size() > 30000) return false;
     std::vector<ArenaEntry> ar(vs.size());
     int64_t off = 128;  // offset 0 is reserved (nullptr gamma terms)

@@ -109,7 +109,7 @@ int fused_make(int kind, bfp_vec_s* a, bfp_vec_s* b, Scal s1, Scal s2, const Win
       f->u.pc.ep = -out->dim; f->u.pc.gs = 0;
       f->u.pc.al = Scal{1, 2, 0}; f->u.pc.be = Scal{1, 2, 0};
       break;
-    case FK_ZERO: break;
+    case FK_ZERO: memset(&f->p, 0, sizeof(f->p)); break;  // no window, no gamma rule
     default: return BFP_ERR_ARG;
   }
   lean_digest(f);

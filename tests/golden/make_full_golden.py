@@ -38,6 +38,10 @@ FULL = {
     "C4": dict(d=3, l_fine=9, cycles=1, rhs_kind=1, fmg=True, p=24),
     "C4_n2": dict(d=3, l_fine=9, cycles=2, rhs_kind=1, fmg=True, p=24),
     "C4_v21_n2": dict(d=3, l_fine=9, cycles=2, rhs_kind=1, fmg=True, nu2=1, p=24),
+    # the fastest variant below the discretisation error (tools/fmg_sweep2.py): V(2,0) x 2,
+    # coarsest level 7^3 with 32 Jacobi sweeps
+    "C4_v20_n2_lc3": dict(d=3, l_fine=9, l_coarse=3, cycles=2, rhs_kind=1, fmg=True, nu2=0,
+                          n_coarse=32, p=24),
 }
 for _p in (4, 8, 16, 32, 48):
     FULL[f"C5_511_p{_p}"] = dict(d=3, l_fine=9, cycles=10, x0_random=True, rhs_kind=2, p=_p)
