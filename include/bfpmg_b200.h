@@ -265,6 +265,13 @@ int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const
                           int min_planes, bfp_mg_t* out);
 /* per local rank: the final iterate / residual (slabs on sharded levels), global rank and
    the lowest sharded level (64: none) */
+/* Transport of the per-op exponent all-reduce of sharded solves created AFTER the call
+ * (DESIGN.md section 9): 0 = default (NCCL groups: peer-memory mailboxes over CUDA IPC when
+ * they can be mapped, else ncclAllReduce; in-process groups: one reduction kernel),
+ * 1 = mailboxes for in-process groups too (the protocol's test path), 2 = never mailboxes.
+ * bfp_mg_transport reports what a solver uses: 0 local kernel, 1 mailboxes, 2 ncclAllReduce. */
+int bfp_set_transport(int transport);
+int bfp_mg_transport(bfp_mg_t mg);
 int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_t* r_final,
                        int* rank, int* lowest_sharded_level);
 

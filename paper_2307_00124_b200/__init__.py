@@ -103,6 +103,7 @@ EXPORTS = [
     "bfp_set_kernel_path", "bfp_vec_download_async_i32", "bfp_vec_create_slab", "bfp_vec_planes",
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
     "bfp_nccl_unique_id", "bfp_mg_create_sharded", "bfp_mg_rank_result", "bfp_dist_create",
+    "bfp_set_transport", "bfp_mg_transport",
     "bfp_dist_destroy", "bfp_dist_stencil_gemv", "bfp_dist_stencil_jacobi",
     "bfp_quantize_exact", "bfp_from_doubles", "bfp_kernel_family_counts",
     "bfp_dot_exact_async", "bfp_dot_value", "bfp_dot_exact192", "bfp_dist_dot_exact",
@@ -180,6 +181,8 @@ def lib() -> C.CDLL:
         "bfp_dist_stencil_jacobi": (i32, [vp, C.POINTER(vp), C.POINTER(vp), S, i32, i64, i64, S,
                                           C.POINTER(vp), vp]),
         "bfp_mg_create_sharded": (i32, [C.POINTER(MgConfig), i32, i32, vp, i32, C.POINTER(vp)]),
+        "bfp_set_transport": (i32, [i32]),
+        "bfp_mg_transport": (i32, [vp]),
         "bfp_mg_rank_result": (i32, [vp, i32, C.POINTER(vp), C.POINTER(vp), C.POINTER(i32),
                                      C.POINTER(i32)]),
         "bfp_mg_kernel_launches": (i64, [vp]),
@@ -919,6 +922,11 @@ class Multigrid:
     def launches(self) -> int:
         return int(lib().bfp_mg_kernel_launches(self.h))
 
+    def transport(self) -> str:
+        """Transport of the per-op exponent all-reduce ("local-kernel", "peer-mailbox",
+        "nccl-allreduce")."""
+        return TRANSPORTS[int(lib().bfp_mg_transport(self.h))]
+
     def result(self, trace_cap: int = 1 << 20):
         n = ((1 << self.cfg.l_fine) - 1) ** self.cfg.d
         x = np.zeros(n, dtype=np.int64)
@@ -941,6 +949,15 @@ class Multigrid:
         x, b, r = C.c_void_p(), C.c_void_p(), C.c_void_p()
         _raise(lib().bfp_mg_vectors(self.h, C.byref(x), C.byref(b), C.byref(r)), "bfp_mg_vectors")
         return x, b, r
+
+
+TRANSPORTS = {0: "local-kernel", 1: "peer-mailbox", 2: "nccl-allreduce"}
+
+
+def set_transport(t: int):
+    """Exponent all-reduce transport of sharded solvers created afterwards
+    (include/bfpmg_b200.h: bfp_set_transport)."""
+    _raise(lib().bfp_set_transport(int(t)), "bfp_set_transport")
 
 
 def launch_count() -> int:

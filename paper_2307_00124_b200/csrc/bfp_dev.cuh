@@ -735,6 +735,28 @@ __device__ inline int win_finalize(const WinParams& p, const WinCtx& c, Hdr* h, 
   return 0;
 }
 
+// multi-rank finalize (one thread): apply the all-reduced partials {mu*, max, -min, err} with
+// the window context recorded by pass 1 -- exactly the single-rank win_finalize
+__device__ inline void finalize_from_partials(const Vec& out, WinParams p, const int64_t* part,
+                                              int storage_bits) {
+  Hdr* h = out.hdr;
+  if (p.mode == MODE_RECOMPUTE && !h->need_recompute) return;  // fast path: nothing ran
+  WinCtx c;
+  c.e_star = h->st_estar;
+  c.mu_tmp = h->st_mutmp;
+  c.lam = p.mode == MODE_RECOMPUTE ? h->lam_out : h->st_lam;
+  c.gm = h->st_gm;
+  c.ge = h->st_ge;
+  c.zd = h->st_zd;
+  c.rs = 0;
+  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
+  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
+  c.skip = 0;
+  p.part = nullptr;
+  win_finalize(p, c, h, (int)part[0], part[1], part[2] == INT64_MAX ? INT64_MIN : -part[2],
+               (int)part[3]);
+}
+
 // Reduction + finalize of a windowed pass.  A multi-block pass 1 (qcomp or nnqcomp)
 // launched with p.defer only accumulates: each block's partial goes to the header with
 // fire-and-forget atomics and block 0 records the window context; the stream-ordered

@@ -48,21 +48,7 @@ using bfp::last_launch;
 __global__ void window_finalize_kernel(Vec out, WinParams p, const int64_t* part, int storage_bits) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   griddep_wait();
-  Hdr* h = out.hdr;
-  if (p.mode == MODE_RECOMPUTE && !h->need_recompute) return;  // fast path: nothing ran
-  WinCtx c;
-  c.e_star = h->st_estar;
-  c.mu_tmp = h->st_mutmp;
-  c.lam = p.mode == MODE_RECOMPUTE ? h->lam_out : h->st_lam;
-  c.gm = h->st_gm;
-  c.ge = h->st_ge;
-  c.zd = h->st_zd;
-  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
-  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
-  c.skip = 0;
-  p.part = nullptr;
-  win_finalize(p, c, h, (int)part[0], part[1], part[2] == INT64_MAX ? INT64_MIN : -part[2],
-               (int)part[3]);
+  finalize_from_partials(out, p, part, storage_bits);
 }
 
 // deferred finalize of a multi-block pass 1 (bfpdev::window_reduce): the blocks'

@@ -34,6 +34,12 @@ using namespace bfp;
 
 namespace {
 
+// exponent all-reduce transport of the sharded solver (bfp_set_transport): 0 = default
+// (in-process groups reduce with one kernel over the ranks' buffers; NCCL groups use the
+// peer-memory mailboxes when CUDA IPC maps them, else ncclAllReduce), 1 = mailboxes also
+// for in-process groups, 2 = never mailboxes
+int g_transport = 0;
+
 enum StepKind {
   ST_IR_RES = 0, ST_IR_CORR, ST_RELAX0, ST_RELAX, ST_V_RES, ST_RESTRICT, ST_V_CORR,
   ST_FMG_PROLONG, ST_FINAL_RES
@@ -934,6 +940,13 @@ struct Comm {
   // first plane) halo planes of the slabs v[i] of the local ranks
   virtual int halo(bfp_vec_s* const* v, int which, cudaStream_t s) = 0;
   virtual int allreduce_max(int64_t* const* part, int n, cudaStream_t s) = 0;
+  // all-reduce fused into the finalize kernel of a sharded op (peer-memory mailboxes, one
+  // rank per process); false: the caller runs allreduce_max + the plain finalize
+  virtual bool fused_finalize(bfp_vec_s* out, WinParams p, int stage, int64_t* part,
+                              cudaStream_t s) {
+    (void)out, (void)p, (void)stage, (void)part, (void)s;
+    return false;
+  }
   // int64 SUM of the exact-dot limb accumulators (4 words per local rank)
   virtual int allreduce_limbs(int64_t* const* acc, cudaStream_t s) = 0;
   // all-gather equal slabs into the full (replicated) vectors, header included
@@ -950,12 +963,107 @@ __global__ void part_max_kernel(int64_t* const* parts, int P, int n) {
 
 static int64_t plane_bytes(const bfp_vec_s* v) { return (v->span / v->nz) * v->ebytes; }
 
+// ---------------------------------------------------------------------------------------
+// Peer-memory all-reduce of the per-op window partials {mu*, max, -min, err}: the cross-GPU
+// form of the paper's atomic-max ParFor, over NVLink peer stores instead
+// of a collective library call.  Every rank owns a MAILBOX in its own device memory that
+// all its peers have mapped (CUDA IPC across processes, plain pointers inside one process):
+//   post: rank r advances its op counter seq and writes {4 values, seq} into slot
+//         [seq & 1][r] of EVERY rank's mailbox (P2P stores, values first, then the flag
+//         after a system-scope fence);
+//   wait: rank r polls the world slots of parity seq & 1 in its OWN mailbox (local memory:
+//         no NVLink round trip) until their flags equal seq, takes the MAX and writes it
+//         back to its partial buffer.
+// MAX is exact and associative, so every rank computes identical values (bit-identical
+// headers for every rank count).  Two parities suffice: a rank posts seq + 2 only after its
+// wait(seq + 1), which needed every peer's post(seq + 1), issued after that peer's
+// wait(seq).  seq lives on the device, so replayed CUDA graphs keep advancing it.  One
+// process per GPU runs post + wait as ONE kernel (the wait spins while the peers' stores
+// arrive); an in-process group of ranks on one device (tests) runs all posts, then all
+// waits, so no kernel ever waits on a later one of the same stream.
+constexpr int kMaxWorld = 64;
+struct Mailbox {
+  int64_t slot[2][kMaxWorld][8];  // [parity][sender] = {v0, v1, v2, v3, seq, -, -, -}
+  unsigned long long seq;
+};
+enum { MB_POST = 1, MB_WAIT = 2 };
+// one block of 32 threads (thread q talks to peer q); returns with part[] = MAX over ranks
+__device__ __forceinline__ void mailbox_exchange(Mailbox* const* peers, int rank, int world,
+                                                 int64_t* part, int n, int phases) {
+  const int q = threadIdx.x;
+  Mailbox* mine = peers[rank];
+  __shared__ unsigned long long s_seq;
+  if (q == 0) {
+    unsigned long long v = mine->seq;
+    if (phases & MB_POST) mine->seq = ++v;
+    s_seq = v;
+  }
+  __syncthreads();
+  const unsigned long long seq = s_seq;
+  const int par = (int)(seq & 1);
+  if ((phases & MB_POST) && q < world) {
+    int64_t* dst = peers[q]->slot[par][rank];
+    for (int k = 0; k < n; ++k) dst[k] = part[k];
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(dst + 4) = seq;
+  }
+  if (phases & MB_WAIT) {
+    int64_t v[4] = {INT64_MIN, INT64_MIN, INT64_MIN, INT64_MIN};
+    if (q < world) {
+      const int64_t* src = mine->slot[par][q];
+      while (*reinterpret_cast<const volatile unsigned long long*>(src + 4) != seq) __nanosleep(32);
+      __threadfence_system();
+      for (int k = 0; k < n; ++k) v[k] = *reinterpret_cast<const volatile int64_t*>(src + k);
+    }
+    for (int k = 0; k < n; ++k) {
+      const int64_t m = bfpdev::shfl_max64(v[k]);
+      if (q == 0) part[k] = m;
+    }
+  }
+  __syncthreads();
+}
+__global__ void mailbox_kernel(Mailbox* const* peers, int rank, int world, int64_t* part, int n,
+                               int phases) {
+  mailbox_exchange(peers, rank, world, part, n, phases);
+}
+// The exchange fused into the finalize of a sharded op (one process per GPU): a rank whose
+// header says the recompute stage has nothing to do returns before the exchange -- every
+// rank holds the same header, so they all skip it together and the op counters stay aligned.
+__global__ void finalize_mailbox_kernel(Vec out, WinParams p, int64_t* part, int storage_bits,
+                                        Mailbox* const* peers, int rank, int world) {
+  griddep_wait();
+  if (p.mode == MODE_RECOMPUTE && !((const volatile Hdr*)out.hdr)->need_recompute) return;
+  mailbox_exchange(peers, rank, world, part, 4, MB_POST | MB_WAIT);
+  if (threadIdx.x == 0) finalize_from_partials(out, p, part, storage_bits);
+}
+
 // all ranks in this process on one device (bit-exact stand-in for the NCCL transport)
 struct LocalComm : Comm {
   int P;
   int64_t** d_ptrs = nullptr;  // device array of the ranks' partial buffers
+  // mailbox transport (bfp_set_transport(1)): the peer-memory protocol with in-process peers
+  Mailbox* boxes = nullptr;
+  Mailbox** d_boxes = nullptr;
+  std::vector<int64_t*> h_parts;
   explicit LocalComm(int p) : P(p) {}
-  ~LocalComm() override { cudaFree(d_ptrs); }
+  ~LocalComm() override {
+    cudaFree(d_ptrs);
+    cudaFree(boxes);
+    cudaFree(d_boxes);
+  }
+  int init_mailboxes() {
+    if (P > 32) return BFP_ERR_ARG;
+    if (cudaMalloc(&boxes, sizeof(Mailbox) * P) != cudaSuccess ||
+        cudaMalloc(&d_boxes, sizeof(Mailbox*) * P) != cudaSuccess)
+      return BFP_ERR_NOMEM;
+    cudaMemset(boxes, 0, sizeof(Mailbox) * P);
+    std::vector<Mailbox*> hp(P);
+    for (int r = 0; r < P; ++r) hp[r] = boxes + r;
+    return cudaMemcpy(d_boxes, hp.data(), sizeof(Mailbox*) * P, cudaMemcpyHostToDevice) ==
+                   cudaSuccess
+               ? BFP_OK
+               : BFP_ERR_CUDA;
+  }
   int nlocal() const override { return P; }
   int halo(bfp_vec_s* const* v, int which, cudaStream_t s) override {
     for (int r = 0; r < P; ++r) {
@@ -973,14 +1081,20 @@ struct LocalComm : Comm {
     return BFP_OK;
   }
   // the ranks' partial buffers (set once at creation)
-  int init(int64_t* const* part) {
+  int init(int64_t* const* part, bool mailbox) {
+    h_parts.assign(part, part + P);
     if (cudaMalloc(&d_ptrs, sizeof(int64_t*) * P) != cudaSuccess) return BFP_ERR_NOMEM;
-    return cudaMemcpy(d_ptrs, part, sizeof(int64_t*) * P, cudaMemcpyHostToDevice) == cudaSuccess
-               ? BFP_OK
-               : BFP_ERR_CUDA;
+    if (cudaMemcpy(d_ptrs, part, sizeof(int64_t*) * P, cudaMemcpyHostToDevice) != cudaSuccess)
+      return BFP_ERR_CUDA;
+    return mailbox ? init_mailboxes() : BFP_OK;
   }
   int allreduce_max(int64_t* const* part, int n, cudaStream_t s) override {
-    (void)part;
+    if (boxes) {  // every rank posts, then every rank waits (one stream: no kernel spins on a later one)
+      for (int r = 0; r < P; ++r) mailbox_kernel<<<1, 32, 0, s>>>(d_boxes, r, P, part[r], n, MB_POST);
+      for (int r = 0; r < P; ++r) mailbox_kernel<<<1, 32, 0, s>>>(d_boxes, r, P, part[r], n, MB_WAIT);
+      count_launch(2 * P);
+      return cudaGetLastError() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+    }
     part_max_kernel<<<1, 32, 0, s>>>(d_ptrs, P, n);
     count_launch();
     const cudaError_t e = cudaGetLastError();
@@ -1053,8 +1167,77 @@ Nccl& nccl() {
 struct NcclComm : Comm {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // peer-memory mailboxes (mapped with CUDA IPC); nullptr: NCCL all-reduce
+  Mailbox* box = nullptr;
+  Mailbox** d_boxes = nullptr;
+  std::vector<Mailbox*> opened;
   ~NcclComm() override {
+    for (Mailbox* m : opened) cudaIpcCloseMemHandle(m);
+    cudaFree(box);
+    cudaFree(d_boxes);
     if (comm) nccl().CommDestroy(comm);
+  }
+  // Allocate this rank's mailbox, exchange the IPC handles (all-gather of the 64-byte
+  // handles through NCCL) and map every peer's.  Any failure (no peer access between two
+  // GPUs, IPC disabled in the container) leaves the NCCL all-reduce in place.
+  int init_mailboxes() {
+    if (world > 32) return BFP_ERR_ARG;
+    if (cudaMalloc(&box, sizeof(Mailbox)) != cudaSuccess) return BFP_ERR_NOMEM;
+    cudaMemset(box, 0, sizeof(Mailbox));
+    std::vector<Mailbox*> hp(world, nullptr);
+    hp[rank] = box;
+    bool ok = true;
+    if (world > 1) {
+      cudaIpcMemHandle_t mine;
+      ok = cudaIpcGetMemHandle(&mine, box) == cudaSuccess;
+      char* d_h = nullptr;
+      ok = ok && cudaMalloc(&d_h, sizeof(mine) * world) == cudaSuccess;
+      if (ok) {
+        cudaMemcpy(d_h + sizeof(mine) * rank, &mine, sizeof(mine), cudaMemcpyHostToDevice);
+        ok = nccl().AllGather(d_h + sizeof(mine) * rank, d_h, sizeof(mine), ncclUint8, comm,
+                              nullptr) == ncclSuccess &&
+             cudaStreamSynchronize(nullptr) == cudaSuccess;
+      }
+      std::vector<cudaIpcMemHandle_t> all(world);
+      if (ok) cudaMemcpy(all.data(), d_h, sizeof(mine) * world, cudaMemcpyDeviceToHost);
+      cudaFree(d_h);
+      for (int q = 0; q < world && ok; ++q) {
+        if (q == rank) continue;
+        void* ptr = nullptr;
+        ok = cudaIpcOpenMemHandle(&ptr, all[q], cudaIpcMemLazyEnablePeerAccess) == cudaSuccess;
+        if (ok) {
+          hp[q] = static_cast<Mailbox*>(ptr);
+          opened.push_back(hp[q]);
+        }
+      }
+    }
+    ok = ok && cudaMalloc(&d_boxes, sizeof(Mailbox*) * world) == cudaSuccess &&
+         cudaMemcpy(d_boxes, hp.data(), sizeof(Mailbox*) * world, cudaMemcpyHostToDevice) ==
+             cudaSuccess;
+    // every rank must end up on the same transport: MIN over the ranks' outcome
+    int64_t* d_ok = nullptr;
+    int64_t h_ok = ok ? 1 : 0;
+    if (cudaMalloc(&d_ok, sizeof(int64_t)) == cudaSuccess) {
+      cudaMemcpy(d_ok, &h_ok, sizeof(h_ok), cudaMemcpyHostToDevice);
+      if (nccl().AllReduce(d_ok, d_ok, 1, ncclInt64, ncclMin, comm, nullptr) != ncclSuccess ||
+          cudaStreamSynchronize(nullptr) != cudaSuccess)
+        h_ok = 0;
+      else
+        cudaMemcpy(&h_ok, d_ok, sizeof(h_ok), cudaMemcpyDeviceToHost);
+      cudaFree(d_ok);
+    } else {
+      h_ok = 0;
+    }
+    cudaGetLastError();
+    if (!h_ok) {
+      for (Mailbox* m : opened) cudaIpcCloseMemHandle(m);
+      opened.clear();
+      cudaFree(box);
+      cudaFree(d_boxes);
+      box = nullptr;
+      d_boxes = nullptr;
+    }
+    return BFP_OK;
   }
   int nlocal() const override { return 1; }
   int halo(bfp_vec_s* const* v, int which, cudaStream_t s) override {
@@ -1076,7 +1259,22 @@ struct NcclComm : Comm {
     ok = (n.GroupEnd() == ncclSuccess) && ok;
     return ok ? BFP_OK : BFP_ERR_CUDA;
   }
+  bool fused_finalize(bfp_vec_s* out, WinParams p, int stage, int64_t* part,
+                      cudaStream_t s) override {
+    if (!box) return false;
+    if (stage == 1) p.mode = MODE_RECOMPUTE;
+    p.part = nullptr;
+    finalize_mailbox_kernel<<<1, 32, 0, s>>>(view(out), p, part, out->ebytes * 8,
+                                             (Mailbox* const*)d_boxes, rank, world);
+    count_launch();
+    return true;
+  }
   int allreduce_max(int64_t* const* part, int cnt, cudaStream_t s) override {
+    if (box) {  // post + wait in one kernel: the peers' kernels run on their own GPUs
+      mailbox_kernel<<<1, 32, 0, s>>>(d_boxes, rank, world, part[0], cnt, MB_POST | MB_WAIT);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? BFP_OK : BFP_ERR_CUDA;
+    }
     return nccl().AllReduce(part[0], part[0], cnt, ncclInt64, ncclMax, comm, s) == ncclSuccess
                ? BFP_OK
                : BFP_ERR_CUDA;
@@ -1135,6 +1333,9 @@ struct bfp_mg_s {
         const int stages = op0.p.mode == MODE_QCOMP ? 2 : 1;
         for (int st = 0; st < stages && !rc; ++st) {
           for (int r = 0; r < P && !rc; ++r) rc = rs[r]->run(rs[r]->plan[i], s, parts[r], st);
+          if (!rc && P == 1 &&
+              comm->fused_finalize(rs[0]->plan[i].out, rs[0]->plan[i].p, st, parts[0], s))
+            continue;  // exchange + finalize in one kernel
           if (!rc) rc = comm->allreduce_max(parts.data(), 4, s);
           for (int r = 0; r < P && !rc; ++r) rc = rs[r]->finalize(rs[r]->plan[i], parts[r], st, s);
         }
@@ -1234,7 +1435,7 @@ int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const
     LocalComm* c = new LocalComm(world);
     rc = make_group(cfg, world, 0, world, min_planes, c, out);  // owns c
     if (rc) return rc;
-    rc = c->init((*out)->parts.data());
+    rc = c->init((*out)->parts.data(), g_transport == 1);
     if (rc) {
       delete *out;
       *out = nullptr;
@@ -1253,7 +1454,21 @@ int bfp_mg_create_sharded(const bfp_mg_config_t* cfg, int world, int rank, const
     delete c;
     return BFP_ERR_CUDA;
   }
+  if (g_transport != 2) c->init_mailboxes();  // falls back to the NCCL all-reduce on failure
   return make_group(cfg, world, rank, 1, min_planes, c, out);
+}
+
+int bfp_set_transport(int t) {
+  if (t < 0 || t > 2) return BFP_ERR_ARG;
+  g_transport = t;
+  return BFP_OK;
+}
+
+int bfp_mg_transport(bfp_mg_t mg) {
+  if (!mg || !mg->comm) return 0;
+  if (auto* l = dynamic_cast<LocalComm*>(mg->comm)) return l->boxes ? 1 : 0;
+  if (auto* n = dynamic_cast<NcclComm*>(mg->comm)) return n->box ? 1 : 2;
+  return 0;
 }
 
 int bfp_mg_destroy(bfp_mg_t mg) {
@@ -1362,7 +1577,7 @@ int bfp_dist_create(int world, int rank, const void* nccl_id, bfp_dist_t* out) {
     d->parts.assign(world, nullptr);
     for (auto& p : d->parts)
       if (cudaMalloc(&p, 4 * sizeof(int64_t)) != cudaSuccess) rc = BFP_ERR_NOMEM;
-    if (!rc) rc = c->init(d->parts.data());
+    if (!rc) rc = c->init(d->parts.data(), g_transport == 1);
   } else {
     if (rank < 0 || rank >= world || !nccl().load()) {
       delete d;
@@ -1378,6 +1593,7 @@ int bfp_dist_create(int world, int rank, const void* nccl_id, bfp_dist_t* out) {
       rc = BFP_ERR_CUDA;
     }
     d->comm = c;
+    if (!rc && g_transport != 2) c->init_mailboxes();  // NCCL all-reduce when they cannot be mapped
     d->parts.assign(1, nullptr);
     if (!rc && cudaMalloc(&d->parts[0], 4 * sizeof(int64_t)) != cudaSuccess) rc = BFP_ERR_NOMEM;
   }

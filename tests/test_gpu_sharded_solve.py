@@ -60,3 +60,31 @@ def test_sharded_solve_matches_unsharded(B, name):
         assert es == e_ref and np.array_equal(xs, x_ref), (name, graph)
         assert hist == h_ref, (name, graph)
         assert trace == t_ref, (name, graph)
+
+
+@pytest.mark.parametrize("name", ["2d_ir_vcycles", "2d_fmg_nnq", "3d_fmg_w4", "3d_ir_int64"])
+def test_sharded_solve_peer_mailbox_transport(B, name):
+    """The peer-memory all-reduce of the window partials (bfp_solver.cu: Mailbox -- every rank
+    posts {mu*, max, -min, err} + its op counter into every peer's mailbox, then reduces its
+    own mailbox's slots) in place of the reduction kernel / ncclAllReduce: same bits for
+    every rank count, stream-ordered and graph-replayed (the op counter lives on the
+    device, so replays keep both slot parities consistent)."""
+    kw, world, minp = CASES[name]
+    cfg = B.mg_config(**kw)
+    ref = B.Multigrid(cfg)
+    ref.solve()
+    x_ref, q_ref, e_ref, h_ref, t_ref = ref.result()
+    B.set_transport(1)
+    try:
+        for graph in (False, True):
+            mg = B.Multigrid(cfg, world=world, min_planes=minp)
+            assert mg.transport() == "peer-mailbox"
+            for _ in range(3):  # odd number of replays: both parities start a solve
+                mg.solve(use_graph=graph)
+            x, q, e, hist, trace = mg.result()
+            xs, es, ls = _gathered_x(B, mg)
+            assert es == e_ref and np.array_equal(xs, x_ref), (name, graph)
+            assert hist == h_ref and trace == t_ref, (name, graph)
+    finally:
+        B.set_transport(0)
+    assert B.Multigrid(cfg, world=world, min_planes=minp).transport() == "local-kernel"
