@@ -362,7 +362,9 @@ __device__ __forceinline__ bool lean_post(const FusedOp& f, const LeanPre& qs, i
         break;
       }
       case FK_RESTRICT:
-        fast = fast && effx + 2 * q.dim + 2 <= 31;
+        // (1,2,1)^d sums of 32-bit operands: 32-bit when they fit, else 64-bit (config 1 runs
+        // its V-cycle at 28 bits: 28 + 4 > 31)
+        o.swap = effx + 2 * q.dim + 2 > 31;
         st.e_star = q.ea + hx.e;
         break;
       case FK_PROLONG:
@@ -470,6 +472,23 @@ __device__ __forceinline__ void lean_eval4(int kind, const LeanRec& s, const Lea
       const int I0 = o & mc, J = (o >> lc) & mc, K = (o >> (2 * lc)) & mc;
       int acc[4] = {0, 0, 0, 0}, w[4];
       RestrictOp ro;
+      if (c.swap) {  // wide: the same sums in 64 bits
+        int64_t a64[4] = {0, 0, 0, 0};
+        const int planes = dim >= 3 ? 3 : 1, rows = dim >= 2 ? 3 : 1;
+        for (int pz = 0; pz < planes; ++pz)
+          for (int py = 0; py < rows; ++py) {
+            const int32_t* f = s.x + 2 * I0 + (dim >= 2 ? (2 * J + py) * Nf : 0) +
+                               (dim >= 3 ? (2 * K + pz) * Nf * Nf : 0);
+            const int wy = (dim >= 2 && py == 1 ? 2 : 1) * (dim >= 3 && pz == 1 ? 2 : 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              a64[j] += (int64_t)wy * ((int64_t)(f[2 * j] >> c.sx) + 2 * (int64_t)(f[2 * j + 1] >> c.sx) +
+                                       (int64_t)(f[2 * j + 2] >> c.sx));
+          }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) z[j] = pad[j] ? 0 : a64[j];
+        break;
+      }
       if (dim == 1) {
         ro.template line4<false>(s.x + 2 * I0, c.sx, acc);
       } else {
