@@ -434,7 +434,8 @@ def summary(line):
 
 def run_e2e(args, B, Lb, torch, stream, sp, d, l, p):
     """Same metric through the C-ABI with pinned HOST buffers, pipelined across steps:
-    stream A[k%2] uploads x, b (pitched DMA into the padded layout + header scan) and runs
+    stream A[k%2] uploads x, b (one contiguous H2D copy each into a staging buffer + a scatter
+    kernel into the padded layout) and runs
     the residual into buffer k%2; stream B downloads r of step k (gather + D2H engine)
     while A[(k+1)%2] uploads step k+1 (H2D engine).  `pcie_h2d_gbs`: one step's H2D bytes
     copied alone (the bound of this arm)."""

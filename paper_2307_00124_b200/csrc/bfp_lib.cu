@@ -170,33 +170,6 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(Vec v, const S* src, 
   });
 }
 
-// header of a block whose mantissas were copied straight into the padded storage (pads
-// are zero): max/min of the stored values, (q, e), the T_q check
-template <typename M>
-__global__ void __launch_bounds__(kThreads) header_scan_kernel(Vec v, int64_t q, int64_t e) {
-  Red r;
-  r.init();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x, ng = v.n >> 2;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
-    int64_t t[4];
-    V4<M>::load(v, g * 4, 0, t);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) r.val(t[j]);
-  }
-  reduce_and_finalize(r, v.hdr, [&](int, int64_t mx, int64_t mn, int err) {
-    Hdr* h = v.hdr;
-    h->q = q;
-    h->e = e;
-    h->shift = 0;
-    h->max_m = mx;
-    h->min_m = mn;
-    h->flags = 0;
-    h->need_recompute = 0;
-    int fits = q >= 64 || (msb(mx) <= q && msb(mn) <= q);
-    h->err = err | (fits ? 0 : 3 /* BFP_ERR_DOMAIN */);
-  });
-}
-
 // padded storage -> logical staged array, pending shift applied
 template <typename M, typename D>
 __global__ void __launch_bounds__(kThreads) gather_kernel(Vec v, D* dst) {
@@ -751,28 +724,14 @@ int bfp_vec_destroy(bfp_vec_t v) {
 int64_t bfp_vec_size(bfp_vec_t v) { return v ? v->nlog : -1; }
 
 }  // extern "C"
-// int32 host mantissas of a full 2-D / 3-D grid: one pitched DMA copy straight into the
-// padded layout (interior rows only; pads and halos stay zero) and a header scan, no
-// staging buffer and no scatter kernel
-static int upload_pitched_i32(bfp_vec_t v, const int32_t* m, int64_t q, int64_t e,
-                              cudaStream_t s) {
-  const size_t N = (size_t)1 << v->l, n = N - 1;
-  cudaMemcpy3DParms c = {};
-  c.srcPtr = make_cudaPitchedPtr((void*)m, n * 4, n * 4, n);
-  c.dstPtr = make_cudaPitchedPtr(v->data, N * 4, N * 4, N);
-  c.extent = make_cudaExtent(n * 4, n, v->dim == 3 ? n : 1);
-  c.kind = cudaMemcpyHostToDevice;
-  if (cudaMemcpy3DAsync(&c, s) != cudaSuccess) return BFP_ERR_CUDA;
-  header_scan_kernel<int32_t><<<blocks_for(v->span / 4), kThreads, 0, s>>>(view(v), q, e);
-  count_launch();
-  return last_launch();
-}
-
 template <typename S_>
 static int upload_impl(bfp_vec_t v, const S_* m, int64_t q, int64_t e, void* stream) {
   if (!v || q < 1 || (q > 64)) return BFP_ERR_ARG;
-  if (sizeof(S_) == 4 && v->ebytes == 4 && v->dim >= 2 && full_grid(v) && v->nlog)
-    return upload_pitched_i32(v, (const int32_t*)m, q, e, S(stream));
+  // One contiguous H2D copy into a staging buffer at the full PCIe rate, then a scatter
+  // kernel into the padded layout (HBM speed, hidden behind the next copy).  A pitched DMA
+  // (cudaMemcpy3DAsync) straight into the padded layout was measured 3.2x slower end to
+  // end: 2 KB rows run the copy engine at a quarter of its rate
+  // (profiles/r2/r2h_upload_ab.txt).
   int rc = ensure_stage(v, sizeof(S_) * (size_t)std::max<int64_t>(v->nlog, 1));
   if (rc) return rc;
   if (v->nlog)
