@@ -116,11 +116,11 @@ __device__ __forceinline__ void coarse_pass(const Op& sop, const FusedOp& f, int
   const WinCtx c = sh.c;
   const int64_t need = sh.need;
   if (mode == MODE_NNQ)
-    grid_body<MODE_NNQ, M, Op, false>(op, f.out, f.p, c, r, need);
+    grid_body<MODE_NNQ, M, Op, false>(op, f.out, f.p, c, r, need, threadIdx.x, blockDim.x);
   else if (mode == MODE_QCOMP)
-    grid_body<MODE_QCOMP, M, Op, false>(op, f.out, f.p, c, r, need);
+    grid_body<MODE_QCOMP, M, Op, false>(op, f.out, f.p, c, r, need, threadIdx.x, blockDim.x);
   else
-    grid_body<MODE_RECOMPUTE, M, Op, false>(op, f.out, f.p, c, r, need);
+    grid_body<MODE_RECOMPUTE, M, Op, false>(op, f.out, f.p, c, r, need, threadIdx.x, blockDim.x);
 }
 template <typename M>
 __device__ __noinline__ void coarse_body(const FusedOp& f, int mode, const CoarseShared& sh,

@@ -785,4 +785,33 @@ __device__ inline void window_reduce(Red& r, Hdr* h, const WinParams& p, const W
   }
 }
 
+// deferred finalize of a multi-block pass 1 (window_reduce with p.defer; one thread): the
+// blocks' accumulated {OR, max, min, err} and block 0's window context -> win_finalize, and
+// the accumulators are reset for the next op writing this vector; returns need_recompute
+__device__ inline int deferred_finalize(const Vec& out, WinParams p, int storage_bits) {
+  Hdr* h = out.hdr;
+  const volatile Hdr* vh = h;
+  const uint64_t lo = vh->acc_or_lo, hi = vh->acc_or_hi;
+  const int64_t mx = vh->acc_max, mn = vh->acc_min;
+  const int err = vh->acc_err;
+  WinCtx c;
+  c.e_star = vh->st_estar;
+  c.mu_tmp = vh->st_mutmp;
+  c.lam = vh->st_lam;
+  c.gm = vh->st_gm;
+  c.ge = vh->st_ge;
+  c.zd = vh->st_zd;
+  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
+  c.skip = 0;
+  c.rs = 0;
+  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
+  h->acc_or_lo = 0;
+  h->acc_or_hi = 0;
+  h->acc_max = INT64_MIN;
+  h->acc_min = INT64_MAX;
+  h->acc_err = 0;
+  p.defer = 0;
+  return win_finalize(p, c, h, mu_bits(lo, hi), mx, mn, err);
+}
+
 }  // namespace bfpdev

@@ -221,9 +221,9 @@ template <> struct Lim<int64_t> {
 // SP (int32 storage, GemvOp::eval4_sp): the split window of bulk3_loop -- the stored value
 // t = floor(z / 2^rs) and the low word zl in 64-bit arithmetic, mu* from t (+ rs) or zl.
 template <int MODE, typename M, typename Op>
-__device__ __forceinline__ void grid_loop_sp(Op& op, const Vec& out, const WinCtx& c, Red& r) {
+__device__ __forceinline__ void grid_loop_sp(Op& op, const Vec& out, const WinCtx& c, Red& r,
+                                             int64_t g0, int64_t stride) {
   const int64_t ngroups = out.n >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const SplitWin sw = split_win(op.d, c.rs);
   M mx = Lim<M>::lo, mn = Lim<M>::hi;
   uint64_t ot = 0, oz = 0;
@@ -242,7 +242,7 @@ __device__ __forceinline__ void grid_loop_sp(Op& op, const Vec& out, const WinCt
     }
     V4<M>::store(out, g * 4, tt);
   };
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+  for (int64_t g = g0; g < ngroups; g += stride) {
     int64_t t[4], zl[4];
     op.template eval4_sp<true>(g * 4, sw, t, zl);
     epi(g, t, zl);
@@ -262,9 +262,8 @@ __device__ __forceinline__ void grid_loop_sp(Op& op, const Vec& out, const WinCt
 
 template <int MODE, typename M, typename Op, typename A, bool NC = true>
 __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParams& p,
-                                          const WinCtx& c, Red& r) {
+                                          const WinCtx& c, Red& r, int64_t g0, int64_t stride) {
   const int64_t ngroups = out.n >> 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   M mx = Lim<M>::lo, mn = Lim<M>::hi;
   uint64_t olo = 0, ohi = 0;
   const bool store = c.store_tmp;
@@ -286,7 +285,7 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
 #if BFP_GRID_UNROLL > 1
   // two groups per iteration: the second group's loads are issued before the first
   // group's epilogue (more bytes in flight per thread)
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t g = g0;
   for (; g + stride < ngroups; g += 2 * stride) {
     A z0[4], z1[4];
     op.template eval4<M, A, NC>(g * 4, z0);
@@ -300,7 +299,7 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
     epi(g, z);
   }
 #else
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
+  for (int64_t g = g0; g < ngroups; g += stride) {
     A z[4];
     op.template eval4<M, A, NC>(g * 4, z);
     epi(g, z);
@@ -314,23 +313,27 @@ __device__ __forceinline__ void grid_loop(Op& op, const Vec& out, const WinParam
 
 // SPLIT: the grid kernel's own body may take the split window; the pipelines' exact
 // fallbacks do not (it would only add registers to their hot loops)
+// (g0, stride): the groups this thread owns -- by default the launch grid's; a block that runs
+// an op alone passes its own (grid_finish_kernel)
 template <int MODE, typename M, typename Op, bool NC = true, bool SPLIT = false>
 __device__ __forceinline__ void grid_body(Op& op, const Vec& out, const WinParams& p,
-                                          const WinCtx& c, Red& r, int64_t need) {
+                                          const WinCtx& c, Red& r, int64_t need,
+                                          int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                                          int64_t stride = (int64_t)gridDim.x * blockDim.x) {
   if constexpr (SPLIT && HasSplit<Op>::value && sizeof(M) == 4 && NC && MODE != MODE_NNQ) {
     // int32 storage beyond the narrow path (1-D fine levels: A x sits 2l bits above b)
     if (BFP_GRID_SPLIT && !op.narrow && need <= 127 && op.sp32 && c.store_tmp && c.ls == 0 &&
         c.rs < 64 && need - c.rs <= 63) {
-      grid_loop_sp<MODE, M, Op>(op, out, c, r);
+      grid_loop_sp<MODE, M, Op>(op, out, c, r, g0, stride);
       return;
     }
   }
   if (need > 127)
     r.err = ERR_WIDTH;
   else if (need <= 63)
-    grid_loop<MODE, M, Op, int64_t, NC>(op, out, p, c, r);
+    grid_loop<MODE, M, Op, int64_t, NC>(op, out, p, c, r, g0, stride);
   else
-    grid_loop<MODE, M, Op, i128, NC>(op, out, p, c, r);
+    grid_loop<MODE, M, Op, i128, NC>(op, out, p, c, r, g0, stride);
 }
 
 // One windowed pass over a grid (or 4-padded flat) output: qcomp pass 1,
@@ -453,6 +456,33 @@ __global__ void __launch_bounds__(kThreads) grid_win_kernel(Op op, Vec out, WinP
   BFP_STAMP_END();
 }
 
+
+// Finish of a multi-block qcomp pass 1 on a mid-size grid, in ONE small launch: thread 0
+// applies the deferred finalize (the blocks' accumulated {OR, max, min, err} and block 0's
+// window context -> win_finalize); only when a flag fired does this block run the recompute
+// pass over the whole vector itself (rare; a few tens of microseconds on these sizes).  It
+// replaces the one-thread finalize kernel plus the full-grid recompute launch that exits
+// after one header read: one dependent launch boundary less on every such op.
+template <typename M, typename Op>
+__global__ void __launch_bounds__(kThreads) grid_finish_kernel(Op op, Vec out, WinParams p) {
+  griddep_wait();
+  __shared__ int s_rc;
+  if (threadIdx.x == 0) s_rc = deferred_finalize(out, p, 8 * (int)sizeof(M));
+  __syncthreads();
+  if (!s_rc) return;
+  WinParams p2 = p;
+  p2.mode = MODE_RECOMPUTE;
+  p2.defer = 0;
+  int64_t need = 0;
+  WinCtx c2;
+  block_setup<Op, M>(op, out, p2, c2, need);
+  if (c2.skip) return;
+  Red r2;
+  r2.init();
+  grid_body<MODE_RECOMPUTE, M, Op>(op, out, p2, c2, r2, need, threadIdx.x, blockDim.x);
+  const BlockRed b = block_reduce(r2);
+  if (threadIdx.x == 0) win_finalize(p2, c2, out.hdr, mu_bits(b.lo, b.hi), b.mx, b.mn, b.err);
+}
 
 // ---------------------------------------------------------------------------
 // 2.5-D register march for the 2-D / 3-D stencil ops on int32 storage (the
@@ -2081,6 +2111,11 @@ static inline int check_window(const WinParams& p, const bfp_vec_s* out) {
 #define BFP_SINGLE_BLOCK_GROUPS 512
 #endif
 constexpr int64_t kSingleBlockGroups = BFP_SINGLE_BLOCK_GROUPS;
+// up to this many 4-groups, a multi-block qcomp pass 1 is finished by grid_finish_kernel
+#ifndef BFP_FINISH_GROUPS
+#define BFP_FINISH_GROUPS (1 << 13)  // (a one-block recompute of 32k points: ~20 us, rare)
+#endif
+constexpr int64_t kFinishGroups = BFP_FINISH_GROUPS;
 
 // launch a grid-windowed op: nnqcomp (one pass) or qcomp (pass 1 + recompute)
 template <typename Op>
@@ -2120,6 +2155,16 @@ static inline int launch_grid(const Op& op, bfp_vec_s* out, const WinParams& p0,
     cudaEventRecord(ev.second, s);
   } else {
     go(p);
+  }
+  // mid-size grids: finalize + (rare) recompute by one block in one launch
+  if (p.defer && p.mode == MODE_QCOMP && !g_skip_recompute && !p.part && groups <= kFinishGroups) {
+    p.defer = 0;
+    if (out->ebytes == 4)
+      launch_pdl(grid_finish_kernel<int32_t, Op>, 1, kThreads, 0, s, op, o, p);
+    else
+      launch_pdl(grid_finish_kernel<int64_t, Op>, 1, kThreads, 0, s, op, o, p);
+    count_launch();
+    return last_launch();
   }
   if (p.defer) launch_deferred_finalize(o, p, out->ebytes * 8, s);
   p.defer = 0;

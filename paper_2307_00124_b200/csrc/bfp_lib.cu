@@ -58,29 +58,7 @@ __global__ void deferred_finalize_kernel(Vec out, WinParams p, int storage_bits)
   griddep_wait();
   griddep_launch_dependents();  // dependents still wait for this grid's completion
   if (threadIdx.x != 0) return;
-  Hdr* h = out.hdr;
-  const volatile Hdr* vh = h;
-  const uint64_t lo = vh->acc_or_lo, hi = vh->acc_or_hi;
-  const int64_t mx = vh->acc_max, mn = vh->acc_min;
-  const int err = vh->acc_err;
-  WinCtx c;
-  c.e_star = vh->st_estar;
-  c.mu_tmp = vh->st_mutmp;
-  c.lam = vh->st_lam;
-  c.gm = vh->st_gm;
-  c.ge = vh->st_ge;
-  c.zd = vh->st_zd;
-  c.store_tmp = p.mode == MODE_QCOMP ? (p.w_tmp <= storage_bits && !p.force) : 1;
-  c.skip = 0;
-  c.rs = 0;
-  c.ls = c.lam < 0 ? (int32_t)(-c.lam > 64 ? 64 : -c.lam) : 0;
-  h->acc_or_lo = 0;
-  h->acc_or_hi = 0;
-  h->acc_max = INT64_MIN;
-  h->acc_min = INT64_MAX;
-  h->acc_err = 0;
-  p.defer = 0;
-  win_finalize(p, c, h, mu_bits(lo, hi), mx, mn, err);
+  deferred_finalize(out, p, storage_bits);
 }
 
 namespace bfp {
