@@ -630,14 +630,40 @@ struct JacobiOp {
 };
 
 // z = c*r (pointwise over the storage span; pads stay zero)
+// Pointwise ops with a 32-bit fast loop (grid_loop_pt, bfp_kernels.cuh): int32 storage,
+// coefficients in int32, rows in 64 bits -- point4() gives 4 exact rows from narrow loads.
+template <typename T, typename = void> struct HasPoint {
+  static constexpr bool value = false;
+};
+template <typename T> struct HasPoint<T, decltype((void)T::point_tag)> {
+  static constexpr bool value = true;
+};
+
 struct ScalOp {
   Vec r;
   Scal c;
   int64_t sr;
+  bool p32;  // c.m in int32, pending shift < 32: the 32-bit pointwise loop applies
+  static constexpr int point_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     e_star = c.e + r.hdr->e;
     sr = r.hdr->shift;
     need = msb((int64_t)c.m) + eff_bits(r.hdr) + 1;
+    p32 = fits32(c.m) && sr < 32;
+  }
+  static constexpr int kPointUnroll = 4;
+  struct Raw {
+    int4 v;
+  };
+  __device__ __forceinline__ Raw point_load(int64_t o) const {
+    return Raw{__ldg(reinterpret_cast<const int4*>((const int32_t*)r.data + o))};
+  }
+  __device__ __forceinline__ void point4(const Raw& w, int64_t z[4]) const {
+    const int s = (int)sr, m = (int)c.m;
+    z[0] = mul_wide(m, w.v.x >> s);
+    z[1] = mul_wide(m, w.v.y >> s);
+    z[2] = mul_wide(m, w.v.z >> s);
+    z[3] = mul_wide(m, w.v.w >> s);
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
@@ -653,7 +679,10 @@ struct AxpbyOp {
   Vec x, y;
   Scal al, be;
   int64_t sx, sy, d, zd;
+  bool p32;    // the 32-bit pointwise loop applies: z = x Pa + y Pb with int32 Pa = alpha 2^d+,
+  int da, db;  // Pb = beta 2^d- (here named da, db)
   static constexpr int zd_tag = 0;
+  static constexpr int point_tag = 0;
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const HSnap hx = hsnap(x.hdr), hy = hsnap(y.hdr);
     int64_t dd, es, z = 0;
@@ -665,6 +694,27 @@ struct AxpbyOp {
     zd = z;
     sx = hx.shift;
     sy = hy.shift;
+    // the alignment folded into the coefficients: z = x Pa + y Pb, two IMAD.WIDE
+    const int64_t sa = dd > 0 ? dd : 0, sb = dd < 0 ? -dd : 0;
+    p32 = sx < 32 && sy < 32 && sa <= 30 && sb <= 30 && fits32(al.m) && fits32(be.m) &&
+          fits32(al.m << sa) && fits32(be.m << sb);
+    da = p32 ? (int)(al.m << sa) : 0;  // Pa
+    db = p32 ? (int)(be.m << sb) : 0;  // Pb
+  }
+  static constexpr int kPointUnroll = 2;
+  struct Raw {
+    int4 a, b;
+  };
+  __device__ __forceinline__ Raw point_load(int64_t o) const {
+    return Raw{__ldg(reinterpret_cast<const int4*>((const int32_t*)x.data + o)),
+               __ldg(reinterpret_cast<const int4*>((const int32_t*)y.data + o))};
+  }
+  __device__ __forceinline__ void point4(const Raw& w, int64_t z[4]) const {
+    const int s0 = (int)sx, s1 = (int)sy;
+    const int xa[4] = {w.a.x >> s0, w.a.y >> s0, w.a.z >> s0, w.a.w >> s0};
+    const int yb[4] = {w.b.x >> s1, w.b.y >> s1, w.b.z >> s1, w.b.w >> s1};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = mad_wide(xa[j], da, mul_wide(yb[j], db));
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {
