@@ -978,8 +978,9 @@ static int64_t plane_bytes(const bfp_vec_s* v) { return (v->span / v->nz) * v->e
 // headers for every rank count).  Two parities suffice: a rank posts seq + 2 only after its
 // wait(seq + 1), which needed every peer's post(seq + 1), issued after that peer's
 // wait(seq).  seq lives on the device, so replayed CUDA graphs keep advancing it.  One
-// process per GPU runs post + wait as ONE kernel (the wait spins while the peers' stores
-// arrive); an in-process group of ranks on one device (tests) runs all posts, then all
+// process per GPU runs post + wait as ONE kernel (the wait polls while the peers' stores
+// arrive, for at most ~2 s: a peer that never posts becomes BFP_ERR_CUDA in the op's sticky
+// error word instead of a hang); an in-process group of ranks on one device (tests) runs all posts, then all
 // waits, so no kernel ever waits on a later one of the same stream.
 constexpr int kMaxWorld = 64;
 struct Mailbox {
@@ -1011,9 +1012,20 @@ __device__ __forceinline__ void mailbox_exchange(Mailbox* const* peers, int rank
     int64_t v[4] = {INT64_MIN, INT64_MIN, INT64_MIN, INT64_MIN};
     if (q < world) {
       const int64_t* src = mine->slot[par][q];
-      while (*reinterpret_cast<const volatile unsigned long long*>(src + 4) != seq) __nanosleep(32);
+      // bounded wait (~2 s of SM clocks): a peer that never posts -- a mapping or launch
+      // failure on another rank -- must surface as an error of this op, not hang the GPU
+      const long long t0 = clock64();
+      bool late = false;
+      while (*reinterpret_cast<const volatile unsigned long long*>(src + 4) != seq) {
+        __nanosleep(32);
+        if (clock64() - t0 > (1ll << 32)) {
+          late = true;
+          break;
+        }
+      }
       __threadfence_system();
       for (int k = 0; k < n; ++k) v[k] = *reinterpret_cast<const volatile int64_t*>(src + k);
+      if (late && n > 3) v[3] = 4;  // BFP_ERR_CUDA in the partial's error word (MAX keeps it)
     }
     for (int k = 0; k < n; ++k) {
       const int64_t m = bfpdev::shfl_max64(v[k]);
