@@ -1073,7 +1073,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
   const uint32_t tx_bytes = (uint32_t)(kB3XT + kB3YT) * sizeof(T);
   SplitWin sw{};
   uint64_t ot = 0, oz = 0;  // SP: OR of t ^ sign, zl ^ sign
-  if constexpr (SP) sw = split_win(op.d, c.rs);
+  if constexpr (SP) sw = op.b3_split_setup(c.rs);
   uint32_t parity = 0, eparity = 0;
   for (int item = blockIdx.x; item < tx * ty * chunks; item += gridDim.x) {
     const int tile = item % (tx * ty), ch = item / (tx * ty);
@@ -1151,7 +1151,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         if constexpr (sizeof(T) == 8 && SP) {  // split window (SplitWin)
           const int64_t nb = left + right + u[q] + dn[q] + zp[q] + zn[q];
           int64_t tq, zl;
-          op.template point_sp<SWAP>(6 * C[q] - nb, Yv[q], sw.m0, sw.m1, sw.s1, sw.s2, tq, zl);
+          op.template point_sp<SWAP>(6 * C[q] - nb, C[q], Yv[q], sw, tq, zl);
           if ((q == 3 && xpad) || rowpad) tq = zl = 0;
           if (MODE == MODE_QCOMP) {
             const uint64_t sg = (uint64_t)(tq >> 63);
@@ -1308,8 +1308,8 @@ __global__ void __launch_bounds__(kB3T, b3_minb<T, Op>())
           bulk3_loop<MODE, false, false, T, int64_t>(op, out, p, c, r, R, smem, &tm.x, &tm.y);
       } else if (MODE != MODE_NNQ && op.fwi && c.store_tmp && c.ls == 0 && c.rs < 64) {
         bool split = false;
-        if constexpr (HasSplit<Op>::value) {
-          split = BFP_B3_SPLIT && need - c.rs <= 63;
+        if constexpr (HasB3Split<Op>::value) {
+          split = BFP_B3_SPLIT && op.b3_split_ok(need, c.rs);
           if (split)
             b3_dispatch<MODE, T, int64_t, false, true>(sh, op.fw_swap(), op, out, p, c, r, R, smem, tm);
         }

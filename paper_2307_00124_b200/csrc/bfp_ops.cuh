@@ -338,6 +338,15 @@ template <typename T> struct HasSplit<T, decltype((void)T::split_tag)> {
 };
 
 
+// ops with a split window in the 3-D pipeline (bulk3_loop SP): b3_split_ok / b3_split_setup /
+// point_sp
+template <typename T, typename = void> struct HasB3Split {
+  static constexpr bool value = false;
+};
+template <typename T> struct HasB3Split<T, decltype((void)T::b3split_tag)> {
+  static constexpr bool value = true;
+};
+
 __device__ __forceinline__ SplitWin split_win(int64_t d, int rs) {
   const int ad = (int)(d < 0 ? -d : d);
   SplitWin sw;
@@ -448,13 +457,17 @@ struct GemvOp {
   // (SplitWin, bfp_kernels.cuh); z = X 2^|d| + Y with (X, Y) = (alpha g, beta y) or,
   // SW (d < 0), (beta y, alpha g)
   static constexpr int split_tag = 0;
+  static constexpr int b3split_tag = 0;
+  __device__ __forceinline__ bool b3_split_ok(int64_t need, int rs) const { return need - rs <= 63; }
+  __device__ __forceinline__ SplitWin b3_split_setup(int rs) const { return split_win(d, rs); }
   template <bool SW>
-  __device__ __forceinline__ void point_sp(int64_t g, int64_t yv, uint64_t m0, uint64_t m1,
-                                           int s1, int s2, int64_t& t, int64_t& zl) const {
+  __device__ __forceinline__ void point_sp(int64_t g, int64_t cx, int64_t yv, const SplitWin& w,
+                                           int64_t& t, int64_t& zl) const {
+    (void)cx;
     const int64_t a = al.m * g, b = be.m * yv;  // exact: w64 bounds |a|, |b| < 2^62
     const int64_t X = SW ? b : a, Y = SW ? a : b;
-    zl = (int64_t)((uint64_t)X * m0 + (uint64_t)Y);
-    t = (int64_t)((uint64_t)X * m1 + (uint64_t)(Y >> s1)) >> s2;
+    zl = (int64_t)((uint64_t)X * w.m0 + (uint64_t)Y);
+    t = (int64_t)((uint64_t)X * w.m1 + (uint64_t)(Y >> w.s1)) >> w.s2;
   }
   // split window over int32 storage (grid_loop SP): t = floor(z / 2^rs) and zl = z mod 2^64
   // from 32-bit operand products X = PX * (g | y), Y = QY * (y | g), z = X 2^ad + Y
@@ -558,6 +571,9 @@ struct JacobiOp {
     w64 = w6;
     fwi = w6 && nd <= 127 && dd1 > -64 && dd1 < 64 && dd2 >= 0 && dd2 < 64 && c.m >= 0 &&
           c.m <= 0xffffffffll && bx <= 62;
+    // split window (point_sp): three 32-bit limbs
+    sp96 = fwi && c.m <= 0x7fffffffll && dd1 >= -31 && dd1 <= 31 && nd <= 96;
+    a1 = (int)(dd1 < 0 ? -dd1 : dd1);
     neg1 = dd1 < 0;
     P1 = nar ? (neg1 ? (1 << (int)(-dd1)) : -(1 << (int)dd1)) : 0;
     s2 = nar ? (int)dd2 : 0;
@@ -592,6 +608,71 @@ struct JacobiOp {
   __device__ __forceinline__ W128 point_fw(int64_t g, int64_t cx, int64_t bv) const {
     const W128 r = SW ? w_add(w_shl(bv, (int)-d1), -g) : w_add(w_shl(-g, (int)d1), bv);
     return w_add(w_shl(cx, (int)d2), w_mul_u32(r, (uint32_t)c.m));
+  }
+  // Split window of the int64 Jacobi row (3-D pipeline): z = x 2^d2 + c b 2^a - c g 2^a'
+  // (one of a, a' is |d1| <= 31, the other 0) in three 32-bit limbs.  c v for a 64-bit v is
+  // two IMAD.WIDEs (c v_lo, then c v_hi plus the carry word), the |d1| alignment three funnel
+  // shifts, the sums two carry chains; the stored value is the 64-bit field of z at the
+  // window shift rs < 64 and the low word z mod 2^64 serves mu* exactly as in the
+  // residual's split window (bulk3_loop).  Exact when z fits 96 bits (need <= 96 bounds
+  // every partial sum: the r term's bound is part of need) and 0 <= c < 2^31.
+  bool sp96;
+  int a1;
+  static constexpr int b3split_tag = 0;
+  __device__ __forceinline__ bool b3_split_ok(int64_t need, int rs) const {
+    return sp96 && need - rs <= 63;
+  }
+  __device__ __forceinline__ SplitWin b3_split_setup(int rs) const {
+    SplitWin w{};
+    w.a0 = d2 >= 32;                               // x 2^d2 starts at limb 1
+    w.s1 = (int)(d2 >= 32 ? d2 - 32 : 32 - d2);
+    w.a1 = rs >= 32;                               // the stored field starts at limb 1
+    w.s2 = rs & 31;
+    w.m0 = (uint64_t)c.m;
+    return w;
+  }
+  static __device__ __forceinline__ void mul96(uint32_t cm, int64_t v, uint32_t& p0, uint32_t& p1,
+                                               uint32_t& p2) {
+    uint64_t lo;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(lo) : "r"(cm), "r"((uint32_t)v));
+    const int64_t hi = mad_wide((int)cm, (int)(v >> 32), (int64_t)(lo >> 32));
+    p0 = (uint32_t)lo, p1 = (uint32_t)hi, p2 = (uint32_t)((uint64_t)hi >> 32);
+  }
+  template <bool SW>
+  __device__ __forceinline__ void point_sp(int64_t g, int64_t cx, int64_t bv, const SplitWin& w,
+                                           int64_t& t, int64_t& zl) const {
+    const uint32_t cm = (uint32_t)w.m0;
+    uint32_t q0, q1, q2, b0, b1, b2;
+    mul96(cm, g, q0, q1, q2);
+    mul96(cm, bv, b0, b1, b2);
+    if (SW) {  // d1 < 0: the b term carries 2^|d1|
+      b2 = __funnelshift_l(b1, b2, a1), b1 = __funnelshift_l(b0, b1, a1), b0 <<= a1;
+    } else {
+      q2 = __funnelshift_l(q1, q2, a1), q1 = __funnelshift_l(q0, q1, a1), q0 <<= a1;
+    }
+    uint32_t x0, x1, x2;
+    if (w.a0) {
+      const uint64_t xs = (uint64_t)cx << w.s1;
+      x0 = 0, x1 = (uint32_t)xs, x2 = (uint32_t)(xs >> 32);
+    } else {
+      const int64_t xs = cx >> w.s1;  // s1 = 32 - d2 in [1, 32]
+      x0 = (uint32_t)cx << ((32 - w.s1) & 31), x1 = (uint32_t)xs, x2 = (uint32_t)((uint64_t)xs >> 32);
+    }
+    uint32_t z0, z1, z2;
+    asm("sub.cc.u32 %0, %3, %6;\n\tsubc.cc.u32 %1, %4, %7;\n\tsubc.u32 %2, %5, %8;"
+        : "=r"(z0), "=r"(z1), "=r"(z2)
+        : "r"(b0), "r"(b1), "r"(b2), "r"(q0), "r"(q1), "r"(q2));
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+        : "+r"(z0), "+r"(z1), "+r"(z2)
+        : "r"(x0), "r"(x1), "r"(x2));
+    zl = (int64_t)(((uint64_t)z1 << 32) | z0);
+    uint32_t tl, th;
+    if (w.a1) {
+      tl = __funnelshift_r(z1, z2, w.s2), th = (uint32_t)((int)z2 >> w.s2);
+    } else {
+      tl = __funnelshift_r(z0, z1, w.s2), th = __funnelshift_r(z1, z2, w.s2);
+    }
+    t = (int64_t)(((uint64_t)th << 32) | tl);
   }
   template <typename M, typename A, bool NC = true>
   __device__ __forceinline__ void eval4(int64_t o, A z[4]) {

@@ -422,6 +422,36 @@ def test_int64_residual_windows_vs_oracle(B, p):
             assert (res.overflow, res.underflow) == (bool(fl[0]), bool(fl[1])), (off, ge)
 
 
+@pytest.mark.parametrize("p", [32, 40, 48, 52])
+def test_int64_jacobi_windows_vs_oracle(B, p):
+    """3-D int64 Jacobi updates through the bulk pipeline over the regimes of the
+    three-limb split window (JacobiOp::point_sp, bfp_ops.cuh): b ahead of and behind the
+    stencil term (d1 of both signs, beyond +-31 for the two-word fallback), x aligned above
+    and below limb 1 (d2 around 32), window shift rs around 32, coefficients of 8..30 bits,
+    overflow and underflow flags."""
+    d, l = 3, 7
+    ox, obb = ob.gen_uniform(d, l, p, 5, 1), ob.gen_sine(d, l, p)
+    gx = ggrid(B, d, l, ox.m, ox.q, ox.e, mb=8)
+    done = 0
+    for off in (-45, -20, -6, 0, 7, 25, 40):
+        bo = ob.OBlock(obb.m, obb.q, obb.e + off)
+        gb = ggrid(B, d, l, bo.m, bo.q, bo.e, mb=8)
+        for qc, ge in ((8, 4), (16, -30), (16, 0), (16, 12), (24, 5), (30, 20), (16, 60)):
+            c = B.jacobi_coeff(d, l, qc)
+            g = B.Scalar(1 << 14, 16, ge)
+            try:
+                j = B.jacobi(gx, gb, c, p, p + 3, g)
+            except B.WidthError:  # exact row beyond 127 bits: outside the product's range
+                assert p >= 40 and abs(off) >= 25, (off, qc, ge)
+                continue
+            done += 1
+            wj, fl = ob.jacobi(d, l, ox, bo, (c.m, c.q, c.e), "q", p, p + 3, g.m, g.e)
+            m, q, e = j.z.download()
+            assert e == wj.e and np.array_equal(m, wj.m), (off, qc, ge)
+            assert (j.overflow, j.underflow) == (bool(fl[0]), bool(fl[1])), (off, qc, ge)
+    assert done >= 30
+
+
 @pytest.mark.parametrize("l", [18, 20, 24])
 def test_1d_wide_alignment_residual_vs_oracle(B, l):
     """1-D residuals at config-1 scale and beyond: h^-2 = 2^{2l} puts A x ~2l bits above
