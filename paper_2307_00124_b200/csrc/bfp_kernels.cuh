@@ -810,13 +810,16 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       __syncthreads();
       continue;
     }
-    const bool xpad = c0 + 4 * t + 3 == N - 1;
+    const bool xpad = strip == strips - 1 && t == kBulkT - 1;  // c0 + 4 t + 3 == N - 1
     const int lane = t & 31;
+    // the step of the grid's last (pad) row within this chunk, or -1
+    const int64_t ps = N - 1 - Z0 - j0;
+    const int pad_s = ps >= 0 && ps < rows ? (int)ps : -1;
+    int32_t* orow = O + (int64_t)j0 * N + c0 + 4 * t;
     // running ring indices (no 64-bit modulo in the step loop)
     int sp = (int)((j0 - 1 + kBulkXS) % kBulkXS), sc = (int)(j0 % kBulkXS);
     int sn = (int)((j0 + 1) % kBulkXS), sy_ = (int)(j0 % kBulkYS);
-    for (int s = 0; s < rows; ++s) {
-      const int64_t j = j0 + s;
+    for (int s = 0; s < rows; ++s, orow += N) {
       mbar_wait(&bar[sy_], (parity >> sy_) & 1u);
       parity ^= 1u << sy_;
       const int32_t* xc = xsl + sc * kBulkXW + 4 + 4 * t;
@@ -834,14 +837,16 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
       const int Dn[4] = {d.x >> sx, d.y >> sx, d.z >> sx, d.w >> sx};
       const int Yv[4] = {y4.x >> sy, y4.y >> sy, y4.z >> sy, y4.w >> sy};
       const int nb[4] = {(lf >> sx) + C[1], C[0] + C[2], C[1] + C[3], C[2] + (rt >> sx)};
-      int32_t tt[4];
-      const bool rowpad = j + Z0 == N - 1;
+      int32_t tt[4] = {0, 0, 0, 0};
+      if (s == pad_s) {  // the pad row: exact zeros (uniform branch, one row of the grid)
+        mx = mx < 0 ? 0 : mx;
+        mn = mn > 0 ? 0 : mn;
+      } else {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int g = 4 * C[k] - (nb[k] + U[k] + Dn[k]);
         int64_t z = op.template point_t<SWAP>(g, C[k], Yv[k]);
         if (k == 3 && xpad) z = 0;
-        if (rowpad) z = 0;
         if constexpr (FW) {
           if (MODE == MODE_QCOMP) or_mag<int64_t>(z, olo, ohi);
           tt[k] = (int32_t)__funnelshift_r((uint32_t)z, (uint32_t)((uint64_t)z >> 32), c.rs);
@@ -854,7 +859,8 @@ __device__ __forceinline__ void bulk_loop(const Op& op, const Vec& out, const Wi
         mx = tt[k] > mx ? tt[k] : mx;
         mn = tt[k] < mn ? tt[k] : mn;
       }
-      *reinterpret_cast<int4*>(O + j * N + c0 + 4 * t) = make_int4(tt[0], tt[1], tt[2], tt[3]);
+      }
+      *reinterpret_cast<int4*>(orow) = make_int4(tt[0], tt[1], tt[2], tt[3]);
       // ring slots freed by this step: x row j-1 (slot sp) and y row j / its barrier (slot sy_)
       const int free_x = sp, free_y = sy_;
       sp = sc;

@@ -536,7 +536,7 @@ struct JacobiOp {
   bool w64;   // 64-bit stencil and r-term products (int64 storage)
   bool fwi;   // ... and every alignment shift < 64: two-word rows (W128)
   bool neg1;  // d1 < 0: the b term carries the power of two
-  int P1, s2;
+  int Pg, Pb, s2;
   int64_t zd;
   static constexpr int zd_tag = 0;
   static constexpr int b3_depth = 4, b3_minb = 3;  // bulk3 tuning (int32; B3Tune)
@@ -575,16 +575,18 @@ struct JacobiOp {
     sp96 = fwi && c.m <= 0x7fffffffll && dd1 >= -31 && dd1 <= 31 && nd <= 96;
     a1 = (int)(dd1 < 0 ? -dd1 : dd1);
     neg1 = dd1 < 0;
-    P1 = nar ? (neg1 ? (1 << (int)(-dd1)) : -(1 << (int)dd1)) : 0;
+    Pg = nar ? (neg1 ? -1 : -(1 << (int)dd1)) : 0;
+    Pb = nar ? (neg1 ? (1 << (int)(-dd1)) : 1) : 0;
     s2 = nar ? (int)dd2 : 0;
   }
   __host__ __device__ __forceinline__ const Vec& sv() const { return x; }
   __host__ __device__ __forceinline__ const Vec& yv2() const { return b; }
   __device__ __forceinline__ int shs() const { return (int)sx; }
   __device__ __forceinline__ int shy() const { return (int)sb; }
+  // r = b 2^max(-d1,0) - g 2^max(d1,0) as two IMAD.WIDEs (no per-point selects on the sign
+  // of d1): (Pg, Pb) = (-2^d1, 1) or (-1, 2^-d1)
   __device__ __forceinline__ int64_t rterm(int g, int bv) const {
-    const int X = neg1 ? bv : g, Y = neg1 ? -g : bv;
-    return (int64_t)X * (int64_t)P1 + (int64_t)Y;
+    return mad_wide(g, Pg, mul_wide(bv, Pb));
   }
   __device__ __forceinline__ int64_t point(int g, int cx, int bv) const {
     const int64_t r = rterm(g, bv);
