@@ -1111,8 +1111,16 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
     }
     // column of the lane's point 3 (the only one that can be the x pad, column N-1)
     const int col3 = sizeof(T) == 4 ? 4 * lane + 3 : 64 + 2 * lane + 1;
-    const bool xpad = x0 + col3 == N - 1;
-    const bool ypad = y0 + wy == N - 1;
+    // 32-bit forms of the pad predicates (column 127 of the last tile column, row N-1 of
+    // the last tile row, the step of plane N-1): cheaper to rematerialise in the step loop.
+    // Measured per instantiation (ops_now.py): int64 residual 0.93 -> 0.94, int32 Jacobi
+    // 0.88 -> 0.89, but the int32 residual (64 registers) 0.93 -> 0.87, which keeps the
+    // 64-bit compares.
+    constexpr bool kPad32 = !(sizeof(T) == 4 && HasSplit<Op>::value);
+    const bool xpad = kPad32 ? tile % tx == tx - 1 && lane == 31 : x0 + col3 == N - 1;
+    const bool ypad = kPad32 ? tile / tx == ty - 1 && wy == kB3H - 1 : y0 + wy == N - 1;
+    const int64_t ps = N - 1 - Z0 - k0;
+    const int pad_s = ps >= 0 && ps < planes ? (int)ps : -1;
     int sp = (int)((k0 - 1 + kB3XS) % kB3XS), sc = (int)(k0 % kB3XS);
     int sn = (int)((k0 + 1) % kB3XS), sy_ = (int)(k0 % kB3YS);
     for (int s = 0; s < planes; ++s) {
@@ -1150,7 +1158,7 @@ __device__ __forceinline__ void bulk3_loop(const Op& op, const Vec& out, const W
         Lf[3] = C[2], Rt[3] = lane == 31 ? rt0 : b;
       }
       T tt[4];
-      const bool rowpad = ypad || k + Z0 == N - 1;
+      const bool rowpad = ypad || (kPad32 ? s == pad_s : k + Z0 == N - 1);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const V left = Lf[q], right = Rt[q];
