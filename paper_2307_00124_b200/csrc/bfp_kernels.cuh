@@ -1420,7 +1420,13 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
   const uint32_t cbytes = (uint32_t)(kP3CW * kP3CH * sizeof(T)), ybytes = (uint32_t)(kP3YT * sizeof(T));
   uint32_t ring = 0;  // ring position of the item's step 0 (both roles advance it alike)
   // local coarse rows of fine row y0 + wy and the coarse column of this thread's 4 points
-  const int r0 = ((wy - 1) >> 1) + 1, r1 = (wy >> 1) + 1, col = 2 * lane + 4;
+  // (int32: fine columns 4 lane .. 4 lane + 3 from coarse 2 lane - 1 .. 2 lane + 1; int64:
+  // split pairs, fine columns 2 lane, 2 lane + 1 | 64 + 2 lane, 64 + 2 lane + 1 from coarse
+  // lane - 1, lane | 32 + lane - 1, 32 + lane, so that every 16-byte store and shared load
+  // of the warp is contiguous)
+  const int r0 = ((wy - 1) >> 1) + 1, r1 = (wy >> 1) + 1;
+  const int col = (sizeof(T) == 4 ? 2 * lane : lane) + 4;
+  const int xoff = sizeof(T) == 4 ? 4 * lane : 2 * lane;  // fine column of point 0
   // int32 fast window: z = g Pg + y Py as two IMAD.WIDE (no operand selects).  No pad
   // masking there: a fine pad index has both coarse taps on the coarse pad (index N/2 - 1,
   // stored zero) and y's own pad is zero, so its row is 0 Pg + 0 Py.
@@ -1455,9 +1461,9 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
       ring += (uint32_t)pairs + 1u;
       continue;
     }
-    const bool xpad = x0 + 4 * lane + 3 == N - 1;
+    const bool xpad = x0 + (sizeof(T) == 4 ? 4 * lane + 3 : 64 + 2 * lane + 1) == N - 1;
     const bool ypad = y0 + wy == N - 1;
-    T* dstp = O + 2 * K0 * N2 + (y0 + wy) * N + x0 + 4 * lane;
+    T* dstp = O + 2 * K0 * N2 + (y0 + wy) * N + x0 + xoff;
     V Sp[4] = {0, 0, 0, 0};  // S_{K-1}
     for (int j = 0; j <= pairs; ++j) {
       const uint32_t g = ring + (uint32_t)j, slot = g % kP3S;
@@ -1469,11 +1475,19 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
           const T* row = cb + (rr ? r1 : r0) * kP3CW + col;
-          const V a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
-          acc[0] += a + b;
-          acc[1] += 2 * b;
-          acc[2] += b + e;
-          acc[3] += 2 * e;
+          if constexpr (sizeof(T) == 4) {
+            const V a = row[-1] >> sc, b = row[0] >> sc, e = row[1] >> sc;
+            acc[0] += a + b;
+            acc[1] += 2 * b;
+            acc[2] += b + e;
+            acc[3] += 2 * e;
+          } else {
+            const V a = row[-1] >> sc, b = row[0] >> sc, a2 = row[31] >> sc, b2 = row[32] >> sc;
+            acc[0] += a + b;
+            acc[1] += 2 * b;
+            acc[2] += a2 + b2;
+            acc[3] += 2 * b2;
+          }
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) Sc[q] = acc[q];
@@ -1516,13 +1530,13 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
           const int64_t k = 2 * (K0 + s) + h;  // local fine plane
           V yv[4] = {0, 0, 0, 0};
           if (Op::kCorr) {
-            const T* yp = ysl + (slot * 2 + h) * kP3YT + wy * kP3W + 4 * lane;
+            const T* yp = ysl + (slot * 2 + h) * kP3YT + wy * kP3W + xoff;
             if constexpr (sizeof(T) == 4) {
               const int4 y4 = *reinterpret_cast<const int4*>(yp);
               yv[0] = y4.x >> sy, yv[1] = y4.y >> sy, yv[2] = y4.z >> sy, yv[3] = y4.w >> sy;
             } else {
-              const longlong2 a = reinterpret_cast<const longlong2*>(yp)[0];
-              const longlong2 b = reinterpret_cast<const longlong2*>(yp)[1];
+              const longlong2 a = *reinterpret_cast<const longlong2*>(yp);
+              const longlong2 b = *reinterpret_cast<const longlong2*>(yp + 64);
               yv[0] = a.x >> sy, yv[1] = a.y >> sy, yv[2] = b.x >> sy, yv[3] = b.y >> sy;
             }
           }
@@ -1552,12 +1566,12 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
             mx = tt[q] > mx ? tt[q] : mx;
             mn = tt[q] < mn ? tt[q] : mn;
           }
-          T* dst = O + k * N2 + (y0 + wy) * N + x0 + 4 * lane;
+          T* dst = O + k * N2 + (y0 + wy) * N + x0 + xoff;
           if constexpr (sizeof(T) == 4) {
             *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
           } else {
-            reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
-            reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+            *reinterpret_cast<longlong2*>(dst) = make_longlong2(tt[0], tt[1]);
+            *reinterpret_cast<longlong2*>(dst + 64) = make_longlong2(tt[2], tt[3]);
           }
         }
       }
