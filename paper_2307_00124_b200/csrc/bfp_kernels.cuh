@@ -1723,17 +1723,51 @@ __device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
 #pragma unroll
       for (int q = 0; q < 4; ++q) Ts[q] = acc[q];
     };
-    const bool xpad = x0 + 4 * cxq + 3 == Nc - 1;
+    // int64 storage: the thread's 4 coarse points are columns cxq + 16 q (not 4 cxq + q), so
+    // that the 16-byte shared loads of a half-warp are contiguous (the 4-consecutive layout
+    // strides them by 64 bytes: 4-way bank conflicts, short-scoreboard-bound at 0.75 of
+    // HBM).  Per plane: A = sum_py w_py f(2I), B = sum_py w_py f(2I + 1) from one longlong2
+    // per row and point; T(I) = A(I) + 2 B(I) + A(I + 1), A(I + 1) from lane + 1 by shuffle
+    // (lane 15 of the half-warp: lane 0's next point, or the tile's halo column 128).
+    [[maybe_unused]] auto T_of64 = [&](int64_t f, V Ts[4]) {
+      const T* base = fsl + (int)((f - 2 * K0) % kR3FS) * kR3FT + 4 + 2 * cxq;
+      V A[5] = {0, 0, 0, 0, 0}, Bs[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int py = 0; py < 3; ++py) {
+        const T* row = base + (frow + py) * kR3FW;
+        const V wy = py == 1 ? 2 : 1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const longlong2 a = *reinterpret_cast<const longlong2*>(row + 32 * q);
+          A[q] += wy * (V)(a.x >> sh);
+          Bs[q] += wy * (V)(a.y >> sh);
+        }
+        A[4] += wy * (V)(row[128 - 2 * cxq] >> sh);  // fine column 128 of the row (broadcast)
+      }
+      const int src = (t & 16) | ((cxq + 1) & 15);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const V nxt = __shfl_sync(0xffffffffu, cxq == 0 ? A[q + 1] : A[q], src);
+        Ts[q] = A[q] + 2 * Bs[q] + nxt;
+      }
+    };
+    const bool xpad = sizeof(T) == 4 ? x0 + 4 * cxq + 3 == Nc - 1 : x0 + cxq + 48 == Nc - 1;
     const bool ypad = y0 + cy == Nc - 1;
     V Tp[4] = {0, 0, 0, 0};  // T_{2K}
     for (int s = 0; s < steps; ++s) {
       const int64_t Kc = K0 + s;
       mbar_wait(&bar[s % kR3B], (parity >> (s % kR3B)) & 1u);
       parity ^= 1u << (s % kR3B);
-      if (s == 0) T_of(2 * Kc, Tp);
       V T1[4], T2[4];
-      T_of(2 * Kc + 1, T1);
-      T_of(2 * Kc + 2, T2);
+      if constexpr (sizeof(T) == 4) {
+        if (s == 0) T_of(2 * Kc, Tp);
+        T_of(2 * Kc + 1, T1);
+        T_of(2 * Kc + 2, T2);
+      } else {
+        if (s == 0) T_of64(2 * Kc, Tp);
+        T_of64(2 * Kc + 1, T1);
+        T_of64(2 * Kc + 2, T2);
+      }
       const bool rowpad = ypad || Kc + Z0 == Nc - 1;
       T tt[4];
 #pragma unroll
@@ -1755,12 +1789,13 @@ __device__ __forceinline__ void rst3_loop(const RestrictOp& op, const Vec& out,
         mx = tt[q] > mx ? tt[q] : mx;
         mn = tt[q] < mn ? tt[q] : mn;
       }
-      T* dst = O + Kc * Nc2 + (y0 + cy) * Nc + x0 + 4 * cxq;
       if constexpr (sizeof(T) == 4) {
+        T* dst = O + Kc * Nc2 + (y0 + cy) * Nc + x0 + 4 * cxq;
         *reinterpret_cast<int4*>(dst) = make_int4(tt[0], tt[1], tt[2], tt[3]);
       } else {
-        reinterpret_cast<longlong2*>(dst)[0] = make_longlong2(tt[0], tt[1]);
-        reinterpret_cast<longlong2*>(dst)[1] = make_longlong2(tt[2], tt[3]);
+        T* dst = O + Kc * Nc2 + (y0 + cy) * Nc + x0 + cxq;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[16 * q] = tt[q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) Tp[q] = T2[q];
