@@ -228,7 +228,8 @@ typedef struct {
      supplies the derived Chebyshev scalars: ref_c1 = c1 rounded to the hierarchy
      precision (ExtFloat), ref_kres = add_up(2 c1, 1) / 4, ref_c1d / ref_c2d[l] = c1 / c2
      floor-quantised at wdot_l (quantize_scalar_floor); rhs_kind 1 = h^2 / 2^d * the
-     config's d pi^2 prod sin (the D^-1-scaled load up to a constant). */
+     config's d pi^2 prod sin (the D^-1-scaled load up to a constant); rhs_kind 3 = the
+     caller's vectors (bfp_mg_level_rhs), e.g. the FEM load by quadrature. */
   int ref_mode;
   bfp_xf_t ref_c1, ref_kres;
   bfp_scalar_t ref_c1d[32], ref_c2d[32];
@@ -251,6 +252,12 @@ int bfp_mg_result(bfp_mg_t mg, int64_t* x, bfp_header_t* xh, double* hist, int h
                   void* stream);
 /* handles to the solver's finest-level vectors (x, b) for benchmarks */
 int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r);
+/* rhs_kind 3 (caller-provided right-hand sides; the reference's hierarchy keeps one D^-1-scaled
+   FEM load vector per level, Hierarchy::setup_scaling, P/src/multigrid.cpp:286-289): the
+   handle of level `level`'s b (FMG: every level; otherwise the finest) and its mantissa
+   bytes.  The solver zero-initialises it at create; the caller writes it (bfp_quantize_exact,
+   bfp_vec_upload, ...) before a solve.  Single-rank solvers only. */
+int bfp_mg_level_rhs(bfp_mg_t mg, int level, bfp_vec_t* b, int* mant_bytes);
 int64_t bfp_mg_kernel_launches(bfp_mg_t mg);
 
 /* ---- sharded solve ----

@@ -280,6 +280,16 @@ class Multigrid {
     hist.resize((std::size_t)nh);
     return {BfpBlock::vec(std::move(x), h.q, h.e), hist};
   }
+  /// rhs_kind 3: write level `level`'s right-hand side as entries z_i 2^k_i, floor-quantised
+  /// at w (the reference's quantize_vec of the D^-1-scaled load, P/src/multigrid.cpp:231)
+  void set_level_rhs(int level, const std::vector<std::int64_t>& z,
+                     const std::vector<std::int64_t>& k, std::int64_t w, void* stream = nullptr) {
+    bfp_vec_t b = nullptr;
+    check(bfp_mg_level_rhs(mg_, level, &b, nullptr), "bfp_mg_level_rhs");
+    if (z.size() != k.size()) check(BFP_ERR_ARG, "set_level_rhs: size mismatch");
+    check(bfp_quantize_exact(z.data(), k.data(), (std::int64_t)z.size(), w, b, stream),
+          "bfp_quantize_exact");
+  }
 
  private:
   bfp_mg_config_t cfg_;

@@ -359,3 +359,72 @@ class RefMg:
             x = cfg.x0 if cfg.x0 is not None else P.zero_vec(((1 << l) - 1) ** cfg.d, cfg.w[l])
             self.res.x = self.ir(l, x, cfg.cycles)
         return self.res
+
+
+# ---------------------------------------------------------------------------
+# FEM load vectors (the right-hand sides of the reference's Poisson problems)
+
+def _fem_load_1d(level: int, k: int, prec: int):
+    """assemble_1d_full's load against g(x) = sin(k pi x) for degree 1, m_order 1
+    (P/src/fem.cpp:316-336), in the reference's loop order: elements, quadrature points
+    (ElementRule(degree + 1): Gauss-Legendre nodes mapped to [0, 1], weights on [-1, 1],
+    Jacobian h / 2, :286-296), local basis functions a = 0 (1 - xi) and a = 1 (xi);
+    fma_acc into load[span - degree + a] with span = degree + el.  Index 0 and 2^level are
+    the boundary functions; the interior is 1 .. 2^level - 1 (interior_offset = 1 for
+    Dirichlet p = 1).  MPFR at 400 bits there, mpmath at `prec` here (see fem_rhs)."""
+    import mpmath as mp
+    n_el = 1 << level
+    with mp.workprec(prec):
+        h = mp.ldexp(mp.mpf(1), -level)
+        jac = h / 2
+        gn = [-1 / mp.sqrt(3), 1 / mp.sqrt(3)]      # gauss_legendre(2)
+        gw = [mp.mpf(1), mp.mpf(1)]
+        nodes01 = [(v + 1) / 2 for v in gn]
+        load = [mp.mpf(0)] * (n_el + 1)
+        for el in range(n_el):
+            for q in range(2):
+                xq = (el + nodes01[q]) * h
+                xi = nodes01[q]
+                ders0 = [1 - xi, xi]                 # hat functions on the element
+                fq = mp.sin(k * mp.pi * xq) * (gw[q] * jac)
+                for a in range(2):
+                    load[el + a] = load[el + a] + fq * ders0[a]
+        # An entry that vanishes by symmetry (sin(2 pi x) phi_i at x_i = 1/2: the two
+        # elements' contributions cancel) is rounding noise of relative size 2^-prec, in
+        # the reference as well (2^-400 there), and floor() of noise is 0 or -1 by the
+        # sign of the noise.  The restatement takes the mathematical value 0 -- the one
+        # documented deviation (DESIGN.md section 11).
+        cut = mp.ldexp(h * h, -(prec // 2))  # the entries' natural size is ~ k pi h^2
+        return [mp.mpf(0) if abs(v) <= cut else v for v in load[1:n_el]]
+
+
+def fem_rhs(d: int, level: int, w: int, prec: int = 600) -> P.Block:
+    """Level `level`'s right-hand side as the reference quantises it: the FEM load vector
+    (assemble, P/src/fem.cpp:426-457: 1-D f = Manufactured::f = 9 pi^2 sin(3 pi x), :99-103;
+    2-D b[i1 n + i2] = 13 pi^2 load_sin2pi[i1] load_sin3pi[i2]) divided by the level's
+    diagonal (Hierarchy::setup_scaling, P/src/multigrid.cpp:286-289; diag = 2 / h in 1-D,
+    8 / 3 in 2-D) and floor-quantised at w = wcheck (quantize_vec = from_extfloat,
+    P/src/multigrid.cpp:231, P/src/bfp.cpp:189-194).
+
+    The reference rounds every ExtFloat operation to 400 bits; this restatement evaluates
+    at `prec` >= 440 bits and floors the result, which gives the same block unless an
+    entry lies within ~2^-380 (relative) of a quantisation boundary (the entries are
+    transcendental; SURVEY 8(f)-1 asks for exactly this)."""
+    import mpmath as mp
+    with mp.workprec(prec):
+        pi2 = mp.pi * mp.pi
+        l3 = _fem_load_1d(level, 3, prec)
+        if d == 1:
+            diag = 2 / mp.ldexp(mp.mpf(1), -level)
+            vals = [(9 * pi2) * v / diag for v in l3]
+        else:
+            l2 = _fem_load_1d(level, 2, prec)
+            c = 13 * pi2
+            diag = mp.mpf(8) / 3
+            vals = [((c * a) * b) / diag for a in l2 for b in l3]
+    z, k = [], []
+    for v in vals:
+        sign, man, exp, _ = v._mpf_
+        z.append(-int(man) if sign else int(man))
+        k.append(int(exp))
+    return P.quantize_exact(z, k, w)

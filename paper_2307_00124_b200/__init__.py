@@ -98,7 +98,7 @@ EXPORTS = [
     "bfp_spmv_csr", "bfp_gemv_csr", "bfp_qcomp_rows", "bfp_stencil_gemv", "bfp_stencil_jacobi",
     "bfp_scal", "bfp_restrict_fw", "bfp_prolong", "bfp_prolong_correct", "bfp_jacobi_coeff",
     "bfp_gen_uniform", "bfp_gen_sine", "bfp_mg_create", "bfp_mg_destroy", "bfp_mg_solve",
-    "bfp_mg_result", "bfp_mg_vectors", "bfp_mg_kernel_launches", "bfp_status_string",
+    "bfp_mg_result", "bfp_mg_vectors", "bfp_mg_level_rhs", "bfp_mg_kernel_launches", "bfp_status_string",
     "bfp_device_sync", "bfp_launch_count", "bfp_profile_enable", "bfp_profile_read",
     "bfp_set_kernel_path", "bfp_vec_download_async_i32", "bfp_vec_create_slab", "bfp_vec_planes",
     "bfp_stencil_gemv_part", "bfp_stencil_jacobi_part", "bfp_window_finalize",
@@ -171,6 +171,7 @@ def lib() -> C.CDLL:
         "bfp_mg_result": (i32, [vp, vp, C.POINTER(_Header), vp, i32, C.POINTER(i32), vp, i64,
                                 pi64, vp]),
         "bfp_mg_vectors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+        "bfp_mg_level_rhs": (i32, [vp, i32, C.POINTER(vp), C.POINTER(i32)]),
         "bfp_nccl_unique_id": (i32, [vp, i32]),
         "bfp_quantize_exact": (i32, [vp, vp, i64, i64, vp, vp]),
         "bfp_from_doubles": (i32, [vp, i64, i64, vp, vp]),
@@ -614,13 +615,15 @@ def prolong_correct(ec, y, w_out, w_tmp, gamma, nn=False):
 
 
 def quantize_exact(z: Sequence[int], k: Sequence[int], w: int, mant_bytes: int = 8,
-                   dim: int = 0, level: int = 0) -> BfpVec:
-    """quantize_exact (src/bfp.cpp:163-187) of entries z_i 2^k_i on the device (int64 z)."""
+                   dim: int = 0, level: int = 0, out: Optional[BfpVec] = None) -> BfpVec:
+    """quantize_exact (src/bfp.cpp:163-187) of entries z_i 2^k_i on the device (int64 z),
+    into a new vector or into `out`."""
     za = np.ascontiguousarray(np.asarray(z, dtype=np.int64))
     ka = np.ascontiguousarray(np.asarray(k, dtype=np.int64))
     if za.shape != ka.shape:
         raise InvalidArgument(ERR_ARG, "quantize_exact: size mismatch")
-    out = BfpVec.grid(dim, level, mant_bytes) if dim else BfpVec.flat(len(za), mant_bytes)
+    if out is None:
+        out = BfpVec.grid(dim, level, mant_bytes) if dim else BfpVec.flat(len(za), mant_bytes)
     _raise(lib().bfp_quantize_exact(za.ctypes.data_as(C.c_void_p), ka.ctypes.data_as(C.c_void_p),
                                     len(za), w, out.h, _s()), "quantize_exact")
     return out
@@ -944,6 +947,16 @@ class Multigrid:
     def trace(self, trace_cap: int = 1 << 20) -> SolverTrace:
         """The solve's records as the reference's SolverTrace."""
         return SolverTrace(self.result(trace_cap)[4])
+
+    def level_rhs(self, level: int) -> BfpVec:
+        """The solver's right-hand side of `level` (rhs_kind 3: written by the caller before a
+        solve; include/bfpmg_b200.h: bfp_mg_level_rhs).  The solver owns the vector."""
+        b, mb = C.c_void_p(), C.c_int()
+        _raise(lib().bfp_mg_level_rhs(self.h, level, C.byref(b), C.byref(mb)), "bfp_mg_level_rhs")
+        v = BfpVec(b.value, self.cfg.d, level, mb.value)
+        v._owned = False
+        v._keep = self  # the handle lives as long as the solver
+        return v
 
     def vectors(self):
         x, b, r = C.c_void_p(), C.c_void_p(), C.c_void_p()

@@ -1556,6 +1556,17 @@ int bfp_mg_vectors(bfp_mg_t mg, bfp_vec_t* x, bfp_vec_t* b, bfp_vec_t* r) {
   return BFP_OK;
 }
 
+int bfp_mg_level_rhs(bfp_mg_t mg, int level, bfp_vec_t* b, int* mant_bytes) {
+  if (!mg || !b || mg->rs.size() != 1) return BFP_ERR_ARG;
+  RankSolver* s = mg->r0();
+  if (s->world > 1 || level < 1 || level > s->cfg.l_fine || level >= (int)s->lev.size() ||
+      !s->lev[level].b)
+    return BFP_ERR_ARG;
+  *b = s->lev[level].b;
+  if (mant_bytes) *mant_bytes = s->ebytes;
+  return BFP_OK;
+}
+
 int bfp_mg_rank_result(bfp_mg_t mg, int local_rank, bfp_vec_t* x_final, bfp_vec_t* r_final,
                        int* rank, int* lowest_sharded_level) {
   if (!mg || local_rank < 0 || local_rank >= (int)mg->rs.size()) return BFP_ERR_ARG;

@@ -167,3 +167,78 @@ def recompute_table(level: int, rho: float, eta: float, w, wdot=None, wcheck=Non
         tr = mg.trace()
         rows.append((cap, tr.recomputes_at_level(level), tr.calls_at_level(level)))
     return rows
+
+
+# ---------------------------------------------------------------------------
+# FEM load vector of the reference's manufactured problems (rhs_kind 3)
+
+def fem_load_1d(level: int, k: int, prec: int = 480):
+    """integral of sin(k pi x) phi_i(x) over (0, 1), i = 1 .. 2^level - 1, for the p = 1 hat
+    basis by the reference's element rule: Gauss-Legendre with degree + 1 = 2 points per
+    element, weights on [-1, 1] times the Jacobian h / 2 (assemble_1d_full and ElementRule,
+    P/src/fem.cpp:286-296, 316-336).  The reference evaluates in 400-bit MPFR; here mpmath
+    at `prec` >= 440 bits, which floor-quantises to the same block unless an entry lies
+    within 2^-380 (relative) of a quantisation boundary.  Returns mpmath values."""
+    import mpmath as mp
+    n = 1 << level
+    with mp.workprec(prec):
+        h = mp.ldexp(mp.mpf(1), -level)
+        g = 1 / mp.sqrt(3)
+        nodes = [(1 - g) / 2, (1 + g) / 2]
+        kpi = k * mp.pi
+        s = [[mp.sin(kpi * ((el + nq) * h)) for nq in nodes] for el in range(n)]
+        half = h / 2
+        # phi_i = xi on element i - 1, 1 - xi on element i (xi the element-local coordinate)
+        load = [half * (s[i - 1][0] * nodes[0] + s[i - 1][1] * nodes[1] +
+                        s[i][0] * (1 - nodes[0]) + s[i][1] * (1 - nodes[1]))
+                for i in range(1, n)]
+        # entries that vanish by symmetry (sin(2 pi x) at x_i = 1/2) are rounding noise, here
+        # and in the reference's MPFR evaluation alike; they are taken as exactly 0
+        cut = mp.ldexp(h * h, -(prec // 2))  # against the entries' natural size ~ k pi h^2
+        return [mp.mpf(0) if abs(v) <= cut else v for v in load]
+
+
+def _zk62(v) -> Tuple[int, int]:
+    """An mpmath value as z 2^k with |z| < 2^62, floored: exact under a later floor
+    quantisation at w <= 62 (nested floors with 2^k dividing 2^e_out)."""
+    sign, man, exp, bc = v._mpf_
+    z = -int(man) if sign else int(man)
+    s = max(0, bc - 62)
+    return z >> s, exp + s
+
+
+def fem_rhs(d: int, level: int, prec: int = 480):
+    """The D^-1-scaled load vector of level `level` (Hierarchy::setup_scaling,
+    P/src/multigrid.cpp:286-289: b / diag(A)) of the reference's Poisson problems as (z, k)
+    lists for quantize_exact, x fastest:
+      1-D  f = 9 pi^2 sin(3 pi x)  (Manufactured::f, P/src/fem.cpp:99-103), D = 2 / h;
+      2-D  f = 13 pi^2 sin(2 pi x1) sin(3 pi x2) as the outer product of two 1-D loads,
+           b[i1 n + i2] = 13 pi^2 l2[i1] l3[i2]  (assemble, P/src/fem.cpp:441-456), D = 8/3."""
+    import mpmath as mp
+    if d not in (1, 2):
+        raise ValueError("fem_rhs: d = 1 or 2")
+    with mp.workprec(prec):
+        pi2 = mp.pi * mp.pi
+        l3 = fem_load_1d(level, 3, prec)
+        if d == 1:
+            c = 9 * pi2 * mp.ldexp(mp.mpf(1), -level) / 2
+            vals = [c * v for v in l3]
+        else:
+            l2 = fem_load_1d(level, 2, prec)
+            c = 13 * pi2 * 3 / 8
+            vals = [(c * a) * b for a in l2 for b in l3]
+        zk = [_zk62(v) for v in vals]
+    return [z for z, _ in zk], [k for _, k in zk]
+
+
+def set_fem_rhs(mg, prec: int = 480):
+    """Write the FEM load vectors into a rhs_kind = 3 solver (every level of an FMG
+    hierarchy, else the finest), floor-quantised at each level's wcheck on the device
+    (bfp_quantize_exact into the handles of bfp_mg_level_rhs)."""
+    from . import quantize_exact
+    cfg = mg.cfg
+    lo = (1 if cfg.ref_mode else cfg.l_coarse) if cfg.fmg else cfg.l_fine
+    for l in range(lo, cfg.l_fine + 1):
+        z, k = fem_rhs(cfg.d, l, prec)
+        w = cfg.pc[l] or cfg.p[l]
+        quantize_exact(z, k, w, out=mg.level_rhs(l))

@@ -31,6 +31,8 @@ def _rhs(kind, L, wcheck, seed, fmg, d=1):
             b = P.gen_sine(d, l, wcheck[l])
             if any(b.m):
                 b.e -= 2 * l + d
+        elif kind == 3:  # the FEM load vector by quadrature, D^-1-scaled
+            b = R.fem_rhs(d, l, wcheck[l])
         elif kind == 0:
             b = P.gen_uniform(d, l, wcheck[l], seed, 2)
         else:
@@ -46,6 +48,9 @@ CASES = [
     dict(L=7, w=16, wdot=16, wcheck=20, rho=2.02, eta=0.15, cycles=5, fmg=False, rhs=0, x0=True),
     dict(L=6, w=40, wdot=36, wcheck=44, rho=2.0, eta=0.5, cycles=3, fmg=False, rhs=1),
     dict(L=5, w=12, wdot=12, wcheck=12, rho=2.02, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
+    # the reference's own right-hand side: FEM load of 9 pi^2 sin(3 pi x) by 2-point Gauss
+    dict(L=7, w=20, wdot=16, wcheck=24, rho=2.02, eta=0.3, cycles=1, fmg=True, rhs=3),
+    dict(L=6, w=40, wdot=36, wcheck=44, rho=2.0, eta=0.3, cycles=3, fmg=False, rhs=3),
     # 2-D: rho = lambda_max(D^-1 A) of the 9-point operator is < 2 (Gershgorin); the
     # reference estimates it by power iteration (P/src/linalg.cpp:272-295), injected here
     dict(d=2, L=5, w=20, wdot=16, wcheck=24, rho=1.6, eta=0.3, cycles=1, fmg=True, rhs=1),
@@ -54,10 +59,12 @@ CASES = [
     dict(d=2, L=5, w=16, wdot=16, wcheck=20, rho=1.7, eta=0.2, cycles=4, fmg=False, rhs=0, x0=True),
     dict(d=2, L=6, w=40, wdot=36, wcheck=44, rho=1.6, eta=0.5, cycles=2, fmg=False, rhs=1),
     dict(d=2, L=4, w=8, wdot=8, wcheck=8, rho=1.6, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
+    dict(d=2, L=5, w=20, wdot=16, wcheck=24, rho=1.6, eta=0.3, cycles=1, fmg=True, rhs=3),
+    dict(d=2, L=4, w=40, wdot=36, wcheck=44, rho=1.6, eta=0.3, cycles=2, fmg=False, rhs=3),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c.get('d', 1)}_L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}")
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c.get('d', 1)}_L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}_rhs{c['rhs']}")
 def test_refmode_gpu_vs_pyref(B, case):
     L, d = case["L"], case.get("d", 1)
     w, wd, wc = (_levels(case[k], L) for k in ("w", "wdot", "wcheck"))
@@ -71,6 +78,9 @@ def test_refmode_gpu_vs_pyref(B, case):
                            rhs_kind=case["rhs"], seed=seed, d=d)
     for graph in (False, True):
         mg = B.Multigrid(gcfg)
+        if case["rhs"] == 3:
+            from paper_2307_00124_b200 import refmode
+            refmode.set_fem_rhs(mg)
         mg.solve(use_graph=graph)
         x, q, e, hist, tr = mg.result(trace_cap=1 << 14)
         assert [tuple(t) for t in tr] == [tuple(t) for t in want.trace], graph
