@@ -1369,16 +1369,38 @@ template <typename T> constexpr int p3_ct() {  // coarse slot in elements (128-B
   return (int)(((kP3CW * kP3CH * sizeof(T) + 127) / 128 * 128) / sizeof(T));
 }
 constexpr int kP3YT = kP3W * kP3H;                               // one y box
+// Ring depth (fine-plane pairs in flight) and resident CTAs per SM, per op and storage type
+// (tools/ab_p3.sh, profiles/r2/r2j_ab_p3.txt): the plain prolongation streams 1.4 / 2.9 KB
+// coarse boxes and wants a deeper ring; prolong + correct moves two 4 / 8 KB fine boxes per
+// pair and runs best with a shallow ring and more CTAs.
 #ifndef BFP_P3_D
-#define BFP_P3_D 2
+#define BFP_P3_D 3
 #endif
-#ifndef BFP_P3_MINB  // resident CTAs per SM of the int32 instantiation
+#ifndef BFP_P3_DC
+#define BFP_P3_DC 1
+#endif
+#ifndef BFP_P3_MINB  // int32 storage
 #define BFP_P3_MINB 3
 #endif
-constexpr int kP3D = BFP_P3_D;                                    // pairs in flight
-constexpr int kP3S = kP3D + 1;                                   // slots / barriers
-template <typename T> constexpr size_t p3_smem() {
-  return (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T) + 2 * kP3S * 8 + 128 + 64;
+#ifndef BFP_P3_MINBC
+#define BFP_P3_MINBC 4
+#endif
+#ifndef BFP_P3_MINB64  // int64 storage
+#define BFP_P3_MINB64 2
+#endif
+#ifndef BFP_P3_MINBC64
+#define BFP_P3_MINBC64 2
+#endif
+template <typename Op> constexpr int p3_d() { return Op::kCorr ? BFP_P3_DC : BFP_P3_D; }
+template <typename Op> constexpr int p3_s() { return p3_d<Op>() + 1; }  // slots / barriers
+template <typename T, typename Op> constexpr int p3_minb() {
+  return sizeof(T) == 4 ? (Op::kCorr ? BFP_P3_MINBC : BFP_P3_MINB)
+                        : (Op::kCorr ? BFP_P3_MINBC64 : BFP_P3_MINB64);
+}
+// the y part of a slot: two fine boxes (prolong + correct only)
+template <typename Op> constexpr int p3_ys() { return Op::kCorr ? 2 * kP3YT : 0; }
+template <typename T, typename Op> constexpr size_t p3_smem() {
+  return (size_t)p3_s<Op>() * (p3_ct<T>() + p3_ys<Op>()) * sizeof(T) + 2 * p3_s<Op>() * 8 + 128 + 64;
 }
 struct P3Maps {
   CUtensorMap c, y;
@@ -1405,8 +1427,9 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
   using V = typename std::conditional<sizeof(T) == 4, int, int64_t>::type;
   constexpr int kP3CT = p3_ct<T>();
   T* csl = reinterpret_cast<T*>(smem);
+  constexpr int kP3S = p3_s<Op>();
   T* ysl = csl + kP3S * kP3CT;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ysl + kP3S * 2 * kP3YT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ysl + kP3S * p3_ys<Op>());
   uint64_t* empty = full + kP3S;
   T* O = (T*)out.data;
   const int sc = op.shc(), sy = op.shy();
@@ -1589,7 +1612,7 @@ __device__ __forceinline__ void pro3_loop(const Op& op, const Vec& out, const Wi
 }
 
 template <int MODE, typename T, typename Op>
-__global__ void __launch_bounds__(kP3T + 32, sizeof(T) == 4 ? BFP_P3_MINB : 2)
+__global__ void __launch_bounds__(kP3T + 32, p3_minb<T, Op>())
     pro3_win_kernel(Op op, Vec out, WinParams p, int R, const __grid_constant__ P3Maps tm) {
   extern __shared__ __align__(128) char smem_raw[];
   char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
@@ -1602,8 +1625,9 @@ __global__ void __launch_bounds__(kP3T + 32, sizeof(T) == 4 ? BFP_P3_MINB : 2)
   r.init();
   const bool fast = sizeof(T) == 4 ? (op.narrow && need <= 63) : op.wide;
   if (fast) {
+    constexpr int kP3S = p3_s<Op>();
     uint64_t* bar =
-        reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (p3_ct<T>() + 2 * kP3YT) * sizeof(T));
+        reinterpret_cast<uint64_t*>(smem + (size_t)kP3S * (p3_ct<T>() + p3_ys<Op>()) * sizeof(T));
     if (threadIdx.x == 0) {
       for (int k = 0; k < kP3S; ++k) {
         mbar_init(&bar[k], 1);                    // full: the producer's expect_tx arrival
@@ -2375,7 +2399,7 @@ static inline int launch_bulk3(const Op& op, bfp_vec_s* out, const WinParams& p0
 template <typename T, typename Op>
 static inline int launch_pro3(const Op& op, bfp_vec_s* out, const WinParams& p0,
                               cudaStream_t s) {
-  constexpr size_t kP3Smem = p3_smem<T>();
+  constexpr size_t kP3Smem = p3_smem<T, Op>();
   int rc = check_window(p0, out);
   if (rc) return rc;
   Vec o = view(out);
