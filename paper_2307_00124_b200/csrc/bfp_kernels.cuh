@@ -964,20 +964,31 @@ constexpr int kB3W = 128, kB3H = 8, kB3T = kB3W / 4 * kB3H;  // 256 threads
 // planes in flight (D; rings of D+3 x and D+1 y slots) and resident CTAs per SM the
 // kernel is compiled for, per storage type and op, swept on the B200 after the balanced
 // march depth (tools/ab_b3.sh, profiles/r1_ab_b3.txt; 3-D 511^3 int32 / 1023^3 int64):
-// int32 residual D = 2 at 4 CTAs/SM (0.92 of HBM; D = 3: 0.81), int32 Jacobi D = 4 at 3
-// CTAs/SM (0.84; D = 3 at 4: 0.81), int64 D = 3 at 2 CTAs/SM (residual 0.92, Jacobi
-// 0.71; D = 2: 0.89 / 0.71, D = 4: 0.75 / 0.56).  -DBFP_B3_D / -DBFP_B3_MINB override (A/B).
+// int32 residual D = 2 at 4 CTAs/SM (0.92 of HBM; D = 3: 0.81), int64 D = 3 at 2 CTAs/SM
+// (residual 0.94, Jacobi 0.82; D = 2: 0.93 / 0.81, D = 4: 0.77 / 0.65).  The int32 Jacobi
+// was D = 4 at 3 CTAs/SM in round 1; after its step loop shrank (two-IMAD.WIDE r term),
+// D = 3 at 4 CTAs/SM: 0.89 -> 0.91 (tools/ab_b3j.sh, profiles/r2/r2j_ab_b3j.txt).
+// -DBFP_B3_D / -DBFP_B3_MINB / -DBFP_B3_DJ / -DBFP_B3_MINBJ / -DBFP_B3_D64(J) override (A/B).
 template <typename Op, typename = void> struct B3Tune {
   static constexpr int D = 2, MINB = 4;
 };
 template <typename Op> struct B3Tune<Op, decltype((void)Op::b3_depth)> {
   static constexpr int D = Op::b3_depth, MINB = Op::b3_minb;
 };
+#ifndef BFP_B3_D64
+#define BFP_B3_D64 3
+#endif
+template <typename Op, typename = void> struct B3Tune64 {
+  static constexpr int D = BFP_B3_D64;
+};
+template <typename Op> struct B3Tune64<Op, decltype((void)Op::b3_depth64)> {
+  static constexpr int D = Op::b3_depth64;
+};
 template <typename T, typename Op> constexpr int b3_d() {
 #ifdef BFP_B3_D
   return BFP_B3_D;
 #else
-  return sizeof(T) == 8 ? 3 : B3Tune<Op>::D;
+  return sizeof(T) == 8 ? B3Tune64<Op>::D : B3Tune<Op>::D;
 #endif
 }
 template <typename T, typename Op> constexpr int b3_minb() {

@@ -539,7 +539,17 @@ struct JacobiOp {
   int Pg, Pb, s2;
   int64_t zd;
   static constexpr int zd_tag = 0;
-  static constexpr int b3_depth = 4, b3_minb = 3;  // bulk3 tuning (int32; B3Tune)
+#ifndef BFP_B3_DJ
+#define BFP_B3_DJ 3
+#endif
+#ifndef BFP_B3_MINBJ
+#define BFP_B3_MINBJ 4
+#endif
+#ifndef BFP_B3_D64J
+#define BFP_B3_D64J 3
+#endif
+  static constexpr int b3_depth = BFP_B3_DJ, b3_minb = BFP_B3_MINBJ;  // bulk3 tuning (int32; B3Tune)
+  static constexpr int b3_depth64 = BFP_B3_D64J;                       // (int64 storage)
   __device__ void setup(int64_t& e_star, int64_t& need) {
     const HSnap hx = hsnap(x.hdr), hb = hsnap(b.hdr);
     const int64_t ge = 2 * l + hx.e;
