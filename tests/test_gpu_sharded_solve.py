@@ -40,6 +40,8 @@ CASES = {
     "3d_fmg_w4": (dict(d=3, l_fine=6, cycles=1, rhs_kind=1, fmg=True, p=24), 4, 4),
     "3d_ir_int64": (dict(d=3, l_fine=6, cycles=2, x0_random=True, rhs_kind=2, p=40), 4, 4),
     "3d_fmg_l7": (dict(d=3, l_fine=7, cycles=1, rhs_kind=1, fmg=True, p=24), 2, 16),
+    # int64 storage through the tiled marches (split-pair prolongation, strided restriction)
+    "3d_fmg_l7_int64": (dict(d=3, l_fine=7, cycles=1, rhs_kind=1, fmg=True, p=40), 2, 16),
 }
 
 

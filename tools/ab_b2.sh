@@ -1,5 +1,7 @@
-# 2-D bulk pipeline depth / CTAs-per-SM sweep per op (builds from tools/ab_build.sh)
-for rep in 1 2; do
-for v in ${VARIANTS:-b2d2m4 b2d3m4 b2d4m3 b2d3m3}; do
-  BFPMG_LIB=paper_2307_00124_b200/_ab/$v/libbfpmg_b200.so python tools/ab_ops.py 2 12 residual,jacobi 2>&1 | grep -v Warn | sed "s/^/$v /"
-done; done
+#!/bin/bash
+# 2-D bulk pipeline ring depth x resident CTAs sweep: variants built into _ab/<name>
+cd "${GRAFT_REPO_ROOT:-.}"
+for v in ${VARIANTS:-base b24 b43 b34 b42 b23 b52}; do
+  if [ $v = base ]; then unset BFPMG_LIB; else export BFPMG_LIB=$PWD/paper_2307_00124_b200/_ab/$v/libbfpmg_b200.so; fi
+  python tools/ops_now.py residual jacobi 2>&1 | grep "^C2" | sed "s/^/$v /"
+done
