@@ -12,10 +12,11 @@ after the D = I scaling (P/src/multigrid.cpp:278-306):
 Vectors are in lexicographic order, x fastest (kron row index = iy * n + ix).
 
 Operators are quantised with quantize_csr (:216-229) at wcheck / wdot / w, the
-Chebyshev coefficients with chebyshev_coeffs_q (:183-193) from injected rho and eta
-(the power iteration of max_gen_eig_upper is not restated), rounded to nearest at the
+Chebyshev coefficients with chebyshev_coeffs_q (:183-193) from rho and eta (rho injected
+or power_rho below: max_gen_eig_upper by power iteration), rounded to nearest at the
 hierarchy precision (ExtFloat::from_mpq, P/src/extfloat.cpp:21-25) and floor-quantised
-at wdot (quantize_scalar_floor, :233-241).  The right-hand side is injected per level.
+at wdot (quantize_scalar_floor, :233-241).  The right-hand side is injected per level
+(fem_rhs below: the reference's FEM load vector).
 
 The gamma chain follows gamma_policy_eval (:121-155) with ExtFloat semantics:
 mul_up / add_up round up at the operands' maximal precision (P/src/extfloat.cpp:131-140),
@@ -428,3 +429,75 @@ def fem_rhs(d: int, level: int, w: int, prec: int = 600) -> P.Block:
         z.append(-int(man) if sign else int(man))
         k.append(int(exp))
     return P.quantize_exact(z, k, w)
+
+
+# ---------------------------------------------------------------------------
+# rho by power iteration (Hierarchy::setup_scaling, P/src/multigrid.cpp:277-280)
+
+def _rn(v: Fraction, prec: int) -> Fraction:
+    """MPFR_RNDN at prec bits of a signed rational."""
+    return -_round(-v, prec, False) if v < 0 else _round(v, prec, False)
+
+
+def _fem_rows(d: int, level: int, prec: int):
+    """a_sym of the p = 1 discretisation by rows (columns ascending, as band_to_csr_interior
+    and kron_sum produce them, P/src/fem.cpp:426-431) and its diagonal, up to the common
+    power of two 1/h that scales nothing in the iteration: 1-D tridiag(-1, 2, -1);
+    2-D A1 (x) M1 + M1 (x) A1 = (8/3, -1/3 x 8), its non-dyadic entries rounded to nearest
+    at prec (the reference's come out of the 400-bit quadrature within a few ulps of that)."""
+    n = (1 << level) - 1
+    rows = []
+    if d == 1:
+        for i in range(n):
+            rows.append([(j, Fraction(2 if j == i else -1)) for j in (i - 1, i, i + 1) if 0 <= j < n])
+        return rows, [Fraction(2)] * n
+    c, o = _rn(Fraction(8, 3), prec), _rn(Fraction(-1, 3), prec)
+    for i1 in range(n):
+        for i2 in range(n):
+            r = []
+            for j1 in (i1 - 1, i1, i1 + 1):
+                for j2 in (i2 - 1, i2, i2 + 1):
+                    if 0 <= j1 < n and 0 <= j2 < n:
+                        r.append((j1 * n + j2, c if (j1, j2) == (i1, i2) else o))
+            rows.append(r)
+    return rows, [c] * (n * n)
+
+
+def power_rho(d: int, l_est: int, prec: int = 400, max_iter: int = 400,
+              rel_tol: float = 1e-12) -> Fraction:
+    """rho = max_gen_eig_upper(a_sym, diag) (P/src/multigrid.cpp:206-209) on level l_est:
+    power_max_gen (P/src/linalg.cpp:272-295) -- start vector 1 + (i mod 7)/8, per iteration
+    spmv (mpfr_fma accumulation per row, :30-39), the Rayleigh quotient in the D inner
+    product (dot = fma chain, :47-51; den += (d_i x_i) x_i), the relative-change stop after
+    it > 2, x <- D^-1 A x normalised by its inf-norm -- with every operation rounded to
+    nearest at prec like MPFR_RNDN, then mul_up by from_mpq(101/100).  With the default
+    400 iterations and 1e-12 the stop never triggers on these operators (the gap ratio at
+    level 5 is 0.993): the value is the 400th Rayleigh quotient, ~1e-3 below lambda_max.
+    Exact rationals rounded after each operation, so the restatement IS correctly rounded;
+    what differs from the reference is only the last ulps of the 2-D matrix entries."""
+    rows, diag = _fem_rows(d, l_est, prec)
+    n = len(rows)
+    x = [Fraction(8 + (i % 7), 8) for i in range(n)]
+    tol = Fraction(rel_tol)
+    lam = lam_prev = Fraction(0)
+    for it in range(max_iter):
+        ax = []
+        for r in rows:
+            y = Fraction(0)
+            for j, a in r:
+                y = _rn(y + a * x[j], prec)
+            ax.append(y)
+        num = Fraction(0)
+        for xi, yi in zip(x, ax):
+            num = _rn(num + xi * yi, prec)
+        den = Fraction(0)
+        for xi, di in zip(x, diag):
+            den = _rn(den + _rn(di * xi, prec) * xi, prec)
+        lam = _rn(num / den, prec)
+        if it > 2 and abs(_rn(lam - lam_prev, prec)) <= _rn(tol * abs(lam), prec):
+            break
+        lam_prev = lam
+        x = [_rn(yi / di, prec) for yi, di in zip(ax, diag)]
+        nrm = max(abs(v) for v in x)
+        x = [_rn(v / nrm, prec) for v in x]
+    return _round(lam * _rn(Fraction(101, 100), prec), prec, True)

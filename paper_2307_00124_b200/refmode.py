@@ -242,3 +242,65 @@ def set_fem_rhs(mg, prec: int = 480):
         z, k = fem_rhs(cfg.d, l, prec)
         w = cfg.pc[l] or cfg.p[l]
         quantize_exact(z, k, w, out=mg.level_rhs(l))
+
+
+# ---------------------------------------------------------------------------
+# rho by power iteration (Hierarchy::setup_scaling)
+
+_RHO_CACHE = {}
+
+
+def estimate_rho(d: int, l_est: int = 5, prec: int = 400, max_iter: int = 400,
+                 rel_tol: float = 1e-12) -> Fraction:
+    """rho as the reference's Hierarchy::setup_scaling derives it
+    (P/src/multigrid.cpp:277-280): max_gen_eig_upper = 1.01 (rounded up) times the power
+    iteration power_max_gen of D^-1 A on level l_est (P/src/linalg.cpp:272-295; the drivers
+    pass l_est = min(5, levels)), in correctly rounded prec-bit arithmetic (mpmath: exact
+    products added with one rounding = mpfr_fma).  The operator is the p = 1 stiffness up
+    to its power-of-two 1/h: 1-D tridiag(-1, 2, -1), 2-D (8/3, -1/3 x 8).  Returns the exact
+    value of the prec-bit result; pass it as `rho` to mg_config_ref."""
+    key = (d, l_est, prec, max_iter, rel_tol)
+    if key in _RHO_CACHE:
+        return _RHO_CACHE[key]
+    import mpmath as mp
+    if d not in (1, 2):
+        raise ValueError("estimate_rho: d = 1 or 2")
+    n1 = (1 << l_est) - 1
+    with mp.workprec(prec):
+        if d == 1:
+            n = n1
+            cen, off = mp.mpf(2), mp.mpf(-1)
+            nbr = [[j for j in (i - 1, i, i + 1) if 0 <= j < n] for i in range(n)]
+        else:
+            n = n1 * n1
+            cen, off = mp.mpf(8) / 3, mp.mpf(-1) / 3
+            nbr = [[j1 * n1 + j2 for j1 in (i1 - 1, i1, i1 + 1) for j2 in (i2 - 1, i2, i2 + 1)
+                    if 0 <= j1 < n1 and 0 <= j2 < n1] for i1 in range(n1) for i2 in range(n1)]
+        fma = lambda acc, a, b: mp.fadd(mp.fmul(a, b, exact=True), acc)  # noqa: E731
+        x = [mp.mpf(8 + (i % 7)) / 8 for i in range(n)]
+        tol = mp.mpf(rel_tol)
+        lam = lam_prev = mp.mpf(0)
+        for it in range(max_iter):
+            ax = []
+            for i in range(n):
+                y = mp.mpf(0)
+                for j in nbr[i]:
+                    y = fma(y, cen if j == i else off, x[j])
+                ax.append(y)
+            num = den = mp.mpf(0)
+            for xi, yi in zip(x, ax):
+                num = fma(num, xi, yi)
+            for xi in x:
+                den = fma(den, cen * xi, xi)
+            lam = num / den
+            if it > 2 and abs(lam - lam_prev) <= tol * abs(lam):
+                break
+            lam_prev = lam
+            x = [yi / cen for yi in ax]
+            nrm = max(abs(v) for v in x)
+            x = [v / nrm for v in x]
+        rho = mp.fmul(lam, mp.mpf(101) / 100, rounding="u")
+        sign, man, exp, _ = rho._mpf_
+    out = Fraction(int(man)) * Fraction(2) ** int(exp)
+    _RHO_CACHE[key] = -out if sign else out
+    return _RHO_CACHE[key]

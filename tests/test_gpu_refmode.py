@@ -51,6 +51,8 @@ CASES = [
     # the reference's own right-hand side: FEM load of 9 pi^2 sin(3 pi x) by 2-point Gauss
     dict(L=7, w=20, wdot=16, wcheck=24, rho=2.02, eta=0.3, cycles=1, fmg=True, rhs=3),
     dict(L=6, w=40, wdot=36, wcheck=44, rho=2.0, eta=0.3, cycles=3, fmg=False, rhs=3),
+    # the reference's whole setup: rho by power iteration on level min(5, L), FEM load
+    dict(L=6, w=24, wdot=20, wcheck=28, rho="auto", eta=0.3, cycles=1, fmg=True, rhs=3),
     # 2-D: rho = lambda_max(D^-1 A) of the 9-point operator is < 2 (Gershgorin); the
     # reference estimates it by power iteration (P/src/linalg.cpp:272-295), injected here
     dict(d=2, L=5, w=20, wdot=16, wcheck=24, rho=1.6, eta=0.3, cycles=1, fmg=True, rhs=1),
@@ -61,15 +63,20 @@ CASES = [
     dict(d=2, L=4, w=8, wdot=8, wcheck=8, rho=1.6, eta=0.3, cycles=2, fmg=False, rhs=2, x0=True),
     dict(d=2, L=5, w=20, wdot=16, wcheck=24, rho=1.6, eta=0.3, cycles=1, fmg=True, rhs=3),
     dict(d=2, L=4, w=40, wdot=36, wcheck=44, rho=1.6, eta=0.3, cycles=2, fmg=False, rhs=3),
+    dict(d=2, L=3, w=24, wdot=20, wcheck=28, rho="auto", eta=0.3, cycles=2, fmg=True, rhs=3),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c.get('d', 1)}_L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}_rhs{c['rhs']}")
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"d{c.get('d', 1)}_L{c['L']}_{'fmg' if c['fmg'] else 'ir'}_w{c['w'] if isinstance(c['w'], int) else 'prog'}_rhs{c['rhs']}{'_rhoauto' if c['rho'] == 'auto' else ''}")
 def test_refmode_gpu_vs_pyref(B, case):
     L, d = case["L"], case.get("d", 1)
     w, wd, wc = (_levels(case[k], L) for k in ("w", "wdot", "wcheck"))
     seed = 3
     x0 = P.gen_uniform(d, L, w[L], seed, 1) if case.get("x0") else None
+    if case["rho"] == "auto":  # Hierarchy::setup_scaling: oracle restatement vs host code
+        from paper_2307_00124_b200 import refmode
+        case = dict(case, rho=refmode.estimate_rho(d, min(5, L)))
+        assert case["rho"] == R.power_rho(d, min(5, L))
     cfg = R.RefConfig(l_fine=L, w=w, wdot=wd, wcheck=wc, rho=case["rho"], eta=case["eta"],
                       cycles=case["cycles"], fmg=case["fmg"], x0=x0, d=d)
     want = R.RefMg(cfg, _rhs(case["rhs"], L, wc, seed, case["fmg"], d)).run()
