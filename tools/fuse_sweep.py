@@ -1,5 +1,5 @@
 """Solve time vs the coarse-level fusion threshold (fuse_points), results checked equal.
-python tools/fuse_sweep.py [C1 C2 ...]"""
+python tools/fuse_sweep.py [C1 C2 ...]   (FUSE_POINTS=0,64,... overrides the thresholds)"""
 import os
 import sys
 import time
@@ -17,7 +17,7 @@ names = sys.argv[1:] or ["C1", "C2", "C4"]
 for name in names:
     kw = dict(next(v for k, v in bench.SOLVES.items() if k.startswith(name)))
     ref = None
-    for fp in (0, 64, 512, 4096, 32768):
+    for fp in [int(v) for v in os.environ.get("FUSE_POINTS", "0,64,512,4096,32768").split(",")]:
         mg = B.Multigrid(B.mg_config(**kw, fuse_points=fp))
         mg.solve(use_graph=True)
         torch.cuda.synchronize()
