@@ -91,7 +91,8 @@ def test_slab_ranges():
         D.slab_ranges(3, 8)
 
 
-@pytest.mark.parametrize("d,l,P", [(2, 11, 4), (3, 7, 2), (3, 7, 8), (3, 7, 64)])
+@pytest.mark.parametrize("d,l,P", [(2, 11, 4), (3, 7, 2), (3, 7, 8), (3, 7, 64),
+                                   (3, 8, 2), (3, 8, 4)])  # l = 8: slabs through the tiled-TMA march
 def test_native_dist_ops_match_unsharded(B, d, l, P):
     """The native sharded ops (bfp_dist_*: halo, partial windows, MAX all-reduce and
     finalize enqueued in C++) equal the unsharded ops bit-exactly."""
