@@ -120,3 +120,42 @@ def test_native_dist_ops_match_unsharded(B, d, l, P):
         got, e = _gather([D.Slab(r, v) for r, v in enumerate(js)])
         m, q, er = B.jacobi(gx, ref.z, c, p, p + 5, g, nn=nn).z.download()
         assert e == er and np.array_equal(got, m), ("jacobi", d, l, P, g, nn)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_native_dist_ops_int64_l8(B, P):
+    """int64 storage (p = 40) at 3-D l = 8: the slabs (plane offset z0 > 0) run the tiled-TMA
+    march with the split windows (residual: SplitWin, Jacobi: three limbs) and the 32-bit pad
+    predicates; equal to the unsharded ops bit for bit."""
+    from paper_2307_00124_b200 import dist as D
+    d, l, p = 3, 8, 40
+    ranges = D.slab_ranges(l, P)
+    n = (1 << l) - 1
+    per = n * n
+    gx = B.gen_uniform(B.BfpVec.grid(d, l, 8), p, 5, 1)
+    gb = B.gen_sine(B.BfpVec.grid(d, l, 8), p)
+
+    def scatter(full):
+        m, q, e = full.download()
+        out = []
+        for lo, hi in ranges:
+            v = B.BfpVec.slab(d, l, lo, hi, 8)
+            v.upload(m[lo * per: min(hi, n) * per], q, e)
+            out.append(v)
+        return out
+    xs, bs = scatter(gx), scatter(gb)
+    ops = B.DistOps(P)
+    c = B.jacobi_coeff(d, l, 16)
+    g_exact = B.inf_norm_upper(B.residual(gx, gb, p, p + 5, B.Scalar(1 << 14, 16, 0)).z)
+    for g in (g_exact, B.Scalar(1 << 14, 16, 0)):
+        outs = [B.BfpVec.slab(d, l, lo, hi, 8) for (lo, hi) in ranges]
+        ops.gemv(xs, bs, B.bfp_minus_one(), B.bfp_one(), p, p + 5, g, outs)
+        got, e = _gather([D.Slab(r, v) for r, v in enumerate(outs)])
+        ref = B.residual(gx, gb, p, p + 5, g)
+        m, q, er = ref.z.download()
+        assert e == er and np.array_equal(got, m), (P, g)
+        js = [B.BfpVec.slab(d, l, lo, hi, 8) for (lo, hi) in ranges]
+        ops.jacobi(xs, outs, c, p, p + 3, g, js)
+        got, e = _gather([D.Slab(r, v) for r, v in enumerate(js)])
+        m, q, er = B.jacobi(gx, ref.z, c, p, p + 3, g).z.download()
+        assert e == er and np.array_equal(got, m), ("jacobi", P, g)
