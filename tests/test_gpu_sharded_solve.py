@@ -42,6 +42,8 @@ CASES = {
     "3d_fmg_l7": (dict(d=3, l_fine=7, cycles=1, rhs_kind=1, fmg=True, p=24), 2, 16),
     # int64 storage through the tiled marches (split-pair prolongation, strided restriction)
     "3d_fmg_l7_int64": (dict(d=3, l_fine=7, cycles=1, rhs_kind=1, fmg=True, p=40), 2, 16),
+    # ... and l = 8: the tiled int64 stencil march and the int64 restriction (coarse l = 7) on slabs
+    "3d_fmg_l8_int64": (dict(d=3, l_fine=8, cycles=1, rhs_kind=1, fmg=True, p=40), 2, 16),
 }
 
 
